@@ -1,0 +1,361 @@
+"""Generate tests/golden/*.npz from the REFERENCE itself (build container only).
+
+Imports the read-only reference package from /root/reference/pkg/src and
+records its outputs on fixed, seeded inputs.  The fixtures pin
+`oracle/fednl_oracle.py` (tests/test_oracle_golden.py) and are the targets of
+the GPU parity tests.  /root/reference does not exist on the GPU box, so the
+vectors are committed.  Run:
+
+    OPENBLAS_NUM_THREADS=1 python oracle/make_golden.py
+
+Every fixture is small (the whole directory stays well under 2 MB).
+"""
+
+from __future__ import annotations
+
+import os
+import sys
+
+os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")
+os.environ.setdefault("PYTHONDONTWRITEBYTECODE", "1")
+sys.dont_write_bytecode = True
+
+import numpy as np  # noqa: E402
+
+REF = "/root/reference/pkg/src"
+HERE = os.path.dirname(os.path.abspath(__file__))
+OUT = os.path.join(os.path.dirname(HERE), "tests", "golden")
+
+sys.path.insert(0, REF)
+from fednl import linalg, oracle, rng  # noqa: E402
+from fednl.algorithms import RunConfig  # noqa: E402
+from fednl.compressors import CompressorKind, CompressorSpec, compress  # noqa: E402
+from fednl.data import (  # noqa: E402
+    RawDataset,
+    augment_and_shard,
+    generate_synthetic,
+    normalize_labels,
+)
+from fednl.runtime import simulate  # noqa: E402
+
+# The BASELINE configs; the shapes are used at reduced rounds.
+BASELINE = {
+    "c0": dict(d=301, n=142, ni=350, density=0.04, p_pos=0.3, lam=1e-3,
+               algorithm="fednl", kind="topk", k=2408, alpha=1.0, rounds=100),
+    "c1": dict(d=124, n=80, ni=407, density=0.11, p_pos=0.24, lam=1e-3,
+               algorithm="fednl", kind="randseqk", k=992, alpha=None, rounds=200),
+    "c2": dict(d=69, n=100, ni=110, density=0.44, p_pos=0.5, lam=1e-3,
+               algorithm="fednl-ls", kind="toplek", k=69, alpha=None, rounds=200),
+    "c3": dict(d=301, n=142, ni=350, density=0.04, p_pos=0.3, lam=1e-3,
+               algorithm="fednl-pp", kind="randk", k=301, alpha=None, rounds=500, tau=12),
+}
+
+
+def binary_raw(num_features: int, m: int, density: float, p_pos: float, seed: int) -> RawDataset:
+    """SURVEY §8(d) binary generator built with the reference's own Prg."""
+    prg = rng.Prg(seed)
+    feats = prg.f64_block(m * num_features).reshape(m, num_features) < density
+    labels = np.where(prg.f64_block(m) < p_pos, 1.0, -1.0)
+    rows = []
+    for j in range(m):
+        nz = np.flatnonzero(feats[j])
+        rows.append((nz.astype(np.int64) + 1, np.ones(len(nz))))
+    return RawDataset(labels=labels, rows=rows, num_features=num_features)
+
+
+def baseline_shards(name: str, seed: int = 1):
+    c = BASELINE[name]
+    ds = binary_raw(c["d"] - 1, c["n"] * c["ni"], c["density"], c["p_pos"], seed)
+    return augment_and_shard(ds, c["n"], run_seed=seed, lam=c["lam"])
+
+
+def make_shards(num_features, m, n, seed, lam=1e-3):
+    ds = generate_synthetic(num_features, m, seed=seed)
+    normalize_labels(ds)
+    return augment_and_shard(ds, n, run_seed=seed, lam=lam)
+
+
+def rows_arrays(rows):
+    return dict(
+        round=np.array([r.round for r in rows], dtype=np.int64),
+        grad_norm=np.array([r.grad_norm for r in rows]),
+        f_value=np.array([r.f_value for r in rows]),
+        bytes_up=np.array([r.bytes_up_cum for r in rows], dtype=np.int64),
+        bytes_down=np.array([r.bytes_down_cum for r in rows], dtype=np.int64),
+        ls_steps=np.array([r.ls_steps for r in rows], dtype=np.int64),
+    )
+
+
+def gen_rng():
+    out = {}
+    p = rng.Prg(0)
+    out["seed0_stream"] = np.array([p.next_u64() for _ in range(5)], dtype=np.uint64)
+    seeds = [0, 1, 42, 0xDEADBEEF, (1 << 64) - 1, 0x9E3779B97F4A7C15]
+    out["stream_seeds"] = np.array(seeds, dtype=np.uint64)
+    out["streams"] = np.stack([rng.Prg(s).u64_block(64) for s in seeds])
+    out["f64_streams"] = np.stack([rng.Prg(s).f64_block(64) for s in seeds])
+    bounds = [1, 2, 3, 10, 69, 80, 100, 131, 142, 2415, 7750, 45451, 524800,
+              (1 << 63) + 12345, (1 << 64) - 1]
+    out["rr_bounds"] = np.array(bounds, dtype=np.uint64)
+    rr = np.zeros((len(seeds), len(bounds), 8), dtype=np.uint64)
+    nxt = np.zeros((len(seeds), len(bounds)), dtype=np.uint64)
+    for a, s in enumerate(seeds):
+        for b, bd in enumerate(bounds):
+            p = rng.Prg(s)
+            rr[a, b] = [p.randrange(bd) for _ in range(8)]
+            nxt[a, b] = p.next_u64()  # draw consumption check
+    out["randrange"] = rr
+    out["randrange_next"] = nxt
+    # partial shuffles at the RandK and PP shapes
+    ps = {}
+    for key, (n, k, s) in {
+        "randk_c3": (45451, 301, rng.derive_round_seed(1, 5, 7)),
+        "pp_c3": (142, 12, rng.mix64(1 ^ rng.TAG_MASTER)),
+        "small": (10, 4, 123),
+        "full": (17, 17, 9),
+    }.items():
+        ps[key] = rng.Prg(s).partial_shuffle_prefix(n, k)
+        out[f"pshuffle_{key}"] = ps[key]
+        out[f"pshuffle_{key}_args"] = np.array([n, k, s], dtype=np.uint64)
+    # the persistent master subset stream over 20 rounds (algorithms.py:422-425)
+    mp = rng.derive_stream(1, rng.TAG_MASTER)
+    out["pp_subsets_c3"] = np.stack(
+        [np.sort(mp.partial_shuffle_prefix(142, 12)) for _ in range(20)]
+    )
+    grid = np.zeros((4, 6, 6), dtype=np.uint64)
+    for a, rs in enumerate([0, 1, 123, (1 << 64) - 1]):
+        for c in range(6):
+            for r in range(6):
+                grid[a, c, r] = rng.derive_round_seed(rs, c * 1000 + c, r * 77 + r)
+    out["round_seed_grid"] = grid
+    out["tags"] = np.array([rng.TAG_SHUFFLE, rng.TAG_SYNTH, rng.TAG_MASTER], dtype=np.uint64)
+    return out
+
+
+def compress_cases():
+    """Packed inputs exercising ties, zeros, small/large k."""
+    cases = []
+    g = np.random.default_rng(2024)
+    for d in (2, 3, 5, 9, 24):
+        w = linalg.packed_length(d)
+        a = g.standard_normal((d, d))
+        cases.append((f"gauss{d}", d, linalg.pack_upper(np.asfortranarray((a + a.T) / 2))))
+    for d in (7, 24, 40):
+        w = linalg.packed_length(d)
+        # quantised values: heavy ties across the k-th boundary, both signs
+        v = g.integers(-3, 4, w).astype(float) * 0.125
+        cases.append((f"ties{d}", d, v))
+    cases.append(("onehot6", 6, np.eye(1, 21, 7).ravel() * -2.5))
+    cases.append(("const5", 5, np.full(15, 0.75)))
+    cases.append(("zeros4", 4, np.zeros(10)))
+    # the round-0 difference of a real c2-shaped client (x = 0): Hessian - lam I
+    sh = baseline_shards("c2")[3]
+    x = np.zeros(sh.dim)
+    s = oracle.new_scratch(sh)
+    oracle.refresh_scratch(sh, x, s)
+    h = oracle.hessian(sh, x, s)
+    linalg.add_to_diagonal(h, -sh.lam)
+    cases.append(("c2client3_round0", sh.dim, linalg.pack_upper(h)))
+    return cases
+
+
+def gen_compress():
+    out = {}
+    names = []
+    for name, d, pk in compress_cases():
+        w = linalg.packed_length(d)
+        m = linalg.unpack_to_symmetric(np.asarray(pk, dtype=float), d)
+        out[f"{name}__input"] = np.asarray(pk, dtype=float)
+        out[f"{name}__d"] = np.array(d)
+        names.append(name)
+        ks = sorted({1, 2, max(1, w // 7), max(1, w // 2), w})
+        for k in ks:
+            for kind, weighted in (("topk", False), ("topk", True), ("toplek", False),
+                                   ("randk", False), ("randseqk", False)):
+                for seed in (0, 77, 0xABCDEF):
+                    spec = CompressorSpec(CompressorKind(kind), k=k, topk_weighted=weighted)
+                    prg = rng.Prg(seed)
+                    delta = compress(m, spec, prg)
+                    tag = f"{name}__{kind}{'W' if weighted else ''}__k{k}__s{seed}"
+                    out[tag + "__idx"] = np.asarray(delta.indices, dtype=np.uint32)
+                    out[tag + "__val"] = np.asarray(delta.values, dtype=float)
+                    out[tag + "__next"] = np.array(prg.next_u64(), dtype=np.uint64)
+                    if kind == "topk":
+                        break  # deterministic: one seed is enough
+        for kind in ("identity", "natural"):
+            spec = CompressorSpec(CompressorKind(kind))
+            prg = rng.Prg(5)
+            delta = compress(m, spec, prg)
+            tag = f"{name}__{kind}__s5"
+            out[tag + "__val"] = np.asarray(delta.values, dtype=float)
+            out[tag + "__next"] = np.array(prg.next_u64(), dtype=np.uint64)
+    out["case_names"] = np.array(names)
+    return out
+
+
+def gen_oracle():
+    out = {}
+    shards = make_shards(6, 90, 3, seed=5, lam=0.01)
+    g = np.random.default_rng(9)
+    xs = [np.zeros(7), g.standard_normal(7), 30.0 * g.standard_normal(7)]
+    for ci, sh in enumerate(shards):
+        out[f"bmat{ci}"] = np.asfortranarray(sh.bmat)
+        for xi, x in enumerate(xs):
+            s = oracle.new_scratch(sh)
+            oracle.refresh_scratch(sh, x, s)
+            out[f"f_{ci}_{xi}"] = np.array(oracle.f_value(sh, x, s))
+            out[f"grad_{ci}_{xi}"] = oracle.gradient(sh, x, s)
+            out[f"hess_{ci}_{xi}"] = linalg.pack_upper(oracle.hessian(sh, x, s))
+    out["xs"] = np.stack(xs)
+    out["lam"] = np.array(0.01)
+    return out
+
+
+def gen_linalg():
+    out = {}
+    g = np.random.default_rng(31)
+    for d in (1, 2, 10, 50, 301):
+        a = g.standard_normal((d, d))
+        spd = np.asfortranarray(a @ a.T / d + np.eye(d))
+        b = g.standard_normal(d)
+        out[f"spd{d}"] = linalg.pack_upper(spd)
+        out[f"rhs{d}"] = b
+        out[f"sol{d}"] = linalg.cholesky_solve(spd, b)
+    bad = np.asfortranarray([[1.0, 2.0], [2.0, 1.0]])
+    try:
+        linalg.cholesky_factor(bad)
+    except linalg.NotPositiveDefiniteError as e:
+        out["npd_pk"] = linalg.pack_upper(bad)
+        out["npd_pivot"] = np.array([e.pivot_index, e.pivot_value])
+    a = g.standard_normal((12, 12))
+    ind = np.asfortranarray(a @ a.T)
+    ind[7, 7] = -50.0
+    try:
+        linalg.cholesky_factor(ind)
+    except linalg.NotPositiveDefiniteError as e:
+        out["npd2_pk"] = linalg.pack_upper(ind)
+        out["npd2_pivot"] = np.array([e.pivot_index, e.pivot_value])
+    return out
+
+
+SIM_CASES = {
+    # name: (generator args, RunConfig kwargs)
+    "fednl_identity": (("synth", 6, 80, 4, 2), dict(rounds=12)),
+    "fednl_topk": (("synth", 8, 120, 5, 3), dict(rounds=10, compressor=("topk", 9))),
+    "fednl_topkW": (("synth", 8, 120, 5, 3), dict(rounds=10, compressor=("topk", 9, True))),
+    "fednl_toplek": (("synth", 8, 120, 5, 4), dict(rounds=10, compressor=("toplek", 9))),
+    "fednl_randk": (("synth", 8, 120, 5, 5), dict(rounds=10, compressor=("randk", 9))),
+    "fednl_randseqk": (("synth", 8, 120, 5, 6), dict(rounds=10, compressor=("randseqk", 9))),
+    "fednl_natural": (("synth", 8, 120, 5, 7), dict(rounds=8, compressor=("natural",))),
+    "fednl_alpha1_stop": (("synth", 5, 60, 2, 6), dict(rounds=50, alpha=1.0,
+                                                         compressor=("topk", 4), stop_grad_norm=1e-9)),
+    "fednl_zero_init": (("synth", 6, 80, 4, 8), dict(rounds=6, hessian_init="zero",
+                                                       compressor=("topk", 8))),
+    "fednl_exact_init": (("synth", 6, 80, 4, 9), dict(rounds=6, hessian_init="exact",
+                                                        compressor=("randseqk", 8))),
+    "ls_topk": (("synth", 8, 120, 4, 10), dict(rounds=10, algorithm="fednl-ls", compressor=("topk", 9))),
+    "ls_toplek": (("synth", 8, 120, 4, 11), dict(rounds=10, algorithm="fednl-ls",
+                                                  compressor=("toplek", 12))),
+    "pp_randk": (("synth", 8, 150, 6, 12), dict(rounds=15, algorithm="fednl-pp", tau=2,
+                                                 compressor=("randk", 9))),
+    "pp_topk": (("synth", 8, 150, 6, 13), dict(rounds=15, algorithm="fednl-pp", tau=3,
+                                                compressor=("topk", 9))),
+    "pp_identity_stop": (("synth", 4, 60, 4, 8), dict(rounds=60, algorithm="fednl-pp", tau=2,
+                                                       stop_grad_norm=1e-10)),
+    # BASELINE shapes at reduced round counts
+    "c0_r4": (("baseline", "c0"), dict(rounds=4)),
+    "c1_r30": (("baseline", "c1"), dict(rounds=30)),
+    "c2_r30": (("baseline", "c2"), dict(rounds=30)),
+    "c3_r30": (("baseline", "c3"), dict(rounds=30)),
+}
+
+
+def build_case(name):
+    gen, kw = SIM_CASES[name]
+    kw = dict(kw)
+    if gen[0] == "synth":
+        _, nf, m, n, seed = gen
+        shards = make_shards(nf, m, n, seed)
+        kw.setdefault("run_seed", seed)
+    else:
+        c = BASELINE[gen[1]]
+        shards = baseline_shards(gen[1], seed=1)
+        kw.setdefault("run_seed", 1)
+        kw.setdefault("algorithm", c["algorithm"])
+        kw.setdefault("compressor", (c["kind"], c["k"]))
+        kw.setdefault("alpha", c["alpha"])
+        if "tau" in c:
+            kw.setdefault("tau", c["tau"])
+    comp = kw.pop("compressor", ("identity",))
+    spec = CompressorSpec(CompressorKind(comp[0]), k=comp[1] if len(comp) > 1 else None,
+                          topk_weighted=comp[2] if len(comp) > 2 else False)
+    cfg = RunConfig(compressor=spec, **kw)
+    return cfg, shards
+
+
+def gen_sim():
+    out = {}
+    for name in SIM_CASES:
+        cfg, shards = build_case(name)
+        rows = simulate(cfg, shards)
+        for k, v in rows_arrays(rows).items():
+            out[f"{name}__{k}"] = v
+        print(f"  sim {name}: {len(rows)} rows, final |g|={rows[-1].grad_norm:.3e}")
+    return out
+
+
+def gen_data():
+    """Checksums of the reference's shards for every BASELINE shape (c0-c3)."""
+    out = {}
+    for name in ("c0", "c1", "c2"):
+        shards = baseline_shards(name, seed=1)
+        out[f"{name}__colsum"] = np.stack([s.bmat.sum(axis=0) for s in shards[:4]])
+        out[f"{name}__rowsum"] = np.stack([s.bmat.sum(axis=1) for s in shards])
+        out[f"{name}__first_col"] = np.stack([s.bmat[:, 0] for s in shards])
+    sh = make_shards(6, 90, 3, seed=5, lam=0.01)
+    out["synth_6_90_3_5"] = np.stack([s.bmat for s in sh])
+    return out
+
+
+def gen_topk_c0():
+    """Round-0 TopK index sets of the first clients at the full c0 shape.
+
+    At x = 0 every sigmoid is 1/2, so H_i - lam I has massive exact ties at
+    the k-th boundary; the reference's lexsort tie rule decides them.
+    """
+    out = {}
+    shards = baseline_shards("c0", seed=1)
+    spec = CompressorSpec(CompressorKind.TOPK, k=2408)
+    for cid in (0, 1, 77, 141):
+        sh = shards[cid]
+        x = np.zeros(sh.dim)
+        s = oracle.new_scratch(sh)
+        oracle.refresh_scratch(sh, x, s)
+        h = oracle.hessian(sh, x, s)
+        hest = linalg.new_matrix(sh.dim)
+        linalg.add_to_diagonal(hest, sh.lam)
+        delta = compress(h - hest, spec, rng.derive_round_prg(1, cid, 0))
+        out[f"cid{cid}__idx"] = delta.indices
+        out[f"cid{cid}__val"] = delta.values
+    return out
+
+
+def main():
+    os.makedirs(OUT, exist_ok=True)
+    for fname, fn in (
+        ("rng.npz", gen_rng),
+        ("compress.npz", gen_compress),
+        ("oracle.npz", gen_oracle),
+        ("linalg.npz", gen_linalg),
+        ("data.npz", gen_data),
+        ("topk_c0_round0.npz", gen_topk_c0),
+        ("simulate.npz", gen_sim),
+    ):
+        print(f"generating {fname}")
+        np.savez_compressed(os.path.join(OUT, fname), **fn())
+    for f in sorted(os.listdir(OUT)):
+        print(f"{f}: {os.path.getsize(os.path.join(OUT, f))} bytes")
+
+
+if __name__ == "__main__":
+    main()
