@@ -1,0 +1,202 @@
+/*
+ * fednl_b200.h — C ABI of the B200-native FedNL round (libfednl_b200.so).
+ *
+ * Drop-in boundary for the reference's simulated FedNL path
+ * (arxiv/paper_2410_08760, /root/reference/pkg/src/fednl).  The reference is
+ * pure Python/numpy; the entry points below replace, one for one, the
+ * Python-level operations its simulator drives (citations are reference
+ * file:line).  The Python package paper_2410_08760_b200 binds them with
+ * ctypes; INTEGRATION.md shows the stub a reference maintainer would add.
+ *
+ * Conventions
+ *   - Plain pointers and sizes only; every pointer argument is HOST memory.
+ *     Device memory, the CUDA stream and the captured round graphs are owned
+ *     by the opaque context and never cross the ABI.
+ *   - Packed symmetric layout: upper triangle, column-wise,
+ *     t(i, j) = j (j + 1) / 2 + i for i <= j   (reference linalg.py:54-58).
+ *   - Shards: n host pointers, each an F-order (column-major) d x n_i double
+ *     matrix whose column j is label_j * (features_j, 1)  (oracle.py:33-46).
+ *   - Return value 0 = ok, otherwise an FB_ERR_* code; fb_last_error() and
+ *     fb_get_status() give the detail.  A context is not re-entrant: one host
+ *     thread per context.
+ */
+#ifndef FEDNL_B200_H
+#define FEDNL_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- return / status codes ------------------------------------------- */
+#define FB_OK 0
+#define FB_ERR_CUDA 1          /* CUDA runtime/driver failure                */
+#define FB_ERR_INVALID 2       /* bad argument / config (-> ValueError)      */
+#define FB_ERR_NOT_PD 3        /* linalg.py:24-33 NotPositiveDefiniteError   */
+#define FB_ERR_NONFINITE 4     /* compressors.py:134 non-finite input        */
+#define FB_ERR_DIVERGED 5      /* algorithms.py:52-57 DivergenceError        */
+#define FB_ERR_LINE_SEARCH 6   /* algorithms.py:41-49 LineSearchError        */
+#define FB_ERR_UNSUPPORTED 7   /* outside this build's envelope              */
+#define FB_ERR_LS_PENDING 8    /* internal: line search needs more trials    */
+
+/* compressor kinds (compressors.py:41-47) */
+#define FB_KIND_IDENTITY 0
+#define FB_KIND_TOPK 1
+#define FB_KIND_TOPLEK 2
+#define FB_KIND_RANDK 3
+#define FB_KIND_RANDSEQK 4
+#define FB_KIND_NATURAL 5
+
+/* algorithms (algorithms.py:35) */
+#define FB_ALG_FEDNL 0
+#define FB_ALG_LS 1
+#define FB_ALG_PP 2
+
+/* hessian_init (algorithms.py:37) */
+#define FB_INIT_LAMBDA_IDENTITY 0
+#define FB_INIT_ZERO 1
+#define FB_INIT_EXACT 2
+
+/* Mirror of the trajectory-defining RunConfig fields (algorithms.py:60-120)
+ * plus the shard shape.  alpha is the RESOLVED step (resolve_alpha,
+ * algorithms.py:138-139); ls_steps_table[s] = ls_gamma ** s as the host
+ * evaluates it (algorithms.py:305), s = 0..60. */
+typedef struct fb_config {
+  int32_t d;              /* dimension (features + intercept)          */
+  int32_t n_clients;      /* n                                          */
+  int32_t n_samples;      /* n_i, equal for every client                */
+  int32_t algorithm;      /* FB_ALG_*                                   */
+  int32_t kind;           /* FB_KIND_*                                  */
+  int32_t k;              /* budget for the sparse kinds, else 0        */
+  int32_t topk_weighted;  /* CompressorSpec.topk_weighted               */
+  int32_t tau;            /* FedNL-PP participants per round            */
+  int32_t hessian_init;   /* FB_INIT_*                                  */
+  int32_t reserved0;
+  double alpha;
+  double lam;
+  double ls_c;
+  double ls_gamma;
+  uint64_t run_seed;
+  double ls_steps_table[61];
+} fb_config;
+
+/* Detail of the last failure raised by a round (mirrors the reference's
+ * exception payloads). */
+typedef struct fb_status {
+  int32_t code;           /* FB_ERR_* or 0                               */
+  int32_t round;          /* round at which it was raised                */
+  int32_t pivot_index;    /* NotPositiveDefiniteError.pivot_index        */
+  int32_t client;         /* client whose input was non-finite           */
+  double pivot_value;     /* NotPositiveDefiniteError.pivot_value        */
+  double f_start;         /* LineSearchError: f at x                      */
+  double f_best;          /* LineSearchError: best trial f                */
+} fb_status;
+
+/* Per-kernel device time of the most recent fb_run_rounds(..., timed=1),
+ * averaged over its rounds (CUDA events on the launching stream). */
+typedef struct fb_profile {
+  int32_t rounds;
+  int32_t launches_per_round;   /* kernels launched per round            */
+  double ms_oracle;             /* margins + gradient                    */
+  double ms_hessian;            /* DMMA Hessian + shift-difference epilogue */
+  double ms_reduce;             /* cross-client reductions                */
+  double ms_compress;           /* compressor                             */
+  double ms_solve;              /* master Cholesky solve                  */
+  double ms_fold;               /* fused shift update + master fold       */
+  double ms_round;              /* whole round (graph launch to end)      */
+} fb_profile;
+
+/* ---- lifecycle -------------------------------------------------------- */
+/* Validate cfg, allocate every device buffer, build TMA descriptors.
+ * Replaces runtime.simulate's setup (runtime.py:145-155). */
+int fb_create(const fb_config* cfg, void** ctx);
+void fb_destroy(void* ctx);
+const char* fb_last_error(void* ctx);
+int fb_get_status(void* ctx, fb_status* out);
+int fb_device_info(char* name, int32_t name_len, int32_t* sm_count, int32_t* cc_major,
+                   int32_t* cc_minor);
+
+/* ---- data ------------------------------------------------------------- */
+/* Copy n shards to HBM (feature-major, sample-contiguous rows).  Host memory
+ * is only borrowed for the call.  Replaces ClientShard residency
+ * (oracle.py:33-46, data.py:186-213). */
+int fb_upload_shards(void* ctx, const double* const* bmats);
+
+/* ---- run -------------------------------------------------------------- */
+/* Round-0 state: client/master Hessian estimates per hessian_init and, for
+ * FedNL-PP, the shift / shifted-gradient state (algorithms.py:195-223,
+ * 331-349).  x0 may be NULL (zeros, as runtime.py:224). */
+int fb_init_state(void* ctx, const double* x0);
+
+/* Run rounds [first_round, first_round + count) — the body of
+ * runtime._simulate_loop (runtime.py:235-271).  Per round r (index
+ * i = r - first_round): grad_norm[i], f_value[i], ls_steps[i] as in the
+ * MetricsRow; entry_counts[i*n + c] = compressed entry count of client c
+ * (-1 when c did not participate, FedNL-PP); wall_ms[i] = device time from
+ * the start of the call to the end of round r.  When timed != 0 per-kernel
+ * CUDA-event times are collected (fb_get_profile).  Stops early at the first
+ * failure (status set, *rounds_done = rounds completed) or when
+ * stop_grad_norm >= 0 and a row's grad_norm <= stop_grad_norm. */
+int fb_run_rounds(void* ctx, int32_t first_round, int32_t count, double stop_grad_norm,
+                  int32_t timed, double* grad_norm, double* f_value, int32_t* ls_steps,
+                  int32_t* entry_counts, double* wall_ms, int32_t* rounds_done);
+
+/* ||mean grad(x)|| and mean f(x) at the current iterate (the final row,
+ * runtime.py:273-275). */
+int fb_final_eval(void* ctx, double* grad_norm, double* f_value);
+
+int fb_get_profile(void* ctx, fb_profile* out);
+
+/* ---- state taps (teacher forcing / debugging) ------------------------- */
+int fb_get_x(void* ctx, double* x);
+int fb_set_x(void* ctx, const double* x);
+/* client Hessian estimates H_i^k of clients [c0, c1), packed, row-major */
+int fb_get_client_hest(void* ctx, int32_t c0, int32_t c1, double* out);
+int fb_set_client_hest(void* ctx, int32_t c0, int32_t c1, const double* in);
+int fb_get_master_hest(void* ctx, double* out);
+int fb_set_master_hest(void* ctx, const double* in);
+/* FedNL-PP running state: master shift / gvec, per-client shift / gvec */
+int fb_get_pp_state(void* ctx, double* shift, double* gvec, double* cli_shift, double* cli_gvec);
+/* last round's packed difference D_i = H_i(x) - H_i^k of client cid */
+int fb_get_round_diff(void* ctx, int32_t cid, double* out);
+/* last round's compressed delta of client cid: ascending packed indices,
+ * values (already scaled for the Rand kinds), count */
+int fb_get_round_delta(void* ctx, int32_t cid, uint32_t* idx, double* val, int32_t* count);
+/* mean gradient of the last round and per-client gradients [n*d] */
+int fb_get_round_grads(void* ctx, double* mean_grad, double* client_grads);
+
+/* ---- leaf operations (parity entry points) ---------------------------- */
+/* compress(m, spec, prg) for every client at once (compressors.py:350-370):
+ * diffs = [n*w] packed inputs, seeds[c] = the fresh Prg's seed.  Outputs
+ * idx/val [n*w] (first count[c] valid per client), count [n], draws [n] =
+ * number of u64 draws consumed from each stream.  Returns FB_ERR_NONFINITE
+ * (status.client set) on a non-finite input. */
+int fb_compress(void* ctx, const double* diffs, const uint64_t* seeds, uint32_t* idx,
+                double* val, int32_t* count, int32_t* draws);
+/* local f / gradient / packed Hessian of every client at x
+ * (oracle.py:74-139); any output may be NULL. */
+int fb_oracle_eval(void* ctx, const double* x, double* f, double* grad, double* hess_packed);
+/* solve (H + shift I) z = rhs from packed H (algorithms.py:361-367 option b,
+ * linalg.py:151-186); FB_ERR_NOT_PD with status.pivot_* on failure. */
+int fb_shifted_solve(void* ctx, const double* h_packed, double shift, const double* rhs,
+                     double* z);
+
+/* ---- context-free device SplitMix64 (rng.py:37-136) -------------------- */
+int fb_prg_u64(uint64_t seed, int32_t count, uint64_t* out);
+/* reps draws of randrange(bounds[b]) from a fresh Prg(seed) per bound;
+ * out[b*reps + r]; next[b] = the following next_u64() */
+int fb_prg_randrange(uint64_t seed, const uint64_t* bounds, int32_t n_bounds, int32_t reps,
+                     uint64_t* out, uint64_t* next);
+int fb_prg_partial_shuffle(uint64_t seed, int64_t n, int32_t k, int64_t* out);
+int fb_round_seeds(uint64_t run_seed, int32_t n_clients, int32_t rnd, uint64_t* out);
+
+/* ---- measurement ------------------------------------------------------ */
+/* fp64 peak of this device: register-resident DMMA (mma.sync f64) and DFMA
+ * loops, TFLOP/s. */
+int fb_fp64_peak(double* dmma_tflops, double* dfma_tflops);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* FEDNL_B200_H */

@@ -1,0 +1,487 @@
+// compress_kernels.cuh — Hessian-shift compressors on packed differences
+// (reference compressors.py:132-370).
+//
+// Output of every kind, per client c:
+//   bitmap[c][wb]   selected packed positions (bit t%32 of word t/32)
+//   count[c]        number of entries (0 for an all-zero difference: no draws)
+//   idx/val lists   ascending positions and their values (values scaled by
+//                   w/k for the Rand kinds), capacity `cap` per client
+//   draws[c]        u64 draws consumed from the client's round stream
+// Dense kinds (identity, natural) set count = w and leave the bitmap unused.
+//
+// Bit-exactness notes:
+//  * TopK ranks |v| (or wt v v), descending, ties to the smaller position
+//    (np.lexsort, compressors.py:139-141).  |v| >= 0 doubles order like their
+//    63-bit patterns, so an exact radix select over (key, position) is used.
+//  * TopLEK replicates numpy's pairwise np.sum over the sorted energies and
+//    the sequential cumsum / division / searchsorted of toplek_plan.
+//  * Rand values are fl(v * (w / k)) with w / k a correctly rounded double.
+#pragma once
+#include "common.cuh"
+
+namespace fb {
+
+constexpr int TK_THREADS = 1024;
+constexpr int TK_NW = TK_THREADS / 32;
+
+// energy = (wt * v) * v exactly as numpy evaluates weights * packed * packed
+__device__ __forceinline__ double energy_of(double v, int64_t t) {
+  const double wt = packed_is_diag_fast(t) ? 1.0 : 2.0;
+  return __dmul_rn(__dmul_rn(wt, v), v);
+}
+__device__ __forceinline__ uint64_t rank_key(double v, int64_t t, int weighted) {
+  if (weighted) return static_cast<uint64_t>(__double_as_longlong(energy_of(v, t)));
+  return static_cast<uint64_t>(__double_as_longlong(v)) & 0x7FFFFFFFFFFFFFFFull;
+}
+
+// exclusive block scan of ints (blockDim.x a multiple of 32, <= 1024);
+// the block total is returned through `total`.  ws: 64 ints of smem.
+__device__ __forceinline__ int block_excl_scan(int v, int* ws, int* total) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  int x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  __syncthreads();
+  if (lane == 31) ws[wid] = x;
+  __syncthreads();
+  if (wid == 0) {
+    int s = (lane < nw) ? ws[lane] : 0;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, s, o);
+      if (lane >= o) s += y;
+    }
+    ws[32 + lane] = s;  // inclusive warp totals
+  }
+  __syncthreads();
+  const int before = (wid == 0) ? 0 : ws[32 + wid - 1];
+  *total = ws[32 + nw - 1];
+  return before + x - v;
+}
+
+__device__ __forceinline__ void clear_row(uint32_t* row, int wb) {
+  for (int q = threadIdx.x; q < wb; q += blockDim.x) row[q] = 0u;
+}
+
+// Compact a bitmap row into ascending (idx, val) lists; val = fl(v * scale)
+// when scale != 1 (Rand kinds).  Whole block, any blockDim multiple of 32.
+__device__ void compact_bitmap(const uint32_t* __restrict__ row, int wb,
+                               const double* __restrict__ v, double scale, uint32_t* idx,
+                               double* val, int* ws) {
+  int carry = 0;
+  for (int base = 0; base < wb; base += blockDim.x) {
+    const int q = base + threadIdx.x;
+    const uint32_t word = (q < wb) ? row[q] : 0u;
+    int total;
+    int off = block_excl_scan(__popc(word), ws, &total) + carry;
+    uint32_t m = word;
+    while (m) {
+      const int bit = __ffs(m) - 1;
+      m &= m - 1;
+      const int64_t t = static_cast<int64_t>(q) * 32 + bit;
+      idx[off] = static_cast<uint32_t>(t);
+      val[off] = (scale == 1.0) ? v[t] : __dmul_rn(v[t], scale);
+      ++off;
+    }
+    carry += total;
+    __syncthreads();
+  }
+}
+
+// ------------------------------------------------------------------- TopK
+// grid n_active, block 1024.
+__global__ void __launch_bounds__(TK_THREADS) k_topk(
+    const DevCtl* __restrict__ ctl, const double* __restrict__ D, int64_t w, int wb, int k,
+    int weighted, const int32_t* __restrict__ clients, const int32_t* __restrict__ flags,
+    uint32_t* __restrict__ bitmap, int32_t* __restrict__ count, uint32_t* __restrict__ idx_list,
+    double* __restrict__ val_list, int cap, int32_t* __restrict__ draws) {
+  if (ctl && ctl->halt) return;
+  __shared__ uint32_t hist[2048];
+  __shared__ int ws[64];
+  __shared__ int s_digit, s_above;
+  const int c = client_of(clients, blockIdx.x);
+  const double* v = D + static_cast<int64_t>(c) * w;
+  uint32_t* brow = bitmap + static_cast<int64_t>(c) * wb;
+  if (threadIdx.x == 0 && draws) draws[c] = 0;
+  if (!(flags[c] & 2)) {  // all-zero difference: empty delta, no draws
+    clear_row(brow, wb);
+    if (threadIdx.x == 0) count[c] = 0;
+    return;
+  }
+  const int lane = threadIdx.x & 31;
+  constexpr int LO[6] = {52, 41, 30, 19, 8, 0};
+  constexpr int BITS[6] = {11, 11, 11, 11, 11, 8};
+  uint64_t prefix = 0;  // selected digits so far (key >> (LO[L] + BITS[L]))
+  int need = k;
+  bool take_all = false;
+  int lo = 0;
+  for (int L = 0; L < 6; ++L) {
+    lo = LO[L];
+    const int bits = BITS[L];
+    const int hi = lo + bits;
+    const uint32_t mask = (1u << bits) - 1u;
+    for (int i = threadIdx.x; i < 2048; i += TK_THREADS) hist[i] = 0u;
+    __syncthreads();
+    for (int64_t base = 0; base < w; base += TK_THREADS) {
+      const int64_t t = base + threadIdx.x;
+      uint32_t dig = 0xFFFFFFFFu;
+      if (t < w) {
+        const uint64_t key = rank_key(v[t], t, weighted);
+        if ((hi >= 64 ? 0ull : (key >> hi)) == prefix) dig = static_cast<uint32_t>(key >> lo) & mask;
+      }
+      const uint32_t peers = __match_any_sync(0xffffffffu, dig);
+      if (dig != 0xFFFFFFFFu && lane == __ffs(peers) - 1) atomicAdd(&hist[dig], __popc(peers));
+    }
+    __syncthreads();
+    // locate the digit holding the need-th largest key: bins scanned from the top
+    {
+      const int b0 = 2047 - 2 * threadIdx.x, b1 = b0 - 1;  // descending pair
+      const int c0 = static_cast<int>(hist[b0]), c1 = static_cast<int>(hist[b1]);
+      int total;
+      const int above0 = block_excl_scan(c0 + c1, ws, &total);
+      const int above1 = above0 + c0;
+      if (above0 < need && need <= above0 + c0) { s_digit = b0; s_above = above0; }
+      if (c1 > 0 && above1 < need && need <= above1 + c1) { s_digit = b1; s_above = above1; }
+    }
+    __syncthreads();
+    const int dg = s_digit;
+    need -= s_above;
+    prefix = (prefix << bits) | static_cast<uint64_t>(dg);
+    const bool all = (static_cast<int>(hist[dg]) == need);
+    __syncthreads();
+    if (all) { take_all = true; break; }
+  }
+  // final pass: ascending compaction of {key > T} U {first `need` of key == T}
+  int carry_sel = 0, carry_eq = 0;
+  uint32_t* il = idx_list + static_cast<int64_t>(c) * cap;
+  double* vl = val_list + static_cast<int64_t>(c) * cap;
+  for (int64_t base = 0; base < w; base += TK_THREADS) {
+    const int64_t t = base + threadIdx.x;
+    int gt = 0, eq = 0;
+    double vt = 0.0;
+    if (t < w) {
+      vt = v[t];
+      const uint64_t hk = rank_key(vt, t, weighted) >> lo;
+      gt = hk > prefix;
+      eq = hk == prefix;
+    }
+    int sel = gt | eq;
+    if (!take_all) {
+      int tot_eq;
+      const int r = block_excl_scan(eq, ws, &tot_eq) + carry_eq;
+      carry_eq += tot_eq;
+      sel = gt | (eq & (r < need));
+    }
+    int tot_sel;
+    const int pos = block_excl_scan(sel, ws, &tot_sel) + carry_sel;
+    carry_sel += tot_sel;
+    if (sel) {
+      il[pos] = static_cast<uint32_t>(t);
+      vl[pos] = vt;
+    }
+    const uint32_t word = __ballot_sync(0xffffffffu, sel);
+    if (lane == 0 && t < w + 31) {
+      const int64_t q = t >> 5;
+      if (q < wb) brow[q] = word;
+    }
+  }
+  if (threadIdx.x == 0) count[c] = carry_sel;
+}
+
+// --------------------------------------------------------------- RandSeqK
+// grid n_active, block 256.  s = randrange(w) is the first and only draw
+// (compressors.py:259-264); positions (s + j) mod w, sorted.
+__global__ void __launch_bounds__(256) k_randseqk(
+    const DevCtl* __restrict__ ctl, const double* __restrict__ D, int64_t w, int wb, int k,
+    const int32_t* __restrict__ clients, const int32_t* __restrict__ flags, uint64_t run_seed,
+    const uint64_t* __restrict__ seeds, uint32_t* __restrict__ bitmap,
+    int32_t* __restrict__ count, uint32_t* __restrict__ idx_list, double* __restrict__ val_list,
+    int cap, int32_t* __restrict__ draws) {
+  if (ctl && ctl->halt) return;
+  __shared__ int64_t s_start;
+  const int c = client_of(clients, blockIdx.x);
+  uint32_t* brow = bitmap + static_cast<int64_t>(c) * wb;
+  if (!(flags[c] & 2)) {
+    clear_row(brow, wb);
+    if (threadIdx.x == 0) { count[c] = 0; if (draws) draws[c] = 0; }
+    return;
+  }
+  if (threadIdx.x == 0) {
+    const uint64_t seed = seeds ? seeds[blockIdx.x] : round_seed(run_seed, c, ctl->round);
+    Prg p(seed);
+    s_start = static_cast<int64_t>(p.randrange(static_cast<uint64_t>(w)));
+    if (draws) draws[c] = p.draws;
+    count[c] = k;
+  }
+  __syncthreads();
+  const int64_t s = s_start;
+  const int64_t wrap = (s + k > w) ? s + k - w : 0;
+  const double scale = static_cast<double>(w) / static_cast<double>(k);
+  const double* v = D + static_cast<int64_t>(c) * w;
+  uint32_t* il = idx_list + static_cast<int64_t>(c) * cap;
+  double* vl = val_list + static_cast<int64_t>(c) * cap;
+  for (int i = threadIdx.x; i < k; i += blockDim.x) {
+    const int64_t t = (i < wrap) ? i : s + (i - wrap);
+    il[i] = static_cast<uint32_t>(t);
+    vl[i] = __dmul_rn(v[t], scale);
+  }
+  for (int q = threadIdx.x; q < wb; q += blockDim.x) {
+    uint32_t word = 0u;
+    for (int bit = 0; bit < 32; ++bit) {
+      const int64_t t = static_cast<int64_t>(q) * 32 + bit;
+      if (t >= w) break;
+      const bool in = (t >= s && t < s + k) || (t < wrap);
+      word |= static_cast<uint32_t>(in) << bit;
+    }
+    brow[q] = word;
+  }
+}
+
+// ------------------------------------------------------------------ RandK
+// Partial Fisher-Yates prefix (rng.py:106-118, compressors.py:261-262).
+// grid n_active, block 32 (one warp per client).  The k draws are generated
+// in parallel from the counter-based stream; a rejection anywhere (probability
+// < k w / 2^64) drops to the exact sequential loop.  The swap chain then runs
+// on lane 0 over a sparse pool (open-addressing table in shared memory).
+constexpr int RK_TABLE = 16384;  // entries (key, value) -> 128 KB
+__device__ __forceinline__ int rk_slot(int32_t* keys, int32_t key) {
+  uint32_t h = (static_cast<uint32_t>(key) * 2654435761u) & (RK_TABLE - 1);
+  while (keys[h] != -1 && keys[h] != key) h = (h + 1) & (RK_TABLE - 1);
+  return static_cast<int>(h);
+}
+__global__ void __launch_bounds__(32) k_randk(
+    const DevCtl* __restrict__ ctl, const double* __restrict__ D, int64_t w, int wb, int k,
+    const int32_t* __restrict__ clients, const int32_t* __restrict__ flags, uint64_t run_seed,
+    const uint64_t* __restrict__ seeds, uint32_t* __restrict__ bitmap,
+    int32_t* __restrict__ count, uint32_t* __restrict__ idx_list, double* __restrict__ val_list,
+    int cap, int32_t* __restrict__ draws, int64_t* __restrict__ jbuf) {
+  if (ctl && ctl->halt) return;
+  extern __shared__ int32_t tab[];  // keys[RK_TABLE], vals[RK_TABLE]
+  __shared__ int ws[64];
+  __shared__ int s_reject;
+  int32_t* keys = tab;
+  int32_t* vals = tab + RK_TABLE;
+  const int c = client_of(clients, blockIdx.x);
+  const int lane = threadIdx.x;
+  uint32_t* brow = bitmap + static_cast<int64_t>(c) * wb;
+  clear_row(brow, wb);
+  if (!(flags[c] & 2)) {
+    if (lane == 0) { count[c] = 0; if (draws) draws[c] = 0; }
+    return;
+  }
+  const uint64_t seed = seeds ? seeds[blockIdx.x] : round_seed(run_seed, c, ctl->round);
+  int64_t* js = jbuf + static_cast<int64_t>(blockIdx.x) * cap;
+  if (lane == 0) s_reject = 0;
+  for (int i = lane; i < RK_TABLE; i += 32) keys[i] = -1;
+  __syncwarp();
+  // parallel draw i (1-based i+1) under the no-rejection hypothesis
+  for (int i = lane; i < k; i += 32) {
+    const uint64_t b = static_cast<uint64_t>(w - i);
+    const uint64_t u = scramble(seed + static_cast<uint64_t>(i + 1) * GOLDEN);
+    if (u < (0ull - b) % b) s_reject = 1;
+    js[i] = i + static_cast<int64_t>(u % b);
+  }
+  __syncwarp();
+  if (lane == 0) {
+    int ndraw = k;
+    if (s_reject) {  // exact sequential replay
+      Prg p(seed);
+      for (int i = 0; i < k; ++i) js[i] = i + static_cast<int64_t>(p.randrange(w - i));
+      ndraw = p.draws;
+    }
+    for (int i = 0; i < k; ++i) {
+      const int32_t j = static_cast<int32_t>(js[i]);
+      const int si = rk_slot(keys, i);
+      const int32_t vi = (keys[si] == i) ? vals[si] : i;
+      const int sj = rk_slot(keys, j);
+      const int32_t vj = (keys[sj] == j) ? vals[sj] : j;
+      keys[sj] = j; vals[sj] = vi;
+      const int si2 = rk_slot(keys, i);
+      keys[si2] = i; vals[si2] = vj;
+      atomicOr(&brow[vj >> 5], 1u << (vj & 31));
+    }
+    count[c] = k;
+    if (draws) draws[c] = ndraw;
+  }
+  __syncwarp();
+  __threadfence_block();
+  const double scale = static_cast<double>(w) / static_cast<double>(k);
+  compact_bitmap(brow, wb, D + static_cast<int64_t>(c) * w, scale,
+                 idx_list + static_cast<int64_t>(c) * cap, val_list + static_cast<int64_t>(c) * cap,
+                 ws);
+}
+
+// ----------------------------------------------------------------- TopLEK
+// grid n_active, block 1024, dynamic smem P * 12 bytes (P = pow2 >= w).
+// Full bitonic sort of (energy desc, position asc) so that numpy's pairwise
+// np.sum over the sorted energies can be replayed (compressors.py:179-233).
+__device__ double np_pairwise(const double* a, int n) {
+  if (n < 8) {
+    double r = 0.0;
+    for (int i = 0; i < n; ++i) r = __dadd_rn(r, a[i]);
+    return r;
+  }
+  if (n <= 128) {
+    double r[8];
+    for (int j = 0; j < 8; ++j) r[j] = a[j];
+    int i = 8;
+    for (; i < n - (n % 8); i += 8)
+      for (int j = 0; j < 8; ++j) r[j] = __dadd_rn(r[j], a[i + j]);
+    double res = __dadd_rn(__dadd_rn(__dadd_rn(r[0], r[1]), __dadd_rn(r[2], r[3])),
+                           __dadd_rn(__dadd_rn(r[4], r[5]), __dadd_rn(r[6], r[7])));
+    for (; i < n; ++i) res = __dadd_rn(res, a[i]);
+    return res;
+  }
+  int n2 = n / 2;
+  n2 -= n2 % 8;
+  return __dadd_rn(np_pairwise(a, n2), np_pairwise(a + n2, n - n2));
+}
+
+__global__ void __launch_bounds__(TK_THREADS) k_toplek(
+    DevCtl* __restrict__ ctl, const double* __restrict__ D, int64_t w, int wb, int k,
+    const int32_t* __restrict__ clients, const int32_t* __restrict__ flags, uint64_t run_seed,
+    const uint64_t* __restrict__ seeds, uint32_t* __restrict__ bitmap,
+    int32_t* __restrict__ count, uint32_t* __restrict__ idx_list, double* __restrict__ val_list,
+    int cap, int32_t* __restrict__ draws, int P) {
+  if (ctl && ctl->halt) return;
+  extern __shared__ uint8_t tl_raw[];
+  double* en = reinterpret_cast<double*>(tl_raw);                    // [P]
+  uint32_t* pos = reinterpret_cast<uint32_t*>(tl_raw + 8 * static_cast<size_t>(P));  // [P]
+  __shared__ int ws[64];
+  __shared__ int s_t;
+  const int c = client_of(clients, blockIdx.x);
+  const double* v = D + static_cast<int64_t>(c) * w;
+  uint32_t* brow = bitmap + static_cast<int64_t>(c) * wb;
+  clear_row(brow, wb);
+  if (!(flags[c] & 2)) {
+    if (threadIdx.x == 0) { count[c] = 0; if (draws) draws[c] = 0; }
+    return;
+  }
+  for (int i = threadIdx.x; i < P; i += blockDim.x) {
+    if (i < w) { en[i] = energy_of(v[i], i); pos[i] = i; }
+    else { en[i] = 0.0; pos[i] = 0xFFFFFFFFu; }
+  }
+  __syncthreads();
+  // bitonic sort: "before" = larger energy, then smaller position
+  for (int size = 2; size <= P; size <<= 1) {
+    for (int stride = size >> 1; stride > 0; stride >>= 1) {
+      for (int i = threadIdx.x; i < P; i += blockDim.x) {
+        const int j = i ^ stride;
+        if (j > i) {
+          const bool up = ((i & size) == 0);
+          const double ei = en[i], ej = en[j];
+          const uint32_t pi = pos[i], pj = pos[j];
+          const bool j_before_i = (ej > ei) || (ej == ei && pj < pi);
+          if (j_before_i == up) {
+            en[i] = ej; en[j] = ei;
+            pos[i] = pj; pos[j] = pi;
+          }
+        }
+      }
+      __syncthreads();
+    }
+  }
+  if (threadIdx.x == 0) {
+    const double total = np_pairwise(en, static_cast<int>(w));
+    const uint64_t seed = seeds ? seeds[blockIdx.x] : round_seed(run_seed, c, ctl->round);
+    Prg p(seed);
+    int tsel;
+    if (!(total > 0.0)) {  // compressors.py:185-186
+      ctl->bad_client = c;
+      raise_status(ctl, ST_TOPLEK_ZERO);
+      tsel = 0;
+    } else {
+      const double target = static_cast<double>(k) / static_cast<double>(w);
+      // shares[i] = cumsum[i] / total; first i with shares[i] >= target
+      double cum = 0.0, s_prev = 0.0, s_cur = 0.0;
+      int hi = -1;
+      for (int i = 0; i < k; ++i) {
+        cum = __dadd_rn(cum, en[i]);
+        const double sh = __ddiv_rn(cum, total);
+        if (sh >= target) { hi = i; s_cur = sh; break; }
+        s_prev = sh;
+      }
+      int lo_t, hi_t;
+      double p_lo;
+      if (hi < 0) {  // searchsorted index >= k
+        lo_t = hi_t = k; p_lo = 1.0;
+      } else {
+        hi_t = hi + 1;
+        lo_t = hi_t - 1;
+        const double share_lo = (lo_t == 0) ? 0.0 : s_prev;
+        const double share_hi = s_cur;
+        if (share_hi <= share_lo || share_hi <= target) {
+          lo_t = hi_t; p_lo = 1.0;
+        } else {
+          p_lo = __ddiv_rn(__dsub_rn(share_hi, target), __dsub_rn(share_hi, share_lo));
+          p_lo = fmin(fmax(p_lo, 0.0), 1.0);
+        }
+      }
+      tsel = (p.next_f64() < p_lo) ? lo_t : hi_t;
+    }
+    s_t = tsel;
+    count[c] = tsel;
+    if (draws) draws[c] = p.draws;
+  }
+  __syncthreads();
+  const int tsel = s_t;
+  for (int i = threadIdx.x; i < tsel; i += blockDim.x) {
+    const uint32_t t = pos[i];
+    atomicOr(&brow[t >> 5], 1u << (t & 31));
+  }
+  __syncthreads();
+  compact_bitmap(brow, wb, v, 1.0, idx_list + static_cast<int64_t>(c) * cap,
+                 val_list + static_cast<int64_t>(c) * cap, ws);
+}
+
+// --------------------------------------------------------- identity / natural
+// Dense kinds: count = w (or 0).  Natural rounds every coordinate to one of
+// its bracketing powers of two with draw t+1 of the stream
+// (compressors.py:289-336); the rounded values overwrite `out` (may alias D).
+__global__ void __launch_bounds__(256) k_dense_kind(
+    const DevCtl* __restrict__ ctl, const double* D, double* out,  // may alias
+    int64_t w, int natural, const int32_t* __restrict__ clients,
+    const int32_t* __restrict__ flags, uint64_t run_seed, const uint64_t* __restrict__ seeds,
+    int32_t* __restrict__ count, int32_t* __restrict__ draws) {
+  if (ctl && ctl->halt) return;
+  const int c = client_of(clients, blockIdx.y);
+  const bool nonzero = flags[c] & 2;
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    count[c] = nonzero ? static_cast<int32_t>(w) : 0;
+    if (draws) draws[c] = (nonzero && natural) ? static_cast<int32_t>(w) : 0;
+  }
+  if (!nonzero) return;
+  const int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (t >= w) return;
+  const double x = D[static_cast<int64_t>(c) * w + t];
+  if (!natural) {
+    if (out != D) out[static_cast<int64_t>(c) * w + t] = x;
+    return;
+  }
+  const uint64_t seed = seeds ? seeds[blockIdx.y] : round_seed(run_seed, c, ctl->round);
+  const double u =
+      static_cast<double>(scramble(seed + static_cast<uint64_t>(t + 1) * GOLDEN) >> 11) * 0x1.0p-53;
+  const double tiny = 0x1.0p-1022, huge = 0x1.0p+1023;
+  const double mag = fabs(x);
+  double low = 0.0, high = 0.0, p_up = 0.0;
+  if (mag >= tiny && mag < huge) {
+    int e;
+    frexp(mag, &e);
+    low = ldexp(0.5, e);
+    high = ldexp(1.0, e);
+    p_up = __ddiv_rn(__dsub_rn(mag, low), low);
+  } else if (mag > 0.0 && mag < tiny) {
+    high = tiny;
+    p_up = __ddiv_rn(mag, tiny);
+  } else if (mag >= huge) {
+    low = huge;
+    high = huge;
+  }
+  const double r = (u < p_up) ? high : low;
+  out[static_cast<int64_t>(c) * w + t] = (x < 0.0) ? -r : r;
+}
+
+}  // namespace fb

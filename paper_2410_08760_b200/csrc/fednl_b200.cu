@@ -1,0 +1,1241 @@
+// fednl_b200.cu — libfednl_b200.so: context, round graphs and the C ABI
+// declared in include/fednl_b200.h.
+//
+// One context = one simulated FedNL run on one GPU: all client shards, the
+// per-client Hessian estimates, the master state and the per-round scratch
+// live in HBM; each round is a captured CUDA graph replayed back to back
+// (the round index lives in device memory), so the host issues one graph
+// launch per round and reads the metrics rows once per chunk.
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/fednl_b200.h"
+#include "common.cuh"
+#include "compress_kernels.cuh"
+#include "fp64_peak.cuh"
+#include "hessian_dmma.cuh"
+#include "oracle_kernels.cuh"
+#include "round_kernels.cuh"
+#include "solve_kernels.cuh"
+
+using namespace fb;
+
+namespace {
+
+constexpr int ROW_CHUNK = 256;  // rounds per graph-replay chunk
+
+enum EvSlot {
+  EV_START = 0,
+  EV_ORACLE_END,
+  EV_HESS_END,
+  EV_REDUCE_END,
+  EV_COMP_START,
+  EV_COMP_END,
+  EV_SOLVE_END,
+  EV_FOLD_START,
+  EV_FOLD_END,
+  EV_END,
+  EV_COUNT
+};
+
+struct Ctx {
+  fb_config cfg{};
+  int d = 0, n = 0, ni = 0, ldj = 0, ldh = 0, nblk = 0, nb_tiles = 0, n_pairs = 0, wb = 0;
+  int cap = 0, tau = 0, n_active_max = 0;
+  int64_t w = 0;
+  double alpha_n = 0.0, rand_scale = 1.0;
+  int solve_cs = 1, solve_stage = 0;
+  size_t solve_smem = 0;
+  int toplek_P = 0;
+  bool uploaded = false, initialised = false;
+  std::string err;
+
+  cudaStream_t st = nullptr, st2 = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+
+  DevCtl* ctl = nullptr;
+  double *Bt = nullptr, *x = nullptr, *x_new = nullptr, *pvec = nullptr, *zbuf = nullptr;
+  double *hcoef = nullptr, *gcoef = nullptr, *loss_part = nullptr, *grad = nullptr;
+  double *gbar = nullptr, *f_cli = nullptr, *shift_cli = nullptr, *frob_part = nullptr;
+  int32_t* flags = nullptr;
+  double *hest = nullptr, *D = nullptr, *hmas = nullptr, *M = nullptr, *zeros_w = nullptr;
+  uint32_t* bitmap = nullptr;
+  int32_t *count = nullptr, *draws = nullptr;
+  uint32_t* idx_list = nullptr;
+  double* val_list = nullptr;
+  int64_t* jbuf = nullptr;
+  uint64_t* seeds = nullptr;
+  RoundScalars* sc = nullptr;
+  double *steps_table = nullptr, *trial_x = nullptr, *ls_loss_part = nullptr;
+  int32_t *subset = nullptr, *pool = nullptr;
+  double *hess_part = nullptr, *cli_shift = nullptr, *cli_gvec = nullptr, *gvec = nullptr;
+  double *pp_shift = nullptr, *dshift = nullptr, *dgvec = nullptr, *scalar = nullptr;
+  double *row_grad = nullptr, *row_f = nullptr;
+  int32_t *row_counts = nullptr, *row_ls = nullptr;
+
+  CUtensorMap tmap{};
+
+  cudaGraph_t graph = nullptr;
+  cudaGraphExec_t gexec = nullptr;
+  cudaEvent_t ev_fixed[EV_COUNT] = {};
+  cudaGraphNode_t ev_node[EV_COUNT] = {};
+  bool ev_used[EV_COUNT] = {};
+  std::vector<cudaEvent_t> ev_pool;  // [ROW_CHUNK][EV_COUNT]
+  fb_profile prof{};
+  int launches_per_round = 0;
+
+  std::vector<void*> allocs;
+};
+
+thread_local std::string g_err;
+
+#define CK(call)                                                                   \
+  do {                                                                             \
+    cudaError_t e_ = (call);                                                       \
+    if (e_ != cudaSuccess) {                                                       \
+      char b_[512];                                                                \
+      snprintf(b_, sizeof b_, "%s failed: %s (%s:%d)", #call, cudaGetErrorString(e_), \
+               __FILE__, __LINE__);                                                \
+      ctx->err = b_;                                                               \
+      return FB_ERR_CUDA;                                                          \
+    }                                                                              \
+  } while (0)
+
+#define CKL()                                                                      \
+  do {                                                                             \
+    cudaError_t e_ = cudaGetLastError();                                           \
+    if (e_ != cudaSuccess) {                                                       \
+      char b_[512];                                                                \
+      snprintf(b_, sizeof b_, "kernel launch failed: %s (%s:%d)", cudaGetErrorString(e_), \
+               __FILE__, __LINE__);                                                \
+      ctx->err = b_;                                                               \
+      return FB_ERR_CUDA;                                                          \
+    }                                                                              \
+  } while (0)
+
+template <typename T>
+int dalloc(Ctx* ctx, T** p, size_t count) {
+  if (count == 0) count = 1;
+  void* q = nullptr;
+  CK(cudaMalloc(&q, count * sizeof(T)));
+  CK(cudaMemset(q, 0, count * sizeof(T)));
+  ctx->allocs.push_back(q);
+  *p = static_cast<T*>(q);
+  return FB_OK;
+}
+
+#define TRY(expr)              \
+  do {                         \
+    int r_ = (expr);           \
+    if (r_ != FB_OK) return r_; \
+  } while (0)
+
+int invalid(Ctx* ctx, const char* msg) {
+  if (ctx) ctx->err = msg;
+  else g_err = msg;
+  return FB_ERR_INVALID;
+}
+
+// ---------------------------------------------------------------- TMA map
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                  const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                  const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                  CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+int make_tmap(Ctx* ctx) {
+  void* fn = nullptr;
+  cudaDriverEntryPointQueryResult q;
+  CK(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q));
+  if (q != cudaDriverEntryPointSuccess || !fn) {
+    ctx->err = "cuTensorMapEncodeTiled entry point not found";
+    return FB_ERR_CUDA;
+  }
+  const cuuint64_t dims[3] = {static_cast<cuuint64_t>(ctx->ni), static_cast<cuuint64_t>(ctx->d),
+                              static_cast<cuuint64_t>(ctx->n)};
+  const cuuint64_t strides[2] = {static_cast<cuuint64_t>(ctx->ldj) * 8,
+                                 static_cast<cuuint64_t>(ctx->ldj) * ctx->d * 8};
+  const cuuint32_t box[3] = {HKC, HT, 1};
+  const cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = reinterpret_cast<EncodeTiledFn>(fn)(
+      &ctx->tmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, ctx->Bt, dims, strides, box, estr,
+      CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    ctx->err = "cuTensorMapEncodeTiled failed (code " + std::to_string(static_cast<int>(r)) + ")";
+    return FB_ERR_CUDA;
+  }
+  return FB_OK;
+}
+
+// -------------------------------------------------------------- launchers
+int launch_margins(Ctx* ctx, cudaStream_t s, const double* x, const int32_t* clients, int n_active,
+                   bool with_ctl = true) {
+  dim3 grid(ctx->nblk, n_active);
+  k_margins<<<grid, MARGIN_THREADS, ctx->d * sizeof(double), s>>>(
+      with_ctl ? ctx->ctl : nullptr, ctx->Bt, ctx->d, ctx->ni, ctx->ldj, ctx->ldh, x, clients,
+      ctx->hcoef, ctx->gcoef, ctx->loss_part, ctx->nblk);
+  CKL();
+  return FB_OK;
+}
+int launch_gradient(Ctx* ctx, cudaStream_t s, const double* x, const int32_t* clients,
+                    int n_active, bool with_ctl = true) {
+  dim3 grid((ctx->d + 7) / 8, n_active);
+  k_gradient<<<grid, 256, 0, s>>>(with_ctl ? ctx->ctl : nullptr, ctx->Bt, ctx->d, ctx->ni,
+                                  ctx->ldj, ctx->ldh, x, ctx->cfg.lam, clients, ctx->gcoef,
+                                  ctx->grad);
+  CKL();
+  return FB_OK;
+}
+int launch_hessian(Ctx* ctx, cudaStream_t s, const int32_t* clients, int n_active,
+                   const double* hest, int64_t hest_stride, double* D, double* hess_out,
+                   bool with_ctl = true) {
+  dim3 grid(ctx->n_pairs, n_active);
+  k_hessian<<<grid, HTHREADS, HESS_SMEM, s>>>(ctx->tmap, with_ctl ? ctx->ctl : nullptr, ctx->d,
+                                              ctx->ni, ctx->ldh, ctx->hcoef, ctx->cfg.lam, clients,
+                                              hest, hest_stride, D, hess_out, ctx->frob_part,
+                                              ctx->flags);
+  CKL();
+  return FB_OK;
+}
+int launch_reduce(Ctx* ctx, cudaStream_t s, const double* x, const int32_t* clients, int n_active,
+                  int n_div, bool with_frob, double* row_grad, double* row_f) {
+  k_reduce<<<1, 1024, 0, s>>>(ctx->ctl, n_active, clients, n_div, ctx->d, ctx->ni, ctx->nblk,
+                              ctx->n_pairs, x, ctx->cfg.lam, ctx->grad, ctx->loss_part,
+                              with_frob ? ctx->frob_part : nullptr, ctx->flags, ctx->gbar,
+                              ctx->f_cli, ctx->shift_cli, ctx->sc, row_grad, row_f);
+  CKL();
+  return FB_OK;
+}
+// compressor of the configured kind over `n_active` clients; seeds null =
+// per-(client, round) streams from the device round counter.
+int launch_compress(Ctx* ctx, cudaStream_t s, const int32_t* clients, int n_active,
+                    const uint64_t* seeds, double* dense_out, bool with_ctl = true) {
+  const fb_config& c = ctx->cfg;
+  DevCtl* ctl = with_ctl ? ctx->ctl : nullptr;
+  switch (c.kind) {
+    case FB_KIND_TOPK:
+      k_topk<<<n_active, TK_THREADS, 0, s>>>(ctl, ctx->D, ctx->w, ctx->wb, c.k, c.topk_weighted,
+                                             clients, ctx->flags, ctx->bitmap, ctx->count,
+                                             ctx->idx_list, ctx->val_list, ctx->cap, ctx->draws);
+      break;
+    case FB_KIND_RANDSEQK:
+      k_randseqk<<<n_active, 256, 0, s>>>(ctl, ctx->D, ctx->w, ctx->wb, c.k, clients, ctx->flags,
+                                          c.run_seed, seeds, ctx->bitmap, ctx->count,
+                                          ctx->idx_list, ctx->val_list, ctx->cap, ctx->draws);
+      break;
+    case FB_KIND_RANDK:
+      k_randk<<<n_active, 32, 2 * RK_TABLE * sizeof(int32_t), s>>>(
+          ctl, ctx->D, ctx->w, ctx->wb, c.k, clients, ctx->flags, c.run_seed, seeds, ctx->bitmap,
+          ctx->count, ctx->idx_list, ctx->val_list, ctx->cap, ctx->draws, ctx->jbuf);
+      break;
+    case FB_KIND_TOPLEK:
+      k_toplek<<<n_active, TK_THREADS, static_cast<size_t>(ctx->toplek_P) * 12, s>>>(
+          ctl ? ctl : ctx->ctl, ctx->D, ctx->w, ctx->wb, c.k, clients, ctx->flags, c.run_seed,
+          seeds, ctx->bitmap, ctx->count, ctx->idx_list, ctx->val_list, ctx->cap, ctx->draws,
+          ctx->toplek_P);
+      break;
+    case FB_KIND_IDENTITY:
+    case FB_KIND_NATURAL: {
+      dim3 grid(static_cast<unsigned>((ctx->w + 255) / 256), n_active);
+      k_dense_kind<<<grid, 256, 0, s>>>(ctl, ctx->D, dense_out ? dense_out : ctx->D, ctx->w,
+                                        c.kind == FB_KIND_NATURAL, clients, ctx->flags,
+                                        c.run_seed, seeds, ctx->count, ctx->draws);
+      break;
+    }
+    default:
+      return invalid(ctx, "unknown compressor kind");
+  }
+  CKL();
+  return FB_OK;
+}
+int launch_solve(Ctx* ctx, cudaStream_t s, const double* hpk, const double* shift_ptr,
+                 const double* rhs, const double* x, double* z, double* x_out, int mode,
+                 int ignore_halt) {
+  cudaLaunchConfig_t lc{};
+  lc.gridDim = dim3(ctx->solve_cs);
+  lc.blockDim = dim3(CH_THREADS);
+  lc.dynamicSmemBytes = ctx->solve_smem;
+  lc.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = ctx->solve_cs;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  lc.attrs = attr;
+  lc.numAttrs = 1;
+  CK(cudaLaunchKernelEx(&lc, k_chol_solve, ctx->ctl, ctx->d, hpk, shift_ptr, rhs, x, ctx->M, z,
+                        x_out, mode, ctx->solve_stage, ignore_halt));
+  return FB_OK;
+}
+int launch_fold(Ctx* ctx, cudaStream_t s, const int32_t* clients, int n_active, double* hest,
+                double* hmas) {
+  const int dense = (ctx->cfg.kind == FB_KIND_IDENTITY || ctx->cfg.kind == FB_KIND_NATURAL);
+  k_fold<<<static_cast<unsigned>((ctx->w + 255) / 256), 256, 0, s>>>(
+      ctx->ctl, ctx->w, ctx->wb, n_active, clients, dense, ctx->rand_scale, ctx->cfg.alpha,
+      ctx->alpha_n, ctx->D, ctx->bitmap, ctx->count, hest, hmas);
+  CKL();
+  return FB_OK;
+}
+
+int record(Ctx* ctx, EvSlot slot, cudaStream_t s) {
+  ctx->ev_used[slot] = true;
+  CK(cudaEventRecord(ctx->ev_fixed[slot], s));
+  return FB_OK;
+}
+
+// ---------------------------------------------------------- round bodies
+int enqueue_fednl_round(Ctx* ctx) {
+  cudaStream_t s = ctx->st;
+  const int n = ctx->n;
+  const bool ls = ctx->cfg.algorithm == FB_ALG_LS;
+  TRY(record(ctx, EV_START, s));
+  CK(cudaMemsetAsync(ctx->flags, 0, sizeof(int32_t) * n, s));
+  TRY(launch_margins(ctx, s, ctx->x, nullptr, n));
+  TRY(launch_gradient(ctx, s, ctx->x, nullptr, n));
+  TRY(record(ctx, EV_ORACLE_END, s));
+  TRY(launch_hessian(ctx, s, nullptr, n, ctx->hest, ctx->w, ctx->D, nullptr));
+  TRY(record(ctx, EV_HESS_END, s));
+  TRY(launch_reduce(ctx, s, ctx->x, nullptr, n, n, true, ctx->row_grad, ctx->row_f));
+  TRY(record(ctx, EV_REDUCE_END, s));
+  // fork: compressor on st2 while the master solves on st
+  CK(cudaEventRecord(ctx->ev_fork, s));
+  CK(cudaStreamWaitEvent(ctx->st2, ctx->ev_fork, 0));
+  TRY(record(ctx, EV_COMP_START, ctx->st2));
+  TRY(launch_compress(ctx, ctx->st2, nullptr, n, nullptr, nullptr));
+  TRY(record(ctx, EV_COMP_END, ctx->st2));
+  CK(cudaEventRecord(ctx->ev_join, ctx->st2));
+  TRY(launch_solve(ctx, s, ctx->hmas, &ctx->sc->shift_mean, ctx->gbar, ctx->x, ctx->pvec,
+                   ctx->x_new, ls ? 2 : 0, 0));
+  TRY(record(ctx, EV_SOLVE_END, s));
+  int launches = 8;
+  if (ls) {
+    k_dot<<<1, 256, 0, s>>>(ctx->ctl, ctx->d, ctx->gbar, ctx->pvec, ctx->sc);
+    CKL();
+    dim3 grid(ctx->nblk, n);
+    k_ls_trials<<<grid, MARGIN_THREADS, LS_BATCH * ctx->d * sizeof(double), s>>>(
+        ctx->ctl, ctx->Bt, ctx->d, ctx->ni, ctx->ldj, ctx->x, ctx->pvec, ctx->steps_table, n,
+        ctx->trial_x, ctx->ls_loss_part, ctx->nblk);
+    CKL();
+    k_ls_decide<<<1, 256, 0, s>>>(ctx->ctl, ctx->d, n, ctx->ni, ctx->nblk, ctx->cfg.lam,
+                                  ctx->cfg.ls_c, ctx->steps_table, ctx->trial_x,
+                                  ctx->ls_loss_part, ctx->sc, ctx->x_new, LS_BATCH);
+    CKL();
+    launches += 3;
+  }
+  CK(cudaStreamWaitEvent(s, ctx->ev_join, 0));
+  TRY(record(ctx, EV_FOLD_START, s));
+  TRY(launch_fold(ctx, s, nullptr, n, ctx->hest, ctx->hmas));
+  TRY(record(ctx, EV_FOLD_END, s));
+  k_finish<<<1, 256, 0, s>>>(ctx->ctl, ctx->d, n, n, nullptr, ctx->x, ctx->x_new, 1, ctx->count,
+                             ctx->row_counts, ctx->row_ls);
+  CKL();
+  TRY(record(ctx, EV_END, s));
+  ctx->launches_per_round = launches;
+  return FB_OK;
+}
+
+// post-line-search tail of an LS round (fold + finish), launched directly by
+// the host after it drove extra trial batches
+int enqueue_ls_tail(Ctx* ctx) {
+  cudaStream_t s = ctx->st;
+  TRY(launch_fold(ctx, s, nullptr, ctx->n, ctx->hest, ctx->hmas));
+  k_finish<<<1, 256, 0, s>>>(ctx->ctl, ctx->d, ctx->n, ctx->n, nullptr, ctx->x, ctx->x_new, 1,
+                             ctx->count, ctx->row_counts, ctx->row_ls);
+  CKL();
+  return FB_OK;
+}
+
+__global__ void k_check_finite(DevCtl* ctl, int d, const double* x) {
+  if (ctl->halt) return;
+  __shared__ int bad;
+  if (threadIdx.x == 0) bad = 0;
+  __syncthreads();
+  for (int a = threadIdx.x; a < d; a += blockDim.x)
+    if (!isfinite(x[a])) bad = 1;
+  __syncthreads();
+  if (threadIdx.x == 0 && bad) raise_status(ctl, ST_DIVERGED);
+}
+
+int enqueue_pp_round(Ctx* ctx) {
+  cudaStream_t s = ctx->st;
+  const int n = ctx->n, tau = ctx->tau;
+  TRY(record(ctx, EV_START, s));
+  // metric probes over all clients at the current iterate (runtime.py:237-238)
+  TRY(launch_margins(ctx, s, ctx->x, nullptr, n));
+  TRY(launch_gradient(ctx, s, ctx->x, nullptr, n));
+  TRY(launch_reduce(ctx, s, ctx->x, nullptr, n, n, false, ctx->row_grad, ctx->row_f));
+  // participants and the new point (algorithms.py:422-433)
+  k_pp_select<<<1, 32, 0, s>>>(ctx->ctl, n, tau, ctx->subset, ctx->pool);
+  CKL();
+  TRY(launch_solve(ctx, s, ctx->hmas, ctx->pp_shift, ctx->gvec, nullptr, ctx->pvec, ctx->x, 1, 0));
+  k_check_finite<<<1, 256, 0, s>>>(ctx->ctl, ctx->d, ctx->x);
+  CKL();
+  TRY(record(ctx, EV_SOLVE_END, s));
+  // participants' oracle at x_new (algorithms.py:240-249)
+  CK(cudaMemsetAsync(ctx->flags, 0, sizeof(int32_t) * n, s));
+  TRY(launch_margins(ctx, s, ctx->x, ctx->subset, tau));
+  TRY(launch_gradient(ctx, s, ctx->x, ctx->subset, tau));
+  TRY(record(ctx, EV_ORACLE_END, s));
+  TRY(launch_hessian(ctx, s, ctx->subset, tau, ctx->hest, ctx->w, ctx->D, ctx->hess_part));
+  TRY(record(ctx, EV_HESS_END, s));
+  k_check_flags_pp<<<1, 32, 0, s>>>(ctx->ctl, tau, ctx->subset, ctx->flags);
+  CKL();
+  TRY(record(ctx, EV_REDUCE_END, s));
+  TRY(record(ctx, EV_COMP_START, s));
+  TRY(launch_compress(ctx, s, ctx->subset, tau, nullptr, nullptr));
+  TRY(record(ctx, EV_COMP_END, s));
+  TRY(record(ctx, EV_FOLD_START, s));
+  TRY(launch_fold(ctx, s, ctx->subset, tau, ctx->hest, nullptr));
+  k_pp_client<<<tau, 256, 0, s>>>(ctx->ctl, ctx->d, ctx->subset, ctx->hest, ctx->hess_part, ctx->x,
+                                  ctx->grad, ctx->cli_shift, ctx->cli_gvec, ctx->dshift,
+                                  ctx->dgvec);
+  CKL();
+  k_pp_master<<<1, 256, 0, s>>>(ctx->ctl, ctx->d, n, tau, ctx->dshift, ctx->dgvec, ctx->gvec,
+                                ctx->pp_shift);
+  CKL();
+  TRY(launch_fold(ctx, s, ctx->subset, tau, nullptr, ctx->hmas));
+  TRY(record(ctx, EV_FOLD_END, s));
+  k_finish<<<1, 256, 0, s>>>(ctx->ctl, ctx->d, n, tau, ctx->subset, ctx->x, nullptr, 0, ctx->count,
+                             ctx->row_counts, ctx->row_ls);
+  CKL();
+  TRY(record(ctx, EV_END, s));
+  ctx->launches_per_round = 15;
+  return FB_OK;
+}
+
+int build_graph(Ctx* ctx) {
+  if (ctx->gexec) return FB_OK;
+  for (int i = 0; i < EV_COUNT; ++i) ctx->ev_used[i] = false;
+  CK(cudaStreamBeginCapture(ctx->st, cudaStreamCaptureModeThreadLocal));
+  int r = (ctx->cfg.algorithm == FB_ALG_PP) ? enqueue_pp_round(ctx) : enqueue_fednl_round(ctx);
+  cudaGraph_t g = nullptr;
+  cudaError_t e = cudaStreamEndCapture(ctx->st, &g);
+  if (r != FB_OK) {
+    if (g) cudaGraphDestroy(g);
+    return r;
+  }
+  CK(e);
+  ctx->graph = g;
+  // locate the event-record nodes so timed runs can retarget them
+  size_t nn = 0;
+  CK(cudaGraphGetNodes(g, nullptr, &nn));
+  std::vector<cudaGraphNode_t> nodes(nn);
+  CK(cudaGraphGetNodes(g, nodes.data(), &nn));
+  for (auto nd : nodes) {
+    cudaGraphNodeType ty;
+    CK(cudaGraphNodeGetType(nd, &ty));
+    if (ty != cudaGraphNodeTypeEventRecord) continue;
+    cudaEvent_t ev;
+    CK(cudaGraphEventRecordNodeGetEvent(nd, &ev));
+    for (int i = 0; i < EV_COUNT; ++i)
+      if (ev == ctx->ev_fixed[i]) ctx->ev_node[i] = nd;
+  }
+  CK(cudaGraphInstantiate(&ctx->gexec, g, 0));
+  return FB_OK;
+}
+
+int read_status(Ctx* ctx, DevCtl* host_ctl) {
+  CK(cudaMemcpyAsync(host_ctl, ctx->ctl, sizeof(DevCtl), cudaMemcpyDeviceToHost, ctx->st));
+  CK(cudaStreamSynchronize(ctx->st));
+  return FB_OK;
+}
+
+int status_to_code(int32_t code) {
+  switch (code) {
+    case ST_OK: return FB_OK;
+    case ST_NOT_PD: return FB_ERR_NOT_PD;
+    case ST_NONFINITE: return FB_ERR_NONFINITE;
+    case ST_TOPLEK_ZERO: return FB_ERR_INVALID;
+    case ST_DIVERGED: return FB_ERR_DIVERGED;
+    case ST_LINE_SEARCH: return FB_ERR_LINE_SEARCH;
+    case ST_LS_PENDING: return FB_ERR_LS_PENDING;
+    default: return FB_ERR_CUDA;
+  }
+}
+
+int clear_status(Ctx* ctx) {
+  DevCtl h;
+  TRY(read_status(ctx, &h));
+  h.halt = 0;
+  h.code = 0;
+  h.code_round = 0;
+  h.ls_next = 0;
+  CK(cudaMemcpyAsync(ctx->ctl, &h, sizeof(DevCtl), cudaMemcpyHostToDevice, ctx->st));
+  CK(cudaStreamSynchronize(ctx->st));
+  return FB_OK;
+}
+
+}  // namespace
+
+// ======================================================================
+// C ABI
+// ======================================================================
+extern "C" {
+
+const char* fb_last_error(void* handle) {
+  Ctx* ctx = static_cast<Ctx*>(handle);
+  return ctx ? ctx->err.c_str() : g_err.c_str();
+}
+
+int fb_device_info(char* name, int32_t name_len, int32_t* sm_count, int32_t* cc_major,
+                   int32_t* cc_minor) {
+  int dev = 0;
+  cudaDeviceProp p;
+  if (cudaGetDevice(&dev) != cudaSuccess || cudaGetDeviceProperties(&p, dev) != cudaSuccess) {
+    g_err = "no CUDA device";
+    return FB_ERR_CUDA;
+  }
+  if (name && name_len > 0) {
+    strncpy(name, p.name, name_len - 1);
+    name[name_len - 1] = 0;
+  }
+  if (sm_count) *sm_count = p.multiProcessorCount;
+  if (cc_major) *cc_major = p.major;
+  if (cc_minor) *cc_minor = p.minor;
+  return FB_OK;
+}
+
+int fb_create(const fb_config* cfg_in, void** out) {
+  if (!cfg_in || !out) return invalid(nullptr, "null argument");
+  *out = nullptr;
+  const fb_config& c = *cfg_in;
+  if (c.d < 1 || c.n_clients < 1 || c.n_samples < 1) return invalid(nullptr, "bad shape");
+  if (c.d > 1024) return invalid(nullptr, "d > 1024 is outside this build's envelope");
+  if (c.n_clients >= (1 << 24)) return invalid(nullptr, "too many clients");
+  const int64_t w = packed_len(c.d);
+  if (c.kind < FB_KIND_IDENTITY || c.kind > FB_KIND_NATURAL) return invalid(nullptr, "bad kind");
+  const bool sparse = c.kind == FB_KIND_TOPK || c.kind == FB_KIND_TOPLEK ||
+                      c.kind == FB_KIND_RANDK || c.kind == FB_KIND_RANDSEQK;
+  if (sparse && (c.k < 1 || c.k > w)) return invalid(nullptr, "k out of range");
+  if (c.algorithm == FB_ALG_PP && (c.tau < 1 || c.tau > c.n_clients))
+    return invalid(nullptr, "tau out of range");
+  if (c.kind == FB_KIND_TOPLEK && w > 8192)
+    return invalid(nullptr, "toplek with d(d+1)/2 > 8192 is outside this build's envelope");
+  if (c.kind == FB_KIND_RANDK && std::min<int64_t>(w, 2 * static_cast<int64_t>(c.k)) > 12000)
+    return invalid(nullptr, "randk with min(w, 2k) > 12000 is outside this build's envelope");
+
+  Ctx* ctx = new Ctx();
+  ctx->cfg = c;
+  ctx->d = c.d;
+  ctx->n = c.n_clients;
+  ctx->ni = c.n_samples;
+  ctx->w = w;
+  ctx->ldj = (c.n_samples + 1) & ~1;
+  ctx->ldh = (c.n_samples + 15) & ~15;
+  ctx->nblk = (ctx->ldh + MARGIN_THREADS - 1) / MARGIN_THREADS;
+  ctx->nb_tiles = (c.d + HT - 1) / HT;
+  ctx->n_pairs = ctx->nb_tiles * (ctx->nb_tiles + 1) / 2;
+  ctx->wb = static_cast<int>((w + 31) / 32);
+  ctx->cap = sparse ? c.k : 1;
+  ctx->tau = c.algorithm == FB_ALG_PP ? c.tau : c.n_clients;
+  ctx->alpha_n = c.alpha / static_cast<double>(c.n_clients);
+  ctx->rand_scale = (c.kind == FB_KIND_RANDK || c.kind == FB_KIND_RANDSEQK)
+                        ? static_cast<double>(w) / static_cast<double>(c.k)
+                        : 1.0;
+  ctx->toplek_P = 1;
+  while (ctx->toplek_P < w) ctx->toplek_P <<= 1;
+  // master solve: a cluster of up to 8 CTAs; panel staged in smem when it fits
+  ctx->solve_cs = c.d >= 96 ? CH_MAX_CLUSTER : 1;
+  const size_t pan = static_cast<size_t>(c.d) * CH_PLD * sizeof(double);
+  ctx->solve_stage = pan <= 190 * 1024 ? 1 : 0;
+  ctx->solve_smem = ctx->solve_stage ? pan : 0;
+
+  int rc = FB_OK;
+  auto fail = [&](int code) {
+    rc = code;
+    g_err = ctx->err;
+    fb_destroy(ctx);
+    return code;
+  };
+  if (cudaSetDevice(0) != cudaSuccess) {
+    ctx->err = "cudaSetDevice(0) failed";
+    return fail(FB_ERR_CUDA);
+  }
+  int dev = 0;
+  cudaDeviceProp prop;
+  if (cudaGetDeviceProperties(&prop, dev) != cudaSuccess || prop.major != 10) {
+    ctx->err = "libfednl_b200 needs an sm_100 (B200) device";
+    return fail(FB_ERR_CUDA);
+  }
+#define CKC(call)                                                     \
+  do {                                                                \
+    cudaError_t e_ = (call);                                          \
+    if (e_ != cudaSuccess) {                                          \
+      ctx->err = std::string(#call) + ": " + cudaGetErrorString(e_);  \
+      return fail(FB_ERR_CUDA);                                       \
+    }                                                                 \
+  } while (0)
+  CKC(cudaStreamCreateWithFlags(&ctx->st, cudaStreamNonBlocking));
+  CKC(cudaStreamCreateWithFlags(&ctx->st2, cudaStreamNonBlocking));
+  CKC(cudaEventCreateWithFlags(&ctx->ev_fork, cudaEventDisableTiming));
+  CKC(cudaEventCreateWithFlags(&ctx->ev_join, cudaEventDisableTiming));
+  for (int i = 0; i < EV_COUNT; ++i) CKC(cudaEventCreate(&ctx->ev_fixed[i]));
+  ctx->ev_pool.resize(static_cast<size_t>(ROW_CHUNK) * EV_COUNT);
+  for (auto& e : ctx->ev_pool) CKC(cudaEventCreate(&e));
+  CKC(cudaFuncSetAttribute(k_hessian, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           static_cast<int>(HESS_SMEM)));
+  CKC(cudaFuncSetAttribute(k_randk, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           static_cast<int>(2 * RK_TABLE * sizeof(int32_t))));
+  CKC(cudaFuncSetAttribute(k_toplek, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           static_cast<int>(static_cast<size_t>(std::max(ctx->toplek_P, 1)) * 12)));
+  CKC(cudaFuncSetAttribute(k_chol_solve, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           static_cast<int>(std::max<size_t>(ctx->solve_smem, 1))));
+  CKC(cudaFuncSetAttribute(k_chol_solve, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+
+  const int n = ctx->n, d = ctx->d;
+  const size_t wn = static_cast<size_t>(w) * n;
+  const int tau = ctx->tau;
+  if (dalloc(ctx, &ctx->ctl, 1) || dalloc(ctx, &ctx->Bt, static_cast<size_t>(n) * d * ctx->ldj) ||
+      dalloc(ctx, &ctx->x, d) || dalloc(ctx, &ctx->x_new, d) || dalloc(ctx, &ctx->pvec, d) ||
+      dalloc(ctx, &ctx->zbuf, d) ||
+      dalloc(ctx, &ctx->hcoef, static_cast<size_t>(n) * ctx->ldh) ||
+      dalloc(ctx, &ctx->gcoef, static_cast<size_t>(n) * ctx->ldh) ||
+      dalloc(ctx, &ctx->loss_part, static_cast<size_t>(n) * ctx->nblk) ||
+      dalloc(ctx, &ctx->grad, static_cast<size_t>(n) * d) || dalloc(ctx, &ctx->gbar, d) ||
+      dalloc(ctx, &ctx->f_cli, n) || dalloc(ctx, &ctx->shift_cli, n) ||
+      dalloc(ctx, &ctx->frob_part, static_cast<size_t>(n) * ctx->n_pairs) ||
+      dalloc(ctx, &ctx->flags, n) || dalloc(ctx, &ctx->hest, wn) || dalloc(ctx, &ctx->D, wn) ||
+      dalloc(ctx, &ctx->hmas, w) || dalloc(ctx, &ctx->zeros_w, w) ||
+      dalloc(ctx, &ctx->M, static_cast<size_t>(d) * d) ||
+      dalloc(ctx, &ctx->bitmap, static_cast<size_t>(n) * ctx->wb) || dalloc(ctx, &ctx->count, n) ||
+      dalloc(ctx, &ctx->draws, n) ||
+      dalloc(ctx, &ctx->idx_list, static_cast<size_t>(n) * ctx->cap) ||
+      dalloc(ctx, &ctx->val_list, static_cast<size_t>(n) * ctx->cap) ||
+      dalloc(ctx, &ctx->jbuf, static_cast<size_t>(n) * ctx->cap) || dalloc(ctx, &ctx->seeds, n) ||
+      dalloc(ctx, &ctx->sc, 1) || dalloc(ctx, &ctx->steps_table, 64) ||
+      dalloc(ctx, &ctx->trial_x, static_cast<size_t>(LS_BATCH) * d) ||
+      dalloc(ctx, &ctx->ls_loss_part, static_cast<size_t>(LS_BATCH) * n * ctx->nblk) ||
+      dalloc(ctx, &ctx->subset, std::max(tau, 1)) || dalloc(ctx, &ctx->pool, n) ||
+      dalloc(ctx, &ctx->hess_part, c.algorithm == FB_ALG_PP ? static_cast<size_t>(tau) * w : 1) ||
+      dalloc(ctx, &ctx->cli_shift, n) ||
+      dalloc(ctx, &ctx->cli_gvec, c.algorithm == FB_ALG_PP ? static_cast<size_t>(n) * d : 1) ||
+      dalloc(ctx, &ctx->gvec, d) || dalloc(ctx, &ctx->pp_shift, 1) ||
+      dalloc(ctx, &ctx->dshift, std::max(tau, 1)) ||
+      dalloc(ctx, &ctx->dgvec, static_cast<size_t>(std::max(tau, 1)) * d) ||
+      dalloc(ctx, &ctx->scalar, 4) || dalloc(ctx, &ctx->row_grad, ROW_CHUNK) ||
+      dalloc(ctx, &ctx->row_f, ROW_CHUNK) ||
+      dalloc(ctx, &ctx->row_counts, static_cast<size_t>(ROW_CHUNK) * n) ||
+      dalloc(ctx, &ctx->row_ls, ROW_CHUNK)) {
+    return fail(FB_ERR_CUDA);
+  }
+  double steps[64];
+  for (int i = 0; i < 64; ++i) steps[i] = c.ls_steps_table[i <= 60 ? i : 60];
+  CKC(cudaMemcpy(ctx->steps_table, steps, sizeof steps, cudaMemcpyHostToDevice));
+  if (make_tmap(ctx) != FB_OK) return fail(FB_ERR_CUDA);
+  *out = ctx;
+  return rc;
+#undef CKC
+}
+
+void fb_destroy(void* handle) {
+  Ctx* ctx = static_cast<Ctx*>(handle);
+  if (!ctx) return;
+  if (ctx->gexec) cudaGraphExecDestroy(ctx->gexec);
+  if (ctx->graph) cudaGraphDestroy(ctx->graph);
+  for (void* p : ctx->allocs) cudaFree(p);
+  for (auto& e : ctx->ev_pool) if (e) cudaEventDestroy(e);
+  for (auto& e : ctx->ev_fixed) if (e) cudaEventDestroy(e);
+  if (ctx->ev_fork) cudaEventDestroy(ctx->ev_fork);
+  if (ctx->ev_join) cudaEventDestroy(ctx->ev_join);
+  if (ctx->st) cudaStreamDestroy(ctx->st);
+  if (ctx->st2) cudaStreamDestroy(ctx->st2);
+  delete ctx;
+}
+
+int fb_get_status(void* handle, fb_status* out) {
+  Ctx* ctx = static_cast<Ctx*>(handle);
+  if (!ctx || !out) return invalid(ctx, "null argument");
+  DevCtl h;
+  TRY(read_status(ctx, &h));
+  out->code = status_to_code(h.code);
+  out->round = h.code_round;
+  out->pivot_index = h.pivot_index;
+  out->client = h.bad_client;
+  out->pivot_value = h.pivot_value;
+  out->f_start = h.f_start;
+  out->f_best = h.f_best;
+  return FB_OK;
+}
+
+// Shards -> Bt[c][a][j] (feature-major, sample rows padded to ldj).
+__global__ void k_transpose_shard(const double* __restrict__ src, double* __restrict__ dst, int d,
+                                  int ni, int ldj) {
+  __shared__ double tile[32][33];
+  const int j0 = blockIdx.x * 32, a0 = blockIdx.y * 32;
+  for (int r = threadIdx.y; r < 32; r += blockDim.y) {
+    const int j = j0 + r, a = a0 + threadIdx.x;
+    tile[r][threadIdx.x] = (j < ni && a < d) ? src[a + static_cast<int64_t>(j) * d] : 0.0;
+  }
+  __syncthreads();
+  for (int r = threadIdx.y; r < 32; r += blockDim.y) {
+    const int a = a0 + r, j = j0 + threadIdx.x;
+    if (a < d && j < ldj) dst[static_cast<int64_t>(a) * ldj + j] = tile[threadIdx.x][r];
+  }
+}
+
+int fb_upload_shards(void* handle, const double* const* bmats) {
+  Ctx* ctx = static_cast<Ctx*>(handle);
+  if (!ctx || !bmats) return invalid(ctx, "null argument");
+  const int d = ctx->d, ni = ctx->ni;
+  const size_t bytes = static_cast<size_t>(d) * ni * sizeof(double);
+  double* stage[2] = {nullptr, nullptr};
+  CK(cudaMalloc(&stage[0], bytes));
+  CK(cudaMalloc(&stage[1], bytes));
+  for (int c = 0; c < ctx->n; ++c) {
+    if (!bmats[c]) {
+      cudaFree(stage[0]);
+      cudaFree(stage[1]);
+      return invalid(ctx, "null shard pointer");
+    }
+    double* sbuf = stage[c & 1];
+    CK(cudaMemcpyAsync(sbuf, bmats[c], bytes, cudaMemcpyHostToDevice, ctx->st));
+    dim3 grid((ctx->ldj + 31) / 32, (d + 31) / 32);
+    k_transpose_shard<<<grid, dim3(32, 8), 0, ctx->st>>>(
+        sbuf, ctx->Bt + static_cast<size_t>(c) * d * ctx->ldj, d, ni, ctx->ldj);
+    CKL();
+  }
+  CK(cudaStreamSynchronize(ctx->st));
+  cudaFree(stage[0]);
+  cudaFree(stage[1]);
+  ctx->uploaded = true;
+  return FB_OK;
+}
+
+int fb_init_state(void* handle, const double* x0) {
+  Ctx* ctx = static_cast<Ctx*>(handle);
+  if (!ctx) return invalid(ctx, "null argument");
+  if (!ctx->uploaded) return invalid(ctx, "shards not uploaded");
+  const fb_config& c = ctx->cfg;
+  cudaStream_t s = ctx->st;
+  const int n = ctx->n, d = ctx->d;
+  DevCtl h{};
+  h.master_state = mix64(c.run_seed ^ TAG_MASTER);  // derive_stream(seed, TAG_MASTER)
+  CK(cudaMemcpyAsync(ctx->ctl, &h, sizeof h, cudaMemcpyHostToDevice, s));
+  if (x0) CK(cudaMemcpyAsync(ctx->x, x0, sizeof(double) * d, cudaMemcpyHostToDevice, s));
+  else CK(cudaMemsetAsync(ctx->x, 0, sizeof(double) * d, s));
+  CK(cudaMemsetAsync(ctx->gvec, 0, sizeof(double) * d, s));
+  CK(cudaMemsetAsync(ctx->pp_shift, 0, sizeof(double), s));
+  const double diag = (c.hessian_init == FB_INIT_LAMBDA_IDENTITY) ? c.lam : 0.0;
+  dim3 gi(static_cast<unsigned>((ctx->w + 255) / 256), n + 1);
+  k_init_diag<<<gi, 256, 0, s>>>(ctx->w, n, diag, ctx->hest, ctx->hmas);
+  CKL();
+  const bool pp = c.algorithm == FB_ALG_PP;
+  if (c.hessian_init == FB_INIT_EXACT || pp) {
+    CK(cudaMemsetAsync(ctx->flags, 0, sizeof(int32_t) * n, s));
+    TRY(launch_margins(ctx, s, ctx->x, nullptr, n));
+    TRY(launch_gradient(ctx, s, ctx->x, nullptr, n));
+    if (c.hessian_init == FB_INIT_EXACT) {
+      // D = H - 0 = H exactly; H_i^0 = H_i(x0), master = mean (algorithms.py:207-209, 336-341)
+      TRY(launch_hessian(ctx, s, nullptr, n, ctx->zeros_w, 0, ctx->hest, nullptr));
+      k_mean_packed<<<static_cast<unsigned>((ctx->w + 255) / 256), 256, 0, s>>>(ctx->w, n,
+                                                                               ctx->hest, ctx->hmas);
+      CKL();
+    }
+    if (pp) {
+      TRY(launch_hessian(ctx, s, nullptr, n, ctx->hest, ctx->w, ctx->D, nullptr));
+      k_pp_init_client<<<n, 256, 0, s>>>(d, ctx->n_pairs, ctx->hest, ctx->x, ctx->grad,
+                                          ctx->frob_part, ctx->cli_shift, ctx->cli_gvec);
+      CKL();
+      k_pp_init_master<<<1, 256, 0, s>>>(d, n, ctx->cli_shift, ctx->cli_gvec, ctx->gvec,
+                                         ctx->pp_shift);
+      CKL();
+    }
+  }
+  CK(cudaStreamSynchronize(s));
+  ctx->initialised = true;
+  return FB_OK;
+}
+
+int fb_run_rounds(void* handle, int32_t first_round, int32_t count, double stop_grad_norm,
+                  int32_t timed, double* grad_norm, double* f_value, int32_t* ls_steps,
+                  int32_t* entry_counts, double* wall_ms, int32_t* rounds_done) {
+  Ctx* ctx = static_cast<Ctx*>(handle);
+  if (!ctx) return invalid(ctx, "null argument");
+  if (!ctx->initialised) return invalid(ctx, "state not initialised");
+  if (count < 0 || first_round < 0) return invalid(ctx, "bad round range");
+  if (rounds_done) *rounds_done = 0;
+  TRY(build_graph(ctx));
+  cudaStream_t s = ctx->st;
+  const int n = ctx->n;
+  DevCtl h;
+  TRY(read_status(ctx, &h));
+  if (h.halt) return status_to_code(h.code);
+  if (h.round != first_round) {
+    h.round = first_round;
+  }
+  cudaEvent_t t0;
+  CK(cudaEventCreate(&t0));
+  CK(cudaEventRecord(t0, s));
+  std::vector<double> kt(EV_COUNT, 0.0);
+  int timed_rounds = 0;
+  int done = 0;
+  int rc = FB_OK;
+  std::vector<double> rg(ROW_CHUNK), rf(ROW_CHUNK);
+  std::vector<int32_t> rls(ROW_CHUNK), rcnt(static_cast<size_t>(ROW_CHUNK) * n);
+  std::vector<cudaEvent_t> ends(ROW_CHUNK);
+  for (auto& e : ends) CK(cudaEventCreate(&e));
+  while (done < count && rc == FB_OK) {
+    const int chunk = std::min(ROW_CHUNK, count - done);
+    h.row_base = first_round + done;
+    h.round = first_round + done;
+    CK(cudaMemcpyAsync(ctx->ctl, &h, sizeof h, cudaMemcpyHostToDevice, s));
+    for (int i = 0; i < chunk; ++i) {
+      if (timed) {
+        for (int e = 0; e < EV_COUNT; ++e)
+          if (ctx->ev_node[e])
+            CK(cudaGraphExecEventRecordNodeSetEvent(ctx->gexec, ctx->ev_node[e],
+                                                    ctx->ev_pool[static_cast<size_t>(i) * EV_COUNT + e]));
+      }
+      CK(cudaGraphLaunch(ctx->gexec, s));
+      CK(cudaEventRecord(ends[i], s));
+    }
+    // drive line-search continuations (rare: no trial in the first batch passed)
+    TRY(read_status(ctx, &h));
+    while (h.code == ST_LS_PENDING) {
+      const int r = h.round;
+      dim3 grid(ctx->nblk, n);
+      k_ls_trials<<<grid, MARGIN_THREADS, LS_BATCH * ctx->d * sizeof(double), s>>>(
+          ctx->ctl, ctx->Bt, ctx->d, ctx->ni, ctx->ldj, ctx->x, ctx->pvec, ctx->steps_table, n,
+          ctx->trial_x, ctx->ls_loss_part, ctx->nblk);
+      CKL();
+      k_ls_decide<<<1, 256, 0, s>>>(ctx->ctl, ctx->d, n, ctx->ni, ctx->nblk, ctx->cfg.lam,
+                                    ctx->cfg.ls_c, ctx->steps_table, ctx->trial_x,
+                                    ctx->ls_loss_part, ctx->sc, ctx->x_new, LS_BATCH);
+      CKL();
+      TRY(read_status(ctx, &h));
+      if (h.code == 0 && !h.halt) {
+        TRY(enqueue_ls_tail(ctx));
+        const int next = r + 1;
+        const int slot_done = next - (first_round + done);
+        for (int i = slot_done; i < chunk; ++i) {
+          CK(cudaGraphLaunch(ctx->gexec, s));
+          CK(cudaEventRecord(ends[i], s));
+        }
+        TRY(read_status(ctx, &h));
+      }
+    }
+    const int completed = h.round - (first_round + done);
+    CK(cudaMemcpyAsync(rg.data(), ctx->row_grad, sizeof(double) * chunk, cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(rf.data(), ctx->row_f, sizeof(double) * chunk, cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(rls.data(), ctx->row_ls, sizeof(int32_t) * chunk, cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(rcnt.data(), ctx->row_counts, sizeof(int32_t) * chunk * n,
+                       cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    int take = std::min(completed, chunk);
+    bool stop = false;
+    for (int i = 0; i < take; ++i) {
+      const int o = done + i;
+      if (grad_norm) grad_norm[o] = rg[i];
+      if (f_value) f_value[o] = rf[i];
+      if (ls_steps) ls_steps[o] = rls[i];
+      if (entry_counts)
+        memcpy(entry_counts + static_cast<size_t>(o) * n, rcnt.data() + static_cast<size_t>(i) * n,
+               sizeof(int32_t) * n);
+      if (wall_ms) {
+        float ms = 0.f;
+        CK(cudaEventElapsedTime(&ms, t0, ends[i]));
+        wall_ms[o] = ms;
+      }
+      if (timed && ctx->ev_node[EV_START] && !h.halt) {
+        const cudaEvent_t* ev = &ctx->ev_pool[static_cast<size_t>(i) * EV_COUNT];
+        auto el = [&](int a, int b) {
+          if (!ctx->ev_node[a] || !ctx->ev_node[b]) return 0.0;
+          float v = 0.f;
+          if (cudaEventElapsedTime(&v, ev[a], ev[b]) != cudaSuccess) return 0.0;
+          return static_cast<double>(v);
+        };
+        kt[0] += el(EV_START, EV_ORACLE_END);
+        kt[1] += el(EV_ORACLE_END, EV_HESS_END);
+        kt[2] += el(EV_HESS_END, EV_REDUCE_END);
+        kt[3] += el(EV_COMP_START, EV_COMP_END);
+        kt[4] += (ctx->cfg.algorithm == FB_ALG_PP) ? el(EV_START, EV_SOLVE_END)
+                                                    : el(EV_REDUCE_END, EV_SOLVE_END);
+        kt[5] += el(EV_FOLD_START, EV_FOLD_END);
+        kt[6] += el(EV_START, EV_END);
+        ++timed_rounds;
+      }
+      if (stop_grad_norm >= 0.0 && rg[i] <= stop_grad_norm) {
+        done += i + 1;
+        stop = true;
+        break;
+      }
+    }
+    if (stop) break;
+    done += take;
+    if (h.code != 0) {
+      rc = status_to_code(h.code);
+      break;
+    }
+    if (take < chunk) {
+      rc = FB_ERR_CUDA;
+      ctx->err = "round graph stopped without a status";
+      break;
+    }
+  }
+  cudaGetLastError();
+  for (auto& e : ends) cudaEventDestroy(e);
+  cudaEventDestroy(t0);
+  if (timed && timed_rounds > 0) {
+    fb_profile& p = ctx->prof;
+    p.rounds = timed_rounds;
+    p.launches_per_round = ctx->launches_per_round;
+    p.ms_oracle = kt[0] / timed_rounds;
+    p.ms_hessian = kt[1] / timed_rounds;
+    p.ms_reduce = kt[2] / timed_rounds;
+    p.ms_compress = kt[3] / timed_rounds;
+    p.ms_solve = kt[4] / timed_rounds;
+    p.ms_fold = kt[5] / timed_rounds;
+    p.ms_round = kt[6] / timed_rounds;
+  }
+  if (rounds_done) *rounds_done = done;
+  if (rc != FB_OK && ctx->err.empty()) ctx->err = "round failed (see fb_get_status)";
+  return rc;
+}
+
+int fb_get_profile(void* handle, fb_profile* out) {
+  Ctx* ctx = static_cast<Ctx*>(handle);
+  if (!ctx || !out) return invalid(ctx, "null argument");
+  *out = ctx->prof;
+  return FB_OK;
+}
+
+int fb_final_eval(void* handle, double* grad_norm, double* f_value) {
+  Ctx* ctx = static_cast<Ctx*>(handle);
+  if (!ctx) return invalid(ctx, "null argument");
+  cudaStream_t s = ctx->st;
+  DevCtl h;
+  TRY(read_status(ctx, &h));
+  if (h.halt) return status_to_code(h.code);
+  TRY(launch_margins(ctx, s, ctx->x, nullptr, ctx->n));
+  TRY(launch_gradient(ctx, s, ctx->x, nullptr, ctx->n));
+  TRY(launch_reduce(ctx, s, ctx->x, nullptr, ctx->n, ctx->n, false, nullptr, nullptr));
+  RoundScalars sc;
+  CK(cudaMemcpyAsync(&sc, ctx->sc, sizeof sc, cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  if (grad_norm) *grad_norm = sc.grad_norm;
+  if (f_value) *f_value = sc.f_mean;
+  return FB_OK;
+}
+
+// ---------------------------------------------------------------- state taps
+#define COPY_OUT(dst, src, bytes)                                                   \
+  do {                                                                              \
+    CK(cudaMemcpyAsync((dst), (src), (bytes), cudaMemcpyDeviceToHost, ctx->st));    \
+    CK(cudaStreamSynchronize(ctx->st));                                             \
+  } while (0)
+#define COPY_IN(dst, src, bytes)                                                    \
+  do {                                                                              \
+    CK(cudaMemcpyAsync((dst), (src), (bytes), cudaMemcpyHostToDevice, ctx->st));    \
+    CK(cudaStreamSynchronize(ctx->st));                                             \
+  } while (0)
+
+int fb_get_x(void* handle, double* x) {
+  Ctx* ctx = static_cast<Ctx*>(handle);
+  if (!ctx || !x) return invalid(ctx, "null argument");
+  COPY_OUT(x, ctx->x, sizeof(double) * ctx->d);
+  return FB_OK;
+}
+int fb_set_x(void* handle, const double* x) {
+  Ctx* ctx = static_cast<Ctx*>(handle);
+  if (!ctx || !x) return invalid(ctx, "null argument");
+  COPY_IN(ctx->x, x, sizeof(double) * ctx->d);
+  return FB_OK;
+}
+int fb_get_client_hest(void* handle, int32_t c0, int32_t c1, double* out) {
+  Ctx* ctx = static_cast<Ctx*>(handle);
+  if (!ctx || !out || c0 < 0 || c1 > ctx->n || c0 > c1) return invalid(ctx, "bad client range");
+  COPY_OUT(out, ctx->hest + static_cast<size_t>(c0) * ctx->w, sizeof(double) * ctx->w * (c1 - c0));
+  return FB_OK;
+}
+int fb_set_client_hest(void* handle, int32_t c0, int32_t c1, const double* in) {
+  Ctx* ctx = static_cast<Ctx*>(handle);
+  if (!ctx || !in || c0 < 0 || c1 > ctx->n || c0 > c1) return invalid(ctx, "bad client range");
+  COPY_IN(ctx->hest + static_cast<size_t>(c0) * ctx->w, in, sizeof(double) * ctx->w * (c1 - c0));
+  return FB_OK;
+}
+int fb_get_master_hest(void* handle, double* out) {
+  Ctx* ctx = static_cast<Ctx*>(handle);
+  if (!ctx || !out) return invalid(ctx, "null argument");
+  COPY_OUT(out, ctx->hmas, sizeof(double) * ctx->w);
+  return FB_OK;
+}
+int fb_set_master_hest(void* handle, const double* in) {
+  Ctx* ctx = static_cast<Ctx*>(handle);
+  if (!ctx || !in) return invalid(ctx, "null argument");
+  COPY_IN(ctx->hmas, in, sizeof(double) * ctx->w);
+  return FB_OK;
+}
+int fb_get_pp_state(void* handle, double* shift, double* gvec, double* cli_shift,
+                    double* cli_gvec) {
+  Ctx* ctx = static_cast<Ctx*>(handle);
+  if (!ctx) return invalid(ctx, "null argument");
+  if (shift) COPY_OUT(shift, ctx->pp_shift, sizeof(double));
+  if (gvec) COPY_OUT(gvec, ctx->gvec, sizeof(double) * ctx->d);
+  if (cli_shift) COPY_OUT(cli_shift, ctx->cli_shift, sizeof(double) * ctx->n);
+  if (cli_gvec && ctx->cfg.algorithm == FB_ALG_PP)
+    COPY_OUT(cli_gvec, ctx->cli_gvec, sizeof(double) * ctx->n * ctx->d);
+  return FB_OK;
+}
+int fb_get_round_diff(void* handle, int32_t cid, double* out) {
+  Ctx* ctx = static_cast<Ctx*>(handle);
+  if (!ctx || !out || cid < 0 || cid >= ctx->n) return invalid(ctx, "bad client");
+  COPY_OUT(out, ctx->D + static_cast<size_t>(cid) * ctx->w, sizeof(double) * ctx->w);
+  return FB_OK;
+}
+int fb_get_round_delta(void* handle, int32_t cid, uint32_t* idx, double* val, int32_t* count) {
+  Ctx* ctx = static_cast<Ctx*>(handle);
+  if (!ctx || cid < 0 || cid >= ctx->n) return invalid(ctx, "bad client");
+  int32_t cnt = 0;
+  COPY_OUT(&cnt, ctx->count + cid, sizeof(int32_t));
+  if (count) *count = cnt;
+  const int kind = ctx->cfg.kind;
+  if (kind == FB_KIND_IDENTITY || kind == FB_KIND_NATURAL) {
+    if (val && cnt > 0) COPY_OUT(val, ctx->D + static_cast<size_t>(cid) * ctx->w, sizeof(double) * ctx->w);
+    return FB_OK;
+  }
+  if (idx && cnt > 0)
+    COPY_OUT(idx, ctx->idx_list + static_cast<size_t>(cid) * ctx->cap, sizeof(uint32_t) * cnt);
+  if (val && cnt > 0)
+    COPY_OUT(val, ctx->val_list + static_cast<size_t>(cid) * ctx->cap, sizeof(double) * cnt);
+  return FB_OK;
+}
+int fb_get_round_grads(void* handle, double* mean_grad, double* client_grads) {
+  Ctx* ctx = static_cast<Ctx*>(handle);
+  if (!ctx) return invalid(ctx, "null argument");
+  if (mean_grad) COPY_OUT(mean_grad, ctx->gbar, sizeof(double) * ctx->d);
+  if (client_grads) COPY_OUT(client_grads, ctx->grad, sizeof(double) * ctx->d * ctx->n);
+  return FB_OK;
+}
+
+// ------------------------------------------------------------- leaf ops
+
+// flags (nonfinite | nonzero) of injected packed differences
+__global__ void k_diff_flags(const double* __restrict__ D, int64_t w, int32_t* __restrict__ flags) {
+  const int c = blockIdx.y;
+  const int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  int f = 0;
+  if (t < w) {
+    const double v = D[static_cast<int64_t>(c) * w + t];
+    if (!isfinite(v)) f |= 1;
+    if (v != 0.0) f |= 2;
+  }
+  f = __reduce_or_sync(0xffffffffu, f);
+  if ((threadIdx.x & 31) == 0 && f) atomicOr(&flags[c], f);
+}
+
+int fb_compress(void* handle, const double* diffs, const uint64_t* seeds, uint32_t* idx,
+                double* val, int32_t* count, int32_t* draws) {
+  Ctx* ctx = static_cast<Ctx*>(handle);
+  if (!ctx || !diffs || !seeds) return invalid(ctx, "null argument");
+  cudaStream_t s = ctx->st;
+  TRY(clear_status(ctx));
+  const int n = ctx->n;
+  const int64_t w = ctx->w;
+  CK(cudaMemcpyAsync(ctx->D, diffs, sizeof(double) * w * n, cudaMemcpyHostToDevice, s));
+  CK(cudaMemcpyAsync(ctx->seeds, seeds, sizeof(uint64_t) * n, cudaMemcpyHostToDevice, s));
+  CK(cudaMemsetAsync(ctx->flags, 0, sizeof(int32_t) * n, s));
+  k_diff_flags<<<dim3(static_cast<unsigned>((w + 255) / 256), n), 256, 0, s>>>(ctx->D, w, ctx->flags);
+  CKL();
+  std::vector<int32_t> fl(n);
+  CK(cudaMemcpyAsync(fl.data(), ctx->flags, sizeof(int32_t) * n, cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  for (int c = 0; c < n; ++c) {
+    if (fl[c] & 1) {
+      DevCtl h;
+      TRY(read_status(ctx, &h));
+      h.bad_client = c;
+      h.code = ST_NONFINITE;
+      h.halt = 0;
+      CK(cudaMemcpy(ctx->ctl, &h, sizeof h, cudaMemcpyHostToDevice));
+      ctx->err = "cannot compress a matrix with non-finite entries";
+      return FB_ERR_NONFINITE;
+    }
+  }
+  TRY(launch_compress(ctx, s, nullptr, n, ctx->seeds, nullptr, false));
+  std::vector<int32_t> cnt(n);
+  CK(cudaMemcpyAsync(cnt.data(), ctx->count, sizeof(int32_t) * n, cudaMemcpyDeviceToHost, s));
+  if (draws) CK(cudaMemcpyAsync(draws, ctx->draws, sizeof(int32_t) * n, cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  DevCtl h;
+  TRY(read_status(ctx, &h));
+  if (h.code == ST_TOPLEK_ZERO) {
+    TRY(clear_status(ctx));
+    ctx->err = "toplek plan needs positive total energy";
+    return FB_ERR_INVALID;
+  }
+  if (count) memcpy(count, cnt.data(), sizeof(int32_t) * n);
+  const bool dense = ctx->cfg.kind == FB_KIND_IDENTITY || ctx->cfg.kind == FB_KIND_NATURAL;
+  for (int c = 0; c < n; ++c) {
+    if (cnt[c] == 0) continue;
+    if (dense) {
+      if (val) CK(cudaMemcpyAsync(val + static_cast<size_t>(c) * w, ctx->D + static_cast<size_t>(c) * w,
+                                  sizeof(double) * w, cudaMemcpyDeviceToHost, s));
+    } else {
+      if (idx) CK(cudaMemcpyAsync(idx + static_cast<size_t>(c) * w, ctx->idx_list + static_cast<size_t>(c) * ctx->cap,
+                                  sizeof(uint32_t) * cnt[c], cudaMemcpyDeviceToHost, s));
+      if (val) CK(cudaMemcpyAsync(val + static_cast<size_t>(c) * w, ctx->val_list + static_cast<size_t>(c) * ctx->cap,
+                                  sizeof(double) * cnt[c], cudaMemcpyDeviceToHost, s));
+    }
+  }
+  CK(cudaStreamSynchronize(s));
+  return FB_OK;
+}
+
+int fb_oracle_eval(void* handle, const double* x, double* f, double* grad, double* hess_packed) {
+  Ctx* ctx = static_cast<Ctx*>(handle);
+  if (!ctx || !x) return invalid(ctx, "null argument");
+  if (!ctx->uploaded) return invalid(ctx, "shards not uploaded");
+  cudaStream_t s = ctx->st;
+  const int n = ctx->n, d = ctx->d;
+  DevCtl h;
+  TRY(read_status(ctx, &h));
+  if (h.halt) TRY(clear_status(ctx));
+  CK(cudaMemcpyAsync(ctx->x_new, x, sizeof(double) * d, cudaMemcpyHostToDevice, s));
+  CK(cudaMemsetAsync(ctx->flags, 0, sizeof(int32_t) * n, s));
+  TRY(launch_margins(ctx, s, ctx->x_new, nullptr, n));
+  TRY(launch_gradient(ctx, s, ctx->x_new, nullptr, n));
+  if (hess_packed) TRY(launch_hessian(ctx, s, nullptr, n, ctx->zeros_w, 0, ctx->D, nullptr));
+  // f via the reduction kernel without touching the row buffers or status
+  k_reduce<<<1, 1024, 0, s>>>(ctx->ctl, n, nullptr, n, d, ctx->ni, ctx->nblk, ctx->n_pairs,
+                              ctx->x_new, ctx->cfg.lam, ctx->grad, ctx->loss_part, nullptr,
+                              ctx->flags, ctx->gbar, ctx->f_cli, ctx->shift_cli, ctx->sc, nullptr,
+                              nullptr);
+  CKL();
+  if (f) CK(cudaMemcpyAsync(f, ctx->f_cli, sizeof(double) * n, cudaMemcpyDeviceToHost, s));
+  if (grad) CK(cudaMemcpyAsync(grad, ctx->grad, sizeof(double) * n * d, cudaMemcpyDeviceToHost, s));
+  if (hess_packed)
+    CK(cudaMemcpyAsync(hess_packed, ctx->D, sizeof(double) * n * ctx->w, cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  return FB_OK;
+}
+
+int fb_shifted_solve(void* handle, const double* h_packed, double shift, const double* rhs,
+                     double* z) {
+  Ctx* ctx = static_cast<Ctx*>(handle);
+  if (!ctx || !h_packed || !rhs || !z) return invalid(ctx, "null argument");
+  cudaStream_t s = ctx->st;
+  const int d = ctx->d;
+  DevCtl h;
+  TRY(read_status(ctx, &h));
+  if (h.halt) TRY(clear_status(ctx));
+  CK(cudaMemcpyAsync(ctx->D, h_packed, sizeof(double) * ctx->w, cudaMemcpyHostToDevice, s));
+  CK(cudaMemcpyAsync(ctx->scalar, &shift, sizeof(double), cudaMemcpyHostToDevice, s));
+  CK(cudaMemcpyAsync(ctx->zbuf, rhs, sizeof(double) * d, cudaMemcpyHostToDevice, s));
+  TRY(launch_solve(ctx, s, ctx->D, ctx->scalar, ctx->zbuf, nullptr, ctx->pvec, nullptr, 2, 1));
+  CK(cudaStreamSynchronize(s));
+  TRY(read_status(ctx, &h));
+  if (h.code == ST_NOT_PD) {
+    ctx->err = "matrix is not positive definite";
+    // keep pivot info readable via fb_get_status, but un-halt the context
+    h.halt = 0;
+    CK(cudaMemcpy(ctx->ctl, &h, sizeof h, cudaMemcpyHostToDevice));
+    return FB_ERR_NOT_PD;
+  }
+  COPY_OUT(z, ctx->pvec, sizeof(double) * d);
+  return FB_OK;
+}
+
+// ------------------------------------------------------ context-free PRG
+
+__global__ void k_prg_u64(uint64_t seed, int count, uint64_t* out) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < count) out[i] = scramble(seed + static_cast<uint64_t>(i + 1) * GOLDEN);
+}
+__global__ void k_prg_randrange(uint64_t seed, const uint64_t* bounds, int nb, int reps,
+                                uint64_t* out, uint64_t* next) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= nb) return;
+  Prg p(seed);
+  for (int r = 0; r < reps; ++r) out[static_cast<int64_t>(b) * reps + r] = p.randrange(bounds[b]);
+  next[b] = p.next_u64();
+}
+__global__ void k_prg_pshuffle(uint64_t seed, int64_t n, int k, int64_t* out, int64_t* pool) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  Prg p(seed);
+  for (int64_t i = 0; i < n; ++i) pool[i] = i;
+  for (int i = 0; i < k; ++i) {
+    const int64_t j = i + static_cast<int64_t>(p.randrange(static_cast<uint64_t>(n - i)));
+    const int64_t t = pool[i];
+    pool[i] = pool[j];
+    pool[j] = t;
+    out[i] = pool[i];
+  }
+}
+__global__ void k_round_seeds(uint64_t run_seed, int n, int rnd, uint64_t* out) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c < n) out[c] = round_seed(run_seed, c, rnd);
+}
+
+#define G_CK(call)                                                                  \
+  do {                                                                              \
+    cudaError_t e_ = (call);                                                        \
+    if (e_ != cudaSuccess) {                                                        \
+      g_err = std::string(#call) + ": " + cudaGetErrorString(e_);                   \
+      return FB_ERR_CUDA;                                                           \
+    }                                                                               \
+  } while (0)
+
+int fb_prg_u64(uint64_t seed, int32_t count, uint64_t* out) {
+  if (!out || count < 0) return invalid(nullptr, "bad argument");
+  uint64_t* d = nullptr;
+  G_CK(cudaMalloc(&d, sizeof(uint64_t) * std::max(count, 1)));
+  k_prg_u64<<<(count + 255) / 256 + 1, 256>>>(seed, count, d);
+  G_CK(cudaGetLastError());
+  G_CK(cudaMemcpy(out, d, sizeof(uint64_t) * count, cudaMemcpyDeviceToHost));
+  cudaFree(d);
+  return FB_OK;
+}
+int fb_prg_randrange(uint64_t seed, const uint64_t* bounds, int32_t n_bounds, int32_t reps,
+                     uint64_t* out, uint64_t* next) {
+  if (!bounds || !out || !next || n_bounds < 0 || reps < 0) return invalid(nullptr, "bad argument");
+  for (int i = 0; i < n_bounds; ++i)
+    if (bounds[i] == 0) return invalid(nullptr, "bound must be positive");
+  uint64_t *db, *dout, *dnext;
+  G_CK(cudaMalloc(&db, sizeof(uint64_t) * std::max(n_bounds, 1)));
+  G_CK(cudaMalloc(&dout, sizeof(uint64_t) * std::max(n_bounds * reps, 1)));
+  G_CK(cudaMalloc(&dnext, sizeof(uint64_t) * std::max(n_bounds, 1)));
+  G_CK(cudaMemcpy(db, bounds, sizeof(uint64_t) * n_bounds, cudaMemcpyHostToDevice));
+  k_prg_randrange<<<(n_bounds + 63) / 64 + 1, 64>>>(seed, db, n_bounds, reps, dout, dnext);
+  G_CK(cudaGetLastError());
+  G_CK(cudaMemcpy(out, dout, sizeof(uint64_t) * n_bounds * reps, cudaMemcpyDeviceToHost));
+  G_CK(cudaMemcpy(next, dnext, sizeof(uint64_t) * n_bounds, cudaMemcpyDeviceToHost));
+  cudaFree(db);
+  cudaFree(dout);
+  cudaFree(dnext);
+  return FB_OK;
+}
+int fb_prg_partial_shuffle(uint64_t seed, int64_t n, int32_t k, int64_t* out) {
+  if (!out || k < 0 || k > n || n > (int64_t(1) << 28)) return invalid(nullptr, "bad argument");
+  int64_t *dout, *dpool;
+  G_CK(cudaMalloc(&dout, sizeof(int64_t) * std::max(k, 1)));
+  G_CK(cudaMalloc(&dpool, sizeof(int64_t) * std::max<int64_t>(n, 1)));
+  k_prg_pshuffle<<<1, 32>>>(seed, n, k, dout, dpool);
+  G_CK(cudaGetLastError());
+  G_CK(cudaMemcpy(out, dout, sizeof(int64_t) * k, cudaMemcpyDeviceToHost));
+  cudaFree(dout);
+  cudaFree(dpool);
+  return FB_OK;
+}
+int fb_round_seeds(uint64_t run_seed, int32_t n_clients, int32_t rnd, uint64_t* out) {
+  if (!out || n_clients < 0 || rnd < 0) return invalid(nullptr, "bad argument");
+  uint64_t* d;
+  G_CK(cudaMalloc(&d, sizeof(uint64_t) * std::max(n_clients, 1)));
+  k_round_seeds<<<(n_clients + 255) / 256 + 1, 256>>>(run_seed, n_clients, rnd, d);
+  G_CK(cudaGetLastError());
+  G_CK(cudaMemcpy(out, d, sizeof(uint64_t) * n_clients, cudaMemcpyDeviceToHost));
+  cudaFree(d);
+  return FB_OK;
+}
+
+int fb_fp64_peak(double* dmma_tflops, double* dfma_tflops) {
+  return fp64_peak_measure(dmma_tflops, dfma_tflops, &g_err);
+}
+
+}  // extern "C"

@@ -1,0 +1,183 @@
+// hessian_dmma.cuh — batched upper-triangular Hessian on fp64 tensor cores,
+// fused with the FedNL shift difference (reference oracle.py:124-139,
+// algorithms.py:228-231, linalg.py:139-148).
+//
+// For every client c and every 64x64 tile pair (I <= J) of its upper
+// triangle:
+//     S[a][b] = sum_j Bt[c][a][j] * h_c[j] * Bt[c][b][j]      (DMMA.8x8x4)
+//     H       = S (+ lam on the diagonal)
+//     D[c][t] = H - Hest[c][t]            packed t = b(b+1)/2 + a, a <= b
+//     frob_part[c][pair] = sum wt * D^2   (wt = 1 diagonal, 2 off-diagonal)
+//     flags[c] |= 1 (non-finite D) | 2 (nonzero D)
+// Optionally H itself is written (`hess_out`, FedNL-PP / exact init).
+//
+// Operands are staged by TMA: box {16 samples, 64 features} per operand and
+// stage, SWIZZLE_128B, NSTAGE-deep mbarrier ring; the h chunk rides on the
+// same barrier as a 128 B bulk copy.  Each of the 4 warps owns a 32x32
+// quadrant as 4x4 m8n8k4 fragments (32 fp64 accumulators per thread).  The
+// A fragment is scaled by h_j in registers (one DMUL per 16 DMMA).
+#pragma once
+#include "common.cuh"
+
+namespace fb {
+
+constexpr int HT = 64;          // tile edge (features)
+constexpr int HKC = 16;         // samples per stage (128 B rows)
+constexpr int HSTAGE = 4;       // pipeline depth
+constexpr int HTHREADS = 128;   // 4 warps
+constexpr int HC_LD = HT + 1;   // epilogue staging pitch
+
+struct HessSmem {
+  double a[HSTAGE][HT * HKC];  // 8 KB per stage, 1024 B aligned (swizzle-128B)
+  double b[HSTAGE][HT * HKC];
+  double h[HSTAGE][HKC];
+  uint64_t full[HSTAGE];
+  double red[HTHREADS / 32];
+  int flag_or;
+};
+constexpr size_t HESS_SMEM = sizeof(HessSmem) + 1024;  // + alignment slack
+
+// element (r, s) of a [64 rows][16 doubles] SWIZZLE_128B tile, in doubles
+__device__ __forceinline__ int swz(int r, int s) {
+  return r * HKC + ((((s >> 1) ^ (r & 7)) << 1) | (s & 1));
+}
+
+__device__ __forceinline__ void dmma_8x8x4(double (&c)[2], double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+               : "+d"(c[0]), "+d"(c[1])
+               : "d"(a), "d"(b));
+}
+
+// grid (n_pairs, n_active), block 128, dynamic smem HESS_SMEM.
+__global__ void __launch_bounds__(HTHREADS) k_hessian(
+    const __grid_constant__ CUtensorMap tmap_b, const DevCtl* __restrict__ ctl, int d, int ni,
+    int ldh, const double* __restrict__ hcoef, double lam, const int32_t* __restrict__ clients,
+    const double* __restrict__ hest, int64_t hest_stride, double* __restrict__ D,
+    double* __restrict__ hess_out, double* __restrict__ frob_part, int32_t* __restrict__ flags) {
+  if (ctl && ctl->halt) return;
+  extern __shared__ uint8_t smem_raw[];
+  HessSmem& sm = *reinterpret_cast<HessSmem*>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
+
+  const int slot = blockIdx.y;
+  const int c = client_of(clients, slot);
+  const int pair = blockIdx.x;
+  // pair -> (I, J), I <= J, column-wise like the packed layout
+  int J = static_cast<int>((sqrtf(8.0f * pair + 1.0f) - 1.0f) * 0.5f);
+  while ((J + 1) * (J + 2) / 2 <= pair) ++J;
+  while (J * (J + 1) / 2 > pair) --J;
+  const int I = pair - J * (J + 1) / 2;
+  const bool diag = (I == J);
+  const int n_pairs = gridDim.x;
+
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int g = lane >> 2, t = lane & 3;
+  const int rowbase = 32 * (warp & 1), colbase = 32 * (warp >> 1);
+  // on a diagonal tile the lower-left quadrant is entirely below the diagonal
+  const bool active = !(diag && rowbase > colbase);
+
+  const int nk = (ni + HKC - 1) / HKC;
+  const double* hrow = hcoef + static_cast<int64_t>(c) * ldh;
+  const uint32_t stage_bytes = (diag ? 1u : 2u) * HT * HKC * 8u + HKC * 8u;
+
+  if (tid == 0) {
+    tma_prefetch_desc(&tmap_b);
+    for (int s = 0; s < HSTAGE; ++s) mbar_init(&sm.full[s], 1);
+    fence_barrier_init();
+    sm.flag_or = 0;
+  }
+  __syncthreads();
+
+  auto issue = [&](int it) {
+    const int s = it % HSTAGE;
+    mbar_arrive_expect_tx(&sm.full[s], stage_bytes);
+    tma_load_3d(sm.a[s], &tmap_b, &sm.full[s], it * HKC, I * HT, c);
+    if (!diag) tma_load_3d(sm.b[s], &tmap_b, &sm.full[s], it * HKC, J * HT, c);
+    bulk_load(sm.h[s], hrow + it * HKC, HKC * 8, &sm.full[s]);
+  };
+  if (tid == 0) {
+    for (int it = 0; it < HSTAGE && it < nk; ++it) issue(it);
+  }
+
+  double acc[4][4][2];
+#pragma unroll
+  for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+    for (int ni2 = 0; ni2 < 4; ++ni2) acc[mi][ni2][0] = acc[mi][ni2][1] = 0.0;
+
+  for (int it = 0; it < nk; ++it) {
+    const int s = it % HSTAGE;
+    mbar_wait(&sm.full[s], (it / HSTAGE) & 1);
+    const double* sa = sm.a[s];
+    const double* sb = diag ? sm.a[s] : sm.b[s];
+    if (active) {
+#pragma unroll
+      for (int kk = 0; kk < HKC / 4; ++kk) {
+        const int ks = 4 * kk + t;
+        const double hv = sm.h[s][ks];
+        double af[4], bf[4];
+#pragma unroll
+        for (int mi = 0; mi < 4; ++mi) af[mi] = sa[swz(rowbase + 8 * mi + g, ks)] * hv;
+#pragma unroll
+        for (int nj = 0; nj < 4; ++nj) bf[nj] = sb[swz(colbase + 8 * nj + g, ks)];
+#pragma unroll
+        for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+          for (int nj = 0; nj < 4; ++nj) dmma_8x8x4(acc[mi][nj], af[mi], bf[nj]);
+      }
+    }
+    __syncthreads();  // every warp is done with stage s
+    if (tid == 0 && it + HSTAGE < nk) issue(it + HSTAGE);
+  }
+
+  // ---- epilogue: stage the tile column-major, then stream packed columns
+  double* cs = &sm.a[0][0];  // [64 cols][HC_LD] — reuses the pipeline ring
+  if (active) {
+#pragma unroll
+    for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+      for (int nj = 0; nj < 4; ++nj)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int r = rowbase + 8 * mi + g;
+          const int col = colbase + 8 * nj + 2 * t + e;
+          cs[col * HC_LD + r] = acc[mi][nj][e];
+        }
+  }
+  __syncthreads();
+
+  const double* hest_c = hest + static_cast<int64_t>(c) * hest_stride;
+  const int64_t w = packed_len(d);
+  double* Dc = D + static_cast<int64_t>(c) * w;
+  double* Hc = hess_out ? hess_out + static_cast<int64_t>(slot) * w : nullptr;
+  double part = 0.0;
+  int fl = 0;
+  for (int col = warp; col < HT; col += 4) {
+    const int b = J * HT + col;
+    if (b >= d) break;
+    const int64_t cbase = packed_at(0, b);
+    for (int r = lane; r < HT; r += 32) {
+      const int a = I * HT + r;
+      if (a > b || a >= d) continue;
+      const int64_t tt = cbase + a;
+      double hv = cs[col * HC_LD + r];
+      if (a == b) hv = __dadd_rn(hv, lam);
+      const double dv = __dsub_rn(hv, hest_c[tt]);
+      Dc[tt] = dv;
+      if (Hc) Hc[tt] = hv;
+      const double wt = (a == b) ? 1.0 : 2.0;
+      part = fma(__dmul_rn(wt, dv), dv, part);
+      if (!isfinite(dv)) fl |= 1;
+      if (dv != 0.0) fl |= 2;
+    }
+  }
+  const double tot = block_sum(part, sm.red);
+  if (fl) atomicOr(&sm.flag_or, fl);
+  __syncthreads();
+  if (tid == 0) {
+    frob_part[static_cast<int64_t>(c) * n_pairs + pair] = tot;
+    if (sm.flag_or) atomicOr(&flags[c], sm.flag_or);
+  }
+}
+
+}  // namespace fb

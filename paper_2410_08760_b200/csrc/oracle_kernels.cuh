@@ -1,0 +1,144 @@
+// oracle_kernels.cuh — batched logistic oracle (reference oracle.py:64-121).
+//
+// HBM layout of the design matrices (built by fb_upload_shards):
+//   Bt[c][a][j], c < n clients, a < d features, j < ldj samples (ldj even,
+//   zero padded) — feature-major, sample-contiguous rows.  This is the
+//   transpose of each shard's F-order d x n_i matrix viewed per client, so a
+//   TMA box {16 samples, 64 features} lands as 64 rows of 128 B
+//   (SWIZZLE_128B) for the DMMA Hessian, and the margins pass below reads
+//   sample-contiguous rows coalesced.
+//
+// Per-sample coefficients (length ldh = round_up(n_i, 16), zero padded):
+//   hcoef = sigma (1 - sigma) / n_i      (oracle.py:133)
+//   gcoef = (sigma - 1) / n_i            (oracle.py:116)
+#pragma once
+#include "common.cuh"
+
+namespace fb {
+
+constexpr int MARGIN_THREADS = 128;
+
+// stable logistic, oracle.py:64-71
+__device__ __forceinline__ double stable_sigmoid(double m) {
+  if (m >= 0.0) return 1.0 / (1.0 + exp(-m));
+  const double e = exp(m);
+  return e / (1.0 + e);
+}
+// log(1 + exp(-m)) without overflow, oracle.py:99-103
+__device__ __forceinline__ double softplus_neg(double m) {
+  if (m >= 0.0) return log1p(exp(-m));
+  return -m + log1p(exp(m));
+}
+
+// Margins m_j = <B_j, x>, sigmoids, per-sample Hessian / gradient
+// coefficients, and per-block partial sums of the loss (for f_value).
+// grid (ceil(ldh / 128), n_active), block 128, dynamic smem d doubles.
+__global__ void __launch_bounds__(MARGIN_THREADS) k_margins(
+    const DevCtl* __restrict__ ctl, const double* __restrict__ Bt, int d, int ni, int ldj,
+    int ldh, const double* __restrict__ x, const int32_t* __restrict__ clients,
+    double* __restrict__ hcoef, double* __restrict__ gcoef, double* __restrict__ loss_part,
+    int nblk) {
+  if (ctl && ctl->halt) return;
+  extern __shared__ double xs[];
+  __shared__ double red[MARGIN_THREADS / 32];
+  const int c = client_of(clients, blockIdx.y);
+  for (int a = threadIdx.x; a < d; a += blockDim.x) xs[a] = x[a];
+  __syncthreads();
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  double loss = 0.0;
+  if (j < ni) {
+    const double* col = Bt + static_cast<int64_t>(c) * d * ldj + j;
+    double m0 = 0.0, m1 = 0.0, m2 = 0.0, m3 = 0.0;
+    int a = 0;
+    for (; a + 3 < d; a += 4) {
+      m0 = fma(__ldg(col + static_cast<int64_t>(a) * ldj), xs[a], m0);
+      m1 = fma(__ldg(col + static_cast<int64_t>(a + 1) * ldj), xs[a + 1], m1);
+      m2 = fma(__ldg(col + static_cast<int64_t>(a + 2) * ldj), xs[a + 2], m2);
+      m3 = fma(__ldg(col + static_cast<int64_t>(a + 3) * ldj), xs[a + 3], m3);
+    }
+    for (; a < d; ++a) m0 = fma(__ldg(col + static_cast<int64_t>(a) * ldj), xs[a], m0);
+    const double m = (m0 + m1) + (m2 + m3);
+    const double sig = stable_sigmoid(m);
+    const double inv_n = static_cast<double>(ni);
+    hcoef[static_cast<int64_t>(c) * ldh + j] = __ddiv_rn(__dmul_rn(sig, __dsub_rn(1.0, sig)), inv_n);
+    gcoef[static_cast<int64_t>(c) * ldh + j] = __ddiv_rn(__dsub_rn(sig, 1.0), inv_n);
+    loss = softplus_neg(m);
+  } else if (j < ldh) {
+    hcoef[static_cast<int64_t>(c) * ldh + j] = 0.0;
+    gcoef[static_cast<int64_t>(c) * ldh + j] = 0.0;
+  }
+  const double s = block_sum(loss, red);
+  if (threadIdx.x == 0) loss_part[static_cast<int64_t>(c) * nblk + blockIdx.x] = s;
+}
+
+// Local gradients g_c = B_c gcoef_c + lam x (oracle.py:108-121).
+// grid (ceil(d / 8), n_active), block 256: one warp per feature row.
+__global__ void __launch_bounds__(256) k_gradient(
+    const DevCtl* __restrict__ ctl, const double* __restrict__ Bt, int d, int ni, int ldj,
+    int ldh, const double* __restrict__ x, double lam, const int32_t* __restrict__ clients,
+    const double* __restrict__ gcoef, double* __restrict__ grad) {
+  if (ctl && ctl->halt) return;
+  const int c = client_of(clients, blockIdx.y);
+  const int a = blockIdx.x * 8 + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (a >= d) return;
+  const double* row = Bt + (static_cast<int64_t>(c) * d + a) * ldj;
+  const double* gc = gcoef + static_cast<int64_t>(c) * ldh;
+  double s0 = 0.0, s1 = 0.0;
+  int j = lane;
+  for (; j + 32 < ni; j += 64) {
+    s0 = fma(__ldg(row + j), __ldg(gc + j), s0);
+    s1 = fma(__ldg(row + j + 32), __ldg(gc + j + 32), s1);
+  }
+  if (j < ni) s0 = fma(__ldg(row + j), __ldg(gc + j), s0);
+  const double s = warp_sum(s0 + s1);
+  if (lane == 0) grad[static_cast<int64_t>(c) * d + a] = __dadd_rn(s, __dmul_rn(lam, x[a]));
+}
+
+// Line-search trials (algorithms.py:304-309, runtime.py:203-208):
+// trial_s = x - step_s * p for s in [s0, s0 + S); per client and trial the
+// loss partial sums.  grid (ceil(ni / 128), n), block 128,
+// dynamic smem S * d doubles.
+constexpr int LS_BATCH = 4;
+__global__ void __launch_bounds__(MARGIN_THREADS) k_ls_trials(
+    const DevCtl* __restrict__ ctl, const double* __restrict__ Bt, int d, int ni, int ldj,
+    const double* __restrict__ x, const double* __restrict__ p,
+    const double* __restrict__ steps_table, int n_clients, double* __restrict__ trial_x,
+    double* __restrict__ loss_part, int nblk) {
+  if (ctl->halt && ctl->code != ST_LS_PENDING) return;
+  extern __shared__ double xt[];  // [LS_BATCH][d]
+  __shared__ double red[MARGIN_THREADS / 32];
+  const int s0 = ctl->ls_next;
+  const int c = blockIdx.y;
+  for (int e = threadIdx.x; e < LS_BATCH * d; e += blockDim.x) {
+    const int s = e / d, a = e - s * d;
+    const int si = s0 + s;
+    const double step = steps_table[si <= 60 ? si : 60];
+    xt[e] = __dsub_rn(x[a], __dmul_rn(step, p[a]));
+  }
+  __syncthreads();
+  if (blockIdx.x == 0 && blockIdx.y == 0) {
+    for (int e = threadIdx.x; e < LS_BATCH * d; e += blockDim.x) trial_x[e] = xt[e];
+  }
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  double m[LS_BATCH];
+#pragma unroll
+  for (int s = 0; s < LS_BATCH; ++s) m[s] = 0.0;
+  if (j < ni) {
+    const double* col = Bt + static_cast<int64_t>(c) * d * ldj + j;
+    for (int a = 0; a < d; ++a) {
+      const double b = __ldg(col + static_cast<int64_t>(a) * ldj);
+#pragma unroll
+      for (int s = 0; s < LS_BATCH; ++s) m[s] = fma(b, xt[s * d + a], m[s]);
+    }
+  }
+#pragma unroll
+  for (int s = 0; s < LS_BATCH; ++s) {
+    const double loss = (j < ni) ? softplus_neg(m[s]) : 0.0;
+    const double tot = block_sum(loss, red);
+    if (threadIdx.x == 0)
+      loss_part[(static_cast<int64_t>(s) * n_clients + c) * nblk + blockIdx.x] = tot;
+  }
+}
+
+}  // namespace fb

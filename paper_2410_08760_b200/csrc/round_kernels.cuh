@@ -1,0 +1,401 @@
+// round_kernels.cuh — cross-client reductions, the fused shift + master fold,
+// FedNL-PP bookkeeping and the round epilogue (reference algorithms.py,
+// runtime.py).  Every reduction over clients runs in ascending client id
+// with sequential adds, so results do not depend on launch shape.
+#pragma once
+#include "common.cuh"
+
+namespace fb {
+
+// Cross-client reductions of one round (algorithms.py:351-359, 399-402;
+// runtime.py:189-201).  Single CTA of 1024 threads.
+//   f_cli[c]    = sum_b loss_part[c][b] / n_i + (0.5 lam) <x, x>
+//   shift_cli[c]= sqrt(sum_p frob_part[c][p])           (if frob_part)
+//   gbar        = (sum_c grad_c) / n_div
+//   out[0] = ||gbar||, out[1] = (sum_c f_c) / n_div, out[2] = (sum shift)/n_div
+// A non-finite difference raises ST_NONFINITE (compressors.py:134-135).
+struct RoundScalars {
+  double grad_norm;
+  double f_mean;
+  double shift_mean;
+  double decrement;  // LS: <gbar, p>
+  double xx;
+};
+
+__global__ void __launch_bounds__(1024) k_reduce(
+    DevCtl* __restrict__ ctl, int n_active, const int32_t* __restrict__ clients, int n_div, int d,
+    int ni, int nblk, int n_pairs, const double* __restrict__ x, double lam,
+    const double* __restrict__ grad, const double* __restrict__ loss_part,
+    const double* __restrict__ frob_part, const int32_t* __restrict__ flags,
+    double* __restrict__ gbar, double* __restrict__ f_cli, double* __restrict__ shift_cli,
+    RoundScalars* __restrict__ out, double* __restrict__ row_grad, double* __restrict__ row_f) {
+  if (ctl->halt) return;
+  __shared__ double red[32];
+  __shared__ int s_bad;
+  if (threadIdx.x == 0) s_bad = 0x7fffffff;
+  double xx_part = 0.0;
+  for (int a = threadIdx.x; a < d; a += blockDim.x) xx_part = fma(x[a], x[a], xx_part);
+  const double xx = block_sum(xx_part, red);
+  const double reg = __dmul_rn(__dmul_rn(0.5, lam), xx);
+  for (int s = threadIdx.x; s < n_active; s += blockDim.x) {
+    const int c = client_of(clients, s);
+    double ls = 0.0;
+    for (int b = 0; b < nblk; ++b) ls = __dadd_rn(ls, loss_part[static_cast<int64_t>(c) * nblk + b]);
+    f_cli[c] = __dadd_rn(__ddiv_rn(ls, static_cast<double>(ni)), reg);
+    if (frob_part) {
+      double fp = 0.0;
+      for (int p = 0; p < n_pairs; ++p) fp = __dadd_rn(fp, frob_part[static_cast<int64_t>(c) * n_pairs + p]);
+      shift_cli[c] = sqrt(fp);
+      if (flags[c] & 1) atomicMin(&s_bad, c);
+    }
+  }
+  for (int a = threadIdx.x; a < d; a += blockDim.x) {
+    double s = 0.0;
+    for (int i = 0; i < n_active; ++i) {
+      const int c = client_of(clients, i);
+      s = __dadd_rn(s, grad[static_cast<int64_t>(c) * d + a]);
+    }
+    gbar[a] = __ddiv_rn(s, static_cast<double>(n_div));
+  }
+  __syncthreads();
+  double gg = 0.0;
+  for (int a = threadIdx.x; a < d; a += blockDim.x) gg = fma(gbar[a], gbar[a], gg);
+  const double gn2 = block_sum(gg, red);
+  if (threadIdx.x == 0) {
+    double fs = 0.0, ss = 0.0;
+    for (int i = 0; i < n_active; ++i) {
+      const int c = client_of(clients, i);
+      fs = __dadd_rn(fs, f_cli[c]);
+      if (frob_part) ss = __dadd_rn(ss, shift_cli[c]);
+    }
+    out->grad_norm = sqrt(gn2);
+    out->f_mean = __ddiv_rn(fs, static_cast<double>(n_div));
+    out->shift_mean = __ddiv_rn(ss, static_cast<double>(n_div));
+    out->xx = xx;
+    const int slot = ctl->round - ctl->row_base;
+    if (row_grad) row_grad[slot] = out->grad_norm;
+    if (row_f) row_f[slot] = out->f_mean;
+    if (frob_part && s_bad != 0x7fffffff) {
+      ctl->bad_client = s_bad;
+      raise_status(ctl, ST_NONFINITE);
+    }
+  }
+}
+
+// Fused client shift update + master fold (compressors.py:373-393,
+// algorithms.py:234, 369-372).  One thread per packed position t; clients in
+// ascending id:  Hest[c][t] = fl(Hest + fl(alpha v)),
+//                Hmas[t]    = fl(Hmas + fl((alpha / n) v)).
+// v = D[c][t] (TopK/TopLEK/identity/natural-rounded) or fl(D * w/k) (Rand).
+// An unselected entry contributes nothing (the reference's sparse fold).
+__global__ void __launch_bounds__(256) k_fold(
+    const DevCtl* __restrict__ ctl, int64_t w, int wb, int n_active,
+    const int32_t* __restrict__ clients, int dense, double scale, double alpha, double alpha_n,
+    const double* __restrict__ D, const uint32_t* __restrict__ bitmap,
+    const int32_t* __restrict__ count, double* __restrict__ hest, double* __restrict__ hmas) {
+  if (ctl->halt) return;
+  const int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (t >= w) return;
+  const int64_t q = t >> 5;
+  const uint32_t bit = 1u << (t & 31);
+  double h = hmas ? hmas[t] : 0.0;
+  for (int i = 0; i < n_active; ++i) {
+    const int c = client_of(clients, i);
+    if (count[c] == 0) continue;
+    if (!dense && !(bitmap[static_cast<int64_t>(c) * wb + q] & bit)) continue;
+    double v = D[static_cast<int64_t>(c) * w + t];
+    if (scale != 1.0) v = __dmul_rn(v, scale);
+    if (hest) {
+      double* hp = hest + static_cast<int64_t>(c) * w + t;
+      *hp = __dadd_rn(*hp, __dmul_rn(alpha, v));
+    }
+    if (hmas) h = __dadd_rn(h, __dmul_rn(alpha_n, v));
+  }
+  if (hmas) hmas[t] = h;
+}
+
+// Round epilogue (algorithms.py:385-387): x <- x_new, round += 1,
+// DivergenceError on a non-finite iterate; per-client entry counts into the
+// row buffers (-1 for clients that did not participate).
+__global__ void __launch_bounds__(256) k_finish(
+    DevCtl* __restrict__ ctl, int d, int n, int n_active, const int32_t* __restrict__ clients,
+    double* __restrict__ x, const double* __restrict__ x_new, int copy_x,
+    const int32_t* __restrict__ count, int32_t* __restrict__ row_counts,
+    int32_t* __restrict__ row_ls) {
+  if (ctl->halt) return;
+  __shared__ int bad;
+  if (threadIdx.x == 0) bad = 0;
+  __syncthreads();
+  for (int a = threadIdx.x; a < d; a += blockDim.x) {
+    const double v = copy_x ? x_new[a] : x[a];
+    if (copy_x) x[a] = v;
+    if (!isfinite(v)) bad = 1;
+  }
+  const int slot = ctl->round - ctl->row_base;
+  if (row_counts) {
+    int32_t* rc = row_counts + static_cast<int64_t>(slot) * n;
+    if (clients) {
+      for (int c = threadIdx.x; c < n; c += blockDim.x) rc[c] = -1;
+      __syncthreads();
+      for (int i = threadIdx.x; i < n_active; i += blockDim.x) rc[clients[i]] = count[clients[i]];
+    } else {
+      for (int c = threadIdx.x; c < n; c += blockDim.x) rc[c] = count[c];
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    if (row_ls) row_ls[slot] = ctl->ls_steps;
+    ctl->round += 1;
+    if (bad) raise_status(ctl, ST_DIVERGED);
+  }
+}
+
+// ------------------------------------------------------------------ FedNL-PP
+
+// Participant subset of the round: the persistent TAG_MASTER stream's
+// partial Fisher-Yates prefix of range(n) of length tau, sorted ascending
+// (algorithms.py:422-425).  One thread.
+__global__ void k_pp_select(DevCtl* __restrict__ ctl, int n, int tau, int32_t* __restrict__ subset,
+                            int32_t* __restrict__ pool) {
+  if (ctl->halt) return;
+  if (threadIdx.x != 0) return;
+  Prg p(ctl->master_state);
+  for (int i = 0; i < n; ++i) pool[i] = i;
+  for (int i = 0; i < tau; ++i) {
+    const int j = i + static_cast<int>(p.randrange(static_cast<uint64_t>(n - i)));
+    const int32_t tmp = pool[i];
+    pool[i] = pool[j];
+    pool[j] = tmp;
+  }
+  ctl->master_state = p.state;
+  for (int i = 0; i < tau; ++i) subset[i] = pool[i];
+  for (int i = 1; i < tau; ++i) {  // insertion sort (tau is small)
+    const int32_t v = subset[i];
+    int j = i - 1;
+    while (j >= 0 && subset[j] > v) { subset[j + 1] = subset[j]; --j; }
+    subset[j + 1] = v;
+  }
+}
+
+// Per participant after its shift update (algorithms.py:250-256):
+//   shift_new = ||Hest_c - hess||_F,  gvec_new = Hest_c x + shift_new x - grad_c
+// and the increments against the stored client state.  grid tau, block 256.
+__global__ void __launch_bounds__(256) k_pp_client(
+    const DevCtl* __restrict__ ctl, int d, const int32_t* __restrict__ subset,
+    const double* __restrict__ hest, const double* __restrict__ hess_part,
+    const double* __restrict__ x, const double* __restrict__ grad,
+    double* __restrict__ cli_shift, double* __restrict__ cli_gvec,
+    double* __restrict__ dshift, double* __restrict__ dgvec) {
+  if (ctl->halt) return;
+  __shared__ double red[8];
+  __shared__ double s_shift;
+  const int slot = blockIdx.x;
+  const int c = subset[slot];
+  const int64_t w = packed_len(d);
+  const double* hc = hest + static_cast<int64_t>(c) * w;
+  const double* hp = hess_part + static_cast<int64_t>(slot) * w;
+  double part = 0.0;
+  for (int64_t t = threadIdx.x; t < w; t += blockDim.x) {
+    const double dv = __dsub_rn(hc[t], hp[t]);
+    const double wt = packed_is_diag_fast(t) ? 1.0 : 2.0;
+    part = fma(__dmul_rn(wt, dv), dv, part);
+  }
+  const double tot = block_sum(part, red);
+  if (threadIdx.x == 0) s_shift = sqrt(tot);
+  __syncthreads();
+  const double sh = s_shift;
+  for (int a = threadIdx.x; a < d; a += blockDim.x) {
+    // row a of the symmetric matrix from packed storage
+    double s = 0.0;
+    for (int b = 0; b < d; ++b) {
+      const int64_t tt = (a <= b) ? packed_at(a, b) : packed_at(b, a);
+      s = fma(hc[tt], x[b], s);
+    }
+    const double gnew = __dsub_rn(__dadd_rn(s, __dmul_rn(sh, x[a])), grad[static_cast<int64_t>(c) * d + a]);
+    const double gold = cli_gvec[static_cast<int64_t>(c) * d + a];
+    dgvec[static_cast<int64_t>(slot) * d + a] = __dsub_rn(gnew, gold);
+    cli_gvec[static_cast<int64_t>(c) * d + a] = gnew;
+  }
+  if (threadIdx.x == 0) {
+    dshift[slot] = __dsub_rn(sh, cli_shift[c]);
+    cli_shift[c] = sh;
+  }
+}
+
+// Master running averages (algorithms.py:435-441): ascending participants,
+// gvec = gvec + dg / n, shift += ds / n.  Single CTA.
+__global__ void __launch_bounds__(256) k_pp_master(
+    const DevCtl* __restrict__ ctl, int d, int n, int tau, const double* __restrict__ dshift,
+    const double* __restrict__ dgvec, double* __restrict__ gvec, double* __restrict__ shift) {
+  if (ctl->halt) return;
+  const double nn = static_cast<double>(n);
+  for (int a = threadIdx.x; a < d; a += blockDim.x) {
+    double g = gvec[a];
+    for (int i = 0; i < tau; ++i) g = __dadd_rn(g, __ddiv_rn(dgvec[static_cast<int64_t>(i) * d + a], nn));
+    gvec[a] = g;
+  }
+  if (threadIdx.x == 0) {
+    double s = *shift;
+    for (int i = 0; i < tau; ++i) s = __dadd_rn(s, __ddiv_rn(dshift[i], nn));
+    *shift = s;
+  }
+}
+
+// k_check_flags_pp: non-finite participant difference -> ST_NONFINITE
+__global__ void k_check_flags_pp(DevCtl* ctl, int tau, const int32_t* subset,
+                                 const int32_t* flags) {
+  if (ctl->halt) return;
+  if (threadIdx.x != 0) return;
+  for (int i = 0; i < tau; ++i) {
+    const int c = subset ? subset[i] : i;
+    if (flags[c] & 1) {
+      ctl->bad_client = c;
+      raise_status(ctl, ST_NONFINITE);
+      return;
+    }
+  }
+}
+
+// ------------------------------------------------------------ initialisation
+
+// Hest[c] = lam I (or 0) for every client, Hmas likewise
+// (algorithms.py:202-206, 334-335).  grid (ceil(w/256), n + 1).
+__global__ void k_init_diag(int64_t w, int n, double diag_value, double* __restrict__ hest,
+                            double* __restrict__ hmas) {
+  const int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (t >= w) return;
+  const double v = packed_is_diag_fast(t) ? diag_value : 0.0;
+  if (blockIdx.y < static_cast<unsigned>(n)) hest[static_cast<int64_t>(blockIdx.y) * w + t] = v;
+  else if (hmas) hmas[t] = v;
+}
+
+// exact init (algorithms.py:336-341): Hmas = (sum_c Hest_c) / n, ascending c.
+__global__ void k_mean_packed(int64_t w, int n, const double* __restrict__ hest,
+                              double* __restrict__ hmas) {
+  const int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (t >= w) return;
+  double s = 0.0;
+  for (int c = 0; c < n; ++c) s = __dadd_rn(s, hest[static_cast<int64_t>(c) * w + t]);
+  hmas[t] = __ddiv_rn(s, static_cast<double>(n));
+}
+
+// PP init (algorithms.py:211-222, 342-349) for all clients at x0:
+// cli_shift[c] = ||Hest_c - hess_c|| (= sqrt of the Hessian kernel's
+// Frobenius partials), cli_gvec[c] = Hest_c x0 + shift x0 - grad_c.
+__global__ void __launch_bounds__(256) k_pp_init_client(
+    int d, int n_pairs, const double* __restrict__ hest, const double* __restrict__ x,
+    const double* __restrict__ grad, const double* __restrict__ frob_part,
+    double* __restrict__ cli_shift, double* __restrict__ cli_gvec) {
+  const int c = blockIdx.x;
+  const int64_t w = packed_len(d);
+  const double* hc = hest + static_cast<int64_t>(c) * w;
+  double fp = 0.0;
+  for (int p = 0; p < n_pairs; ++p) fp = __dadd_rn(fp, frob_part[static_cast<int64_t>(c) * n_pairs + p]);
+  const double sh = sqrt(fp);
+  for (int a = threadIdx.x; a < d; a += blockDim.x) {
+    double s = 0.0;
+    for (int b = 0; b < d; ++b) {
+      const int64_t tt = (a <= b) ? packed_at(a, b) : packed_at(b, a);
+      s = fma(hc[tt], x[b], s);
+    }
+    cli_gvec[static_cast<int64_t>(c) * d + a] =
+        __dsub_rn(__dadd_rn(s, __dmul_rn(sh, x[a])), grad[static_cast<int64_t>(c) * d + a]);
+  }
+  if (threadIdx.x == 0) cli_shift[c] = sh;
+}
+
+__global__ void k_pp_init_master(int d, int n, const double* __restrict__ cli_shift,
+                                 const double* __restrict__ cli_gvec, double* __restrict__ gvec,
+                                 double* __restrict__ shift) {
+  for (int a = threadIdx.x; a < d; a += blockDim.x) {
+    double s = 0.0;
+    for (int c = 0; c < n; ++c) s = __dadd_rn(s, cli_gvec[static_cast<int64_t>(c) * d + a]);
+    gvec[a] = __ddiv_rn(s, static_cast<double>(n));
+  }
+  if (threadIdx.x == 0) {
+    double s = 0.0;
+    for (int c = 0; c < n; ++c) s = __dadd_rn(s, cli_shift[c]);
+    *shift = __ddiv_rn(s, static_cast<double>(n));
+  }
+}
+
+// ------------------------------------------------------------- line search
+
+// After a trial batch: f_trial[s] = mean_c (loss_sum / n_i + reg(trial_s));
+// accept the first s with f_trial <= f_x - c * step * decrement
+// (algorithms.py:302-311).  On acceptance x_new = trial; if the batch is
+// exhausted, ST_LS_PENDING (host drives more batches); past s = 60,
+// ST_LINE_SEARCH.  Single CTA of 256 threads.
+__global__ void __launch_bounds__(256) k_ls_decide(
+    DevCtl* __restrict__ ctl, int d, int n, int ni, int nblk, double lam, double ls_c,
+    const double* __restrict__ steps_table, const double* __restrict__ trial_x,
+    const double* __restrict__ loss_part, RoundScalars* __restrict__ sc,
+    double* __restrict__ x_new, int batch) {
+  if (ctl->halt && ctl->code != ST_LS_PENDING) return;
+  __shared__ double red[8];
+  __shared__ int s_acc;
+  __shared__ double s_fbest;
+  const int s0 = ctl->ls_next;
+  if (threadIdx.x == 0) { s_acc = -1; s_fbest = (s0 == 0) ? INFINITY : ctl->f_best; }
+  __syncthreads();
+  for (int s = 0; s < batch; ++s) {
+    const int si = s0 + s;
+    const double* xt = trial_x + static_cast<int64_t>(s) * d;
+    double part = 0.0;
+    for (int a = threadIdx.x; a < d; a += blockDim.x) part = fma(xt[a], xt[a], part);
+    const double xx = block_sum(part, red);
+    if (threadIdx.x == 0 && s_acc < 0 && si <= 60) {
+      const double reg = __dmul_rn(__dmul_rn(0.5, lam), xx);
+      double tot = 0.0;
+      for (int c = 0; c < n; ++c) {
+        double ls = 0.0;
+        for (int b = 0; b < nblk; ++b)
+          ls = __dadd_rn(ls, loss_part[(static_cast<int64_t>(s) * n + c) * nblk + b]);
+        tot = __dadd_rn(tot, __dadd_rn(__ddiv_rn(ls, static_cast<double>(ni)), reg));
+      }
+      const double ft = __ddiv_rn(tot, static_cast<double>(n));
+      const double step = steps_table[si];
+      const double rhs = __dsub_rn(sc->f_mean, __dmul_rn(__dmul_rn(ls_c, step), sc->decrement));
+      if (ft <= rhs) s_acc = si;
+      else s_fbest = fmin(s_fbest, ft);
+    }
+    __syncthreads();
+  }
+  const int acc = s_acc;
+  if (acc >= 0) {
+    const double* xt = trial_x + static_cast<int64_t>(acc - s0) * d;
+    for (int a = threadIdx.x; a < d; a += blockDim.x) x_new[a] = xt[a];
+  }
+  if (threadIdx.x == 0) {
+    if (acc >= 0) {
+      ctl->ls_steps = acc;
+      ctl->ls_next = 0;
+      if (ctl->code == ST_LS_PENDING) { ctl->code = 0; ctl->halt = 0; }
+    } else if (s0 + batch > 60) {
+      ctl->f_start = sc->f_mean;
+      ctl->f_best = s_fbest;
+      if (ctl->code == ST_LS_PENDING) ctl->code = 0;
+      raise_status(ctl, ST_LINE_SEARCH);
+    } else {
+      ctl->f_best = s_fbest;
+      ctl->ls_next = s0 + batch;
+      if (ctl->code == 0) { ctl->code = ST_LS_PENDING; ctl->code_round = ctl->round; }
+      ctl->halt = 1;
+    }
+  }
+}
+
+// decrement = <gbar, p> (algorithms.py:302)
+__global__ void __launch_bounds__(256) k_dot(const DevCtl* __restrict__ ctl, int d,
+                                             const double* __restrict__ a,
+                                             const double* __restrict__ b,
+                                             RoundScalars* __restrict__ sc) {
+  if (ctl->halt) return;
+  __shared__ double red[8];
+  double part = 0.0;
+  for (int i = threadIdx.x; i < d; i += blockDim.x) part = fma(a[i], b[i], part);
+  const double s = block_sum(part, red);
+  if (threadIdx.x == 0) sc->decrement = s;
+}
+
+}  // namespace fb

@@ -1,0 +1,276 @@
+"""FedNLEngine — one device context holding a whole simulated FedNL run.
+
+Owns the C-ABI context (include/fednl_b200.h): shards in HBM, every client's
+packed Hessian estimate, the master state and the captured round graph.
+`runtime.simulate` drives it; tests use its state taps for teacher forcing.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _lib
+from .config import (
+    KIND_CODE,
+    CompressorKind,
+    DivergenceError,
+    LineSearchError,
+    NotPositiveDefiniteError,
+    RunConfig,
+    packed_length,
+    resolve_alpha,
+)
+
+
+@dataclass
+class RoundBatch:
+    """Per-round outputs of `FedNLEngine.run_rounds`."""
+
+    grad_norm: np.ndarray
+    f_value: np.ndarray
+    ls_steps: np.ndarray
+    entry_counts: np.ndarray  # [rounds, n] (-1 = did not participate)
+    wall_ms: np.ndarray
+    done: int
+
+
+def _fb_config(cfg: RunConfig, d: int, n: int, ni: int) -> _lib.FbConfig:
+    w = packed_length(d)
+    cfg.compressor.validate(w)
+    c = _lib.FbConfig()
+    c.d, c.n_clients, c.n_samples = d, n, ni
+    c.algorithm = _lib.ALG_CODE[cfg.algorithm]
+    c.kind = KIND_CODE[cfg.compressor.kind]
+    c.k = cfg.compressor.k or 0
+    c.topk_weighted = int(bool(cfg.compressor.topk_weighted))
+    c.tau = cfg.tau or 0
+    c.hessian_init = _lib.INIT_CODE[cfg.hessian_init]
+    c.alpha = float(resolve_alpha(cfg, w))
+    c.lam = float(cfg.lam)
+    c.ls_c = float(cfg.ls_c)
+    c.ls_gamma = float(cfg.ls_gamma)
+    c.run_seed = int(cfg.run_seed)
+    for s in range(61):  # gamma ** s exactly as the host evaluates it (algorithms.py:305)
+        c.ls_steps_table[s] = cfg.ls_gamma ** s
+    return c
+
+
+class FedNLEngine:
+    """Device-resident FedNL run.  Not re-entrant; one host thread."""
+
+    def __init__(self, cfg: RunConfig, d: int, n_clients: int, n_samples: int, lam: float | None = None):
+        if cfg.option != "b":
+            raise NotImplementedError(
+                "option 'a' (eigenvalue clamp) is outside this build's envelope (SURVEY §8(f))"
+            )
+        self.lib = _lib.load()
+        self.cfg = cfg
+        self.d, self.n, self.ni = d, n_clients, n_samples
+        self.w = packed_length(d)
+        fc = _fb_config(cfg, d, n_clients, n_samples)
+        if lam is not None:
+            fc.lam = float(lam)
+        self.alpha = fc.alpha
+        h = C.c_void_p()
+        rc = self.lib.fb_create(C.byref(fc), C.byref(h))
+        if rc != _lib.FB_OK:
+            msg = _lib.last_error(None)
+            if rc == _lib.FB_ERR_INVALID:
+                raise ValueError(msg)
+            raise RuntimeError(f"fb_create failed (code {rc}): {msg}")
+        self.h = h
+        self.round = 0
+
+    # ---------------------------------------------------------------- basics
+    def close(self) -> None:
+        if getattr(self, "h", None):
+            self.lib.fb_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+    def _check(self, rc: int, what: str) -> None:
+        if rc == _lib.FB_OK:
+            return
+        st = self.status()
+        msg = _lib.last_error(self.h)
+        if rc == _lib.FB_ERR_NOT_PD:
+            raise NotPositiveDefiniteError(st.pivot_index, st.pivot_value)
+        if rc == _lib.FB_ERR_NONFINITE:
+            raise ValueError("cannot compress a matrix with non-finite entries")
+        if rc == _lib.FB_ERR_DIVERGED:
+            raise DivergenceError(st.round)
+        if rc == _lib.FB_ERR_LINE_SEARCH:
+            raise LineSearchError(st.round, st.f_start, st.f_best)
+        if rc == _lib.FB_ERR_INVALID:
+            raise ValueError(msg or what)
+        raise RuntimeError(f"{what} failed (code {rc}): {msg}")
+
+    def status(self) -> _lib.FbStatus:
+        st = _lib.FbStatus()
+        self.lib.fb_get_status(self.h, C.byref(st))
+        return st
+
+    # ------------------------------------------------------------------ data
+    def upload(self, bmats: list[np.ndarray]) -> None:
+        if len(bmats) != self.n:
+            raise ValueError(f"expected {self.n} shards, got {len(bmats)}")
+        keep = []
+        ptrs = (C.POINTER(C.c_double) * self.n)()
+        for c, b in enumerate(bmats):
+            if b.shape != (self.d, self.ni):
+                raise ValueError(f"shard {c} has shape {b.shape}, expected {(self.d, self.ni)}")
+            a = np.asfortranarray(b, dtype=np.float64)
+            keep.append(a)
+            ptrs[c] = a.ctypes.data_as(C.POINTER(C.c_double))
+        self._check(self.lib.fb_upload_shards(self.h, ptrs), "fb_upload_shards")
+
+    def init_state(self, x0: np.ndarray | None = None) -> None:
+        x = None if x0 is None else np.ascontiguousarray(x0, dtype=np.float64)
+        self._check(self.lib.fb_init_state(self.h, _lib.ptr(x)), "fb_init_state")
+        self.round = 0
+
+    # ------------------------------------------------------------------- run
+    def run_rounds(self, count: int, stop_grad_norm: float | None = None,
+                   timed: bool = False, first_round: int | None = None) -> RoundBatch:
+        r0 = self.round if first_round is None else first_round
+        g = np.zeros(count)
+        f = np.zeros(count)
+        ls = np.zeros(count, dtype=np.int32)
+        cnt = np.zeros((count, self.n), dtype=np.int32)
+        wall = np.zeros(count)
+        done = C.c_int32(0)
+        rc = self.lib.fb_run_rounds(
+            self.h, r0, count, -1.0 if stop_grad_norm is None else float(stop_grad_norm),
+            int(timed), _lib.ptr(g), _lib.ptr(f), _lib.ptr(ls, C.c_int32),
+            _lib.ptr(cnt, C.c_int32), _lib.ptr(wall), C.byref(done))
+        self.round = r0 + done.value
+        self._check(rc, "fb_run_rounds")
+        k = done.value
+        return RoundBatch(g[:k], f[:k], ls[:k], cnt[:k], wall[:k], k)
+
+    def final_eval(self) -> tuple[float, float]:
+        g, f = C.c_double(), C.c_double()
+        self._check(self.lib.fb_final_eval(self.h, C.byref(g), C.byref(f)), "fb_final_eval")
+        return g.value, f.value
+
+    def profile(self) -> dict:
+        p = _lib.FbProfile()
+        self._check(self.lib.fb_get_profile(self.h, C.byref(p)), "fb_get_profile")
+        return {k: getattr(p, k) for k, _ in p._fields_}
+
+    # ------------------------------------------------------------ state taps
+    def get_x(self) -> np.ndarray:
+        x = np.zeros(self.d)
+        self._check(self.lib.fb_get_x(self.h, _lib.ptr(x)), "fb_get_x")
+        return x
+
+    def set_x(self, x: np.ndarray) -> None:
+        a = np.ascontiguousarray(x, dtype=np.float64)
+        self._check(self.lib.fb_set_x(self.h, _lib.ptr(a)), "fb_set_x")
+
+    def get_client_hest(self, c0: int = 0, c1: int | None = None) -> np.ndarray:
+        c1 = self.n if c1 is None else c1
+        out = np.zeros((c1 - c0, self.w))
+        self._check(self.lib.fb_get_client_hest(self.h, c0, c1, _lib.ptr(out)), "fb_get_client_hest")
+        return out
+
+    def set_client_hest(self, values: np.ndarray, c0: int = 0) -> None:
+        a = np.ascontiguousarray(values, dtype=np.float64).reshape(-1, self.w)
+        self._check(self.lib.fb_set_client_hest(self.h, c0, c0 + a.shape[0], _lib.ptr(a)),
+                    "fb_set_client_hest")
+
+    def get_master_hest(self) -> np.ndarray:
+        out = np.zeros(self.w)
+        self._check(self.lib.fb_get_master_hest(self.h, _lib.ptr(out)), "fb_get_master_hest")
+        return out
+
+    def set_master_hest(self, values: np.ndarray) -> None:
+        a = np.ascontiguousarray(values, dtype=np.float64)
+        self._check(self.lib.fb_set_master_hest(self.h, _lib.ptr(a)), "fb_set_master_hest")
+
+    def get_pp_state(self):
+        shift = np.zeros(1)
+        gvec = np.zeros(self.d)
+        cs = np.zeros(self.n)
+        cg = np.zeros((self.n, self.d))
+        self._check(self.lib.fb_get_pp_state(self.h, _lib.ptr(shift), _lib.ptr(gvec), _lib.ptr(cs),
+                                             _lib.ptr(cg)), "fb_get_pp_state")
+        return float(shift[0]), gvec, cs, cg
+
+    def round_diff(self, cid: int) -> np.ndarray:
+        out = np.zeros(self.w)
+        self._check(self.lib.fb_get_round_diff(self.h, cid, _lib.ptr(out)), "fb_get_round_diff")
+        return out
+
+    def round_delta(self, cid: int) -> tuple[np.ndarray | None, np.ndarray]:
+        idx = np.zeros(self.w, dtype=np.uint32)
+        val = np.zeros(self.w)
+        cnt = C.c_int32()
+        self._check(self.lib.fb_get_round_delta(self.h, cid, _lib.ptr(idx, C.c_uint32), _lib.ptr(val),
+                                                C.byref(cnt)), "fb_get_round_delta")
+        k = cnt.value
+        kind = self.cfg.compressor.kind
+        if kind in (CompressorKind.IDENTITY, CompressorKind.NATURAL):
+            return None, val if k else np.zeros(0)
+        return idx[:k].copy(), val[:k].copy()
+
+    def round_grads(self) -> tuple[np.ndarray, np.ndarray]:
+        mg = np.zeros(self.d)
+        cg = np.zeros((self.n, self.d))
+        self._check(self.lib.fb_get_round_grads(self.h, _lib.ptr(mg), _lib.ptr(cg)), "fb_get_round_grads")
+        return mg, cg
+
+    # ------------------------------------------------------------- leaf ops
+    def compress(self, diffs: np.ndarray, seeds: np.ndarray):
+        """Compress n packed differences with per-client fresh streams."""
+        D = np.ascontiguousarray(diffs, dtype=np.float64).reshape(self.n, self.w)
+        sd = np.ascontiguousarray(seeds, dtype=np.uint64)
+        idx = np.zeros((self.n, self.w), dtype=np.uint32)
+        val = np.zeros((self.n, self.w))
+        cnt = np.zeros(self.n, dtype=np.int32)
+        drw = np.zeros(self.n, dtype=np.int32)
+        rc = self.lib.fb_compress(self.h, _lib.ptr(D), _lib.ptr(sd, C.c_uint64), _lib.ptr(idx, C.c_uint32),
+                                  _lib.ptr(val), _lib.ptr(cnt, C.c_int32), _lib.ptr(drw, C.c_int32))
+        if rc == _lib.FB_ERR_NONFINITE:
+            raise ValueError("cannot compress a matrix with non-finite entries")
+        self._check(rc, "fb_compress")
+        return idx, val, cnt, drw
+
+    def oracle_eval(self, x: np.ndarray, hessian: bool = True):
+        xa = np.ascontiguousarray(x, dtype=np.float64)
+        f = np.zeros(self.n)
+        g = np.zeros((self.n, self.d))
+        h = np.zeros((self.n, self.w)) if hessian else None
+        self._check(self.lib.fb_oracle_eval(self.h, _lib.ptr(xa), _lib.ptr(f), _lib.ptr(g), _lib.ptr(h)),
+                    "fb_oracle_eval")
+        return f, g, h
+
+    def shifted_solve(self, h_packed: np.ndarray, shift: float, rhs: np.ndarray) -> np.ndarray:
+        hp = np.ascontiguousarray(h_packed, dtype=np.float64)
+        b = np.ascontiguousarray(rhs, dtype=np.float64)
+        z = np.zeros(self.d)
+        self._check(self.lib.fb_shifted_solve(self.h, _lib.ptr(hp), float(shift), _lib.ptr(b), _lib.ptr(z)),
+                    "fb_shifted_solve")
+        return z
+
+
+def fp64_peak() -> tuple[float, float]:
+    """(DMMA TFLOP/s, DFMA TFLOP/s) measured on the current device."""
+    lib = _lib.load()
+    a, b = C.c_double(), C.c_double()
+    _lib.check(lib.fb_fp64_peak(C.byref(a), C.byref(b)), None, "fb_fp64_peak")
+    return a.value, b.value

