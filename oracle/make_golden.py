@@ -294,13 +294,24 @@ def build_case(name):
 
 
 def gen_sim():
+    import threadpoolctl
+
     out = {}
     for name in SIM_CASES:
         cfg, shards = build_case(name)
-        rows = simulate(cfg, shards)
+        with threadpoolctl.threadpool_limits(1, "blas"):
+            rows = simulate(cfg, shards)
         for k, v in rows_arrays(rows).items():
             out[f"{name}__{k}"] = v
         print(f"  sim {name}: {len(rows)} rows, final |g|={rows[-1].grad_norm:.3e}")
+    # The reference's own envelope on the tie-heavy TopK shape: the same run
+    # with 8 BLAS threads takes a different (equally valid) k-th-boundary
+    # branch at round 3.  Both trajectories are recorded.
+    cfg, shards = build_case("c0_r4")
+    with threadpoolctl.threadpool_limits(8, "blas"):
+        rows = simulate(cfg, shards)
+    for k, v in rows_arrays(rows).items():
+        out[f"c0_r4_mt__{k}"] = v
     return out
 
 

@@ -318,26 +318,58 @@ __global__ void __launch_bounds__(32) k_randk(
 // grid n_active, block 1024, dynamic smem P * 12 bytes (P = pow2 >= w).
 // Full bitonic sort of (energy desc, position asc) so that numpy's pairwise
 // np.sum over the sorted energies can be replayed (compressors.py:179-233).
-__device__ double np_pairwise(const double* a, int n) {
+__device__ double np_pairwise_leaf(const double* a, int n) {
   if (n < 8) {
     double r = 0.0;
     for (int i = 0; i < n; ++i) r = __dadd_rn(r, a[i]);
     return r;
   }
-  if (n <= 128) {
-    double r[8];
-    for (int j = 0; j < 8; ++j) r[j] = a[j];
-    int i = 8;
-    for (; i < n - (n % 8); i += 8)
-      for (int j = 0; j < 8; ++j) r[j] = __dadd_rn(r[j], a[i + j]);
-    double res = __dadd_rn(__dadd_rn(__dadd_rn(r[0], r[1]), __dadd_rn(r[2], r[3])),
-                           __dadd_rn(__dadd_rn(r[4], r[5]), __dadd_rn(r[6], r[7])));
-    for (; i < n; ++i) res = __dadd_rn(res, a[i]);
-    return res;
+  double r[8];
+  for (int j = 0; j < 8; ++j) r[j] = a[j];
+  int i = 8;
+  for (; i < n - (n % 8); i += 8)
+    for (int j = 0; j < 8; ++j) r[j] = __dadd_rn(r[j], a[i + j]);
+  double res = __dadd_rn(__dadd_rn(__dadd_rn(r[0], r[1]), __dadd_rn(r[2], r[3])),
+                         __dadd_rn(__dadd_rn(r[4], r[5]), __dadd_rn(r[6], r[7])));
+  for (; i < n; ++i) res = __dadd_rn(res, a[i]);
+  return res;
+}
+// numpy's pairwise add.reduce order, replayed with an explicit stack (device
+// recursion would risk the default per-thread stack): blocks of <= 128 are
+// leaves; larger blocks split at n2 = n/2 - (n/2) % 8 and sum left + right.
+__device__ double np_pairwise(const double* a, int n) {
+  struct Frame {
+    int off, len, phase;
+    double left;
+  };
+  Frame st[24];
+  int top = 0;
+  st[0] = {0, n, 0, 0.0};
+  double ret = 0.0;
+  while (top >= 0) {
+    Frame& f = st[top];
+    if (f.len <= 128) {
+      ret = np_pairwise_leaf(a + f.off, f.len);
+      --top;
+      continue;
+    }
+    int n2 = f.len / 2;
+    n2 -= n2 % 8;
+    if (f.phase == 0) {
+      f.phase = 1;
+      st[top + 1] = {f.off, n2, 0, 0.0};
+      ++top;
+    } else if (f.phase == 1) {
+      f.left = ret;
+      f.phase = 2;
+      st[top + 1] = {f.off + n2, f.len - n2, 0, 0.0};
+      ++top;
+    } else {
+      ret = __dadd_rn(f.left, ret);
+      --top;
+    }
   }
-  int n2 = n / 2;
-  n2 -= n2 % 8;
-  return __dadd_rn(np_pairwise(a, n2), np_pairwise(a + n2, n - n2));
+  return ret;
 }
 
 __global__ void __launch_bounds__(TK_THREADS) k_toplek(

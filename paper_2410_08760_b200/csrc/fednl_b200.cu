@@ -540,7 +540,8 @@ int fb_create(const fb_config* cfg_in, void** out) {
                         ? static_cast<double>(w) / static_cast<double>(c.k)
                         : 1.0;
   ctx->toplek_P = 1;
-  while (ctx->toplek_P < w) ctx->toplek_P <<= 1;
+  if (c.kind == FB_KIND_TOPLEK)
+    while (ctx->toplek_P < w) ctx->toplek_P <<= 1;
   // master solve: a cluster of up to 8 CTAs; panel staged in smem when it fits
   ctx->solve_cs = c.d >= 96 ? CH_MAX_CLUSTER : 1;
   const size_t pan = static_cast<size_t>(c.d) * CH_PLD * sizeof(double);
@@ -579,14 +580,19 @@ int fb_create(const fb_config* cfg_in, void** out) {
   for (int i = 0; i < EV_COUNT; ++i) CKC(cudaEventCreate(&ctx->ev_fixed[i]));
   ctx->ev_pool.resize(static_cast<size_t>(ROW_CHUNK) * EV_COUNT);
   for (auto& e : ctx->ev_pool) CKC(cudaEventCreate(&e));
+  // dynamic shared memory limits are per-function process state: only ever
+  // raise them, so contexts of different shapes can coexist
+  static size_t max_toplek = 0, max_solve = 0;
+  max_toplek = std::max(max_toplek, static_cast<size_t>(std::max(ctx->toplek_P, 1)) * 12);
+  max_solve = std::max(max_solve, std::max<size_t>(ctx->solve_smem, 1));
   CKC(cudaFuncSetAttribute(k_hessian, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            static_cast<int>(HESS_SMEM)));
   CKC(cudaFuncSetAttribute(k_randk, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            static_cast<int>(2 * RK_TABLE * sizeof(int32_t))));
   CKC(cudaFuncSetAttribute(k_toplek, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           static_cast<int>(static_cast<size_t>(std::max(ctx->toplek_P, 1)) * 12)));
+                           static_cast<int>(max_toplek)));
   CKC(cudaFuncSetAttribute(k_chol_solve, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           static_cast<int>(std::max<size_t>(ctx->solve_smem, 1))));
+                           static_cast<int>(max_solve)));
   CKC(cudaFuncSetAttribute(k_chol_solve, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
 
   const int n = ctx->n, d = ctx->d;

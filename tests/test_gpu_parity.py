@@ -269,19 +269,29 @@ def test_round_fold_bit_exact_given_device_deltas(kind, k):
 # --------------------------------------------------------------------- P6
 
 
-def _rows_close(rows, g, name, rel=1e-10, floor=1e-6, f_rel=1e-12):
-    want_g = g[f"{name}__grad_norm"]
-    want_f = g[f"{name}__f_value"]
-    assert [r.round for r in rows] == g[f"{name}__round"].tolist()
-    assert [r.bytes_up_cum for r in rows] == g[f"{name}__bytes_up"].tolist()
-    assert [r.bytes_down_cum for r in rows] == g[f"{name}__bytes_down"].tolist()
-    assert [r.ls_steps for r in rows] == g[f"{name}__ls_steps"].tolist()
+def _rows_close(rows, g, names, rel=1e-10, floor=1e-6, abs_floor=4e-16, f_rel=1e-12):
+    """Row-wise P6 check against one or more of the reference's own valid
+    trajectories (`names`): each row must be within tolerance of at least one.
+
+    grad tolerance: rel * max(g_ref, floor * g_ref[0]) + abs_floor * g_ref[0]
+    (the absolute term is the rounding noise of a mean of n client gradients
+    of size ~g_ref[0], reached in the converged tail).
+    """
+    base = names[0]
+    assert [r.round for r in rows] == g[f"{base}__round"].tolist()
+    assert [r.bytes_up_cum for r in rows] == g[f"{base}__bytes_up"].tolist()
+    assert [r.bytes_down_cum for r in rows] == g[f"{base}__bytes_down"].tolist()
+    assert [r.ls_steps for r in rows] == g[f"{base}__ls_steps"].tolist()
     gn = np.array([r.grad_norm for r in rows])
     fv = np.array([r.f_value for r in rows])
-    tol = rel * np.maximum(want_g, floor * want_g[0])
-    bad = np.flatnonzero(np.abs(gn - want_g) > tol)
-    assert bad.size == 0, (name, bad, gn[bad], want_g[bad])
-    assert np.all(np.abs(fv - want_f) <= f_rel * np.abs(want_f)), name
+    ok = np.zeros(len(rows), dtype=bool)
+    for name in names:
+        want_g = g[f"{name}__grad_norm"]
+        want_f = g[f"{name}__f_value"]
+        tol = rel * np.maximum(want_g, floor * want_g[0]) + abs_floor * want_g[0]
+        ok |= (np.abs(gn - want_g) <= tol) & (np.abs(fv - want_f) <= f_rel * np.abs(want_f))
+    bad = np.flatnonzero(~ok)
+    assert bad.size == 0, (base, bad, gn[bad], fv[bad])
 
 
 SIM = {
@@ -339,8 +349,9 @@ def test_simulate_rows_match_reference(name):
     rows = simulate(cfg, shards)
     g = golden("simulate.npz")
     if name == "c0_r4":
-        # TopK at a real shape: ties at the k-th boundary make the reference
-        # itself move by ~1e-6 between BLAS thread counts
-        _rows_close(rows, g, name, rel=1e-5, f_rel=1e-9)
+        # TopK at a real shape: the reference itself takes either branch of a
+        # k-th-boundary tie at round 3 depending on BLAS threading (SURVEY
+        # §0.4); both trajectories were recorded from the reference.
+        _rows_close(rows, g, ["c0_r4", "c0_r4_mt"])
     else:
-        _rows_close(rows, g, name)
+        _rows_close(rows, g, [name])
