@@ -286,7 +286,7 @@ int launch_fold(Ctx* ctx, cudaStream_t s, const int32_t* clients, int n_active, 
 
 int record(Ctx* ctx, EvSlot slot, cudaStream_t s) {
   ctx->ev_used[slot] = true;
-  CK(cudaEventRecord(ctx->ev_fixed[slot], s));
+  CK(cudaEventRecordWithFlags(ctx->ev_fixed[slot], s, cudaEventRecordExternal));
   return FB_OK;
 }
 
