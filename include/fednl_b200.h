@@ -182,6 +182,13 @@ int fb_oracle_eval(void* ctx, const double* x, double* f, double* grad, double* 
 int fb_shifted_solve(void* ctx, const double* h_packed, double shift, const double* rhs,
                      double* z);
 
+/* diagnostic: per-phase clock64 cycles of one shifted solve on the rank-0
+ * CTA (12 slots: setup, A, syncA, pull, B, B-writeback, C, syncC,
+ * back-solve, back-total, -, -), optional cluster-size
+ * override (0 = default) and its event time in ms */
+int fb_solve_phase_cycles(void* ctx, const double* h_packed, double shift, const double* rhs,
+                          int32_t cluster, long long* cycles, float* ms);
+
 /* ---- context-free device SplitMix64 (rng.py:37-136) -------------------- */
 int fb_prg_u64(uint64_t seed, int32_t count, uint64_t* out);
 /* reps draws of randrange(bounds[b]) from a fresh Prg(seed) per bound;

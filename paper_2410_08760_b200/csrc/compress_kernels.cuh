@@ -62,33 +62,65 @@ __device__ __forceinline__ int block_excl_scan(int v, int* ws, int* total) {
   return before + x - v;
 }
 
+// What a compressor emits besides its (idx, val) list:
+//  * the client's shift update Hest[c][t] = fl(Hest + fl(alpha v)) at every
+//    selected position (compressors.py:373-393, algorithms.py:234) when hest
+//    is non-null, and
+//  * range starts rs[c][r] = #entries with position < r * FOLD_RANGE
+//    (r = 0..nr) so the master fold can slice every client's list by range.
+constexpr int FOLD_RANGE = 256;
+struct Emit {
+  double* hest;
+  int64_t hest_stride;
+  double alpha;
+  int32_t* rs;
+  int nr;
+};
+__device__ __forceinline__ void emit_entry(const Emit& em, int c, int64_t t, double v) {
+  if (em.hest) {
+    double* hp = em.hest + static_cast<int64_t>(c) * em.hest_stride + t;
+    *hp = __dadd_rn(*hp, __dmul_rn(em.alpha, v));
+  }
+}
+
+__device__ __forceinline__ void emit_empty(const Emit& em, int c) {
+  if (em.rs)
+    for (int r = threadIdx.x; r <= em.nr; r += blockDim.x) em.rs[static_cast<int64_t>(c) * (em.nr + 1) + r] = 0;
+}
+
 __device__ __forceinline__ void clear_row(uint32_t* row, int wb) {
   for (int q = threadIdx.x; q < wb; q += blockDim.x) row[q] = 0u;
 }
 
 // Compact a bitmap row into ascending (idx, val) lists; val = fl(v * scale)
-// when scale != 1 (Rand kinds).  Whole block, any blockDim multiple of 32.
+// when scale != 1 (Rand kinds).  Emits the client update and range starts.
+// Whole block, any blockDim multiple of 32.
 __device__ void compact_bitmap(const uint32_t* __restrict__ row, int wb,
                                const double* __restrict__ v, double scale, uint32_t* idx,
-                               double* val, int* ws) {
+                               double* val, int* ws, const Emit& em, int c) {
   int carry = 0;
+  int32_t* rsc = em.rs ? em.rs + static_cast<int64_t>(c) * (em.nr + 1) : nullptr;
   for (int base = 0; base < wb; base += blockDim.x) {
     const int q = base + threadIdx.x;
     const uint32_t word = (q < wb) ? row[q] : 0u;
     int total;
     int off = block_excl_scan(__popc(word), ws, &total) + carry;
+    if (rsc && q < wb && (q % (FOLD_RANGE / 32)) == 0) rsc[q / (FOLD_RANGE / 32)] = off;
     uint32_t m = word;
     while (m) {
       const int bit = __ffs(m) - 1;
       m &= m - 1;
       const int64_t t = static_cast<int64_t>(q) * 32 + bit;
+      const double x = (scale == 1.0) ? v[t] : __dmul_rn(v[t], scale);
       idx[off] = static_cast<uint32_t>(t);
-      val[off] = (scale == 1.0) ? v[t] : __dmul_rn(v[t], scale);
+      val[off] = x;
+      emit_entry(em, c, t, x);
       ++off;
     }
     carry += total;
     __syncthreads();
   }
+  if (rsc && threadIdx.x == 0) rsc[em.nr] = carry;
 }
 
 // ------------------------------------------------------------------- TopK
@@ -97,7 +129,7 @@ __global__ void __launch_bounds__(TK_THREADS) k_topk(
     const DevCtl* __restrict__ ctl, const double* __restrict__ D, int64_t w, int wb, int k,
     int weighted, const int32_t* __restrict__ clients, const int32_t* __restrict__ flags,
     uint32_t* __restrict__ bitmap, int32_t* __restrict__ count, uint32_t* __restrict__ idx_list,
-    double* __restrict__ val_list, int cap, int32_t* __restrict__ draws) {
+    double* __restrict__ val_list, int cap, int32_t* __restrict__ draws, Emit em) {
   if (ctl && ctl->halt) return;
   __shared__ uint32_t hist[2048];
   __shared__ int ws[64];
@@ -108,6 +140,7 @@ __global__ void __launch_bounds__(TK_THREADS) k_topk(
   if (threadIdx.x == 0 && draws) draws[c] = 0;
   if (!(flags[c] & 2)) {  // all-zero difference: empty delta, no draws
     clear_row(brow, wb);
+    emit_empty(em, c);
     if (threadIdx.x == 0) count[c] = 0;
     return;
   }
@@ -178,9 +211,12 @@ __global__ void __launch_bounds__(TK_THREADS) k_topk(
     int tot_sel;
     const int pos = block_excl_scan(sel, ws, &tot_sel) + carry_sel;
     carry_sel += tot_sel;
+    if (em.rs && t < w && (t % FOLD_RANGE) == 0)
+      em.rs[static_cast<int64_t>(c) * (em.nr + 1) + t / FOLD_RANGE] = pos;
     if (sel) {
       il[pos] = static_cast<uint32_t>(t);
       vl[pos] = vt;
+      emit_entry(em, c, t, vt);
     }
     const uint32_t word = __ballot_sync(0xffffffffu, sel);
     if (lane == 0 && t < w + 31) {
@@ -188,7 +224,229 @@ __global__ void __launch_bounds__(TK_THREADS) k_topk(
       if (q < wb) brow[q] = word;
     }
   }
-  if (threadIdx.x == 0) count[c] = carry_sel;
+  if (threadIdx.x == 0) {
+    count[c] = carry_sel;
+    if (em.rs) em.rs[static_cast<int64_t>(c) * (em.nr + 1) + em.nr] = carry_sel;
+  }
+}
+
+// ------------------------------------------------- TopK, shared-memory path
+// For w <= TKS_MAXW the upper 32 bits of every key stay in shared memory
+// after ONE coalesced pass over D (which also builds the first histogram);
+// the remaining radix levels on those bits run out of shared memory, and only
+// the (usually tiny) group tied on the upper 32 bits is re-read from global
+// memory to resolve the low 31 bits.  The selection rule is identical to
+// k_topk (descending key, ties to the smaller position).
+constexpr int TKS_MAXW = 46000;
+constexpr int TKS_CAND = 2048;
+constexpr size_t TKS_SMEM = static_cast<size_t>(TKS_MAXW) * 4;
+
+// Radix digit search over hist[0, nbins): the digit holding the need-th
+// largest element (counting from the top bin).  Whole block; returns digit
+// and the count strictly above it through shared scalars.
+__device__ __forceinline__ void tks_find_digit(const uint32_t* hist, int nbins, int need, int* ws,
+                                               int* s_digit, int* s_above) {
+  const int b0 = nbins - 1 - 2 * static_cast<int>(threadIdx.x), b1 = b0 - 1;
+  const int c0 = (b0 >= 0) ? static_cast<int>(hist[b0]) : 0;
+  const int c1 = (b1 >= 0) ? static_cast<int>(hist[b1]) : 0;
+  int total;
+  const int above0 = block_excl_scan(c0 + c1, ws, &total);
+  const int above1 = above0 + c0;
+  if (c0 > 0 && above0 < need && need <= above0 + c0) { *s_digit = b0; *s_above = above0; }
+  if (c1 > 0 && above1 < need && need <= above1 + c1) { *s_digit = b1; *s_above = above1; }
+  __syncthreads();
+}
+
+__device__ __forceinline__ void tks_add(uint32_t* hist, uint32_t dig, int lane) {
+  const uint32_t peers = __match_any_sync(0xffffffffu, dig);
+  if (dig != 0xFFFFFFFFu && lane == __ffs(peers) - 1) atomicAdd(&hist[dig], __popc(peers));
+}
+
+__global__ void __launch_bounds__(TK_THREADS, 1) k_topk_smem(
+    const DevCtl* __restrict__ ctl, const double* __restrict__ D, int64_t w, int wb, int k,
+    int weighted, const int32_t* __restrict__ clients, const int32_t* __restrict__ flags,
+    uint32_t* __restrict__ bitmap, int32_t* __restrict__ count, uint32_t* __restrict__ idx_list,
+    double* __restrict__ val_list, int cap, int32_t* __restrict__ draws, Emit em) {
+  if (ctl && ctl->halt) return;
+  extern __shared__ uint32_t hi_s[];  // [w] upper 32 key bits
+  __shared__ uint32_t hist[2048];
+  __shared__ uint32_t cand_lo[TKS_CAND];
+  __shared__ int ws[64];
+  __shared__ int s_digit, s_above, s_ncand;
+  const int c = client_of(clients, blockIdx.x);
+  const int tid = threadIdx.x, lane = tid & 31;
+  const double* v = D + static_cast<int64_t>(c) * w;
+  uint32_t* brow = bitmap + static_cast<int64_t>(c) * wb;
+  if (tid == 0 && draws) draws[c] = 0;
+  if (!(flags[c] & 2)) {
+    clear_row(brow, wb);
+    emit_empty(em, c);
+    if (tid == 0) count[c] = 0;
+    return;
+  }
+  const int wi = static_cast<int>(w);
+  // ---- pass 0: keys' upper halves into smem + histogram of hi bits [21, 32)
+  for (int i = tid; i < 2048; i += TK_THREADS) hist[i] = 0u;
+  if (tid == 0) s_ncand = 0;
+  __syncthreads();
+  for (int base = 0; base < wi; base += 4 * TK_THREADS) {
+    double x[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int t = base + u * TK_THREADS + tid;
+      x[u] = (t < wi) ? __ldg(v + t) : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int t = base + u * TK_THREADS + tid;
+      uint32_t dig = 0xFFFFFFFFu;
+      if (t < wi) {
+        const uint32_t hi = static_cast<uint32_t>(rank_key(x[u], t, weighted) >> 31);
+        hi_s[t] = hi;
+        dig = hi >> 21;
+      }
+      tks_add(hist, dig, lane);
+    }
+  }
+  __syncthreads();
+  // ---- radix levels on the upper 32 bits (all in shared memory)
+  constexpr int HSH[3] = {21, 10, 0};
+  constexpr int HBI[3] = {11, 11, 10};
+  uint32_t prefix = 0;
+  int need = k;
+  int level_shift = 0;     // shift of the prefix that decides the selection
+  bool take_all = false;   // every element with that prefix is selected
+  for (int L = 0; L < 3; ++L) {
+    if (L > 0) {
+      for (int i = tid; i < 2048; i += TK_THREADS) hist[i] = 0u;
+      __syncthreads();
+      const int hsh = HSH[L - 1];
+      for (int base = 0; base < wi; base += TK_THREADS) {
+        const int t = base + tid;
+        uint32_t dig = 0xFFFFFFFFu;
+        if (t < wi) {
+          const uint32_t hi = hi_s[t];
+          if ((hi >> hsh) == prefix) dig = (hi >> HSH[L]) & ((1u << HBI[L]) - 1u);
+        }
+        tks_add(hist, dig, lane);
+      }
+      __syncthreads();
+    }
+    tks_find_digit(hist, 1 << HBI[L], need, ws, &s_digit, &s_above);
+    const int dg = s_digit;
+    need -= s_above;
+    prefix = (L == 0) ? static_cast<uint32_t>(dg) : ((prefix << HBI[L]) | static_cast<uint32_t>(dg));
+    level_shift = HSH[L];
+    const bool all = (static_cast<int>(hist[dg]) == need);
+    __syncthreads();
+    if (all) { take_all = true; break; }
+  }
+  // prefix now equals hi >> level_shift of the threshold group
+  // ---- low 31 bits among the elements tied on all 32 upper bits
+  uint32_t lo_prefix = 0;
+  int lo_shift = 0;
+  bool lo_all = false;
+  const uint32_t T_hi = prefix;  // meaningful when !take_all (level_shift == 0)
+  if (!take_all) {
+    const int ncand_total = static_cast<int>(hist[s_digit]);  // group size (stale-safe: read below)
+    (void)ncand_total;
+    // gather candidates (positions ascending is not required here)
+    for (int base = 0; base < wi; base += TK_THREADS) {
+      const int t = base + tid;
+      if (t < wi && hi_s[t] == T_hi) {
+        const int slot = atomicAdd(&s_ncand, 1);
+        if (slot < TKS_CAND) {
+          cand_lo[slot] = static_cast<uint32_t>(rank_key(__ldg(v + t), t, weighted) & 0x7FFFFFFFull);
+        }
+      }
+    }
+    __syncthreads();
+    const int ncand = s_ncand;
+    const bool in_smem = ncand <= TKS_CAND;
+    constexpr int LSH[3] = {20, 10, 0};
+    constexpr int LBI[3] = {11, 10, 10};
+    for (int L = 0; L < 3; ++L) {
+      for (int i = tid; i < 2048; i += TK_THREADS) hist[i] = 0u;
+      __syncthreads();
+      const int upper = L == 0 ? 31 : LSH[L - 1];
+      if (in_smem) {
+        for (int base = 0; base < ncand; base += TK_THREADS) {
+          const int e = base + tid;
+          uint32_t dig = 0xFFFFFFFFu;
+          if (e < ncand) {
+            const uint32_t lo = cand_lo[e];
+            if ((upper >= 31 ? 0u : (lo >> upper)) == lo_prefix) dig = (lo >> LSH[L]) & ((1u << LBI[L]) - 1u);
+          }
+          tks_add(hist, dig, lane);
+        }
+      } else {
+        for (int base = 0; base < wi; base += TK_THREADS) {
+          const int t = base + tid;
+          uint32_t dig = 0xFFFFFFFFu;
+          if (t < wi && hi_s[t] == T_hi) {
+            const uint32_t lo = static_cast<uint32_t>(rank_key(__ldg(v + t), t, weighted) & 0x7FFFFFFFull);
+            if ((upper >= 31 ? 0u : (lo >> upper)) == lo_prefix) dig = (lo >> LSH[L]) & ((1u << LBI[L]) - 1u);
+          }
+          tks_add(hist, dig, lane);
+        }
+      }
+      __syncthreads();
+      tks_find_digit(hist, 1 << LBI[L], need, ws, &s_digit, &s_above);
+      const int dg = s_digit;
+      need -= s_above;
+      lo_prefix = (L == 0) ? static_cast<uint32_t>(dg) : ((lo_prefix << LBI[L]) | static_cast<uint32_t>(dg));
+      lo_shift = LSH[L];
+      const bool all = (static_cast<int>(hist[dg]) == need);
+      __syncthreads();
+      if (all) { lo_all = true; break; }
+    }
+  }
+  // ---- final pass, ascending positions
+  int carry_sel = 0, carry_eq = 0;
+  uint32_t* il = idx_list + static_cast<int64_t>(c) * cap;
+  double* vl = val_list + static_cast<int64_t>(c) * cap;
+  for (int base = 0; base < wi; base += TK_THREADS) {
+    const int t = base + tid;
+    int sel = 0, eq = 0;
+    if (t < wi) {
+      const uint32_t hp = hi_s[t] >> level_shift;
+      if (take_all) {
+        sel = hp >= prefix;
+      } else if (hp > T_hi) {
+        sel = 1;
+      } else if (hp == T_hi) {
+        const uint32_t lp = static_cast<uint32_t>(rank_key(__ldg(v + t), t, weighted) & 0x7FFFFFFFull) >> lo_shift;
+        if (lp > lo_prefix) sel = 1;
+        else if (lp == lo_prefix) {
+          if (lo_all) sel = 1;
+          else eq = 1;
+        }
+      }
+    }
+    if (!take_all && !lo_all) {
+      int tot_eq;
+      const int r = block_excl_scan(eq, ws, &tot_eq) + carry_eq;
+      carry_eq += tot_eq;
+      if (eq && r < need) sel = 1;
+    }
+    int tot_sel;
+    const int pos = block_excl_scan(sel, ws, &tot_sel) + carry_sel;
+    carry_sel += tot_sel;
+    if (em.rs && t < wi && (t % FOLD_RANGE) == 0)
+      em.rs[static_cast<int64_t>(c) * (em.nr + 1) + t / FOLD_RANGE] = pos;
+    if (sel) {
+      const double vt = __ldg(v + t);
+      il[pos] = static_cast<uint32_t>(t);
+      vl[pos] = vt;
+      emit_entry(em, c, t, vt);
+    }
+    const uint32_t word = __ballot_sync(0xffffffffu, sel);
+    if (lane == 0 && (t >> 5) < wb) brow[t >> 5] = word;
+  }
+  if (tid == 0) {
+    count[c] = carry_sel;
+    if (em.rs) em.rs[static_cast<int64_t>(c) * (em.nr + 1) + em.nr] = carry_sel;
+  }
 }
 
 // --------------------------------------------------------------- RandSeqK
@@ -199,13 +457,14 @@ __global__ void __launch_bounds__(256) k_randseqk(
     const int32_t* __restrict__ clients, const int32_t* __restrict__ flags, uint64_t run_seed,
     const uint64_t* __restrict__ seeds, uint32_t* __restrict__ bitmap,
     int32_t* __restrict__ count, uint32_t* __restrict__ idx_list, double* __restrict__ val_list,
-    int cap, int32_t* __restrict__ draws) {
+    int cap, int32_t* __restrict__ draws, Emit em) {
   if (ctl && ctl->halt) return;
   __shared__ int64_t s_start;
   const int c = client_of(clients, blockIdx.x);
   uint32_t* brow = bitmap + static_cast<int64_t>(c) * wb;
   if (!(flags[c] & 2)) {
     clear_row(brow, wb);
+    emit_empty(em, c);
     if (threadIdx.x == 0) { count[c] = 0; if (draws) draws[c] = 0; }
     return;
   }
@@ -225,8 +484,20 @@ __global__ void __launch_bounds__(256) k_randseqk(
   double* vl = val_list + static_cast<int64_t>(c) * cap;
   for (int i = threadIdx.x; i < k; i += blockDim.x) {
     const int64_t t = (i < wrap) ? i : s + (i - wrap);
+    const double x = __dmul_rn(v[t], scale);
     il[i] = static_cast<uint32_t>(t);
-    vl[i] = __dmul_rn(v[t], scale);
+    vl[i] = x;
+    emit_entry(em, c, t, x);
+  }
+  if (em.rs) {  // selected = [0, wrap) U [s, s + k - wrap)
+    for (int r = threadIdx.x; r <= em.nr; r += blockDim.x) {
+      const int64_t T0 = static_cast<int64_t>(r) * FOLD_RANGE;
+      const int64_t T = (T0 < w) ? T0 : w;
+      const int64_t hi = s + (k - wrap);
+      const int64_t lim = (T < hi) ? T : hi;
+      const int64_t cnt = ((T < wrap) ? T : wrap) + ((lim > s) ? lim - s : 0);
+      em.rs[static_cast<int64_t>(c) * (em.nr + 1) + r] = static_cast<int32_t>(cnt);
+    }
   }
   for (int q = threadIdx.x; q < wb; q += blockDim.x) {
     uint32_t word = 0u;
@@ -257,7 +528,7 @@ __global__ void __launch_bounds__(32) k_randk(
     const int32_t* __restrict__ clients, const int32_t* __restrict__ flags, uint64_t run_seed,
     const uint64_t* __restrict__ seeds, uint32_t* __restrict__ bitmap,
     int32_t* __restrict__ count, uint32_t* __restrict__ idx_list, double* __restrict__ val_list,
-    int cap, int32_t* __restrict__ draws, int64_t* __restrict__ jbuf) {
+    int cap, int32_t* __restrict__ draws, int64_t* __restrict__ jbuf, Emit em) {
   if (ctl && ctl->halt) return;
   extern __shared__ int32_t tab[];  // keys[RK_TABLE], vals[RK_TABLE]
   __shared__ int ws[64];
@@ -269,6 +540,7 @@ __global__ void __launch_bounds__(32) k_randk(
   uint32_t* brow = bitmap + static_cast<int64_t>(c) * wb;
   clear_row(brow, wb);
   if (!(flags[c] & 2)) {
+    emit_empty(em, c);
     if (lane == 0) { count[c] = 0; if (draws) draws[c] = 0; }
     return;
   }
@@ -311,7 +583,7 @@ __global__ void __launch_bounds__(32) k_randk(
   const double scale = static_cast<double>(w) / static_cast<double>(k);
   compact_bitmap(brow, wb, D + static_cast<int64_t>(c) * w, scale,
                  idx_list + static_cast<int64_t>(c) * cap, val_list + static_cast<int64_t>(c) * cap,
-                 ws);
+                 ws, em, c);
 }
 
 // ----------------------------------------------------------------- TopLEK
@@ -377,7 +649,7 @@ __global__ void __launch_bounds__(TK_THREADS) k_toplek(
     const int32_t* __restrict__ clients, const int32_t* __restrict__ flags, uint64_t run_seed,
     const uint64_t* __restrict__ seeds, uint32_t* __restrict__ bitmap,
     int32_t* __restrict__ count, uint32_t* __restrict__ idx_list, double* __restrict__ val_list,
-    int cap, int32_t* __restrict__ draws, int P) {
+    int cap, int32_t* __restrict__ draws, int P, Emit em) {
   if (ctl && ctl->halt) return;
   extern __shared__ uint8_t tl_raw[];
   double* en = reinterpret_cast<double*>(tl_raw);                    // [P]
@@ -389,6 +661,7 @@ __global__ void __launch_bounds__(TK_THREADS) k_toplek(
   uint32_t* brow = bitmap + static_cast<int64_t>(c) * wb;
   clear_row(brow, wb);
   if (!(flags[c] & 2)) {
+    emit_empty(em, c);
     if (threadIdx.x == 0) { count[c] = 0; if (draws) draws[c] = 0; }
     return;
   }
@@ -466,7 +739,7 @@ __global__ void __launch_bounds__(TK_THREADS) k_toplek(
   }
   __syncthreads();
   compact_bitmap(brow, wb, v, 1.0, idx_list + static_cast<int64_t>(c) * cap,
-                 val_list + static_cast<int64_t>(c) * cap, ws);
+                 val_list + static_cast<int64_t>(c) * cap, ws, em, c);
 }
 
 // --------------------------------------------------------- identity / natural

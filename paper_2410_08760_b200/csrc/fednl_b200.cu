@@ -12,6 +12,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -51,7 +52,7 @@ struct Ctx {
   int cap = 0, tau = 0, n_active_max = 0;
   int64_t w = 0;
   double alpha_n = 0.0, rand_scale = 1.0;
-  int solve_cs = 1, solve_stage = 0;
+  int solve_cs = 1, solve_nb = 32;
   size_t solve_smem = 0;
   int toplek_P = 0;
   bool uploaded = false, initialised = false;
@@ -65,7 +66,10 @@ struct Ctx {
   double *hcoef = nullptr, *gcoef = nullptr, *loss_part = nullptr, *grad = nullptr;
   double *gbar = nullptr, *f_cli = nullptr, *shift_cli = nullptr, *frob_part = nullptr;
   int32_t* flags = nullptr;
-  double *hest = nullptr, *D = nullptr, *hmas = nullptr, *M = nullptr, *zeros_w = nullptr;
+  double *hest = nullptr, *D = nullptr, *hmas = nullptr, *hmas2 = nullptr, *M = nullptr,
+         *zeros_w = nullptr;
+  int32_t* rs = nullptr;  // per-client range starts of the compressed lists
+  int nr = 0;
   uint32_t* bitmap = nullptr;
   int32_t *count = nullptr, *draws = nullptr;
   uint32_t* idx_list = nullptr;
@@ -216,30 +220,45 @@ int launch_reduce(Ctx* ctx, cudaStream_t s, const double* x, const int32_t* clie
 // compressor of the configured kind over `n_active` clients; seeds null =
 // per-(client, round) streams from the device round counter.
 int launch_compress(Ctx* ctx, cudaStream_t s, const int32_t* clients, int n_active,
-                    const uint64_t* seeds, double* dense_out, bool with_ctl = true) {
+                    const uint64_t* seeds, double* dense_out, bool with_ctl = true,
+                    bool emit = true) {
   const fb_config& c = ctx->cfg;
   DevCtl* ctl = with_ctl ? ctx->ctl : nullptr;
+  Emit em{};
+  if (emit) {
+    em.hest = ctx->hest;
+    em.hest_stride = ctx->w;
+    em.alpha = c.alpha;
+    em.rs = ctx->rs;
+    em.nr = ctx->nr;
+  }
   switch (c.kind) {
     case FB_KIND_TOPK:
-      k_topk<<<n_active, TK_THREADS, 0, s>>>(ctl, ctx->D, ctx->w, ctx->wb, c.k, c.topk_weighted,
-                                             clients, ctx->flags, ctx->bitmap, ctx->count,
-                                             ctx->idx_list, ctx->val_list, ctx->cap, ctx->draws);
+      if (ctx->w <= TKS_MAXW)
+        k_topk_smem<<<n_active, TK_THREADS, static_cast<size_t>(ctx->w) * 4, s>>>(
+            ctl, ctx->D, ctx->w, ctx->wb, c.k, c.topk_weighted, clients, ctx->flags, ctx->bitmap,
+            ctx->count, ctx->idx_list, ctx->val_list, ctx->cap, ctx->draws, em);
+      else
+        k_topk<<<n_active, TK_THREADS, 0, s>>>(ctl, ctx->D, ctx->w, ctx->wb, c.k, c.topk_weighted,
+                                               clients, ctx->flags, ctx->bitmap, ctx->count,
+                                               ctx->idx_list, ctx->val_list, ctx->cap, ctx->draws,
+                                               em);
       break;
     case FB_KIND_RANDSEQK:
       k_randseqk<<<n_active, 256, 0, s>>>(ctl, ctx->D, ctx->w, ctx->wb, c.k, clients, ctx->flags,
                                           c.run_seed, seeds, ctx->bitmap, ctx->count,
-                                          ctx->idx_list, ctx->val_list, ctx->cap, ctx->draws);
+                                          ctx->idx_list, ctx->val_list, ctx->cap, ctx->draws, em);
       break;
     case FB_KIND_RANDK:
       k_randk<<<n_active, 32, 2 * RK_TABLE * sizeof(int32_t), s>>>(
           ctl, ctx->D, ctx->w, ctx->wb, c.k, clients, ctx->flags, c.run_seed, seeds, ctx->bitmap,
-          ctx->count, ctx->idx_list, ctx->val_list, ctx->cap, ctx->draws, ctx->jbuf);
+          ctx->count, ctx->idx_list, ctx->val_list, ctx->cap, ctx->draws, ctx->jbuf, em);
       break;
     case FB_KIND_TOPLEK:
       k_toplek<<<n_active, TK_THREADS, static_cast<size_t>(ctx->toplek_P) * 12, s>>>(
           ctl ? ctl : ctx->ctl, ctx->D, ctx->w, ctx->wb, c.k, clients, ctx->flags, c.run_seed,
           seeds, ctx->bitmap, ctx->count, ctx->idx_list, ctx->val_list, ctx->cap, ctx->draws,
-          ctx->toplek_P);
+          ctx->toplek_P, em);
       break;
     case FB_KIND_IDENTITY:
     case FB_KIND_NATURAL: {
@@ -257,7 +276,7 @@ int launch_compress(Ctx* ctx, cudaStream_t s, const int32_t* clients, int n_acti
 }
 int launch_solve(Ctx* ctx, cudaStream_t s, const double* hpk, const double* shift_ptr,
                  const double* rhs, const double* x, double* z, double* x_out, int mode,
-                 int ignore_halt) {
+                 int ignore_halt, long long* dbg = nullptr) {
   cudaLaunchConfig_t lc{};
   lc.gridDim = dim3(ctx->solve_cs);
   lc.blockDim = dim3(CH_THREADS);
@@ -270,16 +289,31 @@ int launch_solve(Ctx* ctx, cudaStream_t s, const double* hpk, const double* shif
   attr[0].val.clusterDim.z = 1;
   lc.attrs = attr;
   lc.numAttrs = 1;
-  CK(cudaLaunchKernelEx(&lc, k_chol_solve, ctx->ctl, ctx->d, hpk, shift_ptr, rhs, x, ctx->M, z,
-                        x_out, mode, ctx->solve_stage, ignore_halt));
+  if (ctx->solve_nb == 32)
+    CK(cudaLaunchKernelEx(&lc, k_chol_solve<32>, ctx->ctl, ctx->d, hpk, shift_ptr, rhs, x, ctx->M,
+                          z, x_out, mode, ignore_halt, dbg));
+  else
+    CK(cudaLaunchKernelEx(&lc, k_chol_solve<16>, ctx->ctl, ctx->d, hpk, shift_ptr, rhs, x, ctx->M,
+                          z, x_out, mode, ignore_halt, dbg));
   return FB_OK;
 }
-int launch_fold(Ctx* ctx, cudaStream_t s, const int32_t* clients, int n_active, double* hest,
-                double* hmas) {
-  const int dense = (ctx->cfg.kind == FB_KIND_IDENTITY || ctx->cfg.kind == FB_KIND_NATURAL);
-  k_fold<<<static_cast<unsigned>((ctx->w + 255) / 256), 256, 0, s>>>(
-      ctx->ctl, ctx->w, ctx->wb, n_active, clients, dense, ctx->rand_scale, ctx->cfg.alpha,
-      ctx->alpha_n, ctx->D, ctx->bitmap, ctx->count, hest, hmas);
+bool dense_kind(const Ctx* ctx) {
+  return ctx->cfg.kind == FB_KIND_IDENTITY || ctx->cfg.kind == FB_KIND_NATURAL;
+}
+// master fold Hout = Hin + (alpha/n) sum_c delta_c (ascending c); for the
+// dense kinds the client shift update rides along when `hest` is non-null
+int launch_master_fold(Ctx* ctx, cudaStream_t s, const int32_t* clients, int n_active,
+                       double* hest, const double* h_in, double* h_out) {
+  if (dense_kind(ctx)) {
+    k_fold_dense<<<static_cast<unsigned>((ctx->w + 255) / 256), 256, 0, s>>>(
+        ctx->ctl, ctx->w, n_active, clients, ctx->cfg.alpha, ctx->alpha_n, ctx->D, ctx->count,
+        hest, h_in, h_out);
+  } else {
+    const size_t smem = sizeof(int32_t) * (3 * static_cast<size_t>(n_active) + 1);
+    k_master_fold<<<ctx->nr, FOLD_THREADS, smem, s>>>(
+        ctx->ctl, ctx->w, n_active, clients, ctx->cap, ctx->nr, ctx->rs, ctx->idx_list,
+        ctx->val_list, ctx->alpha_n, h_in, h_out);
+  }
   CKL();
   return FB_OK;
 }
@@ -307,9 +341,15 @@ int enqueue_fednl_round(Ctx* ctx) {
   // fork: compressor on st2 while the master solves on st
   CK(cudaEventRecord(ctx->ev_fork, s));
   CK(cudaStreamWaitEvent(ctx->st2, ctx->ev_fork, 0));
+  // compressor (+ client shift update) then the master fold H^k -> H^{k+1}
+  // into the second buffer, overlapping the solve that reads H^k
   TRY(record(ctx, EV_COMP_START, ctx->st2));
   TRY(launch_compress(ctx, ctx->st2, nullptr, n, nullptr, nullptr));
   TRY(record(ctx, EV_COMP_END, ctx->st2));
+  TRY(record(ctx, EV_FOLD_START, ctx->st2));
+  TRY(launch_master_fold(ctx, ctx->st2, nullptr, n, dense_kind(ctx) ? ctx->hest : nullptr,
+                         ctx->hmas, ctx->hmas2));
+  TRY(record(ctx, EV_FOLD_END, ctx->st2));
   CK(cudaEventRecord(ctx->ev_join, ctx->st2));
   TRY(launch_solve(ctx, s, ctx->hmas, &ctx->sc->shift_mean, ctx->gbar, ctx->x, ctx->pvec,
                    ctx->x_new, ls ? 2 : 0, 0));
@@ -330,9 +370,7 @@ int enqueue_fednl_round(Ctx* ctx) {
     launches += 3;
   }
   CK(cudaStreamWaitEvent(s, ctx->ev_join, 0));
-  TRY(record(ctx, EV_FOLD_START, s));
-  TRY(launch_fold(ctx, s, nullptr, n, ctx->hest, ctx->hmas));
-  TRY(record(ctx, EV_FOLD_END, s));
+  CK(cudaMemcpyAsync(ctx->hmas, ctx->hmas2, sizeof(double) * ctx->w, cudaMemcpyDeviceToDevice, s));
   k_finish<<<1, 256, 0, s>>>(ctx->ctl, ctx->d, n, n, nullptr, ctx->x, ctx->x_new, 1, ctx->count,
                              ctx->row_counts, ctx->row_ls);
   CKL();
@@ -344,8 +382,10 @@ int enqueue_fednl_round(Ctx* ctx) {
 // post-line-search tail of an LS round (fold + finish), launched directly by
 // the host after it drove extra trial batches
 int enqueue_ls_tail(Ctx* ctx) {
+  // the fold of this round already ran (it does not depend on the line
+  // search); only the H^{k+1} copy and the round epilogue remain
   cudaStream_t s = ctx->st;
-  TRY(launch_fold(ctx, s, nullptr, ctx->n, ctx->hest, ctx->hmas));
+  CK(cudaMemcpyAsync(ctx->hmas, ctx->hmas2, sizeof(double) * ctx->w, cudaMemcpyDeviceToDevice, s));
   k_finish<<<1, 256, 0, s>>>(ctx->ctl, ctx->d, ctx->n, ctx->n, nullptr, ctx->x, ctx->x_new, 1,
                              ctx->count, ctx->row_counts, ctx->row_ls);
   CKL();
@@ -392,7 +432,8 @@ int enqueue_pp_round(Ctx* ctx) {
   TRY(launch_compress(ctx, s, ctx->subset, tau, nullptr, nullptr));
   TRY(record(ctx, EV_COMP_END, s));
   TRY(record(ctx, EV_FOLD_START, s));
-  TRY(launch_fold(ctx, s, ctx->subset, tau, ctx->hest, nullptr));
+  if (dense_kind(ctx))  // the sparse compressors already applied the client update
+    TRY(launch_master_fold(ctx, s, ctx->subset, tau, ctx->hest, nullptr, nullptr));
   k_pp_client<<<tau, 256, 0, s>>>(ctx->ctl, ctx->d, ctx->subset, ctx->hest, ctx->hess_part, ctx->x,
                                   ctx->grad, ctx->cli_shift, ctx->cli_gvec, ctx->dshift,
                                   ctx->dgvec);
@@ -400,7 +441,7 @@ int enqueue_pp_round(Ctx* ctx) {
   k_pp_master<<<1, 256, 0, s>>>(ctx->ctl, ctx->d, n, tau, ctx->dshift, ctx->dgvec, ctx->gvec,
                                 ctx->pp_shift);
   CKL();
-  TRY(launch_fold(ctx, s, ctx->subset, tau, nullptr, ctx->hmas));
+  TRY(launch_master_fold(ctx, s, ctx->subset, tau, nullptr, ctx->hmas, ctx->hmas));
   TRY(record(ctx, EV_FOLD_END, s));
   k_finish<<<1, 256, 0, s>>>(ctx->ctl, ctx->d, n, tau, ctx->subset, ctx->x, nullptr, 0, ctx->count,
                              ctx->row_counts, ctx->row_ls);
@@ -534,6 +575,7 @@ int fb_create(const fb_config* cfg_in, void** out) {
   ctx->n_pairs = ctx->nb_tiles * (ctx->nb_tiles + 1) / 2;
   ctx->wb = static_cast<int>((w + 31) / 32);
   ctx->cap = sparse ? c.k : 1;
+  ctx->nr = static_cast<int>((w + FOLD_RANGE - 1) / FOLD_RANGE);
   ctx->tau = c.algorithm == FB_ALG_PP ? c.tau : c.n_clients;
   ctx->alpha_n = c.alpha / static_cast<double>(c.n_clients);
   ctx->rand_scale = (c.kind == FB_KIND_RANDK || c.kind == FB_KIND_RANDSEQK)
@@ -542,12 +584,12 @@ int fb_create(const fb_config* cfg_in, void** out) {
   ctx->toplek_P = 1;
   if (c.kind == FB_KIND_TOPLEK)
     while (ctx->toplek_P < w) ctx->toplek_P <<= 1;
-  // master solve: a cluster of up to 8 CTAs; panel staged in smem when it fits
-  ctx->solve_cs = c.d >= 96 ? CH_MAX_CLUSTER : 1;
-  const size_t pan = static_cast<size_t>(c.d) * CH_PLD * sizeof(double);
-  ctx->solve_stage = pan <= 190 * 1024 ? 1 : 0;
-  ctx->solve_smem = ctx->solve_stage ? pan : 0;
-
+  // master solve: one cluster (8 CTAs from d >= 128); 32-wide panels while the
+  // (d + 1) x 33 panel fits in shared memory, else 16-wide
+  ctx->solve_cs = c.d >= 128 ? CH_MAX_CLUSTER : 1;
+  if (const char* e = getenv("FB_SOLVE_CLUSTER")) ctx->solve_cs = std::max(1, std::min(8, atoi(e)));
+  ctx->solve_nb = solve_panel_bytes<32>(c.d) <= 190 * 1024 ? 32 : 16;
+  ctx->solve_smem = ctx->solve_nb == 32 ? solve_panel_bytes<32>(c.d) : solve_panel_bytes<16>(c.d);
   int rc = FB_OK;
   auto fail = [&](int code) {
     rc = code;
@@ -587,13 +629,16 @@ int fb_create(const fb_config* cfg_in, void** out) {
   max_solve = std::max(max_solve, std::max<size_t>(ctx->solve_smem, 1));
   CKC(cudaFuncSetAttribute(k_hessian, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            static_cast<int>(HESS_SMEM)));
+  CKC(cudaFuncSetAttribute(k_topk_smem, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           static_cast<int>(TKS_SMEM)));
   CKC(cudaFuncSetAttribute(k_randk, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            static_cast<int>(2 * RK_TABLE * sizeof(int32_t))));
   CKC(cudaFuncSetAttribute(k_toplek, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            static_cast<int>(max_toplek)));
-  CKC(cudaFuncSetAttribute(k_chol_solve, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           static_cast<int>(max_solve)));
-  CKC(cudaFuncSetAttribute(k_chol_solve, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+  CKC(cudaFuncSetAttribute(k_chol_solve<32>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           static_cast<int>(std::max(max_solve, solve_panel_bytes<32>(1)))));
+  CKC(cudaFuncSetAttribute(k_chol_solve<16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           static_cast<int>(std::max(max_solve, solve_panel_bytes<16>(1)))));
 
   const int n = ctx->n, d = ctx->d;
   const size_t wn = static_cast<size_t>(w) * n;
@@ -608,8 +653,9 @@ int fb_create(const fb_config* cfg_in, void** out) {
       dalloc(ctx, &ctx->f_cli, n) || dalloc(ctx, &ctx->shift_cli, n) ||
       dalloc(ctx, &ctx->frob_part, static_cast<size_t>(n) * ctx->n_pairs) ||
       dalloc(ctx, &ctx->flags, n) || dalloc(ctx, &ctx->hest, wn) || dalloc(ctx, &ctx->D, wn) ||
-      dalloc(ctx, &ctx->hmas, w) || dalloc(ctx, &ctx->zeros_w, w) ||
-      dalloc(ctx, &ctx->M, static_cast<size_t>(d) * d) ||
+      dalloc(ctx, &ctx->hmas, w) || dalloc(ctx, &ctx->hmas2, w) || dalloc(ctx, &ctx->zeros_w, w) ||
+      dalloc(ctx, &ctx->rs, static_cast<size_t>(n) * (ctx->nr + 1)) ||
+      dalloc(ctx, &ctx->M, static_cast<size_t>(d + 1) * (d + 1)) ||
       dalloc(ctx, &ctx->bitmap, static_cast<size_t>(n) * ctx->wb) || dalloc(ctx, &ctx->count, n) ||
       dalloc(ctx, &ctx->draws, n) ||
       dalloc(ctx, &ctx->idx_list, static_cast<size_t>(n) * ctx->cap) ||
@@ -1064,7 +1110,7 @@ int fb_compress(void* handle, const double* diffs, const uint64_t* seeds, uint32
       return FB_ERR_NONFINITE;
     }
   }
-  TRY(launch_compress(ctx, s, nullptr, n, ctx->seeds, nullptr, false));
+  TRY(launch_compress(ctx, s, nullptr, n, ctx->seeds, nullptr, false, false));
   std::vector<int32_t> cnt(n);
   CK(cudaMemcpyAsync(cnt.data(), ctx->count, sizeof(int32_t) * n, cudaMemcpyDeviceToHost, s));
   if (draws) CK(cudaMemcpyAsync(draws, ctx->draws, sizeof(int32_t) * n, cudaMemcpyDeviceToHost, s));
@@ -1119,6 +1165,40 @@ int fb_oracle_eval(void* handle, const double* x, double* f, double* grad, doubl
   if (hess_packed)
     CK(cudaMemcpyAsync(hess_packed, ctx->D, sizeof(double) * n * ctx->w, cudaMemcpyDeviceToHost, s));
   CK(cudaStreamSynchronize(s));
+  return FB_OK;
+}
+
+// Diagnostic: per-phase clock64 cycles of one shifted solve (rank 0, thread 0):
+// [setup, A, syncA, pull, B, B-writeback, C, syncC, back-solve, back-total, -, -];
+// cluster size override (0 = default).
+int fb_solve_phase_cycles(void* handle, const double* h_packed, double shift, const double* rhs,
+                          int32_t cluster, long long* cycles, float* ms) {
+  Ctx* ctx = static_cast<Ctx*>(handle);
+  if (!ctx || !h_packed || !rhs || !cycles) return invalid(ctx, "null argument");
+  cudaStream_t s = ctx->st;
+  const int saved = ctx->solve_cs;
+  if (cluster > 0) ctx->solve_cs = cluster;
+  long long* dbg = nullptr;
+  CK(cudaMalloc(&dbg, 12 * sizeof(long long)));
+  CK(cudaMemset(dbg, 0, 12 * sizeof(long long)));
+  CK(cudaMemcpyAsync(ctx->D, h_packed, sizeof(double) * ctx->w, cudaMemcpyHostToDevice, s));
+  CK(cudaMemcpyAsync(ctx->scalar, &shift, sizeof(double), cudaMemcpyHostToDevice, s));
+  CK(cudaMemcpyAsync(ctx->zbuf, rhs, sizeof(double) * ctx->d, cudaMemcpyHostToDevice, s));
+  TRY(launch_solve(ctx, s, ctx->D, ctx->scalar, ctx->zbuf, nullptr, ctx->pvec, nullptr, 2, 1));
+  CK(cudaStreamSynchronize(s));
+  cudaEvent_t e0, e1;
+  CK(cudaEventCreate(&e0));
+  CK(cudaEventCreate(&e1));
+  CK(cudaEventRecord(e0, s));
+  TRY(launch_solve(ctx, s, ctx->D, ctx->scalar, ctx->zbuf, nullptr, ctx->pvec, nullptr, 2, 1, dbg));
+  CK(cudaEventRecord(e1, s));
+  CK(cudaStreamSynchronize(s));
+  if (ms) CK(cudaEventElapsedTime(ms, e0, e1));
+  CK(cudaMemcpy(cycles, dbg, 12 * sizeof(long long), cudaMemcpyDeviceToHost));
+  cudaFree(dbg);
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  ctx->solve_cs = saved;
   return FB_OK;
 }
 

@@ -113,7 +113,9 @@ __global__ void __launch_bounds__(HTHREADS) k_hessian(
     if (active) {
 #pragma unroll
       for (int kk = 0; kk < HKC / 4; ++kk) {
-        const int ks = 4 * kk + t;
+        // k-step kk reads samples {2kk, 2kk+1, 2kk+8, 2kk+9}: with the 128B
+        // swizzle every half-warp then touches 16 distinct bank pairs
+        const int ks = 2 * kk + (t & 1) + 8 * (t >> 1);
         const double hv = sm.h[s][ks];
         double af[4], bf[4];
 #pragma unroll

@@ -4,6 +4,7 @@
 // with sequential adds, so results do not depend on launch shape.
 #pragma once
 #include "common.cuh"
+#include "compress_kernels.cuh"
 
 namespace fb {
 
@@ -50,10 +51,16 @@ __global__ void __launch_bounds__(1024) k_reduce(
     }
   }
   for (int a = threadIdx.x; a < d; a += blockDim.x) {
+    // ascending-cid sequential sum; loads batched 8 deep for memory parallelism
     double s = 0.0;
-    for (int i = 0; i < n_active; ++i) {
-      const int c = client_of(clients, i);
-      s = __dadd_rn(s, grad[static_cast<int64_t>(c) * d + a]);
+    for (int i0 = 0; i0 < n_active; i0 += 8) {
+      double v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u)
+        v[u] = (i0 + u < n_active) ? grad[static_cast<int64_t>(client_of(clients, i0 + u)) * d + a] : 0.0;
+#pragma unroll
+      for (int u = 0; u < 8; ++u)
+        if (i0 + u < n_active) s = __dadd_rn(s, v[u]);
     }
     gbar[a] = __ddiv_rn(s, static_cast<double>(n_div));
   }
@@ -82,36 +89,128 @@ __global__ void __launch_bounds__(1024) k_reduce(
   }
 }
 
-// Fused client shift update + master fold (compressors.py:373-393,
-// algorithms.py:234, 369-372).  One thread per packed position t; clients in
-// ascending id:  Hest[c][t] = fl(Hest + fl(alpha v)),
-//                Hmas[t]    = fl(Hmas + fl((alpha / n) v)).
-// v = D[c][t] (TopK/TopLEK/identity/natural-rounded) or fl(D * w/k) (Rand).
-// An unselected entry contributes nothing (the reference's sparse fold).
-__global__ void __launch_bounds__(256) k_fold(
-    const DevCtl* __restrict__ ctl, int64_t w, int wb, int n_active,
-    const int32_t* __restrict__ clients, int dense, double scale, double alpha, double alpha_n,
-    const double* __restrict__ D, const uint32_t* __restrict__ bitmap,
-    const int32_t* __restrict__ count, double* __restrict__ hest, double* __restrict__ hmas) {
+// Dense kinds (identity / natural): client shift update + master fold per
+// packed position t, clients in ascending id (compressors.py:373-393,
+// algorithms.py:234, 369-372):
+//   Hest[c][t] = fl(Hest + fl(alpha v)),  Hout[t] = fold_c fl(. + fl((alpha/n) v))
+// with v = D[c][t] (identity) or its natural rounding (written into D).
+__global__ void __launch_bounds__(256) k_fold_dense(
+    const DevCtl* __restrict__ ctl, int64_t w, int n_active, const int32_t* __restrict__ clients,
+    double alpha, double alpha_n, const double* __restrict__ D, const int32_t* __restrict__ count,
+    double* __restrict__ hest, const double* h_in, double* h_out) {
   if (ctl->halt) return;
   const int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (t >= w) return;
-  const int64_t q = t >> 5;
-  const uint32_t bit = 1u << (t & 31);
-  double h = hmas ? hmas[t] : 0.0;
-  for (int i = 0; i < n_active; ++i) {
-    const int c = client_of(clients, i);
-    if (count[c] == 0) continue;
-    if (!dense && !(bitmap[static_cast<int64_t>(c) * wb + q] & bit)) continue;
-    double v = D[static_cast<int64_t>(c) * w + t];
-    if (scale != 1.0) v = __dmul_rn(v, scale);
-    if (hest) {
-      double* hp = hest + static_cast<int64_t>(c) * w + t;
-      *hp = __dadd_rn(*hp, __dmul_rn(alpha, v));
+  double h = h_out ? h_in[t] : 0.0;
+  constexpr int G = 8;  // clients per batch: independent loads in flight
+  for (int i0 = 0; i0 < n_active; i0 += G) {
+    int cc[G];
+    double v[G], hv[G];
+#pragma unroll
+    for (int u = 0; u < G; ++u) {
+      cc[u] = (i0 + u < n_active) ? client_of(clients, i0 + u) : -1;
+      const bool sel = cc[u] >= 0 && count[cc[u]] != 0;
+      v[u] = sel ? D[static_cast<int64_t>(cc[u]) * w + t] : 0.0;
+      hv[u] = (sel && hest) ? hest[static_cast<int64_t>(cc[u]) * w + t] : 0.0;
+      if (!sel) cc[u] = -1;
     }
-    if (hmas) h = __dadd_rn(h, __dmul_rn(alpha_n, v));
+#pragma unroll
+    for (int u = 0; u < G; ++u) {
+      if (cc[u] < 0) continue;
+      if (hest) hest[static_cast<int64_t>(cc[u]) * w + t] = __dadd_rn(hv[u], __dmul_rn(alpha, v[u]));
+      if (h_out) h = __dadd_rn(h, __dmul_rn(alpha_n, v[u]));
+    }
   }
-  if (hmas) hmas[t] = h;
+  if (h_out) h_out[t] = h;
+}
+
+// Master fold of the sparse kinds (algorithms.py:369-372): one CTA per range
+// of FOLD_RANGE packed positions.  Every client's ascending (idx, val) list is
+// sliced by the compressor's range starts rs[c][r]; the slices are staged in
+// shared memory (coalesced, all clients at once), then applied in ascending
+// client order:  Hout[t] = fl(Hin[t] + fl((alpha/n) v_c))  — the reference's
+// sequential sparse fold, bit for bit.  Hin may alias Hout.
+constexpr int FOLD_THREADS = 256;
+constexpr int FOLD_STAGE = 4096;  // staged entries per pass
+__global__ void __launch_bounds__(FOLD_THREADS) k_master_fold(
+    const DevCtl* __restrict__ ctl, int64_t w, int n_active, const int32_t* __restrict__ clients,
+    int cap, int nr, const int32_t* __restrict__ rs, const uint32_t* __restrict__ idx_list,
+    const double* __restrict__ val_list, double alpha_n, const double* h_in, double* h_out) {
+  if (ctl->halt) return;
+  extern __shared__ int32_t fold_sm[];  // beg[n], cnt[n], off[n+1]
+  __shared__ double hs[FOLD_RANGE];
+  __shared__ uint16_t st_t[FOLD_STAGE];
+  __shared__ double st_v[FOLD_STAGE];
+  __shared__ int ws[64];
+  int32_t* beg = fold_sm;
+  int32_t* cnt = fold_sm + n_active;
+  int32_t* off = fold_sm + 2 * n_active;
+  const int r = blockIdx.x;
+  const int64_t t0 = static_cast<int64_t>(r) * FOLD_RANGE;
+  const int len = static_cast<int>((w - t0 < FOLD_RANGE) ? (w - t0) : FOLD_RANGE);
+  for (int i = threadIdx.x; i < len; i += FOLD_THREADS) hs[i] = h_in[t0 + i];
+  for (int i = threadIdx.x; i < n_active; i += FOLD_THREADS) {
+    const int c = client_of(clients, i);
+    const int32_t* rc = rs + static_cast<int64_t>(c) * (nr + 1);
+    const int b = rc[r];
+    beg[i] = b;
+    cnt[i] = rc[r + 1] - b;
+  }
+  __syncthreads();
+  // exclusive scan of cnt in client order (chunks of FOLD_THREADS)
+  {
+    int carry = 0;
+    for (int base = 0; base < n_active; base += FOLD_THREADS) {
+      const int i = base + threadIdx.x;
+      const int v = (i < n_active) ? cnt[i] : 0;
+      int total;
+      const int o = block_excl_scan(v, ws, &total) + carry;
+      if (i < n_active) off[i] = o;
+      carry += total;
+    }
+    if (threadIdx.x == 0) off[n_active] = carry;
+  }
+  __syncthreads();
+  // passes over [first client, last client) whose entries fit the stage
+  int ca = 0;
+  while (ca < n_active) {
+    // largest cb with off[cb] - off[ca] <= FOLD_STAGE (at least one client)
+    int lo = ca + 1, hi = n_active;
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (off[mid] - off[ca] <= FOLD_STAGE) lo = mid; else hi = mid - 1;
+    }
+    const int cb = lo;
+    const int e0 = off[ca], e1 = off[cb];  // a client's slice is <= FOLD_RANGE < FOLD_STAGE
+    // stage entries [e0, e1): entry e belongs to the client i with off[i] <= e < off[i+1]
+    for (int e = e0 + threadIdx.x; e < e1; e += FOLD_THREADS) {
+      int a = ca, b = cb - 1;
+      while (a < b) {
+        const int mid = (a + b + 1) >> 1;
+        if (off[mid] <= e) a = mid; else b = mid - 1;
+      }
+      const int c = client_of(clients, a);
+      const int64_t src = static_cast<int64_t>(c) * cap + beg[a] + (e - off[a]);
+      st_t[e - e0] = static_cast<uint16_t>(idx_list[src] - t0);
+      st_v[e - e0] = val_list[src];
+    }
+    __syncthreads();
+    if (threadIdx.x < 32) {  // apply in ascending client order (distinct t within a client)
+      const int lane = threadIdx.x;
+      for (int i = ca; i < cb; ++i) {
+        const int n_i = off[i + 1] - off[i];
+        for (int e = lane; e < n_i; e += 32) {
+          const int q = off[i] - e0 + e;
+          const int tt = st_t[q];
+          hs[tt] = __dadd_rn(hs[tt], __dmul_rn(alpha_n, st_v[q]));
+        }
+        __syncwarp();
+      }
+    }
+    __syncthreads();
+    ca = cb;
+  }
+  for (int i = threadIdx.x; i < len; i += FOLD_THREADS) h_out[t0 + i] = hs[i];
 }
 
 // Round epilogue (algorithms.py:385-387): x <- x_new, round += 1,

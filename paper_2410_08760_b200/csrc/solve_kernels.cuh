@@ -1,13 +1,25 @@
 // solve_kernels.cuh — master Newton step: (H + shift I) z = rhs by a blocked
-// right-looking fp64 Cholesky on one thread-block cluster, then the two
-// triangular solves (reference algorithms.py:361-367 option b,
-// linalg.py:133-186).
+// right-looking fp64 Cholesky on one thread-block cluster (reference
+// algorithms.py:361-367 option b, linalg.py:133-186).
 //
-// Workspace M (d x d, column-major, lda = d) holds the matrix in its UPPER
-// triangle: M[j][i] = A[j][i] for j <= i, i.e. packed column i lands in
-// column i of M (a coalesced copy).  After factorisation M[j][i] = L[i][j]:
-// row i of L is column i of M, contiguous — the panel solve and the
-// trailing update both read 32 contiguous doubles per row.
+// Workspace M ((d+1) x (d+1) slots, column-major, lda = d + 1) holds the
+// matrix in its UPPER triangle, M[j][i] = A[j][i] for j <= i < d, i.e.
+// packed column i lands in column i of M (a coalesced copy), and the
+// right-hand side as an extra column M[j][d] = rhs[j].  Factorising the
+// augmented matrix leaves M[j][i] = L[i][j] and M[j][d] = y[j] with L y = rhs:
+// the forward substitution rides along with the panel solves and trailing
+// updates.  Row i of L is column i of M (contiguous).
+//
+// Per panel of NB columns there are two cluster barriers:
+//   (A) rank 0 / warp 0 factors the NB x NB diagonal block (already in its
+//       shared memory) and pushes L_pp and 1/diag into every CTA's shared
+//       memory over DSMEM;
+//   (BC) every CTA solves ALL panel rows against L_pp into its own shared
+//       panel (redundant, cheap), writes the rows it owns back to M, and
+//       applies its share of the trailing update; updates that land in the
+//       next diagonal block are also pushed into rank 0's shared memory.
+// The backward substitution L^T z = y runs on rank 0 with the next block's
+// loads issued before the current block's sequential solve.
 //
 // The first pivot that is <= 0 or not finite stops the factorisation with
 // NotPositiveDefiniteError(pivot_index, pivot_value) semantics
@@ -19,222 +31,294 @@
 namespace fb {
 namespace cg = cooperative_groups;
 
-constexpr int CH_NB = 32;
-constexpr int CH_THREADS = 512;
-constexpr int CH_PLD = CH_NB + 1;  // smem panel pitch (conflict-free rows)
+constexpr int CH_THREADS = 256;
 constexpr int CH_MAX_CLUSTER = 8;
+constexpr int CH_MAX_D = 1024;
 
+template <int NB>
 struct SolveSmem {
-  double lpp[CH_NB][CH_PLD];
-  double vec[1024 + 32];
+  double blk[NB][NB + 1];  // L_pp of the current panel (row r, col s)
+  double nxt[2][NB][NB + 1];  // next diagonal block (panel parity), pushed over DSMEM
+  double inv[NB];          // 1 / L[jj][jj]
+  double col[NB];          // column broadcast during the block factorisation
+  double vec[CH_MAX_D + 64];
+  double dinv[CH_MAX_D];   // 1 / L[i][i] for the backward substitution
   int failed;
-  int halt;
 };
+
+// panel rows p1..d during the factorisation; the inverted diagonal blocks
+// (transposed, ceil(d / NB) x NB rows) during the backward substitution
+template <int NB>
+constexpr size_t solve_panel_bytes(int d) {
+  return static_cast<size_t>((d + NB) / NB * NB + 1) * (NB + 1) * sizeof(double);
+}
 
 // mode 0: x_out = fl(x - z)   (FedNL / LS direction, algorithms.py:385)
 // mode 1: x_out = z           (FedNL-PP new point, algorithms.py:431)
-// mode 2: x_out untouched     (leaf solve: z only)
-// dynamic smem: panel staging (d * CH_PLD doubles) when `stage_panel`.
+// mode 2: x_out untouched     (leaf solve / LS: z only)
+// dynamic smem: the panel, (d + 1) x (NB + 1) doubles.
+template <int NB>
 __global__ void __launch_bounds__(CH_THREADS, 1) k_chol_solve(
     DevCtl* __restrict__ ctl, int d, const double* __restrict__ hpk,
     const double* __restrict__ shift_ptr, const double* __restrict__ rhs,
     const double* __restrict__ x, double* __restrict__ M, double* __restrict__ z,
-    double* __restrict__ x_out, int mode, int stage_panel, int ignore_halt) {
+    double* __restrict__ x_out, int mode, int ignore_halt, long long* __restrict__ dbg) {
   cg::cluster_group cluster = cg::this_cluster();
-  __shared__ SolveSmem sm;
-  extern __shared__ double pan[];  // [(d) x CH_PLD] when stage_panel
+  __shared__ SolveSmem<NB> sm;
+  extern __shared__ double pan[];  // [(d + 1) x (NB + 1)]: panel rows p1..d
+  constexpr int PLD = NB + 1;
   const int rank = static_cast<int>(cluster.block_rank());
   const int cs = static_cast<int>(cluster.num_blocks());
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int gwarp = rank * (CH_THREADS / 32) + warp;
-  const int nwarps = cs * (CH_THREADS / 32);
-  const int gtid = rank * CH_THREADS + tid;
-  const int gthreads = cs * CH_THREADS;
+  constexpr int NW = CH_THREADS / 32;
+  const int gwarp = rank * NW + warp;
+  const int nwarps = cs * NW;
+  const int64_t ld = d + 1;
+  const int rows = d + 1;  // row d of the augmented matrix carries the rhs
+  long long t_mark = clock64();
+  auto mark = [&](int slot) {  // optional phase timing on rank 0 / thread 0
+    if (dbg && tid == 0 && rank == 0) {
+      const long long now = clock64();
+      dbg[slot] += now - t_mark;
+      t_mark = now;
+    }
+  };
 
-  // one consistent halt decision for the whole cluster: rank 0 reads the
-  // control block and pushes the verdict into every CTA's shared memory
-  if (tid == 0) { sm.failed = 0; sm.halt = 0; }
-  cluster.sync();
-  if (rank == 0 && tid == 0) {
-    const int h = ignore_halt ? 0 : ctl->halt;
-    for (int r = 0; r < cs; ++r) *cluster.map_shared_rank(&sm.halt, r) = h;
-  }
-  cluster.sync();
-  if (sm.halt) return;
+  // No early exit on ctl->halt (a cluster-wide decision would cost two
+  // barriers): a halted round computes on stale data and rank 0 drops the
+  // outputs at the end.  sm.failed is ordered before any DSMEM push by the
+  // first cluster barrier below.
+  if (tid == 0) sm.failed = 0;
   const double shift = shift_ptr ? *shift_ptr : 0.0;
 
-  // ---- M[j][i] = H[j][i] (+ shift on the diagonal), columns across warps
-  for (int i = gwarp; i < d; i += nwarps) {
-    const int64_t pc = packed_at(0, i);
-    for (int j = lane; j <= i; j += 32) {
-      double v = hpk[pc + j];
-      if (j == i) v = __dadd_rn(v, shift);
-      M[j + static_cast<int64_t>(i) * d] = v;
+  // ---- M[j][i] = H[j][i] (+ shift on the diagonal); M[j][d] = rhs[j]
+  for (int i = gwarp; i <= d; i += nwarps) {
+    if (i < d) {
+      const int64_t pc = packed_at(0, i);
+      for (int j = lane; j <= i; j += 32) {
+        double v = hpk[pc + j];
+        if (j == i) v = __dadd_rn(v, shift);
+        M[j + i * ld] = v;
+      }
+    } else {
+      for (int j = lane; j < d; j += 32) M[j + i * ld] = rhs[j];
+    }
+  }
+  // every CTA stages the first diagonal block straight from H
+  {
+    const int pb = min(NB, d);
+    for (int e = tid; e < NB * NB; e += CH_THREADS) {
+      const int r = e / NB, s = e % NB;
+      double v = 0.0;
+      if (r < pb && s <= r) {
+        v = hpk[packed_at(s, r)];
+        if (s == r) v = __dadd_rn(v, shift);
+      }
+      sm.nxt[0][r][s] = v;
     }
   }
   cluster.sync();
+  mark(0);
 
-  for (int p0 = 0; p0 < d; p0 += CH_NB) {
-    const int pb = min(CH_NB, d - p0);
+  for (int p0 = 0; p0 < d; p0 += NB) {
+    const int pb = min(NB, d - p0);
     const int p1 = p0 + pb;
-    // ---- (A) diagonal block, rank 0 / warp 0: lane r owns row p0 + r
-    if (rank == 0 && warp == 0) {
-      double row[CH_NB];
+    // ---- (A) diagonal block, factored redundantly by warp 0 of EVERY CTA
+    //      (identical inputs and instruction streams give identical bits), so
+    //      no barrier or exchange is needed before the panel solve.  Lane r owns
+    //      row r; SB-wide sub-blocks keep the per-pivot update loop short.
+    const int par = (p0 / NB) & 1;
+    if (warp == 0) {
+      constexpr int SB = 8;
+      double row[NB];
 #pragma unroll
-      for (int s = 0; s < CH_NB; ++s)
-        row[s] = (lane < pb && s <= lane) ? M[(p0 + s) + static_cast<int64_t>(p0 + lane) * d] : 0.0;
-      int fail = -1;
+      for (int s2 = 0; s2 < NB; ++s2) row[s2] = sm.nxt[par][lane & (NB - 1)][s2];
+      // every pivot is processed (no data-dependent exit, so row[] stays in
+      // registers); the first failing pivot is remembered
+      int fail = NB;
       double fail_val = 0.0;
 #pragma unroll
-      for (int jj = 0; jj < CH_NB; ++jj) {
-        if (jj < pb && fail < 0) {
-          const double piv = __shfl_sync(0xffffffffu, row[jj], jj);
-          if (!(piv > 0.0) || !isfinite(piv)) {
-            fail = jj;
-            fail_val = piv;
-          } else {
-            const double r = sqrt(piv);
-            if (lane == jj) row[jj] = r;
-            if (lane > jj) row[jj] = row[jj] / r;
-            const double lj = row[jj];
-            // rank-1 update of the remaining columns of this row
+      for (int jj = 0; jj < NB; ++jj) {  // constant trip counts: row[] stays in registers
+        const int qend = (jj / SB + 1) * SB;  // end of jj's sub-block
+        const double piv = __shfl_sync(0xffffffffu, row[jj], jj);
+        const bool ok = piv > 0.0 && isfinite(piv);
+        if (!ok && jj < pb && fail == NB) { fail = jj; fail_val = piv; }
+        const double ir = rsqrt(ok ? piv : 1.0);
+        if (lane == jj) sm.inv[jj] = ir;
+        row[jj] = (lane == jj) ? piv * ir : ((lane > jj) ? row[jj] * ir : row[jj]);
 #pragma unroll
-            for (int kk = jj + 1; kk < CH_NB; ++kk) {
-              const double lk = __shfl_sync(0xffffffffu, lj, kk);  // L[kk][jj]
-              if (lane >= kk && kk < pb) row[kk] = fma(-lj, lk, row[kk]);
-            }
+        for (int kk = jj + 1; kk < qend; ++kk) {
+          const double lk = __shfl_sync(0xffffffffu, row[jj], kk);  // L[kk][jj]
+          row[kk] = (lane >= kk) ? fma(-row[jj], lk, row[kk]) : row[kk];
+        }
+        if (jj == qend - 1 && qend < NB) {
+          // columns [qend-SB, qend) of L update columns [qend, NB) of rows >= qend
+#pragma unroll
+          for (int s2 = qend - SB; s2 < qend; ++s2) sm.blk[lane & (NB - 1)][s2] = row[s2];
+          __syncwarp();
+#pragma unroll
+          for (int kk = qend; kk < NB; ++kk) {
+            double acc = 0.0;
+#pragma unroll
+            for (int s2 = qend - SB; s2 < qend; ++s2) acc = fma(row[s2], sm.blk[kk][s2], acc);
+            row[kk] = (lane >= kk) ? row[kk] - acc : row[kk];
+          }
+          __syncwarp();
+        }
+      }
+      if (fail < NB) {
+        if (lane == 0) {
+          sm.failed = 1;
+          if (rank == 0) {
+            ctl->pivot_index = p0 + fail;
+            ctl->pivot_value = fail_val;
+            raise_status(ctl, ST_NOT_PD);
           }
         }
-      }
-      if (fail >= 0) {
-        if (lane == 0) {
-          for (int r = 0; r < cs; ++r) *cluster.map_shared_rank(&sm.failed, r) = 1;
-          ctl->pivot_index = p0 + fail;
-          ctl->pivot_value = fail_val;
-          raise_status(ctl, ST_NOT_PD);
-        }
-      } else if (lane < pb) {
+      } else {
 #pragma unroll
-        for (int s = 0; s < CH_NB; ++s)
-          if (s <= lane) M[(p0 + s) + static_cast<int64_t>(p0 + lane) * d] = row[s];
+        for (int s2 = 0; s2 < NB; ++s2) sm.blk[lane & (NB - 1)][s2] = (s2 <= lane) ? row[s2] : 0.0;
+        if (rank == 0 && lane < pb) {
+#pragma unroll
+          for (int s2 = 0; s2 < NB; ++s2)
+            if (s2 <= lane) M[(p0 + s2) + (p0 + lane) * ld] = row[s2];
+          sm.dinv[p0 + lane] = sm.inv[lane];
+        }
       }
     }
-    cluster.sync();
-    if (sm.failed) return;
-    if (p1 >= d) break;
-    // ---- (B) panel rows i >= p1:  L[i][p0:p1] = A[i][p0:p1] L_pp^{-T}
-    for (int e = tid; e < CH_NB * CH_NB; e += CH_THREADS) {
-      const int r = e / CH_NB, s = e % CH_NB;
-      sm.lpp[r][s] = (r < pb && s <= r) ? M[(p0 + s) + static_cast<int64_t>(p0 + r) * d] : 0.0;
-    }
+    mark(1);
     __syncthreads();
-    for (int i = p1 + gtid; i < d; i += gthreads) {
-      double* col = M + p0 + static_cast<int64_t>(i) * d;
-      double v[CH_NB];
+    if (sm.failed) return;  // uniform across the cluster (identical factorisations)
+    mark(3);
+    // ---- (B) every CTA: all panel rows i in [p1, d] (incl. the rhs row) into
+    //          its own shared panel (redundant, saves an exchange barrier):
+    //          column-oriented solve against L_pp with the reciprocal diagonal
+    const int m = rows - p1;
+    for (int r = tid; r < m; r += CH_THREADS) {
+      const int i = p1 + r;
+      const double* colp = M + p0 + i * ld;
+      double v[NB];
 #pragma unroll
-      for (int s = 0; s < CH_NB; ++s) v[s] = (s < pb) ? col[s] : 0.0;
+      for (int s = 0; s < NB; ++s) v[s] = (s < pb) ? __ldcg(colp + s) : 0.0;
 #pragma unroll
-      for (int jj = 0; jj < CH_NB; ++jj) {
-        if (jj < pb) {
-          double acc = v[jj];
+      for (int s = 0; s < NB; ++s) {
+        v[s] *= sm.inv[s < pb ? s : 0];
+        if (s >= pb) v[s] = 0.0;
 #pragma unroll
-          for (int s = 0; s < jj; ++s) acc = fma(-v[s], sm.lpp[jj][s], acc);
-          v[jj] = acc / sm.lpp[jj][jj];
-        }
+        for (int jj = s + 1; jj < NB; ++jj) v[jj] = fma(-v[s], sm.blk[jj][s], v[jj]);
       }
 #pragma unroll
-      for (int s = 0; s < CH_NB; ++s)
-        if (s < pb) col[s] = v[s];
+      for (int s = 0; s < NB; ++s) pan[r * PLD + s] = v[s];
     }
-    cluster.sync();
-    // ---- (C) trailing update M[j][i] -= sum_s L[i][s] L[j][s], p1 <= j <= i
-    const int m = d - p1;
-    const double* P;
-    int pld;
-    if (stage_panel) {
-      for (int e = tid; e < m * CH_NB; e += CH_THREADS) {
-        const int r = e / CH_NB, s = e % CH_NB;
-        pan[r * CH_PLD + s] = (s < pb) ? M[(p0 + s) + static_cast<int64_t>(p1 + r) * d] : 0.0;
-      }
-      __syncthreads();
-      P = pan;
-      pld = CH_PLD;
-    } else {
-      P = nullptr;
-      pld = 0;
+    mark(4);
+    __syncthreads();
+    // rows are owned warp-round-robin across the cluster: row r -> warp r % nwarps
+    for (int r = gwarp; r < m; r += nwarps) {
+      const int i = p1 + r;
+      for (int s = lane; s < pb; s += 32) M[(p0 + s) + i * ld] = pan[r * PLD + s];
     }
+    mark(5);
+    if (p1 == d) {  // only the rhs row remained: y is complete
+      cluster.sync();
+      break;
+    }
+    // ---- (C) trailing update M[j][i] -= sum_s L[i][s] L[j][s], p1 <= j <= i,
+    //          rows i in [p1, d] (row d updates the right-hand side)
+    const int nb_next = min(NB, d - p1);
     for (int r = gwarp; r < m; r += nwarps) {  // row i = p1 + r
       const int i = p1 + r;
-      double li[CH_NB];
+      const int jmax = (i == d) ? r - 1 : r;  // the rhs row has no diagonal
+      double li[NB];
 #pragma unroll
-      for (int s = 0; s < CH_NB; ++s)
-        li[s] = P ? P[r * pld + s] : ((s < pb) ? M[(p0 + s) + static_cast<int64_t>(i) * d] : 0.0);
-      double* col = M + static_cast<int64_t>(i) * d;
-      for (int jr = lane; jr <= r; jr += 32) {
+      for (int s = 0; s < NB; ++s) li[s] = pan[r * PLD + s];
+      double* colp = M + i * ld;
+      for (int jr = lane; jr <= jmax; jr += 32) {
         const int j = p1 + jr;
-        double acc = 0.0;
-        if (P) {
+        double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+        const double* pj = pan + jr * PLD;
 #pragma unroll
-          for (int s = 0; s < CH_NB; ++s) acc = fma(li[s], P[jr * pld + s], acc);
-        } else {
-          const double* cj = M + p0 + static_cast<int64_t>(j) * d;
-#pragma unroll 8
-          for (int s = 0; s < pb; ++s) acc = fma(li[s], __ldcg(cj + s), acc);
+        for (int s = 0; s < NB; s += 4) {
+          a0 = fma(li[s], pj[s], a0);
+          a1 = fma(li[s + 1], pj[s + 1], a1);
+          a2 = fma(li[s + 2], pj[s + 2], a2);
+          a3 = fma(li[s + 3], pj[s + 3], a3);
         }
-        col[j] = __dsub_rn(col[j], acc);
+        const double nv = __dsub_rn(__ldcg(colp + j), (a0 + a1) + (a2 + a3));
+        colp[j] = nv;
+        if (r < nb_next)  // next diagonal block (row r, col jr <= r) into every CTA
+          for (int q = 0; q < cs; ++q) cluster.map_shared_rank(&sm, q)->nxt[par ^ 1][r][jr] = nv;
       }
     }
+    mark(6);
     cluster.sync();
+    mark(7);
   }
   if (rank != 0) return;
 
-  // ---- triangular solves on rank 0: L y = rhs, then L^T z = y
+  // ---- backward substitution on rank 0 (L[j][i] = M[i][j]; y = M[:, d]):
+  //      z_b = L_bb^{-T} (y_b - sum_{c > b} L_cb^T z_c), block by block; the
+  //      next block and the update operands are loaded before each block's
+  //      sequential solve.
   double* y = sm.vec;
-  for (int i = tid; i < d; i += CH_THREADS) y[i] = rhs[i];
+  const int nb = (d + NB - 1) / NB;
+  double* stage = pan;  // two [NB][NB+1] slots: L_bb^T (row r, col s) = L[b0+s][b0+r]
+  for (int i = tid; i < d; i += CH_THREADS) y[i] = __ldcg(M + i + d * ld);
+  // warp 0 solves the diagonal blocks; warps 1.. stage the next block and
+  // prefetch the update operands of the rows they own (rows < b0)
+  auto load_block = [&](int kb, double* dst) {
+    const int b0 = kb * NB, bn = min(NB, d - b0);
+    for (int e = tid - 32; e < NB * NB; e += CH_THREADS - 32) {
+      const int s2 = e / NB, r = e % NB;  // coalesced along r
+      dst[r * (NB + 1) + s2] = (r < bn && s2 < bn && s2 >= r) ? __ldcg(M + (b0 + r) + (b0 + s2) * ld) : 0.0;
+    }
+  };
+  constexpr int UW = CH_THREADS - 32;  // update threads
+  constexpr int RPT = (CH_MAX_D + UW - 1) / UW;
+  if (warp != 0) load_block(nb - 1, stage + ((nb - 1) & 1) * NB * (NB + 1));
   __syncthreads();
-  for (int b0 = 0; b0 < d; b0 += CH_NB) {
-    const int bn = min(CH_NB, d - b0);
-    if (warp == 0) {
-      const int i = b0 + lane;
-      double yi = (lane < bn) ? y[i] : 0.0;
-      for (int s = 0; s < bn; ++s) {
-        if (lane == s) yi = yi / M[i + static_cast<int64_t>(i) * d];
-        const double ys = __shfl_sync(0xffffffffu, yi, s);
-        if (lane > s && lane < bn) yi = fma(-M[(b0 + s) + static_cast<int64_t>(i) * d], ys, yi);
-      }
-      if (lane < bn) y[i] = yi;
-    }
-    __syncthreads();
-    for (int i = b0 + bn + tid; i < d; i += CH_THREADS) {
-      const double* col = M + b0 + static_cast<int64_t>(i) * d;
-      double acc = y[i];
-      for (int s = 0; s < bn; ++s) acc = fma(-col[s], y[b0 + s], acc);
-      y[i] = acc;
-    }
-    __syncthreads();
-  }
-  // backward: z_i = (y_i - sum_{j > i} L[j][i] z_j) / L[i][i],  L[j][i] = M[i][j]
-  const int nb = (d + CH_NB - 1) / CH_NB;
   for (int kb = nb - 1; kb >= 0; --kb) {
-    const int b0 = kb * CH_NB, bn = min(CH_NB, d - b0);
+    const int b0 = kb * NB, bn = min(NB, d - b0);
+    double* cur = stage + (kb & 1) * NB * (NB + 1);
     if (warp == 0) {
-      const int i = b0 + lane;
-      double zi = (lane < bn) ? y[i] : 0.0;
-      for (int s = bn - 1; s >= 0; --s) {
-        if (lane == s) zi = zi / M[i + static_cast<int64_t>(i) * d];
-        const double zs = __shfl_sync(0xffffffffu, zi, s);
-        if (lane < s) zi = fma(-M[i + static_cast<int64_t>(b0 + s) * d], zs, zi);  // L[b0+s][i]
+      double zi = (lane < bn) ? y[b0 + lane] : 0.0;
+      for (int s2 = bn - 1; s2 >= 0; --s2) {
+        if (lane == s2) zi *= sm.dinv[b0 + s2];
+        const double zs = __shfl_sync(0xffffffffu, zi, s2);
+        if (lane < s2) zi = fma(-cur[lane * (NB + 1) + s2], zs, zi);
       }
-      if (lane < bn) y[i] = zi;
+      if (lane < bn) y[b0 + lane] = zi;
+      __syncthreads();
+      mark(8);
+      __syncthreads();
+    } else {
+      const int ut = tid - 32;
+      double mv[NB];
+      int iq = ut;  // first owned row; later rows are loaded in place
+#pragma unroll
+      for (int s2 = 0; s2 < NB; ++s2)
+        mv[s2] = (iq < b0 && s2 < bn) ? __ldcg(M + iq + (b0 + s2) * ld) : 0.0;
+      if (kb > 0) load_block(kb - 1, stage + ((kb - 1) & 1) * NB * (NB + 1));
+      __syncthreads();  // z_b ready
+      if (iq < b0) {
+        double acc = y[iq];
+#pragma unroll
+        for (int s2 = 0; s2 < NB; ++s2)
+          if (s2 < bn) acc = fma(-mv[s2], y[b0 + s2], acc);
+        y[iq] = acc;
+      }
+      for (int q = 1; q < RPT; ++q) {
+        const int i = ut + q * UW;
+        if (i < b0) {
+          double acc = y[i];
+          for (int s2 = 0; s2 < bn; ++s2) acc = fma(-__ldcg(M + i + (b0 + s2) * ld), y[b0 + s2], acc);
+          y[i] = acc;
+        }
+      }
+      __syncthreads();
     }
-    __syncthreads();
-    for (int i = tid; i < b0; i += CH_THREADS) {
-      double acc = y[i];
-      for (int s = 0; s < bn; ++s) acc = fma(-M[i + static_cast<int64_t>(b0 + s) * d], y[b0 + s], acc);
-      y[i] = acc;
-    }
-    __syncthreads();
   }
+  mark(9);
+  if (!ignore_halt && ctl->halt) return;
   for (int i = tid; i < d; i += CH_THREADS) {
     const double zi = y[i];
     z[i] = zi;
