@@ -234,12 +234,22 @@ __global__ void __launch_bounds__(TK_THREADS) k_topk(
 // For w <= TKS_MAXW the upper 32 bits of every key stay in shared memory
 // after ONE coalesced pass over D (which also builds the first histogram);
 // the remaining radix levels on those bits run out of shared memory, and only
-// the (usually tiny) group tied on the upper 32 bits is re-read from global
-// memory to resolve the low 31 bits.  The selection rule is identical to
-// k_topk (descending key, ties to the smaller position).
+// the group tied on the upper 32 bits is re-read from global memory to
+// resolve the low 31 bits; its members' verdicts (greater / tied) are kept
+// as bitmasks so the selection sweeps never touch global memory.  The
+// selection rule is identical to k_topk (descending key, ties to the smaller
+// position).
+//
+// dynamic shared memory: hi[w] u32 | gtm[wb] u32 | eqm[wb] u32 | scratch
+// (histogram + candidates during selection, the position list afterwards)
 constexpr int TKS_MAXW = 46000;
-constexpr int TKS_CAND = 2048;
-constexpr size_t TKS_SMEM = static_cast<size_t>(TKS_MAXW) * 4;
+constexpr int TKS_CAND = 1024;
+constexpr int TKS_SCRATCH = 16384;  // bytes
+constexpr int TKS_POS = TKS_SCRATCH / 4;
+__host__ __device__ constexpr size_t tks_smem_bytes(int64_t w) {
+  return static_cast<size_t>(w) * 4 + 2 * static_cast<size_t>((w + 31) / 32) * 4 + TKS_SCRATCH;
+}
+constexpr size_t TKS_SMEM = tks_smem_bytes(TKS_MAXW);
 
 // Radix digit search over hist[0, nbins): the digit holding the need-th
 // largest element (counting from the top bin).  Whole block; returns digit
@@ -257,9 +267,21 @@ __device__ __forceinline__ void tks_find_digit(const uint32_t* hist, int nbins, 
   __syncthreads();
 }
 
+// Histogram increment with a warp-uniform fast path (tie-heavy inputs put
+// whole warps in one bin): one atomic of the population instead of 32.
 __device__ __forceinline__ void tks_add(uint32_t* hist, uint32_t dig, int lane) {
-  const uint32_t peers = __match_any_sync(0xffffffffu, dig);
-  if (dig != 0xFFFFFFFFu && lane == __ffs(peers) - 1) atomicAdd(&hist[dig], __popc(peers));
+  const uint32_t valid = __ballot_sync(0xffffffffu, dig != 0xFFFFFFFFu);
+  if (!valid) return;
+  const uint32_t first = __shfl_sync(0xffffffffu, dig, __ffs(valid) - 1);
+  if (__all_sync(0xffffffffu, dig == first || dig == 0xFFFFFFFFu)) {
+    if (lane == 0) atomicAdd(&hist[first], __popc(valid));
+  } else if (dig != 0xFFFFFFFFu) {
+    atomicAdd(&hist[dig], 1u);
+  }
+}
+
+__device__ __forceinline__ uint32_t lo_key(const double* v, int t, int weighted) {
+  return static_cast<uint32_t>(rank_key(__ldg(v + t), t, weighted) & 0x7FFFFFFFull);
 }
 
 __global__ void __launch_bounds__(TK_THREADS, 1) k_topk_smem(
@@ -268,13 +290,22 @@ __global__ void __launch_bounds__(TK_THREADS, 1) k_topk_smem(
     uint32_t* __restrict__ bitmap, int32_t* __restrict__ count, uint32_t* __restrict__ idx_list,
     double* __restrict__ val_list, int cap, int32_t* __restrict__ draws, Emit em) {
   if (ctl && ctl->halt) return;
-  extern __shared__ uint32_t hi_s[];  // [w] upper 32 key bits
-  __shared__ uint32_t hist[2048];
-  __shared__ uint32_t cand_lo[TKS_CAND];
+  PhaseClock pc;
+  extern __shared__ uint32_t tks_dyn[];
+  const int wi = static_cast<int>(w);
+  uint32_t* hi_s = tks_dyn;                  // [wi]
+  uint32_t* gtm = tks_dyn + wi;              // [wb] tie group: key greater than threshold
+  uint32_t* eqm = gtm + wb;                  // [wb] tie group: key equal to threshold
+  uint32_t* scratch = eqm + wb;              // TKS_SCRATCH bytes
+  uint32_t* hist = scratch;                  // [2048]
+  uint32_t* cand_lo = scratch + 2048;        // [TKS_CAND]
+  int32_t* cand_t = reinterpret_cast<int32_t*>(scratch + 2048 + TKS_CAND);  // [TKS_CAND]
+  int32_t* pos_list = reinterpret_cast<int32_t*>(scratch);                   // [TKS_POS] later
   __shared__ int ws[64];
   __shared__ int s_digit, s_above, s_ncand;
+  __shared__ int w_gt[TK_NW], w_eq[TK_NW], w_sel_pre[TK_NW], w_eq_pre[TK_NW];
   const int c = client_of(clients, blockIdx.x);
-  const int tid = threadIdx.x, lane = tid & 31;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const double* v = D + static_cast<int64_t>(c) * w;
   uint32_t* brow = bitmap + static_cast<int64_t>(c) * wb;
   if (tid == 0 && draws) draws[c] = 0;
@@ -284,20 +315,21 @@ __global__ void __launch_bounds__(TK_THREADS, 1) k_topk_smem(
     if (tid == 0) count[c] = 0;
     return;
   }
-  const int wi = static_cast<int>(w);
   // ---- pass 0: keys' upper halves into smem + histogram of hi bits [21, 32)
   for (int i = tid; i < 2048; i += TK_THREADS) hist[i] = 0u;
+  for (int i = tid; i < wb; i += TK_THREADS) { gtm[i] = 0u; eqm[i] = 0u; }
   if (tid == 0) s_ncand = 0;
   __syncthreads();
-  for (int base = 0; base < wi; base += 4 * TK_THREADS) {
-    double x[4];
+  constexpr int UNR = 8;  // loads in flight per thread
+  for (int base = 0; base < wi; base += UNR * TK_THREADS) {
+    double x[UNR];
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
+    for (int u = 0; u < UNR; ++u) {
       const int t = base + u * TK_THREADS + tid;
       x[u] = (t < wi) ? __ldg(v + t) : 0.0;
     }
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
+    for (int u = 0; u < UNR; ++u) {
       const int t = base + u * TK_THREADS + tid;
       uint32_t dig = 0xFFFFFFFFu;
       if (t < wi) {
@@ -309,6 +341,7 @@ __global__ void __launch_bounds__(TK_THREADS, 1) k_topk_smem(
     }
   }
   __syncthreads();
+  pc.mark(0);
   // ---- radix levels on the upper 32 bits (all in shared memory)
   constexpr int HSH[3] = {21, 10, 0};
   constexpr int HBI[3] = {11, 11, 10};
@@ -321,12 +354,13 @@ __global__ void __launch_bounds__(TK_THREADS, 1) k_topk_smem(
       for (int i = tid; i < 2048; i += TK_THREADS) hist[i] = 0u;
       __syncthreads();
       const int hsh = HSH[L - 1];
+      const uint32_t dmask = (1u << HBI[L]) - 1u;
       for (int base = 0; base < wi; base += TK_THREADS) {
         const int t = base + tid;
         uint32_t dig = 0xFFFFFFFFu;
         if (t < wi) {
           const uint32_t hi = hi_s[t];
-          if ((hi >> hsh) == prefix) dig = (hi >> HSH[L]) & ((1u << HBI[L]) - 1u);
+          if ((hi >> hsh) == prefix) dig = (hi >> HSH[L]) & dmask;
         }
         tks_add(hist, dig, lane);
       }
@@ -341,54 +375,46 @@ __global__ void __launch_bounds__(TK_THREADS, 1) k_topk_smem(
     __syncthreads();
     if (all) { take_all = true; break; }
   }
-  // prefix now equals hi >> level_shift of the threshold group
-  // ---- low 31 bits among the elements tied on all 32 upper bits
-  uint32_t lo_prefix = 0;
-  int lo_shift = 0;
-  bool lo_all = false;
+  pc.mark(1);
+  // ---- low 31 bits among the elements tied on all 32 upper bits; their
+  //      verdicts go to the gt / eq bitmasks
   const uint32_t T_hi = prefix;  // meaningful when !take_all (level_shift == 0)
   if (!take_all) {
-    const int ncand_total = static_cast<int>(hist[s_digit]);  // group size (stale-safe: read below)
-    (void)ncand_total;
-    // gather candidates (positions ascending is not required here)
     for (int base = 0; base < wi; base += TK_THREADS) {
       const int t = base + tid;
       if (t < wi && hi_s[t] == T_hi) {
         const int slot = atomicAdd(&s_ncand, 1);
         if (slot < TKS_CAND) {
-          cand_lo[slot] = static_cast<uint32_t>(rank_key(__ldg(v + t), t, weighted) & 0x7FFFFFFFull);
+          cand_t[slot] = t;
+          cand_lo[slot] = lo_key(v, t, weighted);
         }
       }
     }
     __syncthreads();
     const int ncand = s_ncand;
     const bool in_smem = ncand <= TKS_CAND;
+    uint32_t lo_prefix = 0;
+    int lo_shift = 0;
+    bool lo_all = false;
     constexpr int LSH[3] = {20, 10, 0};
     constexpr int LBI[3] = {11, 10, 10};
     for (int L = 0; L < 3; ++L) {
       for (int i = tid; i < 2048; i += TK_THREADS) hist[i] = 0u;
       __syncthreads();
       const int upper = L == 0 ? 31 : LSH[L - 1];
-      if (in_smem) {
-        for (int base = 0; base < ncand; base += TK_THREADS) {
-          const int e = base + tid;
-          uint32_t dig = 0xFFFFFFFFu;
-          if (e < ncand) {
-            const uint32_t lo = cand_lo[e];
-            if ((upper >= 31 ? 0u : (lo >> upper)) == lo_prefix) dig = (lo >> LSH[L]) & ((1u << LBI[L]) - 1u);
-          }
-          tks_add(hist, dig, lane);
+      const uint32_t dmask = (1u << LBI[L]) - 1u;
+      const int lim = in_smem ? ncand : wi;
+      for (int base = 0; base < lim; base += TK_THREADS) {
+        const int e = base + tid;
+        uint32_t dig = 0xFFFFFFFFu;
+        bool have = false;
+        uint32_t lo = 0;
+        if (e < lim) {
+          if (in_smem) { lo = cand_lo[e]; have = true; }
+          else if (hi_s[e] == T_hi) { lo = lo_key(v, e, weighted); have = true; }
         }
-      } else {
-        for (int base = 0; base < wi; base += TK_THREADS) {
-          const int t = base + tid;
-          uint32_t dig = 0xFFFFFFFFu;
-          if (t < wi && hi_s[t] == T_hi) {
-            const uint32_t lo = static_cast<uint32_t>(rank_key(__ldg(v + t), t, weighted) & 0x7FFFFFFFull);
-            if ((upper >= 31 ? 0u : (lo >> upper)) == lo_prefix) dig = (lo >> LSH[L]) & ((1u << LBI[L]) - 1u);
-          }
-          tks_add(hist, dig, lane);
-        }
+        if (have && (upper >= 31 ? 0u : (lo >> upper)) == lo_prefix) dig = (lo >> LSH[L]) & dmask;
+        tks_add(hist, dig, lane);
       }
       __syncthreads();
       tks_find_digit(hist, 1 << LBI[L], need, ws, &s_digit, &s_above);
@@ -400,53 +426,120 @@ __global__ void __launch_bounds__(TK_THREADS, 1) k_topk_smem(
       __syncthreads();
       if (all) { lo_all = true; break; }
     }
+    // verdicts of the tie group
+    const int lim = in_smem ? ncand : wi;
+    for (int base = 0; base < lim; base += TK_THREADS) {
+      const int e = base + tid;
+      if (e >= lim) continue;
+      int t;
+      uint32_t lo;
+      if (in_smem) { t = cand_t[e]; lo = cand_lo[e]; }
+      else {
+        if (hi_s[e] != T_hi) continue;
+        t = e;
+        lo = lo_key(v, e, weighted);
+      }
+      const uint32_t lp = lo >> lo_shift;
+      if (lp > lo_prefix || (lo_all && lp == lo_prefix)) atomicOr(&gtm[t >> 5], 1u << (t & 31));
+      else if (lp == lo_prefix) atomicOr(&eqm[t >> 5], 1u << (t & 31));
+    }
+    __syncthreads();
   }
-  // ---- final pass, ascending positions
-  int carry_sel = 0, carry_eq = 0;
-  uint32_t* il = idx_list + static_cast<int64_t>(c) * cap;
-  double* vl = val_list + static_cast<int64_t>(c) * cap;
-  for (int base = 0; base < wi; base += TK_THREADS) {
-    const int t = base + tid;
-    int sel = 0, eq = 0;
+  pc.mark(2);
+  // ---- final selection, ascending positions.  Warp w owns the contiguous
+  //      segment [w*S, (w+1)*S) (S a multiple of 32): a counting sweep, one
+  //      scan over the 32 warp totals, then an emitting sweep.
+  auto classify = [&](int t, uint32_t& gt_bits, uint32_t& eq_bits) {
+    // lane-wise verdicts for t = t0 + lane, returned as warp ballots
+    int gt = 0;
     if (t < wi) {
       const uint32_t hp = hi_s[t] >> level_shift;
-      if (take_all) {
-        sel = hp >= prefix;
-      } else if (hp > T_hi) {
-        sel = 1;
-      } else if (hp == T_hi) {
-        const uint32_t lp = static_cast<uint32_t>(rank_key(__ldg(v + t), t, weighted) & 0x7FFFFFFFull) >> lo_shift;
-        if (lp > lo_prefix) sel = 1;
-        else if (lp == lo_prefix) {
-          if (lo_all) sel = 1;
-          else eq = 1;
-        }
-      }
+      gt = take_all ? (hp >= prefix) : (hp > T_hi);
     }
-    if (!take_all && !lo_all) {
-      int tot_eq;
-      const int r = block_excl_scan(eq, ws, &tot_eq) + carry_eq;
-      carry_eq += tot_eq;
-      if (eq && r < need) sel = 1;
+    gt_bits = __ballot_sync(0xffffffffu, gt);
+    if (!take_all && t - lane < wi) {
+      const int q = (t - lane) >> 5;
+      gt_bits |= gtm[q];
+      eq_bits = eqm[q];
+    } else {
+      eq_bits = 0u;
     }
-    int tot_sel;
-    const int pos = block_excl_scan(sel, ws, &tot_sel) + carry_sel;
-    carry_sel += tot_sel;
-    if (em.rs && t < wi && (t % FOLD_RANGE) == 0)
-      em.rs[static_cast<int64_t>(c) * (em.nr + 1) + t / FOLD_RANGE] = pos;
+  };
+  const int S = ((wi + TK_THREADS - 1) / TK_THREADS) * 32;
+  const int seg0 = warp * S, seg1 = min(wi, seg0 + S);
+  int n_gt = 0, n_eq = 0;
+  for (int t0 = seg0; t0 < seg1; t0 += 32) {
+    uint32_t gb, eb;
+    classify(t0 + lane, gb, eb);
+    n_gt += __popc(gb);
+    n_eq += __popc(eb);
+  }
+  if (lane == 0) { w_gt[warp] = n_gt; w_eq[warp] = n_eq; }
+  __syncthreads();
+  pc.mark(3);
+  if (warp == 0) {
+    int eq_excl = w_eq[lane];
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, eq_excl, o);
+      if (lane >= o) eq_excl += y;
+    }
+    eq_excl -= w_eq[lane];  // exclusive prefix of tied keys
+    const int eq_take = max(0, min(need - eq_excl, w_eq[lane]));
+    const int sel = w_gt[lane] + eq_take;
+    int sel_incl = sel;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, sel_incl, o);
+      if (lane >= o) sel_incl += y;
+    }
+    w_sel_pre[lane] = sel_incl - sel;
+    w_eq_pre[lane] = eq_excl;
+    if (lane == 31) s_above = sel_incl;  // total selected
+  }
+  __syncthreads();
+  const int total = s_above;
+  const bool keep_pos = total <= TKS_POS;
+  uint32_t* il = idx_list + static_cast<int64_t>(c) * cap;
+  double* vl = val_list + static_cast<int64_t>(c) * cap;
+  int32_t* rsc = em.rs ? em.rs + static_cast<int64_t>(c) * (em.nr + 1) : nullptr;
+  int base_sel = w_sel_pre[warp], base_eq = w_eq_pre[warp];
+  const uint32_t lt = (1u << lane) - 1u;
+  for (int t0 = seg0; t0 < seg1; t0 += 32) {
+    const int t = t0 + lane;
+    uint32_t gb, eb;
+    classify(t, gb, eb);
+    const int is_eq = (eb >> lane) & 1;
+    const int rank_eq = base_eq + __popc(eb & lt);
+    const int sel = ((gb >> lane) & 1) | (is_eq & (rank_eq < need));
+    const uint32_t sm_ = __ballot_sync(0xffffffffu, sel);
+    const int pos = base_sel + __popc(sm_ & lt);
+    if (rsc && t < wi && (t % FOLD_RANGE) == 0) rsc[t / FOLD_RANGE] = pos;
     if (sel) {
-      const double vt = __ldg(v + t);
       il[pos] = static_cast<uint32_t>(t);
-      vl[pos] = vt;
-      emit_entry(em, c, t, vt);
+      if (keep_pos) pos_list[pos] = t;
     }
-    const uint32_t word = __ballot_sync(0xffffffffu, sel);
-    if (lane == 0 && (t >> 5) < wb) brow[t >> 5] = word;
+    if (lane == 0) brow[t0 >> 5] = sm_;
+    base_sel += __popc(sm_);
+    base_eq += __popc(eb);
   }
+  pc.mark(4);
   if (tid == 0) {
-    count[c] = carry_sel;
-    if (em.rs) em.rs[static_cast<int64_t>(c) * (em.nr + 1) + em.nr] = carry_sel;
+    count[c] = total;
+    if (rsc) rsc[em.nr] = total;
   }
+  __syncthreads();
+  // values and the client shift update: independent entries, all threads
+  for (int e0 = 0; e0 < total; e0 += 2 * TK_THREADS) {
+    const int ea = e0 + tid, eb2 = e0 + TK_THREADS + tid;
+    const int64_t ta = (ea < total) ? (keep_pos ? pos_list[ea] : il[ea]) : 0;
+    const int64_t tb = (eb2 < total) ? (keep_pos ? pos_list[eb2] : il[eb2]) : 0;
+    const double va = (ea < total) ? __ldg(v + ta) : 0.0;
+    const double vb = (eb2 < total) ? __ldg(v + tb) : 0.0;
+    if (ea < total) { vl[ea] = va; emit_entry(em, c, ta, va); }
+    if (eb2 < total) { vl[eb2] = vb; emit_entry(em, c, tb, vb); }
+  }
+  pc.mark(5);
 }
 
 // --------------------------------------------------------------- RandSeqK

@@ -235,7 +235,7 @@ int launch_compress(Ctx* ctx, cudaStream_t s, const int32_t* clients, int n_acti
   switch (c.kind) {
     case FB_KIND_TOPK:
       if (ctx->w <= TKS_MAXW)
-        k_topk_smem<<<n_active, TK_THREADS, static_cast<size_t>(ctx->w) * 4, s>>>(
+        k_topk_smem<<<n_active, TK_THREADS, tks_smem_bytes(ctx->w), s>>>(
             ctl, ctx->D, ctx->w, ctx->wb, c.k, c.topk_weighted, clients, ctx->flags, ctx->bitmap,
             ctx->count, ctx->idx_list, ctx->val_list, ctx->cap, ctx->draws, em);
       else
@@ -1317,6 +1317,15 @@ int fb_round_seeds(uint64_t run_seed, int32_t n_clients, int32_t rnd, uint64_t* 
   G_CK(cudaGetLastError());
   G_CK(cudaMemcpy(out, d, sizeof(uint64_t) * n_clients, cudaMemcpyDeviceToHost));
   cudaFree(d);
+  return FB_OK;
+}
+
+int fb_debug_counters(int32_t enable, long long* out) {
+  if (out) G_CK(cudaMemcpyFromSymbol(out, g_dbg, sizeof(long long) * 32));
+  long long zero[32] = {};
+  G_CK(cudaMemcpyToSymbol(g_dbg, zero, sizeof zero));
+  const int on = enable ? 1 : 0;
+  G_CK(cudaMemcpyToSymbol(g_dbg_on, &on, sizeof on));
   return FB_OK;
 }
 

@@ -183,16 +183,33 @@ __global__ void __launch_bounds__(FOLD_THREADS) k_master_fold(
     const int cb = lo;
     const int e0 = off[ca], e1 = off[cb];  // a client's slice is <= FOLD_RANGE < FOLD_STAGE
     // stage entries [e0, e1): entry e belongs to the client i with off[i] <= e < off[i+1]
-    for (int e = e0 + threadIdx.x; e < e1; e += FOLD_THREADS) {
-      int a = ca, b = cb - 1;
-      while (a < b) {
-        const int mid = (a + b + 1) >> 1;
-        if (off[mid] <= e) a = mid; else b = mid - 1;
+    constexpr int UF = 4;  // entries per thread in flight
+    for (int eb = e0; eb < e1; eb += UF * FOLD_THREADS) {
+      uint32_t ti[UF];
+      double tv[UF];
+#pragma unroll
+      for (int u = 0; u < UF; ++u) {
+        const int e = eb + u * FOLD_THREADS + threadIdx.x;
+        if (e < e1) {
+          int a = ca, b = cb - 1;
+          while (a < b) {
+            const int mid = (a + b + 1) >> 1;
+            if (off[mid] <= e) a = mid; else b = mid - 1;
+          }
+          const int c = client_of(clients, a);
+          const int64_t src = static_cast<int64_t>(c) * cap + beg[a] + (e - off[a]);
+          ti[u] = idx_list[src];
+          tv[u] = val_list[src];
+        }
       }
-      const int c = client_of(clients, a);
-      const int64_t src = static_cast<int64_t>(c) * cap + beg[a] + (e - off[a]);
-      st_t[e - e0] = static_cast<uint16_t>(idx_list[src] - t0);
-      st_v[e - e0] = val_list[src];
+#pragma unroll
+      for (int u = 0; u < UF; ++u) {
+        const int e = eb + u * FOLD_THREADS + threadIdx.x;
+        if (e < e1) {
+          st_t[e - e0] = static_cast<uint16_t>(ti[u] - t0);
+          st_v[e - e0] = tv[u];
+        }
+      }
     }
     __syncthreads();
     if (threadIdx.x < 32) {  // apply in ascending client order (distinct t within a client)
