@@ -163,6 +163,9 @@ int fb_get_round_diff(void* ctx, int32_t cid, double* out);
 /* last round's compressed delta of client cid: ascending packed indices,
  * values (already scaled for the Rand kinds), count */
 int fb_get_round_delta(void* ctx, int32_t cid, uint32_t* idx, double* val, int32_t* count);
+/* last round's scalars {grad_norm, f_mean, shift_mean, decrement, <x,x>} and
+ * per-client shifts l_i = ||D_i||_F [n] (may be NULL) */
+int fb_get_round_scalars(void* ctx, double* out5, double* client_shift);
 /* mean gradient of the last round and per-client gradients [n*d] */
 int fb_get_round_grads(void* ctx, double* mean_grad, double* client_grads);
 

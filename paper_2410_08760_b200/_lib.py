@@ -105,6 +105,7 @@ PROTOTYPES = {
     "fb_get_round_diff": (C.c_int, [_P, C.c_int32, _D]),
     "fb_get_round_delta": (C.c_int, [_P, C.c_int32, _U32, _D, _I32]),
     "fb_get_round_grads": (C.c_int, [_P, _D, _D]),
+    "fb_get_round_scalars": (C.c_int, [_P, _D, _D]),
     "fb_compress": (C.c_int, [_P, _D, _U64, _U32, _D, _I32, _I32]),
     "fb_oracle_eval": (C.c_int, [_P, _D, _D, _D, _D]),
     "fb_shifted_solve": (C.c_int, [_P, _D, C.c_double, _D, _D]),

@@ -339,6 +339,12 @@ int enqueue_fednl_round(Ctx* ctx) {
   TRY(launch_reduce(ctx, s, ctx->x, nullptr, n, n, true, ctx->row_grad, ctx->row_f));
   TRY(record(ctx, EV_REDUCE_END, s));
   // fork: compressor on st2 while the master solves on st
+  // (FB_SERIAL_ROUND=1 runs them back to back, for diagnosis)
+  static const bool serial = getenv("FB_SERIAL_ROUND") && atoi(getenv("FB_SERIAL_ROUND"));
+  if (serial) {
+    TRY(launch_solve(ctx, s, ctx->hmas, &ctx->sc->shift_mean, ctx->gbar, ctx->x, ctx->pvec,
+                     ctx->x_new, ls ? 2 : 0, 0));
+  }
   CK(cudaEventRecord(ctx->ev_fork, s));
   CK(cudaStreamWaitEvent(ctx->st2, ctx->ev_fork, 0));
   // compressor (+ client shift update) then the master fold H^k -> H^{k+1}
@@ -346,13 +352,16 @@ int enqueue_fednl_round(Ctx* ctx) {
   TRY(record(ctx, EV_COMP_START, ctx->st2));
   TRY(launch_compress(ctx, ctx->st2, nullptr, n, nullptr, nullptr));
   TRY(record(ctx, EV_COMP_END, ctx->st2));
+  static const bool fold_late = getenv("FB_FOLD_LATE") && atoi(getenv("FB_FOLD_LATE"));
   TRY(record(ctx, EV_FOLD_START, ctx->st2));
-  TRY(launch_master_fold(ctx, ctx->st2, nullptr, n, dense_kind(ctx) ? ctx->hest : nullptr,
-                         ctx->hmas, ctx->hmas2));
+  if (!fold_late)
+    TRY(launch_master_fold(ctx, ctx->st2, nullptr, n, dense_kind(ctx) ? ctx->hest : nullptr,
+                           ctx->hmas, ctx->hmas2));
   TRY(record(ctx, EV_FOLD_END, ctx->st2));
   CK(cudaEventRecord(ctx->ev_join, ctx->st2));
-  TRY(launch_solve(ctx, s, ctx->hmas, &ctx->sc->shift_mean, ctx->gbar, ctx->x, ctx->pvec,
-                   ctx->x_new, ls ? 2 : 0, 0));
+  if (!serial)
+    TRY(launch_solve(ctx, s, ctx->hmas, &ctx->sc->shift_mean, ctx->gbar, ctx->x, ctx->pvec,
+                     ctx->x_new, ls ? 2 : 0, 0));
   TRY(record(ctx, EV_SOLVE_END, s));
   int launches = 8;
   if (ls) {
@@ -370,6 +379,9 @@ int enqueue_fednl_round(Ctx* ctx) {
     launches += 3;
   }
   CK(cudaStreamWaitEvent(s, ctx->ev_join, 0));
+  if (fold_late)
+    TRY(launch_master_fold(ctx, s, nullptr, n, dense_kind(ctx) ? ctx->hest : nullptr, ctx->hmas,
+                           ctx->hmas2));
   CK(cudaMemcpyAsync(ctx->hmas, ctx->hmas2, sizeof(double) * ctx->w, cudaMemcpyDeviceToDevice, s));
   k_finish<<<1, 256, 0, s>>>(ctx->ctl, ctx->d, n, n, nullptr, ctx->x, ctx->x_new, 1, ctx->count,
                              ctx->row_counts, ctx->row_ls);
@@ -1058,6 +1070,20 @@ int fb_get_round_delta(void* handle, int32_t cid, uint32_t* idx, double* val, in
     COPY_OUT(val, ctx->val_list + static_cast<size_t>(cid) * ctx->cap, sizeof(double) * cnt);
   return FB_OK;
 }
+int fb_get_round_scalars(void* handle, double* out5, double* client_shift) {
+  Ctx* ctx = static_cast<Ctx*>(handle);
+  if (!ctx || !out5) return invalid(ctx, "null argument");
+  RoundScalars sc;
+  COPY_OUT(&sc, ctx->sc, sizeof sc);
+  out5[0] = sc.grad_norm;
+  out5[1] = sc.f_mean;
+  out5[2] = sc.shift_mean;
+  out5[3] = sc.decrement;
+  out5[4] = sc.xx;
+  if (client_shift) COPY_OUT(client_shift, ctx->shift_cli, sizeof(double) * ctx->n);
+  return FB_OK;
+}
+
 int fb_get_round_grads(void* handle, double* mean_grad, double* client_grads) {
   Ctx* ctx = static_cast<Ctx*>(handle);
   if (!ctx) return invalid(ctx, "null argument");

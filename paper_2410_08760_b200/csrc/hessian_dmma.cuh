@@ -24,14 +24,16 @@ namespace fb {
 constexpr int HT = 64;          // tile edge (features)
 constexpr int HKC = 16;         // samples per stage (128 B rows)
 constexpr int HSTAGE = 4;       // pipeline depth
-constexpr int HTHREADS = 128;   // 4 warps
+constexpr int HCONS = 4;        // consumer (DMMA) warps, one 32x32 quadrant each
+constexpr int HTHREADS = (HCONS + 1) * 32;  // + one TMA producer warp
 constexpr int HC_LD = HT + 1;   // epilogue staging pitch
 
 struct HessSmem {
   double a[HSTAGE][HT * HKC];  // 8 KB per stage, 1024 B aligned (swizzle-128B)
   double b[HSTAGE][HT * HKC];
   double h[HSTAGE][HKC];
-  uint64_t full[HSTAGE];
+  uint64_t full[HSTAGE];       // TMA -> consumers (transaction count)
+  uint64_t empty[HSTAGE];      // consumers -> producer (one arrive per active warp)
   double red[HTHREADS / 32];
   int flag_or;
 };
@@ -48,8 +50,15 @@ __device__ __forceinline__ void dmma_8x8x4(double (&c)[2], double a, double b) {
                : "d"(a), "d"(b));
 }
 
-// grid (n_pairs, n_active), block 128, dynamic smem HESS_SMEM.
-__global__ void __launch_bounds__(HTHREADS) k_hessian(
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+// grid (n_pairs, n_active), block HTHREADS, dynamic smem HESS_SMEM.
+// Warps 0..3 compute (warp q owns quadrant rows 32*(q&1), cols 32*(q>>1));
+// warp 4 is the TMA producer.  Stage s is refilled once every active
+// consumer warp has arrived on empty[s] (no CTA-wide barrier per stage).
+__global__ void __launch_bounds__(HTHREADS, 2) k_hessian(
     const __grid_constant__ CUtensorMap tmap_b, const DevCtl* __restrict__ ctl, int d, int ni,
     int ldh, const double* __restrict__ hcoef, double lam, const int32_t* __restrict__ clients,
     const double* __restrict__ hest, int64_t hest_stride, double* __restrict__ D,
@@ -74,7 +83,8 @@ __global__ void __launch_bounds__(HTHREADS) k_hessian(
   const int g = lane >> 2, t = lane & 3;
   const int rowbase = 32 * (warp & 1), colbase = 32 * (warp >> 1);
   // on a diagonal tile the lower-left quadrant is entirely below the diagonal
-  const bool active = !(diag && rowbase > colbase);
+  const int n_active_warps = diag ? HCONS - 1 : HCONS;
+  const bool consumer = warp < HCONS && !(diag && rowbase > colbase);
 
   const int nk = (ni + HKC - 1) / HKC;
   const double* hrow = hcoef + static_cast<int64_t>(c) * ldh;
@@ -82,41 +92,46 @@ __global__ void __launch_bounds__(HTHREADS) k_hessian(
 
   if (tid == 0) {
     tma_prefetch_desc(&tmap_b);
-    for (int s = 0; s < HSTAGE; ++s) mbar_init(&sm.full[s], 1);
+    for (int s2 = 0; s2 < HSTAGE; ++s2) {
+      mbar_init(&sm.full[s2], 1);
+      mbar_init(&sm.empty[s2], n_active_warps);
+    }
     fence_barrier_init();
     sm.flag_or = 0;
   }
   __syncthreads();
 
-  auto issue = [&](int it) {
-    const int s = it % HSTAGE;
-    mbar_arrive_expect_tx(&sm.full[s], stage_bytes);
-    tma_load_3d(sm.a[s], &tmap_b, &sm.full[s], it * HKC, I * HT, c);
-    if (!diag) tma_load_3d(sm.b[s], &tmap_b, &sm.full[s], it * HKC, J * HT, c);
-    bulk_load(sm.h[s], hrow + it * HKC, HKC * 8, &sm.full[s]);
-  };
-  if (tid == 0) {
-    for (int it = 0; it < HSTAGE && it < nk; ++it) issue(it);
-  }
-
   double acc[4][4][2];
 #pragma unroll
   for (int mi = 0; mi < 4; ++mi)
 #pragma unroll
-    for (int ni2 = 0; ni2 < 4; ++ni2) acc[mi][ni2][0] = acc[mi][ni2][1] = 0.0;
+    for (int nj = 0; nj < 4; ++nj) acc[mi][nj][0] = acc[mi][nj][1] = 0.0;
 
-  for (int it = 0; it < nk; ++it) {
-    const int s = it % HSTAGE;
-    mbar_wait(&sm.full[s], (it / HSTAGE) & 1);
-    const double* sa = sm.a[s];
-    const double* sb = diag ? sm.a[s] : sm.b[s];
-    if (active) {
+  if (warp == HCONS) {
+    // ---------------- TMA producer
+    if (lane == 0) {
+      for (int it = 0; it < nk; ++it) {
+        const int s2 = it % HSTAGE;
+        if (it >= HSTAGE) mbar_wait(&sm.empty[s2], ((it / HSTAGE) - 1) & 1);
+        mbar_arrive_expect_tx(&sm.full[s2], stage_bytes);
+        tma_load_3d(sm.a[s2], &tmap_b, &sm.full[s2], it * HKC, I * HT, c);
+        if (!diag) tma_load_3d(sm.b[s2], &tmap_b, &sm.full[s2], it * HKC, J * HT, c);
+        bulk_load(sm.h[s2], hrow + it * HKC, HKC * 8, &sm.full[s2]);
+      }
+    }
+  } else if (consumer) {
+    // ---------------- DMMA consumers
+    for (int it = 0; it < nk; ++it) {
+      const int s2 = it % HSTAGE;
+      mbar_wait(&sm.full[s2], (it / HSTAGE) & 1);
+      const double* sa = sm.a[s2];
+      const double* sb = diag ? sm.a[s2] : sm.b[s2];
 #pragma unroll
       for (int kk = 0; kk < HKC / 4; ++kk) {
         // k-step kk reads samples {2kk, 2kk+1, 2kk+8, 2kk+9}: with the 128B
         // swizzle every half-warp then touches 16 distinct bank pairs
         const int ks = 2 * kk + (t & 1) + 8 * (t >> 1);
-        const double hv = sm.h[s][ks];
+        const double hv = sm.h[s2][ks];
         double af[4], bf[4];
 #pragma unroll
         for (int mi = 0; mi < 4; ++mi) af[mi] = sa[swz(rowbase + 8 * mi + g, ks)] * hv;
@@ -127,14 +142,15 @@ __global__ void __launch_bounds__(HTHREADS) k_hessian(
 #pragma unroll
           for (int nj = 0; nj < 4; ++nj) dmma_8x8x4(acc[mi][nj], af[mi], bf[nj]);
       }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&sm.empty[s2]);
     }
-    __syncthreads();  // every warp is done with stage s
-    if (tid == 0 && it + HSTAGE < nk) issue(it + HSTAGE);
   }
+  __syncthreads();  // all stages consumed; the ring is free for the epilogue
 
   // ---- epilogue: stage the tile column-major, then stream packed columns
   double* cs = &sm.a[0][0];  // [64 cols][HC_LD] — reuses the pipeline ring
-  if (active) {
+  if (consumer) {
 #pragma unroll
     for (int mi = 0; mi < 4; ++mi)
 #pragma unroll
@@ -154,17 +170,38 @@ __global__ void __launch_bounds__(HTHREADS) k_hessian(
   double* Hc = hess_out ? hess_out + static_cast<int64_t>(slot) * w : nullptr;
   double part = 0.0;
   int fl = 0;
-  for (int col = warp; col < HT; col += 4) {
+  // every warp (producer included) streams columns col = warp, warp + 5, ...;
+  // the H_i^k operands of all its (column, row) pairs are loaded first so
+  // the global-memory latency is paid once per warp, not once per column
+  constexpr int NW = HTHREADS / 32;
+  constexpr int MAXC = (HT + NW - 1) / NW;  // columns per warp
+  double hk[MAXC][2];
+#pragma unroll
+  for (int q = 0; q < MAXC; ++q) {
+    const int col = warp + q * NW;
     const int b = J * HT + col;
-    if (b >= d) break;
+#pragma unroll
+    for (int h2 = 0; h2 < 2; ++h2) {
+      const int a = I * HT + lane + 32 * h2;
+      const bool ok = col < HT && b < d && a <= b && a < d;
+      hk[q][h2] = ok ? __ldg(hest_c + packed_at(a, b)) : 0.0;
+    }
+  }
+#pragma unroll
+  for (int q = 0; q < MAXC; ++q) {
+    const int col = warp + q * NW;
+    const int b = J * HT + col;
+    if (col >= HT || b >= d) continue;
     const int64_t cbase = packed_at(0, b);
-    for (int r = lane; r < HT; r += 32) {
+#pragma unroll
+    for (int h2 = 0; h2 < 2; ++h2) {
+      const int r = lane + 32 * h2;
       const int a = I * HT + r;
       if (a > b || a >= d) continue;
       const int64_t tt = cbase + a;
       double hv = cs[col * HC_LD + r];
       if (a == b) hv = __dadd_rn(hv, lam);
-      const double dv = __dsub_rn(hv, hest_c[tt]);
+      const double dv = __dsub_rn(hv, hk[q][h2]);
       Dc[tt] = dv;
       if (Hc) Hc[tt] = hv;
       const double wt = (a == b) ? 1.0 : 2.0;

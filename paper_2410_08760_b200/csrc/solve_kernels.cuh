@@ -6,9 +6,12 @@
 // matrix in its UPPER triangle, M[j][i] = A[j][i] for j <= i < d, i.e.
 // packed column i lands in column i of M (a coalesced copy), and the
 // right-hand side as an extra column M[j][d] = rhs[j].  Factorising the
-// augmented matrix leaves M[j][i] = L[i][j] and M[j][d] = y[j] with L y = rhs:
-// the forward substitution rides along with the panel solves and trailing
-// updates.  Row i of L is column i of M (contiguous).
+// augmented matrix produces L (L y = rhs, y = "row d" of L): the forward
+// substitution rides along with the panel solves and trailing updates.
+// L is written to the LOWER triangle, M[i][j] = L[i][j] (i >= j), so the
+// upper-triangle inputs of a panel are never overwritten while other CTAs of
+// the cluster may still be reading them (panel solves are redundant per CTA
+// and not separated by a barrier from the owners' write-back).
 //
 // Per panel of NB columns there are two cluster barriers:
 //   (A) rank 0 / warp 0 factors the NB x NB diagonal block (already in its
@@ -89,19 +92,19 @@ __global__ void __launch_bounds__(CH_THREADS, 1) k_chol_solve(
   // outputs at the end.  sm.failed is ordered before any DSMEM push by the
   // first cluster barrier below.
   if (tid == 0) sm.failed = 0;
-  const double shift = shift_ptr ? *shift_ptr : 0.0;
+  const double shift = shift_ptr ? __ldcg(shift_ptr) : 0.0;
 
   // ---- M[j][i] = H[j][i] (+ shift on the diagonal); M[j][d] = rhs[j]
   for (int i = gwarp; i <= d; i += nwarps) {
     if (i < d) {
       const int64_t pc = packed_at(0, i);
       for (int j = lane; j <= i; j += 32) {
-        double v = hpk[pc + j];
+        double v = __ldcg(hpk + pc + j);
         if (j == i) v = __dadd_rn(v, shift);
         M[j + i * ld] = v;
       }
     } else {
-      for (int j = lane; j < d; j += 32) M[j + i * ld] = rhs[j];
+      for (int j = lane; j < d; j += 32) M[j + i * ld] = __ldcg(rhs + j);
     }
   }
   // every CTA stages the first diagonal block straight from H
@@ -111,7 +114,7 @@ __global__ void __launch_bounds__(CH_THREADS, 1) k_chol_solve(
       const int r = e / NB, s = e % NB;
       double v = 0.0;
       if (r < pb && s <= r) {
-        v = hpk[packed_at(s, r)];
+        v = __ldcg(hpk + packed_at(s, r));
         if (s == r) v = __dadd_rn(v, shift);
       }
       sm.nxt[0][r][s] = v;
@@ -181,7 +184,7 @@ __global__ void __launch_bounds__(CH_THREADS, 1) k_chol_solve(
         if (rank == 0 && lane < pb) {
 #pragma unroll
           for (int s2 = 0; s2 < NB; ++s2)
-            if (s2 <= lane) M[(p0 + s2) + (p0 + lane) * ld] = row[s2];
+            if (s2 <= lane) M[(p0 + lane) + (p0 + s2) * ld] = row[s2];  // L, lower storage
           sm.dinv[p0 + lane] = sm.inv[lane];
         }
       }
@@ -215,7 +218,7 @@ __global__ void __launch_bounds__(CH_THREADS, 1) k_chol_solve(
     // rows are owned warp-round-robin across the cluster: row r -> warp r % nwarps
     for (int r = gwarp; r < m; r += nwarps) {
       const int i = p1 + r;
-      for (int s = lane; s < pb; s += 32) M[(p0 + s) + i * ld] = pan[r * PLD + s];
+      for (int s = lane; s < pb; s += 32) M[i + (p0 + s) * ld] = pan[r * PLD + s];  // L[i][p0+s]
     }
     mark(5);
     if (p1 == d) {  // only the rhs row remained: y is complete
@@ -262,14 +265,14 @@ __global__ void __launch_bounds__(CH_THREADS, 1) k_chol_solve(
   double* y = sm.vec;
   const int nb = (d + NB - 1) / NB;
   double* stage = pan;  // two [NB][NB+1] slots: L_bb^T (row r, col s) = L[b0+s][b0+r]
-  for (int i = tid; i < d; i += CH_THREADS) y[i] = __ldcg(M + i + d * ld);
+  for (int i = tid; i < d; i += CH_THREADS) y[i] = __ldcg(M + d + i * ld);  // L[d][i] = y_i
   // warp 0 solves the diagonal blocks; warps 1.. stage the next block and
   // prefetch the update operands of the rows they own (rows < b0)
   auto load_block = [&](int kb, double* dst) {
     const int b0 = kb * NB, bn = min(NB, d - b0);
     for (int e = tid - 32; e < NB * NB; e += CH_THREADS - 32) {
       const int s2 = e / NB, r = e % NB;  // coalesced along r
-      dst[r * (NB + 1) + s2] = (r < bn && s2 < bn && s2 >= r) ? __ldcg(M + (b0 + r) + (b0 + s2) * ld) : 0.0;
+      dst[r * (NB + 1) + s2] = (r < bn && s2 < bn && s2 >= r) ? __ldcg(M + (b0 + s2) + (b0 + r) * ld) : 0.0;
     }
   };
   constexpr int UW = CH_THREADS - 32;  // update threads
@@ -296,7 +299,7 @@ __global__ void __launch_bounds__(CH_THREADS, 1) k_chol_solve(
       int iq = ut;  // first owned row; later rows are loaded in place
 #pragma unroll
       for (int s2 = 0; s2 < NB; ++s2)
-        mv[s2] = (iq < b0 && s2 < bn) ? __ldcg(M + iq + (b0 + s2) * ld) : 0.0;
+        mv[s2] = (iq < b0 && s2 < bn) ? __ldcg(M + (b0 + s2) + iq * ld) : 0.0;
       if (kb > 0) load_block(kb - 1, stage + ((kb - 1) & 1) * NB * (NB + 1));
       __syncthreads();  // z_b ready
       if (iq < b0) {
@@ -310,7 +313,7 @@ __global__ void __launch_bounds__(CH_THREADS, 1) k_chol_solve(
         const int i = ut + q * UW;
         if (i < b0) {
           double acc = y[i];
-          for (int s2 = 0; s2 < bn; ++s2) acc = fma(-__ldcg(M + i + (b0 + s2) * ld), y[b0 + s2], acc);
+          for (int s2 = 0; s2 < bn; ++s2) acc = fma(-__ldcg(M + (b0 + s2) + i * ld), y[b0 + s2], acc);
           y[i] = acc;
         }
       }
@@ -322,7 +325,7 @@ __global__ void __launch_bounds__(CH_THREADS, 1) k_chol_solve(
   for (int i = tid; i < d; i += CH_THREADS) {
     const double zi = y[i];
     z[i] = zi;
-    if (mode == 0) x_out[i] = __dsub_rn(x[i], zi);
+    if (mode == 0) x_out[i] = __dsub_rn(__ldcg(x + i), zi);
     else if (mode == 1) x_out[i] = zi;
   }
 }

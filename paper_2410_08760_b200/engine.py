@@ -228,6 +228,13 @@ class FedNLEngine:
             return None, val if k else np.zeros(0)
         return idx[:k].copy(), val[:k].copy()
 
+    def round_scalars(self) -> tuple[dict, np.ndarray]:
+        out = np.zeros(5)
+        cs = np.zeros(self.n)
+        self._check(self.lib.fb_get_round_scalars(self.h, _lib.ptr(out), _lib.ptr(cs)), "fb_get_round_scalars")
+        keys = ("grad_norm", "f_mean", "shift_mean", "decrement", "xx")
+        return dict(zip(keys, out.tolist())), cs
+
     def round_grads(self) -> tuple[np.ndarray, np.ndarray]:
         mg = np.zeros(self.d)
         cg = np.zeros((self.n, self.d))

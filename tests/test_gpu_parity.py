@@ -412,6 +412,14 @@ def test_teacher_forced_round_c0():
     eng.set_master_hest(h_mas0)
     eng.run_rounds(1, first_round=2)
     swaps = 0
+    sc, cli_shift = eng.round_scalars()
+    ref_shift = np.array([O.frob(ref_diff[c], d) for c in range(n)])
+    assert normwise(cli_shift, ref_shift) <= 1e-10
+    mg, _ = eng.round_grads()
+    ref_g = np.zeros(d)
+    for c in range(n):
+        ref_g += O.local_eval(shards[c].bmat, shards[c].lam, x0, need_hess=False).grad
+    assert normwise(mg, ref_g / n) <= 1e-10
     for c in range(n):
         dv = eng.round_diff(c)
         hmax = np.max(np.abs(ref_diff[c] + h_cli0[c]))
