@@ -192,8 +192,10 @@ int fb_shifted_solve(void* ctx, const double* h_packed, double shift, const doub
 int fb_solve_phase_cycles(void* ctx, const double* h_packed, double shift, const double* rhs,
                           int32_t cluster, long long* cycles, float* ms);
 
-/* diagnostic: read (and zero) the 32 device phase-clock counters that kernels
- * accumulate from thread 0 of block 0 when enabled; `enable` arms the next run */
+/* diagnostic: read (and zero) the device phase-clock counters: out[0..32)
+ * accumulated from thread 0 of block 0 of instrumented kernels, out[32..1056)
+ * per-CTA durations of the last instrumented compressor launch; `enable`
+ * arms the next run */
 int fb_debug_counters(int32_t enable, long long* out);
 
 /* ---- context-free device SplitMix64 (rng.py:37-136) -------------------- */

@@ -247,7 +247,7 @@ constexpr int TKS_CAND = 1024;
 constexpr int TKS_SCRATCH = 16384;  // bytes
 constexpr int TKS_POS = TKS_SCRATCH / 4;
 __host__ __device__ constexpr size_t tks_smem_bytes(int64_t w) {
-  return static_cast<size_t>(w) * 4 + 2 * static_cast<size_t>((w + 31) / 32) * 4 + TKS_SCRATCH;
+  return static_cast<size_t>(w) * 4 + 3 * static_cast<size_t>((w + 31) / 32) * 4 + TKS_SCRATCH;
 }
 constexpr size_t TKS_SMEM = tks_smem_bytes(TKS_MAXW);
 
@@ -283,6 +283,11 @@ __device__ __forceinline__ void tks_add(uint32_t* hist, uint32_t dig, int lane) 
 __device__ __forceinline__ uint32_t lo_key(const double* v, int t, int weighted) {
   return static_cast<uint32_t>(rank_key(__ldg(v + t), t, weighted) & 0x7FFFFFFFull);
 }
+// low 31 key bits, skipping the global re-read when they are known to be zero
+__device__ __forceinline__ uint32_t lo_key_m(const double* v, int t, int weighted,
+                                             const uint32_t* lzm) {
+  return ((lzm[t >> 5] >> (t & 31)) & 1u) ? 0u : lo_key(v, t, weighted);
+}
 
 __global__ void __launch_bounds__(TK_THREADS, 1) k_topk_smem(
     const DevCtl* __restrict__ ctl, const double* __restrict__ D, int64_t w, int wb, int k,
@@ -291,12 +296,14 @@ __global__ void __launch_bounds__(TK_THREADS, 1) k_topk_smem(
     double* __restrict__ val_list, int cap, int32_t* __restrict__ draws, Emit em) {
   if (ctl && ctl->halt) return;
   PhaseClock pc;
+  const long long gt_start = globaltimer_ns();
   extern __shared__ uint32_t tks_dyn[];
   const int wi = static_cast<int>(w);
   uint32_t* hi_s = tks_dyn;                  // [wi]
   uint32_t* gtm = tks_dyn + wi;              // [wb] tie group: key greater than threshold
   uint32_t* eqm = gtm + wb;                  // [wb] tie group: key equal to threshold
-  uint32_t* scratch = eqm + wb;              // TKS_SCRATCH bytes
+  uint32_t* lzm = eqm + wb;                  // [wb] low 31 key bits are zero (no re-read)
+  uint32_t* scratch = lzm + wb;              // TKS_SCRATCH bytes
   uint32_t* hist = scratch;                  // [2048]
   uint32_t* cand_lo = scratch + 2048;        // [TKS_CAND]
   int32_t* cand_t = reinterpret_cast<int32_t*>(scratch + 2048 + TKS_CAND);  // [TKS_CAND]
@@ -317,7 +324,7 @@ __global__ void __launch_bounds__(TK_THREADS, 1) k_topk_smem(
   }
   // ---- pass 0: keys' upper halves into smem + histogram of hi bits [21, 32)
   for (int i = tid; i < 2048; i += TK_THREADS) hist[i] = 0u;
-  for (int i = tid; i < wb; i += TK_THREADS) { gtm[i] = 0u; eqm[i] = 0u; }
+  for (int i = tid; i < wb; i += TK_THREADS) { gtm[i] = 0u; eqm[i] = 0u; lzm[i] = 0u; }
   if (tid == 0) s_ncand = 0;
   __syncthreads();
   constexpr int UNR = 8;  // loads in flight per thread
@@ -332,11 +339,16 @@ __global__ void __launch_bounds__(TK_THREADS, 1) k_topk_smem(
     for (int u = 0; u < UNR; ++u) {
       const int t = base + u * TK_THREADS + tid;
       uint32_t dig = 0xFFFFFFFFu;
+      bool lz = false;
       if (t < wi) {
-        const uint32_t hi = static_cast<uint32_t>(rank_key(x[u], t, weighted) >> 31);
+        const uint64_t key = rank_key(x[u], t, weighted);
+        const uint32_t hi = static_cast<uint32_t>(key >> 31);
         hi_s[t] = hi;
         dig = hi >> 21;
+        lz = (key & 0x7FFFFFFFull) == 0;
       }
+      const uint32_t lzb = __ballot_sync(0xffffffffu, lz);
+      if (lane == 0 && t < wi) lzm[t >> 5] = lzb;
       tks_add(hist, dig, lane);
     }
   }
@@ -380,70 +392,99 @@ __global__ void __launch_bounds__(TK_THREADS, 1) k_topk_smem(
   //      verdicts go to the gt / eq bitmasks
   const uint32_t T_hi = prefix;  // meaningful when !take_all (level_shift == 0)
   if (!take_all) {
+    // gather the tie group (warp-aggregated: one shared atomic per warp) and
+    // count members whose low key bits are not known to be zero
+    __shared__ int s_nnz;
+    if (tid == 0) s_nnz = 0;
+    __syncthreads();
     for (int base = 0; base < wi; base += TK_THREADS) {
       const int t = base + tid;
-      if (t < wi && hi_s[t] == T_hi) {
-        const int slot = atomicAdd(&s_ncand, 1);
+      const bool in = t < wi && hi_s[t] == T_hi;
+      const bool nz = in && !((lzm[t >> 5] >> (t & 31)) & 1u);
+      const uint32_t inb = __ballot_sync(0xffffffffu, in), nzb = __ballot_sync(0xffffffffu, nz);
+      int wbase = 0;
+      if (lane == 0 && inb) {
+        wbase = atomicAdd(&s_ncand, __popc(inb));
+        if (nzb) atomicAdd(&s_nnz, __popc(nzb));
+      }
+      wbase = __shfl_sync(0xffffffffu, wbase, 0);
+      if (in) {
+        const int slot = wbase + __popc(inb & ((1u << lane) - 1u));
         if (slot < TKS_CAND) {
           cand_t[slot] = t;
-          cand_lo[slot] = lo_key(v, t, weighted);
+          cand_lo[slot] = nz ? lo_key(v, t, weighted) : 0u;
         }
       }
     }
     __syncthreads();
     const int ncand = s_ncand;
-    const bool in_smem = ncand <= TKS_CAND;
-    uint32_t lo_prefix = 0;
-    int lo_shift = 0;
-    bool lo_all = false;
-    constexpr int LSH[3] = {20, 10, 0};
-    constexpr int LBI[3] = {11, 10, 10};
-    for (int L = 0; L < 3; ++L) {
-      for (int i = tid; i < 2048; i += TK_THREADS) hist[i] = 0u;
+    if (s_nnz == 0) {
+      // every tied key is exactly T_hi << 31: the whole group is "equal";
+      // the first `need` of them by position are taken in the sweeps
+      for (int base = 0; base < wi; base += TK_THREADS) {
+        const int t = base + tid;
+        const uint32_t eb = __ballot_sync(0xffffffffu, t < wi && hi_s[t] == T_hi);
+        if (lane == 0 && t < wi) eqm[t >> 5] = eb;
+      }
       __syncthreads();
-      const int upper = L == 0 ? 31 : LSH[L - 1];
-      const uint32_t dmask = (1u << LBI[L]) - 1u;
-      const int lim = in_smem ? ncand : wi;
-      for (int base = 0; base < lim; base += TK_THREADS) {
-        const int e = base + tid;
-        uint32_t dig = 0xFFFFFFFFu;
-        bool have = false;
-        uint32_t lo = 0;
-        if (e < lim) {
-          if (in_smem) { lo = cand_lo[e]; have = true; }
-          else if (hi_s[e] == T_hi) { lo = lo_key(v, e, weighted); have = true; }
+    } else {
+      const bool in_smem = ncand <= TKS_CAND;
+      uint32_t lo_prefix = 0;
+      int lo_shift = 0;
+      bool lo_all = false;
+      constexpr int LSH[3] = {20, 10, 0};
+      constexpr int LBI[3] = {11, 10, 10};
+      for (int L = 0; L < 3; ++L) {
+        for (int i = tid; i < 2048; i += TK_THREADS) hist[i] = 0u;
+        __syncthreads();
+        const int upper = L == 0 ? 31 : LSH[L - 1];
+        const uint32_t dmask = (1u << LBI[L]) - 1u;
+        const int lim = in_smem ? ncand : wi;
+        for (int base = 0; base < lim; base += TK_THREADS) {
+          const int e = base + tid;
+          uint32_t dig = 0xFFFFFFFFu;
+          bool have = false;
+          uint32_t lo = 0;
+          if (e < lim) {
+            if (in_smem) { lo = cand_lo[e]; have = true; }
+            else if (hi_s[e] == T_hi) { lo = lo_key_m(v, e, weighted, lzm); have = true; }
+          }
+          if (have && (upper >= 31 ? 0u : (lo >> upper)) == lo_prefix) dig = (lo >> LSH[L]) & dmask;
+          tks_add(hist, dig, lane);
         }
-        if (have && (upper >= 31 ? 0u : (lo >> upper)) == lo_prefix) dig = (lo >> LSH[L]) & dmask;
-        tks_add(hist, dig, lane);
+        __syncthreads();
+        tks_find_digit(hist, 1 << LBI[L], need, ws, &s_digit, &s_above);
+        const int dg = s_digit;
+        need -= s_above;
+        lo_prefix = (L == 0) ? static_cast<uint32_t>(dg) : ((lo_prefix << LBI[L]) | static_cast<uint32_t>(dg));
+        lo_shift = LSH[L];
+        const bool all = (static_cast<int>(hist[dg]) == need);
+        __syncthreads();
+        if (all) { lo_all = true; break; }
+      }
+      // verdicts of the tie group
+      if (in_smem) {
+        for (int e = tid; e < ncand; e += TK_THREADS) {
+          const int t = cand_t[e];
+          const uint32_t lp = cand_lo[e] >> lo_shift;
+          if (lp > lo_prefix || (lo_all && lp == lo_prefix)) atomicOr(&gtm[t >> 5], 1u << (t & 31));
+          else if (lp == lo_prefix) atomicOr(&eqm[t >> 5], 1u << (t & 31));
+        }
+      } else {  // large tie group: warp-aligned sweep, one word per warp ballot
+        for (int base = 0; base < wi; base += TK_THREADS) {
+          const int t = base + tid;
+          int g_ = 0, e_ = 0;
+          if (t < wi && hi_s[t] == T_hi) {
+            const uint32_t lp = lo_key_m(v, t, weighted, lzm) >> lo_shift;
+            g_ = lp > lo_prefix || (lo_all && lp == lo_prefix);
+            e_ = !g_ && lp == lo_prefix;
+          }
+          const uint32_t gb = __ballot_sync(0xffffffffu, g_), eb = __ballot_sync(0xffffffffu, e_);
+          if (lane == 0 && t < wi) { gtm[t >> 5] = gb; eqm[t >> 5] = eb; }
+        }
       }
       __syncthreads();
-      tks_find_digit(hist, 1 << LBI[L], need, ws, &s_digit, &s_above);
-      const int dg = s_digit;
-      need -= s_above;
-      lo_prefix = (L == 0) ? static_cast<uint32_t>(dg) : ((lo_prefix << LBI[L]) | static_cast<uint32_t>(dg));
-      lo_shift = LSH[L];
-      const bool all = (static_cast<int>(hist[dg]) == need);
-      __syncthreads();
-      if (all) { lo_all = true; break; }
     }
-    // verdicts of the tie group
-    const int lim = in_smem ? ncand : wi;
-    for (int base = 0; base < lim; base += TK_THREADS) {
-      const int e = base + tid;
-      if (e >= lim) continue;
-      int t;
-      uint32_t lo;
-      if (in_smem) { t = cand_t[e]; lo = cand_lo[e]; }
-      else {
-        if (hi_s[e] != T_hi) continue;
-        t = e;
-        lo = lo_key(v, e, weighted);
-      }
-      const uint32_t lp = lo >> lo_shift;
-      if (lp > lo_prefix || (lo_all && lp == lo_prefix)) atomicOr(&gtm[t >> 5], 1u << (t & 31));
-      else if (lp == lo_prefix) atomicOr(&eqm[t >> 5], 1u << (t & 31));
-    }
-    __syncthreads();
   }
   pc.mark(2);
   // ---- final selection, ascending positions.  Warp w owns the contiguous
@@ -540,6 +581,12 @@ __global__ void __launch_bounds__(TK_THREADS, 1) k_topk_smem(
     if (eb2 < total) { vl[eb2] = vb; emit_entry(em, c, tb, vb); }
   }
   pc.mark(5);
+  if (g_dbg_on && tid == 0 && blockIdx.x < 1024) {
+    g_dbg_span[2 * blockIdx.x] = gt_start;
+    g_dbg_span[2 * blockIdx.x + 1] = globaltimer_ns();
+    g_dbg_cta[blockIdx.x] = clock64() - pc.t0;
+    if (!take_all) atomicAdd(reinterpret_cast<unsigned long long*>(&g_dbg[16]), 1ull);
+  }
 }
 
 // --------------------------------------------------------------- RandSeqK

@@ -53,13 +53,15 @@ struct Ctx {
   int64_t w = 0;
   double alpha_n = 0.0, rand_scale = 1.0;
   int solve_cs = 1, solve_nb = 32;
+  int prio_high = 0;
+  cudaEvent_t* direct_pool = nullptr;  // non-null: record() targets these (FB_NO_GRAPH)
   size_t solve_smem = 0;
   int toplek_P = 0;
   bool uploaded = false, initialised = false;
   std::string err;
 
   cudaStream_t st = nullptr, st2 = nullptr;
-  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr, ev_solve_launched = nullptr;
 
   DevCtl* ctl = nullptr;
   double *Bt = nullptr, *x = nullptr, *x_new = nullptr, *pvec = nullptr, *zbuf = nullptr;
@@ -276,19 +278,33 @@ int launch_compress(Ctx* ctx, cudaStream_t s, const int32_t* clients, int n_acti
 }
 int launch_solve(Ctx* ctx, cudaStream_t s, const double* hpk, const double* shift_ptr,
                  const double* rhs, const double* x, double* z, double* x_out, int mode,
-                 int ignore_halt, long long* dbg = nullptr) {
+                 int ignore_halt, long long* dbg = nullptr, cudaEvent_t launched = nullptr) {
   cudaLaunchConfig_t lc{};
   lc.gridDim = dim3(ctx->solve_cs);
   lc.blockDim = dim3(CH_THREADS);
   lc.dynamicSmemBytes = ctx->solve_smem;
   lc.stream = s;
-  cudaLaunchAttribute attr[1];
+  cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeClusterDimension;
   attr[0].val.clusterDim.x = ctx->solve_cs;
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
+  // the solve is the round's critical path and needs solve_cs SMs at once:
+  // schedule its cluster ahead of the concurrent compressor's CTAs
+  attr[1].id = cudaLaunchAttributePriority;
+  attr[1].val.priority = ctx->prio_high;
   lc.attrs = attr;
-  lc.numAttrs = 1;
+  lc.numAttrs = 2;
+  cudaLaunchAttribute attr3[3] = {attr[0], attr[1], {}};
+  if (launched) {
+    // fires once every CTA of the cluster is resident: the concurrent
+    // compressor is held back until then, so the solve never waits for SMs
+    attr3[2].id = cudaLaunchAttributeLaunchCompletionEvent;
+    attr3[2].val.launchCompletionEvent.event = launched;
+    attr3[2].val.launchCompletionEvent.flags = 0;
+    lc.attrs = attr3;
+    lc.numAttrs = 3;
+  }
   if (ctx->solve_nb == 32)
     CK(cudaLaunchKernelEx(&lc, k_chol_solve<32>, ctx->ctl, ctx->d, hpk, shift_ptr, rhs, x, ctx->M,
                           z, x_out, mode, ignore_halt, dbg));
@@ -320,6 +336,10 @@ int launch_master_fold(Ctx* ctx, cudaStream_t s, const int32_t* clients, int n_a
 
 int record(Ctx* ctx, EvSlot slot, cudaStream_t s) {
   ctx->ev_used[slot] = true;
+  if (ctx->direct_pool) {  // direct (non-graph) launches: live events
+    CK(cudaEventRecord(ctx->direct_pool[slot], s));
+    return FB_OK;
+  }
   CK(cudaEventRecordWithFlags(ctx->ev_fixed[slot], s, cudaEventRecordExternal));
   return FB_OK;
 }
@@ -338,30 +358,29 @@ int enqueue_fednl_round(Ctx* ctx) {
   TRY(record(ctx, EV_HESS_END, s));
   TRY(launch_reduce(ctx, s, ctx->x, nullptr, n, n, true, ctx->row_grad, ctx->row_f));
   TRY(record(ctx, EV_REDUCE_END, s));
-  // fork: compressor on st2 while the master solves on st
-  // (FB_SERIAL_ROUND=1 runs them back to back, for diagnosis)
+  // fork: the master solve on st, the compressor and master fold on st2.  The
+  // solve's cluster is launched first and the compressor waits for its
+  // launch-completion event (the solve is the critical path and needs
+  // CH_MAX_CLUSTER SMs at once; the compressor would otherwise fill them).
   static const bool serial = getenv("FB_SERIAL_ROUND") && atoi(getenv("FB_SERIAL_ROUND"));
-  if (serial) {
-    TRY(launch_solve(ctx, s, ctx->hmas, &ctx->sc->shift_mean, ctx->gbar, ctx->x, ctx->pvec,
-                     ctx->x_new, ls ? 2 : 0, 0));
-  }
   CK(cudaEventRecord(ctx->ev_fork, s));
   CK(cudaStreamWaitEvent(ctx->st2, ctx->ev_fork, 0));
-  // compressor (+ client shift update) then the master fold H^k -> H^{k+1}
-  // into the second buffer, overlapping the solve that reads H^k
+  TRY(launch_solve(ctx, s, ctx->hmas, &ctx->sc->shift_mean, ctx->gbar, ctx->x, ctx->pvec,
+                   ctx->x_new, ls ? 2 : 0, 0, nullptr, serial ? nullptr : ctx->ev_solve_launched));
+  if (serial) {
+    CK(cudaEventRecord(ctx->ev_solve_launched, s));
+  }
+  CK(cudaStreamWaitEvent(ctx->st2, ctx->ev_solve_launched, 0));
+  static const bool fold_late = getenv("FB_FOLD_LATE") && atoi(getenv("FB_FOLD_LATE"));
   TRY(record(ctx, EV_COMP_START, ctx->st2));
   TRY(launch_compress(ctx, ctx->st2, nullptr, n, nullptr, nullptr));
   TRY(record(ctx, EV_COMP_END, ctx->st2));
-  static const bool fold_late = getenv("FB_FOLD_LATE") && atoi(getenv("FB_FOLD_LATE"));
   TRY(record(ctx, EV_FOLD_START, ctx->st2));
   if (!fold_late)
     TRY(launch_master_fold(ctx, ctx->st2, nullptr, n, dense_kind(ctx) ? ctx->hest : nullptr,
                            ctx->hmas, ctx->hmas2));
   TRY(record(ctx, EV_FOLD_END, ctx->st2));
   CK(cudaEventRecord(ctx->ev_join, ctx->st2));
-  if (!serial)
-    TRY(launch_solve(ctx, s, ctx->hmas, &ctx->sc->shift_mean, ctx->gbar, ctx->x, ctx->pvec,
-                     ctx->x_new, ls ? 2 : 0, 0));
   TRY(record(ctx, EV_SOLVE_END, s));
   int launches = 8;
   if (ls) {
@@ -598,7 +617,9 @@ int fb_create(const fb_config* cfg_in, void** out) {
     while (ctx->toplek_P < w) ctx->toplek_P <<= 1;
   // master solve: one cluster (8 CTAs from d >= 128); 32-wide panels while the
   // (d + 1) x 33 panel fits in shared memory, else 16-wide
-  ctx->solve_cs = c.d >= 128 ? CH_MAX_CLUSTER : 1;
+  // 6 CTAs below d = 512 leave the per-client compressor (one CTA per SM)
+  // enough SMs to run in a single wave next to the solve
+  ctx->solve_cs = c.d < 128 ? 1 : (c.d < 512 ? 6 : CH_MAX_CLUSTER);
   if (const char* e = getenv("FB_SOLVE_CLUSTER")) ctx->solve_cs = std::max(1, std::min(8, atoi(e)));
   ctx->solve_nb = solve_panel_bytes<32>(c.d) <= 190 * 1024 ? 32 : 16;
   ctx->solve_smem = ctx->solve_nb == 32 ? solve_panel_bytes<32>(c.d) : solve_panel_bytes<16>(c.d);
@@ -627,10 +648,16 @@ int fb_create(const fb_config* cfg_in, void** out) {
       return fail(FB_ERR_CUDA);                                       \
     }                                                                 \
   } while (0)
+  {
+    int lo = 0, hi = 0;
+    CKC(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+    ctx->prio_high = hi;
+  }
   CKC(cudaStreamCreateWithFlags(&ctx->st, cudaStreamNonBlocking));
   CKC(cudaStreamCreateWithFlags(&ctx->st2, cudaStreamNonBlocking));
   CKC(cudaEventCreateWithFlags(&ctx->ev_fork, cudaEventDisableTiming));
   CKC(cudaEventCreateWithFlags(&ctx->ev_join, cudaEventDisableTiming));
+  CKC(cudaEventCreateWithFlags(&ctx->ev_solve_launched, cudaEventDisableTiming));
   for (int i = 0; i < EV_COUNT; ++i) CKC(cudaEventCreate(&ctx->ev_fixed[i]));
   ctx->ev_pool.resize(static_cast<size_t>(ROW_CHUNK) * EV_COUNT);
   for (auto& e : ctx->ev_pool) CKC(cudaEventCreate(&e));
@@ -708,6 +735,7 @@ void fb_destroy(void* handle) {
   for (auto& e : ctx->ev_fixed) if (e) cudaEventDestroy(e);
   if (ctx->ev_fork) cudaEventDestroy(ctx->ev_fork);
   if (ctx->ev_join) cudaEventDestroy(ctx->ev_join);
+  if (ctx->ev_solve_launched) cudaEventDestroy(ctx->ev_solve_launched);
   if (ctx->st) cudaStreamDestroy(ctx->st);
   if (ctx->st2) cudaStreamDestroy(ctx->st2);
   delete ctx;
@@ -857,7 +885,15 @@ int fb_run_rounds(void* handle, int32_t first_round, int32_t count, double stop_
             CK(cudaGraphExecEventRecordNodeSetEvent(ctx->gexec, ctx->ev_node[e],
                                                     ctx->ev_pool[static_cast<size_t>(i) * EV_COUNT + e]));
       }
-      CK(cudaGraphLaunch(ctx->gexec, s));
+      static const bool no_graph = getenv("FB_NO_GRAPH") && atoi(getenv("FB_NO_GRAPH"));
+      if (no_graph) {  // diagnostics: the same round body, launched directly
+        ctx->direct_pool = &ctx->ev_pool[static_cast<size_t>(i) * EV_COUNT];
+        const int r2 = (ctx->cfg.algorithm == FB_ALG_PP) ? enqueue_pp_round(ctx) : enqueue_fednl_round(ctx);
+        ctx->direct_pool = nullptr;
+        if (r2 != FB_OK) return r2;
+      } else {
+        CK(cudaGraphLaunch(ctx->gexec, s));
+      }
       CK(cudaEventRecord(ends[i], s));
     }
     // drive line-search continuations (rare: no trial in the first batch passed)
@@ -1348,6 +1384,8 @@ int fb_round_seeds(uint64_t run_seed, int32_t n_clients, int32_t rnd, uint64_t* 
 
 int fb_debug_counters(int32_t enable, long long* out) {
   if (out) G_CK(cudaMemcpyFromSymbol(out, g_dbg, sizeof(long long) * 32));
+  if (out) G_CK(cudaMemcpyFromSymbol(out + 32, g_dbg_cta, sizeof(long long) * 1024));
+  if (out) G_CK(cudaMemcpyFromSymbol(out + 32 + 1024, g_dbg_span, sizeof(long long) * 2048));
   long long zero[32] = {};
   G_CK(cudaMemcpyToSymbol(g_dbg, zero, sizeof zero));
   const int on = enable ? 1 : 0;
