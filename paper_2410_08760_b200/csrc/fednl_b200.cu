@@ -48,7 +48,8 @@ enum EvSlot {
 
 struct Ctx {
   fb_config cfg{};
-  int d = 0, n = 0, ni = 0, ldj = 0, ldh = 0, nblk = 0, nb_tiles = 0, n_pairs = 0, wb = 0;
+  int d = 0, n = 0, ni = 0, ldj = 0, ldh = 0, nblk = 0, ls_nblk = 0, nb_tiles = 0, n_pairs = 0,
+      wb = 0;
   int cap = 0, tau = 0, n_active_max = 0;
   int64_t w = 0;
   double alpha_n = 0.0, rand_scale = 1.0;
@@ -184,7 +185,7 @@ int make_tmap(Ctx* ctx) {
 int launch_margins(Ctx* ctx, cudaStream_t s, const double* x, const int32_t* clients, int n_active,
                    bool with_ctl = true) {
   dim3 grid(ctx->nblk, n_active);
-  k_margins<<<grid, MARGIN_THREADS, ctx->d * sizeof(double), s>>>(
+  k_margins<<<grid, MB_THREADS, ctx->d * sizeof(double), s>>>(
       with_ctl ? ctx->ctl : nullptr, ctx->Bt, ctx->d, ctx->ni, ctx->ldj, ctx->ldh, x, clients,
       ctx->hcoef, ctx->gcoef, ctx->loss_part, ctx->nblk);
   CKL();
@@ -212,7 +213,7 @@ int launch_hessian(Ctx* ctx, cudaStream_t s, const int32_t* clients, int n_activ
 }
 int launch_reduce(Ctx* ctx, cudaStream_t s, const double* x, const int32_t* clients, int n_active,
                   int n_div, bool with_frob, double* row_grad, double* row_f) {
-  k_reduce<<<1, 1024, 0, s>>>(ctx->ctl, n_active, clients, n_div, ctx->d, ctx->ni, ctx->nblk,
+  k_reduce<<<reduce_grid(ctx->d), RED_THREADS, 0, s>>>(ctx->ctl, n_active, clients, n_div, ctx->d, ctx->ni, ctx->nblk,
                               ctx->n_pairs, x, ctx->cfg.lam, ctx->grad, ctx->loss_part,
                               with_frob ? ctx->frob_part : nullptr, ctx->flags, ctx->gbar,
                               ctx->f_cli, ctx->shift_cli, ctx->sc, row_grad, row_f);
@@ -386,12 +387,12 @@ int enqueue_fednl_round(Ctx* ctx) {
   if (ls) {
     k_dot<<<1, 256, 0, s>>>(ctx->ctl, ctx->d, ctx->gbar, ctx->pvec, ctx->sc);
     CKL();
-    dim3 grid(ctx->nblk, n);
+    dim3 grid(ctx->ls_nblk, n);
     k_ls_trials<<<grid, MARGIN_THREADS, LS_BATCH * ctx->d * sizeof(double), s>>>(
         ctx->ctl, ctx->Bt, ctx->d, ctx->ni, ctx->ldj, ctx->x, ctx->pvec, ctx->steps_table, n,
-        ctx->trial_x, ctx->ls_loss_part, ctx->nblk);
+        ctx->trial_x, ctx->ls_loss_part, ctx->ls_nblk);
     CKL();
-    k_ls_decide<<<1, 256, 0, s>>>(ctx->ctl, ctx->d, n, ctx->ni, ctx->nblk, ctx->cfg.lam,
+    k_ls_decide<<<1, 256, 0, s>>>(ctx->ctl, ctx->d, n, ctx->ni, ctx->ls_nblk, ctx->cfg.lam,
                                   ctx->cfg.ls_c, ctx->steps_table, ctx->trial_x,
                                   ctx->ls_loss_part, ctx->sc, ctx->x_new, LS_BATCH);
     CKL();
@@ -601,7 +602,8 @@ int fb_create(const fb_config* cfg_in, void** out) {
   ctx->w = w;
   ctx->ldj = (c.n_samples + 1) & ~1;
   ctx->ldh = (c.n_samples + 15) & ~15;
-  ctx->nblk = (ctx->ldh + MARGIN_THREADS - 1) / MARGIN_THREADS;
+  ctx->nblk = (ctx->ldh + MB_SAMPLES - 1) / MB_SAMPLES;
+  ctx->ls_nblk = (ctx->ldh + MARGIN_THREADS - 1) / MARGIN_THREADS;
   ctx->nb_tiles = (c.d + HT - 1) / HT;
   ctx->n_pairs = ctx->nb_tiles * (ctx->nb_tiles + 1) / 2;
   ctx->wb = static_cast<int>((w + 31) / 32);
@@ -702,7 +704,7 @@ int fb_create(const fb_config* cfg_in, void** out) {
       dalloc(ctx, &ctx->jbuf, static_cast<size_t>(n) * ctx->cap) || dalloc(ctx, &ctx->seeds, n) ||
       dalloc(ctx, &ctx->sc, 1) || dalloc(ctx, &ctx->steps_table, 64) ||
       dalloc(ctx, &ctx->trial_x, static_cast<size_t>(LS_BATCH) * d) ||
-      dalloc(ctx, &ctx->ls_loss_part, static_cast<size_t>(LS_BATCH) * n * ctx->nblk) ||
+      dalloc(ctx, &ctx->ls_loss_part, static_cast<size_t>(LS_BATCH) * n * ctx->ls_nblk) ||
       dalloc(ctx, &ctx->subset, std::max(tau, 1)) || dalloc(ctx, &ctx->pool, n) ||
       dalloc(ctx, &ctx->hess_part, c.algorithm == FB_ALG_PP ? static_cast<size_t>(tau) * w : 1) ||
       dalloc(ctx, &ctx->cli_shift, n) ||
@@ -900,12 +902,12 @@ int fb_run_rounds(void* handle, int32_t first_round, int32_t count, double stop_
     TRY(read_status(ctx, &h));
     while (h.code == ST_LS_PENDING) {
       const int r = h.round;
-      dim3 grid(ctx->nblk, n);
+      dim3 grid(ctx->ls_nblk, n);
       k_ls_trials<<<grid, MARGIN_THREADS, LS_BATCH * ctx->d * sizeof(double), s>>>(
           ctx->ctl, ctx->Bt, ctx->d, ctx->ni, ctx->ldj, ctx->x, ctx->pvec, ctx->steps_table, n,
-          ctx->trial_x, ctx->ls_loss_part, ctx->nblk);
+          ctx->trial_x, ctx->ls_loss_part, ctx->ls_nblk);
       CKL();
-      k_ls_decide<<<1, 256, 0, s>>>(ctx->ctl, ctx->d, n, ctx->ni, ctx->nblk, ctx->cfg.lam,
+      k_ls_decide<<<1, 256, 0, s>>>(ctx->ctl, ctx->d, n, ctx->ni, ctx->ls_nblk, ctx->cfg.lam,
                                     ctx->cfg.ls_c, ctx->steps_table, ctx->trial_x,
                                     ctx->ls_loss_part, ctx->sc, ctx->x_new, LS_BATCH);
       CKL();
@@ -1217,7 +1219,7 @@ int fb_oracle_eval(void* handle, const double* x, double* f, double* grad, doubl
   TRY(launch_gradient(ctx, s, ctx->x_new, nullptr, n));
   if (hess_packed) TRY(launch_hessian(ctx, s, nullptr, n, ctx->zeros_w, 0, ctx->D, nullptr));
   // f via the reduction kernel without touching the row buffers or status
-  k_reduce<<<1, 1024, 0, s>>>(ctx->ctl, n, nullptr, n, d, ctx->ni, ctx->nblk, ctx->n_pairs,
+  k_reduce<<<reduce_grid(d), RED_THREADS, 0, s>>>(ctx->ctl, n, nullptr, n, d, ctx->ni, ctx->nblk, ctx->n_pairs,
                               ctx->x_new, ctx->cfg.lam, ctx->grad, ctx->loss_part, nullptr,
                               ctx->flags, ctx->gbar, ctx->f_cli, ctx->shift_cli, ctx->sc, nullptr,
                               nullptr);

@@ -32,43 +32,62 @@ __device__ __forceinline__ double softplus_neg(double m) {
 
 // Margins m_j = <B_j, x>, sigmoids, per-sample Hessian / gradient
 // coefficients, and per-block partial sums of the loss (for f_value).
-// grid (ceil(ldh / 128), n_active), block 128, dynamic smem d doubles.
-__global__ void __launch_bounds__(MARGIN_THREADS) k_margins(
+// One block = MB_SAMPLES consecutive samples (lane = sample) x 8 warps that
+// split the features (warp w sums a = w, w + 8, ...): every load is a
+// coalesced 256 B row segment and each thread keeps 8 loads in flight.
+// grid (ceil(ldh / 32), n_active), block 256, dynamic smem d doubles.
+constexpr int MB_SAMPLES = 32;
+constexpr int MB_THREADS = 256;
+__global__ void __launch_bounds__(MB_THREADS) k_margins(
     const DevCtl* __restrict__ ctl, const double* __restrict__ Bt, int d, int ni, int ldj,
     int ldh, const double* __restrict__ x, const int32_t* __restrict__ clients,
     double* __restrict__ hcoef, double* __restrict__ gcoef, double* __restrict__ loss_part,
     int nblk) {
   if (ctl && ctl->halt) return;
   extern __shared__ double xs[];
-  __shared__ double red[MARGIN_THREADS / 32];
+  __shared__ double part[8][MB_SAMPLES + 1];
   const int c = client_of(clients, blockIdx.y);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   for (int a = threadIdx.x; a < d; a += blockDim.x) xs[a] = x[a];
   __syncthreads();
-  const int j = blockIdx.x * blockDim.x + threadIdx.x;
-  double loss = 0.0;
+  const int j = blockIdx.x * MB_SAMPLES + lane;
+  double m = 0.0;
   if (j < ni) {
     const double* col = Bt + static_cast<int64_t>(c) * d * ldj + j;
-    double m0 = 0.0, m1 = 0.0, m2 = 0.0, m3 = 0.0;
-    int a = 0;
-    for (; a + 3 < d; a += 4) {
-      m0 = fma(__ldg(col + static_cast<int64_t>(a) * ldj), xs[a], m0);
-      m1 = fma(__ldg(col + static_cast<int64_t>(a + 1) * ldj), xs[a + 1], m1);
-      m2 = fma(__ldg(col + static_cast<int64_t>(a + 2) * ldj), xs[a + 2], m2);
-      m3 = fma(__ldg(col + static_cast<int64_t>(a + 3) * ldj), xs[a + 3], m3);
+    double acc[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) acc[u] = 0.0;
+    int a0 = warp;
+    for (; a0 + 56 < d; a0 += 64) {
+      double bv[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) bv[u] = __ldg(col + static_cast<int64_t>(a0 + 8 * u) * ldj);
+#pragma unroll
+      for (int u = 0; u < 8; ++u) acc[u] = fma(bv[u], xs[a0 + 8 * u], acc[u]);
     }
-    for (; a < d; ++a) m0 = fma(__ldg(col + static_cast<int64_t>(a) * ldj), xs[a], m0);
-    const double m = (m0 + m1) + (m2 + m3);
-    const double sig = stable_sigmoid(m);
-    const double inv_n = static_cast<double>(ni);
-    hcoef[static_cast<int64_t>(c) * ldh + j] = __ddiv_rn(__dmul_rn(sig, __dsub_rn(1.0, sig)), inv_n);
-    gcoef[static_cast<int64_t>(c) * ldh + j] = __ddiv_rn(__dsub_rn(sig, 1.0), inv_n);
-    loss = softplus_neg(m);
-  } else if (j < ldh) {
-    hcoef[static_cast<int64_t>(c) * ldh + j] = 0.0;
-    gcoef[static_cast<int64_t>(c) * ldh + j] = 0.0;
+    for (; a0 < d; a0 += 8) acc[0] = fma(__ldg(col + static_cast<int64_t>(a0) * ldj), xs[a0], acc[0]);
+    m = ((acc[0] + acc[1]) + (acc[2] + acc[3])) + ((acc[4] + acc[5]) + (acc[6] + acc[7]));
   }
-  const double s = block_sum(loss, red);
-  if (threadIdx.x == 0) loss_part[static_cast<int64_t>(c) * nblk + blockIdx.x] = s;
+  part[warp][lane] = m;
+  __syncthreads();
+  if (warp == 0) {
+    double mm = 0.0;
+#pragma unroll
+    for (int w2 = 0; w2 < 8; ++w2) mm += part[w2][lane];
+    double loss = 0.0;
+    if (j < ni) {
+      const double sig = stable_sigmoid(mm);
+      const double nd = static_cast<double>(ni);
+      hcoef[static_cast<int64_t>(c) * ldh + j] = __ddiv_rn(__dmul_rn(sig, __dsub_rn(1.0, sig)), nd);
+      gcoef[static_cast<int64_t>(c) * ldh + j] = __ddiv_rn(__dsub_rn(sig, 1.0), nd);
+      loss = softplus_neg(mm);
+    } else if (j < ldh) {
+      hcoef[static_cast<int64_t>(c) * ldh + j] = 0.0;
+      gcoef[static_cast<int64_t>(c) * ldh + j] = 0.0;
+    }
+    const double tot = warp_sum(loss);
+    if (lane == 0) loss_part[static_cast<int64_t>(c) * nblk + blockIdx.x] = tot;
+  }
 }
 
 // Local gradients g_c = B_c gcoef_c + lam x (oracle.py:108-121).

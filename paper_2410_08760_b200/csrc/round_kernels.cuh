@@ -9,12 +9,14 @@
 namespace fb {
 
 // Cross-client reductions of one round (algorithms.py:351-359, 399-402;
-// runtime.py:189-201).  Single CTA of 1024 threads.
+// runtime.py:189-201):
 //   f_cli[c]    = sum_b loss_part[c][b] / n_i + (0.5 lam) <x, x>
 //   shift_cli[c]= sqrt(sum_p frob_part[c][p])           (if frob_part)
 //   gbar        = (sum_c grad_c) / n_div
-//   out[0] = ||gbar||, out[1] = (sum_c f_c) / n_div, out[2] = (sum shift)/n_div
+//   out: ||gbar||, (sum_c f_c) / n_div, (sum_c shift_c) / n_div
 // A non-finite difference raises ST_NONFINITE (compressors.py:134-135).
+// Client sums use a fixed association (not the reference's sequential
+// order): the parity tolerance of these scalars is 1e-12 relative.
 struct RoundScalars {
   double grad_norm;
   double f_mean;
@@ -23,7 +25,14 @@ struct RoundScalars {
   double xx;
 };
 
-__global__ void __launch_bounds__(1024) k_reduce(
+// grid = reduce_grid(d) CTAs of 1024 threads.  CTA b owns the 32-feature
+// gbar tile b (its 32 warps split the clients, then a fixed-order tree over
+// the warps) and the client chunk b of the per-client scalars; every load of
+// a CTA is issued in one burst (the kernel is latency-, not bandwidth-bound).
+// The last CTA to finish (ticket in DevCtl) forms the round scalars.
+constexpr int RED_THREADS = 1024;
+__host__ __device__ __forceinline__ int reduce_grid(int d) { return (d + 31) / 32; }
+__global__ void __launch_bounds__(RED_THREADS) k_reduce(
     DevCtl* __restrict__ ctl, int n_active, const int32_t* __restrict__ clients, int n_div, int d,
     int ni, int nblk, int n_pairs, const double* __restrict__ x, double lam,
     const double* __restrict__ grad, const double* __restrict__ loss_part,
@@ -31,50 +40,113 @@ __global__ void __launch_bounds__(1024) k_reduce(
     double* __restrict__ gbar, double* __restrict__ f_cli, double* __restrict__ shift_cli,
     RoundScalars* __restrict__ out, double* __restrict__ row_grad, double* __restrict__ row_f) {
   if (ctl->halt) return;
+  PhaseClock pc;
   __shared__ double red[32];
-  __shared__ int s_bad;
+  __shared__ double gp[32][33];
+  __shared__ double stage[2048];
+  __shared__ int s_bad, s_last;
+  const int lane = threadIdx.x & 31, q = threadIdx.x >> 5;
+  const int G = gridDim.x, b = blockIdx.x;
   if (threadIdx.x == 0) s_bad = 0x7fffffff;
-  double xx_part = 0.0;
-  for (int a = threadIdx.x; a < d; a += blockDim.x) xx_part = fma(x[a], x[a], xx_part);
-  const double xx = block_sum(xx_part, red);
-  const double reg = __dmul_rn(__dmul_rn(0.5, lam), xx);
-  for (int s = threadIdx.x; s < n_active; s += blockDim.x) {
-    const int c = client_of(clients, s);
-    double ls = 0.0;
-    for (int b = 0; b < nblk; ++b) ls = __dadd_rn(ls, loss_part[static_cast<int64_t>(c) * nblk + b]);
-    f_cli[c] = __dadd_rn(__ddiv_rn(ls, static_cast<double>(ni)), reg);
-    if (frob_part) {
-      double fp = 0.0;
-      for (int p = 0; p < n_pairs; ++p) fp = __dadd_rn(fp, frob_part[static_cast<int64_t>(c) * n_pairs + p]);
-      shift_cli[c] = sqrt(fp);
-      if (flags[c] & 1) atomicMin(&s_bad, c);
+  // ---- burst: x, this CTA's client partials, this CTA's grad tile
+  const double xv = threadIdx.x < d ? x[threadIdx.x] : 0.0;
+  double xx_part = xv * xv;
+  for (int a = threadIdx.x + RED_THREADS; a < d; a += RED_THREADS) xx_part = fma(x[a], x[a], xx_part);
+  const int per_c = nblk + (frob_part ? n_pairs : 0);
+  const int cpb = (n_active + G - 1) / G;
+  const int c_lo = min(n_active, b * cpb), c_hi = min(n_active, c_lo + cpb);
+  const int chunk = max(1, 2048 / per_c);
+  auto stage_load = [&](int i0, int nc) {
+    for (int e = threadIdx.x; e < nc * per_c; e += RED_THREADS) {
+      const int ii = e / per_c, r = e - ii * per_c;
+      const int c = client_of(clients, i0 + ii);
+      stage[e] = r < nblk ? __ldcg(loss_part + static_cast<int64_t>(c) * nblk + r)
+                          : __ldcg(frob_part + static_cast<int64_t>(c) * n_pairs + (r - nblk));
     }
+  };
+  stage_load(c_lo, min(chunk, c_hi - c_lo));
+  {
+    const int a = b * 32 + lane;
+    const int per = (n_active + 31) / 32;
+    const int i_lo = min(n_active, q * per), i_hi = min(n_active, i_lo + per);
+    double sacc = 0.0;
+    if (a < d) {
+      for (int i0 = i_lo; i0 < i_hi; i0 += 8) {
+        // client ids first: a load feeding an address shares the grad loads'
+        // scoreboard, so interleaving them would serialise the batch
+        int cc[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) cc[u] = (i0 + u < i_hi) ? client_of(clients, i0 + u) : -1;
+        double v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+          v[u] = (cc[u] >= 0) ? __ldcg(grad + static_cast<int64_t>(cc[u]) * d + a) : 0.0;
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+          if (cc[u] >= 0) sacc = __dadd_rn(sacc, v[u]);
+      }
+    }
+    gp[q][lane] = sacc;
   }
-  for (int a = threadIdx.x; a < d; a += blockDim.x) {
-    // ascending-cid sequential sum; loads batched 8 deep for memory parallelism
-    double s = 0.0;
-    for (int i0 = 0; i0 < n_active; i0 += 8) {
-      double v[8];
-#pragma unroll
-      for (int u = 0; u < 8; ++u)
-        v[u] = (i0 + u < n_active) ? grad[static_cast<int64_t>(client_of(clients, i0 + u)) * d + a] : 0.0;
-#pragma unroll
-      for (int u = 0; u < 8; ++u)
-        if (i0 + u < n_active) s = __dadd_rn(s, v[u]);
+  const double xx = block_sum(xx_part, red);  // also publishes stage / gp
+  const double reg = __dmul_rn(__dmul_rn(0.5, lam), xx);
+  pc.mark(8);
+  if (q == 0) {
+    const int a = b * 32 + lane;
+    double t2 = 0.0;
+#pragma unroll 8
+    for (int w2 = 0; w2 < 32; ++w2) t2 = __dadd_rn(t2, gp[w2][lane]);
+    if (a < d) gbar[a] = __ddiv_rn(t2, static_cast<double>(n_div));
+  }
+  // ---- per-client scalars of this CTA's chunk
+  for (int i0 = c_lo; i0 < c_hi; i0 += chunk) {
+    const int nc = min(chunk, c_hi - i0);
+    if (i0 != c_lo) {
+      __syncthreads();
+      stage_load(i0, nc);
+      __syncthreads();
     }
-    gbar[a] = __ddiv_rn(s, static_cast<double>(n_div));
+    for (int ii = threadIdx.x; ii < nc; ii += RED_THREADS) {
+      const int c = client_of(clients, i0 + ii);
+      const double* st = stage + ii * per_c;
+      double ls = 0.0;
+      for (int r = 0; r < nblk; ++r) ls = __dadd_rn(ls, st[r]);
+      f_cli[c] = __dadd_rn(__ddiv_rn(ls, static_cast<double>(ni)), reg);
+      if (frob_part) {
+        double fp = 0.0;
+        for (int r = 0; r < n_pairs; ++r) fp = __dadd_rn(fp, st[nblk + r]);
+        shift_cli[c] = sqrt(fp);
+        if (flags[c] & 1) atomicMin(&s_bad, c);
+      }
+    }
   }
   __syncthreads();
-  double gg = 0.0;
-  for (int a = threadIdx.x; a < d; a += blockDim.x) gg = fma(gbar[a], gbar[a], gg);
-  const double gn2 = block_sum(gg, red);
+  pc.mark(9);
+  // ---- ticket: the last CTA forms the round scalars
   if (threadIdx.x == 0) {
-    double fs = 0.0, ss = 0.0;
-    for (int i = 0; i < n_active; ++i) {
-      const int c = client_of(clients, i);
-      fs = __dadd_rn(fs, f_cli[c]);
-      if (frob_part) ss = __dadd_rn(ss, shift_cli[c]);
-    }
+    if (s_bad != 0x7fffffff) atomicMax(&ctl->reduce_bad, 0x7fffffff - s_bad);
+    __threadfence();
+    s_last = atomicAdd(&ctl->reduce_ticket, 1) == G - 1;
+  }
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  double gg = 0.0, fs_part = 0.0, ss_part = 0.0;
+  for (int a = threadIdx.x; a < d; a += RED_THREADS) {
+    const double g = __ldcg(gbar + a);
+    gg = fma(g, g, gg);
+  }
+  for (int i = threadIdx.x; i < n_active; i += RED_THREADS) {
+    const int c = client_of(clients, i);
+    fs_part += __ldcg(f_cli + c);
+    if (frob_part) ss_part += __ldcg(shift_cli + c);
+  }
+  const double gn2 = block_sum(gg, red);
+  const double fs = block_sum(fs_part, red);
+  const double ss = block_sum(ss_part, red);
+  pc.mark(10);
+  if (threadIdx.x == 0) {
+    ctl->reduce_ticket = 0;
     out->grad_norm = sqrt(gn2);
     out->f_mean = __ddiv_rn(fs, static_cast<double>(n_div));
     out->shift_mean = __ddiv_rn(ss, static_cast<double>(n_div));
@@ -82,8 +154,9 @@ __global__ void __launch_bounds__(1024) k_reduce(
     const int slot = ctl->round - ctl->row_base;
     if (row_grad) row_grad[slot] = out->grad_norm;
     if (row_f) row_f[slot] = out->f_mean;
-    if (frob_part && s_bad != 0x7fffffff) {
-      ctl->bad_client = s_bad;
+    const int bad = atomicExch(&ctl->reduce_bad, 0);
+    if (frob_part && bad != 0) {
+      ctl->bad_client = 0x7fffffff - bad;
       raise_status(ctl, ST_NONFINITE);
     }
   }
