@@ -276,6 +276,20 @@ def run_ours(args) -> dict | None:
 # ------------------------------------------------------ CPU (oracle port)
 
 
+def _limit_blas_threads() -> None:
+    """One BLAS thread per worker: threadpoolctl only limits libraries that are
+    already loaded, so numpy is imported first."""
+    os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")
+    import numpy  # noqa: F401
+
+    try:
+        import threadpoolctl
+
+        threadpoolctl.threadpool_limits(1, "blas")
+    except ImportError:
+        pass
+
+
 def _cpu_sim(config: str, rounds: int, warmup: int, workers: int):
     from oracle import fednl_oracle as O
     from paper_2410_08760_b200.data import baseline_run_config
@@ -296,12 +310,7 @@ def _cpu_sim(config: str, rounds: int, warmup: int, workers: int):
 
 
 def cpu_baseline(config: str, rounds: int = 4) -> dict:
-    try:
-        import threadpoolctl
-
-        threadpoolctl.threadpool_limits(1, "blas")
-    except ImportError:
-        pass
+    _limit_blas_threads()
     workers = os.cpu_count() or 1
     dt = _cpu_sim(config, rounds, 1, workers)
     return {"value": round(rounds / dt, 4), "unit": "rounds/s", "cores": workers, "kind": "port",
@@ -313,12 +322,7 @@ def run_reference(args) -> dict | None:
     rank, world, _ = _env_rank()
     if rank != 0:
         return None
-    try:
-        import threadpoolctl
-
-        threadpoolctl.threadpool_limits(1, "blas")
-    except ImportError:
-        pass
+    _limit_blas_threads()
     workers = os.cpu_count() or 1
     K, W = args.steps, args.warmup
     dt = _cpu_sim(args.config, K, W, workers)

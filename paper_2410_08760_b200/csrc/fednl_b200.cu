@@ -10,7 +10,11 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
 #include <cmath>
+#include <map>
+#include <mutex>
+#include <thread>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -98,7 +102,8 @@ struct Ctx {
   fb_profile prof{};
   int launches_per_round = 0;
 
-  std::vector<void*> allocs;
+  std::vector<std::pair<void*, size_t>> allocs;
+  std::vector<cudaEvent_t> ev_ends;  // per-round end events of a run chunk
 };
 
 thread_local std::string g_err;
@@ -127,13 +132,55 @@ thread_local std::string g_err;
     }                                                                              \
   } while (0)
 
+// Process-wide cache of device buffers: contexts of the same shape (one per
+// simulate() call) reuse their predecessor's allocations instead of paying
+// cudaMalloc / cudaFree every call (the caching-allocator pattern).
+struct DevCache {
+  std::mutex mu;
+  std::multimap<size_t, void*> free;
+  size_t bytes = 0;
+};
+DevCache& dev_cache() {
+  static DevCache* c = new DevCache;  // process lifetime
+  return *c;
+}
+constexpr size_t DEV_CACHE_LIMIT = size_t(32) << 30;
+size_t cache_round(size_t bytes) { return (bytes + 4095) & ~size_t(4095); }
+cudaError_t cache_alloc(void** p, size_t bytes) {
+  DevCache& c = dev_cache();
+  {
+    std::lock_guard<std::mutex> g(c.mu);
+    auto it = c.free.find(bytes);
+    if (it != c.free.end()) {
+      *p = it->second;
+      c.free.erase(it);
+      c.bytes -= bytes;
+      return cudaSuccess;
+    }
+  }
+  return cudaMalloc(p, bytes);
+}
+void cache_release(void* p, size_t bytes) {
+  DevCache& c = dev_cache();
+  std::lock_guard<std::mutex> g(c.mu);
+  if (c.bytes + bytes > DEV_CACHE_LIMIT) {
+    cudaFree(p);
+    return;
+  }
+  c.free.emplace(bytes, p);
+  c.bytes += bytes;
+}
+
+// zero-filled device buffer owned by ctx (zeroing is queued on ctx->st;
+// fb_create synchronises before returning)
 template <typename T>
 int dalloc(Ctx* ctx, T** p, size_t count) {
   if (count == 0) count = 1;
+  const size_t bytes = cache_round(count * sizeof(T));
   void* q = nullptr;
-  CK(cudaMalloc(&q, count * sizeof(T)));
-  CK(cudaMemset(q, 0, count * sizeof(T)));
-  ctx->allocs.push_back(q);
+  CK(cache_alloc(&q, bytes));
+  ctx->allocs.emplace_back(q, bytes);
+  CK(cudaMemsetAsync(q, 0, bytes, ctx->st));
   *p = static_cast<T*>(q);
   return FB_OK;
 }
@@ -363,7 +410,13 @@ int enqueue_fednl_round(Ctx* ctx) {
   // solve's cluster is launched first and the compressor waits for its
   // launch-completion event (the solve is the critical path and needs
   // CH_MAX_CLUSTER SMs at once; the compressor would otherwise fill them).
-  static const bool serial = getenv("FB_SERIAL_ROUND") && atoi(getenv("FB_SERIAL_ROUND"));
+  // Under a profiler's injection library (ncu serialises every launch anyway)
+  // the launch-completion attribute is not supported: order the compressor
+  // after the solve instead.
+  static const bool serial = (getenv("FB_SERIAL_ROUND") && atoi(getenv("FB_SERIAL_ROUND"))) ||
+                             getenv("CUDA_INJECTION64_PATH") != nullptr ||
+                             getenv("NV_NSIGHT_INJECTION_TRANSPORT_TYPE") != nullptr ||
+                             getenv("NV_TPS_LAUNCH_TOKEN") != nullptr;
   CK(cudaEventRecord(ctx->ev_fork, s));
   CK(cudaStreamWaitEvent(ctx->st2, ctx->ev_fork, 0));
   TRY(launch_solve(ctx, s, ctx->hmas, &ctx->sc->shift_mean, ctx->gbar, ctx->x, ctx->pvec,
@@ -637,8 +690,9 @@ int fb_create(const fb_config* cfg_in, void** out) {
     return fail(FB_ERR_CUDA);
   }
   int dev = 0;
-  cudaDeviceProp prop;
-  if (cudaGetDeviceProperties(&prop, dev) != cudaSuccess || prop.major != 10) {
+  int cc_major = 0;
+  if (cudaDeviceGetAttribute(&cc_major, cudaDevAttrComputeCapabilityMajor, dev) != cudaSuccess ||
+      cc_major != 10) {
     ctx->err = "libfednl_b200 needs an sm_100 (B200) device";
     return fail(FB_ERR_CUDA);
   }
@@ -661,8 +715,6 @@ int fb_create(const fb_config* cfg_in, void** out) {
   CKC(cudaEventCreateWithFlags(&ctx->ev_join, cudaEventDisableTiming));
   CKC(cudaEventCreateWithFlags(&ctx->ev_solve_launched, cudaEventDisableTiming));
   for (int i = 0; i < EV_COUNT; ++i) CKC(cudaEventCreate(&ctx->ev_fixed[i]));
-  ctx->ev_pool.resize(static_cast<size_t>(ROW_CHUNK) * EV_COUNT);
-  for (auto& e : ctx->ev_pool) CKC(cudaEventCreate(&e));
   // dynamic shared memory limits are per-function process state: only ever
   // raise them, so contexts of different shapes can coexist
   static size_t max_toplek = 0, max_solve = 0;
@@ -720,7 +772,8 @@ int fb_create(const fb_config* cfg_in, void** out) {
   }
   double steps[64];
   for (int i = 0; i < 64; ++i) steps[i] = c.ls_steps_table[i <= 60 ? i : 60];
-  CKC(cudaMemcpy(ctx->steps_table, steps, sizeof steps, cudaMemcpyHostToDevice));
+  CKC(cudaMemcpyAsync(ctx->steps_table, steps, sizeof steps, cudaMemcpyHostToDevice, ctx->st));
+  CKC(cudaStreamSynchronize(ctx->st));  // zero fills and the table are in place
   if (make_tmap(ctx) != FB_OK) return fail(FB_ERR_CUDA);
   *out = ctx;
   return rc;
@@ -732,7 +785,10 @@ void fb_destroy(void* handle) {
   if (!ctx) return;
   if (ctx->gexec) cudaGraphExecDestroy(ctx->gexec);
   if (ctx->graph) cudaGraphDestroy(ctx->graph);
-  for (void* p : ctx->allocs) cudaFree(p);
+  if (ctx->st) cudaStreamSynchronize(ctx->st);
+  if (ctx->st2) cudaStreamSynchronize(ctx->st2);
+  for (auto& pa : ctx->allocs) cache_release(pa.first, pa.second);
+  for (auto& e : ctx->ev_ends) if (e) cudaEventDestroy(e);
   for (auto& e : ctx->ev_pool) if (e) cudaEventDestroy(e);
   for (auto& e : ctx->ev_fixed) if (e) cudaEventDestroy(e);
   if (ctx->ev_fork) cudaEventDestroy(ctx->ev_fork);
@@ -774,30 +830,101 @@ __global__ void k_transpose_shard(const double* __restrict__ src, double* __rest
   }
 }
 
+// Shard upload: worker threads copy shards into pinned staging slots (two per
+// worker), DMA them on the worker's own stream and transpose them into Bt.
+// Slots, device staging and streams are process-wide and reused by later
+// calls; the call returns once every shard is resident.
+struct UploadLane {
+  double* host[2] = {nullptr, nullptr};
+  double* dev[2] = {nullptr, nullptr};
+  cudaEvent_t done[2] = {nullptr, nullptr};
+  cudaStream_t st = nullptr;
+  size_t cap = 0;
+};
+struct UploadPool {
+  std::mutex mu;
+  std::vector<UploadLane> lanes;
+};
+UploadPool& upload_pool() {
+  static UploadPool* p = new UploadPool;  // process lifetime
+  return *p;
+}
+constexpr int UPLOAD_LANES = 8;
+
 int fb_upload_shards(void* handle, const double* const* bmats) {
   Ctx* ctx = static_cast<Ctx*>(handle);
   if (!ctx || !bmats) return invalid(ctx, "null argument");
-  const int d = ctx->d, ni = ctx->ni;
+  for (int c = 0; c < ctx->n; ++c)
+    if (!bmats[c]) return invalid(ctx, "null shard pointer");
+  const int d = ctx->d, ni = ctx->ni, n = ctx->n;
   const size_t bytes = static_cast<size_t>(d) * ni * sizeof(double);
-  double* stage[2] = {nullptr, nullptr};
-  CK(cudaMalloc(&stage[0], bytes));
-  CK(cudaMalloc(&stage[1], bytes));
-  for (int c = 0; c < ctx->n; ++c) {
-    if (!bmats[c]) {
-      cudaFree(stage[0]);
-      cudaFree(stage[1]);
-      return invalid(ctx, "null shard pointer");
+  UploadPool& pool = upload_pool();
+  std::lock_guard<std::mutex> guard(pool.mu);
+  const int L = std::max(1, std::min(UPLOAD_LANES, n));
+  if (static_cast<int>(pool.lanes.size()) < L) pool.lanes.resize(L);
+  for (int l = 0; l < L; ++l) {
+    UploadLane& ln = pool.lanes[l];
+    if (!ln.st) {
+      CK(cudaStreamCreateWithFlags(&ln.st, cudaStreamNonBlocking));
+      for (int b = 0; b < 2; ++b) CK(cudaEventCreateWithFlags(&ln.done[b], cudaEventDisableTiming));
     }
-    double* sbuf = stage[c & 1];
-    CK(cudaMemcpyAsync(sbuf, bmats[c], bytes, cudaMemcpyHostToDevice, ctx->st));
-    dim3 grid((ctx->ldj + 31) / 32, (d + 31) / 32);
-    k_transpose_shard<<<grid, dim3(32, 8), 0, ctx->st>>>(
-        sbuf, ctx->Bt + static_cast<size_t>(c) * d * ctx->ldj, d, ni, ctx->ldj);
-    CKL();
+    if (ln.cap < bytes) {
+      for (int b = 0; b < 2; ++b) {
+        if (ln.host[b]) cudaFreeHost(ln.host[b]);
+        if (ln.dev[b]) cudaFree(ln.dev[b]);
+        ln.host[b] = nullptr;
+        ln.dev[b] = nullptr;
+      }
+      ln.cap = 0;
+      for (int b = 0; b < 2; ++b) {
+        CK(cudaHostAlloc(&ln.host[b], bytes, cudaHostAllocDefault));
+        CK(cudaMalloc(&ln.dev[b], bytes));
+      }
+      ln.cap = bytes;
+    }
   }
-  CK(cudaStreamSynchronize(ctx->st));
-  cudaFree(stage[0]);
-  cudaFree(stage[1]);
+  // Bt must not be written before ctx->st's zero fills (fb_create) — already
+  // synchronised there; later writers of Bt are ordered after this call.
+  std::atomic<int> failed{0};
+  std::string err;
+  std::mutex err_mu;
+  auto lane_body = [&](int l) {
+    UploadLane& ln = pool.lanes[l];
+    int slot = 0;
+    for (int c = l; c < n && !failed.load(); c += L, slot ^= 1) {
+      cudaError_t e = cudaEventSynchronize(ln.done[slot]);  // slot free again
+      if (e == cudaSuccess) {
+        std::memcpy(ln.host[slot], bmats[c], bytes);
+        e = cudaMemcpyAsync(ln.dev[slot], ln.host[slot], bytes, cudaMemcpyHostToDevice, ln.st);
+      }
+      if (e == cudaSuccess) {
+        dim3 grid((ctx->ldj + 31) / 32, (d + 31) / 32);
+        k_transpose_shard<<<grid, dim3(32, 8), 0, ln.st>>>(
+            ln.dev[slot], ctx->Bt + static_cast<size_t>(c) * d * ctx->ldj, d, ni, ctx->ldj);
+        e = cudaGetLastError();
+      }
+      if (e == cudaSuccess) e = cudaEventRecord(ln.done[slot], ln.st);
+      if (e != cudaSuccess) {
+        std::lock_guard<std::mutex> g(err_mu);
+        err = std::string("shard upload: ") + cudaGetErrorString(e);
+        failed.store(1);
+      }
+    }
+    cudaError_t e = cudaStreamSynchronize(ln.st);
+    if (e != cudaSuccess) {
+      std::lock_guard<std::mutex> g(err_mu);
+      err = std::string("shard upload: ") + cudaGetErrorString(e);
+      failed.store(1);
+    }
+  };
+  std::vector<std::thread> workers;
+  for (int l = 1; l < L; ++l) workers.emplace_back(lane_body, l);
+  lane_body(0);
+  for (auto& t : workers) t.join();
+  if (failed.load()) {
+    ctx->err = err;
+    return FB_ERR_CUDA;
+  }
   ctx->uploaded = true;
   return FB_OK;
 }
@@ -873,8 +1000,16 @@ int fb_run_rounds(void* handle, int32_t first_round, int32_t count, double stop_
   int rc = FB_OK;
   std::vector<double> rg(ROW_CHUNK), rf(ROW_CHUNK);
   std::vector<int32_t> rls(ROW_CHUNK), rcnt(static_cast<size_t>(ROW_CHUNK) * n);
-  std::vector<cudaEvent_t> ends(ROW_CHUNK);
-  for (auto& e : ends) CK(cudaEventCreate(&e));
+  if (ctx->ev_ends.empty()) {
+    ctx->ev_ends.resize(ROW_CHUNK);
+    for (auto& e : ctx->ev_ends) CK(cudaEventCreate(&e));
+  }
+  static const bool no_graph = getenv("FB_NO_GRAPH") && atoi(getenv("FB_NO_GRAPH"));
+  if ((timed || no_graph) && ctx->ev_pool.empty()) {  // per-kernel event slots, on first use
+    ctx->ev_pool.resize(static_cast<size_t>(ROW_CHUNK) * EV_COUNT);
+    for (auto& e : ctx->ev_pool) CK(cudaEventCreate(&e));
+  }
+  std::vector<cudaEvent_t>& ends = ctx->ev_ends;
   while (done < count && rc == FB_OK) {
     const int chunk = std::min(ROW_CHUNK, count - done);
     h.row_base = first_round + done;
@@ -887,7 +1022,6 @@ int fb_run_rounds(void* handle, int32_t first_round, int32_t count, double stop_
             CK(cudaGraphExecEventRecordNodeSetEvent(ctx->gexec, ctx->ev_node[e],
                                                     ctx->ev_pool[static_cast<size_t>(i) * EV_COUNT + e]));
       }
-      static const bool no_graph = getenv("FB_NO_GRAPH") && atoi(getenv("FB_NO_GRAPH"));
       if (no_graph) {  // diagnostics: the same round body, launched directly
         ctx->direct_pool = &ctx->ev_pool[static_cast<size_t>(i) * EV_COUNT];
         const int r2 = (ctx->cfg.algorithm == FB_ALG_PP) ? enqueue_pp_round(ctx) : enqueue_fednl_round(ctx);
@@ -982,7 +1116,6 @@ int fb_run_rounds(void* handle, int32_t first_round, int32_t count, double stop_
     }
   }
   cudaGetLastError();
-  for (auto& e : ends) cudaEventDestroy(e);
   cudaEventDestroy(t0);
   if (timed && timed_rounds > 0) {
     fb_profile& p = ctx->prof;

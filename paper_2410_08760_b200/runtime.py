@@ -169,6 +169,26 @@ def _validate(cfg: RunConfig, shards: list[ClientShard]) -> tuple[int, int, int]
     return n, d, ni
 
 
+def _update_bytes(cfg: RunConfig, d: int, kind: CompressorKind, counts: np.ndarray) -> np.ndarray:
+    """Sum over participants (count >= 0; PP marks absent clients -1) of the
+    CLIENT_UPDATE payload per round: update_payload_size(wire_size_bytes(count))
+    (transport.py:383-388, compressors.py:465-482), vectorised."""
+    c = counts.astype(np.int64)
+    part = c >= 0
+    w = packed_length(d)
+    if kind is CompressorKind.IDENTITY:
+        wire = np.full_like(c, 8 * w)
+    elif kind is CompressorKind.NATURAL:
+        wire = np.full_like(c, (12 * w + 7) // 8)
+    elif kind in (CompressorKind.RANDK, CompressorKind.RANDSEQK) and cfg.reconstruct_indices:
+        wire = 8 + 8 * c
+    else:
+        wire = 12 * c
+    wire = np.where(c == 0, 0, wire)
+    base = update_payload_size(cfg, d, 0)
+    return np.where(part, base + wire, 0).sum(axis=1)
+
+
 def simulate(cfg: RunConfig, shards: list[ClientShard], workers: int = 1,
              engine: FedNLEngine | None = None) -> list[MetricsRow]:
     """Single-process run over in-memory shards, every client on the GPU.
@@ -194,31 +214,24 @@ def simulate(cfg: RunConfig, shards: list[ClientShard], workers: int = 1,
         rows: list[MetricsRow] = []
         kind = cfg.compressor.kind
         stopped = False
+        # per-round uplink bytes of all participants, vectorised over clients
+        up_round = _update_bytes(cfg, d, kind, batch.entry_counts[: batch.done])
+        n_part = (batch.entry_counts[: batch.done] >= 0).sum(axis=1)
         for i in range(batch.done):
-            cnts = batch.entry_counts[i]
-            if cfg.is_pp:
-                part = cnts[cnts >= 0]
-                down += 8 * d * len(part)
-            else:
-                part = cnts
-                down += 8 * d * n
-            for c in part.tolist():
-                up += update_payload_size(cfg, d, wire_size_bytes(kind, d, int(c), cfg.reconstruct_indices))
-            if cfg.is_ls:  # runtime.py:203-208: every trial is traffic
-                trials = int(batch.ls_steps[i]) + 1
-                down += 8 * d * n * trials
-                up += 8 * n * trials
+            n_i = int(n_part[i]) if cfg.is_pp else n
             gn = float(batch.grad_norm[i])
             if cfg.is_pp and cfg.stop_grad_norm is not None and gn <= cfg.stop_grad_norm:
                 # runtime.py:239-242: the probe row is recorded before any traffic
-                if cfg.is_pp:
-                    down -= 8 * d * len(part)
-                    for c in part.tolist():
-                        up -= update_payload_size(cfg, d, wire_size_bytes(kind, d, int(c), cfg.reconstruct_indices))
                 rows.append(MetricsRow(i, t_init + batch.wall_ms[i] * 1e-3, gn, float(batch.f_value[i]),
                                        up, down, 0))
                 stopped = True
                 break
+            down += 8 * d * n_i
+            up += int(up_round[i])
+            if cfg.is_ls:  # runtime.py:203-208: every trial is traffic
+                trials = int(batch.ls_steps[i]) + 1
+                down += 8 * d * n * trials
+                up += 8 * n * trials
             rows.append(MetricsRow(i, t_init + batch.wall_ms[i] * 1e-3, gn, float(batch.f_value[i]),
                                    up, down, int(batch.ls_steps[i])))
             if (not cfg.is_pp) and cfg.stop_grad_norm is not None and gn <= cfg.stop_grad_norm:
