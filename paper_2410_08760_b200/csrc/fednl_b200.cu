@@ -724,6 +724,10 @@ int fb_create(const fb_config* cfg_in, void** out) {
                            static_cast<int>(HESS_SMEM)));
   CKC(cudaFuncSetAttribute(k_topk_smem, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            static_cast<int>(TKS_SMEM)));
+  static size_t max_fold = 0;
+  max_fold = std::max(max_fold, sizeof(int32_t) * (3 * static_cast<size_t>(c.n_clients) + 1));
+  CKC(cudaFuncSetAttribute(k_master_fold, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           static_cast<int>(max_fold)));
   CKC(cudaFuncSetAttribute(k_randk, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            static_cast<int>(2 * RK_TABLE * sizeof(int32_t))));
   CKC(cudaFuncSetAttribute(k_toplek, cudaFuncAttributeMaxDynamicSharedMemorySize,
