@@ -589,6 +589,415 @@ __global__ void __launch_bounds__(TK_THREADS, 1) k_topk_smem(
   }
 }
 
+// ------------------------------------------------- TopK, streaming path
+// For w > TKS_MAXW (c4: w = 524,800) the keys do not fit in shared memory,
+// so D is streamed from HBM, normally ONCE.  Streaming itself runs at HBM
+// speed (tools/probe/stream_bw.cu: 7.3 TB/s for this one-CTA-per-client
+// shape), so the pass is built to be lean in instructions per element:
+//  1. pivots: a strided sample of 2 * TK_THREADS keys is sorted in shared
+//     memory; ranks r -/+ delta around the expected rank of the k-th key give
+//     a window (H_lo, H_hi] of key high words that holds the k-th key with
+//     overwhelming probability;
+//  2. one pass over D: key high word above H_hi -> gt bit (a warp ballot is
+//     the bitmap word: no atomics); inside the window -> (key, position)
+//     appended to a per-client candidate list in global memory (one shared
+//     atomic per warp); exact zeros are tracked as a tie class when the
+//     window reaches down to zero (converged differences);
+//  3. radix levels on the candidate list find the k-th key (ties -> smaller
+//     position via the eq bitmap);
+//  4. word-per-lane selection sweeps (ascending positions), then the values
+//     pass with the client shift update.
+// If the window misses (G >= k, G + M (+ Z) < k, or M > TKST_CAP) the kernel
+// falls back to radix levels over D itself.  Selection rule as everywhere:
+// descending key, ties to the smaller position.
+// dynamic shared memory: gtm[wb] u32 | eqm[wb] u32 | hist[2048] u32 |
+//                        sample[2 * TK_THREADS] u64
+constexpr int TKST_CAP = 65536;  // candidates per client
+constexpr int TKST_SAMPLE = 2 * TK_THREADS;
+__host__ __device__ constexpr size_t tkst_smem_bytes(int64_t w) {
+  return 2 * static_cast<size_t>((w + 31) / 32) * 4 + 2048 * 4 + TKST_SAMPLE * 8;
+}
+constexpr int64_t TKST_MAXW = 700000;  // bitmaps + histogram + sample within 227 KB
+
+__device__ __forceinline__ uint32_t key_hi(double x, int64_t t, int weighted) {
+  return static_cast<uint32_t>(rank_key(x, t, weighted) >> 32);
+}
+
+// Radix levels over the candidate keys whose bits above `top` (exclusive)
+// all equal `prefix >> ...`: 11-bit digits from bit `top` down.  Returns the
+// threshold prefix / shift; need is reduced by the count above it.
+__device__ void tkst_resolve(const uint64_t* __restrict__ ck, int ncand, int top, int& need,
+                             uint32_t* hist, int* ws, int* s_digit, int* s_above,
+                             uint64_t* prefix_io, int* sh_out, bool* all) {
+  const int tid = threadIdx.x, lane = tid & 31;
+  uint64_t pf = *prefix_io;  // key >> (top + 1) of every candidate
+  int hi_excl = top + 1;     // bits >= hi_excl are fixed by pf
+  bool al = false;
+  int sh = 0;
+  while (true) {
+    const int bits = min(11, hi_excl);
+    sh = hi_excl - bits;
+    for (int i = tid; i < 2048; i += blockDim.x) hist[i] = 0u;
+    __syncthreads();
+    const uint32_t dmask = (1u << bits) - 1u;
+    for (int base = 0; base < ncand; base += 4 * blockDim.x) {
+      uint64_t kk[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int e = base + u * blockDim.x + tid;
+        kk[u] = e < ncand ? __ldcg(ck + e) : 0ull;
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int e = base + u * blockDim.x + tid;
+        uint32_t dig = 0xFFFFFFFFu;
+        if (e < ncand && (hi_excl >= 64 ? 0ull : (kk[u] >> hi_excl)) == pf)
+          dig = static_cast<uint32_t>(kk[u] >> sh) & dmask;
+        tks_add(hist, dig, lane);
+      }
+    }
+    __syncthreads();
+    tks_find_digit(hist, 1 << bits, need, ws, s_digit, s_above);
+    const int dg = *s_digit;
+    need -= *s_above;
+    pf = (pf << bits) | static_cast<uint64_t>(dg);
+    const int nbin = static_cast<int>(hist[dg]);
+    __syncthreads();
+    hi_excl = sh;
+    if (nbin == need) { al = true; break; }
+    if (sh == 0) break;
+  }
+  *prefix_io = pf;
+  *sh_out = sh;
+  *all = al;
+}
+
+__global__ void __launch_bounds__(TK_THREADS, 1) k_topk_stream(
+    const DevCtl* __restrict__ ctl, const double* __restrict__ D, int64_t w, int wb, int k,
+    int weighted, const int32_t* __restrict__ clients, const int32_t* __restrict__ flags,
+    uint32_t* __restrict__ bitmap, int32_t* __restrict__ count, uint32_t* __restrict__ idx_list,
+    double* __restrict__ val_list, int cap, int32_t* __restrict__ draws,
+    uint64_t* __restrict__ cand_key, int32_t* __restrict__ cand_pos, Emit em) {
+  if (ctl && ctl->halt) return;
+  PhaseClock pc;
+  extern __shared__ __align__(16) uint32_t tkst_dyn[];
+  const int wi = static_cast<int>(w);
+  uint32_t* gtm = tkst_dyn;        // [wb] selected (greater than the threshold)
+  uint32_t* eqm = gtm + wb;        // [wb] tied with the threshold key
+  uint32_t* hist = eqm + wb;       // [2048]
+  uint64_t* skey = reinterpret_cast<uint64_t*>(hist + 2048);  // [TKST_SAMPLE]
+  __shared__ int ws[64];
+  __shared__ int s_digit, s_above, s_ncand, s_G, s_Z, s_fail;
+  __shared__ int s_hhi, s_hlo, s_zero;
+  __shared__ int w_sel[TK_NW], w_eqc[TK_NW];
+  const int c = client_of(clients, blockIdx.x);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const double* v = D + static_cast<int64_t>(c) * w;
+  uint32_t* brow = bitmap + static_cast<int64_t>(c) * wb;
+  uint64_t* ck = cand_key + static_cast<int64_t>(c) * TKST_CAP;
+  int32_t* cp = cand_pos + static_cast<int64_t>(c) * TKST_CAP;
+  if (tid == 0 && draws) draws[c] = 0;
+  if (!(flags[c] & 2)) {
+    clear_row(brow, wb);
+    emit_empty(em, c);
+    if (tid == 0) count[c] = 0;
+    return;
+  }
+  // ---- 1. window from a strided sample (bitonic sort, descending)
+  {
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      const int i = u * TK_THREADS + tid;
+      const int64_t ts = (static_cast<int64_t>(i) * w) / TKST_SAMPLE;
+      skey[i] = rank_key(__ldg(v + ts), ts, weighted);
+    }
+    for (int i = tid; i < wb; i += TK_THREADS) eqm[i] = 0u;
+    __syncthreads();
+    for (int size = 2; size <= TKST_SAMPLE; size <<= 1) {
+      for (int stride = size >> 1; stride > 0; stride >>= 1) {
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+          const int i = u * TK_THREADS + tid;
+          const int j = i ^ stride;
+          if (j > i) {
+            const uint64_t a = skey[i], b = skey[j];
+            const bool desc = (i & size) == 0;
+            if (desc ? (a < b) : (a > b)) { skey[i] = b; skey[j] = a; }
+          }
+        }
+        __syncthreads();
+      }
+    }
+    if (tid == 0) {
+      const double r = static_cast<double>(k) * TKST_SAMPLE / static_cast<double>(w);
+      const int delta = static_cast<int>(4.0 * sqrt(r) + 16.0);
+      const int ri = static_cast<int>(r);
+      const int r_hi = ri - delta, r_lo = ri + delta;
+      // high words: gt iff hk > hhi; candidate iff hlo < hk <= hhi (signed)
+      int hhi = r_hi >= 0 ? static_cast<int>(skey[r_hi] >> 32) : 0x7FFFFFFF;
+      int hlo = r_lo < TKST_SAMPLE ? static_cast<int>(skey[r_lo] >> 32) - 1 : -1;
+      if (hlo >= hhi) hlo = hhi - 1;
+      // exact zeros become a tie class when the window reaches them
+      s_zero = hlo < 0;
+      if (hlo < 0) hlo = -1;
+      s_hhi = hhi;
+      s_hlo = hlo;
+      s_ncand = 0;
+      s_G = 0;
+      s_Z = 0;
+      s_fail = 0;
+    }
+    __syncthreads();
+  }
+  pc.mark(0);
+  const int hhi = s_hhi, hlo = s_hlo;
+  const bool track_zero = s_zero;
+  // ---- 2. one classification pass over D
+  constexpr int UNR = 8;
+  {
+    int z_acc = 0;
+    for (int base = 0; base < wi; base += UNR * TK_THREADS) {
+      double x[UNR];
+#pragma unroll
+      for (int u = 0; u < UNR; ++u) {
+        const int t = base + u * TK_THREADS + tid;
+        x[u] = (t < wi) ? __ldcs(v + t) : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < UNR; ++u) {
+        const int t = base + u * TK_THREADS + tid;
+        const uint64_t key = rank_key(x[u], t, weighted);
+        const int hk = (t < wi) ? static_cast<int>(key >> 32) : -2;
+        const bool gt = hk > hhi;
+        bool mid = hk > hlo && hk <= hhi;
+        if (track_zero) {
+          const bool z = t < wi && key == 0ull;
+          mid = mid && !z;
+          const uint32_t zb = __ballot_sync(0xffffffffu, z);
+          if (lane == 0 && t - lane < wi) { eqm[t >> 5] = zb; z_acc += __popc(zb); }
+        }
+        const uint32_t gb = __ballot_sync(0xffffffffu, gt);
+        const uint32_t mb = __ballot_sync(0xffffffffu, mid);
+        if (lane == 0 && t - lane < wi) gtm[t >> 5] = gb;  // the word is owned by this warp
+        if (mb) {
+          int wbase = 0;
+          if (lane == 0) wbase = atomicAdd(&s_ncand, __popc(mb));
+          wbase = __shfl_sync(0xffffffffu, wbase, 0);
+          if (mid) {
+            const int slot = wbase + __popc(mb & ((1u << lane) - 1u));
+            if (slot < TKST_CAP) {
+              ck[slot] = key;
+              cp[slot] = t;
+            }
+          }
+        }
+      }
+    }
+    if (track_zero && lane == 0) atomicAdd(&s_Z, z_acc);
+    __syncthreads();
+    // G = number of gt bits (a cheap sweep over the bitmap)
+    int g = 0;
+    for (int q = tid; q < wb; q += TK_THREADS) g += __popc(gtm[q]);
+    g = warp_sum_int(g);
+    if (lane == 0) atomicAdd(&s_G, g);
+    __syncthreads();
+  }
+  pc.mark(1);
+  // ---- 3. decide where the k-th key is
+  int need = k;  // after this block: number of eq-class keys to take by position
+  {
+    const int G = s_G, M = s_ncand, Z = track_zero ? s_Z : 0;
+    const bool ok = G < k && G + M + Z >= k && M <= TKST_CAP;
+    if (ok && G + M >= k) {
+      // the k-th key is a candidate; zeros (if tracked) are not needed
+      if (track_zero)
+        for (int i = tid; i < wb; i += TK_THREADS) eqm[i] = 0u;
+      need = k - G;
+      __syncthreads();
+      const int top = 32 + (31 - __clz(static_cast<unsigned>((hlo + 1) ^ hhi) | 1u));
+      uint64_t pf = static_cast<uint64_t>(static_cast<uint32_t>(hhi)) >> (top - 31);
+      int sh;
+      bool all;
+      tkst_resolve(ck, M, top, need, hist, ws, &s_digit, &s_above, &pf, &sh, &all);
+      for (int e = tid; e < M; e += TK_THREADS) {
+        const uint64_t hp = __ldcg(ck + e) >> sh;
+        const int t = __ldcg(cp + e);
+        if (hp > pf || (all && hp == pf)) atomicOr(&gtm[t >> 5], 1u << (t & 31));
+        else if (hp == pf) atomicOr(&eqm[t >> 5], 1u << (t & 31));
+      }
+      if (all) need = 0;
+      __syncthreads();
+    } else if (ok) {
+      // every candidate is taken; the first k - G - M zeros complete the set
+      for (int e = tid; e < M; e += TK_THREADS) {
+        const int t = __ldcg(cp + e);
+        atomicOr(&gtm[t >> 5], 1u << (t & 31));
+      }
+      need = k - G - M;
+      __syncthreads();
+    } else {
+      // the window missed: radix levels over D itself
+      if (tid == 0) s_fail = 1;
+      constexpr int NL = 6;
+      constexpr int SH[NL] = {52, 41, 30, 19, 8, 0};
+      constexpr int BI[NL] = {11, 11, 11, 11, 11, 8};
+      uint64_t prefix = 0;
+      int L = 0;
+      bool take_all = false;
+      for (; L < NL; ++L) {
+        for (int i = tid; i < 2048; i += TK_THREADS) hist[i] = 0u;
+        __syncthreads();
+        const int sh = SH[L], up = (L == 0) ? 63 : SH[L - 1];
+        const uint32_t dmask = (1u << BI[L]) - 1u;
+        for (int t = tid; t < wi; t += TK_THREADS) {
+          const uint64_t key = rank_key(__ldcs(v + t), t, weighted);
+          uint32_t dig = 0xFFFFFFFFu;
+          if ((up >= 63 ? 0ull : (key >> up)) == prefix) dig = static_cast<uint32_t>(key >> sh) & dmask;
+          tks_add(hist, dig, lane);
+        }
+        __syncthreads();
+        tks_find_digit(hist, 1 << BI[L], need, ws, &s_digit, &s_above);
+        const int dg = s_digit;
+        need -= s_above;
+        prefix = (prefix << BI[L]) | static_cast<uint64_t>(dg);
+        const int nbin = static_cast<int>(hist[dg]);
+        __syncthreads();
+        if (nbin == need) { take_all = true; break; }
+      }
+      if (L == NL) L = NL - 1;
+      const int sh = SH[L];
+      for (int base = 0; base < wi; base += TK_THREADS) {
+        const int t = base + tid;
+        bool gt = false, eq = false;
+        if (t < wi) {
+          const uint64_t hp = rank_key(__ldcs(v + t), t, weighted) >> sh;
+          gt = take_all ? hp >= prefix : hp > prefix;
+          eq = !take_all && hp == prefix;
+        }
+        const uint32_t gb = __ballot_sync(0xffffffffu, gt), eb = __ballot_sync(0xffffffffu, eq);
+        if (lane == 0 && t - lane < wi) { gtm[t >> 5] = gb; eqm[t >> 5] = eb; }
+      }
+      if (take_all) need = 0;
+      __syncthreads();
+    }
+  }
+  pc.mark(2);
+  // ---- 4. selection: lane = one bitmap word; a warp covers 32 words per step
+  //         and owns the contiguous word range [warp * SW, (warp + 1) * SW)
+  const int SW = (wb + TK_NW - 1) / TK_NW;
+  const int q0 = warp * SW, q1 = min(wb, q0 + SW);
+  {
+    int ns = 0, ne = 0;
+    for (int q = q0 + lane; q < q1; q += 32) {
+      ns += __popc(gtm[q]);
+      ne += __popc(eqm[q]);
+    }
+    ns = warp_sum_int(ns);
+    ne = warp_sum_int(ne);
+    if (lane == 0) { w_sel[warp] = ns; w_eqc[warp] = ne; }
+  }
+  __syncthreads();
+  if (warp == 0) {
+    const int g = w_sel[lane], e = w_eqc[lane];
+    int e_incl = e;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, e_incl, o);
+      if (lane >= o) e_incl += y;
+    }
+    const int e_excl = e_incl - e;
+    const int e_take = max(0, min(need - e_excl, e));
+    const int sel = g + e_take;
+    int s_incl = sel;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, s_incl, o);
+      if (lane >= o) s_incl += y;
+    }
+    w_sel[lane] = s_incl - sel;  // exclusive selected prefix
+    w_eqc[lane] = e_excl;        // exclusive tied prefix
+    if (lane == 31) s_above = s_incl;
+  }
+  __syncthreads();
+  const int total = s_above;
+  uint32_t* il = idx_list + static_cast<int64_t>(c) * cap;
+  double* vl = val_list + static_cast<int64_t>(c) * cap;
+  int32_t* rsc = em.rs ? em.rs + static_cast<int64_t>(c) * (em.nr + 1) : nullptr;
+  {
+    int base_sel = w_sel[warp], base_eq = w_eqc[warp];
+    for (int qb = q0; qb < q1; qb += 32) {
+      const int q = qb + lane;
+      uint32_t gb = 0u, eb = 0u;
+      if (q < q1) { gb = gtm[q]; eb = eqm[q]; }
+      const int ne = __popc(eb);
+      int e_pre = ne;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, e_pre, o);
+        if (lane >= o) e_pre += y;
+      }
+      const int e_tot = __shfl_sync(0xffffffffu, e_pre, 31);
+      e_pre -= ne;
+      int take = max(0, min(need - (base_eq + e_pre), ne));
+      uint32_t sel = gb;
+      for (uint32_t m = eb; take > 0; --take) {
+        const uint32_t low = m & (0u - m);
+        sel |= low;
+        m ^= low;
+      }
+      const int ns = __popc(sel);
+      int s_pre = ns;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, s_pre, o);
+        if (lane >= o) s_pre += y;
+      }
+      const int s_tot = __shfl_sync(0xffffffffu, s_pre, 31);
+      s_pre -= ns;
+      int pos = base_sel + s_pre;
+      if (q < q1) {
+        if (rsc && (q % (FOLD_RANGE / 32)) == 0) rsc[q / (FOLD_RANGE / 32)] = pos;
+        brow[q] = sel;
+        for (uint32_t m = sel; m; m &= m - 1) il[pos++] = static_cast<uint32_t>(q * 32 + __ffs(m) - 1);
+      }
+      base_sel += s_tot;
+      base_eq += e_tot;
+    }
+  }
+  if (tid == 0) {
+    count[c] = total;
+    if (rsc) rsc[em.nr] = total;
+  }
+  __syncthreads();
+  pc.mark(3);
+  // ---- values and the client shift update: 8 independent entries per thread
+  for (int e0 = 0; e0 < total; e0 += 8 * TK_THREADS) {
+    int64_t tt[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int e = e0 + u * TK_THREADS + tid;
+      tt[u] = e < total ? static_cast<int64_t>(__ldcg(il + e)) : -1;
+    }
+    double vv[8], hv[8];
+    double* hrow = em.hest ? em.hest + static_cast<int64_t>(c) * em.hest_stride : nullptr;
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      vv[u] = tt[u] >= 0 ? __ldg(v + tt[u]) : 0.0;
+      hv[u] = (hrow && tt[u] >= 0) ? hrow[tt[u]] : 0.0;  // positions are distinct
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int e = e0 + u * TK_THREADS + tid;
+      if (tt[u] >= 0) {
+        vl[e] = vv[u];
+        if (hrow) hrow[tt[u]] = __dadd_rn(hv[u], __dmul_rn(em.alpha, vv[u]));  // emit_entry
+      }
+    }
+  }
+  pc.mark(4);
+  if (g_dbg_on && tid == 0 && s_fail) atomicAdd(reinterpret_cast<unsigned long long*>(&g_dbg[17]), 1ull);
+}
+
 // --------------------------------------------------------------- RandSeqK
 // grid n_active, block 256.  s = randrange(w) is the first and only draw
 // (compressors.py:259-264); positions (s + j) mod w, sorted.

@@ -82,6 +82,8 @@ struct Ctx {
   uint32_t* idx_list = nullptr;
   double* val_list = nullptr;
   int64_t* jbuf = nullptr;
+  uint64_t* cand_key = nullptr;  // TopK streaming path: threshold-bin candidates
+  int32_t* cand_pos = nullptr;
   uint64_t* seeds = nullptr;
   RoundScalars* sc = nullptr;
   double *steps_table = nullptr, *trial_x = nullptr, *ls_loss_part = nullptr;
@@ -288,6 +290,11 @@ int launch_compress(Ctx* ctx, cudaStream_t s, const int32_t* clients, int n_acti
         k_topk_smem<<<n_active, TK_THREADS, tks_smem_bytes(ctx->w), s>>>(
             ctl, ctx->D, ctx->w, ctx->wb, c.k, c.topk_weighted, clients, ctx->flags, ctx->bitmap,
             ctx->count, ctx->idx_list, ctx->val_list, ctx->cap, ctx->draws, em);
+      else if (ctx->w <= TKST_MAXW)
+        k_topk_stream<<<n_active, TK_THREADS, tkst_smem_bytes(ctx->w), s>>>(
+            ctl, ctx->D, ctx->w, ctx->wb, c.k, c.topk_weighted, clients, ctx->flags, ctx->bitmap,
+            ctx->count, ctx->idx_list, ctx->val_list, ctx->cap, ctx->draws, ctx->cand_key,
+            ctx->cand_pos, em);
       else
         k_topk<<<n_active, TK_THREADS, 0, s>>>(ctl, ctx->D, ctx->w, ctx->wb, c.k, c.topk_weighted,
                                                clients, ctx->flags, ctx->bitmap, ctx->count,
@@ -724,6 +731,8 @@ int fb_create(const fb_config* cfg_in, void** out) {
                            static_cast<int>(HESS_SMEM)));
   CKC(cudaFuncSetAttribute(k_topk_smem, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            static_cast<int>(TKS_SMEM)));
+  CKC(cudaFuncSetAttribute(k_topk_stream, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           static_cast<int>(tkst_smem_bytes(TKST_MAXW))));
   static size_t max_fold = 0;
   max_fold = std::max(max_fold, sizeof(int32_t) * (3 * static_cast<size_t>(c.n_clients) + 1));
   CKC(cudaFuncSetAttribute(k_master_fold, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -739,6 +748,7 @@ int fb_create(const fb_config* cfg_in, void** out) {
 
   const int n = ctx->n, d = ctx->d;
   const size_t wn = static_cast<size_t>(w) * n;
+  const bool stream_topk = c.kind == FB_KIND_TOPK && w > TKS_MAXW && w <= TKST_MAXW;
   const int tau = ctx->tau;
   if (dalloc(ctx, &ctx->ctl, 1) || dalloc(ctx, &ctx->Bt, static_cast<size_t>(n) * d * ctx->ldj) ||
       dalloc(ctx, &ctx->x, d) || dalloc(ctx, &ctx->x_new, d) || dalloc(ctx, &ctx->pvec, d) ||
@@ -749,7 +759,7 @@ int fb_create(const fb_config* cfg_in, void** out) {
       dalloc(ctx, &ctx->grad, static_cast<size_t>(n) * d) || dalloc(ctx, &ctx->gbar, d) ||
       dalloc(ctx, &ctx->f_cli, n) || dalloc(ctx, &ctx->shift_cli, n) ||
       dalloc(ctx, &ctx->frob_part, static_cast<size_t>(n) * ctx->n_pairs) ||
-      dalloc(ctx, &ctx->flags, n) || dalloc(ctx, &ctx->hest, wn) || dalloc(ctx, &ctx->D, wn) ||
+      dalloc(ctx, &ctx->flags, n) || dalloc(ctx, &ctx->hest, wn) || dalloc(ctx, &ctx->D, wn + 2) ||
       dalloc(ctx, &ctx->hmas, w) || dalloc(ctx, &ctx->hmas2, w) || dalloc(ctx, &ctx->zeros_w, w) ||
       dalloc(ctx, &ctx->rs, static_cast<size_t>(n) * (ctx->nr + 1)) ||
       dalloc(ctx, &ctx->M, static_cast<size_t>(d + 1) * (d + 1)) ||
@@ -758,6 +768,8 @@ int fb_create(const fb_config* cfg_in, void** out) {
       dalloc(ctx, &ctx->idx_list, static_cast<size_t>(n) * ctx->cap) ||
       dalloc(ctx, &ctx->val_list, static_cast<size_t>(n) * ctx->cap) ||
       dalloc(ctx, &ctx->jbuf, static_cast<size_t>(n) * ctx->cap) || dalloc(ctx, &ctx->seeds, n) ||
+      dalloc(ctx, &ctx->cand_key, stream_topk ? static_cast<size_t>(n) * TKST_CAP : 1) ||
+      dalloc(ctx, &ctx->cand_pos, stream_topk ? static_cast<size_t>(n) * TKST_CAP : 1) ||
       dalloc(ctx, &ctx->sc, 1) || dalloc(ctx, &ctx->steps_table, 64) ||
       dalloc(ctx, &ctx->trial_x, static_cast<size_t>(LS_BATCH) * d) ||
       dalloc(ctx, &ctx->ls_loss_part, static_cast<size_t>(LS_BATCH) * n * ctx->ls_nblk) ||

@@ -147,6 +147,30 @@ def test_compressors_bit_exact_at_c0_size(kind, k):
         assert np.array_equal(got[c].values, want.values), c
 
 
+@pytest.mark.parametrize("k", [8192, 1, 524800])
+def test_topk_streaming_path_bit_exact_at_c4_size(k):
+    """w = 524,800 (c4) runs the streaming TopK (keys do not fit in shared
+    memory): candidate path, exact-tie path, zero ties, take-all."""
+    d = 1024
+    w = O.packed_len(d)
+    rng = np.random.default_rng(23)
+    P = rng.standard_normal((7, w))
+    P[1] = np.round(P[1] * 4) / 4  # few distinct values: huge exact-tie bins
+    P[2] = 0.0  # empty delta
+    P[3, ::3] = 0.0
+    P[4] = 1.0 + rng.random(w)  # one exponent: the candidate list decides
+    P[5] = 0.0
+    P[5, rng.choice(w, 100, replace=False)] = rng.standard_normal(100)  # zeros complete the set
+    P[6] = P[0] * 1e-300  # subnormal-heavy keys
+    seeds = [O.round_seed(3, c, 1) for c in range(7)]
+    got = leaf.compress_packed_batch(P, d, CompressorSpec(CompressorKind.TOPK, k=k), seeds)
+    for c in range(7):
+        want = O.compress_packed(P[c], d, "topk", k, O.SplitMix64(seeds[c]))
+        assert got[c].entry_count == want.count, c
+        assert np.array_equal(got[c].indices, want.indices), c
+        assert np.array_equal(got[c].values, want.values), c
+
+
 def test_toplek_bit_exact_at_c2_size():
     d = 69
     w = O.packed_len(d)
