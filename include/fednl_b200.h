@@ -186,9 +186,12 @@ int fb_shifted_solve(void* ctx, const double* h_packed, double shift, const doub
                      double* z);
 
 /* diagnostic: per-phase clock64 cycles of one shifted solve on the rank-0
- * CTA (12 slots: setup, A, syncA, pull, B, B-writeback, C, syncC,
- * back-solve, back-total, -, -), optional cluster-size
- * override (0 = default) and its event time in ms */
+ * CTA.  cluster > 0: the cluster-redundant solver with that cluster size,
+ * 12 slots (setup, A, syncA, pull, B, B-writeback, C, syncC, back-solve,
+ * back-total, -, -).  cluster == 0: the default solver; for the
+ * panel-owning solver cycles must hold 16 + 64 * 16 slots (16 phase slots,
+ * then per-panel globaltimer stamps).  ms = event time of an uninstrumented
+ * run of the same solve. */
 int fb_solve_phase_cycles(void* ctx, const double* h_packed, double shift, const double* rhs,
                           int32_t cluster, long long* cycles, float* ms);
 

@@ -58,6 +58,9 @@ struct Ctx {
   int64_t w = 0;
   double alpha_n = 0.0, rand_scale = 1.0;
   int solve_cs = 1, solve_nb = 32;
+  bool solve_panels = false;  // k_chol_panels (d <= CP_MAX_D) instead of k_chol_solve
+  int cp_kp = 1, cp_cs = 1;
+  double* Lg = nullptr;       // k_chol_panels: released L panels
   int prio_high = 0;
   cudaEvent_t* direct_pool = nullptr;  // non-null: record() targets these (FB_NO_GRAPH)
   size_t solve_smem = 0;
@@ -333,39 +336,48 @@ int launch_compress(Ctx* ctx, cudaStream_t s, const int32_t* clients, int n_acti
 }
 int launch_solve(Ctx* ctx, cudaStream_t s, const double* hpk, const double* shift_ptr,
                  const double* rhs, const double* x, double* z, double* x_out, int mode,
-                 int ignore_halt, long long* dbg = nullptr, cudaEvent_t launched = nullptr) {
+                 int ignore_halt, long long* dbg = nullptr, cudaEvent_t launched = nullptr,
+                 bool force_old = false) {
+  const bool panels = ctx->solve_panels && !force_old;
+  const int cs = panels ? ctx->cp_cs : ctx->solve_cs;
   cudaLaunchConfig_t lc{};
-  lc.gridDim = dim3(ctx->solve_cs);
+  lc.gridDim = dim3(cs);
   lc.blockDim = dim3(CH_THREADS);
-  lc.dynamicSmemBytes = ctx->solve_smem;
+  lc.dynamicSmemBytes = panels ? static_cast<size_t>(ctx->cp_kp) * cp_panel_bytes(ctx->d) : ctx->solve_smem;
   lc.stream = s;
-  cudaLaunchAttribute attr[2];
+  cudaLaunchAttribute attr[3];
   attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = ctx->solve_cs;
+  attr[0].val.clusterDim.x = cs;
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
-  // the solve is the round's critical path and needs solve_cs SMs at once:
+  // the solve is the round's critical path and needs cs SMs at once:
   // schedule its cluster ahead of the concurrent compressor's CTAs
   attr[1].id = cudaLaunchAttributePriority;
   attr[1].val.priority = ctx->prio_high;
   lc.attrs = attr;
   lc.numAttrs = 2;
-  cudaLaunchAttribute attr3[3] = {attr[0], attr[1], {}};
   if (launched) {
     // fires once every CTA of the cluster is resident: the concurrent
     // compressor is held back until then, so the solve never waits for SMs
-    attr3[2].id = cudaLaunchAttributeLaunchCompletionEvent;
-    attr3[2].val.launchCompletionEvent.event = launched;
-    attr3[2].val.launchCompletionEvent.flags = 0;
-    lc.attrs = attr3;
+    attr[2].id = cudaLaunchAttributeLaunchCompletionEvent;
+    attr[2].val.launchCompletionEvent.event = launched;
+    attr[2].val.launchCompletionEvent.flags = 0;
     lc.numAttrs = 3;
   }
-  if (ctx->solve_nb == 32)
+  if (panels) {
+    if (ctx->cp_kp == 1)
+      CK(cudaLaunchKernelEx(&lc, k_chol_panels<1>, ctx->ctl, ctx->d, hpk, shift_ptr, rhs, x, ctx->Lg,
+                            z, x_out, mode, ignore_halt, dbg));
+    else
+      CK(cudaLaunchKernelEx(&lc, k_chol_panels<2>, ctx->ctl, ctx->d, hpk, shift_ptr, rhs, x, ctx->Lg,
+                            z, x_out, mode, ignore_halt, dbg));
+  } else if (ctx->solve_nb == 32) {
     CK(cudaLaunchKernelEx(&lc, k_chol_solve<32>, ctx->ctl, ctx->d, hpk, shift_ptr, rhs, x, ctx->M,
                           z, x_out, mode, ignore_halt, dbg));
-  else
+  } else {
     CK(cudaLaunchKernelEx(&lc, k_chol_solve<16>, ctx->ctl, ctx->d, hpk, shift_ptr, rhs, x, ctx->M,
                           z, x_out, mode, ignore_halt, dbg));
+  }
   return FB_OK;
 }
 bool dense_kind(const Ctx* ctx) {
@@ -684,6 +696,17 @@ int fb_create(const fb_config* cfg_in, void** out) {
   ctx->solve_cs = c.d < 128 ? 1 : (c.d < 512 ? 6 : CH_MAX_CLUSTER);
   if (const char* e = getenv("FB_SOLVE_CLUSTER")) ctx->solve_cs = std::max(1, std::min(8, atoi(e)));
   ctx->solve_nb = solve_panel_bytes<32>(c.d) <= 190 * 1024 ? 32 : 16;
+  {
+    // panel-owning solve: one or two 32-column panels per CTA of a portable
+    // (<= 8) cluster, while the panels fit in shared memory
+    const int npan = (c.d + CP_NB - 1) / CP_NB;
+    ctx->cp_kp = npan <= CH_MAX_CLUSTER ? 1 : 2;
+    ctx->cp_cs = (npan + ctx->cp_kp - 1) / ctx->cp_kp;
+    // (three panels or fewer: the cluster-redundant solver is faster)
+    ctx->solve_panels = npan >= 4 && c.d <= CP_MAX_D && ctx->cp_cs <= CH_MAX_CLUSTER &&
+                        static_cast<size_t>(ctx->cp_kp) * cp_panel_bytes(c.d) <= 196 * 1024 &&
+                        !(getenv("FB_SOLVE_OLD") && atoi(getenv("FB_SOLVE_OLD")));
+  }
   ctx->solve_smem = ctx->solve_nb == 32 ? solve_panel_bytes<32>(c.d) : solve_panel_bytes<16>(c.d);
   int rc = FB_OK;
   auto fail = [&](int code) {
@@ -743,6 +766,12 @@ int fb_create(const fb_config* cfg_in, void** out) {
                            static_cast<int>(max_toplek)));
   CKC(cudaFuncSetAttribute(k_chol_solve<32>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            static_cast<int>(std::max(max_solve, solve_panel_bytes<32>(1)))));
+  static size_t max_cp = 0;
+  max_cp = std::max(max_cp, static_cast<size_t>(ctx->cp_kp) * cp_panel_bytes(c.d));
+  CKC(cudaFuncSetAttribute(k_chol_panels<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           static_cast<int>(std::min<size_t>(max_cp, 196 * 1024))));
+  CKC(cudaFuncSetAttribute(k_chol_panels<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           static_cast<int>(std::min<size_t>(max_cp, 196 * 1024))));
   CKC(cudaFuncSetAttribute(k_chol_solve<16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            static_cast<int>(std::max(max_solve, solve_panel_bytes<16>(1)))));
 
@@ -763,6 +792,8 @@ int fb_create(const fb_config* cfg_in, void** out) {
       dalloc(ctx, &ctx->hmas, w) || dalloc(ctx, &ctx->hmas2, w) || dalloc(ctx, &ctx->zeros_w, w) ||
       dalloc(ctx, &ctx->rs, static_cast<size_t>(n) * (ctx->nr + 1)) ||
       dalloc(ctx, &ctx->M, static_cast<size_t>(d + 1) * (d + 1)) ||
+      dalloc(ctx, &ctx->Lg, ctx->solve_panels ? static_cast<size_t>((d + CP_NB - 1) / CP_NB) *
+                                                    cp_rows(d) * CP_LS : 1) ||
       dalloc(ctx, &ctx->bitmap, static_cast<size_t>(n) * ctx->wb) || dalloc(ctx, &ctx->count, n) ||
       dalloc(ctx, &ctx->draws, n) ||
       dalloc(ctx, &ctx->idx_list, static_cast<size_t>(n) * ctx->cap) ||
@@ -1392,22 +1423,34 @@ int fb_solve_phase_cycles(void* handle, const double* h_packed, double shift, co
   const int saved = ctx->solve_cs;
   if (cluster > 0) ctx->solve_cs = cluster;
   long long* dbg = nullptr;
-  CK(cudaMalloc(&dbg, 12 * sizeof(long long)));
-  CK(cudaMemset(dbg, 0, 12 * sizeof(long long)));
+  constexpr int NDBG = 16 + 64 * 16;  // phase cycles + per-panel timestamps
+  CK(cudaMalloc(&dbg, NDBG * sizeof(long long)));
+  CK(cudaMemset(dbg, 0, NDBG * sizeof(long long)));
   CK(cudaMemcpyAsync(ctx->D, h_packed, sizeof(double) * ctx->w, cudaMemcpyHostToDevice, s));
   CK(cudaMemcpyAsync(ctx->scalar, &shift, sizeof(double), cudaMemcpyHostToDevice, s));
   CK(cudaMemcpyAsync(ctx->zbuf, rhs, sizeof(double) * ctx->d, cudaMemcpyHostToDevice, s));
-  TRY(launch_solve(ctx, s, ctx->D, ctx->scalar, ctx->zbuf, nullptr, ctx->pvec, nullptr, 2, 1));
+  const bool old = cluster > 0;
+  TRY(launch_solve(ctx, s, ctx->D, ctx->scalar, ctx->zbuf, nullptr, ctx->pvec, nullptr, 2, 1, nullptr,
+                   nullptr, old));
   CK(cudaStreamSynchronize(s));
   cudaEvent_t e0, e1;
   CK(cudaEventCreate(&e0));
   CK(cudaEventCreate(&e1));
-  CK(cudaEventRecord(e0, s));
-  TRY(launch_solve(ctx, s, ctx->D, ctx->scalar, ctx->zbuf, nullptr, ctx->pvec, nullptr, 2, 1, dbg));
-  CK(cudaEventRecord(e1, s));
+  // plain timing first (no instrumentation), then the instrumented run
+  float plain_ms = 0.f;
+  for (int rep = 0; rep < 2; ++rep) {
+    CK(cudaEventRecord(e0, s));
+    TRY(launch_solve(ctx, s, ctx->D, ctx->scalar, ctx->zbuf, nullptr, ctx->pvec, nullptr, 2, 1,
+                     rep ? dbg : nullptr, nullptr, old));
+    CK(cudaEventRecord(e1, s));
+    if (rep == 0) {
+      CK(cudaStreamSynchronize(s));
+      CK(cudaEventElapsedTime(&plain_ms, e0, e1));
+    }
+  }
   CK(cudaStreamSynchronize(s));
-  if (ms) CK(cudaEventElapsedTime(ms, e0, e1));
-  CK(cudaMemcpy(cycles, dbg, 12 * sizeof(long long), cudaMemcpyDeviceToHost));
+  if (ms) *ms = plain_ms;
+  CK(cudaMemcpy(cycles, dbg, (cluster == 0 ? NDBG : 12) * sizeof(long long), cudaMemcpyDeviceToHost));
   cudaFree(dbg);
   cudaEventDestroy(e0);
   cudaEventDestroy(e1);

@@ -44,15 +44,6 @@ __device__ __forceinline__ int swz(int r, int s) {
   return r * HKC + ((((s >> 1) ^ (r & 7)) << 1) | (s & 1));
 }
 
-__device__ __forceinline__ void dmma_8x8x4(double (&c)[2], double a, double b) {
-  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
-               : "+d"(c[0]), "+d"(c[1])
-               : "d"(a), "d"(b));
-}
-
-__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
-}
 
 // grid (n_pairs, n_active), block HTHREADS, dynamic smem HESS_SMEM.
 // Warps 0..3 compute (warp q owns quadrant rows 32*(q&1), cols 32*(q>>1));

@@ -331,3 +331,441 @@ __global__ void __launch_bounds__(CH_THREADS, 1) k_chol_solve(
 }
 
 }  // namespace fb
+
+namespace fb {
+
+// ===========================================================================
+// k_chol_panels — panel-owning blocked Cholesky for d <= CP_MAX_D.
+//
+// The matrix is cut into 32-column panels; panel p lives in the shared
+// memory of cluster CTA p % cs (KP = 1 or 2 panels per CTA), as rows
+// ("slots") i - p0 of columns [p0, p0 + 32) of the lower triangle plus the
+// right-hand side as a final slot (the forward substitution rides along).
+// Per panel p its owner
+//   A  factors the 32 x 32 diagonal block (warp 0) and forms T = L_pp^-1,
+//      while its other warps finish the pending update of the panel's lower
+//      rows from panel p - 1,
+//   B  solves the rows below the block, X = A T^T, on the fp64 tensor cores
+//      (mma.sync m8n8k4 / DMMA), writes L_p to global memory and releases it
+//      to every CTA through a cluster-scope mbarrier arrive.
+// Every CTA applies L_p to its own later panels as soon as it is released
+// (C_q -= L_p L_p^T restricted to panel q, DMMA, operands from L2) — the
+// panel that is factored next gets its diagonal rows first (lookahead), so
+// the critical path per panel is one release + 4 DMMA row tiles + the block
+// factor + the TRSM.  The backward substitution runs panel by panel from the
+// last: the owner of panel b forms z_b = T_b^T (y_b - w_b), where w_b was
+// accumulated from the z of later panels as they were released, and pushes
+// z_b into every CTA over DSMEM.
+//
+// The factorisation order differs from the reference's column loop
+// (linalg.py:151-170); results agree to rounding (parity bar 1e-10).  The
+// first pivot that is <= 0 or not finite raises NotPositiveDefiniteError
+// (index, value) semantics, pivots being produced in index order.
+// ===========================================================================
+constexpr int CP_NB = 32;
+constexpr int CP_LS = 36;  // slot stride (doubles): conflict-free DMMA fragment loads
+constexpr int CP_MAXP = 16;
+constexpr int CP_MAX_D = CP_MAXP * CP_NB;
+
+struct CpSmem {
+  double T[2][CP_NB][CP_LS];  // inverse diagonal blocks of the own panels
+  double z[CP_MAX_D];         // solution entries released so far
+  double w[2][CP_NB];         // back-substitution accumulators of the own panels
+  double part[8][CP_NB];
+  double inv[CP_NB];
+  uint64_t barL[CP_MAXP], barZ[CP_MAXP];
+  int failed;
+};
+
+__host__ __device__ constexpr int cp_rows(int d) { return (d > CP_NB ? d : CP_NB) + 1; }
+__host__ __device__ constexpr size_t cp_panel_bytes(int d) {
+  return static_cast<size_t>(cp_rows(d)) * CP_LS * sizeof(double);
+}
+
+// C_q[slots] -= L_p[rows] L_p[jrows]^T for q's slots in [s_lo, s_hi] (row
+// tiles of 8, warps [w_lo, w_hi) round robin).  L_p is read from global
+// (__ldcg: written by another SM during this launch) or from local shared
+// memory.
+template <bool GLOBAL>
+__device__ __forceinline__ void cp_update(const double* __restrict__ Lp, int p, int q,
+                                          double* __restrict__ Pq, int d, int s_lo, int s_hi,
+                                          int w_lo, int w_hi) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (warp < w_lo || warp >= w_hi) return;
+  const int p0 = p * CP_NB, q0 = q * CP_NB;
+  const int nreal_q = d - q0, rs_q = max(nreal_q, CP_NB), rs_p = max(d - p0, CP_NB);
+  const int off = q0 - p0;
+  auto ld = [&](int slot, int col) -> double {
+    const double* a = Lp + static_cast<int64_t>(slot) * CP_LS + col;
+    return GLOBAL ? __ldcg(a) : *a;
+  };
+  // B fragments: b = L_p[j][k], j = q0 + 8 ct + (lane >> 2), k = 4 ks + (lane & 3)
+  double b[8][4];
+#pragma unroll
+  for (int ct = 0; ct < 4; ++ct) {
+    const int jj = ct * 8 + (lane >> 2);
+    const bool ok = q0 + jj < d;
+#pragma unroll
+    for (int ks = 0; ks < 8; ++ks) b[ks][ct] = ok ? ld(off + jj, ks * 4 + (lane & 3)) : 0.0;
+  }
+  const int t_lo = s_lo >> 3, t_hi = s_hi >> 3;
+  for (int tile = t_lo + (warp - w_lo); tile <= t_hi; tile += (w_hi - w_lo)) {
+    const int r = tile * 8 + (lane >> 2);  // this lane's A row slot
+    int src = -1;
+    if (r >= s_lo && r <= s_hi) {
+      if (r < nreal_q) src = r + off;
+      else if (r == rs_q) src = rs_p;
+    }
+    double a[8];
+#pragma unroll
+    for (int ks = 0; ks < 8; ++ks) a[ks] = src >= 0 ? -ld(src, ks * 4 + (lane & 3)) : 0.0;
+    // C fragments: rows tile*8 + (lane >> 2), cols 8 ct + 2 (lane & 3) + {0, 1}
+    const int cr = tile * 8 + (lane >> 2);
+    const bool cok = cr >= s_lo && cr <= s_hi && (cr < nreal_q || cr == rs_q);
+    double acc[4][2];
+#pragma unroll
+    for (int ct = 0; ct < 4; ++ct) {
+      const int cc = ct * 8 + 2 * (lane & 3);
+      acc[ct][0] = cok ? Pq[cr * CP_LS + cc] : 0.0;
+      acc[ct][1] = cok ? Pq[cr * CP_LS + cc + 1] : 0.0;
+    }
+#pragma unroll
+    for (int ks = 0; ks < 8; ++ks)
+#pragma unroll
+      for (int ct = 0; ct < 4; ++ct) dmma_8x8x4(acc[ct], a[ks], b[ks][ct]);
+    if (cok) {
+#pragma unroll
+      for (int ct = 0; ct < 4; ++ct) {
+        const int cc = ct * 8 + 2 * (lane & 3);
+        Pq[cr * CP_LS + cc] = acc[ct][0];
+        Pq[cr * CP_LS + cc + 1] = acc[ct][1];
+      }
+    }
+  }
+}
+
+template <int KP>
+__global__ void __launch_bounds__(CH_THREADS, 1) k_chol_panels(
+    DevCtl* __restrict__ ctl, int d, const double* __restrict__ hpk,
+    const double* __restrict__ shift_ptr, const double* __restrict__ rhs,
+    const double* __restrict__ x, double* __restrict__ Lg, double* __restrict__ z,
+    double* __restrict__ x_out, int mode, int ignore_halt, long long* __restrict__ dbg) {
+  cg::cluster_group cluster = cg::this_cluster();
+  __shared__ CpSmem sm;
+  extern __shared__ __align__(16) double cpan[];
+  const int rank = static_cast<int>(cluster.block_rank());
+  const int cs = static_cast<int>(cluster.num_blocks());
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int npan = (d + CP_NB - 1) / CP_NB;
+  const int RS = cp_rows(d);
+  const double shift = shift_ptr ? __ldcg(shift_ptr) : 0.0;
+  long long t_mark = clock64();
+  auto mark = [&](int slot) {
+    if (dbg && tid == 0 && rank == 0) {
+      const long long now = clock64();
+      dbg[slot] += now - t_mark;
+      t_mark = now;
+    }
+  };
+  auto P = [&](int k) { return cpan + static_cast<size_t>(k) * RS * CP_LS; };
+  // diagnostics: per-panel global timestamps (fb_debug_counters)
+  auto stamp = [&](int p, int k) {  // dbg[16 + 16 p + k], thread 0 of each CTA
+    if (dbg && tid == 0 && p < 64) dbg[16 + p * 16 + k] = globaltimer_ns();
+  };
+  auto Lglob = [&](int p) { return Lg + static_cast<size_t>(p) * RS * CP_LS; };
+  const int last_own = rank + ((npan - 1 - rank) / cs) * cs;  // highest own panel (rank < npan)
+
+  if (tid == 0) {
+    for (int p = 0; p < npan; ++p) {
+      mbar_init(&sm.barL[p], 1);
+      mbar_init(&sm.barZ[p], 1);
+    }
+    fence_barrier_init();
+    sm.failed = 0;
+  }
+  // ---- own panels from packed H (lower A[i][j] = H[j][i], i >= j), + shift
+  //      on the diagonal, identity padding, right-hand side as the last slot
+#pragma unroll
+  for (int k = 0; k < KP; ++k) {
+    const int q = rank + k * cs;
+    if (q >= npan) break;
+    const int q0 = q * CP_NB, nreal = d - q0, rs = max(nreal, CP_NB), pb = min(CP_NB, nreal);
+    double* Pq = P(k);
+    for (int e = tid; e < (rs + 1) * CP_NB; e += CH_THREADS) {
+      const int r = e / CP_NB, c = e % CP_NB;
+      double v = 0.0;
+      if (r == rs) {
+        v = c < pb ? __ldcg(rhs + q0 + c) : 0.0;
+      } else if (r < nreal) {
+        const int i = q0 + r, j = q0 + c;
+        if (c < pb && j <= i) {
+          v = __ldcg(hpk + static_cast<int64_t>(i) * (i + 1) / 2 + j);
+          if (i == j) v = __dadd_rn(v, shift);
+        }
+      } else {
+        v = (r == c) ? 1.0 : 0.0;  // padding of the last panel's diagonal block
+      }
+      Pq[r * CP_LS + c] = v;
+    }
+  }
+  cluster.sync();  // barriers initialised cluster-wide before any remote arrive
+  mark(0);
+
+  // ---- factorisation
+  for (int p = 0; p < npan; ++p) {
+    const int owner = p % cs, kp = p / cs;
+    const int p0 = p * CP_NB;
+    if (rank == owner) {
+      double* Pp = P(kp);
+      const int nreal = d - p0, rs = max(nreal, CP_NB), pb = min(CP_NB, nreal);
+      // (A) warp 0: diagonal block + inverse; warps 1..7: pending update of
+      //     the lower rows from panel p - 1
+      stamp(p, 0);
+      if (warp == 0) {
+        constexpr int SB = 8;
+        double row[CP_NB];
+#pragma unroll
+        for (int s2 = 0; s2 < CP_NB; ++s2) row[s2] = Pp[lane * CP_LS + s2];
+        int fail = CP_NB;
+        double fail_val = 0.0;
+#pragma unroll
+        for (int jj = 0; jj < CP_NB; ++jj) {
+          const int qend = (jj / SB + 1) * SB;
+          const double piv = __shfl_sync(0xffffffffu, row[jj], jj);
+          const bool ok = piv > 0.0 && isfinite(piv);
+          if (!ok && jj < pb && fail == CP_NB) { fail = jj; fail_val = piv; }
+          const double ir = rsqrt(ok ? piv : 1.0);
+          if (lane == jj) sm.inv[jj] = ir;
+          row[jj] = (lane == jj) ? piv * ir : ((lane > jj) ? row[jj] * ir : row[jj]);
+#pragma unroll
+          for (int kk = jj + 1; kk < qend; ++kk) {
+            const double lk = __shfl_sync(0xffffffffu, row[jj], kk);
+            row[kk] = (lane >= kk) ? fma(-row[jj], lk, row[kk]) : row[kk];
+          }
+          if (jj == qend - 1 && qend < CP_NB) {
+#pragma unroll
+            for (int s2 = qend - SB; s2 < qend; ++s2) sm.T[kp][lane][s2] = row[s2];
+            __syncwarp();
+#pragma unroll
+            for (int kk = qend; kk < CP_NB; ++kk) {
+              double acc = 0.0;
+#pragma unroll
+              for (int s2 = qend - SB; s2 < qend; ++s2) acc = fma(row[s2], sm.T[kp][kk][s2], acc);
+              row[kk] = (lane >= kk) ? row[kk] - acc : row[kk];
+            }
+            __syncwarp();
+          }
+        }
+        if (fail < CP_NB) {
+          if (lane == 0) {
+            sm.failed = 1;
+            ctl->pivot_index = p0 + fail;
+            ctl->pivot_value = fail_val;
+            raise_status(ctl, ST_NOT_PD);
+          }
+        } else {
+#pragma unroll
+          for (int s2 = 0; s2 < CP_NB; ++s2) Pp[lane * CP_LS + s2] = (s2 <= lane) ? row[s2] : 0.0;
+          __syncwarp();
+          // T = L^-1 (lower): lane c owns column c; t[r] = (delta_rc - sum_k L[r][k] t[k]) / L[r][r]
+          double t[CP_NB];
+#pragma unroll
+          for (int r = 0; r < CP_NB; ++r) {
+            double acc = (r == lane) ? 1.0 : 0.0;
+#pragma unroll
+            for (int k2 = 0; k2 < r; ++k2) acc = fma(-Pp[r * CP_LS + k2], t[k2], acc);
+            t[r] = acc * sm.inv[r];
+          }
+#pragma unroll
+          for (int r = 0; r < CP_NB; ++r) sm.T[kp][r][lane] = t[r];
+        }
+        mark(3);
+        stamp(p, 1);
+      } else if (p > 0) {
+        const int pp = p - 1;
+        if ((pp % cs) == rank) {
+          cp_update<false>(P(pp / cs), pp, p, Pp, d, CP_NB, rs, 1, 8);
+        } else {
+          cp_update<true>(Lglob(pp), pp, p, Pp, d, CP_NB, rs, 1, 8);
+        }
+      }
+      __syncthreads();
+      stamp(p, 2);
+      mark(4);
+      if (sm.failed) {
+        // release every waiter with the failure flag set
+        if (tid < cs && tid != rank) {
+          int* rf = cluster.map_shared_rank(&sm.failed, tid);
+          *rf = 1;
+          for (int q = p; q < npan; ++q) mbar_arrive_remote(&sm.barL[q], static_cast<uint32_t>(tid));
+        }
+        break;
+      }
+      // (B) rows below the block: X = A T^T (in place), 8-row tiles per warp
+      {
+        double bt[8][4];
+#pragma unroll
+        for (int ct = 0; ct < 4; ++ct)
+#pragma unroll
+          for (int ks = 0; ks < 8; ++ks) bt[ks][ct] = sm.T[kp][ct * 8 + (lane >> 2)][ks * 4 + (lane & 3)];
+        const int t_lo = CP_NB / 8, t_hi = rs / 8;
+        for (int tile = t_lo + warp; tile <= t_hi; tile += 8) {
+          const int r = tile * 8 + (lane >> 2);
+          const bool ok = r < nreal || r == rs;
+          double a[8];
+#pragma unroll
+          for (int ks = 0; ks < 8; ++ks) a[ks] = ok ? Pp[r * CP_LS + ks * 4 + (lane & 3)] : 0.0;
+          double acc[4][2] = {};
+#pragma unroll
+          for (int ks = 0; ks < 8; ++ks)
+#pragma unroll
+            for (int ct = 0; ct < 4; ++ct) dmma_8x8x4(acc[ct], a[ks], bt[ks][ct]);
+          __syncwarp();
+          if (ok) {
+#pragma unroll
+            for (int ct = 0; ct < 4; ++ct) {
+              const int cc = ct * 8 + 2 * (lane & 3);
+              Pp[r * CP_LS + cc] = acc[ct][0];
+              Pp[r * CP_LS + cc + 1] = acc[ct][1];
+            }
+          }
+        }
+      }
+      __syncthreads();
+      stamp(p, 4);
+      mark(5);
+      // L_p (rows below the block + rhs) to global for the other CTAs, then
+      // release it
+      if (p < npan - 1 && cs > 1) {
+        double* G = Lglob(p);
+        for (int e = CP_NB * CP_NB + tid; e < (rs + 1) * CP_NB; e += CH_THREADS) {
+          const int r = e / CP_NB, c = e % CP_NB;
+          G[r * CP_LS + c] = Pp[r * CP_LS + c];
+        }
+        __syncthreads();
+        if (tid == 0) {
+          for (int r2 = 0; r2 < cs; ++r2)
+            if (r2 != rank && r2 + ((npan - 1 - r2) / cs) * cs > p)  // r2 owns a later panel
+              mbar_arrive_remote(&sm.barL[p], static_cast<uint32_t>(r2));
+        }
+      }
+      mark(6);
+    } else if (last_own > p) {
+      mbar_wait_cluster(&sm.barL[p], 0);
+      mark(7);
+      if (sm.failed) break;
+    }
+    // apply L_p to the own panels after p (the next one: diagonal rows only;
+    // its lower rows follow in that panel's step A)
+#pragma unroll
+    for (int k = 0; k < KP; ++k) {
+      const int q = rank + k * cs;
+      if (q <= p || q >= npan) continue;
+      const int rs_q = max(d - q * CP_NB, CP_NB);
+      const int s_hi = (q == p + 1) ? CP_NB - 1 : rs_q;
+      if (rank == owner)
+        cp_update<false>(P(kp), p, q, P(k), d, 0, s_hi, 0, 8);
+      else
+        cp_update<true>(Lglob(p), p, q, P(k), d, 0, s_hi, 0, 8);
+    }
+    __syncthreads();
+    mark(8);
+  }
+  mark(1);
+  if (rank == 0) stamp(63, 0);
+  cluster.sync();  // failure flags settled cluster-wide
+  if (rank == 0) stamp(63, 1);
+  if (!sm.failed) {
+    // ---- backward substitution: L^T z = y, panel by panel from the last
+    if (tid < 2 * CP_NB) sm.w[tid / CP_NB][tid % CP_NB] = 0.0;
+    __syncthreads();
+    const int first_own = rank;
+    for (int b = npan - 1; b >= 0; --b) {
+      const int owner = b % cs, kb = b / cs;
+      const int b0 = b * CP_NB, bn = min(CP_NB, d - b0);
+      if (rank == owner) {
+        stamp(b, 8);
+        if (warp == 0) {
+          const double* Pb = P(kb);
+          const int rs = max(d - b0, CP_NB);
+          // r_t = y_t - w_t;  z_s = sum_{t >= s} T[t][s] r_t
+          const double rl = (lane < bn) ? __dsub_rn(Pb[rs * CP_LS + lane], sm.w[kb][lane]) : 0.0;
+          double zs = 0.0;
+          // r broadcast through shared memory (shuffles here would take the
+          // slow collective path: the warp may still be split by polling)
+          sm.part[0][lane] = rl;
+          __syncwarp();
+#pragma unroll 8
+          for (int t2 = 0; t2 < CP_NB; ++t2)
+            if (t2 >= lane) zs = fma(sm.T[kb][t2][lane], sm.part[0][t2], zs);
+          if (lane == 0) stamp(b, 10);
+          __syncwarp();
+          if (lane < bn) {
+            sm.z[b0 + lane] = zs;
+            for (int r2 = 0; r2 < cs; ++r2)  // CTAs owning a panel before b
+              if (r2 != rank && r2 < b) *cluster.map_shared_rank(&sm.z[b0 + lane], r2) = zs;
+          }
+          __syncwarp();
+          if (lane == 0) {
+            stamp(b, 11);
+            for (int r2 = 0; r2 < cs; ++r2)
+              if (r2 != rank && r2 < b) mbar_arrive_remote(&sm.barZ[b], static_cast<uint32_t>(r2));
+            stamp(b, 12);
+          }
+        }
+        __syncthreads();
+      } else if (first_own < b) {
+        mbar_wait_cluster(&sm.barZ[b], 0);
+        if (b - 1 >= 0 && (b - 1) % cs == rank) stamp(b, 9);
+      } else {
+        continue;
+      }
+      // w_q[j] += sum_{i in panel b} L_q[i][j] z_i for own panels q < b
+#pragma unroll
+      for (int k = 0; k < KP; ++k) {
+        const int q = rank + k * cs;
+        if (q >= b || q >= npan) continue;
+        const double* Pq = P(k);
+        const int q0 = q * CP_NB;
+        // warp w sums rows b0 + 4w .. 4w + 3 for column j = lane
+        double s = 0.0;
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int ii = warp * 4 + u;
+          if (ii < bn) s = fma(Pq[(b0 + ii - q0) * CP_LS + lane], sm.z[b0 + ii], s);
+        }
+        sm.part[warp][lane] = s;
+        __syncthreads();
+        if (warp == 0) {
+          double acc = sm.w[k][lane];
+#pragma unroll
+          for (int w2 = 0; w2 < 8; ++w2) acc += sm.part[w2][lane];
+          sm.w[k][lane] = acc;
+        }
+        __syncthreads();
+      }
+      if (b - 1 >= 0 && (b - 1) % cs == rank) stamp(b, 13);
+    }
+    mark(2);
+    if (rank == 0) stamp(63, 2);
+    // ---- outputs of the own panels
+    if (ignore_halt || !ctl->halt) {
+#pragma unroll
+      for (int k = 0; k < KP; ++k) {
+        const int q = rank + k * cs;
+        if (q >= npan) break;
+        const int q0 = q * CP_NB, bn = min(CP_NB, d - q0);
+        if (tid < bn) {
+          const int i = q0 + tid;
+          const double zi = sm.z[i];
+          z[i] = zi;
+          if (mode == 0) x_out[i] = __dsub_rn(__ldcg(x + i), zi);
+          else if (mode == 1) x_out[i] = zi;
+        }
+      }
+    }
+  }
+  cluster.sync();  // no CTA leaves while its shared memory may be addressed
+}
+
+}  // namespace fb
