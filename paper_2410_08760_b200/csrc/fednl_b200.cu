@@ -256,10 +256,10 @@ int launch_hessian(Ctx* ctx, cudaStream_t s, const int32_t* clients, int n_activ
                    const double* hest, int64_t hest_stride, double* D, double* hess_out,
                    bool with_ctl = true) {
   dim3 grid(ctx->n_pairs, n_active);
-  k_hessian<<<grid, HTHREADS, HESS_SMEM, s>>>(ctx->tmap, with_ctl ? ctx->ctl : nullptr, ctx->d,
-                                              ctx->ni, ctx->ldh, ctx->hcoef, ctx->cfg.lam, clients,
-                                              hest, hest_stride, D, hess_out, ctx->frob_part,
-                                              ctx->flags);
+  auto kern = ctx->ni <= 1024 ? k_hessian<3> : k_hessian<2>;
+  kern<<<grid, HTHREADS, HESS_SMEM, s>>>(ctx->tmap, with_ctl ? ctx->ctl : nullptr, ctx->d, ctx->ni,
+                                         ctx->ldh, ctx->hcoef, ctx->cfg.lam, clients, hest,
+                                         hest_stride, D, hess_out, ctx->frob_part, ctx->flags);
   CKL();
   return FB_OK;
 }
@@ -750,7 +750,9 @@ int fb_create(const fb_config* cfg_in, void** out) {
   static size_t max_toplek = 0, max_solve = 0;
   max_toplek = std::max(max_toplek, static_cast<size_t>(std::max(ctx->toplek_P, 1)) * 12);
   max_solve = std::max(max_solve, std::max<size_t>(ctx->solve_smem, 1));
-  CKC(cudaFuncSetAttribute(k_hessian, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  CKC(cudaFuncSetAttribute(k_hessian<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           static_cast<int>(HESS_SMEM)));
+  CKC(cudaFuncSetAttribute(k_hessian<3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            static_cast<int>(HESS_SMEM)));
   CKC(cudaFuncSetAttribute(k_topk_smem, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            static_cast<int>(TKS_SMEM)));

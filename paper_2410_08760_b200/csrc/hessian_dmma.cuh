@@ -49,7 +49,11 @@ __device__ __forceinline__ int swz(int r, int s) {
 // Warps 0..3 compute (warp q owns quadrant rows 32*(q&1), cols 32*(q>>1));
 // warp 4 is the TMA producer.  Stage s is refilled once every active
 // consumer warp has arrived on empty[s] (no CTA-wide barrier per stage).
-__global__ void __launch_bounds__(HTHREADS, 2) k_hessian(
+// MINB = CTAs per SM the register budget is cut for: 3 for short sample
+// loops (c0-c3: the epilogue and pipeline fill of one CTA hide behind the
+// others), 2 for long ones (c4: n_i = 2048, fewer registers cost more).
+template <int MINB>
+__global__ void __launch_bounds__(HTHREADS, MINB) k_hessian(
     const __grid_constant__ CUtensorMap tmap_b, const DevCtl* __restrict__ ctl, int d, int ni,
     int ldh, const double* __restrict__ hcoef, double lam, const int32_t* __restrict__ clients,
     const double* __restrict__ hest, int64_t hest_stride, double* __restrict__ D,
