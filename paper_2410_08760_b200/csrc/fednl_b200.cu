@@ -256,10 +256,13 @@ int launch_hessian(Ctx* ctx, cudaStream_t s, const int32_t* clients, int n_activ
                    const double* hest, int64_t hest_stride, double* D, double* hess_out,
                    bool with_ctl = true) {
   dim3 grid(ctx->n_pairs, n_active);
-  auto kern = ctx->ni <= 1024 ? k_hessian<3> : k_hessian<2>;
+  // 2 CTAs per SM (the 3-CTA register budget measured slower once the ring
+  // release was made safe, see mbar_arrive_dep)
+  auto kern = k_hessian<2>;
   kern<<<grid, HTHREADS, HESS_SMEM, s>>>(ctx->tmap, with_ctl ? ctx->ctl : nullptr, ctx->d, ctx->ni,
                                          ctx->ldh, ctx->hcoef, ctx->cfg.lam, clients, hest,
-                                         hest_stride, D, hess_out, ctx->frob_part, ctx->flags);
+                                         hest_stride, D, hess_out, ctx->frob_part, ctx->flags,
+                                         0u /* zero_mask: see mbar_arrive_after */);
   CKL();
   return FB_OK;
 }
@@ -751,8 +754,6 @@ int fb_create(const fb_config* cfg_in, void** out) {
   max_toplek = std::max(max_toplek, static_cast<size_t>(std::max(ctx->toplek_P, 1)) * 12);
   max_solve = std::max(max_solve, std::max<size_t>(ctx->solve_smem, 1));
   CKC(cudaFuncSetAttribute(k_hessian<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           static_cast<int>(HESS_SMEM)));
-  CKC(cudaFuncSetAttribute(k_hessian<3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            static_cast<int>(HESS_SMEM)));
   CKC(cudaFuncSetAttribute(k_topk_smem, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            static_cast<int>(TKS_SMEM)));

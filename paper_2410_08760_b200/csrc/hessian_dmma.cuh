@@ -39,6 +39,19 @@ struct HessSmem {
 };
 constexpr size_t HESS_SMEM = sizeof(HessSmem) + 1024;  // + alignment slack
 
+// The consumers hand a ring slot back to the TMA with an mbarrier arrive
+// whose address depends (through `zero_mask`: a kernel argument that is 0 at
+// run time but unknown to ptxas) on every fragment value the warp loaded
+// from the slot.  Without that dependency ptxas hoists the arrive above the
+// stage's last fragment loads, and the next TMA fill of the slot races them.
+__device__ __forceinline__ void mbar_arrive_dep(uint64_t* bar, uint32_t dep, uint32_t zero_mask) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar) + (dep & zero_mask))
+               : "memory");
+}
+__device__ __forceinline__ uint32_t dep_of(double v) {
+  return static_cast<uint32_t>(__double2hiint(v));
+}
+
 // element (r, s) of a [64 rows][16 doubles] SWIZZLE_128B tile, in doubles
 __device__ __forceinline__ int swz(int r, int s) {
   return r * HKC + ((((s >> 1) ^ (r & 7)) << 1) | (s & 1));
@@ -49,15 +62,14 @@ __device__ __forceinline__ int swz(int r, int s) {
 // Warps 0..3 compute (warp q owns quadrant rows 32*(q&1), cols 32*(q>>1));
 // warp 4 is the TMA producer.  Stage s is refilled once every active
 // consumer warp has arrived on empty[s] (no CTA-wide barrier per stage).
-// MINB = CTAs per SM the register budget is cut for: 3 for short sample
-// loops (c0-c3: the epilogue and pipeline fill of one CTA hide behind the
-// others), 2 for long ones (c4: n_i = 2048, fewer registers cost more).
+// MINB = CTAs per SM the register budget is cut for (2 is used).
 template <int MINB>
 __global__ void __launch_bounds__(HTHREADS, MINB) k_hessian(
     const __grid_constant__ CUtensorMap tmap_b, const DevCtl* __restrict__ ctl, int d, int ni,
     int ldh, const double* __restrict__ hcoef, double lam, const int32_t* __restrict__ clients,
     const double* __restrict__ hest, int64_t hest_stride, double* __restrict__ D,
-    double* __restrict__ hess_out, double* __restrict__ frob_part, int32_t* __restrict__ flags) {
+    double* __restrict__ hess_out, double* __restrict__ frob_part, int32_t* __restrict__ flags,
+    uint32_t zero_mask) {
   if (ctl && ctl->halt) return;
   extern __shared__ uint8_t smem_raw[];
   HessSmem& sm = *reinterpret_cast<HessSmem*>(
@@ -121,6 +133,7 @@ __global__ void __launch_bounds__(HTHREADS, MINB) k_hessian(
       mbar_wait(&sm.full[s2], (it / HSTAGE) & 1);
       const double* sa = sm.a[s2];
       const double* sb = diag ? sm.a[s2] : sm.b[s2];
+      uint32_t ldep = 0;  // every value loaded from the slot feeds the release
 #pragma unroll
       for (int kk = 0; kk < HKC / 4; ++kk) {
         // k-step kk reads samples {2kk, 2kk+1, 2kk+8, 2kk+9}: with the 128B
@@ -133,12 +146,14 @@ __global__ void __launch_bounds__(HTHREADS, MINB) k_hessian(
 #pragma unroll
         for (int nj = 0; nj < 4; ++nj) bf[nj] = sb[swz(colbase + 8 * nj + g, ks)];
 #pragma unroll
+        for (int q = 0; q < 4; ++q) ldep ^= dep_of(af[q]) ^ dep_of(bf[q]);
+#pragma unroll
         for (int mi = 0; mi < 4; ++mi)
 #pragma unroll
           for (int nj = 0; nj < 4; ++nj) dmma_8x8x4(acc[mi][nj], af[mi], bf[nj]);
       }
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&sm.empty[s2]);
+      // release the slot once every fragment load of this stage completed
+      if (lane == 0) mbar_arrive_dep(&sm.empty[s2], ldep, zero_mask);
     }
   }
   __syncthreads();  // all stages consumed; the ring is free for the epilogue

@@ -506,3 +506,37 @@ def test_round_fold_bit_exact_at_baseline_shape(name):
     assert not bad, bad[:5]
     assert np.array_equal(eng.get_master_hest(), h_mas)
     eng.close()
+
+
+@pytest.mark.parametrize("name", ["c0", "c3"])
+def test_round0_shift_norms_match_oracle(name):
+    """Every client's l_i = ||H_i(x0) - H_i^0||_F and D_i at x0 = 0 against the
+    oracle at 1e-10 (FedNL round 0; FedNL-PP initial shifts).  Guards the
+    Hessian's TMA ring hand-off: a slot released before its fragment loads
+    completed once corrupted single samples of D for a fraction of clients."""
+    shards = D.baseline_shards(name)
+    cfg = D.baseline_run_config(name, rounds=2)
+    d, lam = shards[0].dim, shards[0].lam
+    eng = FedNLEngine(cfg, d, len(shards), shards[0].n_samples, lam=lam)
+    try:
+        eng.upload([s.bmat for s in shards])
+        eng.init_state()
+        w = d * (d + 1) // 2
+        diag_idx = np.array([j * (j + 1) // 2 + j for j in range(d)])
+        wt = np.full(w, 2.0)
+        wt[diag_idx] = 1.0
+        if name == "c3":
+            got = np.asarray(eng.get_pp_state()[2])  # per-client shifts after init
+        else:
+            eng.run_rounds(1)
+            got = eng.round_scalars()[1]
+        for c in range(len(shards)):
+            ev = O.local_eval(shards[c].bmat, lam, np.zeros(d), need_hess=True, need_f=False)
+            want_d = ev.hess.copy()
+            want_d[diag_idx] -= lam
+            want = np.sqrt(np.sum(wt * want_d * want_d))
+            assert abs(got[c] - want) <= 1e-10 * want, (c, got[c], want)
+            if name == "c0":
+                assert normwise(eng.round_diff(c), want_d, np.max(np.abs(ev.hess))) <= 1e-10, c
+    finally:
+        eng.close()
