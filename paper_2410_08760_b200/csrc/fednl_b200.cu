@@ -252,9 +252,11 @@ int launch_gradient(Ctx* ctx, cudaStream_t s, const double* x, const int32_t* cl
   CKL();
   return FB_OK;
 }
+// fuse_grad: the diagonal-tile CTAs also compute the local gradients at x
+// (ctx->grad), replacing k_gradient in the FedNL round
 int launch_hessian(Ctx* ctx, cudaStream_t s, const int32_t* clients, int n_active,
                    const double* hest, int64_t hest_stride, double* D, double* hess_out,
-                   bool with_ctl = true) {
+                   bool with_ctl = true, const double* fuse_grad_x = nullptr) {
   dim3 grid(ctx->n_pairs, n_active);
   // 2 CTAs per SM (the 3-CTA register budget measured slower once the ring
   // release was made safe, see mbar_arrive_dep)
@@ -262,7 +264,8 @@ int launch_hessian(Ctx* ctx, cudaStream_t s, const int32_t* clients, int n_activ
   kern<<<grid, HTHREADS, HESS_SMEM, s>>>(ctx->tmap, with_ctl ? ctx->ctl : nullptr, ctx->d, ctx->ni,
                                          ctx->ldh, ctx->hcoef, ctx->cfg.lam, clients, hest,
                                          hest_stride, D, hess_out, ctx->frob_part, ctx->flags,
-                                         0u /* zero_mask: see mbar_arrive_after */);
+                                         0u /* zero_mask: see mbar_arrive_dep */, ctx->gcoef,
+                                         fuse_grad_x, fuse_grad_x ? ctx->grad : nullptr);
   CKL();
   return FB_OK;
 }
@@ -422,9 +425,9 @@ int enqueue_fednl_round(Ctx* ctx) {
   TRY(record(ctx, EV_START, s));
   CK(cudaMemsetAsync(ctx->flags, 0, sizeof(int32_t) * n, s));
   TRY(launch_margins(ctx, s, ctx->x, nullptr, n));
-  TRY(launch_gradient(ctx, s, ctx->x, nullptr, n));
   TRY(record(ctx, EV_ORACLE_END, s));
-  TRY(launch_hessian(ctx, s, nullptr, n, ctx->hest, ctx->w, ctx->D, nullptr));
+  // Hessian + D + Frobenius partials, with the local gradients fused in
+  TRY(launch_hessian(ctx, s, nullptr, n, ctx->hest, ctx->w, ctx->D, nullptr, true, ctx->x));
   TRY(record(ctx, EV_HESS_END, s));
   TRY(launch_reduce(ctx, s, ctx->x, nullptr, n, n, true, ctx->row_grad, ctx->row_f));
   TRY(record(ctx, EV_REDUCE_END, s));

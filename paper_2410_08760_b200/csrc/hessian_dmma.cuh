@@ -32,6 +32,7 @@ struct HessSmem {
   double a[HSTAGE][HT * HKC];  // 8 KB per stage, 1024 B aligned (swizzle-128B)
   double b[HSTAGE][HT * HKC];
   double h[HSTAGE][HKC];
+  double gc[HSTAGE][HKC];      // gradient coefficients (fused gradient, diagonal tiles)
   uint64_t full[HSTAGE];       // TMA -> consumers (transaction count)
   uint64_t empty[HSTAGE];      // consumers -> producer (one arrive per active warp)
   double red[HTHREADS / 32];
@@ -69,7 +70,8 @@ __global__ void __launch_bounds__(HTHREADS, MINB) k_hessian(
     int ldh, const double* __restrict__ hcoef, double lam, const int32_t* __restrict__ clients,
     const double* __restrict__ hest, int64_t hest_stride, double* __restrict__ D,
     double* __restrict__ hess_out, double* __restrict__ frob_part, int32_t* __restrict__ flags,
-    uint32_t zero_mask) {
+    uint32_t zero_mask, const double* __restrict__ gcoef, const double* __restrict__ x,
+    double* __restrict__ grad) {
   if (ctl && ctl->halt) return;
   extern __shared__ uint8_t smem_raw[];
   HessSmem& sm = *reinterpret_cast<HessSmem*>(
@@ -89,13 +91,20 @@ __global__ void __launch_bounds__(HTHREADS, MINB) k_hessian(
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int g = lane >> 2, t = lane & 3;
   const int rowbase = 32 * (warp & 1), colbase = 32 * (warp >> 1);
-  // on a diagonal tile the lower-left quadrant is entirely below the diagonal
-  const int n_active_warps = diag ? HCONS - 1 : HCONS;
+  // on a diagonal tile the lower-left quadrant is entirely below the diagonal;
+  // with `grad` set that warp computes the local gradient of the tile's 64
+  // features from the same stages instead (oracle.py:108-121, fused: B is
+  // streamed once for the Hessian and the gradient)
+  const bool fuse_grad = diag && grad != nullptr;
+  const int n_active_warps = (diag && !fuse_grad) ? HCONS - 1 : HCONS;
   const bool consumer = warp < HCONS && !(diag && rowbase > colbase);
+  const bool grad_warp = fuse_grad && warp < HCONS && rowbase > colbase;
 
   const int nk = (ni + HKC - 1) / HKC;
   const double* hrow = hcoef + static_cast<int64_t>(c) * ldh;
-  const uint32_t stage_bytes = (diag ? 1u : 2u) * HT * HKC * 8u + HKC * 8u;
+  const double* grow = fuse_grad ? gcoef + static_cast<int64_t>(c) * ldh : nullptr;
+  const uint32_t stage_bytes =
+      (diag ? 1u : 2u) * HT * HKC * 8u + HKC * 8u + (fuse_grad ? HKC * 8u : 0u);
 
   if (tid == 0) {
     tma_prefetch_desc(&tmap_b);
@@ -124,7 +133,34 @@ __global__ void __launch_bounds__(HTHREADS, MINB) k_hessian(
         tma_load_3d(sm.a[s2], &tmap_b, &sm.full[s2], it * HKC, I * HT, c);
         if (!diag) tma_load_3d(sm.b[s2], &tmap_b, &sm.full[s2], it * HKC, J * HT, c);
         bulk_load(sm.h[s2], hrow + it * HKC, HKC * 8, &sm.full[s2]);
+        if (fuse_grad) bulk_load(sm.gc[s2], grow + it * HKC, HKC * 8, &sm.full[s2]);
       }
+    }
+  } else if (grad_warp) {
+    // ---------------- fused gradient: lane owns features r = lane, lane + 32
+    double g0 = 0.0, g1 = 0.0;
+    for (int it = 0; it < nk; ++it) {
+      const int s2 = it % HSTAGE;
+      mbar_wait(&sm.full[s2], (it / HSTAGE) & 1);
+      const double* sa = sm.a[s2];
+      uint32_t ldep = 0;
+#pragma unroll
+      for (int k2 = 0; k2 < HKC; ++k2) {
+        const double gk = sm.gc[s2][k2];
+        const double v0 = sa[swz(lane, k2)], v1 = sa[swz(lane + 32, k2)];
+        ldep ^= dep_of(v0) ^ dep_of(v1) ^ dep_of(gk);
+        g0 = fma(v0, gk, g0);
+        g1 = fma(v1, gk, g1);
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive_dep(&sm.empty[s2], ldep, zero_mask);
+    }
+    const double* xc = x;
+#pragma unroll
+    for (int h2 = 0; h2 < 2; ++h2) {
+      const int a = I * HT + lane + 32 * h2;
+      if (a < d)
+        grad[static_cast<int64_t>(c) * d + a] = __dadd_rn(h2 ? g1 : g0, __dmul_rn(lam, xc[a]));
     }
   } else if (consumer) {
     // ---------------- DMMA consumers
