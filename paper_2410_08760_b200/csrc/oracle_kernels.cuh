@@ -32,11 +32,12 @@ __device__ __forceinline__ double softplus_neg(double m) {
 
 // Margins m_j = <B_j, x>, sigmoids, per-sample Hessian / gradient
 // coefficients, and per-block partial sums of the loss (for f_value).
-// One block = MB_SAMPLES consecutive samples (lane = sample) x 8 warps that
-// split the features (warp w sums a = w, w + 8, ...): every load is a
-// coalesced 256 B row segment and each thread keeps 8 loads in flight.
-// grid (ceil(ldh / 32), n_active), block 256, dynamic smem d doubles.
-constexpr int MB_SAMPLES = 32;
+// One block = MB_SAMPLES consecutive samples (lane = 2 samples, one 16-byte
+// load) x 8 warps that split the features (warp w sums a = w, w + 8, ...):
+// every load instruction reads a contiguous 512 B row segment and each
+// thread keeps 8 of them in flight.
+// grid (ceil(ldh / 64), n_active), block 256, dynamic smem d doubles.
+constexpr int MB_SAMPLES = 64;
 constexpr int MB_THREADS = 256;
 __global__ void __launch_bounds__(MB_THREADS) k_margins(
     const DevCtl* __restrict__ ctl, const double* __restrict__ Bt, int d, int ni, int ldj,
@@ -45,49 +46,65 @@ __global__ void __launch_bounds__(MB_THREADS) k_margins(
     int nblk) {
   if (ctl && ctl->halt) return;
   extern __shared__ double xs[];
-  __shared__ double part[8][MB_SAMPLES + 1];
+  __shared__ double part[8][MB_SAMPLES + 2];
+  __shared__ double red[2];
   const int c = client_of(clients, blockIdx.y);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   for (int a = threadIdx.x; a < d; a += blockDim.x) xs[a] = x[a];
   __syncthreads();
-  const int j = blockIdx.x * MB_SAMPLES + lane;
-  double m = 0.0;
-  if (j < ni) {
-    const double* col = Bt + static_cast<int64_t>(c) * d * ldj + j;
-    double acc[8];
+  const int j = blockIdx.x * MB_SAMPLES + 2 * lane;  // this lane's samples j, j + 1
+  double m0 = 0.0, m1 = 0.0;
+  if (j < ldj) {  // ldj even: j + 1 < ldj too (zero padded beyond ni)
+    const double2* col = reinterpret_cast<const double2*>(Bt + static_cast<int64_t>(c) * d * ldj + j);
+    const int64_t rs = ldj / 2;  // row stride in double2
+    double2 acc[4];
 #pragma unroll
-    for (int u = 0; u < 8; ++u) acc[u] = 0.0;
+    for (int u = 0; u < 4; ++u) acc[u] = make_double2(0.0, 0.0);
     int a0 = warp;
     for (; a0 + 56 < d; a0 += 64) {
-      double bv[8];
+      double2 bv[8];
 #pragma unroll
-      for (int u = 0; u < 8; ++u) bv[u] = __ldg(col + static_cast<int64_t>(a0 + 8 * u) * ldj);
+      for (int u = 0; u < 8; ++u) bv[u] = __ldcs(col + static_cast<int64_t>(a0 + 8 * u) * rs);
 #pragma unroll
-      for (int u = 0; u < 8; ++u) acc[u] = fma(bv[u], xs[a0 + 8 * u], acc[u]);
+      for (int u = 0; u < 8; ++u) {
+        const double xa = xs[a0 + 8 * u];
+        acc[u & 3].x = fma(bv[u].x, xa, acc[u & 3].x);
+        acc[u & 3].y = fma(bv[u].y, xa, acc[u & 3].y);
+      }
     }
-    for (; a0 < d; a0 += 8) acc[0] = fma(__ldg(col + static_cast<int64_t>(a0) * ldj), xs[a0], acc[0]);
-    m = ((acc[0] + acc[1]) + (acc[2] + acc[3])) + ((acc[4] + acc[5]) + (acc[6] + acc[7]));
+    for (; a0 < d; a0 += 8) {
+      const double2 bv = __ldcs(col + static_cast<int64_t>(a0) * rs);
+      acc[0].x = fma(bv.x, xs[a0], acc[0].x);
+      acc[0].y = fma(bv.y, xs[a0], acc[0].y);
+    }
+    m0 = (acc[0].x + acc[1].x) + (acc[2].x + acc[3].x);
+    m1 = (acc[0].y + acc[1].y) + (acc[2].y + acc[3].y);
   }
-  part[warp][lane] = m;
+  part[warp][2 * lane] = m0;
+  part[warp][2 * lane + 1] = m1;
   __syncthreads();
-  if (warp == 0) {
+  if (warp < 2) {  // thread = one sample of the block
+    const int sl = warp * 32 + lane;
+    const int js = blockIdx.x * MB_SAMPLES + sl;
     double mm = 0.0;
 #pragma unroll
-    for (int w2 = 0; w2 < 8; ++w2) mm += part[w2][lane];
+    for (int w2 = 0; w2 < 8; ++w2) mm += part[w2][sl];
     double loss = 0.0;
-    if (j < ni) {
+    if (js < ni) {
       const double sig = stable_sigmoid(mm);
       const double nd = static_cast<double>(ni);
-      hcoef[static_cast<int64_t>(c) * ldh + j] = __ddiv_rn(__dmul_rn(sig, __dsub_rn(1.0, sig)), nd);
-      gcoef[static_cast<int64_t>(c) * ldh + j] = __ddiv_rn(__dsub_rn(sig, 1.0), nd);
+      hcoef[static_cast<int64_t>(c) * ldh + js] = __ddiv_rn(__dmul_rn(sig, __dsub_rn(1.0, sig)), nd);
+      gcoef[static_cast<int64_t>(c) * ldh + js] = __ddiv_rn(__dsub_rn(sig, 1.0), nd);
       loss = softplus_neg(mm);
-    } else if (j < ldh) {
-      hcoef[static_cast<int64_t>(c) * ldh + j] = 0.0;
-      gcoef[static_cast<int64_t>(c) * ldh + j] = 0.0;
+    } else if (js < ldh) {
+      hcoef[static_cast<int64_t>(c) * ldh + js] = 0.0;
+      gcoef[static_cast<int64_t>(c) * ldh + js] = 0.0;
     }
     const double tot = warp_sum(loss);
-    if (lane == 0) loss_part[static_cast<int64_t>(c) * nblk + blockIdx.x] = tot;
+    if (lane == 0) red[warp] = tot;
   }
+  __syncthreads();
+  if (threadIdx.x == 0) loss_part[static_cast<int64_t>(c) * nblk + blockIdx.x] = red[0] + red[1];
 }
 
 // Local gradients g_c = B_c gcoef_c + lam x (oracle.py:108-121).
