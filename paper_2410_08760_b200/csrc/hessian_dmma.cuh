@@ -106,6 +106,7 @@ __global__ void __launch_bounds__(HTHREADS, MINB) k_hessian(
   const uint32_t stage_bytes =
       (diag ? 1u : 2u) * HT * HKC * 8u + HKC * 8u + (fuse_grad ? HKC * 8u : 0u);
 
+  const long long t_start = clock64();
   if (tid == 0) {
     tma_prefetch_desc(&tmap_b);
     for (int s2 = 0; s2 < HSTAGE; ++s2) {
@@ -193,6 +194,7 @@ __global__ void __launch_bounds__(HTHREADS, MINB) k_hessian(
     }
   }
   __syncthreads();  // all stages consumed; the ring is free for the epilogue
+  const long long t_main = clock64();
 
   // ---- epilogue: stage the tile column-major, then stream packed columns
   double* cs = &sm.a[0][0];  // [64 cols][HC_LD] — reuses the pipeline ring
@@ -262,6 +264,12 @@ __global__ void __launch_bounds__(HTHREADS, MINB) k_hessian(
   if (tid == 0) {
     frob_part[static_cast<int64_t>(c) * n_pairs + pair] = tot;
     if (sm.flag_or) atomicOr(&flags[c], sm.flag_or);
+    if (g_dbg_on) {  // diagnostics: CTA-summed mainloop / epilogue cycles
+      const long long t_end = clock64();
+      atomicAdd(reinterpret_cast<unsigned long long*>(&g_dbg[20]), static_cast<unsigned long long>(t_main - t_start));
+      atomicAdd(reinterpret_cast<unsigned long long*>(&g_dbg[21]), static_cast<unsigned long long>(t_end - t_main));
+      atomicAdd(reinterpret_cast<unsigned long long*>(&g_dbg[22]), 1ull);
+    }
   }
 }
 
