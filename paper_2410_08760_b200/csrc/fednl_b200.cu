@@ -270,11 +270,13 @@ int launch_hessian(Ctx* ctx, cudaStream_t s, const int32_t* clients, int n_activ
   return FB_OK;
 }
 int launch_reduce(Ctx* ctx, cudaStream_t s, const double* x, const int32_t* clients, int n_active,
-                  int n_div, bool with_frob, double* row_grad, double* row_f) {
+                  int n_div, bool with_frob, double* row_grad, double* row_f,
+                  const double* l2_prefetch = nullptr) {
   k_reduce<<<reduce_grid(ctx->d), RED_THREADS, 0, s>>>(ctx->ctl, n_active, clients, n_div, ctx->d, ctx->ni, ctx->nblk,
                               ctx->n_pairs, x, ctx->cfg.lam, ctx->grad, ctx->loss_part,
                               with_frob ? ctx->frob_part : nullptr, ctx->flags, ctx->gbar,
-                              ctx->f_cli, ctx->shift_cli, ctx->sc, row_grad, row_f);
+                              ctx->f_cli, ctx->shift_cli, ctx->sc, row_grad, row_f, l2_prefetch,
+                              static_cast<int64_t>(ctx->w) * 8);
   CKL();
   return FB_OK;
 }
@@ -429,7 +431,7 @@ int enqueue_fednl_round(Ctx* ctx) {
   // Hessian + D + Frobenius partials, with the local gradients fused in
   TRY(launch_hessian(ctx, s, nullptr, n, ctx->hest, ctx->w, ctx->D, nullptr, true, ctx->x));
   TRY(record(ctx, EV_HESS_END, s));
-  TRY(launch_reduce(ctx, s, ctx->x, nullptr, n, n, true, ctx->row_grad, ctx->row_f));
+  TRY(launch_reduce(ctx, s, ctx->x, nullptr, n, n, true, ctx->row_grad, ctx->row_f, ctx->hmas));
   TRY(record(ctx, EV_REDUCE_END, s));
   // fork: the master solve on st, the compressor and master fold on st2.  The
   // solve's cluster is launched first and the compressor waits for its
@@ -1408,7 +1410,7 @@ int fb_oracle_eval(void* handle, const double* x, double* f, double* grad, doubl
   k_reduce<<<reduce_grid(d), RED_THREADS, 0, s>>>(ctx->ctl, n, nullptr, n, d, ctx->ni, ctx->nblk, ctx->n_pairs,
                               ctx->x_new, ctx->cfg.lam, ctx->grad, ctx->loss_part, nullptr,
                               ctx->flags, ctx->gbar, ctx->f_cli, ctx->shift_cli, ctx->sc, nullptr,
-                              nullptr);
+                              nullptr, nullptr, 0);
   CKL();
   if (f) CK(cudaMemcpyAsync(f, ctx->f_cli, sizeof(double) * n, cudaMemcpyDeviceToHost, s));
   if (grad) CK(cudaMemcpyAsync(grad, ctx->grad, sizeof(double) * n * d, cudaMemcpyDeviceToHost, s));

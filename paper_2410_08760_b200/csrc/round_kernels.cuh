@@ -38,9 +38,15 @@ __global__ void __launch_bounds__(RED_THREADS) k_reduce(
     const double* __restrict__ grad, const double* __restrict__ loss_part,
     const double* __restrict__ frob_part, const int32_t* __restrict__ flags,
     double* __restrict__ gbar, double* __restrict__ f_cli, double* __restrict__ shift_cli,
-    RoundScalars* __restrict__ out, double* __restrict__ row_grad, double* __restrict__ row_f) {
+    RoundScalars* __restrict__ out, double* __restrict__ row_grad, double* __restrict__ row_f,
+    const double* __restrict__ l2_prefetch, int64_t l2_prefetch_bytes) {
   if (ctl->halt) return;
   PhaseClock pc;
+  // warm L2 with the next kernel's input (the master H^k for the solve)
+  if (l2_prefetch)
+    for (int64_t off = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) * 128;
+         off < l2_prefetch_bytes; off += static_cast<int64_t>(gridDim.x) * blockDim.x * 128)
+      asm volatile("prefetch.global.L2 [%0];" ::"l"(reinterpret_cast<const char*>(l2_prefetch) + off));
   __shared__ double red[32];
   __shared__ double gp[32][33];
   __shared__ double stage[2048];

@@ -491,21 +491,39 @@ __global__ void __launch_bounds__(CH_THREADS, 1) k_chol_panels(
     if (q >= npan) break;
     const int q0 = q * CP_NB, nreal = d - q0, rs = max(nreal, CP_NB), pb = min(CP_NB, nreal);
     double* Pq = P(k);
-    for (int e = tid; e < (rs + 1) * CP_NB; e += CH_THREADS) {
-      const int r = e / CP_NB, c = e % CP_NB;
-      double v = 0.0;
-      if (r == rs) {
-        v = c < pb ? __ldcg(rhs + q0 + c) : 0.0;
-      } else if (r < nreal) {
-        const int i = q0 + r, j = q0 + c;
-        if (c < pb && j <= i) {
-          v = __ldcg(hpk + static_cast<int64_t>(i) * (i + 1) / 2 + j);
-          if (i == j) v = __dadd_rn(v, shift);
+    // 8 independent loads in flight per thread (the setup is on the critical
+    // path and H^k is usually not in L2 after the Hessian pass)
+    constexpr int UL = 8;
+    const int n_el = (rs + 1) * CP_NB;
+    for (int e0 = tid; e0 < n_el; e0 += UL * CH_THREADS) {
+      double v[UL];
+#pragma unroll
+      for (int u = 0; u < UL; ++u) {
+        const int e = e0 + u * CH_THREADS;
+        const int r = e / CP_NB, c = e % CP_NB;
+        double vv = 0.0;
+        if (e < n_el) {
+          if (r == rs) {
+            vv = c < pb ? __ldcg(rhs + q0 + c) : 0.0;
+          } else if (r < nreal) {
+            const int i = q0 + r, j = q0 + c;
+            if (c < pb && j <= i) vv = __ldcg(hpk + static_cast<int64_t>(i) * (i + 1) / 2 + j);
+          } else {
+            vv = (r == c) ? 1.0 : 0.0;  // padding of the last panel's diagonal block
+          }
         }
-      } else {
-        v = (r == c) ? 1.0 : 0.0;  // padding of the last panel's diagonal block
+        v[u] = vv;
       }
-      Pq[r * CP_LS + c] = v;
+#pragma unroll
+      for (int u = 0; u < UL; ++u) {
+        const int e = e0 + u * CH_THREADS;
+        if (e < n_el) {
+          const int r = e / CP_NB, c = e % CP_NB;
+          double vv = v[u];
+          if (r < nreal && r == c) vv = __dadd_rn(vv, shift);
+          Pq[r * CP_LS + c] = vv;
+        }
+      }
     }
   }
   cluster.sync();  // barriers initialised cluster-wide before any remote arrive
@@ -650,17 +668,36 @@ __global__ void __launch_bounds__(CH_THREADS, 1) k_chol_panels(
         }
       }
       mark(6);
+      // updates from L_{p-1} deferred by the lookahead (own panels after p)
+      if (p > 0) {
+        const int pp = p - 1;
+#pragma unroll
+        for (int k = 0; k < KP; ++k) {
+          const int q = rank + k * cs;
+          if (q <= p || q >= npan) continue;
+          const int rs_q = max(d - q * CP_NB, CP_NB);
+          if (pp % cs == rank)
+            cp_update<false>(P(pp / cs), pp, q, P(k), d, 0, rs_q, 0, 8);
+          else
+            cp_update<true>(Lglob(pp), pp, q, P(k), d, 0, rs_q, 0, 8);
+        }
+        __syncthreads();
+      }
     } else if (last_own > p) {
       mbar_wait_cluster(&sm.barL[p], 0);
       mark(7);
       if (sm.failed) break;
     }
-    // apply L_p to the own panels after p (the next one: diagonal rows only;
-    // its lower rows follow in that panel's step A)
+    // apply L_p to the own panels after p.  Lookahead: if the next panel is
+    // ours, only its diagonal rows now (its lower rows follow in its step A)
+    // and the other own panels' updates are deferred until that panel is
+    // factored and released.
+    const bool next_mine = p + 1 < npan && (p + 1) % cs == rank;
 #pragma unroll
     for (int k = 0; k < KP; ++k) {
       const int q = rank + k * cs;
       if (q <= p || q >= npan) continue;
+      if (next_mine && q != p + 1) continue;  // deferred (applied after p + 1's release)
       const int rs_q = max(d - q * CP_NB, CP_NB);
       const int s_hi = (q == p + 1) ? CP_NB - 1 : rs_q;
       if (rank == owner)
