@@ -1062,59 +1062,97 @@ __global__ void __launch_bounds__(256) k_randseqk(
 
 // ------------------------------------------------------------------ RandK
 // Partial Fisher-Yates prefix (rng.py:106-118, compressors.py:261-262).
-// grid n_active, block 32 (one warp per client).  The k draws are generated
-// in parallel from the counter-based stream; a rejection anywhere (probability
+// grid n_active, block RK_THREADS.  The k draws are generated in parallel
+// from the counter-based stream; a rejection anywhere (probability
 // < k w / 2^64) drops to the exact sequential loop.  The swap chain then runs
-// on lane 0 over a sparse pool (open-addressing table in shared memory).
+// on one thread over a sparse pool (open-addressing table in shared memory)
+// and marks the selected positions in a shared-memory bitmap; the bitmap is
+// compacted in ascending order by the whole block and the entries are
+// emitted in parallel (values scaled by w/k, client shift update, range
+// starts).
+// dynamic smem: pool region | draws[k] | bitmap[wb]; the pool region holds
+// either the whole pool (w <= RK_DIRECT_W) or keys[RK_TABLE] | vals[RK_TABLE]
 constexpr int RK_TABLE = 16384;  // entries (key, value) -> 128 KB
+constexpr int RK_THREADS = 256;
+constexpr int64_t RK_DIRECT_W = 46000;  // pools this small live directly in shared memory
+__host__ __device__ constexpr size_t rk_pool_words(int64_t w) {
+  return static_cast<size_t>(w <= RK_DIRECT_W ? (w > 2 * RK_TABLE ? w : 2 * RK_TABLE) : 2 * RK_TABLE);
+}
+__host__ __device__ constexpr size_t rk_smem_bytes(int k, int wb, int64_t w) {
+  return (rk_pool_words(w) + static_cast<size_t>(k) + static_cast<size_t>(wb)) * 4;
+}
 __device__ __forceinline__ int rk_slot(int32_t* keys, int32_t key) {
   uint32_t h = (static_cast<uint32_t>(key) * 2654435761u) & (RK_TABLE - 1);
   while (keys[h] != -1 && keys[h] != key) h = (h + 1) & (RK_TABLE - 1);
   return static_cast<int>(h);
 }
-__global__ void __launch_bounds__(32) k_randk(
+__global__ void __launch_bounds__(RK_THREADS) k_randk(
     const DevCtl* __restrict__ ctl, const double* __restrict__ D, int64_t w, int wb, int k,
     const int32_t* __restrict__ clients, const int32_t* __restrict__ flags, uint64_t run_seed,
     const uint64_t* __restrict__ seeds, uint32_t* __restrict__ bitmap,
     int32_t* __restrict__ count, uint32_t* __restrict__ idx_list, double* __restrict__ val_list,
-    int cap, int32_t* __restrict__ draws, int64_t* __restrict__ jbuf, Emit em) {
+    int cap, int32_t* __restrict__ draws, Emit em) {
   if (ctl && ctl->halt) return;
-  extern __shared__ int32_t tab[];  // keys[RK_TABLE], vals[RK_TABLE]
-  __shared__ int ws[64];
-  __shared__ int s_reject;
+  extern __shared__ int32_t tab[];
   int32_t* keys = tab;
   int32_t* vals = tab + RK_TABLE;
+  const size_t pw = rk_pool_words(w);
+  int32_t* js = tab + pw;                                   // [k]
+  uint32_t* bm = reinterpret_cast<uint32_t*>(tab + pw + k);  // [wb]
+  __shared__ int ws[64];
+  __shared__ int s_reject;
   const int c = client_of(clients, blockIdx.x);
-  const int lane = threadIdx.x;
+  const int tid = threadIdx.x;
   uint32_t* brow = bitmap + static_cast<int64_t>(c) * wb;
-  clear_row(brow, wb);
   if (!(flags[c] & 2)) {
+    clear_row(brow, wb);
     emit_empty(em, c);
-    if (lane == 0) { count[c] = 0; if (draws) draws[c] = 0; }
+    if (tid == 0) { count[c] = 0; if (draws) draws[c] = 0; }
     return;
   }
   const uint64_t seed = seeds ? seeds[blockIdx.x] : round_seed(run_seed, c, ctl->round);
-  int64_t* js = jbuf + static_cast<int64_t>(blockIdx.x) * cap;
-  if (lane == 0) s_reject = 0;
-  for (int i = lane; i < RK_TABLE; i += 32) keys[i] = -1;
-  __syncwarp();
+  if (tid == 0) s_reject = 0;
+  if (w > RK_DIRECT_W)
+    for (int i = tid; i < RK_TABLE; i += RK_THREADS) keys[i] = -1;
+  for (int q = tid; q < wb; q += RK_THREADS) bm[q] = 0u;
+  __syncthreads();
   // parallel draw i (1-based i+1) under the no-rejection hypothesis
-  for (int i = lane; i < k; i += 32) {
+  for (int i = tid; i < k; i += RK_THREADS) {
     const uint64_t b = static_cast<uint64_t>(w - i);
     const uint64_t u = scramble(seed + static_cast<uint64_t>(i + 1) * GOLDEN);
     if (u < (0ull - b) % b) s_reject = 1;
-    js[i] = i + static_cast<int64_t>(u % b);
+    js[i] = i + static_cast<int32_t>(u % b);
   }
-  __syncwarp();
-  if (lane == 0) {
-    int ndraw = k;
-    if (s_reject) {  // exact sequential replay
-      Prg p(seed);
-      for (int i = 0; i < k; ++i) js[i] = i + static_cast<int64_t>(p.randrange(w - i));
-      ndraw = p.draws;
+  __syncthreads();
+  if (tid == 0 && s_reject) {  // exact sequential replay of the draws
+    Prg p(seed);
+    for (int i = 0; i < k; ++i) js[i] = i + static_cast<int32_t>(p.randrange(w - i));
+    s_reject = p.draws;  // reused: number of draws
+  } else if (tid == 0) {
+    s_reject = -1;
+  }
+  __syncthreads();
+  if (w <= RK_DIRECT_W) {
+    // small pool: the pool itself in shared memory (over the hash table)
+    int32_t* pool = tab;
+    for (int t = tid; t < w; t += RK_THREADS) pool[t] = t;
+    __syncthreads();
+    if (tid == 0) {
+      for (int i = 0; i < k; ++i) {
+        const int32_t j = js[i];
+        const int32_t vi = pool[i], vj = pool[j];
+        pool[j] = vi;
+        pool[i] = vj;
+      }
     }
+    __syncthreads();
+    for (int i = tid; i < k; i += RK_THREADS) {
+      const int32_t v = pool[i];
+      atomicOr(&bm[v >> 5], 1u << (v & 31));
+    }
+  } else if (tid == 0) {
     for (int i = 0; i < k; ++i) {
-      const int32_t j = static_cast<int32_t>(js[i]);
+      const int32_t j = js[i];
       const int si = rk_slot(keys, i);
       const int32_t vi = (keys[si] == i) ? vals[si] : i;
       const int sj = rk_slot(keys, j);
@@ -1122,17 +1160,43 @@ __global__ void __launch_bounds__(32) k_randk(
       keys[sj] = j; vals[sj] = vi;
       const int si2 = rk_slot(keys, i);
       keys[si2] = i; vals[si2] = vj;
-      atomicOr(&brow[vj >> 5], 1u << (vj & 31));
+      bm[vj >> 5] |= 1u << (vj & 31);
     }
-    count[c] = k;
-    if (draws) draws[c] = ndraw;
   }
-  __syncwarp();
-  __threadfence_block();
+  if (tid == 0) {
+    count[c] = k;
+    if (draws) draws[c] = s_reject >= 0 ? s_reject : k;
+  }
+  __syncthreads();
+  // ascending compaction: thread = one bitmap word, block-wide scan; the
+  // positions go to idx_list (global) and the bitmap row is written out
+  uint32_t* il = idx_list + static_cast<int64_t>(c) * cap;
+  double* vl = val_list + static_cast<int64_t>(c) * cap;
+  int32_t* rsc = em.rs ? em.rs + static_cast<int64_t>(c) * (em.nr + 1) : nullptr;
+  int carry = 0;
+  for (int base = 0; base < wb; base += RK_THREADS) {
+    const int q = base + tid;
+    const uint32_t word = (q < wb) ? bm[q] : 0u;
+    int total;
+    int off = block_excl_scan(__popc(word), ws, &total) + carry;
+    if (q < wb) {
+      brow[q] = word;
+      if (rsc && (q % (FOLD_RANGE / 32)) == 0) rsc[q / (FOLD_RANGE / 32)] = off;
+      for (uint32_t m = word; m; m &= m - 1) il[off++] = static_cast<uint32_t>(q * 32 + __ffs(m) - 1);
+    }
+    carry += total;
+  }
+  if (rsc && tid == 0) rsc[em.nr] = carry;
+  __syncthreads();
+  // values (scaled by w / k) and the client shift update, all entries in parallel
   const double scale = static_cast<double>(w) / static_cast<double>(k);
-  compact_bitmap(brow, wb, D + static_cast<int64_t>(c) * w, scale,
-                 idx_list + static_cast<int64_t>(c) * cap, val_list + static_cast<int64_t>(c) * cap,
-                 ws, em, c);
+  const double* v = D + static_cast<int64_t>(c) * w;
+  for (int e = tid; e < k; e += RK_THREADS) {
+    const int64_t t = __ldcg(il + e);
+    const double x = __dmul_rn(__ldg(v + t), scale);
+    vl[e] = x;
+    emit_entry(em, c, t, x);
+  }
 }
 
 // ----------------------------------------------------------------- TopLEK

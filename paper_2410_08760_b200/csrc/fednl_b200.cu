@@ -61,6 +61,7 @@ struct Ctx {
   bool solve_panels = false;  // k_chol_panels (d <= CP_MAX_D) instead of k_chol_solve
   int cp_kp = 1, cp_cs = 1;
   double* Lg = nullptr;       // k_chol_panels: released L panels
+  double* pp_shift_part = nullptr;  // FedNL-PP: Frobenius partials [tau][PP_SB]
   int prio_high = 0;
   cudaEvent_t* direct_pool = nullptr;  // non-null: record() targets these (FB_NO_GRAPH)
   size_t solve_smem = 0;
@@ -84,7 +85,6 @@ struct Ctx {
   int32_t *count = nullptr, *draws = nullptr;
   uint32_t* idx_list = nullptr;
   double* val_list = nullptr;
-  int64_t* jbuf = nullptr;
   uint64_t* cand_key = nullptr;  // TopK streaming path: threshold-bin candidates
   int32_t* cand_pos = nullptr;
   uint64_t* seeds = nullptr;
@@ -318,9 +318,9 @@ int launch_compress(Ctx* ctx, cudaStream_t s, const int32_t* clients, int n_acti
                                           ctx->idx_list, ctx->val_list, ctx->cap, ctx->draws, em);
       break;
     case FB_KIND_RANDK:
-      k_randk<<<n_active, 32, 2 * RK_TABLE * sizeof(int32_t), s>>>(
+      k_randk<<<n_active, RK_THREADS, rk_smem_bytes(c.k, ctx->wb, ctx->w), s>>>(
           ctl, ctx->D, ctx->w, ctx->wb, c.k, clients, ctx->flags, c.run_seed, seeds, ctx->bitmap,
-          ctx->count, ctx->idx_list, ctx->val_list, ctx->cap, ctx->draws, ctx->jbuf, em);
+          ctx->count, ctx->idx_list, ctx->val_list, ctx->cap, ctx->draws, em);
       break;
     case FB_KIND_TOPLEK:
       k_toplek<<<n_active, TK_THREADS, static_cast<size_t>(ctx->toplek_P) * 12, s>>>(
@@ -546,9 +546,12 @@ int enqueue_pp_round(Ctx* ctx) {
   TRY(record(ctx, EV_FOLD_START, s));
   if (dense_kind(ctx))  // the sparse compressors already applied the client update
     TRY(launch_master_fold(ctx, s, ctx->subset, tau, ctx->hest, nullptr, nullptr));
-  k_pp_client<<<tau, 256, 0, s>>>(ctx->ctl, ctx->d, ctx->subset, ctx->hest, ctx->hess_part, ctx->x,
-                                  ctx->grad, ctx->cli_shift, ctx->cli_gvec, ctx->dshift,
-                                  ctx->dgvec);
+  k_pp_shift_part<<<dim3(PP_SB, tau), 256, 0, s>>>(ctx->ctl, ctx->d, ctx->subset, ctx->hest,
+                                                   ctx->hess_part, ctx->pp_shift_part);
+  CKL();
+  k_pp_client<<<dim3((ctx->d + 7) / 8, tau), 256, 0, s>>>(
+      ctx->ctl, ctx->d, ctx->subset, ctx->hest, ctx->pp_shift_part, ctx->x, ctx->grad,
+      ctx->cli_shift, ctx->cli_gvec, ctx->dshift, ctx->dgvec);
   CKL();
   k_pp_master<<<1, 256, 0, s>>>(ctx->ctl, ctx->d, n, tau, ctx->dshift, ctx->dgvec, ctx->gvec,
                                 ctx->pp_shift);
@@ -559,7 +562,7 @@ int enqueue_pp_round(Ctx* ctx) {
                              ctx->row_counts, ctx->row_ls);
   CKL();
   TRY(record(ctx, EV_END, s));
-  ctx->launches_per_round = 15;
+  ctx->launches_per_round = 16;
   return FB_OK;
 }
 
@@ -673,6 +676,9 @@ int fb_create(const fb_config* cfg_in, void** out) {
     return invalid(nullptr, "toplek with d(d+1)/2 > 8192 is outside this build's envelope");
   if (c.kind == FB_KIND_RANDK && std::min<int64_t>(w, 2 * static_cast<int64_t>(c.k)) > 12000)
     return invalid(nullptr, "randk with min(w, 2k) > 12000 is outside this build's envelope");
+  if (c.kind == FB_KIND_RANDK &&
+      rk_smem_bytes(c.k, static_cast<int>((w + 31) / 32), w) > rk_smem_bytes(6000, 16400, 524800))
+    return invalid(nullptr, "randk needs k <= 6000 and d <= 1024 in this build");
 
   Ctx* ctx = new Ctx();
   ctx->cfg = c;
@@ -769,7 +775,7 @@ int fb_create(const fb_config* cfg_in, void** out) {
   CKC(cudaFuncSetAttribute(k_master_fold, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            static_cast<int>(max_fold)));
   CKC(cudaFuncSetAttribute(k_randk, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           static_cast<int>(2 * RK_TABLE * sizeof(int32_t))));
+                           static_cast<int>(rk_smem_bytes(6000, 16400, 524800))));
   CKC(cudaFuncSetAttribute(k_toplek, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            static_cast<int>(max_toplek)));
   CKC(cudaFuncSetAttribute(k_chol_solve<32>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -806,7 +812,7 @@ int fb_create(const fb_config* cfg_in, void** out) {
       dalloc(ctx, &ctx->draws, n) ||
       dalloc(ctx, &ctx->idx_list, static_cast<size_t>(n) * ctx->cap) ||
       dalloc(ctx, &ctx->val_list, static_cast<size_t>(n) * ctx->cap) ||
-      dalloc(ctx, &ctx->jbuf, static_cast<size_t>(n) * ctx->cap) || dalloc(ctx, &ctx->seeds, n) ||
+      dalloc(ctx, &ctx->seeds, n) ||
       dalloc(ctx, &ctx->cand_key, stream_topk ? static_cast<size_t>(n) * TKST_CAP : 1) ||
       dalloc(ctx, &ctx->cand_pos, stream_topk ? static_cast<size_t>(n) * TKST_CAP : 1) ||
       dalloc(ctx, &ctx->sc, 1) || dalloc(ctx, &ctx->steps_table, 64) ||
@@ -818,6 +824,7 @@ int fb_create(const fb_config* cfg_in, void** out) {
       dalloc(ctx, &ctx->cli_gvec, c.algorithm == FB_ALG_PP ? static_cast<size_t>(n) * d : 1) ||
       dalloc(ctx, &ctx->gvec, d) || dalloc(ctx, &ctx->pp_shift, 1) ||
       dalloc(ctx, &ctx->dshift, std::max(tau, 1)) ||
+      dalloc(ctx, &ctx->pp_shift_part, static_cast<size_t>(std::max(tau, 1)) * PP_SB) ||
       dalloc(ctx, &ctx->dgvec, static_cast<size_t>(std::max(tau, 1)) * d) ||
       dalloc(ctx, &ctx->scalar, 4) || dalloc(ctx, &ctx->row_grad, ROW_CHUNK) ||
       dalloc(ctx, &ctx->row_f, ROW_CHUNK) ||

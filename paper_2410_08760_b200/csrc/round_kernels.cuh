@@ -374,44 +374,64 @@ __global__ void k_pp_select(DevCtl* __restrict__ ctl, int n, int tau, int32_t* _
 
 // Per participant after its shift update (algorithms.py:250-256):
 //   shift_new = ||Hest_c - hess||_F,  gvec_new = Hest_c x + shift_new x - grad_c
-// and the increments against the stored client state.  grid tau, block 256.
-__global__ void __launch_bounds__(256) k_pp_client(
+// and the increments against the stored client state.
+// k_pp_shift_part: grid (PP_SB, tau), block 256 — Frobenius partials.
+// k_pp_client:     grid (ceil(d / 8), tau), block 256 — one warp per row a of
+//   Hest_c x (b <= a: packed column a, contiguous; b > a: packed columns b);
+//   the CTAs of a client each fold the PP_SB partials in the same order.
+constexpr int PP_SB = 16;
+__global__ void __launch_bounds__(256) k_pp_shift_part(
     const DevCtl* __restrict__ ctl, int d, const int32_t* __restrict__ subset,
     const double* __restrict__ hest, const double* __restrict__ hess_part,
-    const double* __restrict__ x, const double* __restrict__ grad,
-    double* __restrict__ cli_shift, double* __restrict__ cli_gvec,
-    double* __restrict__ dshift, double* __restrict__ dgvec) {
+    double* __restrict__ shift_part) {
   if (ctl->halt) return;
   __shared__ double red[8];
-  __shared__ double s_shift;
-  const int slot = blockIdx.x;
+  const int slot = blockIdx.y;
   const int c = subset[slot];
   const int64_t w = packed_len(d);
   const double* hc = hest + static_cast<int64_t>(c) * w;
   const double* hp = hess_part + static_cast<int64_t>(slot) * w;
   double part = 0.0;
-  for (int64_t t = threadIdx.x; t < w; t += blockDim.x) {
+  for (int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; t < w;
+       t += static_cast<int64_t>(gridDim.x) * blockDim.x) {
     const double dv = __dsub_rn(hc[t], hp[t]);
     const double wt = packed_is_diag_fast(t) ? 1.0 : 2.0;
     part = fma(__dmul_rn(wt, dv), dv, part);
   }
   const double tot = block_sum(part, red);
-  if (threadIdx.x == 0) s_shift = sqrt(tot);
-  __syncthreads();
-  const double sh = s_shift;
-  for (int a = threadIdx.x; a < d; a += blockDim.x) {
-    // row a of the symmetric matrix from packed storage
+  if (threadIdx.x == 0) shift_part[slot * PP_SB + blockIdx.x] = tot;
+}
+
+__global__ void __launch_bounds__(256) k_pp_client(
+    const DevCtl* __restrict__ ctl, int d, const int32_t* __restrict__ subset,
+    const double* __restrict__ hest, const double* __restrict__ shift_part,
+    const double* __restrict__ x, const double* __restrict__ grad,
+    double* __restrict__ cli_shift, double* __restrict__ cli_gvec,
+    double* __restrict__ dshift, double* __restrict__ dgvec) {
+  if (ctl->halt) return;
+  const int slot = blockIdx.y;
+  const int c = subset[slot];
+  const int64_t w = packed_len(d);
+  const double* hc = hest + static_cast<int64_t>(c) * w;
+  double tot = 0.0;
+  for (int q = 0; q < PP_SB; ++q) tot += shift_part[slot * PP_SB + q];
+  const double sh = sqrt(tot);
+  const int lane = threadIdx.x & 31;
+  const int a = blockIdx.x * 8 + (threadIdx.x >> 5);
+  if (a < d) {
     double s = 0.0;
-    for (int b = 0; b < d; ++b) {
-      const int64_t tt = (a <= b) ? packed_at(a, b) : packed_at(b, a);
-      s = fma(hc[tt], x[b], s);
+    const int64_t ca = packed_at(0, a);
+    for (int b = lane; b <= a; b += 32) s = fma(__ldg(hc + ca + b), __ldg(x + b), s);
+    for (int b = a + 1 + lane; b < d; b += 32) s = fma(__ldg(hc + packed_at(a, b)), __ldg(x + b), s);
+    s = warp_sum(s);
+    if (lane == 0) {
+      const double gnew = __dsub_rn(__dadd_rn(s, __dmul_rn(sh, x[a])), grad[static_cast<int64_t>(c) * d + a]);
+      const double gold = cli_gvec[static_cast<int64_t>(c) * d + a];
+      dgvec[static_cast<int64_t>(slot) * d + a] = __dsub_rn(gnew, gold);
+      cli_gvec[static_cast<int64_t>(c) * d + a] = gnew;
     }
-    const double gnew = __dsub_rn(__dadd_rn(s, __dmul_rn(sh, x[a])), grad[static_cast<int64_t>(c) * d + a]);
-    const double gold = cli_gvec[static_cast<int64_t>(c) * d + a];
-    dgvec[static_cast<int64_t>(slot) * d + a] = __dsub_rn(gnew, gold);
-    cli_gvec[static_cast<int64_t>(c) * d + a] = gnew;
   }
-  if (threadIdx.x == 0) {
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
     dshift[slot] = __dsub_rn(sh, cli_shift[c]);
     cli_shift[c] = sh;
   }

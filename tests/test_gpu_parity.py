@@ -171,6 +171,23 @@ def test_topk_streaming_path_bit_exact_at_c4_size(k):
         assert np.array_equal(got[c].values, want.values), c
 
 
+def test_randk_hash_pool_path_bit_exact():
+    """w = 80,200 > RK_DIRECT_W: the swap chain runs over the hashed pool."""
+    d = 400
+    w = O.packed_len(d)
+    rng = np.random.default_rng(5)
+    P = rng.standard_normal((3, w))
+    P[1] = 0.0
+    seeds = [O.round_seed(11, c, 2) for c in range(3)]
+    for k in (400, 6000):
+        got = leaf.compress_packed_batch(P, d, CompressorSpec(CompressorKind.RANDK, k=k), seeds)
+        for c in range(3):
+            want = O.compress_packed(P[c], d, "randk", k, O.SplitMix64(seeds[c]))
+            assert got[c].entry_count == want.count, (k, c)
+            assert np.array_equal(got[c].indices, want.indices), (k, c)
+            assert np.array_equal(got[c].values, want.values), (k, c)
+
+
 def test_toplek_bit_exact_at_c2_size():
     d = 69
     w = O.packed_len(d)
