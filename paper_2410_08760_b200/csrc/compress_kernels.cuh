@@ -1257,6 +1257,159 @@ __device__ double np_pairwise(const double* a, int n) {
   return ret;
 }
 
+// Block bitonic sort of (energy desc, position asc) with the data in
+// registers: element i = tid + blockDim * r (r < R).  Strides >= blockDim
+// pair elements of the same thread, strides < 32 lanes of the same warp
+// (shuffles); only strides in [32, blockDim) go through shared memory.
+// Sorted result written back to en / pos.
+__device__ __forceinline__ bool tl_before(double ea, uint32_t pa, double eb, uint32_t pb) {
+  return ea > eb || (ea == eb && pa < pb);
+}
+template <int R>
+__device__ void tl_bitonic_sort(double* en, uint32_t* pos, int P) {
+  const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31;
+  double e[R];
+  uint32_t q[R];
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    e[r] = en[tid + nt * r];
+    q[r] = pos[tid + nt * r];
+  }
+  for (int size = 2; size <= P; size <<= 1) {
+    for (int stride = size >> 1; stride > 0; stride >>= 1) {
+      if (stride >= nt) {  // partner in this thread: r ^ (stride / nt)
+        const int rs = stride / nt;
+#pragma unroll
+        for (int RS = 1; RS < R; RS <<= 1) {  // compile-time partner offsets (registers)
+          if (rs != RS) continue;
+#pragma unroll
+          for (int r = 0; r < R; ++r) {
+            const int r2 = r ^ RS;
+            if (r2 > r) {
+              const int i = tid + nt * r;
+              const bool up = (i & size) == 0;
+              const bool swap = tl_before(e[r2], q[r2], e[r], q[r]) == up;
+              const double er = e[r], er2 = e[r2];
+              const uint32_t qr = q[r], qr2 = q[r2];
+              e[r] = swap ? er2 : er;
+              e[r2] = swap ? er : er2;
+              q[r] = swap ? qr2 : qr;
+              q[r2] = swap ? qr : qr2;
+            }
+          }
+        }
+      } else if (stride < 32) {  // partner lane ^ stride
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+          const int i = tid + nt * r;
+          const double eo = __shfl_xor_sync(0xffffffffu, e[r], stride);
+          const uint32_t qo = __shfl_xor_sync(0xffffffffu, q[r], stride);
+          const bool up = (i & size) == 0;
+          const bool lower = (lane & stride) == 0;  // i < partner
+          // the lower index keeps the "before" element when ascending in our order
+          const bool keep_before = (lower == up);
+          const bool other_before = tl_before(eo, qo, e[r], q[r]);
+          if (other_before == keep_before) { e[r] = eo; q[r] = qo; }
+        }
+      } else {  // partner in another warp of the block: through shared memory
+        __syncthreads();
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+          en[tid + nt * r] = e[r];
+          pos[tid + nt * r] = q[r];
+        }
+        __syncthreads();
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+          const int i = tid + nt * r;
+          const int j = i ^ stride;
+          const double eo = en[j];
+          const uint32_t qo = pos[j];
+          const bool up = (i & size) == 0;
+          const bool keep_before = ((i < j) == up);
+          const bool other_before = tl_before(eo, qo, e[r], q[r]);
+          if (other_before == keep_before) { e[r] = eo; q[r] = qo; }
+        }
+      }
+    }
+  }
+  __syncthreads();
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    en[tid + nt * r] = e[r];
+    pos[tid + nt * r] = q[r];
+  }
+  __syncthreads();
+}
+
+// numpy's pairwise sum, block-parallel: thread 0 lists the recursion's
+// leaves (<= 128 elements, left to right), the leaves are summed in parallel
+// (np_pairwise_leaf), then thread 0 folds them along the same recursion.
+// Identical rounding to np_pairwise.  Whole block; result in thread 0.
+constexpr int NPW_MAX_LEAVES = 512;
+__device__ double np_pairwise_block(const double* a, int n, double* lsum, int* loff, int* llen,
+                                    int* s_nleaf) {
+  if (threadIdx.x == 0) {
+    int st_off[24], st_len[24];
+    int top = 0, nl = 0;
+    st_off[0] = 0;
+    st_len[0] = n;
+    while (top >= 0) {  // preorder, left child first: leaves come out left to right
+      const int off = st_off[top], len = st_len[top];
+      --top;
+      if (len <= 128) {
+        loff[nl] = off;
+        llen[nl] = len;
+        ++nl;
+        continue;
+      }
+      int n2 = len / 2;
+      n2 -= n2 % 8;
+      ++top; st_off[top] = off + n2; st_len[top] = len - n2;  // right (popped later)
+      ++top; st_off[top] = off;      st_len[top] = n2;        // left (popped first)
+    }
+    *s_nleaf = nl;
+  }
+  __syncthreads();
+  const int nl = *s_nleaf;
+  for (int i = threadIdx.x; i < nl; i += blockDim.x) lsum[i] = np_pairwise_leaf(a + loff[i], llen[i]);
+  __syncthreads();
+  double ret = 0.0;
+  if (threadIdx.x == 0) {
+    struct Frame {
+      int len, phase;
+      double left;
+    };
+    Frame st[24];
+    int top = 0, next = 0;
+    st[0] = {n, 0, 0.0};
+    while (top >= 0) {
+      Frame& f = st[top];
+      if (f.len <= 128) {
+        ret = lsum[next++];
+        --top;
+        continue;
+      }
+      int n2 = f.len / 2;
+      n2 -= n2 % 8;
+      if (f.phase == 0) {
+        f.phase = 1;
+        st[top + 1] = {n2, 0, 0.0};
+        ++top;
+      } else if (f.phase == 1) {
+        f.left = ret;
+        f.phase = 2;
+        st[top + 1] = {f.len - n2, 0, 0.0};
+        ++top;
+      } else {
+        ret = __dadd_rn(f.left, ret);
+        --top;
+      }
+    }
+  }
+  return ret;
+}
+
 __global__ void __launch_bounds__(TK_THREADS) k_toplek(
     DevCtl* __restrict__ ctl, const double* __restrict__ D, int64_t w, int wb, int k,
     const int32_t* __restrict__ clients, const int32_t* __restrict__ flags, uint64_t run_seed,
@@ -1264,11 +1417,14 @@ __global__ void __launch_bounds__(TK_THREADS) k_toplek(
     int32_t* __restrict__ count, uint32_t* __restrict__ idx_list, double* __restrict__ val_list,
     int cap, int32_t* __restrict__ draws, int P, Emit em) {
   if (ctl && ctl->halt) return;
+  PhaseClock pc;
   extern __shared__ uint8_t tl_raw[];
   double* en = reinterpret_cast<double*>(tl_raw);                    // [P]
   uint32_t* pos = reinterpret_cast<uint32_t*>(tl_raw + 8 * static_cast<size_t>(P));  // [P]
   __shared__ int ws[64];
-  __shared__ int s_t;
+  __shared__ int s_t, s_nleaf;
+  __shared__ double lsum[NPW_MAX_LEAVES];
+  __shared__ int loff[NPW_MAX_LEAVES], llen[NPW_MAX_LEAVES];
   const int c = client_of(clients, blockIdx.x);
   const double* v = D + static_cast<int64_t>(c) * w;
   uint32_t* brow = bitmap + static_cast<int64_t>(c) * wb;
@@ -1283,27 +1439,18 @@ __global__ void __launch_bounds__(TK_THREADS) k_toplek(
     else { en[i] = 0.0; pos[i] = 0xFFFFFFFFu; }
   }
   __syncthreads();
+  pc.mark(24);
   // bitonic sort: "before" = larger energy, then smaller position
-  for (int size = 2; size <= P; size <<= 1) {
-    for (int stride = size >> 1; stride > 0; stride >>= 1) {
-      for (int i = threadIdx.x; i < P; i += blockDim.x) {
-        const int j = i ^ stride;
-        if (j > i) {
-          const bool up = ((i & size) == 0);
-          const double ei = en[i], ej = en[j];
-          const uint32_t pi = pos[i], pj = pos[j];
-          const bool j_before_i = (ej > ei) || (ej == ei && pj < pi);
-          if (j_before_i == up) {
-            en[i] = ej; en[j] = ei;
-            pos[i] = pj; pos[j] = pi;
-          }
-        }
-      }
-      __syncthreads();
-    }
+  switch (P / static_cast<int>(blockDim.x)) {  // P >= blockDim (host pads P)
+    case 1: tl_bitonic_sort<1>(en, pos, P); break;
+    case 2: tl_bitonic_sort<2>(en, pos, P); break;
+    case 4: tl_bitonic_sort<4>(en, pos, P); break;
+    case 8: tl_bitonic_sort<8>(en, pos, P); break;
+    default: tl_bitonic_sort<16>(en, pos, P); break;
   }
+  pc.mark(25);
+  const double total = np_pairwise_block(en, static_cast<int>(w), lsum, loff, llen, &s_nleaf);
   if (threadIdx.x == 0) {
-    const double total = np_pairwise(en, static_cast<int>(w));
     const uint64_t seed = seeds ? seeds[blockIdx.x] : round_seed(run_seed, c, ctl->round);
     Prg p(seed);
     int tsel;
@@ -1345,14 +1492,17 @@ __global__ void __launch_bounds__(TK_THREADS) k_toplek(
     if (draws) draws[c] = p.draws;
   }
   __syncthreads();
+  pc.mark(26);
   const int tsel = s_t;
   for (int i = threadIdx.x; i < tsel; i += blockDim.x) {
     const uint32_t t = pos[i];
     atomicOr(&brow[t >> 5], 1u << (t & 31));
   }
   __syncthreads();
+  pc.mark(27);
   compact_bitmap(brow, wb, v, 1.0, idx_list + static_cast<int64_t>(c) * cap,
                  val_list + static_cast<int64_t>(c) * cap, ws, em, c);
+  pc.mark(28);
 }
 
 // --------------------------------------------------------- identity / natural

@@ -702,7 +702,7 @@ int fb_create(const fb_config* cfg_in, void** out) {
                         : 1.0;
   ctx->toplek_P = 1;
   if (c.kind == FB_KIND_TOPLEK)
-    while (ctx->toplek_P < w) ctx->toplek_P <<= 1;
+    while (ctx->toplek_P < w || ctx->toplek_P < TK_THREADS) ctx->toplek_P <<= 1;
   // master solve: one cluster (8 CTAs from d >= 128); 32-wide panels while the
   // (d + 1) x 33 panel fits in shared memory, else 16-wide
   // 6 CTAs below d = 512 leave the per-client compressor (one CTA per SM)

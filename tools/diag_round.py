@@ -19,6 +19,7 @@ print("event profile (ms):", {k: round(v, 4) for k, v in eng.profile().items() i
 lib.fb_debug_counters(0, buf)
 print("hessian CTA-avg cycles: mainloop %.0f epilogue %.0f (CTAs %.0f)" % (buf[20] / max(buf[22], 1), buf[21] / max(buf[22], 1), buf[22] / R))
 print(name, "per-round cycles (k):", [round(buf[i] / R / 1e3, 1) for i in range(16)], "not-take-all CTAs:", buf[16] / R)
+print("slots 24-28 (k):", [round(buf[i] / R / 1e3, 1) for i in range(24, 29)])
 cta = np.array([buf[32 + i] for i in range(len(shards))]) / 1e3
 print("last round per-CTA kcycles: min %.1f median %.1f max %.1f" % (cta.min(), np.median(cta), cta.max()))
 print("slowest clients", np.argsort(-cta)[:8], np.sort(cta)[::-1][:8])
