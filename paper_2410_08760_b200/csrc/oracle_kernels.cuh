@@ -162,7 +162,17 @@ __global__ void __launch_bounds__(MARGIN_THREADS) k_ls_trials(
   for (int s = 0; s < LS_BATCH; ++s) m[s] = 0.0;
   if (j < ni) {
     const double* col = Bt + static_cast<int64_t>(c) * d * ldj + j;
-    for (int a = 0; a < d; ++a) {
+    int a = 0;
+    for (; a + 8 <= d; a += 8) {  // 8 independent loads in flight
+      double b[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) b[u] = __ldg(col + static_cast<int64_t>(a + u) * ldj);
+#pragma unroll
+      for (int u = 0; u < 8; ++u)
+#pragma unroll
+        for (int s = 0; s < LS_BATCH; ++s) m[s] = fma(b[u], xt[s * d + a + u], m[s]);
+    }
+    for (; a < d; ++a) {
       const double b = __ldg(col + static_cast<int64_t>(a) * ldj);
 #pragma unroll
       for (int s = 0; s < LS_BATCH; ++s) m[s] = fma(b, xt[s * d + a], m[s]);

@@ -541,6 +541,7 @@ __global__ void k_pp_init_master(int d, int n, const double* __restrict__ cli_sh
 // (algorithms.py:302-311).  On acceptance x_new = trial; if the batch is
 // exhausted, ST_LS_PENDING (host drives more batches); past s = 60,
 // ST_LINE_SEARCH.  Single CTA of 256 threads.
+constexpr int LS_DECIDE_MAXN = 4096;
 __global__ void __launch_bounds__(256) k_ls_decide(
     DevCtl* __restrict__ ctl, int d, int n, int ni, int nblk, double lam, double ls_c,
     const double* __restrict__ steps_table, const double* __restrict__ trial_x,
@@ -550,6 +551,7 @@ __global__ void __launch_bounds__(256) k_ls_decide(
   __shared__ double red[8];
   __shared__ int s_acc;
   __shared__ double s_fbest;
+  __shared__ double s_lsum[LS_DECIDE_MAXN];  // per-client loss sums of one trial
   const int s0 = ctl->ls_next;
   if (threadIdx.x == 0) { s_acc = -1; s_fbest = (s0 == 0) ? INFINITY : ctl->f_best; }
   __syncthreads();
@@ -558,15 +560,32 @@ __global__ void __launch_bounds__(256) k_ls_decide(
     const double* xt = trial_x + static_cast<int64_t>(s) * d;
     double part = 0.0;
     for (int a = threadIdx.x; a < d; a += blockDim.x) part = fma(xt[a], xt[a], part);
-    const double xx = block_sum(part, red);
+    // per-client sums of the trial's loss partials, in parallel (client order
+    // is restored by the sequential fold below)
+    for (int c = threadIdx.x; c < n && c < LS_DECIDE_MAXN; c += blockDim.x) {
+      double ls = 0.0;
+      for (int b = 0; b < nblk; ++b)
+        ls = __dadd_rn(ls, __ldcg(loss_part + (static_cast<int64_t>(s) * n + c) * nblk + b));
+      s_lsum[c] = ls;
+    }
+    const double xx = block_sum(part, red);  // also publishes s_lsum
+    const double reg = __dmul_rn(__dmul_rn(0.5, lam), xx);
+    for (int c = threadIdx.x; c < n && c < LS_DECIDE_MAXN; c += blockDim.x)  // f_c, in parallel
+      s_lsum[c] = __dadd_rn(__ddiv_rn(s_lsum[c], static_cast<double>(ni)), reg);
+    __syncthreads();
     if (threadIdx.x == 0 && s_acc < 0 && si <= 60) {
-      const double reg = __dmul_rn(__dmul_rn(0.5, lam), xx);
       double tot = 0.0;
       for (int c = 0; c < n; ++c) {
-        double ls = 0.0;
-        for (int b = 0; b < nblk; ++b)
-          ls = __dadd_rn(ls, loss_part[(static_cast<int64_t>(s) * n + c) * nblk + b]);
-        tot = __dadd_rn(tot, __dadd_rn(__ddiv_rn(ls, static_cast<double>(ni)), reg));
+        double fc;
+        if (c < LS_DECIDE_MAXN) {
+          fc = s_lsum[c];
+        } else {
+          double ls = 0.0;
+          for (int b = 0; b < nblk; ++b)
+            ls = __dadd_rn(ls, __ldcg(loss_part + (static_cast<int64_t>(s) * n + c) * nblk + b));
+          fc = __dadd_rn(__ddiv_rn(ls, static_cast<double>(ni)), reg);
+        }
+        tot = __dadd_rn(tot, fc);
       }
       const double ft = __ddiv_rn(tot, static_cast<double>(n));
       const double step = steps_table[si];
