@@ -718,7 +718,7 @@ int fb_create(const fb_config* cfg_in, void** out) {
     ctx->cp_cs = (npan + ctx->cp_kp - 1) / ctx->cp_kp;
     // (three panels or fewer: the cluster-redundant solver is faster)
     ctx->solve_panels = npan >= 4 && c.d <= CP_MAX_D && ctx->cp_cs <= CH_MAX_CLUSTER &&
-                        static_cast<size_t>(ctx->cp_kp) * cp_panel_bytes(c.d) <= 196 * 1024 &&
+                        static_cast<size_t>(ctx->cp_kp) * cp_panel_bytes(c.d) <= CP_DYN_SMEM_MAX &&
                         !(getenv("FB_SOLVE_OLD") && atoi(getenv("FB_SOLVE_OLD")));
   }
   ctx->solve_smem = ctx->solve_nb == 32 ? solve_panel_bytes<32>(c.d) : solve_panel_bytes<16>(c.d);
@@ -783,9 +783,9 @@ int fb_create(const fb_config* cfg_in, void** out) {
   static size_t max_cp = 0;
   max_cp = std::max(max_cp, static_cast<size_t>(ctx->cp_kp) * cp_panel_bytes(c.d));
   CKC(cudaFuncSetAttribute(k_chol_panels<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           static_cast<int>(std::min<size_t>(max_cp, 196 * 1024))));
+                           static_cast<int>(std::min<size_t>(max_cp, CP_DYN_SMEM_MAX))));
   CKC(cudaFuncSetAttribute(k_chol_panels<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           static_cast<int>(std::min<size_t>(max_cp, 196 * 1024))));
+                           static_cast<int>(std::min<size_t>(max_cp, CP_DYN_SMEM_MAX))));
   CKC(cudaFuncSetAttribute(k_chol_solve<16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            static_cast<int>(std::max(max_solve, solve_panel_bytes<16>(1)))));
 

@@ -373,11 +373,15 @@ struct CpSmem {
   double w[2][CP_NB];         // back-substitution accumulators of the own panels
   double part[8][CP_NB];
   double inv[CP_NB];
-  uint64_t barL[CP_MAXP], barZ[CP_MAXP];
+  double rcv[CP_NB][CP_LS];    // the next own panel's diagonal rows of L_p, pushed over DSMEM
+  uint64_t barL[CP_MAXP], barLd[CP_MAXP], barZ[CP_MAXP];
   int failed;
 };
 
 __host__ __device__ constexpr int cp_rows(int d) { return (d > CP_NB ? d : CP_NB) + 1; }
+// dynamic shared memory for the panels: what the 227 KB per CTA leaves
+// next to the static CpSmem
+constexpr size_t CP_DYN_SMEM_MAX = 227 * 1024 - sizeof(CpSmem) - 512;
 __host__ __device__ constexpr size_t cp_panel_bytes(int d) {
   return static_cast<size_t>(cp_rows(d)) * CP_LS * sizeof(double);
 }
@@ -389,14 +393,14 @@ __host__ __device__ constexpr size_t cp_panel_bytes(int d) {
 template <bool GLOBAL>
 __device__ __forceinline__ void cp_update(const double* __restrict__ Lp, int p, int q,
                                           double* __restrict__ Pq, int d, int s_lo, int s_hi,
-                                          int w_lo, int w_hi) {
+                                          int w_lo, int w_hi, int src_slot_off = 0) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (warp < w_lo || warp >= w_hi) return;
   const int p0 = p * CP_NB, q0 = q * CP_NB;
   const int nreal_q = d - q0, rs_q = max(nreal_q, CP_NB), rs_p = max(d - p0, CP_NB);
   const int off = q0 - p0;
   auto ld = [&](int slot, int col) -> double {
-    const double* a = Lp + static_cast<int64_t>(slot) * CP_LS + col;
+    const double* a = Lp + static_cast<int64_t>(slot - src_slot_off) * CP_LS + col;
     return GLOBAL ? __ldcg(a) : *a;
   };
   // B fragments: b = L_p[j][k], j = q0 + 8 ct + (lane >> 2), k = 4 ks + (lane & 3)
@@ -478,6 +482,7 @@ __global__ void __launch_bounds__(CH_THREADS, 1) k_chol_panels(
   if (tid == 0) {
     for (int p = 0; p < npan; ++p) {
       mbar_init(&sm.barL[p], 1);
+      mbar_init(&sm.barLd[p], 1);
       mbar_init(&sm.barZ[p], 1);
     }
     fence_barrier_init();
@@ -604,6 +609,7 @@ __global__ void __launch_bounds__(CH_THREADS, 1) k_chol_panels(
         if ((pp % cs) == rank) {
           cp_update<false>(P(pp / cs), pp, p, Pp, d, CP_NB, rs, 1, 8);
         } else {
+          mbar_wait_cluster(&sm.barL[pp], 0);  // the L2 copy of L_{p-1}
           cp_update<true>(Lglob(pp), pp, p, Pp, d, CP_NB, rs, 1, 8);
         }
       }
@@ -615,19 +621,30 @@ __global__ void __launch_bounds__(CH_THREADS, 1) k_chol_panels(
         if (tid < cs && tid != rank) {
           int* rf = cluster.map_shared_rank(&sm.failed, tid);
           *rf = 1;
-          for (int q = p; q < npan; ++q) mbar_arrive_remote(&sm.barL[q], static_cast<uint32_t>(tid));
+          for (int q = p; q < npan; ++q) {
+            mbar_arrive_remote(&sm.barL[q], static_cast<uint32_t>(tid));
+            mbar_arrive_remote(&sm.barLd[q], static_cast<uint32_t>(tid));
+          }
         }
         break;
       }
-      // (B) rows below the block: X = A T^T (in place), 8-row tiles per warp
+      // (B) rows below the block: X = A T^T (in place), 8-row tiles per warp.
+      //     Warps 0..3 take slots 32..63 first — the next panel's diagonal
+      //     rows — and push them into the next owner's shared memory (DSMEM)
+      //     with an early release, so that panel's factorisation can start
+      //     before this TRSM and the L2 copy are done.
       {
+        const int nxt_owner = (p + 1) % cs;
+        const bool push = p + 1 < npan && nxt_owner != rank;
+        double(*rcv_remote)[CP_LS] =
+            push ? cluster.map_shared_rank(sm.rcv, static_cast<unsigned>(nxt_owner)) : nullptr;
         double bt[8][4];
 #pragma unroll
         for (int ct = 0; ct < 4; ++ct)
 #pragma unroll
           for (int ks = 0; ks < 8; ++ks) bt[ks][ct] = sm.T[kp][ct * 8 + (lane >> 2)][ks * 4 + (lane & 3)];
         const int t_lo = CP_NB / 8, t_hi = rs / 8;
-        for (int tile = t_lo + warp; tile <= t_hi; tile += 8) {
+        auto do_tile = [&](int tile, bool to_next) {
           const int r = tile * 8 + (lane >> 2);
           const bool ok = r < nreal || r == rs;
           double a[8];
@@ -645,8 +662,23 @@ __global__ void __launch_bounds__(CH_THREADS, 1) k_chol_panels(
               const int cc = ct * 8 + 2 * (lane & 3);
               Pp[r * CP_LS + cc] = acc[ct][0];
               Pp[r * CP_LS + cc + 1] = acc[ct][1];
+              if (to_next && r < 2 * CP_NB) {
+                rcv_remote[r - CP_NB][cc] = acc[ct][0];
+                rcv_remote[r - CP_NB][cc + 1] = acc[ct][1];
+              }
             }
           }
+        };
+        if (warp < 4) {
+          const int tile = t_lo + warp;  // slots 32 + 8 warp ..
+          if (tile <= t_hi) do_tile(tile, push);
+          if (push) {
+            asm volatile("bar.sync 1, 128;" ::: "memory");
+            if (tid == 0) mbar_arrive_remote(&sm.barLd[p], static_cast<uint32_t>(nxt_owner));
+          }
+          for (int t2 = t_lo + 8 + warp; t2 <= t_hi; t2 += 8) do_tile(t2, false);
+        } else {
+          for (int t2 = t_lo + 4 + (warp - 4); t2 <= t_hi; t2 += 8) do_tile(t2, false);
         }
       }
       __syncthreads();
@@ -684,7 +716,15 @@ __global__ void __launch_bounds__(CH_THREADS, 1) k_chol_panels(
         __syncthreads();
       }
     } else if (last_own > p) {
-      mbar_wait_cluster(&sm.barL[p], 0);
+      if ((p + 1) % cs == rank) {
+        // our panel is next: its diagonal rows from the pushed rows of L_p
+        mbar_wait_cluster(&sm.barLd[p], 0);
+        if (sm.failed) break;
+        cp_update<false>(&sm.rcv[0][0], p, p + 1, P((p + 1) / cs), d, 0, CP_NB - 1, 0, 8, CP_NB);
+        __syncthreads();
+      } else {
+        mbar_wait_cluster(&sm.barL[p], 0);
+      }
       mark(7);
       if (sm.failed) break;
     }
@@ -698,6 +738,7 @@ __global__ void __launch_bounds__(CH_THREADS, 1) k_chol_panels(
       const int q = rank + k * cs;
       if (q <= p || q >= npan) continue;
       if (next_mine && q != p + 1) continue;  // deferred (applied after p + 1's release)
+      if (next_mine && rank != owner) continue;  // done from the DSMEM push above
       const int rs_q = max(d - q * CP_NB, CP_NB);
       const int s_hi = (q == p + 1) ? CP_NB - 1 : rs_q;
       if (rank == owner)
