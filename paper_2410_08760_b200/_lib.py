@@ -13,7 +13,8 @@ import os
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libfednl_b200.so")
+# FB_LIB_PATH: load another build of the same library (A/B experiments)
+LIB_PATH = os.environ.get("FB_LIB_PATH") or os.path.join(HERE, "libfednl_b200.so")
 
 FB_OK = 0
 FB_ERR_CUDA = 1
