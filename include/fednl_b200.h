@@ -117,9 +117,27 @@ int fb_get_status(void* ctx, fb_status* out);
 int fb_device_info(char* name, int32_t name_len, int32_t* sm_count, int32_t* cc_major,
                    int32_t* cc_minor);
 
+/* ---- multi-GPU: client sharding ------------------------------------------ */
+/* Client ranges over `world` GPUs, one process per GPU: rank
+ * r owns clients [r*ceil(n/world), (r+1)*ceil(n/world)) ∩ [0, n); each round
+ * every rank computes its clients' oracle, Hessian and compressed deltas,
+ * all-gathers the per-client gradients / loss / Frobenius partials / flags
+ * and the deltas over NCCL (NVLink), and runs the same reduction, master
+ * solve and ascending-client fold as one GPU would — so every rank holds the
+ * bit-identical master state and trajectory.  NCCL (libnccl.so.2) is loaded
+ * on first use.  The reference is single-process (runtime.simulate); this
+ * replaces its per-client loop (runtime.py:255-268) across GPUs. */
+#define FB_NCCL_ID_BYTES 128
+/* a fresh NCCL unique id (rank 0 creates it and shares it out of band) */
+int fb_nccl_unique_id(uint8_t* out);
+/* before fb_upload_shards; FedNL only.  world == 1 runs the sharded path on
+ * one GPU (NCCL with one rank). */
+int fb_set_shard(void* ctx, int32_t world, int32_t rank, const uint8_t* nccl_id);
+
 /* ---- data ------------------------------------------------------------- */
-/* Copy n shards to HBM (feature-major, sample-contiguous rows).  Host memory
- * is only borrowed for the call.  Replaces ClientShard residency
+/* Copy n shards to HBM (feature-major, sample-contiguous rows; under
+ * fb_set_shard only this rank's clients are read).  Host memory is only
+ * borrowed for the call.  Replaces ClientShard residency
  * (oracle.py:33-46, data.py:186-213). */
 int fb_upload_shards(void* ctx, const double* const* bmats);
 

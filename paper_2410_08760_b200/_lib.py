@@ -90,6 +90,8 @@ PROTOTYPES = {
     "fb_last_error": (C.c_char_p, [_P]),
     "fb_get_status": (C.c_int, [_P, C.POINTER(FbStatus)]),
     "fb_device_info": (C.c_int, [C.c_char_p, C.c_int32, _I32, _I32, _I32]),
+    "fb_nccl_unique_id": (C.c_int, [C.POINTER(C.c_uint8)]),
+    "fb_set_shard": (C.c_int, [_P, C.c_int32, C.c_int32, C.POINTER(C.c_uint8)]),
     "fb_upload_shards": (C.c_int, [_P, C.POINTER(_D)]),
     "fb_init_state": (C.c_int, [_P, _D]),
     "fb_run_rounds": (C.c_int, [_P, C.c_int32, C.c_int32, C.c_double, C.c_int32, _D, _D, _I32,

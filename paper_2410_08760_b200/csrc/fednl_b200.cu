@@ -8,6 +8,8 @@
 // launch per round and reads the metrics rows once per chunk.
 #include <cuda.h>
 #include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <nccl.h>  // types only: the library is dlopen'ed on first use
 
 #include <algorithm>
 #include <atomic>
@@ -62,6 +64,12 @@ struct Ctx {
   int cp_kp = 1, cp_cs = 1;
   double* Lg = nullptr;       // k_chol_panels: released L panels
   double* pp_shift_part = nullptr;  // FedNL-PP: Frobenius partials [tau][PP_SB]
+  // client sharding over `world` GPUs (fb_set_shard): this rank owns clients
+  // [c_lo, c_hi) of blocks of npr; per-client exchange arrays are padded to
+  // world * npr clients so an in-place ncclAllGather fills them
+  int world = 1, rank = 0, npr = 0, c_lo = 0, c_hi = 0;
+  int32_t* local_clients = nullptr;  // device [c_hi - c_lo] = c_lo, c_lo + 1, ...
+  ncclComm_t comm = nullptr;
   int prio_high = 0;
   cudaEvent_t* direct_pool = nullptr;  // non-null: record() targets these (FB_NO_GRAPH)
   size_t solve_smem = 0;
@@ -201,6 +209,11 @@ int invalid(Ctx* ctx, const char* msg) {
   else g_err = msg;
   return FB_ERR_INVALID;
 }
+int fail_code(Ctx* ctx, int code, const char* msg) {
+  if (ctx) ctx->err = msg;
+  else g_err = msg;
+  return code;
+}
 
 // ---------------------------------------------------------------- TMA map
 typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
@@ -234,6 +247,54 @@ int make_tmap(Ctx* ctx) {
 }
 
 // -------------------------------------------------------------- launchers
+// ------------------------------------------------------------------ NCCL
+// Loaded with dlopen the first time sharding is requested, so single-GPU use
+// has no NCCL dependency (and an already loaded libnccl — e.g. torch's — is
+// reused: same soname).
+struct NcclApi {
+  bool tried = false, ok = false;
+  ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*AllGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+  const char* (*GetErrorString)(ncclResult_t) = nullptr;
+};
+NcclApi& nccl_api() {
+  static NcclApi api;
+  if (!api.tried) {
+    api.tried = true;
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+    if (h) {
+      api.GetUniqueId = reinterpret_cast<decltype(api.GetUniqueId)>(dlsym(h, "ncclGetUniqueId"));
+      api.CommInitRank = reinterpret_cast<decltype(api.CommInitRank)>(dlsym(h, "ncclCommInitRank"));
+      api.AllGather = reinterpret_cast<decltype(api.AllGather)>(dlsym(h, "ncclAllGather"));
+      api.CommDestroy = reinterpret_cast<decltype(api.CommDestroy)>(dlsym(h, "ncclCommDestroy"));
+      api.GetErrorString = reinterpret_cast<decltype(api.GetErrorString)>(dlsym(h, "ncclGetErrorString"));
+      api.ok = api.GetUniqueId && api.CommInitRank && api.AllGather && api.CommDestroy && api.GetErrorString;
+    }
+  }
+  return api;
+}
+#define NCK(call)                                                                    \
+  do {                                                                               \
+    ncclResult_t r_ = (call);                                                        \
+    if (r_ != ncclSuccess) {                                                         \
+      ctx->err = std::string(#call) + ": " + nccl_api().GetErrorString(r_);          \
+      return FB_ERR_CUDA;                                                            \
+    }                                                                                \
+  } while (0)
+
+// in-place all-gather of a per-client array: this rank's block of npr
+// clients (`per` elements each) at element offset rank * npr * per
+template <typename T>
+int gather_clients(Ctx* ctx, T* base, size_t per, ncclDataType_t type, cudaStream_t s) {
+  const size_t cnt = static_cast<size_t>(ctx->npr) * per;
+  NCK(nccl_api().AllGather(base + static_cast<size_t>(ctx->rank) * cnt, base, cnt, type, ctx->comm, s));
+  return FB_OK;
+}
+bool sharded(const Ctx* ctx) { return ctx->world > 1 || ctx->comm != nullptr; }
+
 int launch_margins(Ctx* ctx, cudaStream_t s, const double* x, const int32_t* clients, int n_active,
                    bool with_ctl = true) {
   dim3 grid(ctx->nblk, n_active);
@@ -426,10 +487,19 @@ int enqueue_fednl_round(Ctx* ctx) {
   const bool ls = ctx->cfg.algorithm == FB_ALG_LS;
   TRY(record(ctx, EV_START, s));
   CK(cudaMemsetAsync(ctx->flags, 0, sizeof(int32_t) * n, s));
-  TRY(launch_margins(ctx, s, ctx->x, nullptr, n));
+  const bool shd = sharded(ctx);
+  const int32_t* loc = shd ? ctx->local_clients : nullptr;  // this rank's clients
+  const int n_loc = shd ? ctx->c_hi - ctx->c_lo : n;
+  TRY(launch_margins(ctx, s, ctx->x, loc, n_loc));
   TRY(record(ctx, EV_ORACLE_END, s));
   // Hessian + D + Frobenius partials, with the local gradients fused in
-  TRY(launch_hessian(ctx, s, nullptr, n, ctx->hest, ctx->w, ctx->D, nullptr, true, ctx->x));
+  TRY(launch_hessian(ctx, s, loc, n_loc, ctx->hest, ctx->w, ctx->D, nullptr, true, ctx->x));
+  if (shd) {  // every rank gets every client's oracle outputs (same reduction order)
+    TRY(gather_clients(ctx, ctx->grad, ctx->d, ncclFloat64, s));
+    TRY(gather_clients(ctx, ctx->loss_part, ctx->nblk, ncclFloat64, s));
+    TRY(gather_clients(ctx, ctx->frob_part, ctx->n_pairs, ncclFloat64, s));
+    TRY(gather_clients(ctx, ctx->flags, 1, ncclInt32, s));
+  }
   TRY(record(ctx, EV_HESS_END, s));
   TRY(launch_reduce(ctx, s, ctx->x, nullptr, n, n, true, ctx->row_grad, ctx->row_f, ctx->hmas));
   TRY(record(ctx, EV_REDUCE_END, s));
@@ -454,7 +524,13 @@ int enqueue_fednl_round(Ctx* ctx) {
   CK(cudaStreamWaitEvent(ctx->st2, ctx->ev_solve_launched, 0));
   static const bool fold_late = getenv("FB_FOLD_LATE") && atoi(getenv("FB_FOLD_LATE"));
   TRY(record(ctx, EV_COMP_START, ctx->st2));
-  TRY(launch_compress(ctx, ctx->st2, nullptr, n, nullptr, nullptr));
+  TRY(launch_compress(ctx, ctx->st2, loc, n_loc, nullptr, nullptr));
+  if (shd) {  // every rank folds every client's delta (ascending client id)
+    TRY(gather_clients(ctx, ctx->idx_list, ctx->cap, ncclUint32, ctx->st2));
+    TRY(gather_clients(ctx, ctx->val_list, ctx->cap, ncclFloat64, ctx->st2));
+    TRY(gather_clients(ctx, ctx->count, 1, ncclInt32, ctx->st2));
+    TRY(gather_clients(ctx, ctx->rs, ctx->nr + 1, ncclInt32, ctx->st2));
+  }
   TRY(record(ctx, EV_COMP_END, ctx->st2));
   TRY(record(ctx, EV_FOLD_START, ctx->st2));
   if (!fold_late)
@@ -686,6 +762,9 @@ int fb_create(const fb_config* cfg_in, void** out) {
   ctx->n = c.n_clients;
   ctx->ni = c.n_samples;
   ctx->w = w;
+  ctx->npr = c.n_clients;
+  ctx->c_lo = 0;
+  ctx->c_hi = c.n_clients;
   ctx->ldj = (c.n_samples + 1) & ~1;
   ctx->ldh = (c.n_samples + 15) & ~15;
   ctx->nblk = (ctx->ldh + MB_SAMPLES - 1) / MB_SAMPLES;
@@ -849,6 +928,7 @@ void fb_destroy(void* handle) {
   if (ctx->graph) cudaGraphDestroy(ctx->graph);
   if (ctx->st) cudaStreamSynchronize(ctx->st);
   if (ctx->st2) cudaStreamSynchronize(ctx->st2);
+  if (ctx->comm) nccl_api().CommDestroy(ctx->comm);
   for (auto& pa : ctx->allocs) cache_release(pa.first, pa.second);
   for (auto& e : ctx->ev_ends) if (e) cudaEventDestroy(e);
   for (auto& e : ctx->ev_pool) if (e) cudaEventDestroy(e);
@@ -913,10 +993,67 @@ UploadPool& upload_pool() {
 }
 constexpr int UPLOAD_LANES = 8;
 
+int fb_nccl_unique_id(uint8_t* out) {
+  if (!out) return invalid(nullptr, "null argument");
+  NcclApi& api = nccl_api();
+  if (!api.ok) return invalid(nullptr, "libnccl.so.2 could not be loaded");
+  ncclUniqueId id;
+  const ncclResult_t r = api.GetUniqueId(&id);
+  if (r != ncclSuccess) {
+    g_err = std::string("ncclGetUniqueId: ") + api.GetErrorString(r);
+    return FB_ERR_CUDA;
+  }
+  static_assert(sizeof(ncclUniqueId) == FB_NCCL_ID_BYTES, "unique id size");
+  std::memcpy(out, &id, sizeof id);
+  return FB_OK;
+}
+
+int fb_set_shard(void* handle, int32_t world, int32_t rank, const uint8_t* nccl_id) {
+  Ctx* ctx = static_cast<Ctx*>(handle);
+  if (!ctx || !nccl_id) return invalid(ctx, "null argument");
+  if (world < 1 || rank < 0 || rank >= world) return invalid(ctx, "bad world / rank");
+  if (ctx->uploaded || ctx->initialised) return invalid(ctx, "fb_set_shard must precede fb_upload_shards");
+  if (ctx->cfg.algorithm != FB_ALG_FEDNL)
+    return fail_code(ctx, FB_ERR_UNSUPPORTED, "client sharding is implemented for FedNL (not LS / PP)");
+  NcclApi& api = nccl_api();
+  if (!api.ok) return invalid(ctx, "libnccl.so.2 could not be loaded");
+  const int n = ctx->n;
+  ctx->world = world;
+  ctx->rank = rank;
+  ctx->npr = (n + world - 1) / world;
+  ctx->c_lo = std::min(n, rank * ctx->npr);
+  ctx->c_hi = std::min(n, ctx->c_lo + ctx->npr);
+  const size_t n_pad = static_cast<size_t>(world) * ctx->npr;
+  // exchange arrays padded to whole blocks (slots >= n are never consumed)
+  if (dalloc(ctx, &ctx->grad, n_pad * ctx->d) || dalloc(ctx, &ctx->loss_part, n_pad * ctx->nblk) ||
+      dalloc(ctx, &ctx->frob_part, n_pad * ctx->n_pairs) || dalloc(ctx, &ctx->flags, n_pad) ||
+      dalloc(ctx, &ctx->idx_list, n_pad * ctx->cap) || dalloc(ctx, &ctx->val_list, n_pad * ctx->cap) ||
+      dalloc(ctx, &ctx->count, n_pad) || dalloc(ctx, &ctx->rs, n_pad * (ctx->nr + 1)) ||
+      dalloc(ctx, &ctx->local_clients, std::max(1, ctx->c_hi - ctx->c_lo)))
+    return FB_ERR_CUDA;
+  std::vector<int32_t> loc(std::max(1, ctx->c_hi - ctx->c_lo));
+  for (int c = ctx->c_lo; c < ctx->c_hi; ++c) loc[c - ctx->c_lo] = c;
+  CK(cudaMemcpyAsync(ctx->local_clients, loc.data(), sizeof(int32_t) * loc.size(),
+                     cudaMemcpyHostToDevice, ctx->st));
+  CK(cudaStreamSynchronize(ctx->st));
+  ncclUniqueId id;
+  std::memcpy(&id, nccl_id, sizeof id);
+  NCK(api.CommInitRank(&ctx->comm, world, id, rank));
+  if (ctx->gexec) {  // the round graph is rebuilt for the sharded body
+    cudaGraphExecDestroy(ctx->gexec);
+    ctx->gexec = nullptr;
+  }
+  if (ctx->graph) {
+    cudaGraphDestroy(ctx->graph);
+    ctx->graph = nullptr;
+  }
+  return FB_OK;
+}
+
 int fb_upload_shards(void* handle, const double* const* bmats) {
   Ctx* ctx = static_cast<Ctx*>(handle);
   if (!ctx || !bmats) return invalid(ctx, "null argument");
-  for (int c = 0; c < ctx->n; ++c)
+  for (int c = ctx->c_lo; c < ctx->c_hi; ++c)
     if (!bmats[c]) return invalid(ctx, "null shard pointer");
   const int d = ctx->d, ni = ctx->ni, n = ctx->n;
   const size_t bytes = static_cast<size_t>(d) * ni * sizeof(double);
@@ -953,7 +1090,7 @@ int fb_upload_shards(void* handle, const double* const* bmats) {
   auto lane_body = [&](int l) {
     UploadLane& ln = pool.lanes[l];
     int slot = 0;
-    for (int c = l; c < n && !failed.load(); c += L, slot ^= 1) {
+    for (int c = ctx->c_lo + l; c < ctx->c_hi && !failed.load(); c += L, slot ^= 1) {
       cudaError_t e = cudaEventSynchronize(ln.done[slot]);  // slot free again
       if (e == cudaSuccess) {
         std::memcpy(ln.host[slot], bmats[c], bytes);
@@ -1210,8 +1347,15 @@ int fb_final_eval(void* handle, double* grad_norm, double* f_value) {
   DevCtl h;
   TRY(read_status(ctx, &h));
   if (h.halt) return status_to_code(h.code);
-  TRY(launch_margins(ctx, s, ctx->x, nullptr, ctx->n));
-  TRY(launch_gradient(ctx, s, ctx->x, nullptr, ctx->n));
+  const bool shd = sharded(ctx);
+  const int32_t* loc = shd ? ctx->local_clients : nullptr;
+  const int n_loc = shd ? ctx->c_hi - ctx->c_lo : ctx->n;
+  TRY(launch_margins(ctx, s, ctx->x, loc, n_loc));
+  TRY(launch_gradient(ctx, s, ctx->x, loc, n_loc));
+  if (shd) {
+    TRY(gather_clients(ctx, ctx->grad, ctx->d, ncclFloat64, s));
+    TRY(gather_clients(ctx, ctx->loss_part, ctx->nblk, ncclFloat64, s));
+  }
   TRY(launch_reduce(ctx, s, ctx->x, nullptr, ctx->n, ctx->n, false, nullptr, nullptr));
   RoundScalars sc;
   CK(cudaMemcpyAsync(&sc, ctx->sc, sizeof sc, cudaMemcpyDeviceToHost, s));

@@ -125,12 +125,25 @@ class FedNLEngine:
         return st
 
     # ------------------------------------------------------------------ data
+    def set_shard(self, world: int, rank: int, nccl_id: bytes) -> None:
+        """Own clients [rank*ceil(n/world), ...) and exchange with the other
+        ranks over NCCL each round (before `upload`; FedNL only)."""
+        if len(nccl_id) != 128:
+            raise ValueError("nccl_id must be the 128-byte ncclUniqueId")
+        buf = (C.c_uint8 * 128).from_buffer_copy(nccl_id)
+        self._check(self.lib.fb_set_shard(self.h, int(world), int(rank), buf), "fb_set_shard")
+        self.world, self.rank = int(world), int(rank)
+
     def upload(self, bmats: list[np.ndarray]) -> None:
         if len(bmats) != self.n:
             raise ValueError(f"expected {self.n} shards, got {len(bmats)}")
         keep = []
         ptrs = (C.POINTER(C.c_double) * self.n)()
+        lo, hi = shard_range(self.n, getattr(self, "world", 1), getattr(self, "rank", 0))
         for c, b in enumerate(bmats):
+            if b is None and not lo <= c < hi:  # another rank's client (sharded)
+                ptrs[c] = None
+                continue
             if b.shape != (self.d, self.ni):
                 raise ValueError(f"shard {c} has shape {b.shape}, expected {(self.d, self.ni)}")
             a = np.asfortranarray(b, dtype=np.float64)
@@ -273,6 +286,21 @@ class FedNLEngine:
         self._check(self.lib.fb_shifted_solve(self.h, _lib.ptr(hp), float(shift), _lib.ptr(b), _lib.ptr(z)),
                     "fb_shifted_solve")
         return z
+
+
+def nccl_unique_id() -> bytes:
+    """A fresh ncclUniqueId (rank 0 makes it; broadcast it to the other ranks)."""
+    lib = _lib.load()
+    buf = (C.c_uint8 * 128)()
+    _lib.check(lib.fb_nccl_unique_id(buf), None, "fb_nccl_unique_id")
+    return bytes(buf)
+
+
+def shard_range(n: int, world: int, rank: int) -> tuple[int, int]:
+    """Clients [lo, hi) owned by `rank` (fb_set_shard's partition)."""
+    npr = (n + world - 1) // world
+    lo = min(n, rank * npr)
+    return lo, min(n, lo + npr)
 
 
 def fp64_peak() -> tuple[float, float]:

@@ -557,3 +557,28 @@ def test_round0_shift_norms_match_oracle(name):
                 assert normwise(eng.round_diff(c), want_d, np.max(np.abs(ev.hess))) <= 1e-10, c
     finally:
         eng.close()
+
+
+def test_sharded_path_world1_matches_unsharded():
+    """The client-sharded round (NCCL all-gathers inside the captured graph)
+    with one rank reproduces the single-GPU trajectory bit for bit."""
+    from paper_2410_08760_b200.engine import nccl_unique_id
+
+    shards = D.baseline_shards("c0")
+    cfg = D.baseline_run_config("c0", rounds=6)
+    d, n, ni, lam = shards[0].dim, len(shards), shards[0].n_samples, shards[0].lam
+    out = []
+    for shard in (False, True):
+        eng = FedNLEngine(cfg, d, n, ni, lam=lam)
+        try:
+            if shard:
+                eng.set_shard(1, 0, nccl_unique_id())
+            eng.upload([s.bmat for s in shards])
+            eng.init_state()
+            b = eng.run_rounds(6)
+            out.append((b.grad_norm.copy(), b.f_value.copy(), b.entry_counts.copy(), eng.get_x(),
+                        eng.get_master_hest(), eng.final_eval()))
+        finally:
+            eng.close()
+    for a, b in zip(out[0], out[1]):
+        assert np.array_equal(np.asarray(a), np.asarray(b))
