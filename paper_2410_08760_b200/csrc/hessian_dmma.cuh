@@ -59,6 +59,47 @@ __device__ __forceinline__ int swz(int r, int s) {
 }
 
 
+// One consumer warp's mainloop over all K-chunks, specialised at compile time
+// for its 32x32 quadrant: MR x NC valid 8x8 fragments (rows / columns past d
+// in the last tile are skipped, rounded up to 2 or 4) and TRI = a diagonal
+// quadrant, whose fragments strictly below the diagonal are skipped.  No
+// runtime branch sits between the DMMAs.
+template <int MR, int NC, bool TRI>
+__device__ __forceinline__ void hess_consume(HessSmem& sm, bool diag, int nk, int rowbase,
+                                             int colbase, int g, int t, int lane,
+                                             uint32_t zero_mask, double (&acc)[4][4][2]) {
+  for (int it = 0; it < nk; ++it) {
+    const int s2 = it % HSTAGE;
+    mbar_wait(&sm.full[s2], (it / HSTAGE) & 1);
+    const double* sa = sm.a[s2];
+    const double* sb = diag ? sm.a[s2] : sm.b[s2];
+    uint32_t ldep = 0;  // every value loaded from the slot feeds the release
+#pragma unroll
+    for (int kk = 0; kk < HKC / 4; ++kk) {
+      // k-step kk reads samples {2kk, 2kk+1, 2kk+8, 2kk+9}: with the 128B
+      // swizzle every half-warp then touches 16 distinct bank pairs
+      const int ks = 2 * kk + (t & 1) + 8 * (t >> 1);
+      const double hv = sm.h[s2][ks];
+      double af[4], bf[4];
+#pragma unroll
+      for (int mi = 0; mi < MR; ++mi) af[mi] = sa[swz(rowbase + 8 * mi + g, ks)] * hv;
+#pragma unroll
+      for (int nj = 0; nj < NC; ++nj) bf[nj] = sb[swz(colbase + 8 * nj + g, ks)];
+#pragma unroll
+      for (int q = 0; q < MR; ++q) ldep ^= dep_of(af[q]);
+#pragma unroll
+      for (int q = 0; q < NC; ++q) ldep ^= dep_of(bf[q]);
+#pragma unroll
+      for (int mi = 0; mi < MR; ++mi)
+#pragma unroll
+        for (int nj = 0; nj < NC; ++nj)
+          if (!TRI || mi <= nj) dmma_8x8x4(acc[mi][nj], af[mi], bf[nj]);
+    }
+    // release the slot once every fragment load of this stage completed
+    if (lane == 0) mbar_arrive_dep(&sm.empty[s2], ldep, zero_mask);
+  }
+}
+
 // grid (n_pairs, n_active), block HTHREADS, dynamic smem HESS_SMEM.
 // Warps 0..3 compute (warp q owns quadrant rows 32*(q&1), cols 32*(q>>1));
 // warp 4 is the TMA producer.  Stage s is refilled once every active
@@ -164,33 +205,21 @@ __global__ void __launch_bounds__(HTHREADS, MINB) k_hessian(
         grad[static_cast<int64_t>(c) * d + a] = __dadd_rn(h2 ? g1 : g0, __dmul_rn(lam, xc[a]));
     }
   } else if (consumer) {
-    // ---------------- DMMA consumers
-    for (int it = 0; it < nk; ++it) {
-      const int s2 = it % HSTAGE;
-      mbar_wait(&sm.full[s2], (it / HSTAGE) & 1);
-      const double* sa = sm.a[s2];
-      const double* sb = diag ? sm.a[s2] : sm.b[s2];
-      uint32_t ldep = 0;  // every value loaded from the slot feeds the release
-#pragma unroll
-      for (int kk = 0; kk < HKC / 4; ++kk) {
-        // k-step kk reads samples {2kk, 2kk+1, 2kk+8, 2kk+9}: with the 128B
-        // swizzle every half-warp then touches 16 distinct bank pairs
-        const int ks = 2 * kk + (t & 1) + 8 * (t >> 1);
-        const double hv = sm.h[s2][ks];
-        double af[4], bf[4];
-#pragma unroll
-        for (int mi = 0; mi < 4; ++mi) af[mi] = sa[swz(rowbase + 8 * mi + g, ks)] * hv;
-#pragma unroll
-        for (int nj = 0; nj < 4; ++nj) bf[nj] = sb[swz(colbase + 8 * nj + g, ks)];
-#pragma unroll
-        for (int q = 0; q < 4; ++q) ldep ^= dep_of(af[q]) ^ dep_of(bf[q]);
-#pragma unroll
-        for (int mi = 0; mi < 4; ++mi)
-#pragma unroll
-          for (int nj = 0; nj < 4; ++nj) dmma_8x8x4(acc[mi][nj], af[mi], bf[nj]);
-      }
-      // release the slot once every fragment load of this stage completed
-      if (lane == 0) mbar_arrive_dep(&sm.empty[s2], ldep, zero_mask);
+    // ---------------- DMMA consumers, specialised per quadrant shape
+    const int vr = (d - (I * HT + rowbase) + 7) / 8, vc = (d - (J * HT + colbase) + 7) / 8;
+    const int mr = vr >= 3 ? 4 : 2, nc = vc >= 3 ? 4 : 2;  // vr, vc >= 1 for an active quadrant
+    const bool tri = diag && rowbase == colbase;
+    if (tri) {
+      if (mr == 4) hess_consume<4, 4, true>(sm, diag, nk, rowbase, colbase, g, t, lane, zero_mask, acc);
+      else hess_consume<2, 2, true>(sm, diag, nk, rowbase, colbase, g, t, lane, zero_mask, acc);
+    } else if (mr == 4 && nc == 4) {
+      hess_consume<4, 4, false>(sm, diag, nk, rowbase, colbase, g, t, lane, zero_mask, acc);
+    } else if (mr == 4) {
+      hess_consume<4, 2, false>(sm, diag, nk, rowbase, colbase, g, t, lane, zero_mask, acc);
+    } else if (nc == 4) {
+      hess_consume<2, 4, false>(sm, diag, nk, rowbase, colbase, g, t, lane, zero_mask, acc);
+    } else {
+      hess_consume<2, 2, false>(sm, diag, nk, rowbase, colbase, g, t, lane, zero_mask, acc);
     }
   }
   __syncthreads();  // all stages consumed; the ring is free for the epilogue
