@@ -406,7 +406,7 @@ int launch_compress(Ctx* ctx, cudaStream_t s, const int32_t* clients, int n_acti
 int launch_solve(Ctx* ctx, cudaStream_t s, const double* hpk, const double* shift_ptr,
                  const double* rhs, const double* x, double* z, double* x_out, int mode,
                  int ignore_halt, long long* dbg = nullptr, cudaEvent_t launched = nullptr,
-                 bool force_old = false) {
+                 bool force_old = false, bool after_reduce = false) {
   const bool panels = ctx->solve_panels && !force_old;
   const int cs = panels ? ctx->cp_cs : ctx->solve_cs;
   cudaLaunchConfig_t lc{};
@@ -414,7 +414,7 @@ int launch_solve(Ctx* ctx, cudaStream_t s, const double* hpk, const double* shif
   lc.blockDim = dim3(CH_THREADS);
   lc.dynamicSmemBytes = panels ? static_cast<size_t>(ctx->cp_kp) * cp_panel_bytes(ctx->d) : ctx->solve_smem;
   lc.stream = s;
-  cudaLaunchAttribute attr[3];
+  cudaLaunchAttribute attr[4];
   attr[0].id = cudaLaunchAttributeClusterDimension;
   attr[0].val.clusterDim.x = cs;
   attr[0].val.clusterDim.y = 1;
@@ -428,10 +428,16 @@ int launch_solve(Ctx* ctx, cudaStream_t s, const double* hpk, const double* shif
   if (launched) {
     // fires once every CTA of the cluster is resident: the concurrent
     // compressor is held back until then, so the solve never waits for SMs
-    attr[2].id = cudaLaunchAttributeLaunchCompletionEvent;
-    attr[2].val.launchCompletionEvent.event = launched;
-    attr[2].val.launchCompletionEvent.flags = 0;
-    lc.numAttrs = 3;
+    attr[lc.numAttrs].id = cudaLaunchAttributeLaunchCompletionEvent;
+    attr[lc.numAttrs].val.launchCompletionEvent.event = launched;
+    attr[lc.numAttrs].val.launchCompletionEvent.flags = 0;
+    ++lc.numAttrs;
+  }
+  if (after_reduce && panels) {
+    // programmatic dependent launch: the panel setup overlaps k_reduce
+    attr[lc.numAttrs].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[lc.numAttrs].val.programmaticStreamSerializationAllowed = 1;
+    ++lc.numAttrs;
   }
   if (panels) {
     if (ctx->cp_kp == 1)
@@ -517,7 +523,8 @@ int enqueue_fednl_round(Ctx* ctx) {
   CK(cudaEventRecord(ctx->ev_fork, s));
   CK(cudaStreamWaitEvent(ctx->st2, ctx->ev_fork, 0));
   TRY(launch_solve(ctx, s, ctx->hmas, &ctx->sc->shift_mean, ctx->gbar, ctx->x, ctx->pvec,
-                   ctx->x_new, ls ? 2 : 0, 0, nullptr, serial ? nullptr : ctx->ev_solve_launched));
+                   ctx->x_new, ls ? 2 : 0, 0, nullptr, serial ? nullptr : ctx->ev_solve_launched,
+                   false, !serial));
   if (serial) {
     CK(cudaEventRecord(ctx->ev_solve_launched, s));
   }

@@ -40,6 +40,8 @@ __global__ void __launch_bounds__(RED_THREADS) k_reduce(
     double* __restrict__ gbar, double* __restrict__ f_cli, double* __restrict__ shift_cli,
     RoundScalars* __restrict__ out, double* __restrict__ row_grad, double* __restrict__ row_f,
     const double* __restrict__ l2_prefetch, int64_t l2_prefetch_bytes) {
+  // the next kernel (the master solve) may start its H^k setup now
+  asm volatile("griddepcontrol.launch_dependents;");
   if (ctl->halt) return;
   PhaseClock pc;
   // warm L2 with the next kernel's input (the master H^k for the solve)

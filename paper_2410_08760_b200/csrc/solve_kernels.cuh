@@ -474,7 +474,6 @@ __global__ void __launch_bounds__(CH_THREADS, 1) k_chol_panels(
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int npan = (d + CP_NB - 1) / CP_NB;
   const int RS = cp_rows(d);
-  const double shift = shift_ptr ? __ldcg(shift_ptr) : 0.0;
   long long t_mark = clock64();
   auto mark = [&](int slot) {
     if (dbg && tid == 0 && rank == 0) {
@@ -521,7 +520,7 @@ __global__ void __launch_bounds__(CH_THREADS, 1) k_chol_panels(
         double vv = 0.0;
         if (e < n_el) {
           if (r == rs) {
-            vv = c < pb ? __ldcg(rhs + q0 + c) : 0.0;
+            vv = 0.0;  // right-hand side: after the dependency wait below
           } else if (r < nreal) {
             const int i = q0 + r, j = q0 + c;
             if (c < pb && j <= i) vv = __ldcg(hpk + static_cast<int64_t>(i) * (i + 1) / 2 + j);
@@ -534,13 +533,26 @@ __global__ void __launch_bounds__(CH_THREADS, 1) k_chol_panels(
 #pragma unroll
       for (int u = 0; u < UL; ++u) {
         const int e = e0 + u * CH_THREADS;
-        if (e < n_el) {
-          const int r = e / CP_NB, c = e % CP_NB;
-          double vv = v[u];
-          if (r < nreal && r == c) vv = __dadd_rn(vv, shift);
-          Pq[r * CP_LS + c] = vv;
-        }
+        if (e < n_el) Pq[(e / CP_NB) * CP_LS + e % CP_NB] = v[u];
       }
+    }
+  }
+  // H^k is ready before the round reduction finishes (programmatic dependent
+  // launch: this kernel may start while k_reduce still runs); the shift and
+  // the right-hand side come from k_reduce, so wait for it here.  Without a
+  // programmatic dependency the wait returns at once.
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  const double shift = shift_ptr ? __ldcg(shift_ptr) : 0.0;
+  __syncthreads();
+#pragma unroll
+  for (int k = 0; k < KP; ++k) {
+    const int q = rank + k * cs;
+    if (q >= npan) break;
+    const int q0 = q * CP_NB, nreal = d - q0, rs = max(nreal, CP_NB), pb = min(CP_NB, nreal);
+    double* Pq = P(k);
+    if (tid < CP_NB) {
+      Pq[rs * CP_LS + tid] = tid < pb ? __ldcg(rhs + q0 + tid) : 0.0;
+      if (tid < pb) Pq[tid * CP_LS + tid] = __dadd_rn(Pq[tid * CP_LS + tid], shift);
     }
   }
   cluster.sync();  // barriers initialised cluster-wide before any remote arrive
