@@ -370,7 +370,7 @@ constexpr int CP_MAXP = 16;
 // its scheduler / the smem pipe slow it (measured: excluding warp 4 cut the
 // per-panel factor from 8.6 to 7.5 us)
 #ifndef CP_REST_WARPS
-#define CP_REST_WARPS 0xEEu
+#define CP_REST_WARPS 0xECu
 #endif
 constexpr int CP_MAX_D = CP_MAXP * CP_NB;
 
@@ -382,6 +382,7 @@ struct CpSmem {
   double inv[CP_NB];
   double rcv[CP_NB][CP_LS];    // the next own panel's diagonal rows of L_p, pushed over DSMEM
   uint64_t barL[CP_MAXP], barLd[CP_MAXP], barZ[CP_MAXP];
+  uint64_t barF[CP_NB];  // block factor: pivot j's row and 1/sqrt published
   int failed;
 };
 
@@ -489,6 +490,7 @@ __global__ void __launch_bounds__(CH_THREADS, 1) k_chol_panels(
   };
   auto Lglob = [&](int p) { return Lg + static_cast<size_t>(p) * RS * CP_LS; };
   const int last_own = rank + ((npan - 1 - rank) / cs) * cs;  // highest own panel (rank < npan)
+  int fac_uses = 0;  // block factors done by this CTA (parity of sm.barF)
 
   if (tid == 0) {
     for (int p = 0; p < npan; ++p) {
@@ -496,10 +498,11 @@ __global__ void __launch_bounds__(CH_THREADS, 1) k_chol_panels(
       mbar_init(&sm.barLd[p], 1);
       mbar_init(&sm.barZ[p], 1);
     }
+    for (int j = 0; j < CP_NB; ++j) mbar_init(&sm.barF[j], 1);
     fence_barrier_init();
     sm.failed = 0;
   }
-  // ---- own panels from packed H (lower A[i][j] = H[j][i], i >= j), + shift
+  // ---- own panels from packed H (A[i][j] = H[min][max]), + shift
   //      on the diagonal, identity padding, right-hand side as the last slot
 #pragma unroll
   for (int k = 0; k < KP; ++k) {
@@ -522,8 +525,11 @@ __global__ void __launch_bounds__(CH_THREADS, 1) k_chol_panels(
           if (r == rs) {
             vv = 0.0;  // right-hand side: after the dependency wait below
           } else if (r < nreal) {
+            // the diagonal block in full (the block factor reads it as
+            // symmetric columns), the rows below as the lower triangle
             const int i = q0 + r, j = q0 + c;
-            if (c < pb && j <= i) vv = __ldcg(hpk + static_cast<int64_t>(i) * (i + 1) / 2 + j);
+            const int hi = max(i, j), lo = min(i, j);
+            if (c < pb) vv = __ldcg(hpk + static_cast<int64_t>(hi) * (hi + 1) / 2 + lo);
           } else {
             vv = (r == c) ? 1.0 : 0.0;  // padding of the last panel's diagonal block
           }
@@ -569,65 +575,81 @@ __global__ void __launch_bounds__(CH_THREADS, 1) k_chol_panels(
       //     the lower rows from panel p - 1
       stamp(p, 0);
       if (warp == 0) {
-        constexpr int SB = 8;
-        double row[CP_NB];
+        // Block factor on the symmetric Schur complement, lane c owning
+        // column c (a[r] = S[r][c]).  By symmetry lane c's multiplier
+        // S[c][j] is its own a[j], so per pivot only 1/sqrt(S[j][j]) crosses
+        // lanes (shared memory, no shuffle); row j of S is published for the
+        // trailing updates and for warp 1, which forms T = L^-1 alongside.
+        double* rows = &sm.rcv[0][0];  // free while this CTA factors (stride CP_LS)
+        double a[CP_NB];
 #pragma unroll
-        for (int s2 = 0; s2 < CP_NB; ++s2) row[s2] = Pp[lane * CP_LS + s2];
-        int fail = CP_NB;
-        double fail_val = 0.0;
+        for (int r = 0; r < CP_NB; ++r) a[r] = Pp[r * CP_LS + lane];
+        double myir = 0.0, mypiv = 0.0;
+        rows[lane] = a[0];
+        {
+          const double y = rsqrt_nr(a[0]);
+          if (lane == 0) { sm.inv[0] = y; mypiv = a[0]; }
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&sm.barF[0]);
+        double ir = sm.inv[0];
 #pragma unroll
-        for (int jj = 0; jj < CP_NB; ++jj) {
-          const int qend = (jj / SB + 1) * SB;
-          const double piv = __shfl_sync(0xffffffffu, row[jj], jj);
-          const bool ok = piv > 0.0 && isfinite(piv);
-          if (!ok && jj < pb && fail == CP_NB) { fail = jj; fail_val = piv; }
-          const double ir = rsqrt(ok ? piv : 1.0);
-          if (lane == jj) sm.inv[jj] = ir;
-          row[jj] = (lane == jj) ? piv * ir : ((lane > jj) ? row[jj] * ir : row[jj]);
-#pragma unroll
-          for (int kk = jj + 1; kk < qend; ++kk) {
-            const double lk = __shfl_sync(0xffffffffu, row[jj], kk);
-            row[kk] = (lane >= kk) ? fma(-row[jj], lk, row[kk]) : row[kk];
+        for (int j = 0; j < CP_NB; ++j) {
+          const double* b = rows + j * CP_LS;
+          myir = (lane == j) ? ir : myir;
+          const double ir2 = ir * ir;
+          const double m = (lane > j) ? a[j] * ir2 : 0.0;  // columns < j are final
+          if (j + 1 < CP_NB) {
+            a[j + 1] = fma(-m, b[j + 1], a[j + 1]);
+            rows[(j + 1) * CP_LS + lane] = a[j + 1];
+            const double y = rsqrt_nr(a[j + 1]);
+            mypiv = (lane == j + 1) ? a[j + 1] : mypiv;
+            if (lane == j + 1) sm.inv[j + 1] = y;
           }
-          if (jj == qend - 1 && qend < CP_NB) {
 #pragma unroll
-            for (int s2 = qend - SB; s2 < qend; ++s2) sm.T[kp][lane][s2] = row[s2];
-            __syncwarp();
-#pragma unroll
-            for (int kk = qend; kk < CP_NB; ++kk) {
-              double acc = 0.0;
-#pragma unroll
-              for (int s2 = qend - SB; s2 < qend; ++s2) acc = fma(row[s2], sm.T[kp][kk][s2], acc);
-              row[kk] = (lane >= kk) ? row[kk] - acc : row[kk];
-            }
-            __syncwarp();
+          for (int r = j + 2; r < CP_NB; ++r) a[r] = fma(-m, b[r], a[r]);
+          __syncwarp();
+          if (j + 1 < CP_NB) {
+            if (lane == 0) mbar_arrive(&sm.barF[j + 1]);
+            ir = sm.inv[j + 1];
           }
         }
-        if (fail < CP_NB) {
+        // first pivot (in index order) that is <= 0 or not finite
+        const unsigned bad = __ballot_sync(0xffffffffu, lane < pb && !(mypiv > 0.0 && isfinite(mypiv)));
+        if (bad) {
+          const int fail = __ffs(bad) - 1;
+          const double fv = __shfl_sync(0xffffffffu, mypiv, fail);
           if (lane == 0) {
             sm.failed = 1;
             ctl->pivot_index = p0 + fail;
-            ctl->pivot_value = fail_val;
+            ctl->pivot_value = fv;
             raise_status(ctl, ST_NOT_PD);
           }
         } else {
 #pragma unroll
-          for (int s2 = 0; s2 < CP_NB; ++s2) Pp[lane * CP_LS + s2] = (s2 <= lane) ? row[s2] : 0.0;
-          __syncwarp();
-          // T = L^-1 (lower): lane c owns column c; t[r] = (delta_rc - sum_k L[r][k] t[k]) / L[r][r]
-          double t[CP_NB];
-#pragma unroll
-          for (int r = 0; r < CP_NB; ++r) {
-            double acc = (r == lane) ? 1.0 : 0.0;
-#pragma unroll
-            for (int k2 = 0; k2 < r; ++k2) acc = fma(-Pp[r * CP_LS + k2], t[k2], acc);
-            t[r] = acc * sm.inv[r];
-          }
-#pragma unroll
-          for (int r = 0; r < CP_NB; ++r) sm.T[kp][r][lane] = t[r];
+          for (int r = 0; r < CP_NB; ++r) Pp[r * CP_LS + lane] = (r >= lane) ? a[r] * myir : 0.0;
         }
         mark(3);
         stamp(p, 1);
+      } else if (warp == 1) {
+        // T = L^-1, right-looking, lane c owning column c, one pivot behind
+        // warp 0: t_j = t[j] / L_jj, t[r] -= L[r][j] t_j with L[r][j] = S_j[r] ir_j
+        const double* rows = &sm.rcv[0][0];
+        const uint32_t par = static_cast<uint32_t>(fac_uses & 1);
+        double t[CP_NB];
+#pragma unroll
+        for (int r = 0; r < CP_NB; ++r) t[r] = (r == lane) ? 1.0 : 0.0;
+#pragma unroll
+        for (int j = 0; j < CP_NB; ++j) {
+          mbar_wait(&sm.barF[j], par);
+          const double irj = sm.inv[j];
+          const double u = t[j] * irj * irj;
+          t[j] *= irj;
+#pragma unroll
+          for (int r = j + 1; r < CP_NB; ++r) t[r] = fma(-u, rows[j * CP_LS + r], t[r]);
+        }
+#pragma unroll
+        for (int r = 0; r < CP_NB; ++r) sm.T[kp][r][lane] = t[r];
       } else if (p > 0 && ((CP_REST_WARPS >> warp) & 1u)) {
         const int pp = p - 1;
         if ((pp % cs) == rank) {
@@ -638,6 +660,7 @@ __global__ void __launch_bounds__(CH_THREADS, 1) k_chol_panels(
         }
       }
       __syncthreads();
+      ++fac_uses;
       stamp(p, 2);
       mark(4);
       if (sm.failed) {
