@@ -62,6 +62,7 @@ struct Ctx {
   int solve_cs = 1, solve_nb = 32;
   bool solve_panels = false;  // k_chol_panels (d <= CP_MAX_D) instead of k_chol_solve
   int cp_kp = 1, cp_cs = 1;
+  bool topk_stream = false;  // one-pass sampled-window TopK (else the shared-memory radix)
   double* Lg = nullptr;       // k_chol_panels: released L panels
   double* pp_shift_part = nullptr;  // FedNL-PP: Frobenius partials [tau][PP_SB]
   // client sharding over `world` GPUs (fb_set_shard): this rank owns clients
@@ -358,7 +359,7 @@ int launch_compress(Ctx* ctx, cudaStream_t s, const int32_t* clients, int n_acti
   }
   switch (c.kind) {
     case FB_KIND_TOPK:
-      if (ctx->w <= TKS_MAXW)
+      if (ctx->w <= TKS_MAXW && !ctx->topk_stream)
         k_topk_smem<<<n_active, TK_THREADS, tks_smem_bytes(ctx->w), s>>>(
             ctl, ctx->D, ctx->w, ctx->wb, c.k, c.topk_weighted, clients, ctx->flags, ctx->bitmap,
             ctx->count, ctx->idx_list, ctx->val_list, ctx->cap, ctx->draws, em);
@@ -412,7 +413,9 @@ int launch_solve(Ctx* ctx, cudaStream_t s, const double* hpk, const double* shif
   cudaLaunchConfig_t lc{};
   lc.gridDim = dim3(cs);
   lc.blockDim = dim3(CH_THREADS);
-  lc.dynamicSmemBytes = panels ? static_cast<size_t>(ctx->cp_kp) * cp_panel_bytes(ctx->d) : ctx->solve_smem;
+  lc.dynamicSmemBytes = panels ? static_cast<size_t>(ctx->cp_kp) * cp_panel_bytes(ctx->d) +
+                                     (dbg ? CP_STAMP_BYTES : 0)
+                               : ctx->solve_smem;
   lc.stream = s;
   cudaLaunchAttribute attr[4];
   attr[0].id = cudaLaunchAttributeClusterDimension;
@@ -869,15 +872,17 @@ int fb_create(const fb_config* cfg_in, void** out) {
   static size_t max_cp = 0;
   max_cp = std::max(max_cp, static_cast<size_t>(ctx->cp_kp) * cp_panel_bytes(c.d));
   CKC(cudaFuncSetAttribute(k_chol_panels<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           static_cast<int>(std::min<size_t>(max_cp, CP_DYN_SMEM_MAX))));
+                           static_cast<int>(std::min<size_t>(max_cp + CP_STAMP_BYTES, CP_DYN_SMEM_MAX))));
   CKC(cudaFuncSetAttribute(k_chol_panels<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           static_cast<int>(std::min<size_t>(max_cp, CP_DYN_SMEM_MAX))));
+                           static_cast<int>(std::min<size_t>(max_cp + CP_STAMP_BYTES, CP_DYN_SMEM_MAX))));
   CKC(cudaFuncSetAttribute(k_chol_solve<16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            static_cast<int>(std::max(max_solve, solve_panel_bytes<16>(1)))));
 
   const int n = ctx->n, d = ctx->d;
   const size_t wn = static_cast<size_t>(w) * n;
-  const bool stream_topk = c.kind == FB_KIND_TOPK && w > TKS_MAXW && w <= TKST_MAXW;
+  const bool stream_topk = c.kind == FB_KIND_TOPK && w <= TKST_MAXW &&
+                           (w > TKS_MAXW || getenv("FB_TOPK_STREAM") != nullptr);
+  ctx->topk_stream = stream_topk;
   const int tau = ctx->tau;
   if (dalloc(ctx, &ctx->ctl, 1) || dalloc(ctx, &ctx->Bt, static_cast<size_t>(n) * d * ctx->ldj) ||
       dalloc(ctx, &ctx->x, d) || dalloc(ctx, &ctx->x_new, d) || dalloc(ctx, &ctx->pvec, d) ||

@@ -369,6 +369,9 @@ constexpr int CP_MAXP = 16;
 // block: the block factor is latency-bound on shuffles, and warps sharing
 // its scheduler / the smem pipe slow it (measured: excluding warp 4 cut the
 // per-panel factor from 8.6 to 7.5 us)
+#ifndef CP_NO_PUSH
+#define CP_NO_PUSH 0
+#endif
 #ifndef CP_REST_WARPS
 #define CP_REST_WARPS 0xECu
 #endif
@@ -390,6 +393,10 @@ __host__ __device__ constexpr int cp_rows(int d) { return (d > CP_NB ? d : CP_NB
 // dynamic shared memory for the panels: what the 227 KB per CTA leaves
 // next to the static CpSmem
 constexpr size_t CP_DYN_SMEM_MAX = 227 * 1024 - sizeof(CpSmem) - 512;
+// diagnostics (fb_solve_phase_cycles): per-CTA timestamps staged in dynamic
+// shared memory after the panels, flushed at the end (a global store per
+// stamp would itself stall behind the SM's outstanding memory traffic)
+constexpr size_t CP_STAMP_BYTES = 64 * 16 * sizeof(long long);
 __host__ __device__ constexpr size_t cp_panel_bytes(int d) {
   return static_cast<size_t>(cp_rows(d)) * CP_LS * sizeof(double);
 }
@@ -485,9 +492,15 @@ __global__ void __launch_bounds__(CH_THREADS, 1) k_chol_panels(
   };
   auto P = [&](int k) { return cpan + static_cast<size_t>(k) * RS * CP_LS; };
   // diagnostics: per-panel global timestamps (fb_debug_counters)
+  long long* stamps = reinterpret_cast<long long*>(cpan + static_cast<size_t>(KP) * RS * CP_LS);
   auto stamp = [&](int p, int k) {  // dbg[16 + 16 p + k], thread 0 of each CTA
-    if (dbg && tid == 0 && p < 64) dbg[16 + p * 16 + k] = globaltimer_ns();
+    if (dbg && tid == 0 && p < 64) stamps[p * 16 + k] = globaltimer_ns();
   };
+  auto stamp_w = [&](int p, int k, int w) {  // the same from lane 0 of warp w
+    if (dbg && tid == 32 * w && p < 64) stamps[p * 16 + k] = globaltimer_ns();
+  };
+  if (dbg)
+    for (int i = tid; i < 64 * 16; i += CH_THREADS) stamps[i] = 0;
   auto Lglob = [&](int p) { return Lg + static_cast<size_t>(p) * RS * CP_LS; };
   const int last_own = rank + ((npan - 1 - rank) / cs) * cs;  // highest own panel (rank < npan)
   int fac_uses = 0;  // block factors done by this CTA (parity of sm.barF)
@@ -682,7 +695,7 @@ __global__ void __launch_bounds__(CH_THREADS, 1) k_chol_panels(
       //     before this TRSM and the L2 copy are done.
       {
         const int nxt_owner = (p + 1) % cs;
-        const bool push = p + 1 < npan && nxt_owner != rank;
+        const bool push = !CP_NO_PUSH && p + 1 < npan && nxt_owner != rank;
         double(*rcv_remote)[CP_LS] =
             push ? cluster.map_shared_rank(sm.rcv, static_cast<unsigned>(nxt_owner)) : nullptr;
         double bt[8][4];
@@ -691,6 +704,9 @@ __global__ void __launch_bounds__(CH_THREADS, 1) k_chol_panels(
 #pragma unroll
           for (int ks = 0; ks < 8; ++ks) bt[ks][ct] = sm.T[kp][ct * 8 + (lane >> 2)][ks * 4 + (lane & 3)];
         const int t_lo = CP_NB / 8, t_hi = rs / 8;
+        // L_p's lower rows (+ rhs) also go to global memory for the other
+        // CTAs' updates, straight from the tile registers
+        double* G = (p < npan - 1 && cs > 1) ? Lglob(p) : nullptr;
         auto do_tile = [&](int tile, bool to_next) {
           const int r = tile * 8 + (lane >> 2);
           const bool ok = r < nreal || r == rs;
@@ -707,39 +723,38 @@ __global__ void __launch_bounds__(CH_THREADS, 1) k_chol_panels(
 #pragma unroll
             for (int ct = 0; ct < 4; ++ct) {
               const int cc = ct * 8 + 2 * (lane & 3);
-              Pp[r * CP_LS + cc] = acc[ct][0];
-              Pp[r * CP_LS + cc + 1] = acc[ct][1];
-              if (to_next && r < 2 * CP_NB) {
-                rcv_remote[r - CP_NB][cc] = acc[ct][0];
-                rcv_remote[r - CP_NB][cc + 1] = acc[ct][1];
-              }
+              const double2 v2 = make_double2(acc[ct][0], acc[ct][1]);
+              *reinterpret_cast<double2*>(Pp + r * CP_LS + cc) = v2;
+              if (to_next && r < 2 * CP_NB) *reinterpret_cast<double2*>(&rcv_remote[r - CP_NB][cc]) = v2;
+              if (G) __stcg(reinterpret_cast<double2*>(G + r * CP_LS + cc), v2);
             }
           }
         };
         if (warp < 4) {
           const int tile = t_lo + warp;  // slots 32 + 8 warp ..
           if (tile <= t_hi) do_tile(tile, push);
+          stamp(p, 3);
           if (push) {
-            asm volatile("bar.sync 1, 128;" ::: "memory");
+            asm volatile("bar.sync 1, 256;" ::: "memory");
             if (tid == 0) mbar_arrive_remote(&sm.barLd[p], static_cast<uint32_t>(nxt_owner));
           }
+          stamp(p, 5);
           for (int t2 = t_lo + 8 + warp; t2 <= t_hi; t2 += 8) do_tile(t2, false);
+          stamp(p, 6);
         } else {
+          // the next panel's diagonal rows (warps 0..3) go first: the DMMA
+          // pipes are shared per SM sub-partition
+          if (push) asm volatile("bar.sync 1, 256;" ::: "memory");
           for (int t2 = t_lo + 4 + (warp - 4); t2 <= t_hi; t2 += 8) do_tile(t2, false);
+          stamp_w(p, 7, 4);
         }
       }
       __syncthreads();
       stamp(p, 4);
       mark(5);
-      // L_p (rows below the block + rhs) to global for the other CTAs, then
-      // release it
+      // release L_p (written to global by the tiles above; the CTA barrier
+      // orders those stores before thread 0's cluster-scope release)
       if (p < npan - 1 && cs > 1) {
-        double* G = Lglob(p);
-        for (int e = CP_NB * CP_NB + tid; e < (rs + 1) * CP_NB; e += CH_THREADS) {
-          const int r = e / CP_NB, c = e % CP_NB;
-          G[r * CP_LS + c] = Pp[r * CP_LS + c];
-        }
-        __syncthreads();
         if (tid == 0) {
           for (int r2 = 0; r2 < cs; ++r2)
             if (r2 != rank && r2 + ((npan - 1 - r2) / cs) * cs > p)  // r2 owns a later panel
@@ -747,6 +762,7 @@ __global__ void __launch_bounds__(CH_THREADS, 1) k_chol_panels(
         }
       }
       mark(6);
+      stamp(p, 14);
       // updates from L_{p-1} deferred by the lookahead (own panels after p)
       if (p > 0) {
         const int pp = p - 1;
@@ -762,8 +778,9 @@ __global__ void __launch_bounds__(CH_THREADS, 1) k_chol_panels(
         }
         __syncthreads();
       }
+      stamp(p, 15);
     } else if (last_own > p) {
-      if ((p + 1) % cs == rank) {
+      if (!CP_NO_PUSH && (p + 1) % cs == rank) {
         // our panel is next: its diagonal rows from the pushed rows of L_p
         mbar_wait_cluster(&sm.barLd[p], 0);
         if (sm.failed) break;
@@ -785,7 +802,7 @@ __global__ void __launch_bounds__(CH_THREADS, 1) k_chol_panels(
       const int q = rank + k * cs;
       if (q <= p || q >= npan) continue;
       if (next_mine && q != p + 1) continue;  // deferred (applied after p + 1's release)
-      if (next_mine && rank != owner) continue;  // done from the DSMEM push above
+      if (!CP_NO_PUSH && next_mine && rank != owner) continue;  // done from the DSMEM push above
       const int rs_q = max(d - q * CP_NB, CP_NB);
       const int s_hi = (q == p + 1) ? CP_NB - 1 : rs_q;
       if (rank == owner)
@@ -891,6 +908,9 @@ __global__ void __launch_bounds__(CH_THREADS, 1) k_chol_panels(
     }
   }
   cluster.sync();  // no CTA leaves while its shared memory may be addressed
+  if (dbg)
+    for (int i = tid; i < 64 * 16; i += CH_THREADS)
+      if (stamps[i]) dbg[16 + i] = stamps[i];
 }
 
 }  // namespace fb

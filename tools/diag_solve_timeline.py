@@ -18,9 +18,9 @@ for d in [int(a) for a in sys.argv[1:]] or [301]:
     sp = np.array([cyc[16 + i] for i in range(1024)]).reshape(64, 16).astype(np.int64)
     npan = (d + 31) // 32
     t0 = sp[0, 0]
-    names = ["fstart", "f_w0done", "A_sync", "early_rel", "trsm_done", "recvE", "diagupd", "-", "bs_own", "bs_recv", "z_done", "st_done", "arr_done", "acc_done", "-", "-"]
+    names = ["fstart", "f_w0done", "A_sync", "w0tile1", "trsm_done", "w0rel", "w0done", "w4done", "bs_own", "bs_recv", "z_done", "st_done", "arr_done", "acc_done", "L2rel", "defer"]
     print(f"d={d} total {ms.value*1e3:.1f} us")
     for p in range(npan):
-        print(f"  p={p:2d} " + " ".join((f"{n}={(sp[p, k]-t0)/1e3:7.2f}" if k not in (7, 15) else f"{n}={sp[p, k]}") if sp[p, k] else f"{n}=   -   " for k, n in enumerate(names)))
+        print(f"  p={p:2d} " + " ".join((f"{n}={(sp[p, k]-t0)/1e3:7.2f}" if True else "") if sp[p, k] else f"{n}=   -   " for k, n in enumerate(names)))
     print("  end-factor %.2f  after-csync %.2f  bs-done %.2f" % tuple((sp[63, k] - t0) / 1e3 for k in range(3)))
     eng.close()
