@@ -618,6 +618,7 @@ __host__ __device__ constexpr size_t tkst_smem_bytes(int64_t w) {
   return 2 * static_cast<size_t>((w + 31) / 32) * 4 + 2048 * 4 + TKST_SAMPLE * 8;
 }
 constexpr int64_t TKST_MAXW = 700000;  // bitmaps + histogram + sample within 227 KB
+constexpr int64_t TKST_MINW = 32768;   // below: the shared-memory radix (k_topk_smem)
 
 __device__ __forceinline__ uint32_t key_hi(double x, int64_t t, int weighted) {
   return static_cast<uint32_t>(rank_key(x, t, weighted) >> 32);
@@ -703,39 +704,65 @@ __global__ void __launch_bounds__(TK_THREADS, 1) k_topk_stream(
     if (tid == 0) count[c] = 0;
     return;
   }
-  // ---- 1. window from a strided sample (bitonic sort, descending)
+  // ---- 1. window from a strided sample: the sample's key high words at the
+  //      two ranks ri -/+ delta, to 22 bits by two 11-bit radix levels
+  //      (rounded outwards: a slightly wider window, never a narrower one)
   {
+    uint32_t sk[2];
 #pragma unroll
     for (int u = 0; u < 2; ++u) {
       const int i = u * TK_THREADS + tid;
       const int64_t ts = (static_cast<int64_t>(i) * w) / TKST_SAMPLE;
-      skey[i] = rank_key(__ldg(v + ts), ts, weighted);
+      sk[u] = key_hi(__ldg(v + ts), ts, weighted);
     }
+    uint32_t* hist2 = reinterpret_cast<uint32_t*>(skey);  // [2048] second histogram
     for (int i = tid; i < wb; i += TK_THREADS) eqm[i] = 0u;
+    for (int i = tid; i < 2048; i += TK_THREADS) { hist[i] = 0u; hist2[i] = 0u; }
     __syncthreads();
-    for (int size = 2; size <= TKST_SAMPLE; size <<= 1) {
-      for (int stride = size >> 1; stride > 0; stride >>= 1) {
 #pragma unroll
-        for (int u = 0; u < 2; ++u) {
-          const int i = u * TK_THREADS + tid;
-          const int j = i ^ stride;
-          if (j > i) {
-            const uint64_t a = skey[i], b = skey[j];
-            const bool desc = (i & size) == 0;
-            if (desc ? (a < b) : (a > b)) { skey[i] = b; skey[j] = a; }
-          }
-        }
-        __syncthreads();
-      }
+    for (int u = 0; u < 2; ++u) tks_add(hist, sk[u] >> 21, lane);
+    __syncthreads();
+    const double r = static_cast<double>(k) * TKST_SAMPLE / static_cast<double>(w);
+    const int delta = static_cast<int>(4.0 * sqrt(r) + 16.0);
+    const int ri = static_cast<int>(r);
+    const int r_hi = ri - delta, r_lo = ri + delta;  // ranks in descending order
+    const bool has_hi = r_hi >= 0, has_lo = r_lo < TKST_SAMPLE;
+    int d1_hi = 0, d1_lo = 0, need_hi = r_hi + 1, need_lo = r_lo + 1;
+    if (has_hi) {
+      tks_find_digit(hist, 2048, need_hi, ws, &s_digit, &s_above);
+      d1_hi = s_digit;
+      need_hi -= s_above;
+      __syncthreads();
+    }
+    if (has_lo) {
+      tks_find_digit(hist, 2048, need_lo, ws, &s_digit, &s_above);
+      d1_lo = s_digit;
+      need_lo -= s_above;
+      __syncthreads();
+    }
+    // level 2: bits 20..10 of the keys in the two level-1 bins
+    for (int i = tid; i < 2048; i += TK_THREADS) hist[i] = 0u;
+    __syncthreads();
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      const uint32_t top = sk[u] >> 21, dg = (sk[u] >> 10) & 2047u;
+      tks_add(hist, (has_hi && top == static_cast<uint32_t>(d1_hi)) ? dg : 0xFFFFFFFFu, lane);
+      tks_add(hist2, (has_lo && top == static_cast<uint32_t>(d1_lo)) ? dg : 0xFFFFFFFFu, lane);
+    }
+    __syncthreads();
+    int hhi = 0x7FFFFFFF, hlo = -1;
+    if (has_hi) {
+      tks_find_digit(hist, 2048, need_hi, ws, &s_digit, &s_above);
+      hhi = static_cast<int>((static_cast<uint32_t>(d1_hi) << 21) | (static_cast<uint32_t>(s_digit) << 10) | 1023u);
+      __syncthreads();
+    }
+    if (has_lo) {
+      tks_find_digit(hist2, 2048, need_lo, ws, &s_digit, &s_above);
+      hlo = static_cast<int>((static_cast<uint32_t>(d1_lo) << 21) | (static_cast<uint32_t>(s_digit) << 10)) - 1;
+      __syncthreads();
     }
     if (tid == 0) {
-      const double r = static_cast<double>(k) * TKST_SAMPLE / static_cast<double>(w);
-      const int delta = static_cast<int>(4.0 * sqrt(r) + 16.0);
-      const int ri = static_cast<int>(r);
-      const int r_hi = ri - delta, r_lo = ri + delta;
       // high words: gt iff hk > hhi; candidate iff hlo < hk <= hhi (signed)
-      int hhi = r_hi >= 0 ? static_cast<int>(skey[r_hi] >> 32) : 0x7FFFFFFF;
-      int hlo = r_lo < TKST_SAMPLE ? static_cast<int>(skey[r_lo] >> 32) - 1 : -1;
       if (hlo >= hhi) hlo = hhi - 1;
       // exact zeros become a tie class when the window reaches them
       s_zero = hlo < 0;

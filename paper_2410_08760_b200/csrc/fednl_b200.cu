@@ -880,8 +880,11 @@ int fb_create(const fb_config* cfg_in, void** out) {
 
   const int n = ctx->n, d = ctx->d;
   const size_t wn = static_cast<size_t>(w) * n;
+  // one-pass sampled-window TopK from TKST_MINW up (c0: w = 45,451): one
+  // read of D plus candidate work beats the shared-memory radix's passes
+  const char* ts_env = getenv("FB_TOPK_STREAM");
   const bool stream_topk = c.kind == FB_KIND_TOPK && w <= TKST_MAXW &&
-                           (w > TKS_MAXW || getenv("FB_TOPK_STREAM") != nullptr);
+                           (ts_env ? atoi(ts_env) != 0 : (w > TKS_MAXW || w >= TKST_MINW));
   ctx->topk_stream = stream_topk;
   const int tau = ctx->tau;
   if (dalloc(ctx, &ctx->ctl, 1) || dalloc(ctx, &ctx->Bt, static_cast<size_t>(n) * d * ctx->ldj) ||
