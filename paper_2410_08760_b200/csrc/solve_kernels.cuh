@@ -390,6 +390,11 @@ struct CpSmem {
 };
 
 __host__ __device__ constexpr int cp_rows(int d) { return (d > CP_NB ? d : CP_NB) + 1; }
+// bytes of L_p's slots 32..63 (the next panel's diagonal rows, plus the
+// right-hand side slot when it falls there) pushed to the next owner
+__host__ __device__ constexpr uint32_t cp_push_bytes(int d, int p) {
+  return static_cast<uint32_t>((d - p * 32 >= 64 ? 32 : (d - p * 32 - 32) + 1) * 32 * 8);
+}
 // dynamic shared memory for the panels: what the 227 KB per CTA leaves
 // next to the static CpSmem
 constexpr size_t CP_DYN_SMEM_MAX = 227 * 1024 - sizeof(CpSmem) - 512;
@@ -513,6 +518,14 @@ __global__ void __launch_bounds__(CH_THREADS, 1) k_chol_panels(
     }
     for (int j = 0; j < CP_NB; ++j) mbar_init(&sm.barF[j], 1);
     fence_barrier_init();
+    // the backward substitution's z_b arrives by st.async (complete_tx): this
+    // CTA's single arrival on barZ[b] is the byte count it expects
+    for (int b = 0; b < npan; ++b)
+      if (rank < b && rank != b % cs)
+        mbar_arrive_expect_tx(&sm.barZ[b], static_cast<uint32_t>(min(CP_NB, d - b * CP_NB)) * 8u);
+    // likewise the next panel's diagonal rows of L_p (pushed in step B of p)
+    for (int p = 0; p + 1 < npan; ++p)
+      if ((p + 1) % cs == rank && p % cs != rank) mbar_arrive_expect_tx(&sm.barLd[p], cp_push_bytes(d, p));
     sm.failed = 0;
   }
   // ---- own panels from packed H (A[i][j] = H[min][max]), + shift
@@ -681,9 +694,12 @@ __global__ void __launch_bounds__(CH_THREADS, 1) k_chol_panels(
         if (tid < cs && tid != rank) {
           int* rf = cluster.map_shared_rank(&sm.failed, tid);
           *rf = 1;
+          fence_cluster();
           for (int q = p; q < npan; ++q) {
             mbar_arrive_remote(&sm.barL[q], static_cast<uint32_t>(tid));
-            mbar_arrive_remote(&sm.barLd[q], static_cast<uint32_t>(tid));
+            // barLd[q] of the next owner waits for transaction bytes
+            if (q + 1 < npan && (q + 1) % cs == tid && q % cs != tid)
+              mbar_complete_tx_remote(mapa_u32(&sm.barLd[q], static_cast<uint32_t>(tid)), cp_push_bytes(d, q));
           }
         }
         break;
@@ -696,8 +712,10 @@ __global__ void __launch_bounds__(CH_THREADS, 1) k_chol_panels(
       {
         const int nxt_owner = (p + 1) % cs;
         const bool push = !CP_NO_PUSH && p + 1 < npan && nxt_owner != rank;
-        double(*rcv_remote)[CP_LS] =
-            push ? cluster.map_shared_rank(sm.rcv, static_cast<unsigned>(nxt_owner)) : nullptr;
+        // the next owner's rcv rows and barLd[p] in the cluster window: the
+        // head tiles land there as st.async stores completing its barrier
+        const uint32_t rcv_r = push ? mapa_u32(&sm.rcv[0][0], static_cast<uint32_t>(nxt_owner)) : 0u;
+        const uint32_t bar_r = push ? mapa_u32(&sm.barLd[p], static_cast<uint32_t>(nxt_owner)) : 0u;
         double bt[8][4];
 #pragma unroll
         for (int ct = 0; ct < 4; ++ct)
@@ -725,7 +743,8 @@ __global__ void __launch_bounds__(CH_THREADS, 1) k_chol_panels(
               const int cc = ct * 8 + 2 * (lane & 3);
               const double2 v2 = make_double2(acc[ct][0], acc[ct][1]);
               *reinterpret_cast<double2*>(Pp + r * CP_LS + cc) = v2;
-              if (to_next && r < 2 * CP_NB) *reinterpret_cast<double2*>(&rcv_remote[r - CP_NB][cc]) = v2;
+              if (to_next && r < 2 * CP_NB)
+                st_async_v2f64(rcv_r + static_cast<uint32_t>(((r - CP_NB) * CP_LS + cc) * 8), bar_r, v2.x, v2.y);
               if (G) __stcg(reinterpret_cast<double2*>(G + r * CP_LS + cc), v2);
             }
           }
@@ -734,10 +753,7 @@ __global__ void __launch_bounds__(CH_THREADS, 1) k_chol_panels(
           const int tile = t_lo + warp;  // slots 32 + 8 warp ..
           if (tile <= t_hi) do_tile(tile, push);
           stamp(p, 3);
-          if (push) {
-            asm volatile("bar.sync 1, 256;" ::: "memory");
-            if (tid == 0) mbar_arrive_remote(&sm.barLd[p], static_cast<uint32_t>(nxt_owner));
-          }
+          if (push) asm volatile("bar.arrive 1, 256;" ::: "memory");
           stamp(p, 5);
           for (int t2 = t_lo + 8 + warp; t2 <= t_hi; t2 += 8) do_tile(t2, false);
           stamp(p, 6);
@@ -841,21 +857,14 @@ __global__ void __launch_bounds__(CH_THREADS, 1) k_chol_panels(
           for (int t2 = 0; t2 < CP_NB; ++t2)
             if (t2 >= lane) zs = fma(sm.T[kb][t2][lane], sm.part[0][t2], zs);
           if (lane == 0) stamp(b, 10);
-          __syncwarp();
-          if (lane < bn) {
-            sm.z[b0 + lane] = zs;
-            for (int r2 = 0; r2 < cs; ++r2)  // CTAs owning a panel before b
-              if (r2 != rank && r2 < b) *cluster.map_shared_rank(&sm.z[b0 + lane], r2) = zs;
-          }
-          __syncwarp();
-          if (lane == 0) {
-            stamp(b, 11);
-            for (int r2 = 0; r2 < cs; ++r2)
-              if (r2 != rank && r2 < b) mbar_arrive_remote(&sm.barZ[b], static_cast<uint32_t>(r2));
-            stamp(b, 12);
-          }
+          if (lane < bn) sm.z[b0 + lane] = zs;
         }
         __syncthreads();
+        // z_b to every CTA owning a panel before b, one warp per CTA, as
+        // st.async stores that complete the receiver's barZ[b] transaction
+        if (warp < cs && warp != rank && warp < b && lane < bn)
+          st_async_f64(&sm.z[b0 + lane], &sm.barZ[b], static_cast<uint32_t>(warp), sm.z[b0 + lane]);
+        stamp(b, 11);
       } else if (first_own < b) {
         mbar_wait_cluster(&sm.barZ[b], 0);
         if (b - 1 >= 0 && (b - 1) % cs == rank) stamp(b, 9);
