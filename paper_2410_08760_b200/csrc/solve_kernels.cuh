@@ -383,25 +383,36 @@ struct CpSmem {
   double w[2][CP_NB];         // back-substitution accumulators of the own panels
   double part[8][CP_NB];
   double inv[CP_NB];
-  double rcv[CP_NB][CP_LS];    // the next own panel's diagonal rows of L_p, pushed over DSMEM
-  uint64_t barL[CP_MAXP], barLd[CP_MAXP], barZ[CP_MAXP];
-  uint64_t barF[CP_NB];  // block factor: pivot j's row and 1/sqrt published
+  // slots 32..95 of L_{q-1} for the own panel q factored next, pushed over
+  // DSMEM by its owner: rows 0..31 are q's diagonal rows (and the B operand
+  // of every pending update of q), rows 32..63 the A operand of q's head
+  double rcv[2 * CP_NB][CP_LS];
+  uint64_t barL[CP_MAXP];    // L2 copy of L_p released
+  uint64_t barLd[CP_MAXP];   // rcv rows 0..31 landed (transaction bytes)
+  uint64_t barLd2[CP_MAXP];  // rcv rows 32..63 landed (transaction bytes)
+  uint64_t barZ[CP_MAXP];    // z_b landed (transaction bytes)
+  uint64_t barRF;            // the next owner's rcv is free again (second push)
+  uint64_t barF[CP_NB];      // block factor: pivot j's row and 1/sqrt published
   int failed;
 };
 
 __host__ __device__ constexpr int cp_rows(int d) { return (d > CP_NB ? d : CP_NB) + 1; }
-// bytes of L_p's slots 32..63 (the next panel's diagonal rows, plus the
-// right-hand side slot when it falls there) pushed to the next owner
-__host__ __device__ constexpr uint32_t cp_push_bytes(int d, int p) {
-  return static_cast<uint32_t>((d - p * 32 >= 64 ? 32 : (d - p * 32 - 32) + 1) * 32 * 8);
+// bytes of L_p's slots [lo, lo + 32) (lo = 32: the next panel's diagonal
+// rows; lo = 64: the A rows of its head update) pushed to the next owner:
+// real rows plus the right-hand side slot when it falls in the range
+__host__ __device__ constexpr uint32_t cp_push_bytes(int d, int p, int lo) {
+  return static_cast<uint32_t>(
+      ((d - p * 32 - lo < 0 ? 0 : (d - p * 32 - lo > 32 ? 32 : d - p * 32 - lo)) +
+       ((d - p * 32 >= lo && d - p * 32 < lo + 32) ? 1 : 0)) * 32 * 8);
 }
 // dynamic shared memory for the panels: what the 227 KB per CTA leaves
 // next to the static CpSmem
-constexpr size_t CP_DYN_SMEM_MAX = 227 * 1024 - sizeof(CpSmem) - 512;
 // diagnostics (fb_solve_phase_cycles): per-CTA timestamps staged in dynamic
 // shared memory after the panels, flushed at the end (a global store per
-// stamp would itself stall behind the SM's outstanding memory traffic)
-constexpr size_t CP_STAMP_BYTES = 64 * 16 * sizeof(long long);
+// stamp would itself stall behind the SM's outstanding memory traffic);
+// rows 0..CP_MAXP-1 per panel, row CP_MAXP for the end markers (p = 63)
+constexpr size_t CP_STAMP_BYTES = (CP_MAXP + 1) * 16 * sizeof(long long);
+constexpr size_t CP_DYN_SMEM_MAX = 227 * 1024 - sizeof(CpSmem) - 512 - CP_STAMP_BYTES;
 __host__ __device__ constexpr size_t cp_panel_bytes(int d) {
   return static_cast<size_t>(cp_rows(d)) * CP_LS * sizeof(double);
 }
@@ -473,6 +484,47 @@ __device__ __forceinline__ void cp_update(const double* __restrict__ Lp, int p, 
   }
 }
 
+// One 8-row tile (slots 8 tile ..) of panel q -= L_pp[A rows] (L_pp slots
+// 32..63)^T, pp = q - 1: the A rows (slots + 32, the right-hand side slot
+// mapped to L_pp's) come from the released L2 copy of L_pp, the B rows from
+// this CTA's pushed copy `Bs` (rcv rows 0..31).  One warp.
+__device__ __forceinline__ void cp_tile_update_l2(const double* __restrict__ Lsrc,
+                                                  const double* __restrict__ Bs, double* __restrict__ Pq,
+                                                  int tile, int d, int q0, int nreal_q, int rs_q, int rs_pp) {
+  const int lane = threadIdx.x & 31;
+  const int r = tile * 8 + (lane >> 2);
+  int src = -1;
+  if (r < nreal_q) src = r + CP_NB;
+  else if (r == rs_q) src = rs_pp;
+  double a[8];
+#pragma unroll
+  for (int ks = 0; ks < 8; ++ks)
+    a[ks] = src >= 0 ? -__ldcg(Lsrc + static_cast<int64_t>(src) * CP_LS + ks * 4 + (lane & 3)) : 0.0;
+  const bool cok = r < nreal_q || r == rs_q;
+  double acc[4][2];
+#pragma unroll
+  for (int ct = 0; ct < 4; ++ct) {
+    const int cc = ct * 8 + 2 * (lane & 3);
+    acc[ct][0] = cok ? Pq[r * CP_LS + cc] : 0.0;
+    acc[ct][1] = cok ? Pq[r * CP_LS + cc + 1] : 0.0;
+  }
+#pragma unroll
+  for (int ct = 0; ct < 4; ++ct) {
+    const int jj = ct * 8 + (lane >> 2);
+    const bool ok = q0 + jj < d;
+#pragma unroll
+    for (int ks = 0; ks < 8; ++ks)
+      dmma_8x8x4(acc[ct], a[ks], ok ? Bs[jj * CP_LS + ks * 4 + (lane & 3)] : 0.0);
+  }
+  if (cok) {
+#pragma unroll
+    for (int ct = 0; ct < 4; ++ct) {
+      const int cc = ct * 8 + 2 * (lane & 3);
+      *reinterpret_cast<double2*>(Pq + r * CP_LS + cc) = make_double2(acc[ct][0], acc[ct][1]);
+    }
+  }
+}
+
 template <int KP>
 __global__ void __launch_bounds__(CH_THREADS, 1) k_chol_panels(
     DevCtl* __restrict__ ctl, int d, const double* __restrict__ hpk,
@@ -498,14 +550,15 @@ __global__ void __launch_bounds__(CH_THREADS, 1) k_chol_panels(
   auto P = [&](int k) { return cpan + static_cast<size_t>(k) * RS * CP_LS; };
   // diagnostics: per-panel global timestamps (fb_debug_counters)
   long long* stamps = reinterpret_cast<long long*>(cpan + static_cast<size_t>(KP) * RS * CP_LS);
+  auto srow = [&](int p) { return p < CP_MAXP ? p : (p == 63 ? CP_MAXP : -1); };
   auto stamp = [&](int p, int k) {  // dbg[16 + 16 p + k], thread 0 of each CTA
-    if (dbg && tid == 0 && p < 64) stamps[p * 16 + k] = globaltimer_ns();
+    if (dbg && tid == 0 && srow(p) >= 0) stamps[srow(p) * 16 + k] = globaltimer_ns();
   };
   auto stamp_w = [&](int p, int k, int w) {  // the same from lane 0 of warp w
-    if (dbg && tid == 32 * w && p < 64) stamps[p * 16 + k] = globaltimer_ns();
+    if (dbg && tid == 32 * w && srow(p) >= 0) stamps[srow(p) * 16 + k] = globaltimer_ns();
   };
   if (dbg)
-    for (int i = tid; i < 64 * 16; i += CH_THREADS) stamps[i] = 0;
+    for (int i = tid; i < (CP_MAXP + 1) * 16; i += CH_THREADS) stamps[i] = 0;
   auto Lglob = [&](int p) { return Lg + static_cast<size_t>(p) * RS * CP_LS; };
   const int last_own = rank + ((npan - 1 - rank) / cs) * cs;  // highest own panel (rank < npan)
   int fac_uses = 0;  // block factors done by this CTA (parity of sm.barF)
@@ -514,8 +567,10 @@ __global__ void __launch_bounds__(CH_THREADS, 1) k_chol_panels(
     for (int p = 0; p < npan; ++p) {
       mbar_init(&sm.barL[p], 1);
       mbar_init(&sm.barLd[p], 1);
+      mbar_init(&sm.barLd2[p], 1);
       mbar_init(&sm.barZ[p], 1);
     }
+    mbar_init(&sm.barRF, 1);
     for (int j = 0; j < CP_NB; ++j) mbar_init(&sm.barF[j], 1);
     fence_barrier_init();
     // the backward substitution's z_b arrives by st.async (complete_tx): this
@@ -523,9 +578,12 @@ __global__ void __launch_bounds__(CH_THREADS, 1) k_chol_panels(
     for (int b = 0; b < npan; ++b)
       if (rank < b && rank != b % cs)
         mbar_arrive_expect_tx(&sm.barZ[b], static_cast<uint32_t>(min(CP_NB, d - b * CP_NB)) * 8u);
-    // likewise the next panel's diagonal rows of L_p (pushed in step B of p)
+    // likewise L_p's slots 32..95 pushed to the next owner in step B of p
     for (int p = 0; p + 1 < npan; ++p)
-      if ((p + 1) % cs == rank && p % cs != rank) mbar_arrive_expect_tx(&sm.barLd[p], cp_push_bytes(d, p));
+      if ((p + 1) % cs == rank) {
+        mbar_arrive_expect_tx(&sm.barLd[p], cp_push_bytes(d, p, 32));
+        mbar_arrive_expect_tx(&sm.barLd2[p], cp_push_bytes(d, p, 64));
+      }
     sm.failed = 0;
   }
   // ---- own panels from packed H (A[i][j] = H[min][max]), + shift
@@ -590,23 +648,32 @@ __global__ void __launch_bounds__(CH_THREADS, 1) k_chol_panels(
   cluster.sync();  // barriers initialised cluster-wide before any remote arrive
   mark(0);
 
-  // ---- factorisation
+  // ---- factorisation.  Panel p - 1's owner pushes L_{p-1}'s slots 32..95
+  //      into panel p's owner (rcv): rows 0..31 give p's diagonal block its
+  //      last update (barLd), rows 32..63 the update of p's head slots
+  //      32..63 (barLd2) — the rows whose TRSM p pushes on in turn — so the
+  //      chain from factor to factor never waits for an L2 round trip.  The
+  //      rest of p's rows take L_{p-1} from its L2 copy (barL), fused with
+  //      their TRSM in step B.  cs >= 4 here: consecutive panels always have
+  //      different owners.
   for (int p = 0; p < npan; ++p) {
     const int owner = p % cs, kp = p / cs;
     const int p0 = p * CP_NB;
     if (rank == owner) {
       double* Pp = P(kp);
       const int nreal = d - p0, rs = max(nreal, CP_NB), pb = min(CP_NB, nreal);
-      // (A) warp 0: diagonal block + inverse; warps 1..7: pending update of
-      //     the lower rows from panel p - 1
+      const int t_lo = CP_NB / 8, t_hi = rs / 8;
+      // (A) warp 0: diagonal block; warp 1: T = L_pp^-1 alongside; the rest:
+      //     the head slots' pending update from the pushed rows
       stamp(p, 0);
       if (warp == 0) {
         // Block factor on the symmetric Schur complement, lane c owning
         // column c (a[r] = S[r][c]).  By symmetry lane c's multiplier
         // S[c][j] is its own a[j], so per pivot only 1/sqrt(S[j][j]) crosses
-        // lanes (shared memory, no shuffle); row j of S is published for the
-        // trailing updates and for warp 1, which forms T = L^-1 alongside.
-        double* rows = &sm.rcv[0][0];  // free while this CTA factors (stride CP_LS)
+        // lanes (shared memory, no shuffle); row j of S is published (in the
+        // T buffer, which warp 1 overwrites only after reading every row)
+        // for the trailing updates and for warp 1.
+        double* rows = &sm.T[kp][0][0];
         double a[CP_NB];
 #pragma unroll
         for (int r = 0; r < CP_NB; ++r) a[r] = Pp[r * CP_LS + lane];
@@ -660,7 +727,7 @@ __global__ void __launch_bounds__(CH_THREADS, 1) k_chol_panels(
       } else if (warp == 1) {
         // T = L^-1, right-looking, lane c owning column c, one pivot behind
         // warp 0: t_j = t[j] / L_jj, t[r] -= L[r][j] t_j with L[r][j] = S_j[r] ir_j
-        const double* rows = &sm.rcv[0][0];
+        const double* rows = &sm.T[kp][0][0];
         const uint32_t par = static_cast<uint32_t>(fac_uses & 1);
         double t[CP_NB];
 #pragma unroll
@@ -674,16 +741,15 @@ __global__ void __launch_bounds__(CH_THREADS, 1) k_chol_panels(
 #pragma unroll
           for (int r = j + 1; r < CP_NB; ++r) t[r] = fma(-u, rows[j * CP_LS + r], t[r]);
         }
+        __syncwarp();  // every lane's last row read precedes the first T store
 #pragma unroll
         for (int r = 0; r < CP_NB; ++r) sm.T[kp][r][lane] = t[r];
       } else if (p > 0 && ((CP_REST_WARPS >> warp) & 1u)) {
-        const int pp = p - 1;
-        if ((pp % cs) == rank) {
-          cp_update<false>(P(pp / cs), pp, p, Pp, d, CP_NB, rs, 1, 8, 0, CP_REST_WARPS);
-        } else {
-          mbar_wait_cluster(&sm.barL[pp], 0);  // the L2 copy of L_{p-1}
-          cp_update<true>(Lglob(pp), pp, p, Pp, d, CP_NB, rs, 1, 8, 0, CP_REST_WARPS);
-        }
+        // head slots 32..63: A = L_{p-1} slots 64..95 (rcv rows 32..63),
+        // B = L_{p-1} slots 32..63 (rcv rows 0..31)
+        mbar_wait_cluster(&sm.barLd2[p - 1], 0);
+        cp_update<false>(&sm.rcv[0][0], p - 1, p, Pp, d, CP_NB, min(2 * CP_NB - 1, rs), 1, 8, CP_NB,
+                         CP_REST_WARPS);
       }
       __syncthreads();
       ++fac_uses;
@@ -697,35 +763,50 @@ __global__ void __launch_bounds__(CH_THREADS, 1) k_chol_panels(
           fence_cluster();
           for (int q = p; q < npan; ++q) {
             mbar_arrive_remote(&sm.barL[q], static_cast<uint32_t>(tid));
-            // barLd[q] of the next owner waits for transaction bytes
-            if (q + 1 < npan && (q + 1) % cs == tid && q % cs != tid)
-              mbar_complete_tx_remote(mapa_u32(&sm.barLd[q], static_cast<uint32_t>(tid)), cp_push_bytes(d, q));
+            // the next owner's barLd / barLd2 wait for transaction bytes
+            if (q + 1 < npan && (q + 1) % cs == tid) {
+              mbar_complete_tx_remote(mapa_u32(&sm.barLd[q], static_cast<uint32_t>(tid)), cp_push_bytes(d, q, 32));
+              mbar_complete_tx_remote(mapa_u32(&sm.barLd2[q], static_cast<uint32_t>(tid)), cp_push_bytes(d, q, 64));
+            }
           }
         }
         break;
       }
-      // (B) rows below the block: X = A T^T (in place), 8-row tiles per warp.
-      //     Warps 0..3 take slots 32..63 first — the next panel's diagonal
-      //     rows — and push them into the next owner's shared memory (DSMEM)
-      //     with an early release, so that panel's factorisation can start
-      //     before this TRSM and the L2 copy are done.
+      // (B) rows below the block: X = A T^T (in place), 8-row tiles.  Warps
+      //     0..3 take the head tiles (slots 32..63, already updated), warps
+      //     4..7 the next four (slots 64..95: their L_{p-1} update first);
+      //     both go to the next owner as st.async stores completing its
+      //     barLd / barLd2.  Then every warp takes the remaining tiles, each
+      //     updated from L_{p-1}'s L2 copy and solved in one pass.  Every
+      //     solved tile is also written to L_p's L2 copy.
       {
         const int nxt_owner = (p + 1) % cs;
-        const bool push = !CP_NO_PUSH && p + 1 < npan && nxt_owner != rank;
-        // the next owner's rcv rows and barLd[p] in the cluster window: the
-        // head tiles land there as st.async stores completing its barrier
+        const bool push = !CP_NO_PUSH && p + 1 < npan;
+        // the next owner's rcv is free once it finished the panel it last
+        // received for (its panel p + 1 - cs)
+        if (push && p + 1 >= cs) mbar_wait_cluster(&sm.barRF, 0);
         const uint32_t rcv_r = push ? mapa_u32(&sm.rcv[0][0], static_cast<uint32_t>(nxt_owner)) : 0u;
         const uint32_t bar_r = push ? mapa_u32(&sm.barLd[p], static_cast<uint32_t>(nxt_owner)) : 0u;
+        const uint32_t bar2_r = push ? mapa_u32(&sm.barLd2[p], static_cast<uint32_t>(nxt_owner)) : 0u;
         double bt[8][4];
 #pragma unroll
         for (int ct = 0; ct < 4; ++ct)
 #pragma unroll
           for (int ks = 0; ks < 8; ++ks) bt[ks][ct] = sm.T[kp][ct * 8 + (lane >> 2)][ks * 4 + (lane & 3)];
-        const int t_lo = CP_NB / 8, t_hi = rs / 8;
-        // L_p's lower rows (+ rhs) also go to global memory for the other
-        // CTAs' updates, straight from the tile registers
         double* G = (p < npan - 1 && cs > 1) ? Lglob(p) : nullptr;
-        auto do_tile = [&](int tile, bool to_next) {
+        const double* Lprev = p > 0 ? Lglob(p - 1) : nullptr;
+        const int rs_prev = p > 0 ? max(d - (p - 1) * CP_NB, CP_NB) : 0;
+        bool prev_ready = p == 0;
+        auto update_from_l2 = [&](int tile) {
+          if (p == 0) return;
+          if (!prev_ready) {
+            mbar_wait_cluster(&sm.barL[p - 1], 0);  // L_{p-1}'s L2 copy
+            prev_ready = true;
+          }
+          cp_tile_update_l2(Lprev, &sm.rcv[0][0], Pp, tile, d, p0, nreal, rs, rs_prev);
+          __syncwarp();
+        };
+        auto do_tile = [&](int tile) {
           const int r = tile * 8 + (lane >> 2);
           const bool ok = r < nreal || r == rs;
           double a[8];
@@ -738,59 +819,63 @@ __global__ void __launch_bounds__(CH_THREADS, 1) k_chol_panels(
             for (int ct = 0; ct < 4; ++ct) dmma_8x8x4(acc[ct], a[ks], bt[ks][ct]);
           __syncwarp();
           if (ok) {
+            const bool to_next = push && r < 3 * CP_NB;
+            const uint32_t bar = r < 2 * CP_NB ? bar_r : bar2_r;
 #pragma unroll
             for (int ct = 0; ct < 4; ++ct) {
               const int cc = ct * 8 + 2 * (lane & 3);
               const double2 v2 = make_double2(acc[ct][0], acc[ct][1]);
               *reinterpret_cast<double2*>(Pp + r * CP_LS + cc) = v2;
-              if (to_next && r < 2 * CP_NB)
-                st_async_v2f64(rcv_r + static_cast<uint32_t>(((r - CP_NB) * CP_LS + cc) * 8), bar_r, v2.x, v2.y);
+              if (to_next)
+                st_async_v2f64(rcv_r + static_cast<uint32_t>(((r - CP_NB) * CP_LS + cc) * 8), bar, v2.x, v2.y);
               if (G) __stcg(reinterpret_cast<double2*>(G + r * CP_LS + cc), v2);
             }
           }
         };
         if (warp < 4) {
-          const int tile = t_lo + warp;  // slots 32 + 8 warp ..
-          if (tile <= t_hi) do_tile(tile, push);
+          if (t_lo + warp <= t_hi) do_tile(t_lo + warp);
           stamp(p, 3);
-          if (push) asm volatile("bar.arrive 1, 256;" ::: "memory");
-          stamp(p, 5);
-          for (int t2 = t_lo + 8 + warp; t2 <= t_hi; t2 += 8) do_tile(t2, false);
-          stamp(p, 6);
         } else {
-          // the next panel's diagonal rows (warps 0..3) go first: the DMMA
-          // pipes are shared per SM sub-partition
-          if (push) asm volatile("bar.sync 1, 256;" ::: "memory");
-          for (int t2 = t_lo + 4 + (warp - 4); t2 <= t_hi; t2 += 8) do_tile(t2, false);
-          stamp_w(p, 7, 4);
+          const int tile = t_lo + warp;  // slots 64 + 8 (warp - 4) ..
+          if (tile <= t_hi) {
+            update_from_l2(tile);
+            do_tile(tile);
+          }
+          stamp_w(p, 5, 4);
         }
+        for (int t2 = t_lo + 8 + warp; t2 <= t_hi; t2 += 8) {
+          update_from_l2(t2);
+          do_tile(t2);
+        }
+        stamp(p, 6);
+        stamp_w(p, 7, 4);
       }
       __syncthreads();
       stamp(p, 4);
       mark(5);
-      // release L_p (written to global by the tiles above; the CTA barrier
-      // orders those stores before thread 0's cluster-scope release)
-      if (p < npan - 1 && cs > 1) {
-        if (tid == 0) {
+      // release L_p's L2 copy (the CTA barrier orders every warp's stores
+      // before thread 0's cluster-scope release)
+      if (tid == 0) {
+        if (p < npan - 1 && cs > 1)
           for (int r2 = 0; r2 < cs; ++r2)
             if (r2 != rank && r2 + ((npan - 1 - r2) / cs) * cs > p)  // r2 owns a later panel
               mbar_arrive_remote(&sm.barL[p], static_cast<uint32_t>(r2));
-        }
+        // rcv is no longer needed: its next push (for panel p + cs) may come
+        if (p + cs < npan)
+          mbar_arrive_remote(&sm.barRF, static_cast<uint32_t>((p + cs - 1) % cs));
       }
       mark(6);
       stamp(p, 14);
       // updates from L_{p-1} deferred by the lookahead (own panels after p)
-      if (p > 0) {
+      if (p > 0 && last_own > p) {
         const int pp = p - 1;
+        mbar_wait_cluster(&sm.barL[pp], 0);  // (complete: re-checked per warp)
 #pragma unroll
         for (int k = 0; k < KP; ++k) {
           const int q = rank + k * cs;
           if (q <= p || q >= npan) continue;
           const int rs_q = max(d - q * CP_NB, CP_NB);
-          if (pp % cs == rank)
-            cp_update<false>(P(pp / cs), pp, q, P(k), d, 0, rs_q, 0, 8);
-          else
-            cp_update<true>(Lglob(pp), pp, q, P(k), d, 0, rs_q, 0, 8);
+          cp_update<true>(Lglob(pp), pp, q, P(k), d, 0, rs_q, 0, 8);
         }
         __syncthreads();
       }
@@ -809,22 +894,20 @@ __global__ void __launch_bounds__(CH_THREADS, 1) k_chol_panels(
       if (sm.failed) break;
     }
     // apply L_p to the own panels after p.  Lookahead: if the next panel is
-    // ours, only its diagonal rows now (its lower rows follow in its step A)
-    // and the other own panels' updates are deferred until that panel is
-    // factored and released.
+    // ours, its diagonal rows were updated from the push above and its other
+    // rows follow in its own steps A / B; the other own panels' updates are
+    // deferred until that panel is factored and released.
     const bool next_mine = p + 1 < npan && (p + 1) % cs == rank;
 #pragma unroll
     for (int k = 0; k < KP; ++k) {
       const int q = rank + k * cs;
       if (q <= p || q >= npan) continue;
-      if (next_mine && q != p + 1) continue;  // deferred (applied after p + 1's release)
-      if (!CP_NO_PUSH && next_mine && rank != owner) continue;  // done from the DSMEM push above
+      if (next_mine) continue;
       const int rs_q = max(d - q * CP_NB, CP_NB);
-      const int s_hi = (q == p + 1) ? CP_NB - 1 : rs_q;
       if (rank == owner)
-        cp_update<false>(P(kp), p, q, P(k), d, 0, s_hi, 0, 8);
+        cp_update<false>(P(kp), p, q, P(k), d, 0, rs_q, 0, 8);
       else
-        cp_update<true>(Lglob(p), p, q, P(k), d, 0, s_hi, 0, 8);
+        cp_update<true>(Lglob(p), p, q, P(k), d, 0, rs_q, 0, 8);
     }
     __syncthreads();
     mark(8);
@@ -918,8 +1001,10 @@ __global__ void __launch_bounds__(CH_THREADS, 1) k_chol_panels(
   }
   cluster.sync();  // no CTA leaves while its shared memory may be addressed
   if (dbg)
-    for (int i = tid; i < 64 * 16; i += CH_THREADS)
-      if (stamps[i]) dbg[16 + i] = stamps[i];
+    for (int i = tid; i < (CP_MAXP + 1) * 16; i += CH_THREADS) {
+      const int row = i / 16, k = i % 16;
+      if (stamps[i]) dbg[16 + (row < CP_MAXP ? row : 63) * 16 + k] = stamps[i];
+    }
 }
 
 }  // namespace fb

@@ -22,5 +22,6 @@ for d in [int(a) for a in sys.argv[1:]] or [301]:
     print(f"d={d} total {ms.value*1e3:.1f} us")
     for p in range(npan):
         print(f"  p={p:2d} " + " ".join((f"{n}={(sp[p, k]-t0)/1e3:7.2f}" if True else "") if sp[p, k] else f"{n}=   -   " for k, n in enumerate(names)))
+    print("  rank-0 phase kcycles (mark slots 0..8):", [round(cyc[i] / 1e3, 1) for i in range(9)])
     print("  end-factor %.2f  after-csync %.2f  bs-done %.2f" % tuple((sp[63, k] - t0) / 1e3 for k in range(3)))
     eng.close()
