@@ -369,6 +369,9 @@ constexpr int CP_MAXP = 16;
 // block: the block factor is latency-bound on shuffles, and warps sharing
 // its scheduler / the smem pipe slow it (measured: excluding warp 4 cut the
 // per-panel factor from 8.6 to 7.5 us)
+#ifndef CP_MARKS
+#define CP_MARKS 0
+#endif
 #ifndef CP_NO_PUSH
 #define CP_NO_PUSH 0
 #endif
@@ -541,7 +544,7 @@ __global__ void __launch_bounds__(CH_THREADS, 1) k_chol_panels(
   const int RS = cp_rows(d);
   long long t_mark = clock64();
   auto mark = [&](int slot) {
-    if (dbg && tid == 0 && rank == 0) {
+    if (CP_MARKS && dbg && tid == 0 && rank == 0) {
       const long long now = clock64();
       dbg[slot] += now - t_mark;
       t_mark = now;
@@ -551,12 +554,20 @@ __global__ void __launch_bounds__(CH_THREADS, 1) k_chol_panels(
   // diagnostics: per-panel global timestamps (fb_debug_counters)
   long long* stamps = reinterpret_cast<long long*>(cpan + static_cast<size_t>(KP) * RS * CP_LS);
   auto srow = [&](int p) { return p < CP_MAXP ? p : (p == 63 ? CP_MAXP : -1); };
-  auto stamp = [&](int p, int k) {  // dbg[16 + 16 p + k], thread 0 of each CTA
-    if (dbg && tid == 0 && srow(p) >= 0) stamps[srow(p) * 16 + k] = globaltimer_ns();
+  // a predicated store, not a branch: a branch taken by one lane would leave
+  // the warp split for the code that follows (twice the issue slots)
+  auto stamp_if = [&](bool on, int p, int k) {
+    if (dbg) {
+      const long long tv = globaltimer_ns();
+      const int row = srow(p);
+      const uint32_t addr = smem_u32(stamps + (row < 0 ? 0 : row) * 16 + k);
+      asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %2, 0;\n\t@q st.shared.u64 [%0], %1;\n\t}" ::"r"(addr),
+                   "l"(tv), "r"(static_cast<uint32_t>(on && row >= 0))
+                   : "memory");
+    }
   };
-  auto stamp_w = [&](int p, int k, int w) {  // the same from lane 0 of warp w
-    if (dbg && tid == 32 * w && srow(p) >= 0) stamps[srow(p) * 16 + k] = globaltimer_ns();
-  };
+  auto stamp = [&](int p, int k) { stamp_if(tid == 0, p, k); };  // dbg[16 + 16 p + k], thread 0
+  auto stamp_w = [&](int p, int k, int w) { stamp_if(tid == 32 * w, p, k); };  // lane 0 of warp w
   if (dbg)
     for (int i = tid; i < (CP_MAXP + 1) * 16; i += CH_THREADS) stamps[i] = 0;
   auto Lglob = [&](int p) { return Lg + static_cast<size_t>(p) * RS * CP_LS; };
