@@ -63,6 +63,7 @@ struct Ctx {
   bool solve_panels = false;  // k_chol_panels (d <= CP_MAX_D) instead of k_chol_solve
   int cp_kp = 1, cp_cs = 1;
   bool topk_stream = false;  // one-pass sampled-window TopK (else the shared-memory radix)
+  int num_sms = 148;
   double* Lg = nullptr;       // k_chol_panels: released L panels
   double* pp_shift_part = nullptr;  // FedNL-PP: Frobenius partials [tau][PP_SB]
   // client sharding over `world` GPUs (fb_set_shard): this rank owns clients
@@ -298,10 +299,18 @@ bool sharded(const Ctx* ctx) { return ctx->world > 1 || ctx->comm != nullptr; }
 
 int launch_margins(Ctx* ctx, cudaStream_t s, const double* x, const int32_t* clients, int n_active,
                    bool with_ctl = true) {
-  dim3 grid(ctx->nblk, n_active);
-  k_margins<<<grid, MB_THREADS, ctx->d * sizeof(double), s>>>(
-      with_ctl ? ctx->ctl : nullptr, ctx->Bt, ctx->d, ctx->ni, ctx->ldj, ctx->ldh, x, clients,
-      ctx->hcoef, ctx->gcoef, ctx->loss_part, ctx->nblk);
+  if (n_active >= ctx->num_sms * 3 / 4 && mc_smem_bytes(ctx->d, ctx->ldj) <= MC_SMEM_MAX &&
+      !getenv("FB_MARGINS_OLD")) {
+    // enough clients to fill the GPU: one CTA streams each client's rows
+    k_margins_cpc<<<n_active, MC_THREADS, mc_smem_bytes(ctx->d, ctx->ldj), s>>>(
+        with_ctl ? ctx->ctl : nullptr, ctx->Bt, ctx->d, ctx->ni, ctx->ldj, ctx->ldh, x, clients,
+        ctx->hcoef, ctx->gcoef, ctx->loss_part, ctx->nblk);
+  } else {
+    dim3 grid(ctx->nblk, n_active);
+    k_margins<<<grid, MB_THREADS, ctx->d * sizeof(double), s>>>(
+        with_ctl ? ctx->ctl : nullptr, ctx->Bt, ctx->d, ctx->ni, ctx->ldj, ctx->ldh, x, clients,
+        ctx->hcoef, ctx->gcoef, ctx->loss_part, ctx->nblk);
+  }
   CKL();
   return FB_OK;
 }
@@ -829,6 +838,7 @@ int fb_create(const fb_config* cfg_in, void** out) {
     ctx->err = "libfednl_b200 needs an sm_100 (B200) device";
     return fail(FB_ERR_CUDA);
   }
+  cudaDeviceGetAttribute(&ctx->num_sms, cudaDevAttrMultiProcessorCount, dev);
 #define CKC(call)                                                     \
   do {                                                                \
     cudaError_t e_ = (call);                                          \
@@ -857,6 +867,8 @@ int fb_create(const fb_config* cfg_in, void** out) {
                            static_cast<int>(HESS_SMEM)));
   CKC(cudaFuncSetAttribute(k_topk_smem, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            static_cast<int>(TKS_SMEM)));
+  CKC(cudaFuncSetAttribute(k_margins_cpc, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           static_cast<int>(MC_SMEM_MAX)));
   CKC(cudaFuncSetAttribute(k_topk_stream, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            static_cast<int>(tkst_smem_bytes(TKST_MAXW))));
   static size_t max_fold = 0;

@@ -107,6 +107,106 @@ __global__ void __launch_bounds__(MB_THREADS) k_margins(
   if (threadIdx.x == 0) loss_part[static_cast<int64_t>(c) * nblk + blockIdx.x] = red[0] + red[1];
 }
 
+// The same outputs with one CTA per client (used when the clients alone
+// fill the GPU): the client's B_c (d x ldj doubles, contiguous) is streamed
+// once front to back.  Thread t owns the sample pair sp = t % SP (SP =
+// ldj / 2) in row group g = t / SP (G groups: rows a = g, g + G, ...), so
+// every row is read as one contiguous segment and each thread keeps 8 rows in
+// flight; the G partial margins are summed in a fixed order.  The loss
+// partials per 64-sample block are formed exactly as k_margins forms them.
+// grid n_active, block MC_THREADS, dynamic smem (d + G * 2 * SPc) doubles
+// where SPc = min(SP, MC_THREADS) (sample pairs per chunk).
+constexpr int MC_THREADS = 1024;
+__host__ __device__ constexpr int mc_pairs(int ldj) { return ldj / 2 < MC_THREADS ? ldj / 2 : MC_THREADS; }
+__host__ __device__ constexpr int mc_groups(int ldj) {
+  return MC_THREADS / mc_pairs(ldj) > 32 ? 32 : MC_THREADS / mc_pairs(ldj);
+}
+__host__ __device__ constexpr size_t mc_smem_bytes(int d, int ldj) {
+  return (static_cast<size_t>(d) + static_cast<size_t>(mc_groups(ldj)) * 2 * mc_pairs(ldj)) * sizeof(double);
+}
+constexpr size_t MC_SMEM_MAX = 96 * 1024;
+__global__ void __launch_bounds__(MC_THREADS) k_margins_cpc(
+    const DevCtl* __restrict__ ctl, const double* __restrict__ Bt, int d, int ni, int ldj,
+    int ldh, const double* __restrict__ x, const int32_t* __restrict__ clients,
+    double* __restrict__ hcoef, double* __restrict__ gcoef, double* __restrict__ loss_part,
+    int nblk) {
+  if (ctl && ctl->halt) return;
+  extern __shared__ double mcs[];
+  __shared__ double red[MC_THREADS / 32];
+  const int c = client_of(clients, blockIdx.x);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int SPc = mc_pairs(ldj), G = mc_groups(ldj);
+  double* xs = mcs;
+  double* part = mcs + d;  // [G][2 * SPc]
+  for (int a = tid; a < d; a += MC_THREADS) xs[a] = x[a];
+  __syncthreads();
+  const int SP = ldj / 2;
+  const int g = tid / SPc, sp_l = tid % SPc;
+  const double2* base = reinterpret_cast<const double2*>(Bt + static_cast<int64_t>(c) * d * ldj);
+  const int64_t rs = ldj / 2;  // row stride in double2
+  for (int sp0 = 0; sp0 < SP; sp0 += SPc) {
+    // ---- partial margins of this chunk's sample pairs over row group g
+    const int sp = sp0 + sp_l;
+    if (g < G && sp < SP) {
+      const double2* col = base + sp;
+      double2 acc[2] = {make_double2(0.0, 0.0), make_double2(0.0, 0.0)};
+      int a = g;
+      for (; a + 7 * G < d; a += 8 * G) {
+        double2 bv[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) bv[u] = __ldcs(col + static_cast<int64_t>(a + u * G) * rs);
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const double xa = xs[a + u * G];
+          acc[u & 1].x = fma(bv[u].x, xa, acc[u & 1].x);
+          acc[u & 1].y = fma(bv[u].y, xa, acc[u & 1].y);
+        }
+      }
+      for (; a < d; a += G) {
+        const double2 bv = __ldcs(col + static_cast<int64_t>(a) * rs);
+        acc[0].x = fma(bv.x, xs[a], acc[0].x);
+        acc[0].y = fma(bv.y, xs[a], acc[0].y);
+      }
+      part[g * 2 * SPc + 2 * sp_l] = acc[0].x + acc[1].x;
+      part[g * 2 * SPc + 2 * sp_l + 1] = acc[0].y + acc[1].y;
+    }
+    __syncthreads();
+    // ---- coefficients and loss partials of the chunk's samples
+    const int js0 = 2 * sp0;
+    for (int t0 = 0; t0 < 2 * SPc; t0 += MC_THREADS) {
+      const int sl = t0 + tid, js = js0 + sl;
+      double loss = 0.0;
+      if (sl < 2 * SPc && js < ldh) {
+        double mm = 0.0;
+        for (int g2 = 0; g2 < G; ++g2) mm += part[g2 * 2 * SPc + sl];
+        if (js < ni) {
+          const double sig = stable_sigmoid(mm);
+          const double nd = static_cast<double>(ni);
+          hcoef[static_cast<int64_t>(c) * ldh + js] = __ddiv_rn(__dmul_rn(sig, __dsub_rn(1.0, sig)), nd);
+          gcoef[static_cast<int64_t>(c) * ldh + js] = __ddiv_rn(__dsub_rn(sig, 1.0), nd);
+          loss = softplus_neg(mm);
+        } else {
+          hcoef[static_cast<int64_t>(c) * ldh + js] = 0.0;
+          gcoef[static_cast<int64_t>(c) * ldh + js] = 0.0;
+        }
+      }
+      const double tot = warp_sum(loss);
+      if (lane == 0) red[warp] = tot;
+      __syncthreads();
+      // block b = 64 consecutive samples: the sum of its two 32-sample warps
+      const int b = (js0 + t0) / 64 + tid;
+      if (tid < MC_THREADS / 64 && b < nblk && 64 * tid < 2 * SPc - t0)
+        loss_part[static_cast<int64_t>(c) * nblk + b] = red[2 * tid] + red[2 * tid + 1];
+      __syncthreads();
+    }
+  }
+  // padding samples past the last pair (ldj <= js < ldh) carry no weight
+  for (int js = 2 * SP + tid; js < ldh; js += MC_THREADS) {
+    hcoef[static_cast<int64_t>(c) * ldh + js] = 0.0;
+    gcoef[static_cast<int64_t>(c) * ldh + js] = 0.0;
+  }
+}
+
 // Local gradients g_c = B_c gcoef_c + lam x (oracle.py:108-121).
 // grid (ceil(d / 8), n_active), block 256: one warp per feature row.
 __global__ void __launch_bounds__(256) k_gradient(
