@@ -191,23 +191,28 @@ def run_ours(args) -> dict | None:
     eng.upload([s.bmat for s in shards])
     eng.init_state()
     eng.run_rounds(W)  # warm-up: graph capture, caches, clocks
-    plain = eng.run_rounds(K)  # same K rounds without per-kernel event retargeting
-    plain_ms = float(plain.wall_ms[-1])
     if dist is not None:
         dist.barrier()
+    # timed region: the production round graph (CUDA events only at round
+    # boundaries: a per-kernel event-record node between two kernels costs
+    # their launch overlap, 24 us per c0 round)
     with ClockSampler(local) as clk:
         t0 = time.perf_counter()
-        batch = eng.run_rounds(K, timed=True)
+        batch = eng.run_rounds(K)
         wall = time.perf_counter() - t0
-    prof = eng.profile()
     dev_ms = float(batch.wall_ms[-1])  # device time of the K rounds (events)
+    # per-kernel CUDA events (roofline, kernels_ms): the same rounds with the
+    # event-instrumented graph, right after the timed region
+    inst = eng.run_rounds(K, timed=True)
+    inst_ms = float(inst.wall_ms[-1])
+    prof = eng.profile()
     eng.close()
 
     # ---- multi-rank: max device time over ranks
     if dist is not None:
-        t = torch.tensor([dev_ms, plain_ms], dtype=torch.float64)
+        t = torch.tensor([dev_ms, inst_ms], dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        dev_ms, plain_ms = float(t[0].item()), float(t[1].item())
+        dev_ms, inst_ms = float(t[0].item()), float(t[1].item())
         dist.barrier()
     jobs = 1 if sharded else world  # replicas each run the whole job
     value = jobs * K / (dev_ms * 1e-3)
@@ -298,6 +303,8 @@ def run_ours(args) -> dict | None:
             "peak_source": "in-repo fp64 DMMA microbenchmark (MEASURED_PEAKS.json has no fp64 entry)",
             "algorithmic_flop_per_launch": counts["hessian_flop"],
             "ms_per_launch": round(hess_ms, 5),
+            "timing": (f"CUDA events around k_hessian on the round stream, {K} rounds of the "
+                       "event-instrumented round graph run right after the timed region"),
         },
         "kernels_ms": {k[3:]: round(v, 5) for k, v in prof.items() if k.startswith("ms_")},
         "memory_kernels": {
@@ -312,7 +319,7 @@ def run_ours(args) -> dict | None:
         "clocks": clk.summary(),
         "device": info["name"],
         "host_wall_s": round(wall, 4),
-        "value_without_kernel_events": round(jobs * K / (plain_ms * 1e-3), 3),
+        "value_with_kernel_events": round(jobs * K / (inst_ms * 1e-3), 3),
         "final_grad_norm_e2e": final_gn,
     }
 
