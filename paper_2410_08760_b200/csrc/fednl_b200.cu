@@ -299,6 +299,14 @@ int gather_clients(Ctx* ctx, T* base, size_t per, ncclDataType_t type, cudaStrea
 }
 bool sharded(const Ctx* ctx) { return ctx->world > 1 || ctx->comm != nullptr; }
 
+// programmatic dependent launch attributes, except under a profiler's
+// injection library (serialised launches there anyway)
+bool pdl_ok(const Ctx*) {
+  static const bool injected = getenv("CUDA_INJECTION64_PATH") != nullptr ||
+                               getenv("NV_NSIGHT_INJECTION_TRANSPORT_TYPE") != nullptr ||
+                               getenv("NV_TPS_LAUNCH_TOKEN") != nullptr;
+  return !injected && !getenv("FB_NO_PDL");
+}
 int launch_margins(Ctx* ctx, cudaStream_t s, const double* x, const int32_t* clients, int n_active,
                    bool with_ctl = true) {
   if (n_active >= ctx->num_sms * 3 / 4 && mc_smem_bytes(ctx->d, ctx->ldj) <= MC_SMEM_MAX &&
@@ -330,27 +338,47 @@ int launch_gradient(Ctx* ctx, cudaStream_t s, const double* x, const int32_t* cl
 int launch_hessian(Ctx* ctx, cudaStream_t s, const int32_t* clients, int n_active,
                    const double* hest, int64_t hest_stride, double* D, double* hess_out,
                    bool with_ctl = true, const double* fuse_grad_x = nullptr) {
-  dim3 grid(ctx->n_pairs, n_active);
   // 2 CTAs per SM (the 3-CTA register budget measured slower once the ring
-  // release was made safe, see mbar_arrive_dep)
-  auto kern = k_hessian<2>;
-  kern<<<grid, HTHREADS, HESS_SMEM, s>>>(ctx->tmap, with_ctl ? ctx->ctl : nullptr, ctx->d, ctx->ni,
-                                         ctx->ldh, ctx->hcoef, ctx->cfg.lam, clients, hest,
-                                         hest_stride, D, hess_out, ctx->frob_part, ctx->flags,
-                                         0u /* zero_mask: see mbar_arrive_dep */, ctx->gcoef,
-                                         fuse_grad_x, fuse_grad_x ? ctx->grad : nullptr);
-  CKL();
+  // release was made safe, see mbar_arrive_dep); programmatic dependent
+  // launch after the margins kernel (the TMA producer waits for it)
+  cudaLaunchConfig_t lc{};
+  lc.gridDim = dim3(ctx->n_pairs, n_active);
+  lc.blockDim = dim3(HTHREADS);
+  lc.dynamicSmemBytes = HESS_SMEM;
+  lc.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  lc.attrs = attr;
+  lc.numAttrs = pdl_ok(ctx) ? 1 : 0;
+  CK(cudaLaunchKernelEx(&lc, k_hessian<2>, ctx->tmap, static_cast<const DevCtl*>(with_ctl ? ctx->ctl : nullptr),
+                        ctx->d, ctx->ni, ctx->ldh, static_cast<const double*>(ctx->hcoef), ctx->cfg.lam, clients,
+                        hest, hest_stride, D, hess_out, ctx->frob_part, ctx->flags,
+                        0u /* zero_mask: see mbar_arrive_dep */, static_cast<const double*>(ctx->gcoef),
+                        fuse_grad_x, fuse_grad_x ? ctx->grad : nullptr));
   return FB_OK;
 }
 int launch_reduce(Ctx* ctx, cudaStream_t s, const double* x, const int32_t* clients, int n_active,
                   int n_div, bool with_frob, double* row_grad, double* row_f,
                   const double* l2_prefetch = nullptr) {
-  k_reduce<<<reduce_grid(ctx->d), RED_THREADS, 0, s>>>(ctx->ctl, n_active, clients, n_div, ctx->d, ctx->ni, ctx->nblk,
-                              ctx->n_pairs, x, ctx->cfg.lam, ctx->grad, ctx->loss_part,
-                              with_frob ? ctx->frob_part : nullptr, ctx->flags, ctx->gbar,
-                              ctx->f_cli, ctx->shift_cli, ctx->sc, row_grad, row_f, l2_prefetch,
-                              static_cast<int64_t>(ctx->w) * 8);
-  CKL();
+  // programmatic dependent launch after the Hessian pass (k_reduce waits for
+  // it after warming L2 with the solve's input)
+  cudaLaunchConfig_t lc{};
+  lc.gridDim = dim3(reduce_grid(ctx->d));
+  lc.blockDim = dim3(RED_THREADS);
+  lc.dynamicSmemBytes = 0;
+  lc.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  lc.attrs = attr;
+  lc.numAttrs = pdl_ok(ctx) ? 1 : 0;
+  CK(cudaLaunchKernelEx(&lc, k_reduce, ctx->ctl, n_active, clients, n_div, ctx->d, ctx->ni, ctx->nblk,
+                        ctx->n_pairs, x, ctx->cfg.lam, static_cast<const double*>(ctx->grad),
+                        static_cast<const double*>(ctx->loss_part),
+                        static_cast<const double*>(with_frob ? ctx->frob_part : nullptr),
+                        static_cast<const int32_t*>(ctx->flags), ctx->gbar, ctx->f_cli, ctx->shift_cli, ctx->sc,
+                        row_grad, row_f, l2_prefetch, static_cast<int64_t>(ctx->w) * 8));
   return FB_OK;
 }
 // compressor of the configured kind over `n_active` clients; seeds null =

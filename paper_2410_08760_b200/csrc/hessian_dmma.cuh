@@ -113,6 +113,8 @@ __global__ void __launch_bounds__(HTHREADS, MINB) k_hessian(
     double* __restrict__ hess_out, double* __restrict__ frob_part, int32_t* __restrict__ flags,
     uint32_t zero_mask, const double* __restrict__ gcoef, const double* __restrict__ x,
     double* __restrict__ grad) {
+  // the round reduction may launch now (it waits for this pass)
+  asm volatile("griddepcontrol.launch_dependents;");
   if (ctl && ctl->halt) return;
   extern __shared__ uint8_t smem_raw[];
   HessSmem& sm = *reinterpret_cast<HessSmem*>(
@@ -168,6 +170,8 @@ __global__ void __launch_bounds__(HTHREADS, MINB) k_hessian(
   if (warp == HCONS) {
     // ---------------- TMA producer
     if (lane == 0) {
+      // programmatic dependent launch: the margins kernel's coefficients
+      asm volatile("griddepcontrol.wait;" ::: "memory");
       for (int it = 0; it < nk; ++it) {
         const int s2 = it % HSTAGE;
         if (it >= HSTAGE) mbar_wait(&sm.empty[s2], ((it / HSTAGE) - 1) & 1);

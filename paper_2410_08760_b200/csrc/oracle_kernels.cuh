@@ -44,6 +44,8 @@ __global__ void __launch_bounds__(MB_THREADS) k_margins(
     int ldh, const double* __restrict__ x, const int32_t* __restrict__ clients,
     double* __restrict__ hcoef, double* __restrict__ gcoef, double* __restrict__ loss_part,
     int nblk) {
+  // the Hessian pass may launch now (it waits for these coefficients)
+  asm volatile("griddepcontrol.launch_dependents;");
   if (ctl && ctl->halt) return;
   extern __shared__ double xs[];
   __shared__ double part[8][MB_SAMPLES + 2];
@@ -130,6 +132,8 @@ __global__ void __launch_bounds__(MC_THREADS) k_margins_cpc(
     int ldh, const double* __restrict__ x, const int32_t* __restrict__ clients,
     double* __restrict__ hcoef, double* __restrict__ gcoef, double* __restrict__ loss_part,
     int nblk) {
+  // the Hessian pass may launch now (it waits for these coefficients)
+  asm volatile("griddepcontrol.launch_dependents;");
   if (ctl && ctl->halt) return;
   extern __shared__ double mcs[];
   __shared__ double red[MC_THREADS / 32];

@@ -49,6 +49,8 @@ __global__ void __launch_bounds__(RED_THREADS) k_reduce(
     for (int64_t off = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) * 128;
          off < l2_prefetch_bytes; off += static_cast<int64_t>(gridDim.x) * blockDim.x * 128)
       asm volatile("prefetch.global.L2 [%0];" ::"l"(reinterpret_cast<const char*>(l2_prefetch) + off));
+  // programmatic dependent launch: the Hessian pass's outputs from here on
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   __shared__ double red[32];
   __shared__ double gp[32][33];
   __shared__ double stage[2048];
