@@ -64,6 +64,12 @@ class ClockSampler:
                  "-lms", "10"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
+            # nvidia-smi needs a moment to start: the timed region begins once
+            # it is sampling, and only samples taken inside the region count
+            t_end = time.time() + 5.0
+            while not self.lines and time.time() < t_end and self.proc.poll() is None:
+                time.sleep(0.005)
+            self.skip = len(self.lines)
         except (OSError, FileNotFoundError):
             self.proc = None
         return self
@@ -73,6 +79,7 @@ class ClockSampler:
             self.lines.append(line.strip())
 
     def __exit__(self, *exc):
+        self.n_in = len(self.lines)
         if self.proc is not None:
             self.proc.terminate()
             try:
@@ -83,7 +90,7 @@ class ClockSampler:
     def summary(self) -> dict:
         sm, smax, reasons = [], 0.0, set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in self.lines:
+        for ln in self.lines[getattr(self, "skip", 0):getattr(self, "n_in", len(self.lines))]:
             p = [x.strip() for x in ln.split(",")]
             if len(p) < 9:
                 continue
@@ -396,7 +403,7 @@ def run_reference(args) -> dict | None:
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=100)
+    ap.add_argument("--steps", type=int, default=500)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--config", default="c0")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
