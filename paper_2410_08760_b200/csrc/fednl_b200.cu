@@ -66,6 +66,7 @@ struct Ctx {
   bool phase_events = false;   // per-kernel event records while capturing (timed runs)
   bool gexec_phase = false;    // the flavour the cached round graph was built with
   int num_sms = 148;
+  int32_t* pair_order = nullptr;  // Hessian tile pairs, costliest first
   double* Lg = nullptr;       // k_chol_panels: released L panels
   double* pp_shift_part = nullptr;  // FedNL-PP: Frobenius partials [tau][PP_SB]
   // client sharding over `world` GPUs (fb_set_shard): this rank owns clients
@@ -342,7 +343,7 @@ int launch_hessian(Ctx* ctx, cudaStream_t s, const int32_t* clients, int n_activ
   // release was made safe, see mbar_arrive_dep); programmatic dependent
   // launch after the margins kernel (the TMA producer waits for it)
   cudaLaunchConfig_t lc{};
-  lc.gridDim = dim3(ctx->n_pairs, n_active);
+  lc.gridDim = dim3(n_active, ctx->n_pairs);
   lc.blockDim = dim3(HTHREADS);
   lc.dynamicSmemBytes = HESS_SMEM;
   lc.stream = s;
@@ -355,7 +356,8 @@ int launch_hessian(Ctx* ctx, cudaStream_t s, const int32_t* clients, int n_activ
                         ctx->d, ctx->ni, ctx->ldh, static_cast<const double*>(ctx->hcoef), ctx->cfg.lam, clients,
                         hest, hest_stride, D, hess_out, ctx->frob_part, ctx->flags,
                         0u /* zero_mask: see mbar_arrive_dep */, static_cast<const double*>(ctx->gcoef),
-                        fuse_grad_x, fuse_grad_x ? ctx->grad : nullptr));
+                        fuse_grad_x, fuse_grad_x ? ctx->grad : nullptr,
+                        static_cast<const int32_t*>(ctx->pair_order)));
   return FB_OK;
 }
 int launch_reduce(Ctx* ctx, cudaStream_t s, const double* x, const int32_t* clients, int n_active,
@@ -965,7 +967,7 @@ int fb_create(const fb_config* cfg_in, void** out) {
       dalloc(ctx, &ctx->draws, n) ||
       dalloc(ctx, &ctx->idx_list, static_cast<size_t>(n) * ctx->cap) ||
       dalloc(ctx, &ctx->val_list, static_cast<size_t>(n) * ctx->cap) ||
-      dalloc(ctx, &ctx->seeds, n) ||
+      dalloc(ctx, &ctx->seeds, n) || dalloc(ctx, &ctx->pair_order, ctx->n_pairs) ||
       dalloc(ctx, &ctx->cand_key, stream_topk ? static_cast<size_t>(n) * TKST_CAP : 1) ||
       dalloc(ctx, &ctx->cand_pos, stream_topk ? static_cast<size_t>(n) * TKST_CAP : 1) ||
       dalloc(ctx, &ctx->sc, 1) || dalloc(ctx, &ctx->steps_table, 64) ||
@@ -988,7 +990,30 @@ int fb_create(const fb_config* cfg_in, void** out) {
   double steps[64];
   for (int i = 0; i < 64; ++i) steps[i] = c.ls_steps_table[i <= 60 ? i : 60];
   CKC(cudaMemcpyAsync(ctx->steps_table, steps, sizeof steps, cudaMemcpyHostToDevice, ctx->st));
-  CKC(cudaStreamSynchronize(ctx->st));  // zero fills and the table are in place
+  // Hessian tile pairs by decreasing DMMA work (fragment products of their
+  // active quadrants, as k_hessian specialises them), ties by pair index
+  std::vector<int32_t> order(ctx->n_pairs);
+  {
+    std::vector<int> cost(ctx->n_pairs, 0);
+    for (int J = 0; J < ctx->nb_tiles; ++J)
+      for (int I = 0; I <= J; ++I) {
+        int cst = 0;
+        for (int qd = 0; qd < 4; ++qd) {
+          const int rb = 32 * (qd & 1), cb = 32 * (qd >> 1);
+          if (I == J && rb > cb) continue;
+          const int vr = (c.d - (I * HT + rb) + 7) / 8, vc = (c.d - (J * HT + cb) + 7) / 8;
+          if (vr < 1 || vc < 1) continue;
+          const int mr = vr >= 3 ? 4 : 2, nc = vc >= 3 ? 4 : 2;
+          cst += (I == J && rb == cb) ? mr * (mr + 1) / 2 : mr * nc;
+        }
+        cost[J * (J + 1) / 2 + I] = cst;
+      }
+    for (int i = 0; i < ctx->n_pairs; ++i) order[i] = i;
+    std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return cost[a] > cost[b]; });
+  }
+  CKC(cudaMemcpyAsync(ctx->pair_order, order.data(), sizeof(int32_t) * ctx->n_pairs,
+                      cudaMemcpyHostToDevice, ctx->st));
+  CKC(cudaStreamSynchronize(ctx->st));  // zero fills and the tables are in place
   if (make_tmap(ctx) != FB_OK) return fail(FB_ERR_CUDA);
   *out = ctx;
   return rc;
