@@ -573,6 +573,9 @@ __global__ void __launch_bounds__(CH_THREADS, 1) k_chol_panels(
   auto Lglob = [&](int p) { return Lg + static_cast<size_t>(p) * RS * CP_LS; };
   const int last_own = rank + ((npan - 1 - rank) / cs) * cs;  // highest own panel (rank < npan)
   int fac_uses = 0;  // block factors done by this CTA (parity of sm.barF)
+  // per own panel: bit p' = L_{p'} still owed to it (deferred by the apply
+  // step while the CTA's next panel was two steps away)
+  uint32_t pend[2] = {0u, 0u};
 
   if (tid == 0) {
     for (int p = 0; p < npan; ++p) {
@@ -887,6 +890,11 @@ __global__ void __launch_bounds__(CH_THREADS, 1) k_chol_panels(
           if (q <= p || q >= npan) continue;
           const int rs_q = max(d - q * CP_NB, CP_NB);
           cp_update<true>(Lglob(pp), pp, q, P(k), d, 0, rs_q, 0, 8);
+          for (uint32_t m = pend[k]; m; m &= m - 1) {
+            const int pq = __ffs(m) - 1;
+            cp_update<true>(Lglob(pq), pq, q, P(k), d, 0, rs_q, 0, 8);
+          }
+          pend[k] = 0u;
         }
         __syncthreads();
       }
@@ -908,12 +916,21 @@ __global__ void __launch_bounds__(CH_THREADS, 1) k_chol_panels(
     // ours, its diagonal rows were updated from the push above and its other
     // rows follow in its own steps A / B; the other own panels' updates are
     // deferred until that panel is factored and released.
+    // Two panels before the next own panel, the other own panels' updates
+    // are owed (pend) until after that panel's step B: this CTA must be free
+    // when the next panel's diagonal rows arrive.
     const bool next_mine = p + 1 < npan && (p + 1) % cs == rank;
+    const int nq = rank > p ? rank : rank + cs;  // next own panel
+    const bool urgent = rank != owner && nq == p + 2 && nq < npan;
 #pragma unroll
     for (int k = 0; k < KP; ++k) {
       const int q = rank + k * cs;
       if (q <= p || q >= npan) continue;
       if (next_mine) continue;
+      if (urgent && q != nq) {
+        pend[k] |= 1u << p;
+        continue;
+      }
       const int rs_q = max(d - q * CP_NB, CP_NB);
       if (rank == owner)
         cp_update<false>(P(kp), p, q, P(k), d, 0, rs_q, 0, 8);
