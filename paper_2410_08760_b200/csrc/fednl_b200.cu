@@ -448,7 +448,7 @@ int launch_compress(Ctx* ctx, cudaStream_t s, const int32_t* clients, int n_acti
 int launch_solve(Ctx* ctx, cudaStream_t s, const double* hpk, const double* shift_ptr,
                  const double* rhs, const double* x, double* z, double* x_out, int mode,
                  int ignore_halt, long long* dbg = nullptr, cudaEvent_t launched = nullptr,
-                 bool force_old = false, bool after_reduce = false) {
+                 bool force_old = false, bool after_reduce = false, const CpRed* red = nullptr) {
   const bool panels = ctx->solve_panels && !force_old;
   const int cs = panels ? ctx->cp_cs : ctx->solve_cs;
   cudaLaunchConfig_t lc{};
@@ -477,6 +477,8 @@ int launch_solve(Ctx* ctx, cudaStream_t s, const double* hpk, const double* shif
     attr[lc.numAttrs].val.launchCompletionEvent.flags = 0;
     ++lc.numAttrs;
   }
+  CpRed rd{};
+  if (red && panels) rd = *red;
   if (after_reduce && panels) {
     // programmatic dependent launch: the panel setup overlaps k_reduce
     attr[lc.numAttrs].id = cudaLaunchAttributeProgrammaticStreamSerialization;
@@ -486,10 +488,10 @@ int launch_solve(Ctx* ctx, cudaStream_t s, const double* hpk, const double* shif
   if (panels) {
     if (ctx->cp_kp == 1)
       CK(cudaLaunchKernelEx(&lc, k_chol_panels<1>, ctx->ctl, ctx->d, hpk, shift_ptr, rhs, x, ctx->Lg,
-                            z, x_out, mode, ignore_halt, dbg));
+                            z, x_out, mode, ignore_halt, dbg, rd));
     else
       CK(cudaLaunchKernelEx(&lc, k_chol_panels<2>, ctx->ctl, ctx->d, hpk, shift_ptr, rhs, x, ctx->Lg,
-                            z, x_out, mode, ignore_halt, dbg));
+                            z, x_out, mode, ignore_halt, dbg, rd));
   } else if (ctx->solve_nb == 32) {
     CK(cudaLaunchKernelEx(&lc, k_chol_solve<32>, ctx->ctl, ctx->d, hpk, shift_ptr, rhs, x, ctx->M,
                           z, x_out, mode, ignore_halt, dbg));
@@ -555,7 +557,31 @@ int enqueue_fednl_round(Ctx* ctx) {
     TRY(gather_clients(ctx, ctx->flags, 1, ncclInt32, s));
   }
   TRY(record(ctx, EV_HESS_END, s));
-  TRY(launch_reduce(ctx, s, ctx->x, nullptr, n, n, true, ctx->row_grad, ctx->row_f, ctx->hmas));
+  // the round reduction: folded into the panel solve's prologue when that
+  // kernel runs (its cluster forms the scalars it needs first), else k_reduce
+  static const bool no_fuse = getenv("FB_NO_FUSED_REDUCE") && atoi(getenv("FB_NO_FUSED_REDUCE"));
+  const bool fuse_red = ctx->solve_panels && !no_fuse;
+  CpRed red{};
+  if (fuse_red) {
+    red.n_active = n;
+    red.n_div = n;
+    red.ni = ctx->ni;
+    red.nblk = ctx->nblk;
+    red.n_pairs = ctx->n_pairs;
+    red.lam = ctx->cfg.lam;
+    red.grad = ctx->grad;
+    red.loss_part = ctx->loss_part;
+    red.frob_part = ctx->frob_part;
+    red.flags = ctx->flags;
+    red.gbar = ctx->gbar;
+    red.f_cli = ctx->f_cli;
+    red.shift_cli = ctx->shift_cli;
+    red.out = ctx->sc;
+    red.row_grad = ctx->row_grad;
+    red.row_f = ctx->row_f;
+  } else {
+    TRY(launch_reduce(ctx, s, ctx->x, nullptr, n, n, true, ctx->row_grad, ctx->row_f, ctx->hmas));
+  }
   TRY(record(ctx, EV_REDUCE_END, s));
   // fork: the master solve on st, the compressor and master fold on st2.  The
   // solve's cluster is launched first and the compressor waits for its
@@ -572,7 +598,7 @@ int enqueue_fednl_round(Ctx* ctx) {
   CK(cudaStreamWaitEvent(ctx->st2, ctx->ev_fork, 0));
   TRY(launch_solve(ctx, s, ctx->hmas, &ctx->sc->shift_mean, ctx->gbar, ctx->x, ctx->pvec,
                    ctx->x_new, ls ? 2 : 0, 0, nullptr, serial ? nullptr : ctx->ev_solve_launched,
-                   false, !serial));
+                   false, !serial, fuse_red ? &red : nullptr));
   if (serial) {
     CK(cudaEventRecord(ctx->ev_solve_launched, s));
   }

@@ -30,6 +30,7 @@
 #pragma once
 #include <cooperative_groups.h>
 #include "common.cuh"
+#include "round_kernels.cuh"
 
 namespace fb {
 namespace cg = cooperative_groups;
@@ -380,6 +381,26 @@ constexpr int CP_MAXP = 16;
 #endif
 constexpr int CP_MAX_D = CP_MAXP * CP_NB;
 
+// The round reduction (k_reduce's outputs, round_kernels.cuh) folded into the
+// solve cluster's prologue: `grad` non-null selects it.  CTA r forms gbar
+// for its own panels' features (exactly the right-hand-side entries it
+// holds) and the per-client scalars of client chunk r; the cluster-wide sums
+// go through DSMEM in rank order, so every CTA derives the same shift.
+struct CpRed {
+  int n_active, n_div, ni, nblk, n_pairs;
+  double lam;
+  const double* grad;        // [n][d] local gradients (Hessian pass)
+  const double* loss_part;   // [n][nblk]
+  const double* frob_part;   // [n][n_pairs]
+  const int32_t* flags;      // [n]
+  double* gbar;              // [d]
+  double* f_cli;             // [n]
+  double* shift_cli;         // [n]
+  RoundScalars* out;
+  double* row_grad;
+  double* row_f;
+};
+
 struct CpSmem {
   double T[2][CP_NB][CP_LS];  // inverse diagonal blocks of the own panels
   double z[CP_MAX_D];         // solution entries released so far
@@ -396,6 +417,10 @@ struct CpSmem {
   uint64_t barZ[CP_MAXP];    // z_b landed (transaction bytes)
   uint64_t barRF;            // the next owner's rcv is free again (second push)
   uint64_t barF[CP_NB];      // block factor: pivot j's row and 1/sqrt published
+  double rpart[4];           // fused reduction: this CTA's partials (gg, fs, ss, bad)
+  double gown[2 * CP_NB];    // fused reduction: gbar of the own panels' features
+  double rscr[8];
+  int rbad;
   int failed;
 };
 
@@ -533,7 +558,7 @@ __global__ void __launch_bounds__(CH_THREADS, 1) k_chol_panels(
     DevCtl* __restrict__ ctl, int d, const double* __restrict__ hpk,
     const double* __restrict__ shift_ptr, const double* __restrict__ rhs,
     const double* __restrict__ x, double* __restrict__ Lg, double* __restrict__ z,
-    double* __restrict__ x_out, int mode, int ignore_halt, long long* __restrict__ dbg) {
+    double* __restrict__ x_out, int mode, int ignore_halt, long long* __restrict__ dbg, CpRed red) {
   cg::cluster_group cluster = cg::this_cluster();
   __shared__ CpSmem sm;
   extern __shared__ __align__(16) double cpan[];
@@ -587,6 +612,7 @@ __global__ void __launch_bounds__(CH_THREADS, 1) k_chol_panels(
     mbar_init(&sm.barRF, 1);
     for (int j = 0; j < CP_NB; ++j) mbar_init(&sm.barF[j], 1);
     fence_barrier_init();
+    sm.rbad = 0x7fffffff;
     // the backward substitution's z_b arrives by st.async (complete_tx): this
     // CTA's single arrival on barZ[b] is the byte count it expects
     for (int b = 0; b < npan; ++b)
@@ -646,7 +672,87 @@ __global__ void __launch_bounds__(CH_THREADS, 1) k_chol_panels(
   // the right-hand side come from k_reduce, so wait for it here.  Without a
   // programmatic dependency the wait returns at once.
   asm volatile("griddepcontrol.wait;" ::: "memory");
-  const double shift = shift_ptr ? __ldcg(shift_ptr) : 0.0;
+  double shift = 0.0;
+  const bool fused = red.grad != nullptr;
+  bool skip_solve = false;  // fused reduction found a non-finite client (uniform)
+  if (fused) {
+    // ---- the round reduction (k_reduce), cluster-parallel
+    const int n = red.n_active;
+    double(*rwork)[2 * CP_NB] = reinterpret_cast<double(*)[2 * CP_NB]>(&sm.T[0][0][0]);  // free until the factor
+    // (a) gbar of the own panels' features: warp w sums clients w, w + 8, ..
+    //     for features lo + lane (+ 32), coalesced; then the 8 warps in order
+    const int q_lo = rank;  // own panels rank, rank + cs (feature slots 0..63)
+    double acc0 = 0.0, acc1 = 0.0;
+    const int a0 = q_lo * CP_NB + lane;
+    const int a1 = (KP > 1 && q_lo + cs < npan) ? (q_lo + cs) * CP_NB + lane : d;
+    for (int c0 = warp; c0 < n; c0 += 8 * 6) {
+      double v0[6], v1[6];
+#pragma unroll
+      for (int u = 0; u < 6; ++u) {
+        const int c = c0 + 8 * u;
+        v0[u] = (c < n && a0 < d) ? __ldcg(red.grad + static_cast<int64_t>(c) * d + a0) : 0.0;
+        v1[u] = (c < n && a1 < d) ? __ldcg(red.grad + static_cast<int64_t>(c) * d + a1) : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < 6; ++u) {
+        acc0 = __dadd_rn(acc0, v0[u]);
+        acc1 = __dadd_rn(acc1, v1[u]);
+      }
+    }
+    rwork[warp][lane] = acc0;
+    rwork[warp][CP_NB + lane] = acc1;
+    // (b) per-client scalars of chunk `rank`
+    const int cpc = (n + cs - 1) / cs;
+    const int c_lo = min(n, rank * cpc), c_hi = min(n, c_lo + cpc);
+    double xx_p = 0.0;
+    for (int a = tid; a < d; a += CH_THREADS) xx_p = fma(x[a], x[a], xx_p);
+    double fs_t = 0.0, ss_t = 0.0;
+    int bad_t = 0x7fffffff;
+    __syncthreads();
+    const double xx = block_sum(xx_p, sm.rscr);
+    const double reg = __dmul_rn(__dmul_rn(0.5, red.lam), xx);
+    if (tid < 2 * CP_NB) {
+      double t2 = 0.0;
+#pragma unroll
+      for (int w2 = 0; w2 < 8; ++w2) t2 = __dadd_rn(t2, rwork[w2][tid]);
+      sm.gown[tid] = __ddiv_rn(t2, static_cast<double>(red.n_div));
+    }
+    for (int c = c_lo + tid; c < c_hi; c += CH_THREADS) {
+      double ls = 0.0, fp = 0.0;
+      for (int r = 0; r < red.nblk; ++r) ls = __dadd_rn(ls, __ldcg(red.loss_part + static_cast<int64_t>(c) * red.nblk + r));
+      for (int r = 0; r < red.n_pairs; ++r) fp = __dadd_rn(fp, __ldcg(red.frob_part + static_cast<int64_t>(c) * red.n_pairs + r));
+      const double fc = __dadd_rn(__ddiv_rn(ls, static_cast<double>(red.ni)), reg);
+      const double sc = sqrt(fp);
+      red.f_cli[c] = fc;
+      red.shift_cli[c] = sc;
+      fs_t += fc;
+      ss_t += sc;
+      if (red.flags[c] & 1) bad_t = min(bad_t, c);
+    }
+    __syncthreads();
+    double gg_t = 0.0;
+    if (tid < 2 * CP_NB) {
+      const int a = tid < CP_NB ? a0 - lane + tid : (a1 < d ? a1 - lane + tid - CP_NB : d);
+      if (a < d) {
+        const double g = sm.gown[tid];
+        red.gbar[a] = g;
+        gg_t = g * g;
+      }
+    }
+    const double gg = block_sum(gg_t, sm.rscr);
+    const double fs = block_sum(fs_t, sm.rscr);
+    const double ss = block_sum(ss_t, sm.rscr);
+    bad_t = __reduce_min_sync(0xffffffffu, bad_t);
+    if (lane == 0 && bad_t != 0x7fffffff) atomicMin(&sm.rbad, bad_t);
+    __syncthreads();
+    if (tid == 0) {
+      sm.rpart[0] = gg;
+      sm.rpart[1] = fs;
+      sm.rpart[2] = ss;
+      sm.rpart[3] = static_cast<double>(sm.rbad);
+      sm.rscr[0] = xx;
+    }
+  }
   __syncthreads();
 #pragma unroll
   for (int k = 0; k < KP; ++k) {
@@ -654,12 +760,47 @@ __global__ void __launch_bounds__(CH_THREADS, 1) k_chol_panels(
     if (q >= npan) break;
     const int q0 = q * CP_NB, nreal = d - q0, rs = max(nreal, CP_NB), pb = min(CP_NB, nreal);
     double* Pq = P(k);
-    if (tid < CP_NB) {
-      Pq[rs * CP_LS + tid] = tid < pb ? __ldcg(rhs + q0 + tid) : 0.0;
-      if (tid < pb) Pq[tid * CP_LS + tid] = __dadd_rn(Pq[tid * CP_LS + tid], shift);
-    }
+    if (tid < CP_NB)
+      Pq[rs * CP_LS + tid] = tid < pb ? (fused ? sm.gown[k * CP_NB + tid] : __ldcg(rhs + q0 + tid)) : 0.0;
   }
-  cluster.sync();  // barriers initialised cluster-wide before any remote arrive
+  cluster.sync();  // barriers initialised and reduction partials published cluster-wide
+  if (fused) {
+    // cluster sums in rank order (identical in every CTA)
+    double gg = 0.0, fs = 0.0, ss = 0.0, bad = 2147483647.0;
+    for (int r2 = 0; r2 < cs; ++r2) {
+      const double* rp = cluster.map_shared_rank(&sm.rpart[0], r2);
+      gg += rp[0];
+      fs += rp[1];
+      ss += rp[2];
+      bad = fmin(bad, rp[3]);
+    }
+    shift = __ddiv_rn(ss, static_cast<double>(red.n_div));
+    if (rank == 0 && tid == 0) {
+      red.out->grad_norm = sqrt(gg);
+      red.out->f_mean = __ddiv_rn(fs, static_cast<double>(red.n_div));
+      red.out->shift_mean = shift;
+      red.out->xx = sm.rscr[0];
+      const int slot = ctl->round - ctl->row_base;
+      if (red.row_grad) red.row_grad[slot] = red.out->grad_norm;
+      if (red.row_f) red.row_f[slot] = red.out->f_mean;
+      if (bad < 2147483647.0) {
+        ctl->bad_client = static_cast<int32_t>(bad);
+        raise_status(ctl, ST_NONFINITE);
+      }
+    }
+    skip_solve = bad < 2147483647.0;  // the same partials in every CTA: no solve this round
+  } else {
+    shift = shift_ptr ? __ldcg(shift_ptr) : 0.0;
+  }
+#pragma unroll
+  for (int k = 0; k < KP; ++k) {
+    const int q = rank + k * cs;
+    if (q >= npan) break;
+    const int pb = min(CP_NB, d - q * CP_NB);
+    double* Pq = P(k);
+    if (tid < pb) Pq[tid * CP_LS + tid] = __dadd_rn(Pq[tid * CP_LS + tid], shift);
+  }
+  __syncthreads();
   mark(0);
 
   // ---- factorisation.  Panel p - 1's owner pushes L_{p-1}'s slots 32..95
@@ -670,7 +811,7 @@ __global__ void __launch_bounds__(CH_THREADS, 1) k_chol_panels(
   //      rest of p's rows take L_{p-1} from its L2 copy (barL), fused with
   //      their TRSM in step B.  cs >= 4 here: consecutive panels always have
   //      different owners.
-  for (int p = 0; p < npan; ++p) {
+  for (int p = 0; p < npan && !skip_solve; ++p) {
     const int owner = p % cs, kp = p / cs;
     const int p0 = p * CP_NB;
     if (rank == owner) {
@@ -944,7 +1085,7 @@ __global__ void __launch_bounds__(CH_THREADS, 1) k_chol_panels(
   if (rank == 0) stamp(63, 0);
   cluster.sync();  // failure flags settled cluster-wide
   if (rank == 0) stamp(63, 1);
-  if (!sm.failed) {
+  if (!sm.failed && !skip_solve) {
     // ---- backward substitution: L^T z = y, panel by panel from the last
     if (tid < 2 * CP_NB) sm.w[tid / CP_NB][tid % CP_NB] = 0.0;
     __syncthreads();
