@@ -685,16 +685,17 @@ __global__ void __launch_bounds__(CH_THREADS, 1) k_chol_panels(
     double acc0 = 0.0, acc1 = 0.0;
     const int a0 = q_lo * CP_NB + lane;
     const int a1 = (KP > 1 && q_lo + cs < npan) ? (q_lo + cs) * CP_NB + lane : d;
-    for (int c0 = warp; c0 < n; c0 += 8 * 6) {
-      double v0[6], v1[6];
+    constexpr int GU = 18;  // clients per warp and batch: n <= 144 in one round trip
+    for (int c0 = warp; c0 < n; c0 += 8 * GU) {
+      double v0[GU], v1[GU];
 #pragma unroll
-      for (int u = 0; u < 6; ++u) {
+      for (int u = 0; u < GU; ++u) {
         const int c = c0 + 8 * u;
         v0[u] = (c < n && a0 < d) ? __ldcg(red.grad + static_cast<int64_t>(c) * d + a0) : 0.0;
         v1[u] = (c < n && a1 < d) ? __ldcg(red.grad + static_cast<int64_t>(c) * d + a1) : 0.0;
       }
 #pragma unroll
-      for (int u = 0; u < 6; ++u) {
+      for (int u = 0; u < GU; ++u) {
         acc0 = __dadd_rn(acc0, v0[u]);
         acc1 = __dadd_rn(acc1, v1[u]);
       }
@@ -717,17 +718,32 @@ __global__ void __launch_bounds__(CH_THREADS, 1) k_chol_panels(
       for (int w2 = 0; w2 < 8; ++w2) t2 = __dadd_rn(t2, rwork[w2][tid]);
       sm.gown[tid] = __ddiv_rn(t2, static_cast<double>(red.n_div));
     }
-    for (int c = c_lo + tid; c < c_hi; c += CH_THREADS) {
+    // warp per client: the lanes load its loss / Frobenius partials at once,
+    // the sums run in partial order through shuffles
+    const int per_c = red.nblk + red.n_pairs;
+    for (int c = c_lo + warp; c < c_hi; c += 8) {
       double ls = 0.0, fp = 0.0;
-      for (int r = 0; r < red.nblk; ++r) ls = __dadd_rn(ls, __ldcg(red.loss_part + static_cast<int64_t>(c) * red.nblk + r));
-      for (int r = 0; r < red.n_pairs; ++r) fp = __dadd_rn(fp, __ldcg(red.frob_part + static_cast<int64_t>(c) * red.n_pairs + r));
+      for (int r0 = 0; r0 < per_c; r0 += 32) {
+        const int r = r0 + lane;
+        const double v = r < red.nblk ? __ldcg(red.loss_part + static_cast<int64_t>(c) * red.nblk + r)
+                         : r < per_c   ? __ldcg(red.frob_part + static_cast<int64_t>(c) * red.n_pairs + (r - red.nblk))
+                                       : 0.0;
+        const int m = min(32, per_c - r0);
+        for (int i = 0; i < m; ++i) {
+          const double vi = __shfl_sync(0xffffffffu, v, i);
+          if (r0 + i < red.nblk) ls = __dadd_rn(ls, vi);
+          else fp = __dadd_rn(fp, vi);
+        }
+      }
       const double fc = __dadd_rn(__ddiv_rn(ls, static_cast<double>(red.ni)), reg);
       const double sc = sqrt(fp);
-      red.f_cli[c] = fc;
-      red.shift_cli[c] = sc;
-      fs_t += fc;
-      ss_t += sc;
-      if (red.flags[c] & 1) bad_t = min(bad_t, c);
+      if (lane == 0) {
+        red.f_cli[c] = fc;
+        red.shift_cli[c] = sc;
+        fs_t += fc;
+        ss_t += sc;
+        if (red.flags[c] & 1) bad_t = min(bad_t, c);
+      }
     }
     __syncthreads();
     double gg_t = 0.0;
