@@ -582,3 +582,31 @@ def test_sharded_path_world1_matches_unsharded():
             eng.close()
     for a, b in zip(out[0], out[1]):
         assert np.array_equal(np.asarray(a), np.asarray(b))
+
+
+@pytest.mark.parametrize("d", [69, 161])  # k_chol_solve path / panel path (fused reduction)
+def test_round_rejects_nonfinite_client_hessian(d):
+    """A client whose data makes H_i(x) - H_i^k non-finite stops the round the
+    way the reference's client compressor does (ValueError), from either
+    round-reduction path."""
+    rng = np.random.default_rng(d)
+    n, ni = 6, 40
+    bmats = []
+    for _ in range(n):
+        feats = (rng.random((d - 1, ni)) < 0.2).astype(np.float64)
+        y = np.where(rng.random(ni) < 0.5, 1.0, -1.0)
+        bmats.append(np.asfortranarray(np.vstack([feats, np.ones((1, ni))]) * y))
+    cfg = RunConfig(algorithm="fednl", compressor=CompressorSpec(CompressorKind.TOPK, k=2 * d),
+                    rounds=3, run_seed=1)
+    eng = FedNLEngine(cfg, d, n, ni, lam=1e-3)
+    try:
+        eng.upload(bmats)
+        eng.init_state()
+        eng.run_rounds(1)  # finite data: fine
+        bad = [b.copy(order="F") for b in bmats]
+        bad[3][5, 7] = np.inf  # client 3's next Hessian is non-finite
+        eng.upload(bad)
+        with pytest.raises(ValueError):
+            eng.run_rounds(1)
+    finally:
+        eng.close()
