@@ -300,6 +300,16 @@ int gather_clients(Ctx* ctx, T* base, size_t per, ncclDataType_t type, cudaStrea
 }
 bool sharded(const Ctx* ctx) { return ctx->world > 1 || ctx->comm != nullptr; }
 
+// clients per Hessian dispatch group: about 2.5 waves of CTAs (2 per SM).
+// Measured at c0 (n=142, 15 pairs): one group (pure costliest-first) 244 us
+// and 586 MB of DRAM traffic, 3 groups of 48: 240 us and 218 MB, 10-client
+// groups 250 us — the group's B rows stay in L2 for its tiles while each
+// group's last wave still ends on the cheap tiles.
+int hess_group(const Ctx* ctx) {
+  static const int env = getenv("FB_HESS_GROUP") ? atoi(getenv("FB_HESS_GROUP")) : 0;
+  if (env > 0) return env;
+  return std::max(1, 5 * ctx->num_sms / std::max(1, ctx->n_pairs));
+}
 // programmatic dependent launch attributes, except under a profiler's
 // injection library (serialised launches there anyway)
 bool pdl_ok(const Ctx*) {
@@ -343,7 +353,7 @@ int launch_hessian(Ctx* ctx, cudaStream_t s, const int32_t* clients, int n_activ
   // release was made safe, see mbar_arrive_dep); programmatic dependent
   // launch after the margins kernel (the TMA producer waits for it)
   cudaLaunchConfig_t lc{};
-  lc.gridDim = dim3(n_active, ctx->n_pairs);
+  lc.gridDim = dim3(n_active * ctx->n_pairs);
   lc.blockDim = dim3(HTHREADS);
   lc.dynamicSmemBytes = HESS_SMEM;
   lc.stream = s;
@@ -357,7 +367,7 @@ int launch_hessian(Ctx* ctx, cudaStream_t s, const int32_t* clients, int n_activ
                         hest, hest_stride, D, hess_out, ctx->frob_part, ctx->flags,
                         0u /* zero_mask: see mbar_arrive_dep */, static_cast<const double*>(ctx->gcoef),
                         fuse_grad_x, fuse_grad_x ? ctx->grad : nullptr,
-                        static_cast<const int32_t*>(ctx->pair_order)));
+                        static_cast<const int32_t*>(ctx->pair_order), ctx->n_pairs, hess_group(ctx)));
   return FB_OK;
 }
 int launch_reduce(Ctx* ctx, cudaStream_t s, const double* x, const int32_t* clients, int n_active,

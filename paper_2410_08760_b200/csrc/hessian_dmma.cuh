@@ -112,7 +112,7 @@ __global__ void __launch_bounds__(HTHREADS, MINB) k_hessian(
     const double* __restrict__ hest, int64_t hest_stride, double* __restrict__ D,
     double* __restrict__ hess_out, double* __restrict__ frob_part, int32_t* __restrict__ flags,
     uint32_t zero_mask, const double* __restrict__ gcoef, const double* __restrict__ x,
-    double* __restrict__ grad, const int32_t* __restrict__ pair_order) {
+    double* __restrict__ grad, const int32_t* __restrict__ pair_order, int n_pairs_arg, int grp) {
   // the round reduction may launch now (it waits for this pass)
   asm volatile("griddepcontrol.launch_dependents;");
   if (ctl && ctl->halt) return;
@@ -120,19 +120,25 @@ __global__ void __launch_bounds__(HTHREADS, MINB) k_hessian(
   HessSmem& sm = *reinterpret_cast<HessSmem*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
 
-  // grid (clients, pairs): CTAs are dispatched client-fastest, pairs in
-  // `pair_order` (costliest tile pairs first: the last wave is the cheap
-  // diagonal / edge tiles, which shortens the tail)
-  const int slot = blockIdx.x;
+  // 1-D grid over (client group, pair, client): groups of `grp` clients in
+  // order (a group's B rows stay in L2 while its tiles run); inside a group
+  // the tile pairs go costliest first (`pair_order`), so every wave — the
+  // last one included — ends on the cheap diagonal / edge tiles
+  const int n_pairs = n_pairs_arg;
+  const int n_act = static_cast<int>(gridDim.x) / n_pairs;
+  const int L = blockIdx.x;
+  const int g0 = (L / (grp * n_pairs)) * grp;  // first client of the group
+  const int gs = min(grp, n_act - g0);
+  const int rem = L - g0 * n_pairs;
+  const int slot = g0 + rem % gs;
   const int c = client_of(clients, slot);
-  const int pair = pair_order[blockIdx.y];
+  const int pair = pair_order[rem / gs];
   // pair -> (I, J), I <= J, column-wise like the packed layout
   int J = static_cast<int>((sqrtf(8.0f * pair + 1.0f) - 1.0f) * 0.5f);
   while ((J + 1) * (J + 2) / 2 <= pair) ++J;
   while (J * (J + 1) / 2 > pair) --J;
   const int I = pair - J * (J + 1) / 2;
   const bool diag = (I == J);
-  const int n_pairs = gridDim.y;
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int g = lane >> 2, t = lane & 3;
