@@ -154,22 +154,19 @@ __global__ void __launch_bounds__(MC_THREADS) k_margins_cpc(
     if (g < G && sp < SP) {
       const double2* col = base + sp;
       double2 acc[2] = {make_double2(0.0, 0.0), make_double2(0.0, 0.0)};
-      int a = g;
-      for (; a + 7 * G < d; a += 8 * G) {
+      // 8 rows per batch, the last batch predicated (no one-row tail loop:
+      // every batch is one memory round trip)
+      for (int a = g; a < d; a += 8 * G) {
         double2 bv[8];
 #pragma unroll
-        for (int u = 0; u < 8; ++u) bv[u] = __ldcs(col + static_cast<int64_t>(a + u * G) * rs);
+        for (int u = 0; u < 8; ++u)  // rows past d re-read row d-1 (weight 0): no branch
+          bv[u] = __ldcs(col + static_cast<int64_t>(min(a + u * G, d - 1)) * rs);
 #pragma unroll
         for (int u = 0; u < 8; ++u) {
-          const double xa = xs[a + u * G];
+          const double xa = a + u * G < d ? xs[a + u * G] : 0.0;
           acc[u & 1].x = fma(bv[u].x, xa, acc[u & 1].x);
           acc[u & 1].y = fma(bv[u].y, xa, acc[u & 1].y);
         }
-      }
-      for (; a < d; a += G) {
-        const double2 bv = __ldcs(col + static_cast<int64_t>(a) * rs);
-        acc[0].x = fma(bv.x, xs[a], acc[0].x);
-        acc[0].y = fma(bv.y, xs[a], acc[0].y);
       }
       part[g * 2 * SPc + 2 * sp_l] = acc[0].x + acc[1].x;
       part[g * 2 * SPc + 2 * sp_l + 1] = acc[0].y + acc[1].y;
