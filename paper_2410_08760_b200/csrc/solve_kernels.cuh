@@ -449,6 +449,46 @@ __host__ __device__ constexpr size_t cp_panel_bytes(int d) {
 // tiles of 8, warps [w_lo, w_hi) round robin).  L_p is read from global
 // (__ldcg: written by another SM during this launch) or from local shared
 // memory.
+// The receiver's diagonal-block update from the pushed rows (slots 0..31 of
+// panel q, A = B = rcv rows 0..31): the four 8-row tiles in column halves
+// over all eight warps (16 DMMAs each).
+__device__ __forceinline__ void cp_update_diag8(const double* __restrict__ Lr, double* __restrict__ Pq,
+                                                int d, int q0, int nreal_q) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int tile = warp & 3, h = warp >> 2;
+  double b[8][2];
+#pragma unroll
+  for (int j = 0; j < 2; ++j) {
+    const int jj = (2 * h + j) * 8 + (lane >> 2);
+    const bool ok = q0 + jj < d;
+#pragma unroll
+    for (int ks = 0; ks < 8; ++ks) b[ks][j] = ok ? Lr[jj * CP_LS + ks * 4 + (lane & 3)] : 0.0;
+  }
+  const int r = tile * 8 + (lane >> 2);
+  const bool rok = r < nreal_q;
+  double a[8];
+#pragma unroll
+  for (int ks = 0; ks < 8; ++ks) a[ks] = rok ? -Lr[r * CP_LS + ks * 4 + (lane & 3)] : 0.0;
+  double acc[2][2];
+#pragma unroll
+  for (int j = 0; j < 2; ++j) {
+    const int cc = (2 * h + j) * 8 + 2 * (lane & 3);
+    acc[j][0] = rok ? Pq[r * CP_LS + cc] : 0.0;
+    acc[j][1] = rok ? Pq[r * CP_LS + cc + 1] : 0.0;
+  }
+#pragma unroll
+  for (int ks = 0; ks < 8; ++ks)
+#pragma unroll
+    for (int j = 0; j < 2; ++j) dmma_8x8x4(acc[j], a[ks], b[ks][j]);
+  if (rok) {
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+      const int cc = (2 * h + j) * 8 + 2 * (lane & 3);
+      *reinterpret_cast<double2*>(Pq + r * CP_LS + cc) = make_double2(acc[j][0], acc[j][1]);
+    }
+  }
+}
+
 template <bool GLOBAL>
 __device__ __forceinline__ void cp_update(const double* __restrict__ Lp, int p, int q,
                                           double* __restrict__ Pq, int d, int s_lo, int s_hi,
@@ -1003,10 +1043,37 @@ __global__ void __launch_bounds__(CH_THREADS, 1) k_chol_panels(
             }
           }
         };
-        if (warp < 4) {
-          if (t_lo + warp <= t_hi) do_tile(t_lo + warp);
+        // the head tiles on all eight warps (column halves: 16 DMMAs each)
+        {
+          const int tile = t_lo + (warp & 3), h = warp >> 2;
+          if (tile <= t_hi) {
+            const int r = tile * 8 + (lane >> 2);
+            double acc[2][2] = {};
+            const bool ok = r < nreal || r == rs;
+            double a[8];
+#pragma unroll
+            for (int ks = 0; ks < 8; ++ks) a[ks] = ok ? Pp[r * CP_LS + ks * 4 + (lane & 3)] : 0.0;
+#pragma unroll
+            for (int ks = 0; ks < 8; ++ks)
+#pragma unroll
+              for (int j = 0; j < 2; ++j) dmma_8x8x4(acc[j], a[ks], h ? bt[ks][2 + j] : bt[ks][j]);
+            asm volatile("bar.sync 1, 256;" ::: "memory");  // both halves read the rows first
+            if (ok) {
+#pragma unroll
+              for (int j = 0; j < 2; ++j) {
+                const int cc = (2 * h + j) * 8 + 2 * (lane & 3);
+                const double2 v2 = make_double2(acc[j][0], acc[j][1]);
+                *reinterpret_cast<double2*>(Pp + r * CP_LS + cc) = v2;
+                if (push) st_async_v2f64(rcv_r + static_cast<uint32_t>(((r - CP_NB) * CP_LS + cc) * 8), bar_r, v2.x, v2.y);
+                if (G) __stcg(reinterpret_cast<double2*>(G + r * CP_LS + cc), v2);
+              }
+            }
+          } else {
+            asm volatile("bar.sync 1, 256;" ::: "memory");
+          }
           stamp(p, 3);
-        } else {
+        }
+        if (warp >= 4) {
           const int tile = t_lo + warp;  // slots 64 + 8 (warp - 4) ..
           if (tile <= t_hi) {
             update_from_l2(tile);
@@ -1061,7 +1128,7 @@ __global__ void __launch_bounds__(CH_THREADS, 1) k_chol_panels(
         // our panel is next: its diagonal rows from the pushed rows of L_p
         mbar_wait_cluster(&sm.barLd[p], 0);
         if (sm.failed) break;
-        cp_update<false>(&sm.rcv[0][0], p, p + 1, P((p + 1) / cs), d, 0, CP_NB - 1, 0, 8, CP_NB);
+        cp_update_diag8(&sm.rcv[0][0], P((p + 1) / cs), d, (p + 1) * CP_NB, d - (p + 1) * CP_NB);
         __syncthreads();
       } else {
         mbar_wait_cluster(&sm.barL[p], 0);
