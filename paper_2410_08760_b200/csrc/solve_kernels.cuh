@@ -1169,69 +1169,45 @@ __global__ void __launch_bounds__(CH_THREADS, 1) k_chol_panels(
   cluster.sync();  // failure flags settled cluster-wide
   if (rank == 0) stamp(63, 1);
   if (!sm.failed && !skip_solve) {
-    // ---- backward substitution: L^T z = y, panel by panel from the last
-    if (tid < 2 * CP_NB) sm.w[tid / CP_NB][tid % CP_NB] = 0.0;
-    __syncthreads();
-    const int first_own = rank;
-    for (int b = npan - 1; b >= 0; --b) {
-      const int owner = b % cs, kb = b / cs;
-      const int b0 = b * CP_NB, bn = min(CP_NB, d - b0);
-      if (rank == owner) {
-        stamp(b, 8);
-        if (warp == 0) {
-          const double* Pb = P(kb);
-          const int rs = max(d - b0, CP_NB);
-          // r_t = y_t - w_t;  z_s = sum_{t >= s} T[t][s] r_t
-          const double rl = (lane < bn) ? __dsub_rn(Pb[rs * CP_LS + lane], sm.w[kb][lane]) : 0.0;
-          double zs = 0.0;
-          // r broadcast through shared memory (shuffles here would take the
-          // slow collective path: the warp may still be split by polling)
-          sm.part[0][lane] = rl;
-          __syncwarp();
-#pragma unroll 8
-          for (int t2 = 0; t2 < CP_NB; ++t2)
-            if (t2 >= lane) zs = fma(sm.T[kb][t2][lane], sm.part[0][t2], zs);
-          if (lane == 0) stamp(b, 10);
-          if (lane < bn) sm.z[b0 + lane] = zs;
-        }
-        __syncthreads();
-        // z_b to every CTA owning a panel before b, one warp per CTA, as
-        // st.async stores that complete the receiver's barZ[b] transaction
-        if (warp < cs && warp != rank && warp < b && lane < bn)
-          st_async_f64(&sm.z[b0 + lane], &sm.barZ[b], static_cast<uint32_t>(warp), sm.z[b0 + lane]);
-        stamp(b, 11);
-      } else if (first_own < b) {
+    // ---- backward substitution: L^T z = y, panel by panel from the last.
+    //      Warp k runs own panel q_k = rank + k cs alone: for every later
+    //      panel b it waits for z_b (barZ[b]: st.async bytes from b's owner,
+    //      or the local arrive of the warp owning b) and accumulates
+    //      w = sum_b L_{q_k}[rows b]^T z_b; then z_{q_k} = T^T (y - w) goes to
+    //      the earlier CTAs as st.async stores.  No CTA-wide barrier per panel.
+    if (warp < KP && rank + warp * cs < npan) {
+      const int k = warp, q = rank + k * cs, q0 = q * CP_NB;
+      const double* Pq = P(k);
+      double wacc = 0.0;
+      for (int b = npan - 1; b > q; --b) {
+        const int b0 = b * CP_NB, bn = min(CP_NB, d - b0);
         mbar_wait_cluster(&sm.barZ[b], 0);
-        if (b - 1 >= 0 && (b - 1) % cs == rank) stamp(b, 9);
-      } else {
-        continue;
+        double acc[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll 8
+        for (int i = 0; i < CP_NB; ++i)
+          if (i < bn) acc[i & 3] = fma(Pq[(b0 + i - q0) * CP_LS + lane], sm.z[b0 + i], acc[i & 3]);
+        wacc += (acc[0] + acc[1]) + (acc[2] + acc[3]);
       }
-      // w_q[j] += sum_{i in panel b} L_q[i][j] z_i for own panels q < b
-#pragma unroll
-      for (int k = 0; k < KP; ++k) {
-        const int q = rank + k * cs;
-        if (q >= b || q >= npan) continue;
-        const double* Pq = P(k);
-        const int q0 = q * CP_NB;
-        // warp w sums rows b0 + 4w .. 4w + 3 for column j = lane
-        double s = 0.0;
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const int ii = warp * 4 + u;
-          if (ii < bn) s = fma(Pq[(b0 + ii - q0) * CP_LS + lane], sm.z[b0 + ii], s);
-        }
-        sm.part[warp][lane] = s;
-        __syncthreads();
-        if (warp == 0) {
-          double acc = sm.w[k][lane];
-#pragma unroll
-          for (int w2 = 0; w2 < 8; ++w2) acc += sm.part[w2][lane];
-          sm.w[k][lane] = acc;
-        }
-        __syncthreads();
+      const int bn = min(CP_NB, d - q0), rs = max(d - q0, CP_NB);
+      // r_t = y_t - w_t;  z_s = sum_{t >= s} T[t][s] r_t
+      sm.part[warp][lane] = (lane < bn) ? __dsub_rn(Pq[rs * CP_LS + lane], wacc) : 0.0;
+      __syncwarp();
+      double zacc[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll 8
+      for (int t2 = 0; t2 < CP_NB; ++t2)
+        if (t2 >= lane) zacc[t2 & 3] = fma(sm.T[k][t2][lane], sm.part[warp][t2], zacc[t2 & 3]);
+      const double zs = (zacc[0] + zacc[1]) + (zacc[2] + zacc[3]);
+      stamp_if(lane == 0, q, 10);
+      if (lane < bn) {
+        sm.z[q0 + lane] = zs;
+        for (int r2 = 0; r2 < cs; ++r2)  // CTAs owning a panel before q
+          if (r2 != rank && r2 < q) st_async_f64(&sm.z[q0 + lane], &sm.barZ[q], static_cast<uint32_t>(r2), zs);
       }
-      if (b - 1 >= 0 && (b - 1) % cs == rank) stamp(b, 13);
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&sm.barZ[q]);  // this CTA's other warp (an earlier own panel)
+      stamp_if(lane == 0, q, 11);
     }
+    __syncthreads();
     mark(2);
     if (rank == 0) stamp(63, 2);
     // ---- outputs of the own panels
