@@ -876,10 +876,13 @@ __global__ void __launch_bounds__(TK_THREADS, 1) k_topk_stream(
         __syncthreads();
         const int sh = SH[L], up = (L == 0) ? 63 : SH[L - 1];
         const uint32_t dmask = (1u << BI[L]) - 1u;
-        for (int t = tid; t < wi; t += TK_THREADS) {
-          const uint64_t key = rank_key(__ldcs(v + t), t, weighted);
+        for (int base = 0; base < wi; base += TK_THREADS) {  // warp-uniform trip count (ballots)
+          const int t = base + tid;
           uint32_t dig = 0xFFFFFFFFu;
-          if ((up >= 63 ? 0ull : (key >> up)) == prefix) dig = static_cast<uint32_t>(key >> sh) & dmask;
+          if (t < wi) {
+            const uint64_t key = rank_key(__ldcs(v + t), t, weighted);
+            if ((up >= 63 ? 0ull : (key >> up)) == prefix) dig = static_cast<uint32_t>(key >> sh) & dmask;
+          }
           tks_add(hist, dig, lane);
         }
         __syncthreads();
@@ -1023,6 +1026,738 @@ __global__ void __launch_bounds__(TK_THREADS, 1) k_topk_stream(
   }
   pc.mark(4);
   if (g_dbg_on && tid == 0 && s_fail) atomicAdd(reinterpret_cast<unsigned long long*>(&g_dbg[17]), 1ull);
+}
+
+// ------------------------------------------- TopK, split streaming path
+// The same selection rule as k_topk_stream (descending key, ties to the
+// smaller position), as three kernels so the one pass over D is spread over
+// many CTAs that each keep a TMA ring of D in flight:
+//  1. k_tks_window (CTA per client): a sample of `ns` keys (ns/8 runs of 8
+//     consecutive positions spread over the row) gives the key
+//     high-word window (hlo, hhi] around the k-th key;
+//  2. k_tks_pass (grid segments x clients): one producer thread streams the
+//     segment of D into a shared-memory ring with 1-D bulk copies
+//     (cp.async.bulk, mbarrier transaction counts); 16 consumer warps
+//     classify each key: above the window -> gt bit (warp ballot = bitmap
+//     word), inside -> the segment's candidate slots, exact zeros -> zero bit
+//     (only when the window reaches zero); per-segment counts (G, M, Z).  The
+//     gt and zero/tie rows are scratch that is all-zero between rounds, so
+//     only nonzero words are stored;
+//  3. k_tks_select (CTA per client): the gt row into shared memory (and the
+//     global row cleared), the k-th key by radix levels over the candidates
+//     (the first level over the candidate list in L2, the threshold digit's
+//     survivors compacted into shared memory for the rest), marks by shared
+//     atomics, then one sweep (contiguous words per thread, block scans) that
+//     takes the first `need` tied positions and writes the list, range
+//     starts, values and the client shift update.
+// A window miss (G >= k, G + M (+ Z) < k) or a segment overflowing its
+// candidate slots falls back to radix levels over D inside k_tks_select.
+constexpr int TKP_CONS = 512;                  // consumer threads
+constexpr int TKP_THREADS = TKP_CONS + 32;     // + the producer warp
+constexpr int TKP_CW = TKP_CONS / 32;          // consumer warps (list regions per segment)
+constexpr int TKP_CH = 2048;                   // positions per ring stage (16 KB)
+constexpr int TKP_NST = 6;                     // ring stages
+constexpr int TKP_STRIDE = TKP_CH + 2;         // stage stride (16-byte aligned, +1 lead)
+constexpr size_t TKP_SMEM = static_cast<size_t>(TKP_NST) * TKP_STRIDE * 8;
+constexpr int TKP_SEGCAP = 16384;              // candidate slots per segment (max)
+constexpr int TKP_MAXSEG = 16;                 // segments per client (max)
+constexpr int TKP_MAXSUB = TKP_MAXSEG * TKP_CONS / 32;  // list regions per client (max)
+constexpr int TKSEL_THREADS = 512;
+constexpr int TKSEL_LCAP = 2048;               // threshold-digit survivors kept in smem
+constexpr int TKW_THREADS = 512;
+constexpr int TKW_MAXSAMPLE = 16 * TKW_THREADS;
+__host__ __device__ constexpr int tks_wbp(int64_t w) {  // bitmap row stride (16-byte rows)
+  return static_cast<int>(((w + 31) / 32 + 3) / 4 * 4);
+}
+__host__ __device__ constexpr size_t tksel_smem_bytes(int64_t w) {
+  return static_cast<size_t>(tks_wbp(w)) * 4 +
+         (static_cast<size_t>(tks_wbp(w)) * 2 > TKSEL_LCAP * 12 ? static_cast<size_t>(tks_wbp(w)) * 2
+                                                                 : TKSEL_LCAP * 12);
+}
+
+struct TkWin {
+  int hhi, hlo, zero, active;
+};
+struct TkSeg {
+  int g, m, z, pad;
+};
+
+// the digit holding the need-th largest element of hist[0, nbins) (counting
+// from the top bin), any blockDim multiple of 32 with nbins <= 4 * blockDim
+__device__ __forceinline__ void tk_find_digit_n(const uint32_t* hist, int nbins, int need, int* ws,
+                                                int* s_digit, int* s_above) {
+  const int per = (nbins + static_cast<int>(blockDim.x) - 1) / static_cast<int>(blockDim.x);
+  const int b0 = nbins - 1 - per * static_cast<int>(threadIdx.x);
+  int cnt[4], sum = 0;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int b = b0 - i;
+    cnt[i] = (i < per && b >= 0) ? static_cast<int>(hist[b]) : 0;
+    sum += cnt[i];
+  }
+  int total;
+  int above = block_excl_scan(sum, ws, &total);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    if (cnt[i] > 0 && above < need && need <= above + cnt[i]) {
+      *s_digit = b0 - i;
+      *s_above = above;
+    }
+    above += cnt[i];
+  }
+  __syncthreads();
+}
+
+// sample position i of ns: run j = i / 8 of ns / 8 runs of 8 consecutive
+// positions (two full sectors) spread evenly over the row
+__host__ __device__ __forceinline__ int64_t tks_sample_pos(int i, int ns, int64_t w) {
+  const int64_t runs = ns / 8;
+  return (static_cast<int64_t>(i >> 3) * (w - 8)) / runs + (i & 7);
+}
+
+__global__ void __launch_bounds__(TKW_THREADS) k_tks_window(
+    const DevCtl* __restrict__ ctl, const double* __restrict__ D, int64_t w, int k, int ns,
+    int weighted, const int32_t* __restrict__ clients, const int32_t* __restrict__ flags,
+    int32_t* __restrict__ draws, TkWin* __restrict__ win) {
+  if (ctl && ctl->halt) return;
+  __shared__ uint32_t hist[2048], hist2[2048];
+  __shared__ int ws[64];
+  __shared__ int s_digit, s_above;
+  const int c = client_of(clients, blockIdx.x);
+  const int tid = threadIdx.x, lane = tid & 31;
+  if (tid == 0 && draws) draws[c] = 0;
+  if (!(flags[c] & 2)) {  // all-zero difference: empty delta, no draws
+    if (tid == 0) win[c] = TkWin{0, 0, 0, 0};
+    return;
+  }
+  const double* v = D + static_cast<int64_t>(c) * w;
+  constexpr int SPT = TKW_MAXSAMPLE / TKW_THREADS;
+  uint32_t sk[SPT];
+#pragma unroll
+  for (int u = 0; u < SPT; ++u) {
+    const int i = u * TKW_THREADS + tid;
+    const int64_t ts = tks_sample_pos(i, ns, w);
+    sk[u] = i < ns ? static_cast<uint32_t>(rank_key(__ldg(v + ts), ts, weighted) >> 32) : 0u;
+  }
+  for (int i = tid; i < 2048; i += TKW_THREADS) { hist[i] = 0u; hist2[i] = 0u; }
+  __syncthreads();
+#pragma unroll
+  for (int u = 0; u < SPT; ++u)
+    tks_add(hist, (u * TKW_THREADS + tid < ns) ? (sk[u] >> 21) : 0xFFFFFFFFu, lane);
+  __syncthreads();
+  const double r = static_cast<double>(k) * ns / static_cast<double>(w);
+  const int delta = static_cast<int>(4.0 * sqrt(r) + 16.0);
+  const int ri = static_cast<int>(r);
+  const int r_hi = ri - delta, r_lo = ri + delta;  // ranks in descending order
+  const bool has_hi = r_hi >= 0, has_lo = r_lo < ns;
+  int d1_hi = 0, d1_lo = 0, need_hi = r_hi + 1, need_lo = r_lo + 1;
+  if (has_hi) {
+    tk_find_digit_n(hist, 2048, need_hi, ws, &s_digit, &s_above);
+    d1_hi = s_digit;
+    need_hi -= s_above;
+    __syncthreads();
+  }
+  if (has_lo) {
+    tk_find_digit_n(hist, 2048, need_lo, ws, &s_digit, &s_above);
+    d1_lo = s_digit;
+    need_lo -= s_above;
+    __syncthreads();
+  }
+  for (int i = tid; i < 2048; i += TKW_THREADS) hist[i] = 0u;
+  __syncthreads();
+#pragma unroll
+  for (int u = 0; u < SPT; ++u) {
+    const bool in = u * TKW_THREADS + tid < ns;
+    const uint32_t top = sk[u] >> 21, dg = (sk[u] >> 10) & 2047u;
+    tks_add(hist, (in && has_hi && top == static_cast<uint32_t>(d1_hi)) ? dg : 0xFFFFFFFFu, lane);
+    tks_add(hist2, (in && has_lo && top == static_cast<uint32_t>(d1_lo)) ? dg : 0xFFFFFFFFu, lane);
+  }
+  __syncthreads();
+  int hhi = 0x7FFFFFFF, hlo = -1;
+  if (has_hi) {
+    tk_find_digit_n(hist, 2048, need_hi, ws, &s_digit, &s_above);
+    hhi = static_cast<int>((static_cast<uint32_t>(d1_hi) << 21) | (static_cast<uint32_t>(s_digit) << 10) | 1023u);
+    __syncthreads();
+  }
+  if (has_lo) {
+    tk_find_digit_n(hist2, 2048, need_lo, ws, &s_digit, &s_above);
+    hlo = static_cast<int>((static_cast<uint32_t>(d1_lo) << 21) | (static_cast<uint32_t>(s_digit) << 10)) - 1;
+    __syncthreads();
+  }
+  if (tid == 0) {
+    if (hlo >= hhi) hlo = hhi - 1;
+    const int zero = hlo < 0;  // exact zeros become a tie class when the window reaches them
+    win[c] = TkWin{hhi, zero ? -1 : hlo, zero, 1};
+  }
+}
+
+__device__ __forceinline__ void mbar_wait_short(uint64_t* bar, uint32_t parity) {
+  for (uint32_t spin = 0; !mbar_try_wait(bar, parity); ++spin) {
+    if (spin > (1u << 20)) asm volatile("trap;");
+  }
+}
+
+__device__ __forceinline__ void bar_sync_named(int id, int nthreads) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+}
+
+// One ring stage (TKP_CH positions) of one consumer warp's share: keys from
+// shared memory, gt / zero bitmap words, and (position, raw value) appends
+// to the warp's own list regions (warp-uniform running counts: no atomics).
+template <bool W, bool Z, bool CHECK>
+__device__ __forceinline__ void tkp_stage(const double* __restrict__ rb, int base, int t1, int hhi,
+                                          int hlo, int tid, int lane, uint32_t* __restrict__ zrow, uint64_t* __restrict__ ck,
+                                          int32_t* __restrict__ cp, uint64_t* __restrict__ gk,
+                                          int32_t* __restrict__ gq, int capw, int& m_cnt,
+                                          int& g_cnt, int& z_cnt) {
+  constexpr int EPT = TKP_CH / TKP_CONS;
+  uint64_t bits[EPT];
+  uint32_t gb[EPT], mb[EPT];
+#pragma unroll
+  for (int u = 0; u < EPT; ++u) {
+    const int tl = u * TKP_CONS + tid;
+    const int t = base + tl;
+    const double x = rb[tl];
+    bits[u] = static_cast<uint64_t>(__double_as_longlong(x));
+    const uint64_t key = W ? rank_key(x, t, 1) : (bits[u] & 0x7FFFFFFFFFFFFFFFull);
+    int hk = static_cast<int>(key >> 32);
+    if (CHECK && t >= t1) hk = -2;
+    const bool gt = hk > hhi;
+    bool mid = hk > hlo && hk <= hhi;
+    if (Z) {
+      const bool z = (!CHECK || t < t1) && key == 0ull;
+      mid = mid && !z;
+      const uint32_t zb = __ballot_sync(0xffffffffu, z);
+      if (lane == 0 && zb) zrow[t >> 5] = zb;
+      z_cnt += __popc(zb);
+    }
+    gb[u] = __ballot_sync(0xffffffffu, gt);
+    mb[u] = __ballot_sync(0xffffffffu, mid);
+  }
+  const uint32_t lt = (1u << lane) - 1u;
+#pragma unroll
+  for (int u = 0; u < EPT; ++u) {
+    const int t = base + u * TKP_CONS + tid;
+    if (gb[u]) {
+      if ((gb[u] >> lane) & 1u) {
+        const int slot = g_cnt + __popc(gb[u] & lt);
+        if (slot < capw) { gk[slot] = bits[u]; gq[slot] = t; }
+      }
+      g_cnt += __popc(gb[u]);
+    }
+    if (mb[u]) {
+      if ((mb[u] >> lane) & 1u) {
+        const int slot = m_cnt + __popc(mb[u] & lt);
+        if (slot < capw) { ck[slot] = bits[u]; cp[slot] = t; }
+      }
+      m_cnt += __popc(mb[u]);
+    }
+  }
+}
+
+template <bool W, bool Z>
+__device__ __forceinline__ void tkp_consume(const double* ring, uint64_t* full, uint64_t* empty,
+                                            int nch, int lead, int t0, int t1, int hhi, int hlo,
+                                            int tid, int lane, uint32_t* zrow,
+                                            uint64_t* ck, int32_t* cp, uint64_t* gk, int32_t* gq,
+                                            int capw, int& m_cnt, int& g_cnt, int& z_cnt) {
+  for (int i = 0; i < nch; ++i) {
+    const int st = i % TKP_NST;
+    mbar_wait_short(&full[st], (i / TKP_NST) & 1);
+    const double* rb = ring + st * TKP_STRIDE + lead;
+    const int base = t0 + i * TKP_CH;
+    if (base + TKP_CH <= t1)
+      tkp_stage<W, Z, false>(rb, base, t1, hhi, hlo, tid, lane, zrow, ck, cp, gk, gq, capw, m_cnt,
+                             g_cnt, z_cnt);
+    else
+      tkp_stage<W, Z, true>(rb, base, t1, hhi, hlo, tid, lane, zrow, ck, cp, gk, gq, capw, m_cnt,
+                            g_cnt, z_cnt);
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[st]);
+  }
+}
+
+// seg[(c * S + s) * TKP_CW + warp] = (G, M, Z) of one consumer warp's share;
+// its list region is slots [((c * S + s) * TKP_CW + warp) * capw, + capw)
+template <bool W>
+__global__ void __launch_bounds__(TKP_THREADS) k_tks_pass(
+    const DevCtl* __restrict__ ctl, const double* __restrict__ D, int64_t w, int wbp, int lseg,
+    int capw, const int32_t* __restrict__ clients, const TkWin* __restrict__ win,
+    uint32_t* __restrict__ eqz, uint64_t* __restrict__ cand_key, int32_t* __restrict__ cand_pos,
+    uint64_t* __restrict__ gt_val, int32_t* __restrict__ gt_pos, TkSeg* __restrict__ seg) {
+  if (ctl && ctl->halt) return;
+  extern __shared__ __align__(128) double ring[];
+  __shared__ __align__(8) uint64_t full[TKP_NST], empty[TKP_NST];
+  const int c = client_of(clients, blockIdx.y);
+  const TkWin wn = win[c];
+  if (!wn.active) return;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int S = gridDim.x, s = blockIdx.x;
+  const int wi = static_cast<int>(w);
+  const int t0 = s * lseg, t1 = min(wi, t0 + lseg);
+  const int nch = (t1 - t0 + TKP_CH - 1) / TKP_CH;
+  const double* v = D + static_cast<int64_t>(c) * w;
+  // bulk copies need 16-byte aligned sources: start one position early on odd rows
+  const int lead = static_cast<int>((reinterpret_cast<uintptr_t>(v + t0) & 15u) >> 3);
+  if (tid == 0) {
+    for (int i = 0; i < TKP_NST; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], TKP_CW);
+    }
+    fence_barrier_init();
+  }
+  __syncthreads();
+  if (warp == TKP_CW) {  // producer
+    if (lane == 0) {
+      for (int i = 0; i < nch; ++i) {
+        const int st = i % TKP_NST;
+        if (i >= TKP_NST) mbar_wait_short(&empty[st], ((i / TKP_NST) - 1) & 1);
+        const int nel = min(TKP_CH, t1 - t0 - i * TKP_CH) + lead;
+        const uint32_t bytes = static_cast<uint32_t>((nel + 1) & ~1) * 8u;
+        mbar_arrive_expect_tx(&full[st], bytes);
+        bulk_load(ring + st * TKP_STRIDE, v + t0 + i * TKP_CH - lead, bytes, &full[st]);
+      }
+    }
+    return;
+  }
+  uint32_t* zrow = eqz + static_cast<int64_t>(c) * wbp;
+  const int64_t sub = (static_cast<int64_t>(c) * S + s) * TKP_CW + warp;
+  const int64_t lbase = sub * capw;
+  int m_cnt = 0, g_cnt = 0, z_cnt = 0;
+  if (wn.zero)
+    tkp_consume<W, true>(ring, full, empty, nch, lead, t0, t1, wn.hhi, wn.hlo, tid, lane, zrow,
+                         cand_key + lbase, cand_pos + lbase, gt_val + lbase, gt_pos + lbase, capw,
+                         m_cnt, g_cnt, z_cnt);
+  else
+    tkp_consume<W, false>(ring, full, empty, nch, lead, t0, t1, wn.hhi, wn.hlo, tid, lane, zrow,
+                          cand_key + lbase, cand_pos + lbase, gt_val + lbase, gt_pos + lbase,
+                          capw, m_cnt, g_cnt, z_cnt);
+  if (lane == 0) seg[sub] = TkSeg{g_cnt, m_cnt, z_cnt, 0};
+}
+
+// radix levels over candidate keys (source `get(e)` for e < cnt) whose bits
+// >= hi_excl equal pf: 11-bit digits downwards, at most `max_levels`.
+// Returns with pf extended by the chosen digits, sh = the bit position of the
+// last digit, need reduced by the counts above, all = the last bin is taken
+// whole.
+template <class Get>
+__device__ void tksel_levels(Get get, int cnt, int& hi_excl, uint64_t& pf, int& need, int& sh,
+                             bool& all, int max_levels, uint32_t* hist, int* ws, int* s_digit,
+                             int* s_above) {
+  const int tid = threadIdx.x, lane = tid & 31;
+  all = false;
+  for (int lv = 0; lv < max_levels && hi_excl > 0; ++lv) {
+    const int bits = min(11, hi_excl);
+    sh = hi_excl - bits;
+    for (int i = tid; i < 2048; i += blockDim.x) hist[i] = 0u;
+    __syncthreads();
+    const uint32_t dmask = (1u << bits) - 1u;
+    for (int base = 0; base < cnt; base += 4 * blockDim.x) {
+      uint64_t kk[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int e = base + u * blockDim.x + tid;
+        kk[u] = e < cnt ? get(e) : 0ull;
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int e = base + u * blockDim.x + tid;
+        uint32_t dig = 0xFFFFFFFFu;
+        if (e < cnt && (hi_excl >= 64 ? 0ull : (kk[u] >> hi_excl)) == pf)
+          dig = static_cast<uint32_t>(kk[u] >> sh) & dmask;
+        tks_add(hist, dig, lane);
+      }
+    }
+    __syncthreads();
+    tk_find_digit_n(hist, 1 << bits, need, ws, s_digit, s_above);
+    const int dg = *s_digit;
+    need -= *s_above;
+    pf = (pf << bits) | static_cast<uint64_t>(dg);
+    const int nbin = static_cast<int>(hist[dg]);
+    __syncthreads();
+    hi_excl = sh;
+    if (nbin == need) { all = true; break; }
+  }
+}
+
+// Warp-per-region iteration over the per-(segment, warp) list regions of one
+// client: region j holds cnt[j] entries at slots [j * capw, + cnt[j]).
+// f(slot, valid) is called warp-uniformly, U slots per lane in flight.
+template <int U, class F>
+__device__ __forceinline__ void tksel_regions(const int* cnt, int nreg, int capw, F f) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  for (int j = warp; j < nreg; j += nw) {
+    const int n = cnt[j];
+    for (int i0 = 0; i0 < n; i0 += 32 * U) {
+      int sl[U];
+      bool ok[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int i = i0 + u * 32 + lane;
+        ok[u] = i < n;
+        sl[u] = j * capw + (ok[u] ? i : 0);
+      }
+      f(sl, ok);
+    }
+  }
+}
+
+__global__ void __launch_bounds__(TKSEL_THREADS) k_tks_select(
+    const double* __restrict__ D, int64_t w, int wbp, int k, int weighted, int S_seg, int capw,
+    const int32_t* __restrict__ clients, const TkWin* __restrict__ win, const TkSeg* __restrict__ seg,
+    uint32_t* __restrict__ eqz, const uint64_t* __restrict__ cand_key,
+    const int32_t* __restrict__ cand_pos, const uint64_t* __restrict__ gt_val,
+    const int32_t* __restrict__ gt_pos, int32_t* __restrict__ count, uint32_t* __restrict__ idx_list,
+    double* __restrict__ val_list, int cap, Emit em) {
+  // no halt check: the tie row must be left clean whenever the pass ran
+  // dynamic: sg[wbp] u32 (the selection row) | union { lkey[LCAP] u64,
+  //          lpos[LCAP] i32 (resolve) ; wrel[wbp] u16 (rank within a thread) }
+  extern __shared__ __align__(16) uint32_t sg[];
+  uint64_t* lkey = reinterpret_cast<uint64_t*>(sg + wbp);
+  int32_t* lpos = reinterpret_cast<int32_t*>(lkey + TKSEL_LCAP);
+  uint16_t* wrel = reinterpret_cast<uint16_t*>(sg + wbp);
+  __shared__ uint32_t hist[2048];
+  __shared__ int mcnt[TKP_MAXSUB], gcnt[TKP_MAXSUB];
+  __shared__ int tbase[TKSEL_THREADS];
+  __shared__ int ws[64];
+  __shared__ int s_digit, s_above, s_nl, s_G, s_M, s_Z, s_over, s_need, s_eqd, s_fail;
+  const int c = client_of(clients, blockIdx.x);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int NR = S_seg * TKP_CW;  // list regions (segment x consumer warp)
+  const int wi = static_cast<int>(w);
+  const int wb = static_cast<int>((w + 31) / 32);
+  const double* v = D + static_cast<int64_t>(c) * w;
+  uint32_t* zrow = eqz + static_cast<int64_t>(c) * wbp;
+  const TkWin wn = win[c];
+  if (!wn.active) {
+    emit_empty(em, c);
+    if (tid == 0) count[c] = 0;
+    return;
+  }
+  {
+    uint4* s4 = reinterpret_cast<uint4*>(sg);
+    for (int i = tid; i < wbp / 4; i += TKSEL_THREADS) s4[i] = make_uint4(0, 0, 0, 0);
+  }
+  const int64_t cbase = static_cast<int64_t>(c) * NR * capw;
+  const uint64_t* ck = cand_key + cbase;
+  const int32_t* cp = cand_pos + cbase;
+  const uint64_t* gk = gt_val + cbase;
+  const int32_t* gq = gt_pos + cbase;
+  // ---- region counts and totals (warp 0)
+  if (warp == 0) {
+    int g = 0, m = 0, z = 0, over = 0;
+    for (int j = lane; j < NR; j += 32) {
+      const TkSeg sr = seg[static_cast<int64_t>(c) * NR + j];
+      over |= (sr.m > capw) | (sr.g > capw);
+      mcnt[j] = min(sr.m, capw);
+      gcnt[j] = min(sr.g, capw);
+      g += sr.g;
+      m += min(sr.m, capw);
+      z += sr.z;
+    }
+    g = warp_sum_int(g);
+    m = warp_sum_int(m);
+    z = warp_sum_int(z);
+    over = __any_sync(0xffffffffu, over);
+    if (lane == 0) {
+      s_G = g;
+      s_M = m;
+      s_Z = z;
+      s_over = over;
+      s_nl = 0;
+      s_eqd = 0;
+      s_fail = 0;
+    }
+  }
+  __syncthreads();
+  const int G = s_G, M = s_M, Z = wn.zero ? s_Z : 0;
+  const bool ok = !s_over && G < k && G + M + Z >= k;
+  constexpr int UB = 4;  // list entries per lane in flight
+  const uint64_t KMASK = 0x7FFFFFFFFFFFFFFFull;
+  auto ckey = [&](int sl) {  // candidate slot -> rank key (raw value bits stored)
+    const uint64_t b = __ldcg(ck + sl);
+    return weighted ? rank_key(__longlong_as_double(static_cast<long long>(b)), __ldcg(cp + sl), 1)
+                    : (b & KMASK);
+  };
+  auto mark = [&](int t) { atomicOr(&sg[t >> 5], 1u << (t & 31)); };
+  auto mark_eq = [&](int t) { atomicOr(&zrow[t >> 5], 1u << (t & 31)); };
+  int need = k;
+  if (ok) {
+    // the selection row from the entries above the window
+    tksel_regions<UB>(gcnt, NR, capw, [&](const int* sl, const bool* vl_) {
+      int tt[UB];
+#pragma unroll
+      for (int u = 0; u < UB; ++u) tt[u] = vl_[u] ? __ldcg(gq + sl[u]) : -1;
+#pragma unroll
+      for (int u = 0; u < UB; ++u)
+        if (tt[u] >= 0) mark(tt[u]);
+    });
+  }
+  if (ok && G + M >= k) {
+    // the k-th key is a candidate; zeros (if tracked) are not needed
+    if (wn.zero) {
+      for (int q = tid; q < wbp; q += TKSEL_THREADS) zrow[q] = 0u;
+      __syncthreads();
+    }
+    need = k - G;
+    const int top = 32 + (31 - __clz(static_cast<unsigned>((wn.hlo + 1) ^ wn.hhi) | 1u));
+    const uint64_t pf0 = static_cast<uint64_t>(static_cast<uint32_t>(wn.hhi)) >> (top - 31);
+    // radix levels over the candidate regions (11 bits below `top` first)
+    // until the threshold digit's bin fits the shared-memory list
+    int hi_excl = top + 1, sh = hi_excl;
+    uint64_t pf = pf0;
+    bool all = false;
+    for (int lv = 0; lv < 6 && hi_excl > 0; ++lv) {
+      const int bits = min(11, hi_excl);
+      sh = hi_excl - bits;
+      const uint32_t dmask = (1u << bits) - 1u;
+      for (int i = tid; i < 2048; i += TKSEL_THREADS) hist[i] = 0u;
+      __syncthreads();
+      tksel_regions<UB>(mcnt, NR, capw, [&](const int* sl, const bool* vl_) {
+        uint64_t kk[UB];
+#pragma unroll
+        for (int u = 0; u < UB; ++u) kk[u] = vl_[u] ? ckey(sl[u]) : 0ull;
+#pragma unroll
+        for (int u = 0; u < UB; ++u) {
+          uint32_t dig = 0xFFFFFFFFu;
+          if (vl_[u] && (kk[u] >> hi_excl) == pf) dig = static_cast<uint32_t>(kk[u] >> sh) & dmask;
+          tks_add(hist, dig, lane);
+        }
+      });
+      __syncthreads();
+      tk_find_digit_n(hist, 1 << bits, need, ws, &s_digit, &s_above);
+      need -= s_above;
+      pf = (pf << bits) | static_cast<uint64_t>(s_digit);
+      const int nbin = static_cast<int>(hist[s_digit]);
+      __syncthreads();
+      hi_excl = sh;
+      if (nbin == need) { all = true; break; }
+      if (nbin <= TKSEL_LCAP) break;
+    }
+    // above the threshold prefix -> selected; in it -> the shared-memory list
+    // (or, when the whole bin is taken, selected as well)
+    tksel_regions<UB>(mcnt, NR, capw, [&](const int* sl, const bool* vl_) {
+      uint64_t kk[UB];
+      int tt[UB];
+#pragma unroll
+      for (int u = 0; u < UB; ++u) {
+        kk[u] = vl_[u] ? ckey(sl[u]) : 0ull;
+        tt[u] = vl_[u] ? __ldcg(cp + sl[u]) : -1;
+      }
+#pragma unroll
+      for (int u = 0; u < UB; ++u) {
+        if (tt[u] < 0) continue;
+        const uint64_t hp = kk[u] >> sh;
+        if (hp > pf || (all && hp == pf)) {
+          mark(tt[u]);
+        } else if (hp == pf) {
+          const int i = atomicAdd(&s_nl, 1);
+          if (i < TKSEL_LCAP) { lkey[i] = kk[u]; lpos[i] = tt[u]; }
+        }
+      }
+    });
+    __syncthreads();
+    if (all) {
+      need = 0;
+    } else if (s_nl <= TKSEL_LCAP) {
+      const int nl = s_nl;
+      auto lk = [&](int e) { return lkey[e]; };
+      tksel_levels(lk, nl, hi_excl, pf, need, sh, all, 64, hist, ws, &s_digit, &s_above);
+      for (int e = tid; e < nl; e += TKSEL_THREADS) {
+        const uint64_t hp = lkey[e] >> sh;
+        if (hp > pf || (all && hp == pf)) mark(lpos[e]);
+        else if (hp == pf) { mark_eq(lpos[e]); s_eqd = 1; }
+      }
+      if (all) need = 0;
+    } else if (tid == 0) {
+      s_fail = 1;  // a tie bin of more than LCAP keys (exact ties): radix over D below
+    }
+  } else if (ok) {
+    // every candidate is taken; the first k - G - M zeros complete the set
+    tksel_regions<UB>(mcnt, NR, capw, [&](const int* sl, const bool* vl_) {
+      int tt[UB];
+#pragma unroll
+      for (int u = 0; u < UB; ++u) tt[u] = vl_[u] ? __ldcg(cp + sl[u]) : -1;
+#pragma unroll
+      for (int u = 0; u < UB; ++u)
+        if (tt[u] >= 0) mark(tt[u]);
+    });
+    need = k - G - M;
+    if (tid == 0) s_eqd = 1;
+  } else if (tid == 0) {
+    s_fail = 1;  // the window missed or a list region overflowed
+  }
+  __syncthreads();
+  if (s_fail) {
+    // radix levels over D itself (the selection and tie rows rewritten word
+    // by word; values gathered from D)
+    need = k;
+    if (tid == 0) s_eqd = 1;
+    constexpr int NL = 6;
+    constexpr int SH[NL] = {52, 41, 30, 19, 8, 0};
+    constexpr int BI[NL] = {11, 11, 11, 11, 11, 8};
+    uint64_t prefix = 0;
+    int L = 0;
+    bool take_all = false;
+    for (; L < NL; ++L) {
+      for (int i = tid; i < 2048; i += TKSEL_THREADS) hist[i] = 0u;
+      __syncthreads();
+      const int sh = SH[L], up = (L == 0) ? 63 : SH[L - 1];
+      const uint32_t dmask = (1u << BI[L]) - 1u;
+      for (int base = 0; base < wi; base += TKSEL_THREADS) {  // warp-uniform trip count (ballots)
+        const int t = base + tid;
+        uint32_t dig = 0xFFFFFFFFu;
+        if (t < wi) {
+          const uint64_t key = rank_key(__ldcg(v + t), t, weighted);
+          if ((up >= 63 ? 0ull : (key >> up)) == prefix) dig = static_cast<uint32_t>(key >> sh) & dmask;
+        }
+        tks_add(hist, dig, lane);
+      }
+      __syncthreads();
+      tk_find_digit_n(hist, 1 << BI[L], need, ws, &s_digit, &s_above);
+      const int dg = s_digit;
+      need -= s_above;
+      prefix = (prefix << BI[L]) | static_cast<uint64_t>(dg);
+      const int nbin = static_cast<int>(hist[dg]);
+      __syncthreads();
+      if (nbin == need) { take_all = true; break; }
+    }
+    if (L == NL) L = NL - 1;
+    const int sh = SH[L];
+    for (int base = 0; base < wb * 32; base += TKSEL_THREADS) {
+      const int t = base + tid;
+      bool gt = false, eq = false;
+      if (t < wi) {
+        const uint64_t hp = rank_key(__ldcg(v + t), t, weighted) >> sh;
+        gt = take_all ? hp >= prefix : hp > prefix;
+        eq = !take_all && hp == prefix;
+      }
+      const uint32_t gb = __ballot_sync(0xffffffffu, gt), eb = __ballot_sync(0xffffffffu, eq);
+      if (lane == 0) { sg[t >> 5] = gb; zrow[t >> 5] = eb; }
+    }
+    if (take_all) need = 0;
+  }
+  if (tid == 0) s_need = need;
+  __syncthreads();
+  need = s_need;
+  const bool gather_all = s_fail;  // values from D for every entry
+  // ---- sweep: thread owns words [q0, q1) (an odd count: conflict-free)
+  int wpt = (wb + TKSEL_THREADS - 1) / TKSEL_THREADS;
+  wpt |= 1;
+  const uint32_t wmag = static_cast<uint32_t>((0x100000000ull + wpt - 1) / wpt);  // q / wpt
+  const int q0 = min(wb, tid * wpt), q1 = min(wb, q0 + wpt);
+  if (s_eqd) {  // take the first `need` tied positions; the tie row keeps
+                // exactly the taken bits (values gathered below, then cleared)
+    int ne = 0;
+    for (int q = q0; q < q1; ++q) ne += __popc(__ldcg(zrow + q));
+    int tot;
+    const int before = block_excl_scan(ne, ws, &tot);
+    int take = max(0, min(need - before, ne));
+    for (int q = q0; q < q1; ++q) {
+      uint32_t e = __ldcg(zrow + q);
+      if (!e) continue;
+      uint32_t add = 0u;
+      for (; take > 0 && e; --take) {
+        const uint32_t low = e & (0u - e);
+        add |= low;
+        e ^= low;
+      }
+      zrow[q] = add;
+      sg[q] |= add;
+    }
+  }
+  int ng = 0;
+  for (int q = q0; q < q1; ++q) ng += __popc(sg[q]);
+  int total;
+  int pos = block_excl_scan(ng, ws, &total);  // (its syncs also retire the lkey/lpos uses)
+  tbase[tid] = pos;
+  uint32_t* il = idx_list + static_cast<int64_t>(c) * cap;
+  double* vl = val_list + static_cast<int64_t>(c) * cap;
+  int32_t* rsc = em.rs ? em.rs + static_cast<int64_t>(c) * (em.nr + 1) : nullptr;
+  for (int q = q0; q < q1; ++q) {
+    wrel[q] = static_cast<uint16_t>(pos - tbase[tid]);
+    if (rsc && (q % (FOLD_RANGE / 32)) == 0) rsc[q / (FOLD_RANGE / 32)] = pos;
+    for (uint32_t m = sg[q]; m; m &= m - 1) il[pos++] = static_cast<uint32_t>(q * 32 + __ffs(m) - 1);
+  }
+  if (tid == 0) {
+    count[c] = total;
+    if (rsc) rsc[em.nr] = total;
+  }
+  __syncthreads();
+  // ---- values (and the client shift update when this kernel owns it)
+  double* hrow = em.hest ? em.hest + static_cast<int64_t>(c) * em.hest_stride : nullptr;
+  auto rank = [&](int t) {
+    const int q = t >> 5;
+    return tbase[__umulhi(static_cast<uint32_t>(q), wmag)] + wrel[q] +
+           __popc(sg[q] & ((1u << (t & 31)) - 1u));
+  };
+  auto put = [&](int t, double x) {
+    const int r = rank(t);
+    vl[r] = x;
+    if (hrow) hrow[t] = __dadd_rn(hrow[t], __dmul_rn(em.alpha, x));  // emit_entry
+  };
+  if (gather_all) {
+    for (int e = tid; e < total; e += TKSEL_THREADS) {
+      const int t = static_cast<int>(il[e]);
+      const double x = __ldg(v + t);
+      vl[e] = x;
+      if (hrow) hrow[t] = __dadd_rn(hrow[t], __dmul_rn(em.alpha, x));
+    }
+    if (s_eqd)
+      for (int q = q0; q < q1; ++q) zrow[q] = 0u;
+  } else {
+    // entries above the window: all selected
+    tksel_regions<UB>(gcnt, NR, capw, [&](const int* sl, const bool* vl_) {
+      int tt[UB];
+      uint64_t xb[UB];
+#pragma unroll
+      for (int u = 0; u < UB; ++u) {
+        tt[u] = vl_[u] ? __ldcg(gq + sl[u]) : -1;
+        xb[u] = vl_[u] ? __ldcg(gk + sl[u]) : 0ull;
+      }
+#pragma unroll
+      for (int u = 0; u < UB; ++u)
+        if (tt[u] >= 0) put(tt[u], __longlong_as_double(static_cast<long long>(xb[u])));
+    });
+    // candidates: the selected ones that are not taken ties
+    const bool eqd = s_eqd;
+    tksel_regions<UB>(mcnt, NR, capw, [&](const int* sl, const bool* vl_) {
+      int tt[UB];
+      uint64_t xb[UB];
+#pragma unroll
+      for (int u = 0; u < UB; ++u) {
+        tt[u] = vl_[u] ? __ldcg(cp + sl[u]) : -1;
+        xb[u] = vl_[u] ? __ldcg(ck + sl[u]) : 0ull;
+      }
+#pragma unroll
+      for (int u = 0; u < UB; ++u) {
+        const int t = tt[u];
+        if (t < 0) continue;
+        const uint32_t bit = 1u << (t & 31);
+        if ((sg[t >> 5] & bit) && !(eqd && (__ldcg(zrow + (t >> 5)) & bit)))
+          put(t, __longlong_as_double(static_cast<long long>(xb[u])));
+      }
+    });
+    // taken ties (zeros or tied candidates): values from D; the tie row cleared
+    if (eqd) {
+      __syncthreads();
+      for (int q = q0; q < q1; ++q) {
+        const uint32_t e = __ldcg(zrow + q);
+        if (!e) continue;
+        zrow[q] = 0u;
+        for (uint32_t m = e; m; m &= m - 1) {
+          const int t = q * 32 + __ffs(m) - 1;
+          put(t, __ldg(v + t));
+        }
+      }
+    }
+  }
+  if (g_dbg_on && tid == 0 && s_fail) {
+    atomicAdd(reinterpret_cast<unsigned long long*>(&g_dbg[17]), 1ull);
+    // which way the window failed: region overflow / G >= k / G + M + Z < k / digit list
+    const int why = s_over ? 24 : (G >= k ? 25 : (G + M + Z < k ? 26 : 27));
+    atomicAdd(reinterpret_cast<unsigned long long*>(&g_dbg[why]), 1ull);
+  }
 }
 
 // --------------------------------------------------------------- RandSeqK

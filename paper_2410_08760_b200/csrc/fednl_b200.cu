@@ -63,6 +63,8 @@ struct Ctx {
   bool solve_panels = false;  // k_chol_panels (d <= CP_MAX_D) instead of k_chol_solve
   int cp_kp = 1, cp_cs = 1;
   bool topk_stream = false;  // one-pass sampled-window TopK (else the shared-memory radix)
+  bool topk_split = false;   // ... as window / segmented pass / select kernels
+  int tks_S = 1, tks_lseg = 0, tks_capseg = 0, tks_ns = 2048;
   bool phase_events = false;   // per-kernel event records while capturing (timed runs)
   bool gexec_phase = false;    // the flavour the cached round graph was built with
   int num_sms = 148;
@@ -100,6 +102,11 @@ struct Ctx {
   double* val_list = nullptr;
   uint64_t* cand_key = nullptr;  // TopK streaming path: threshold-bin candidates
   int32_t* cand_pos = nullptr;
+  TkWin* tks_win = nullptr;      // split TopK: per-client key window
+  TkSeg* tks_seg = nullptr;      // split TopK: per-(client, segment) counts
+  uint64_t* gt_val = nullptr;    // split TopK: entries above the window (raw values)
+  int32_t* gt_pos = nullptr;
+  uint32_t* tks_eqz = nullptr;   // split TopK: zero / tie bit rows (all-zero between rounds)
   uint64_t* seeds = nullptr;
   RoundScalars* sc = nullptr;
   double *steps_table = nullptr, *trial_x = nullptr, *ls_loss_part = nullptr;
@@ -397,7 +404,7 @@ int launch_reduce(Ctx* ctx, cudaStream_t s, const double* x, const int32_t* clie
 // per-(client, round) streams from the device round counter.
 int launch_compress(Ctx* ctx, cudaStream_t s, const int32_t* clients, int n_active,
                     const uint64_t* seeds, double* dense_out, bool with_ctl = true,
-                    bool emit = true) {
+                    bool emit = true, bool client_update_in_fold = false) {
   const fb_config& c = ctx->cfg;
   DevCtl* ctl = with_ctl ? ctx->ctl : nullptr;
   Emit em{};
@@ -414,7 +421,25 @@ int launch_compress(Ctx* ctx, cudaStream_t s, const int32_t* clients, int n_acti
         k_topk_smem<<<n_active, TK_THREADS, tks_smem_bytes(ctx->w), s>>>(
             ctl, ctx->D, ctx->w, ctx->wb, c.k, c.topk_weighted, clients, ctx->flags, ctx->bitmap,
             ctx->count, ctx->idx_list, ctx->val_list, ctx->cap, ctx->draws, em);
-      else if (ctx->w <= TKST_MAXW)
+      else if (ctx->topk_split) {
+        k_tks_window<<<n_active, TKW_THREADS, 0, s>>>(ctl, ctx->D, ctx->w, c.k, ctx->tks_ns,
+                                                      c.topk_weighted, clients, ctx->flags,
+                                                      ctx->draws, ctx->tks_win);
+        CKL();
+        const int capw = ctx->tks_capseg / TKP_CW;
+        auto pass = c.topk_weighted ? k_tks_pass<true> : k_tks_pass<false>;
+        pass<<<dim3(ctx->tks_S, n_active), TKP_THREADS, TKP_SMEM, s>>>(
+            ctl, ctx->D, ctx->w, tks_wbp(ctx->w), ctx->tks_lseg, capw, clients, ctx->tks_win,
+            ctx->tks_eqz, ctx->cand_key, ctx->cand_pos, ctx->gt_val, ctx->gt_pos,
+            ctx->tks_seg);
+        CKL();
+        Emit es = em;
+        if (client_update_in_fold) es.hest = nullptr;
+        k_tks_select<<<n_active, TKSEL_THREADS, tksel_smem_bytes(ctx->w), s>>>(
+            ctx->D, ctx->w, tks_wbp(ctx->w), c.k, c.topk_weighted, ctx->tks_S, capw, clients,
+            ctx->tks_win, ctx->tks_seg, ctx->tks_eqz, ctx->cand_key, ctx->cand_pos,
+            ctx->gt_val, ctx->gt_pos, ctx->count, ctx->idx_list, ctx->val_list, ctx->cap, es);
+      } else if (ctx->w <= TKST_MAXW)
         k_topk_stream<<<n_active, TK_THREADS, tkst_smem_bytes(ctx->w), s>>>(
             ctl, ctx->D, ctx->w, ctx->wb, c.k, c.topk_weighted, clients, ctx->flags, ctx->bitmap,
             ctx->count, ctx->idx_list, ctx->val_list, ctx->cap, ctx->draws, ctx->cand_key,
@@ -517,7 +542,7 @@ bool dense_kind(const Ctx* ctx) {
 // master fold Hout = Hin + (alpha/n) sum_c delta_c (ascending c); for the
 // dense kinds the client shift update rides along when `hest` is non-null
 int launch_master_fold(Ctx* ctx, cudaStream_t s, const int32_t* clients, int n_active,
-                       double* hest, const double* h_in, double* h_out) {
+                       double* hest, const double* h_in, double* h_out, bool client_update = false) {
   if (dense_kind(ctx)) {
     k_fold_dense<<<static_cast<unsigned>((ctx->w + 255) / 256), 256, 0, s>>>(
         ctx->ctl, ctx->w, n_active, clients, ctx->cfg.alpha, ctx->alpha_n, ctx->D, ctx->count,
@@ -526,7 +551,8 @@ int launch_master_fold(Ctx* ctx, cudaStream_t s, const int32_t* clients, int n_a
     const size_t smem = sizeof(int32_t) * (3 * static_cast<size_t>(n_active) + 1);
     k_master_fold<<<ctx->nr, FOLD_THREADS, smem, s>>>(
         ctx->ctl, ctx->w, n_active, clients, ctx->cap, ctx->nr, ctx->rs, ctx->idx_list,
-        ctx->val_list, ctx->alpha_n, h_in, h_out);
+        ctx->val_list, ctx->alpha_n, h_in, h_out, client_update ? ctx->hest : nullptr, ctx->w,
+        ctx->cfg.alpha);
   }
   CKL();
   return FB_OK;
@@ -615,7 +641,10 @@ int enqueue_fednl_round(Ctx* ctx) {
   CK(cudaStreamWaitEvent(ctx->st2, ctx->ev_solve_launched, 0));
   static const bool fold_late = getenv("FB_FOLD_LATE") && atoi(getenv("FB_FOLD_LATE"));
   TRY(record(ctx, EV_COMP_START, ctx->st2));
-  TRY(launch_compress(ctx, ctx->st2, loc, n_loc, nullptr, nullptr));
+  // split TopK: the client shift update runs in the fold (K7), which stages
+  // every client's entries per position range anyway
+  const bool cu_fold = ctx->topk_split && !shd;
+  TRY(launch_compress(ctx, ctx->st2, loc, n_loc, nullptr, nullptr, true, true, cu_fold));
   if (shd) {  // every rank folds every client's delta (ascending client id)
     TRY(gather_clients(ctx, ctx->idx_list, ctx->cap, ncclUint32, ctx->st2));
     TRY(gather_clients(ctx, ctx->val_list, ctx->cap, ncclFloat64, ctx->st2));
@@ -626,11 +655,11 @@ int enqueue_fednl_round(Ctx* ctx) {
   TRY(record(ctx, EV_FOLD_START, ctx->st2));
   if (!fold_late)
     TRY(launch_master_fold(ctx, ctx->st2, nullptr, n, dense_kind(ctx) ? ctx->hest : nullptr,
-                           ctx->hmas, ctx->hmas2));
+                           ctx->hmas, ctx->hmas2, cu_fold));
   TRY(record(ctx, EV_FOLD_END, ctx->st2));
   CK(cudaEventRecord(ctx->ev_join, ctx->st2));
   TRY(record(ctx, EV_SOLVE_END, s));
-  int launches = 8;
+  int launches = ctx->topk_split ? 10 : 8;
   if (ls) {
     k_dot<<<1, 256, 0, s>>>(ctx->ctl, ctx->d, ctx->gbar, ctx->pvec, ctx->sc);
     CKL();
@@ -648,7 +677,7 @@ int enqueue_fednl_round(Ctx* ctx) {
   CK(cudaStreamWaitEvent(s, ctx->ev_join, 0));
   if (fold_late)
     TRY(launch_master_fold(ctx, s, nullptr, n, dense_kind(ctx) ? ctx->hest : nullptr, ctx->hmas,
-                           ctx->hmas2));
+                           ctx->hmas2, cu_fold));
   CK(cudaMemcpyAsync(ctx->hmas, ctx->hmas2, sizeof(double) * ctx->w, cudaMemcpyDeviceToDevice, s));
   k_finish<<<1, 256, 0, s>>>(ctx->ctl, ctx->d, n, n, nullptr, ctx->x, ctx->x_new, 1, ctx->count,
                              ctx->row_counts, ctx->row_ls);
@@ -729,7 +758,7 @@ int enqueue_pp_round(Ctx* ctx) {
                              ctx->row_counts, ctx->row_ls);
   CKL();
   TRY(record(ctx, EV_END, s));
-  ctx->launches_per_round = 16;
+  ctx->launches_per_round = ctx->topk_split ? 18 : 16;
   return FB_OK;
 }
 
@@ -956,6 +985,12 @@ int fb_create(const fb_config* cfg_in, void** out) {
                            static_cast<int>(MC_SMEM_MAX)));
   CKC(cudaFuncSetAttribute(k_topk_stream, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            static_cast<int>(tkst_smem_bytes(TKST_MAXW))));
+  CKC(cudaFuncSetAttribute(k_tks_pass<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           static_cast<int>(TKP_SMEM)));
+  CKC(cudaFuncSetAttribute(k_tks_pass<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           static_cast<int>(TKP_SMEM)));
+  CKC(cudaFuncSetAttribute(k_tks_select, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           static_cast<int>(tksel_smem_bytes(TKST_MAXW))));
   static size_t max_fold = 0;
   max_fold = std::max(max_fold, sizeof(int32_t) * (3 * static_cast<size_t>(c.n_clients) + 1));
   CKC(cudaFuncSetAttribute(k_master_fold, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -983,6 +1018,28 @@ int fb_create(const fb_config* cfg_in, void** out) {
   const bool stream_topk = c.kind == FB_KIND_TOPK && w <= TKST_MAXW &&
                            (ts_env ? atoi(ts_env) != 0 : (w > TKS_MAXW || w >= TKST_MINW));
   ctx->topk_stream = stream_topk;
+  // the stream as many small CTAs (about two waves of 8 per SM) + a select
+  // kernel; FB_TOPK_SPLIT=0 keeps the one-CTA-per-client k_topk_stream
+  const char* sp_env = getenv("FB_TOPK_SPLIT");
+  ctx->topk_split = stream_topk && (sp_env ? atoi(sp_env) != 0
+                                            : static_cast<int64_t>(w) * n >= (int64_t{1} << 26));
+  size_t cand_slots = stream_topk ? static_cast<size_t>(n) * TKST_CAP : 1;
+  if (ctx->topk_split) {
+    // positions per CTA: one wave of two CTAs per SM when that is 8..64
+    // ring stages each, else as close to 64 stages as an even split allows
+    int64_t L = (static_cast<int64_t>(w) * n) / (2 * ctx->num_sms);
+    L = std::min<int64_t>(std::max<int64_t>(L, 8 * TKP_CH), 64 * TKP_CH);
+    int64_t S = std::max<int64_t>(1, (w + L / 2) / L);
+    S = std::min<int64_t>(S, TKP_MAXSEG);
+    int64_t lseg = ((w + S - 1) / S + TKP_CH - 1) / TKP_CH * TKP_CH;
+    ctx->tks_lseg = static_cast<int>(lseg);
+    ctx->tks_S = static_cast<int>((w + lseg - 1) / lseg);
+    ctx->tks_capseg = static_cast<int>(std::min<int64_t>(lseg, TKP_SEGCAP));
+    int ns = 2048;
+    while (ns < TKW_MAXSAMPLE && ns * 64 <= w) ns *= 2;
+    ctx->tks_ns = ns;
+    cand_slots = static_cast<size_t>(n) * ctx->tks_S * ctx->tks_capseg;
+  }
   const int tau = ctx->tau;
   if (dalloc(ctx, &ctx->ctl, 1) || dalloc(ctx, &ctx->Bt, static_cast<size_t>(n) * d * ctx->ldj) ||
       dalloc(ctx, &ctx->x, d) || dalloc(ctx, &ctx->x_new, d) || dalloc(ctx, &ctx->pvec, d) ||
@@ -999,13 +1056,17 @@ int fb_create(const fb_config* cfg_in, void** out) {
       dalloc(ctx, &ctx->M, static_cast<size_t>(d + 1) * (d + 1)) ||
       dalloc(ctx, &ctx->Lg, ctx->solve_panels ? static_cast<size_t>((d + CP_NB - 1) / CP_NB) *
                                                     cp_rows(d) * CP_LS : 1) ||
-      dalloc(ctx, &ctx->bitmap, static_cast<size_t>(n) * ctx->wb) || dalloc(ctx, &ctx->count, n) ||
+      dalloc(ctx, &ctx->bitmap, static_cast<size_t>(n) * tks_wbp(w)) || dalloc(ctx, &ctx->count, n) ||
       dalloc(ctx, &ctx->draws, n) ||
       dalloc(ctx, &ctx->idx_list, static_cast<size_t>(n) * ctx->cap) ||
       dalloc(ctx, &ctx->val_list, static_cast<size_t>(n) * ctx->cap) ||
       dalloc(ctx, &ctx->seeds, n) || dalloc(ctx, &ctx->pair_order, ctx->n_pairs) ||
-      dalloc(ctx, &ctx->cand_key, stream_topk ? static_cast<size_t>(n) * TKST_CAP : 1) ||
-      dalloc(ctx, &ctx->cand_pos, stream_topk ? static_cast<size_t>(n) * TKST_CAP : 1) ||
+      dalloc(ctx, &ctx->cand_key, cand_slots) || dalloc(ctx, &ctx->cand_pos, cand_slots) ||
+      dalloc(ctx, &ctx->tks_win, ctx->topk_split ? n : 1) ||
+      dalloc(ctx, &ctx->gt_val, ctx->topk_split ? cand_slots : 1) ||
+      dalloc(ctx, &ctx->gt_pos, ctx->topk_split ? cand_slots : 1) ||
+      dalloc(ctx, &ctx->tks_seg, ctx->topk_split ? static_cast<size_t>(n) * ctx->tks_S * TKP_CW : 1) ||
+      dalloc(ctx, &ctx->tks_eqz, ctx->topk_split ? static_cast<size_t>(n) * tks_wbp(w) : 1) ||
       dalloc(ctx, &ctx->sc, 1) || dalloc(ctx, &ctx->steps_table, 64) ||
       dalloc(ctx, &ctx->trial_x, static_cast<size_t>(LS_BATCH) * d) ||
       dalloc(ctx, &ctx->ls_loss_part, static_cast<size_t>(LS_BATCH) * n * ctx->ls_nblk) ||

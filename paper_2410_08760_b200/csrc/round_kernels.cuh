@@ -218,7 +218,8 @@ constexpr int FOLD_STAGE = 4096;  // staged entries per pass
 __global__ void __launch_bounds__(FOLD_THREADS) k_master_fold(
     const DevCtl* __restrict__ ctl, int64_t w, int n_active, const int32_t* __restrict__ clients,
     int cap, int nr, const int32_t* __restrict__ rs, const uint32_t* __restrict__ idx_list,
-    const double* __restrict__ val_list, double alpha_n, const double* h_in, double* h_out) {
+    const double* __restrict__ val_list, double alpha_n, const double* h_in, double* h_out,
+    double* __restrict__ hest = nullptr, int64_t hest_stride = 0, double alpha = 0.0) {
   if (ctl->halt) return;
   extern __shared__ int32_t fold_sm[];  // beg[n], cnt[n], off[n+1]
   __shared__ double hs[FOLD_RANGE];
@@ -283,6 +284,10 @@ __global__ void __launch_bounds__(FOLD_THREADS) k_master_fold(
           const int64_t src = static_cast<int64_t>(c) * cap + beg[a] + (e - off[a]);
           ti[u] = idx_list[src];
           tv[u] = val_list[src];
+          if (hest) {  // the client shift update (compressors.py:373-393), distinct (c, t)
+            double* hp = hest + static_cast<int64_t>(c) * hest_stride + ti[u];
+            *hp = __dadd_rn(*hp, __dmul_rn(alpha, tv[u]));
+          }
         }
       }
 #pragma unroll

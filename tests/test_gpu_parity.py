@@ -70,6 +70,17 @@ def test_device_partial_shuffle_and_round_seeds():
 # --------------------------------------------------------------------- P1
 
 
+@pytest.fixture(params=["0", "1"], ids=["stream", "split"])
+def topk_path(request, monkeypatch):
+    """Both large-w TopK paths: the one-CTA-per-client k_topk_stream and the
+    window / segmented pass / select kernels (chosen per context at creation;
+    FB_TOPK_SPLIT forces either, the compress engines are re-created)."""
+    monkeypatch.setenv("FB_TOPK_SPLIT", request.param)
+    leaf._compress_engine.cache_clear()
+    yield request.param
+    leaf._compress_engine.cache_clear()
+
+
 def _golden_compress_cases():
     g = golden("compress.npz")
     for name in g["case_names"].tolist():
@@ -126,7 +137,7 @@ def test_topk_round0_full_c0_shape_ties():
 
 
 @pytest.mark.parametrize("kind,k", [("topk", 2408), ("randseqk", 2408), ("randk", 301), ("topk", 45451)])
-def test_compressors_bit_exact_at_c0_size(kind, k):
+def test_compressors_bit_exact_at_c0_size(kind, k, topk_path):
     """Random and tie-heavy inputs at w = 45451 against the oracle."""
     d = 301
     w = O.packed_len(d)
@@ -148,7 +159,7 @@ def test_compressors_bit_exact_at_c0_size(kind, k):
 
 
 @pytest.mark.parametrize("k", [8192, 1, 524800])
-def test_topk_streaming_path_bit_exact_at_c4_size(k):
+def test_topk_streaming_path_bit_exact_at_c4_size(k, topk_path):
     """w = 524,800 (c4) runs the streaming TopK (keys do not fit in shared
     memory): candidate path, exact-tie path, zero ties, take-all."""
     d = 1024
@@ -169,6 +180,69 @@ def test_topk_streaming_path_bit_exact_at_c4_size(k):
         assert got[c].entry_count == want.count, c
         assert np.array_equal(got[c].indices, want.indices), c
         assert np.array_equal(got[c].values, want.values), c
+
+
+def test_topk_split_path_fallbacks_and_scratch_reuse(topk_path):
+    """c4-like batch (n*w large enough that a segment's candidate slots are
+    fewer than its positions): window miss (the strided sample sees only the
+    small keys), a segment overflowing its candidate slots (one tie bin holds
+    every key), tie bins beyond the select kernel's shared-memory list, zeros
+    completing the set.  The same engine compresses the batch twice in
+    different client orders: the tie/zero scratch rows must come back clean."""
+    d = 1024
+    w = O.packed_len(d)
+    n = 80
+    k = 8192
+    rng = np.random.default_rng(31)
+    P = rng.standard_normal((n, w))
+    i = np.arange(8192)  # the window kernel's sample positions (tks_sample_pos)
+    ts = (i // 8) * (w - 8) // 1024 + i % 8
+    P[1] = 5.0 + rng.random(w)
+    P[1, ts] = 1e-3
+    P[2] = 1.0
+    P[3] = np.round(P[3] * 4) / 4
+    P[4] = 0.0
+    P[4, rng.choice(w, 50, replace=False)] = 1.0
+    P[5] *= rng.random(w) < 0.5
+    P[6] = 0.0
+    spec = CompressorSpec(CompressorKind.TOPK, k=k)
+    check = list(range(8)) + [n - 2, n - 1]
+    for order in (np.arange(n), np.arange(n)[::-1]):
+        Q = np.ascontiguousarray(P[order])
+        seeds = [O.round_seed(5, int(c), 2) for c in order]
+        got = leaf.compress_packed_batch(Q, d, spec, seeds)
+        for slot, c in enumerate(order):
+            if c not in check:
+                continue
+            want = O.compress_packed(P[c], d, "topk", k, O.SplitMix64(seeds[slot]))
+            assert got[slot].entry_count == want.count, c
+            assert np.array_equal(got[slot].indices, want.indices), c
+            assert np.array_equal(got[slot].values, want.values), c
+    # c0 shape (w = 45,451 is not a multiple of the select kernel's block):
+    # window misses both ways, converged-regime zero completion
+    d = 301
+    w = O.packed_len(d)
+    i = np.arange(2048)
+    ts = (i // 8) * (w - 8) // 256 + i % 8
+    P = rng.standard_normal((6, w))
+    P[0] = 5.0 + rng.random(w)
+    P[0, ts] = 1e-3  # G >= k
+    P[1] = 1e-3 * rng.random(w)
+    P[1, ts] = 5.0  # G + M < k
+    P[2] = 0.0
+    P[2, rng.choice(w, 3000, replace=False)] = rng.standard_normal(3000) * 1e-12
+    P[3] = 0.0
+    P[3, 7000:9500] = rng.standard_normal(2500)  # nonzeros clustered away from the sample
+    P[4] = 0.0
+    P[4, ts[::4]] = 1.0
+    seeds = [O.round_seed(6, c, 9) for c in range(6)]
+    for rep in range(2):
+        got = leaf.compress_packed_batch(P, d, CompressorSpec(CompressorKind.TOPK, k=2408), seeds)
+        for c in range(6):
+            want = O.compress_packed(P[c], d, "topk", 2408, O.SplitMix64(seeds[c]))
+            assert got[c].entry_count == want.count, (rep, c)
+            assert np.array_equal(got[c].indices, want.indices), (rep, c)
+            assert np.array_equal(got[c].values, want.values), (rep, c)
 
 
 def test_randk_hash_pool_path_bit_exact():
@@ -305,6 +379,20 @@ def test_round_fold_bit_exact_given_device_deltas(kind, k):
     # and the iterate: x1 = x0 - solve(H_pre + l I, gbar) within 1e-10
     assert np.all(np.isfinite(eng.get_x())) and not np.array_equal(eng.get_x(), x0)
     eng.close()
+
+
+def test_split_topk_rounds_bit_identical_to_stream_path(monkeypatch):
+    """c0 rounds through the split TopK (client shift update moved into the
+    master fold) reproduce the pinned k_topk_stream round bit for bit: same
+    selections, same shift and fold arithmetic, same trajectory."""
+    cfg, shards = sim_case("c0_r4")
+    cfg = RunConfig(compressor=cfg.compressor, rounds=12, alpha=cfg.alpha, run_seed=cfg.run_seed)
+    out = {}
+    for path in ("0", "1"):
+        monkeypatch.setenv("FB_TOPK_SPLIT", path)
+        out[path] = simulate(cfg, shards)
+    for a, b in zip(out["0"], out["1"]):
+        assert (a.round, a.grad_norm, a.f_value, a.bytes_up_cum) == (b.round, b.grad_norm, b.f_value, b.bytes_up_cum)
 
 
 # --------------------------------------------------------------------- P6
