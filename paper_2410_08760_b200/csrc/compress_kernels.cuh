@@ -1071,8 +1071,13 @@ __host__ __device__ constexpr int tks_wbp(int64_t w) {  // bitmap row stride (16
 }
 __host__ __device__ constexpr size_t tksel_smem_bytes(int64_t w) {
   return static_cast<size_t>(tks_wbp(w)) * 4 +
-         (static_cast<size_t>(tks_wbp(w)) * 2 > TKSEL_LCAP * 12 ? static_cast<size_t>(tks_wbp(w)) * 2
-                                                                 : TKSEL_LCAP * 12);
+         ((static_cast<size_t>(tks_wbp(w)) / 8 + 1) * 4 > TKSEL_LCAP * 12
+              ? (static_cast<size_t>(tks_wbp(w)) / 8 + 1) * 4
+              : TKSEL_LCAP * 12);
+}
+
+__host__ __device__ constexpr size_t tkp_smem_bytes(int64_t w) {  // ring, then the selection
+  return TKP_SMEM > tksel_smem_bytes(w) ? TKP_SMEM : tksel_smem_bytes(w);
 }
 
 struct TkWin {
@@ -1115,19 +1120,25 @@ __host__ __device__ __forceinline__ int64_t tks_sample_pos(int i, int ns, int64_
   return (static_cast<int64_t>(i >> 3) * (w - 8)) / runs + (i & 7);
 }
 
-__global__ void __launch_bounds__(TKW_THREADS) k_tks_window(
+__global__ void __launch_bounds__(TKW_THREADS, 2) k_tks_window(
     const DevCtl* __restrict__ ctl, const double* __restrict__ D, int64_t w, int k, int ns,
     int weighted, const int32_t* __restrict__ clients, const int32_t* __restrict__ flags,
-    int32_t* __restrict__ draws, TkWin* __restrict__ win) {
+    int32_t* __restrict__ draws, TkWin* __restrict__ win, int32_t* __restrict__ ticket,
+    int32_t* __restrict__ count, Emit em) {
+  const int c = client_of(clients, blockIdx.x);
+  const int tid = threadIdx.x, lane = tid & 31;
+  if (tid == 0) ticket[c] = 0;  // the pass CTAs of this round count in from zero
   if (ctl && ctl->halt) return;
   __shared__ uint32_t hist[2048], hist2[2048];
   __shared__ int ws[64];
   __shared__ int s_digit, s_above;
-  const int c = client_of(clients, blockIdx.x);
-  const int tid = threadIdx.x, lane = tid & 31;
   if (tid == 0 && draws) draws[c] = 0;
   if (!(flags[c] & 2)) {  // all-zero difference: empty delta, no draws
-    if (tid == 0) win[c] = TkWin{0, 0, 0, 0};
+    if (tid == 0) {
+      win[c] = TkWin{0, 0, 0, 0};
+      count[c] = 0;
+    }
+    emit_empty(em, c);
     return;
   }
   const double* v = D + static_cast<int64_t>(c) * w;
@@ -1277,6 +1288,15 @@ __device__ __forceinline__ void tkp_consume(const double* ring, uint64_t* full, 
   }
 }
 
+__device__ __noinline__ void tks_select_client(
+    int c, uint32_t* sg, const double* __restrict__ D, int64_t w, int wbp, int k, int weighted,
+    int S_seg, int capw, const int32_t* __restrict__ clients, const TkWin* __restrict__ win,
+    const TkSeg* __restrict__ seg, uint32_t* __restrict__ eqz, const uint64_t* __restrict__ cand_key,
+    const int32_t* __restrict__ cand_pos, const uint64_t* __restrict__ gt_val,
+    const int32_t* __restrict__ gt_pos, int32_t* __restrict__ count, uint32_t* __restrict__ idx_list,
+    double* __restrict__ val_list, int cap, Emit em);
+static_assert(FOLD_RANGE == 8 * 32, "the selection's 8-word rank groups are the fold's ranges");
+
 // seg[(c * S + s) * TKP_CW + warp] = (G, M, Z) of one consumer warp's share;
 // its list region is slots [((c * S + s) * TKP_CW + warp) * capw, + capw)
 template <bool W>
@@ -1284,10 +1304,13 @@ __global__ void __launch_bounds__(TKP_THREADS) k_tks_pass(
     const DevCtl* __restrict__ ctl, const double* __restrict__ D, int64_t w, int wbp, int lseg,
     int capw, const int32_t* __restrict__ clients, const TkWin* __restrict__ win,
     uint32_t* __restrict__ eqz, uint64_t* __restrict__ cand_key, int32_t* __restrict__ cand_pos,
-    uint64_t* __restrict__ gt_val, int32_t* __restrict__ gt_pos, TkSeg* __restrict__ seg) {
+    uint64_t* __restrict__ gt_val, int32_t* __restrict__ gt_pos, TkSeg* __restrict__ seg,
+    int32_t* __restrict__ ticket, int k, int32_t* __restrict__ count, uint32_t* __restrict__ idx_list,
+    double* __restrict__ val_list, int cap, Emit em) {
   if (ctl && ctl->halt) return;
   extern __shared__ __align__(128) double ring[];
   __shared__ __align__(8) uint64_t full[TKP_NST], empty[TKP_NST];
+  __shared__ int s_last;
   const int c = client_of(clients, blockIdx.y);
   const TkWin wn = win[c];
   if (!wn.active) return;
@@ -1318,8 +1341,7 @@ __global__ void __launch_bounds__(TKP_THREADS) k_tks_pass(
         bulk_load(ring + st * TKP_STRIDE, v + t0 + i * TKP_CH - lead, bytes, &full[st]);
       }
     }
-    return;
-  }
+  } else {
   uint32_t* zrow = eqz + static_cast<int64_t>(c) * wbp;
   const int64_t sub = (static_cast<int64_t>(c) * S + s) * TKP_CW + warp;
   const int64_t lbase = sub * capw;
@@ -1333,6 +1355,18 @@ __global__ void __launch_bounds__(TKP_THREADS) k_tks_pass(
                           cand_key + lbase, cand_pos + lbase, gt_val + lbase, gt_pos + lbase,
                           capw, m_cnt, g_cnt, z_cnt);
   if (lane == 0) seg[sub] = TkSeg{g_cnt, m_cnt, z_cnt, 0};
+  }
+  // the last of the client's segment CTAs to finish runs its selection (the
+  // ring is free again: its shared memory becomes the selection row)
+  __threadfence();
+  __syncthreads();
+  if (tid == 0) s_last = atomicAdd(&ticket[c], 1) == S - 1;
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  tks_select_client(c, reinterpret_cast<uint32_t*>(ring), D, w, wbp, k, W ? 1 : 0, S, capw, clients,
+                    win, seg, eqz, cand_key, cand_pos, gt_val, gt_pos, count, idx_list, val_list,
+                    cap, em);
 }
 
 // radix levels over candidate keys (source `get(e)` for e < cnt) whose bits
@@ -1402,26 +1436,28 @@ __device__ __forceinline__ void tksel_regions(const int* cnt, int nreg, int capw
   }
 }
 
-__global__ void __launch_bounds__(TKSEL_THREADS) k_tks_select(
-    const double* __restrict__ D, int64_t w, int wbp, int k, int weighted, int S_seg, int capw,
+// The selection of one client, run by the last of its pass CTAs to finish
+// (any blockDim multiple of 32, <= 1024; `sg` = the CTA's dynamic shared
+// memory, tksel_smem_bytes(w) bytes).  Clients with an all-zero difference
+// are emitted by k_tks_window.
+__device__ __noinline__ void tks_select_client(
+    int c, uint32_t* sg, const double* __restrict__ D, int64_t w, int wbp, int k, int weighted, int S_seg, int capw,
     const int32_t* __restrict__ clients, const TkWin* __restrict__ win, const TkSeg* __restrict__ seg,
     uint32_t* __restrict__ eqz, const uint64_t* __restrict__ cand_key,
     const int32_t* __restrict__ cand_pos, const uint64_t* __restrict__ gt_val,
     const int32_t* __restrict__ gt_pos, int32_t* __restrict__ count, uint32_t* __restrict__ idx_list,
     double* __restrict__ val_list, int cap, Emit em) {
-  // no halt check: the tie row must be left clean whenever the pass ran
   // dynamic: sg[wbp] u32 (the selection row) | union { lkey[LCAP] u64,
-  //          lpos[LCAP] i32 (resolve) ; wrel[wbp] u16 (rank within a thread) }
-  extern __shared__ __align__(16) uint32_t sg[];
+  //          lpos[LCAP] i32 (resolve) ; grp[wbp / 8 + 1] i32 (the rank of the
+  //          first entry of every 8-word group, = the fold's range starts) }
   uint64_t* lkey = reinterpret_cast<uint64_t*>(sg + wbp);
   int32_t* lpos = reinterpret_cast<int32_t*>(lkey + TKSEL_LCAP);
-  uint16_t* wrel = reinterpret_cast<uint16_t*>(sg + wbp);
+  int32_t* grp = reinterpret_cast<int32_t*>(sg + wbp);
   __shared__ uint32_t hist[2048];
   __shared__ int mcnt[TKP_MAXSUB], gcnt[TKP_MAXSUB];
-  __shared__ int tbase[TKSEL_THREADS];
+  const int TKSEL_THREADS = blockDim.x;
   __shared__ int ws[64];
   __shared__ int s_digit, s_above, s_nl, s_G, s_M, s_Z, s_over, s_need, s_eqd, s_fail;
-  const int c = client_of(clients, blockIdx.x);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int NR = S_seg * TKP_CW;  // list regions (segment x consumer warp)
   const int wi = static_cast<int>(w);
@@ -1429,11 +1465,6 @@ __global__ void __launch_bounds__(TKSEL_THREADS) k_tks_select(
   const double* v = D + static_cast<int64_t>(c) * w;
   uint32_t* zrow = eqz + static_cast<int64_t>(c) * wbp;
   const TkWin wn = win[c];
-  if (!wn.active) {
-    emit_empty(em, c);
-    if (tid == 0) count[c] = 0;
-    return;
-  }
   {
     uint4* s4 = reinterpret_cast<uint4*>(sg);
     for (int i = tid; i < wbp / 4; i += TKSEL_THREADS) s4[i] = make_uint4(0, 0, 0, 0);
@@ -1447,7 +1478,9 @@ __global__ void __launch_bounds__(TKSEL_THREADS) k_tks_select(
   if (warp == 0) {
     int g = 0, m = 0, z = 0, over = 0;
     for (int j = lane; j < NR; j += 32) {
-      const TkSeg sr = seg[static_cast<int64_t>(c) * NR + j];
+      // written by the other segment CTAs of this kernel: L2, not the read-only path
+      const int4 r4 = __ldcg(reinterpret_cast<const int4*>(seg) + static_cast<int64_t>(c) * NR + j);
+      const TkSeg sr{r4.x, r4.y, r4.z, r4.w};
       over |= (sr.m > capw) | (sr.g > capw);
       mcnt[j] = min(sr.m, capw);
       gcnt[j] = min(sr.g, capw);
@@ -1504,7 +1537,7 @@ __global__ void __launch_bounds__(TKSEL_THREADS) k_tks_select(
     const uint64_t pf0 = static_cast<uint64_t>(static_cast<uint32_t>(wn.hhi)) >> (top - 31);
     // radix levels over the candidate regions (11 bits below `top` first)
     // until the threshold digit's bin fits the shared-memory list
-    int hi_excl = top + 1, sh = hi_excl;
+    int hi_excl = top + 1, sh = hi_excl, nbin = M;
     uint64_t pf = pf0;
     bool all = false;
     for (int lv = 0; lv < 6 && hi_excl > 0; ++lv) {
@@ -1528,14 +1561,16 @@ __global__ void __launch_bounds__(TKSEL_THREADS) k_tks_select(
       tk_find_digit_n(hist, 1 << bits, need, ws, &s_digit, &s_above);
       need -= s_above;
       pf = (pf << bits) | static_cast<uint64_t>(s_digit);
-      const int nbin = static_cast<int>(hist[s_digit]);
+      nbin = static_cast<int>(hist[s_digit]);
       __syncthreads();
       hi_excl = sh;
       if (nbin == need) { all = true; break; }
       if (nbin <= TKSEL_LCAP) break;
     }
     // above the threshold prefix -> selected; in it -> the shared-memory list
-    // (or, when the whole bin is taken, selected as well)
+    // (or, when the whole bin is taken, selected as well; or, when the final
+    // bin is a tie class larger than the list, tie-marked directly)
+    const bool direct = !all && nbin > TKSEL_LCAP;
     tksel_regions<UB>(mcnt, NR, capw, [&](const int* sl, const bool* vl_) {
       uint64_t kk[UB];
       int tt[UB];
@@ -1551,14 +1586,21 @@ __global__ void __launch_bounds__(TKSEL_THREADS) k_tks_select(
         if (hp > pf || (all && hp == pf)) {
           mark(tt[u]);
         } else if (hp == pf) {
-          const int i = atomicAdd(&s_nl, 1);
-          if (i < TKSEL_LCAP) { lkey[i] = kk[u]; lpos[i] = tt[u]; }
+          if (direct) {
+            mark_eq(tt[u]);
+            s_eqd = 1;
+          } else {
+            const int i = atomicAdd(&s_nl, 1);
+            if (i < TKSEL_LCAP) { lkey[i] = kk[u]; lpos[i] = tt[u]; }
+          }
         }
       }
     });
     __syncthreads();
     if (all) {
       need = 0;
+    } else if (direct) {
+      // the eq take below picks the first `need` tied positions
     } else if (s_nl <= TKSEL_LCAP) {
       const int nl = s_nl;
       auto lk = [&](int e) { return lkey[e]; };
@@ -1633,7 +1675,7 @@ __global__ void __launch_bounds__(TKSEL_THREADS) k_tks_select(
         eq = !take_all && hp == prefix;
       }
       const uint32_t gb = __ballot_sync(0xffffffffu, gt), eb = __ballot_sync(0xffffffffu, eq);
-      if (lane == 0) { sg[t >> 5] = gb; zrow[t >> 5] = eb; }
+      if (lane == 0 && (t >> 5) < wb) { sg[t >> 5] = gb; zrow[t >> 5] = eb; }
     }
     if (take_all) need = 0;
   }
@@ -1644,7 +1686,6 @@ __global__ void __launch_bounds__(TKSEL_THREADS) k_tks_select(
   // ---- sweep: thread owns words [q0, q1) (an odd count: conflict-free)
   int wpt = (wb + TKSEL_THREADS - 1) / TKSEL_THREADS;
   wpt |= 1;
-  const uint32_t wmag = static_cast<uint32_t>((0x100000000ull + wpt - 1) / wpt);  // q / wpt
   const int q0 = min(wb, tid * wpt), q1 = min(wb, q0 + wpt);
   if (s_eqd) {  // take the first `need` tied positions; the tie row keeps
                 // exactly the taken bits (values gathered below, then cleared)
@@ -1670,13 +1711,14 @@ __global__ void __launch_bounds__(TKSEL_THREADS) k_tks_select(
   for (int q = q0; q < q1; ++q) ng += __popc(sg[q]);
   int total;
   int pos = block_excl_scan(ng, ws, &total);  // (its syncs also retire the lkey/lpos uses)
-  tbase[tid] = pos;
   uint32_t* il = idx_list + static_cast<int64_t>(c) * cap;
   double* vl = val_list + static_cast<int64_t>(c) * cap;
   int32_t* rsc = em.rs ? em.rs + static_cast<int64_t>(c) * (em.nr + 1) : nullptr;
   for (int q = q0; q < q1; ++q) {
-    wrel[q] = static_cast<uint16_t>(pos - tbase[tid]);
-    if (rsc && (q % (FOLD_RANGE / 32)) == 0) rsc[q / (FOLD_RANGE / 32)] = pos;
+    if ((q & 7) == 0) {
+      grp[q >> 3] = pos;
+      if (rsc) rsc[q >> 3] = pos;  // FOLD_RANGE = 8 words
+    }
     for (uint32_t m = sg[q]; m; m &= m - 1) il[pos++] = static_cast<uint32_t>(q * 32 + __ffs(m) - 1);
   }
   if (tid == 0) {
@@ -1688,8 +1730,9 @@ __global__ void __launch_bounds__(TKSEL_THREADS) k_tks_select(
   double* hrow = em.hest ? em.hest + static_cast<int64_t>(c) * em.hest_stride : nullptr;
   auto rank = [&](int t) {
     const int q = t >> 5;
-    return tbase[__umulhi(static_cast<uint32_t>(q), wmag)] + wrel[q] +
-           __popc(sg[q] & ((1u << (t & 31)) - 1u));
+    int r = grp[q >> 3];
+    for (int qq = q & ~7; qq < q; ++qq) r += __popc(sg[qq]);
+    return r + __popc(sg[q] & ((1u << (t & 31)) - 1u));
   };
   auto put = [&](int t, double x) {
     const int r = rank(t);

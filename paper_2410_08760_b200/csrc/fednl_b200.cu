@@ -106,6 +106,7 @@ struct Ctx {
   TkSeg* tks_seg = nullptr;      // split TopK: per-(client, segment) counts
   uint64_t* gt_val = nullptr;    // split TopK: entries above the window (raw values)
   int32_t* gt_pos = nullptr;
+  int32_t* tks_ticket = nullptr;  // split TopK: finished segment CTAs per client
   uint32_t* tks_eqz = nullptr;   // split TopK: zero / tie bit rows (all-zero between rounds)
   uint64_t* seeds = nullptr;
   RoundScalars* sc = nullptr;
@@ -422,23 +423,19 @@ int launch_compress(Ctx* ctx, cudaStream_t s, const int32_t* clients, int n_acti
             ctl, ctx->D, ctx->w, ctx->wb, c.k, c.topk_weighted, clients, ctx->flags, ctx->bitmap,
             ctx->count, ctx->idx_list, ctx->val_list, ctx->cap, ctx->draws, em);
       else if (ctx->topk_split) {
+        Emit es = em;
+        if (client_update_in_fold) es.hest = nullptr;
         k_tks_window<<<n_active, TKW_THREADS, 0, s>>>(ctl, ctx->D, ctx->w, c.k, ctx->tks_ns,
                                                       c.topk_weighted, clients, ctx->flags,
-                                                      ctx->draws, ctx->tks_win);
+                                                      ctx->draws, ctx->tks_win, ctx->tks_ticket,
+                                                      ctx->count, es);
         CKL();
         const int capw = ctx->tks_capseg / TKP_CW;
         auto pass = c.topk_weighted ? k_tks_pass<true> : k_tks_pass<false>;
-        pass<<<dim3(ctx->tks_S, n_active), TKP_THREADS, TKP_SMEM, s>>>(
+        pass<<<dim3(ctx->tks_S, n_active), TKP_THREADS, tkp_smem_bytes(ctx->w), s>>>(
             ctl, ctx->D, ctx->w, tks_wbp(ctx->w), ctx->tks_lseg, capw, clients, ctx->tks_win,
-            ctx->tks_eqz, ctx->cand_key, ctx->cand_pos, ctx->gt_val, ctx->gt_pos,
-            ctx->tks_seg);
-        CKL();
-        Emit es = em;
-        if (client_update_in_fold) es.hest = nullptr;
-        k_tks_select<<<n_active, TKSEL_THREADS, tksel_smem_bytes(ctx->w), s>>>(
-            ctx->D, ctx->w, tks_wbp(ctx->w), c.k, c.topk_weighted, ctx->tks_S, capw, clients,
-            ctx->tks_win, ctx->tks_seg, ctx->tks_eqz, ctx->cand_key, ctx->cand_pos,
-            ctx->gt_val, ctx->gt_pos, ctx->count, ctx->idx_list, ctx->val_list, ctx->cap, es);
+            ctx->tks_eqz, ctx->cand_key, ctx->cand_pos, ctx->gt_val, ctx->gt_pos, ctx->tks_seg,
+            ctx->tks_ticket, c.k, ctx->count, ctx->idx_list, ctx->val_list, ctx->cap, es);
       } else if (ctx->w <= TKST_MAXW)
         k_topk_stream<<<n_active, TK_THREADS, tkst_smem_bytes(ctx->w), s>>>(
             ctl, ctx->D, ctx->w, ctx->wb, c.k, c.topk_weighted, clients, ctx->flags, ctx->bitmap,
@@ -659,7 +656,7 @@ int enqueue_fednl_round(Ctx* ctx) {
   TRY(record(ctx, EV_FOLD_END, ctx->st2));
   CK(cudaEventRecord(ctx->ev_join, ctx->st2));
   TRY(record(ctx, EV_SOLVE_END, s));
-  int launches = ctx->topk_split ? 10 : 8;
+  int launches = ctx->topk_split ? 9 : 8;
   if (ls) {
     k_dot<<<1, 256, 0, s>>>(ctx->ctl, ctx->d, ctx->gbar, ctx->pvec, ctx->sc);
     CKL();
@@ -758,7 +755,7 @@ int enqueue_pp_round(Ctx* ctx) {
                              ctx->row_counts, ctx->row_ls);
   CKL();
   TRY(record(ctx, EV_END, s));
-  ctx->launches_per_round = ctx->topk_split ? 18 : 16;
+  ctx->launches_per_round = ctx->topk_split ? 17 : 16;
   return FB_OK;
 }
 
@@ -986,11 +983,9 @@ int fb_create(const fb_config* cfg_in, void** out) {
   CKC(cudaFuncSetAttribute(k_topk_stream, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            static_cast<int>(tkst_smem_bytes(TKST_MAXW))));
   CKC(cudaFuncSetAttribute(k_tks_pass<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           static_cast<int>(TKP_SMEM)));
+                           static_cast<int>(tkp_smem_bytes(TKST_MAXW))));
   CKC(cudaFuncSetAttribute(k_tks_pass<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           static_cast<int>(TKP_SMEM)));
-  CKC(cudaFuncSetAttribute(k_tks_select, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           static_cast<int>(tksel_smem_bytes(TKST_MAXW))));
+                           static_cast<int>(tkp_smem_bytes(TKST_MAXW))));
   static size_t max_fold = 0;
   max_fold = std::max(max_fold, sizeof(int32_t) * (3 * static_cast<size_t>(c.n_clients) + 1));
   CKC(cudaFuncSetAttribute(k_master_fold, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1063,6 +1058,7 @@ int fb_create(const fb_config* cfg_in, void** out) {
       dalloc(ctx, &ctx->seeds, n) || dalloc(ctx, &ctx->pair_order, ctx->n_pairs) ||
       dalloc(ctx, &ctx->cand_key, cand_slots) || dalloc(ctx, &ctx->cand_pos, cand_slots) ||
       dalloc(ctx, &ctx->tks_win, ctx->topk_split ? n : 1) ||
+      dalloc(ctx, &ctx->tks_ticket, n) ||
       dalloc(ctx, &ctx->gt_val, ctx->topk_split ? cand_slots : 1) ||
       dalloc(ctx, &ctx->gt_pos, ctx->topk_split ? cand_slots : 1) ||
       dalloc(ctx, &ctx->tks_seg, ctx->topk_split ? static_cast<size_t>(n) * ctx->tks_S * TKP_CW : 1) ||

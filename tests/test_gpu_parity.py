@@ -118,7 +118,7 @@ def test_compressors_bit_exact_on_golden_inputs():
     assert n_checked > 300
 
 
-def test_topk_round0_full_c0_shape_ties():
+def test_topk_round0_full_c0_shape_ties(topk_path):
     g = golden("topk_c0_round0.npz")
     shards = D.baseline_shards("c0")
     d = shards[0].dim
