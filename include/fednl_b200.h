@@ -39,6 +39,7 @@ extern "C" {
 #define FB_ERR_LINE_SEARCH 6   /* algorithms.py:41-49 LineSearchError        */
 #define FB_ERR_UNSUPPORTED 7   /* outside this build's envelope              */
 #define FB_ERR_LS_PENDING 8    /* internal: line search needs more trials    */
+#define FB_ERR_EIGEN 9         /* linalg.py:36 EigenConvergenceError         */
 
 /* compressor kinds (compressors.py:41-47) */
 #define FB_KIND_IDENTITY 0
@@ -52,6 +53,11 @@ extern "C" {
 #define FB_ALG_FEDNL 0
 #define FB_ALG_LS 1
 #define FB_ALG_PP 2
+
+/* Newton system (algorithms.py:361-367): option b = H^k + l^k I, option a =
+ * eigen_clamp_min(H^k, mu) */
+#define FB_OPTION_B 0
+#define FB_OPTION_A 1
 
 /* hessian_init (algorithms.py:37) */
 #define FB_INIT_LAMBDA_IDENTITY 0
@@ -72,13 +78,14 @@ typedef struct fb_config {
   int32_t topk_weighted;  /* CompressorSpec.topk_weighted               */
   int32_t tau;            /* FedNL-PP participants per round            */
   int32_t hessian_init;   /* FB_INIT_*                                  */
-  int32_t reserved0;
+  int32_t option;         /* FB_OPTION_*                                */
   double alpha;
   double lam;
   double ls_c;
   double ls_gamma;
   uint64_t run_seed;
   double ls_steps_table[61];
+  double mu;              /* option a eigenvalue floor (effective_mu)   */
 } fb_config;
 
 /* Detail of the last failure raised by a round (mirrors the reference's
@@ -202,6 +209,13 @@ int fb_oracle_eval(void* ctx, const double* x, double* f, double* grad, double* 
  * linalg.py:151-186); FB_ERR_NOT_PD with status.pivot_* on failure. */
 int fb_shifted_solve(void* ctx, const double* h_packed, double shift, const double* rhs,
                      double* z);
+/* eigen_clamp_min (linalg.py:248-259) of a packed symmetric matrix:
+ * out_packed = (V max(L, floor)) V^T; eigvals (d, nullable) and eigvecs
+ * (d x d column-major, column k = eigenvector k, nullable) as jacobi_eigh
+ * (linalg.py:189-245) returns them; FB_ERR_EIGEN when 30 sweeps do not
+ * converge.  Parallel-order Jacobi on the device. */
+int fb_eigen_clamp(void* ctx, const double* a_packed, double floor, double* out_packed,
+                   double* eigvals, double* eigvecs);
 
 /* diagnostic: per-phase clock64 cycles of one shifted solve on the rank-0
  * CTA.  cluster > 0: the cluster-redundant solver with that cluster size,

@@ -165,6 +165,12 @@ def to_dense(pk: np.ndarray, d: int) -> np.ndarray:
     return out
 
 
+def pack_upper(m: np.ndarray) -> np.ndarray:
+    """Packed upper triangle, column-wise (linalg.py:91-95)."""
+    rows, cols, _ = tri(m.shape[0])
+    return np.ascontiguousarray(m[rows, cols])
+
+
 def diag_positions(d: int) -> np.ndarray:
     j = np.arange(d)
     return j * (j + 1) // 2 + j
@@ -462,6 +468,71 @@ def shifted_solve(h_pk: np.ndarray, d: int, shift: float, rhs: np.ndarray) -> np
     return cholesky_solve(sysm, rhs)
 
 
+class EigenNotConverged(Exception):  # linalg.py:36-37
+    pass
+
+
+def jacobi_eigh(a: np.ndarray, max_sweeps: int = 30, tol_factor: float = 1e-12):
+    """Cyclic Jacobi (linalg.py:189-245): rotations (p, q), p < q in row
+    order, theta / t / c / s as the reference, |a_pq| <= 1e-300 skipped, a_pq
+    set to zero; stop when sqrt(2 sum_{i<j} a_ij^2) <= tol * ||A||_F."""
+    d = a.shape[0]
+    work = np.array(a, dtype=np.float64, order="F", copy=True)
+    vecs = np.eye(d, order="F")
+    iu = np.triu_indices(d)
+    wts = np.where(iu[0] == iu[1], 1.0, 2.0)
+    norm = math.sqrt(float(np.sum(wts * work[iu] ** 2)))
+    thresh = tol_factor * norm
+    if d == 1 or norm == 0.0:
+        return np.diag(work).copy(), vecs
+    iu1 = np.triu_indices(d, 1)
+
+    def off() -> float:
+        o = work[iu1]
+        return math.sqrt(2.0 * float(np.dot(o, o)))
+
+    for _ in range(max_sweeps):
+        if off() <= thresh:
+            return np.diag(work).copy(), vecs
+        for p in range(d - 1):
+            for q in range(p + 1, d):
+                apq = work[p, q]
+                if abs(apq) <= 1e-300:
+                    continue
+                theta = (work[q, q] - work[p, p]) / (2.0 * apq)
+                t = math.copysign(1.0, theta) / (abs(theta) + math.sqrt(theta * theta + 1.0))
+                c = 1.0 / math.sqrt(t * t + 1.0)
+                s = t * c
+                rp, rq = work[p, :].copy(), work[q, :].copy()
+                work[p, :] = c * rp - s * rq
+                work[q, :] = s * rp + c * rq
+                cp, cq = work[:, p].copy(), work[:, q].copy()
+                work[:, p] = c * cp - s * cq
+                work[:, q] = s * cp + c * cq
+                work[p, q] = work[q, p] = 0.0
+                vp, vq = vecs[:, p].copy(), vecs[:, q].copy()
+                vecs[:, p] = c * vp - s * vq
+                vecs[:, q] = s * vp + c * vq
+    if off() <= thresh:
+        return np.diag(work).copy(), vecs
+    raise EigenNotConverged(f"Jacobi did not converge in {max_sweeps} sweeps (dim {d})")
+
+
+def eigen_clamp_min(a: np.ndarray, floor: float) -> np.ndarray:  # linalg.py:248-259
+    vals, vecs = jacobi_eigh(a)
+    out = np.asfortranarray((vecs * np.maximum(vals, floor)) @ vecs.T)
+    iu = np.triu_indices(a.shape[0], 1)
+    out[iu[1], iu[0]] = out[iu]
+    return out
+
+
+def newton_direction(h_pk: np.ndarray, d: int, shift: float, rhs: np.ndarray, option: str,
+                     mu: float) -> np.ndarray:  # algorithms.py:361-367
+    if option == "a":
+        return cholesky_solve(eigen_clamp_min(to_dense(h_pk, d), mu), rhs)
+    return shifted_solve(h_pk, d, shift, rhs)
+
+
 # --------------------------------------------------------------------------
 # configuration helpers (algorithms.py:60-139)
 
@@ -495,6 +566,12 @@ class OracleConfig:
     hessian_init: str = "lambda-identity"
     reconstruct_indices: bool = True
     stop_grad_norm: float | None = None
+    option: str = "b"
+    mu: float | None = None
+
+    @property
+    def effective_mu(self) -> float:  # algorithms.py:107-109
+        return self.lam if self.mu is None else self.mu
 
     @classmethod
     def from_run_config(cls, cfg) -> "OracleConfig":
@@ -505,7 +582,7 @@ class OracleConfig:
             alpha=cfg.alpha, lam=cfg.lam, ls_c=cfg.ls_c, ls_gamma=cfg.ls_gamma,
             tau=cfg.tau, run_seed=cfg.run_seed, hessian_init=cfg.hessian_init,
             reconstruct_indices=cfg.reconstruct_indices,
-            stop_grad_norm=cfg.stop_grad_norm,
+            stop_grad_norm=cfg.stop_grad_norm, option=cfg.option, mu=cfg.mu,
         )
 
 
@@ -704,7 +781,7 @@ class OracleRun:
             for c in range(n):
                 f_now += res[c][3]
             f_now /= n
-            p = shifted_solve(self.h_mas, d, shift, grad)
+            p = newton_direction(self.h_mas, d, shift, grad, cfg.option, cfg.effective_mu)
             dec = float(np.dot(grad, p))
             best = np.inf
             x_new = None
@@ -725,7 +802,7 @@ class OracleRun:
             f_value = f_now
         else:
             f_value = self.mean_f(x_k)
-            p = shifted_solve(self.h_mas, d, shift, grad)
+            p = newton_direction(self.h_mas, d, shift, grad, cfg.option, cfg.effective_mu)
             self.fold(deltas)
             self.x = self.x - p
         self.round += 1

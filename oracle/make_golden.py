@@ -238,6 +238,31 @@ def gen_linalg():
     return out
 
 
+def gen_eigen():
+    """jacobi_eigh / eigen_clamp_min (linalg.py:189-259) of random symmetric,
+    indefinite, diagonal and repeated-eigenvalue matrices."""
+    out = {}
+    g = np.random.default_rng(57)
+    mats = {}
+    for d in (1, 2, 5, 20, 60):
+        a = g.standard_normal((d, d))
+        mats[f"sym{d}"] = (a + a.T) / 2.0
+    mats["diag3"] = np.diag([3.0, -1.0, 2.0])
+    q, _ = np.linalg.qr(g.standard_normal((9, 9)))
+    mats["rep9"] = (q * np.array([-2.0, -2.0, -2.0, 0.1, 0.1, 1.0, 1.0, 1.0, 5.0])) @ q.T
+    a = g.standard_normal((30, 30))
+    mats["spd30"] = a @ a.T / 30.0 + np.eye(30)
+    for name, m in mats.items():
+        m = np.asfortranarray(m)
+        vals, vecs = linalg.jacobi_eigh(m.copy(order="F"))
+        out[f"{name}__pk"] = linalg.pack_upper(m)
+        out[f"{name}__vals_sorted"] = np.sort(vals)
+        for floor in (0.5, 1e-12):
+            out[f"{name}__clamp{floor:g}"] = linalg.pack_upper(linalg.eigen_clamp_min(m, floor))
+    out["names"] = np.array(sorted(mats))
+    return out
+
+
 SIM_CASES = {
     # name: (generator args, RunConfig kwargs)
     "fednl_identity": (("synth", 6, 80, 4, 2), dict(rounds=12)),
@@ -262,6 +287,12 @@ SIM_CASES = {
                                                 compressor=("topk", 9))),
     "pp_identity_stop": (("synth", 4, 60, 4, 8), dict(rounds=60, algorithm="fednl-pp", tau=2,
                                                        stop_grad_norm=1e-10)),
+    # option a (eigen_clamp_min of the estimate, algorithms.py:361-364)
+    "fednl_opt_a": (("synth", 8, 120, 5, 14), dict(rounds=10, option="a", compressor=("topk", 9))),
+    "fednl_opt_a_mu": (("synth", 8, 120, 5, 15), dict(rounds=10, option="a", mu=0.05,
+                                                       compressor=("randseqk", 9))),
+    "ls_opt_a": (("synth", 8, 120, 4, 16), dict(rounds=10, algorithm="fednl-ls", option="a",
+                                                 mu=0.02, compressor=("toplek", 12))),
     # BASELINE shapes at reduced round counts
     "c0_r4": (("baseline", "c0"), dict(rounds=4)),
     "c1_r30": (("baseline", "c1"), dict(rounds=30)),
@@ -293,17 +324,19 @@ def build_case(name):
     return cfg, shards
 
 
-def gen_sim():
+def gen_sim(names=None):
     import threadpoolctl
 
     out = {}
-    for name in SIM_CASES:
+    for name in names or [n for n in SIM_CASES if "opt_a" not in n]:
         cfg, shards = build_case(name)
         with threadpoolctl.threadpool_limits(1, "blas"):
             rows = simulate(cfg, shards)
         for k, v in rows_arrays(rows).items():
             out[f"{name}__{k}"] = v
         print(f"  sim {name}: {len(rows)} rows, final |g|={rows[-1].grad_norm:.3e}")
+    if names is not None:
+        return out
     # The reference's own envelope on the tie-heavy TopK shape: the same run
     # with 8 BLAS threads takes a different (equally valid) k-th-boundary
     # branch at round 3.  Both trajectories are recorded.
@@ -351,7 +384,11 @@ def gen_topk_c0():
     return out
 
 
-def main():
+def gen_sim_opt_a():
+    return gen_sim([n for n in SIM_CASES if "opt_a" in n])
+
+
+def main(only=None):
     os.makedirs(OUT, exist_ok=True)
     for fname, fn in (
         ("rng.npz", gen_rng),
@@ -361,7 +398,11 @@ def main():
         ("data.npz", gen_data),
         ("topk_c0_round0.npz", gen_topk_c0),
         ("simulate.npz", gen_sim),
+        ("eigen.npz", gen_eigen),
+        ("simulate_opt_a.npz", gen_sim_opt_a),
     ):
+        if only and fname not in only:
+            continue
         print(f"generating {fname}")
         np.savez_compressed(os.path.join(OUT, fname), **fn())
     for f in sorted(os.listdir(OUT)):
@@ -369,4 +410,4 @@ def main():
 
 
 if __name__ == "__main__":
-    main()
+    main(sys.argv[1:] or None)

@@ -12,6 +12,7 @@ from .config import (
     CompressorKind,
     CompressorSpec,
     DivergenceError,
+    EigenConvergenceError,
     LineSearchError,
     NotPositiveDefiniteError,
     RunConfig,
@@ -39,6 +40,7 @@ __all__ = [
     "CompressorKind",
     "CompressorSpec",
     "DivergenceError",
+    "EigenConvergenceError",
     "LineSearchError",
     "MetricsRow",
     "NotPositiveDefiniteError",

@@ -24,6 +24,7 @@ FB_ERR_NONFINITE = 4
 FB_ERR_DIVERGED = 5
 FB_ERR_LINE_SEARCH = 6
 FB_ERR_UNSUPPORTED = 7
+FB_ERR_EIGEN = 9
 
 ALG_CODE = {"fednl": 0, "fednl-ls": 1, "fednl-pp": 2}
 INIT_CODE = {"lambda-identity": 0, "zero": 1, "exact": 2}
@@ -40,13 +41,14 @@ class FbConfig(C.Structure):
         ("topk_weighted", C.c_int32),
         ("tau", C.c_int32),
         ("hessian_init", C.c_int32),
-        ("reserved0", C.c_int32),
+        ("option", C.c_int32),
         ("alpha", C.c_double),
         ("lam", C.c_double),
         ("ls_c", C.c_double),
         ("ls_gamma", C.c_double),
         ("run_seed", C.c_uint64),
         ("ls_steps_table", C.c_double * 61),
+        ("mu", C.c_double),
     ]
 
 
@@ -112,6 +114,7 @@ PROTOTYPES = {
     "fb_compress": (C.c_int, [_P, _D, _U64, _U32, _D, _I32, _I32]),
     "fb_oracle_eval": (C.c_int, [_P, _D, _D, _D, _D]),
     "fb_shifted_solve": (C.c_int, [_P, _D, C.c_double, _D, _D]),
+    "fb_eigen_clamp": (C.c_int, [_P, _D, C.c_double, _D, _D, _D]),
     "fb_solve_phase_cycles": (C.c_int, [_P, _D, C.c_double, _D, C.c_int32, C.POINTER(C.c_longlong),
                                         C.POINTER(C.c_float)]),
     "fb_debug_counters": (C.c_int, [C.c_int32, C.POINTER(C.c_longlong)]),

@@ -113,6 +113,10 @@ class DivergenceError(Exception):
         super().__init__(f"non-finite iterate after round {rnd}; run diverged")
 
 
+class EigenConvergenceError(Exception):
+    """Jacobi sweeps exhausted before the off-diagonal mass vanished (linalg.py:36-37)."""
+
+
 class NotPositiveDefiniteError(Exception):
     """First Cholesky pivot that is <= 0 or not finite (linalg.py:24-33)."""
 

@@ -26,6 +26,7 @@
 #include "../../include/fednl_b200.h"
 #include "common.cuh"
 #include "compress_kernels.cuh"
+#include "eig_kernels.cuh"
 #include "fp64_peak.cuh"
 #include "hessian_dmma.cuh"
 #include "oracle_kernels.cuh"
@@ -94,6 +95,7 @@ struct Ctx {
   int32_t* flags = nullptr;
   double *hest = nullptr, *D = nullptr, *hmas = nullptr, *hmas2 = nullptr, *M = nullptr,
          *zeros_w = nullptr;
+  double *eigA = nullptr, *eigV = nullptr, *hclamp = nullptr;  // option a
   int32_t* rs = nullptr;  // per-client range starts of the compressed lists
   int nr = 0;
   uint32_t* bitmap = nullptr;
@@ -593,7 +595,8 @@ int enqueue_fednl_round(Ctx* ctx) {
   // the round reduction: folded into the panel solve's prologue when that
   // kernel runs (its cluster forms the scalars it needs first), else k_reduce
   static const bool no_fuse = getenv("FB_NO_FUSED_REDUCE") && atoi(getenv("FB_NO_FUSED_REDUCE"));
-  const bool fuse_red = ctx->solve_panels && !no_fuse;
+  const bool opt_a = ctx->cfg.option == FB_OPTION_A;
+  const bool fuse_red = ctx->solve_panels && !no_fuse && !opt_a;
   CpRed red{};
   if (fuse_red) {
     red.n_active = n;
@@ -629,9 +632,15 @@ int enqueue_fednl_round(Ctx* ctx) {
                              getenv("NV_TPS_LAUNCH_TOKEN") != nullptr;
   CK(cudaEventRecord(ctx->ev_fork, s));
   CK(cudaStreamWaitEvent(ctx->st2, ctx->ev_fork, 0));
-  TRY(launch_solve(ctx, s, ctx->hmas, &ctx->sc->shift_mean, ctx->gbar, ctx->x, ctx->pvec,
+  if (opt_a) {  // eigen_clamp_min(H^k, mu) of the pre-fold estimate, then its Cholesky solve
+    k_eig_clamp<<<1, EIG_THREADS, eig_smem_bytes(ctx->d), s>>>(
+        ctx->ctl, ctx->d, ctx->hmas, nullptr, ctx->cfg.mu, ctx->eigA, ctx->eigV, ctx->hclamp, nullptr, 0);
+    CKL();
+  }
+  TRY(launch_solve(ctx, s, opt_a ? ctx->hclamp : ctx->hmas,
+                   opt_a ? ctx->zeros_w : &ctx->sc->shift_mean, ctx->gbar, ctx->x, ctx->pvec,
                    ctx->x_new, ls ? 2 : 0, 0, nullptr, serial ? nullptr : ctx->ev_solve_launched,
-                   false, !serial, fuse_red ? &red : nullptr));
+                   false, !serial && !opt_a, fuse_red ? &red : nullptr));
   if (serial) {
     CK(cudaEventRecord(ctx->ev_solve_launched, s));
   }
@@ -818,6 +827,7 @@ int status_to_code(int32_t code) {
     case ST_DIVERGED: return FB_ERR_DIVERGED;
     case ST_LINE_SEARCH: return FB_ERR_LINE_SEARCH;
     case ST_LS_PENDING: return FB_ERR_LS_PENDING;
+    case ST_EIGEN: return FB_ERR_EIGEN;
     default: return FB_ERR_CUDA;
   }
 }
@@ -1047,6 +1057,8 @@ int fb_create(const fb_config* cfg_in, void** out) {
       dalloc(ctx, &ctx->frob_part, static_cast<size_t>(n) * ctx->n_pairs) ||
       dalloc(ctx, &ctx->flags, n) || dalloc(ctx, &ctx->hest, wn) || dalloc(ctx, &ctx->D, wn + 2) ||
       dalloc(ctx, &ctx->hmas, w) || dalloc(ctx, &ctx->hmas2, w) || dalloc(ctx, &ctx->zeros_w, w) ||
+      dalloc(ctx, &ctx->eigA, d > EIG_SMEM_MAX_D ? static_cast<size_t>(d) * d : 1) ||
+      dalloc(ctx, &ctx->eigV, static_cast<size_t>(d) * d) || dalloc(ctx, &ctx->hclamp, w) ||
       dalloc(ctx, &ctx->rs, static_cast<size_t>(n) * (ctx->nr + 1)) ||
       dalloc(ctx, &ctx->M, static_cast<size_t>(d + 1) * (d + 1)) ||
       dalloc(ctx, &ctx->Lg, ctx->solve_panels ? static_cast<size_t>((d + CP_NB - 1) / CP_NB) *
@@ -1806,6 +1818,36 @@ int fb_solve_phase_cycles(void* handle, const double* h_packed, double shift, co
   cudaEventDestroy(e0);
   cudaEventDestroy(e1);
   ctx->solve_cs = saved;
+  return FB_OK;
+}
+
+int fb_eigen_clamp(void* handle, const double* a_packed, double floor, double* out_packed,
+                   double* eigvals, double* eigvecs) {
+  Ctx* ctx = static_cast<Ctx*>(handle);
+  if (!ctx || !a_packed || !out_packed) return invalid(ctx, "null argument");
+  cudaStream_t s = ctx->st;
+  const int d = ctx->d;
+  DevCtl h;
+  TRY(read_status(ctx, &h));
+  if (h.halt) TRY(clear_status(ctx));
+  CK(cudaMemcpyAsync(ctx->D, a_packed, sizeof(double) * ctx->w, cudaMemcpyHostToDevice, s));
+  k_eig_clamp<<<1, EIG_THREADS, eig_smem_bytes(d), s>>>(ctx->ctl, d, ctx->D, nullptr, floor, ctx->eigA,
+                                                       ctx->eigV, ctx->hclamp, ctx->zbuf, 1);
+  CK(cudaGetLastError());
+  CK(cudaStreamSynchronize(s));
+  TRY(read_status(ctx, &h));
+  if (h.code == ST_EIGEN) {
+    ctx->err = "Jacobi did not converge in 30 sweeps";
+    h.halt = 0;
+    h.code = 0;
+    CK(cudaMemcpy(ctx->ctl, &h, sizeof h, cudaMemcpyHostToDevice));
+    return FB_ERR_EIGEN;
+  }
+  COPY_OUT(out_packed, ctx->hclamp, sizeof(double) * ctx->w);
+  if (eigvals) COPY_OUT(eigvals, ctx->zbuf, sizeof(double) * d);
+  if (eigvecs) {  // V^T rows are the eigenvectors: column-major V is V^T row-major
+    COPY_OUT(eigvecs, ctx->eigV, sizeof(double) * d * d);
+  }
   return FB_OK;
 }
 

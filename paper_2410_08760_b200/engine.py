@@ -17,6 +17,7 @@ from .config import (
     KIND_CODE,
     CompressorKind,
     DivergenceError,
+    EigenConvergenceError,
     LineSearchError,
     NotPositiveDefiniteError,
     RunConfig,
@@ -48,6 +49,8 @@ def _fb_config(cfg: RunConfig, d: int, n: int, ni: int) -> _lib.FbConfig:
     c.topk_weighted = int(bool(cfg.compressor.topk_weighted))
     c.tau = cfg.tau or 0
     c.hessian_init = _lib.INIT_CODE[cfg.hessian_init]
+    c.option = 1 if cfg.option == "a" else 0  # FB_OPTION_A / FB_OPTION_B
+    c.mu = float(cfg.effective_mu)
     c.alpha = float(resolve_alpha(cfg, w))
     c.lam = float(cfg.lam)
     c.ls_c = float(cfg.ls_c)
@@ -62,10 +65,6 @@ class FedNLEngine:
     """Device-resident FedNL run.  Not re-entrant; one host thread."""
 
     def __init__(self, cfg: RunConfig, d: int, n_clients: int, n_samples: int, lam: float | None = None):
-        if cfg.option != "b":
-            raise NotImplementedError(
-                "option 'a' (eigenvalue clamp) is outside this build's envelope (SURVEY §8(f))"
-            )
         self.lib = _lib.load()
         self.cfg = cfg
         self.d, self.n, self.ni = d, n_clients, n_samples
@@ -115,6 +114,8 @@ class FedNLEngine:
             raise DivergenceError(st.round)
         if rc == _lib.FB_ERR_LINE_SEARCH:
             raise LineSearchError(st.round, st.f_start, st.f_best)
+        if rc == _lib.FB_ERR_EIGEN:
+            raise EigenConvergenceError(msg or "Jacobi did not converge")
         if rc == _lib.FB_ERR_INVALID:
             raise ValueError(msg or what)
         raise RuntimeError(f"{what} failed (code {rc}): {msg}")
@@ -278,6 +279,18 @@ class FedNLEngine:
         self._check(self.lib.fb_oracle_eval(self.h, _lib.ptr(xa), _lib.ptr(f), _lib.ptr(g), _lib.ptr(h)),
                     "fb_oracle_eval")
         return f, g, h
+
+    def eigen_clamp(self, a_packed: np.ndarray, floor: float, vectors: bool = False):
+        """eigen_clamp_min (linalg.py:248-259) of a packed symmetric matrix:
+        (clamped packed, eigenvalues, eigenvectors as columns | None)."""
+        ap = np.ascontiguousarray(a_packed, dtype=np.float64).reshape(self.w)
+        out = np.zeros(self.w)
+        vals = np.zeros(self.d)
+        vt = np.zeros((self.d, self.d)) if vectors else None
+        self._check(self.lib.fb_eigen_clamp(self.h, _lib.ptr(ap), float(floor), _lib.ptr(out),
+                                            _lib.ptr(vals), _lib.ptr(vt) if vectors else None),
+                    "fb_eigen_clamp")
+        return out, vals, (vt.T.copy() if vectors else None)
 
     def shifted_solve(self, h_packed: np.ndarray, shift: float, rhs: np.ndarray) -> np.ndarray:
         hp = np.ascontiguousarray(h_packed, dtype=np.float64)

@@ -139,3 +139,33 @@ def round_seeds(run_seed: int, n: int, rnd: int) -> np.ndarray:
     _lib.check(_lib.load().fb_round_seeds(run_seed & ((1 << 64) - 1), n, rnd, _lib.ptr(out, C.c_uint64)),
                None, "fb_round_seeds")
     return out
+
+
+def _unpack_symmetric(pk: np.ndarray, d: int) -> np.ndarray:
+    iu = np.triu_indices(d)
+    order = np.lexsort((iu[0], iu[1]))
+    out = np.zeros((d, d), order="F")
+    out[iu[0][order], iu[1][order]] = pk
+    out[iu[1][order], iu[0][order]] = pk
+    return out
+
+
+def jacobi_eigh(a: np.ndarray) -> tuple[np.ndarray, np.ndarray]:
+    """linalg.py:189-245 on the device (parallel-order Jacobi, same rotation,
+    threshold 1e-12 ||A||_F and 30-sweep cap): (eigenvalues, eigenvectors as
+    columns), unsorted; EigenConvergenceError when the sweeps run out."""
+    a = np.asarray(a, dtype=np.float64)
+    d = a.shape[0]
+    if a.shape != (d, d):
+        raise ValueError("matrix must be square")
+    _, vals, vecs = _solve_engine(d).eigen_clamp(_upper_packed(a), -np.inf, vectors=True)
+    return vals, vecs
+
+
+def eigen_clamp_min(a: np.ndarray, floor: float) -> np.ndarray:
+    """linalg.py:248-259 on the device: the symmetric matrix with every
+    eigenvalue below `floor` lifted to it (upper triangle mirrored)."""
+    a = np.asarray(a, dtype=np.float64)
+    d = a.shape[0]
+    out, _, _ = _solve_engine(d).eigen_clamp(_upper_packed(a), float(floor))
+    return _unpack_symmetric(out, d)

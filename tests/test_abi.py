@@ -45,7 +45,7 @@ def test_struct_layouts():
     from paper_2410_08760_b200 import _lib
 
     # fb_config: 10 int32 + 4 double + u64 + 61 double
-    assert ctypes.sizeof(_lib.FbConfig) == 10 * 4 + 4 * 8 + 8 + 61 * 8
+    assert ctypes.sizeof(_lib.FbConfig) == 10 * 4 + 4 * 8 + 8 + 61 * 8 + 8
     assert ctypes.sizeof(_lib.FbStatus) == 4 * 4 + 3 * 8
     assert ctypes.sizeof(_lib.FbProfile) == 2 * 4 + 7 * 8
 

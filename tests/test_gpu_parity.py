@@ -698,3 +698,67 @@ def test_round_rejects_nonfinite_client_hessian(d):
             eng.run_rounds(1)
     finally:
         eng.close()
+
+
+# ------------------------------------------------- option a (eigen clamp)
+
+
+def test_device_jacobi_and_eigen_clamp_against_golden():
+    """linalg.jacobi_eigh / eigen_clamp_min (linalg.py:189-259) on the device
+    against the reference's outputs: eigenvalues, reconstruction and
+    orthonormality as the reference's own tests check them (test_linalg.py:
+    191-226), clamped matrices within 1e-10 normwise, exactly symmetric."""
+    g = golden("eigen.npz")
+    for name in g["names"].tolist():
+        pk = g[f"{name}__pk"]
+        d = int(round((np.sqrt(8 * pk.size + 1) - 1) / 2))
+        m = O.to_dense(pk, d)
+        scale = max(1.0, float(np.abs(m).max()))
+        vals, vecs = leaf.jacobi_eigh(m)
+        assert np.allclose(np.sort(vals), g[f"{name}__vals_sorted"], rtol=0, atol=1e-10 * scale), name
+        assert np.allclose((vecs * vals) @ vecs.T, m, rtol=0, atol=1e-10 * scale), name
+        assert np.allclose(vecs.T @ vecs, np.eye(d), rtol=0, atol=1e-12), name
+        for floor in (0.5, 1e-12):
+            got = leaf.eigen_clamp_min(m, floor)
+            assert np.array_equal(got, got.T), name
+            assert normwise(O.pack_upper(got), g[f"{name}__clamp{floor:g}"], scale) <= 1e-10, (name, floor)
+    # no rotations on a diagonal matrix: values and vectors bit-exact
+    vals, vecs = leaf.jacobi_eigh(np.diag([3.0, -1.0, 2.0]))
+    assert np.array_equal(np.sort(vals), [-1.0, 2.0, 3.0])
+    assert np.array_equal(vecs, np.eye(3))
+
+
+def test_option_a_uses_clamped_system():
+    """test_algorithms.py:399-406: H = diag(-1, 4), mu = 0.5 -> the solve
+    uses diag(0.5, 4); grad (1, 8) gives x = (-2, -2) from x = 0."""
+    sysm = leaf.eigen_clamp_min(np.diag([-1.0, 4.0]), 0.5)
+    p = leaf.cholesky_solve(sysm, np.array([1.0, 8.0]))
+    assert np.allclose(0.0 - p, [-2.0, -2.0], rtol=0, atol=1e-12)
+
+
+OPT_A = {
+    "fednl_opt_a": ((8, 120, 5, 14), dict(rounds=10, option="a", kind="topk", k=9)),
+    "fednl_opt_a_mu": ((8, 120, 5, 15), dict(rounds=10, option="a", mu=0.05, kind="randseqk", k=9)),
+    "ls_opt_a": ((8, 120, 4, 16), dict(rounds=10, algorithm="fednl-ls", option="a", mu=0.02,
+                                       kind="toplek", k=12)),
+}
+
+
+@pytest.mark.parametrize("name", list(OPT_A))
+def test_simulate_option_a_matches_reference(name):
+    (nf, m, n, seed), kw = OPT_A[name]
+    kw = dict(kw)
+    shards = D.make_shards(nf, m, n, seed)
+    spec = CompressorSpec(CompressorKind(kw.pop("kind")), k=kw.pop("k"))
+    rows = simulate(RunConfig(compressor=spec, run_seed=seed, **kw), shards)
+    _rows_close(rows, golden("simulate_opt_a.npz"), [name])
+
+
+def test_option_a_singular_system_raises():
+    """test_cli.py:135-146: option a with a zero estimate and floor 0 is
+    singular at pivot 0 of the very first solve."""
+    shards = D.make_shards(2, 4, 1, 0, lam=0.0)
+    cfg = RunConfig(option="a", mu=0.0, lam=0.0, hessian_init="zero", rounds=1)
+    with pytest.raises(NotPositiveDefiniteError) as e:
+        simulate(cfg, shards)
+    assert e.value.pivot_index == 0
