@@ -70,6 +70,7 @@ struct Ctx {
   bool gexec_phase = false;    // the flavour the cached round graph was built with
   int num_sms = 148;
   int32_t* pair_order = nullptr;  // Hessian tile pairs, costliest first
+  int32_t* hess_dispatch = nullptr;  // per-CTA (pair << 16 | slot) for full-client passes, or null
   double* Lg = nullptr;       // k_chol_panels: released L panels
   double* pp_shift_part = nullptr;  // FedNL-PP: Frobenius partials [tau][PP_SB]
   // client sharding over `world` GPUs (fb_set_shard): this rank owns clients
@@ -372,12 +373,13 @@ int launch_hessian(Ctx* ctx, cudaStream_t s, const int32_t* clients, int n_activ
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   lc.attrs = attr;
   lc.numAttrs = pdl_ok(ctx) ? 1 : 0;
+  const int32_t* disp = (clients == nullptr && n_active == ctx->n) ? ctx->hess_dispatch : nullptr;
   CK(cudaLaunchKernelEx(&lc, k_hessian<2>, ctx->tmap, static_cast<const DevCtl*>(with_ctl ? ctx->ctl : nullptr),
                         ctx->d, ctx->ni, ctx->ldh, static_cast<const double*>(ctx->hcoef), ctx->cfg.lam, clients,
                         hest, hest_stride, D, hess_out, ctx->frob_part, ctx->flags,
                         0u /* zero_mask: see mbar_arrive_dep */, static_cast<const double*>(ctx->gcoef),
                         fuse_grad_x, fuse_grad_x ? ctx->grad : nullptr,
-                        static_cast<const int32_t*>(ctx->pair_order), ctx->n_pairs, hess_group(ctx)));
+                        static_cast<const int32_t*>(ctx->pair_order), ctx->n_pairs, hess_group(ctx), disp));
   return FB_OK;
 }
 int launch_reduce(Ctx* ctx, cudaStream_t s, const double* x, const int32_t* clients, int n_active,
@@ -1118,6 +1120,35 @@ int fb_create(const fb_config* cfg_in, void** out) {
   }
   CKC(cudaMemcpyAsync(ctx->pair_order, order.data(), sizeof(int32_t) * ctx->n_pairs,
                       cudaMemcpyHostToDevice, ctx->st));
+  // Full-client passes: the first wave's two CTAs per SM start on tiles of
+  // different cost (the group's costliest tiles, then its cheapest), so the
+  // co-resident CTAs do not run in lockstep and one's epilogue overlaps the
+  // other's DMMA main loop; the rest of the order is unchanged.
+  static const int hess_order = getenv("FB_HESS_ORDER") ? atoi(getenv("FB_HESS_ORDER")) : 1;
+  std::vector<int32_t> disp;
+  if (hess_order == 1) {
+    const int P = ctx->n_pairs, n_all = ctx->n, grp = hess_group(ctx);
+    disp.resize(static_cast<size_t>(n_all) * P);
+    for (int L = 0; L < n_all * P; ++L) {  // the kernel's default mapping
+      const int g0 = (L / (grp * P)) * grp, gs = std::min(grp, n_all - g0), rem = L - g0 * P;
+      disp[L] = (order[rem / gs] << 16) | (g0 + rem % gs);
+    }
+    const int G0 = std::min(grp, n_all) * P, S = ctx->num_sms;
+    if (G0 >= 3 * S) {
+      std::vector<int32_t> g(disp.begin(), disp.begin() + G0), h;
+      h.insert(h.end(), g.begin(), g.begin() + S);
+      h.insert(h.end(), g.end() - S, g.end());
+      h.insert(h.end(), g.begin() + S, g.end() - S);
+      std::copy(h.begin(), h.end(), disp.begin());
+    } else {
+      disp.clear();
+    }
+  }
+  if (!disp.empty() && n <= 0xFFFF) {
+    if (dalloc(ctx, &ctx->hess_dispatch, disp.size())) return fail(FB_ERR_CUDA);
+    CKC(cudaMemcpyAsync(ctx->hess_dispatch, disp.data(), sizeof(int32_t) * disp.size(),
+                        cudaMemcpyHostToDevice, ctx->st));
+  }
   CKC(cudaStreamSynchronize(ctx->st));  // zero fills and the tables are in place
   if (make_tmap(ctx) != FB_OK) return fail(FB_ERR_CUDA);
   *out = ctx;

@@ -112,7 +112,8 @@ __global__ void __launch_bounds__(HTHREADS, MINB) k_hessian(
     const double* __restrict__ hest, int64_t hest_stride, double* __restrict__ D,
     double* __restrict__ hess_out, double* __restrict__ frob_part, int32_t* __restrict__ flags,
     uint32_t zero_mask, const double* __restrict__ gcoef, const double* __restrict__ x,
-    double* __restrict__ grad, const int32_t* __restrict__ pair_order, int n_pairs_arg, int grp) {
+    double* __restrict__ grad, const int32_t* __restrict__ pair_order, int n_pairs_arg, int grp,
+    const int32_t* __restrict__ dispatch) {
   // the round reduction may launch now (it waits for this pass)
   asm volatile("griddepcontrol.launch_dependents;");
   if (ctl && ctl->halt) return;
@@ -130,9 +131,14 @@ __global__ void __launch_bounds__(HTHREADS, MINB) k_hessian(
   const int g0 = (L / (grp * n_pairs)) * grp;  // first client of the group
   const int gs = min(grp, n_act - g0);
   const int rem = L - g0 * n_pairs;
-  const int slot = g0 + rem % gs;
+  int slot = g0 + rem % gs;
+  int pair = pair_order[rem / gs];
+  if (dispatch) {  // explicit (pair << 16 | client slot) per CTA
+    const int v = dispatch[L];
+    slot = v & 0xFFFF;
+    pair = v >> 16;
+  }
   const int c = client_of(clients, slot);
-  const int pair = pair_order[rem / gs];
   // pair -> (I, J), I <= J, column-wise like the packed layout
   int J = static_cast<int>((sqrtf(8.0f * pair + 1.0f) - 1.0f) * 0.5f);
   while ((J + 1) * (J + 2) / 2 <= pair) ++J;
