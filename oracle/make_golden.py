@@ -384,6 +384,74 @@ def gen_topk_c0():
     return out
 
 
+INGEST_GOOD = (
+    b"# comment line\n"
+    b"+1 1:0.5 3:2 7:-1.25e-3\n"
+    b"\n"
+    b"-1\t2:1 3:1\r\n"
+    b"  +1 4:3.0000000000000004   9:1e300\n"
+    b"-1 1:-0 2:0.1\n"
+    b"+1\n"
+    b"-1 5:7 6:8 8:9\n"
+    b"+1 1:1 2:2 3:3 4:4\n"
+    b"   # indented comment\n"
+    b"-1 9:0.3333333333333333\n"
+)
+INGEST_BAD = {
+    "bad_label": b"+1 1:1\nabc 2:3\n",
+    "three_labels": b"1 1:1\n2 1:1\n3 1:1\n",
+    "no_colon": b"1 1:1\n0 2 3:1\n",
+    "bad_index": b"1 x:1\n",
+    "index_zero": b"1 0:1\n",
+    "not_increasing": b"1 3:1 3:2\n",
+    "decreasing": b"1   5:1   2:2\n",
+    "bad_value": b"1 1:1 2:abc\n",
+    "empty": b"# only\n\n",
+}
+
+
+def gen_ingest():
+    """LIBSVM parse / write / normalize / augment_and_shard / split_rows
+    (data.py:31-254) on crafted inputs, and the ParseError positions."""
+    from fednl.data import ParseError, parse_libsvm, split_rows, write_libsvm
+
+    out = {}
+    ds = parse_libsvm(INGEST_GOOD)
+    out["good__labels"] = ds.labels
+    out["good__num_features"] = np.array(ds.num_features)
+    out["good__lens"] = np.array([len(r[0]) for r in ds.rows])
+    out["good__idx"] = np.concatenate([r[0] for r in ds.rows])
+    out["good__val"] = np.concatenate([r[1] for r in ds.rows])
+    out["good__written"] = np.frombuffer(write_libsvm(ds), dtype=np.uint8)
+    for name, buf in INGEST_BAD.items():
+        try:
+            parse_libsvm(buf)
+            raise AssertionError(name)
+        except ParseError as e:
+            out[f"bad_{name}"] = np.array([e.line, e.col])
+            out[f"bad_{name}__msg"] = np.array(str(e))
+    for pair in ((0.0, 1.0), (-1.0, 1.0), (2.0, 7.0)):
+        raw = RawDataset(labels=np.array([pair[1], pair[0], pair[1]]), rows=[(np.zeros(0, dtype=np.int64), np.zeros(0))] * 3, num_features=1)
+        normalize_labels(raw)
+        out[f"norm_{pair[0]:g}_{pair[1]:g}"] = raw.labels
+    g = np.random.default_rng(3)
+    rows, labels = [], []
+    for i in range(23):
+        nz = np.sort(g.choice(np.arange(1, 12), size=int(g.integers(0, 5)), replace=False))
+        rows.append((nz.astype(np.int64), g.standard_normal(len(nz))))
+        labels.append(1.0 if g.random() < 0.4 else -1.0)
+    big = RawDataset(labels=np.array(labels), rows=rows, num_features=11)
+    out["shard__labels"] = big.labels
+    out["shard__lens"] = np.array([len(r[0]) for r in rows])
+    out["shard__idx"] = np.concatenate([r[0] for r in rows])
+    out["shard__val"] = np.concatenate([r[1] for r in rows])
+    shards = augment_and_shard(big, 4, 9, 0.01)
+    out["shard__bmats"] = np.stack([s.bmat for s in shards])
+    pieces = split_rows(big, 4, 9)
+    out["shard__split_labels"] = np.stack([p.labels for p in pieces])
+    return out
+
+
 def gen_sim_opt_a():
     return gen_sim([n for n in SIM_CASES if "opt_a" in n])
 
@@ -400,6 +468,7 @@ def main(only=None):
         ("simulate.npz", gen_sim),
         ("eigen.npz", gen_eigen),
         ("simulate_opt_a.npz", gen_sim_opt_a),
+        ("ingest.npz", gen_ingest),
     ):
         if only and fname not in only:
             continue

@@ -160,3 +160,17 @@ def baseline_run_config(name: str, rounds: int | None = None, run_seed: int = 1)
         tau=c.get("tau"),
         run_seed=run_seed,
     )
+
+
+# the reference's data-module names for real datasets (data.py:31-254)
+from .ingest import (  # noqa: E402
+    ParseError,
+    RawDataset,
+    augment_and_shard,
+    load_client_shard,
+    load_libsvm,
+    normalize_labels,
+    parse_libsvm,
+    split_rows,
+    write_libsvm,
+)
