@@ -2215,20 +2215,75 @@ __device__ double np_pairwise_block(const double* a, int n, double* lsum, int* l
   return ret;
 }
 
+// numpy's pairwise sum of a[0, n) with the recursion precomputed on the
+// host (it depends on n only): tab = {nl, nn, off[nl], len[nl], left[nn],
+// right[nn]}, leaves left to right, internal nodes in post-order with child
+// c < nl a leaf and c >= nl node c - nl.  Each leaf is summed by 8 threads
+// (one of numpy's 8 accumulators each, combined in numpy's order), the nodes
+// by thread 0 in post-order.  Identical rounding to np_pairwise.  Whole
+// block; the result is returned to every thread.  Scratch: val[nl + nn].
+constexpr int NPW_TAB_LEAVES = 128;  // table path: w <= ~16k (larger w: np_pairwise_block)
+constexpr int NPW_TAB_MAX = 4 * NPW_TAB_LEAVES + 2;
+__device__ double np_pairwise_tab(const double* a, const int32_t* tab, double* val, double* red8) {
+  const int nl = tab[0], nn = tab[1];
+  const int32_t* off = tab + 2;
+  const int32_t* len = off + nl;
+  const int32_t* lft = len + nl;
+  const int32_t* rgt = lft + nn;
+  // 8 threads per leaf: accumulator j of leaf L
+  for (int u = threadIdx.x; u < 8 * nl; u += blockDim.x) {
+    const int L = u >> 3, j = u & 7;
+    const int n = len[L];
+    const double* x = a + off[L];
+    double r = 0.0;
+    if (n >= 8) {
+      r = x[j];
+      const int m8 = n - (n % 8);
+      for (int i = 8; i < m8; i += 8) r = __dadd_rn(r, x[i + j]);
+    }
+    red8[u] = r;
+  }
+  __syncthreads();
+  for (int L = threadIdx.x; L < nl; L += blockDim.x) {
+    const int n = len[L];
+    const double* x = a + off[L];
+    double res;
+    int i;
+    if (n < 8) {
+      res = 0.0;
+      i = 0;
+    } else {
+      const double* r = red8 + 8 * L;
+      res = __dadd_rn(__dadd_rn(__dadd_rn(r[0], r[1]), __dadd_rn(r[2], r[3])),
+                      __dadd_rn(__dadd_rn(r[4], r[5]), __dadd_rn(r[6], r[7])));
+      i = n - (n % 8);
+    }
+    for (; i < n; ++i) res = __dadd_rn(res, x[i]);
+    val[L] = res;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0)
+    for (int q = 0; q < nn; ++q) val[nl + q] = __dadd_rn(val[lft[q]], val[rgt[q]]);
+  __syncthreads();
+  return val[nl + nn - 1];  // the root (the single leaf when nn == 0)
+}
+
 __global__ void __launch_bounds__(TK_THREADS) k_toplek(
     DevCtl* __restrict__ ctl, const double* __restrict__ D, int64_t w, int wb, int k,
     const int32_t* __restrict__ clients, const int32_t* __restrict__ flags, uint64_t run_seed,
     const uint64_t* __restrict__ seeds, uint32_t* __restrict__ bitmap,
     int32_t* __restrict__ count, uint32_t* __restrict__ idx_list, double* __restrict__ val_list,
-    int cap, int32_t* __restrict__ draws, int P, Emit em) {
+    int cap, int32_t* __restrict__ draws, int P, Emit em, const int32_t* __restrict__ npw_tab) {
   if (ctl && ctl->halt) return;
   PhaseClock pc;
+  __shared__ int32_t s_tab[NPW_TAB_MAX];
+  __shared__ double s_red8[8 * NPW_TAB_LEAVES];
   extern __shared__ uint8_t tl_raw[];
   double* en = reinterpret_cast<double*>(tl_raw);                    // [P]
   uint32_t* pos = reinterpret_cast<uint32_t*>(tl_raw + 8 * static_cast<size_t>(P));  // [P]
   __shared__ int ws[64];
   __shared__ int s_t, s_nleaf;
-  __shared__ double lsum[NPW_MAX_LEAVES];
+  __shared__ double lsum[2 * NPW_MAX_LEAVES];
   __shared__ int loff[NPW_MAX_LEAVES], llen[NPW_MAX_LEAVES];
   const int c = client_of(clients, blockIdx.x);
   const double* v = D + static_cast<int64_t>(c) * w;
@@ -2243,6 +2298,10 @@ __global__ void __launch_bounds__(TK_THREADS) k_toplek(
     if (i < w) { en[i] = energy_of(v[i], i); pos[i] = i; }
     else { en[i] = 0.0; pos[i] = 0xFFFFFFFFu; }
   }
+  if (npw_tab) {
+    const int ntab = 2 + 2 * npw_tab[0] + 2 * npw_tab[1];
+    for (int i = threadIdx.x; i < ntab; i += blockDim.x) s_tab[i] = npw_tab[i];
+  }
   __syncthreads();
   pc.mark(24);
   // bitonic sort: "before" = larger energy, then smaller position
@@ -2254,7 +2313,8 @@ __global__ void __launch_bounds__(TK_THREADS) k_toplek(
     default: tl_bitonic_sort<16>(en, pos, P); break;
   }
   pc.mark(25);
-  const double total = np_pairwise_block(en, static_cast<int>(w), lsum, loff, llen, &s_nleaf);
+  const double total = npw_tab ? np_pairwise_tab(en, s_tab, lsum, s_red8)
+                               : np_pairwise_block(en, static_cast<int>(w), lsum, loff, llen, &s_nleaf);
   if (threadIdx.x == 0) {
     const uint64_t seed = seeds ? seeds[blockIdx.x] : round_seed(run_seed, c, ctl->round);
     Prg p(seed);

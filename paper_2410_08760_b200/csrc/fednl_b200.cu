@@ -21,6 +21,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <string>
+#include <functional>
 #include <vector>
 
 #include "../../include/fednl_b200.h"
@@ -83,6 +84,7 @@ struct Ctx {
   cudaEvent_t* direct_pool = nullptr;  // non-null: record() targets these (FB_NO_GRAPH)
   size_t solve_smem = 0;
   int toplek_P = 0;
+  int32_t* npw_tab = nullptr;  // TopLEK: numpy pairwise-sum recursion for n = w
   bool uploaded = false, initialised = false;
   std::string err;
 
@@ -465,7 +467,7 @@ int launch_compress(Ctx* ctx, cudaStream_t s, const int32_t* clients, int n_acti
       k_toplek<<<n_active, TK_THREADS, static_cast<size_t>(ctx->toplek_P) * 12, s>>>(
           ctl ? ctl : ctx->ctl, ctx->D, ctx->w, ctx->wb, c.k, clients, ctx->flags, c.run_seed,
           seeds, ctx->bitmap, ctx->count, ctx->idx_list, ctx->val_list, ctx->cap, ctx->draws,
-          ctx->toplek_P, em);
+          ctx->toplek_P, em, ctx->npw_tab);
       break;
     case FB_KIND_IDENTITY:
     case FB_KIND_NATURAL: {
@@ -1120,6 +1122,37 @@ int fb_create(const fb_config* cfg_in, void** out) {
   }
   CKC(cudaMemcpyAsync(ctx->pair_order, order.data(), sizeof(int32_t) * ctx->n_pairs,
                       cudaMemcpyHostToDevice, ctx->st));
+  if (c.kind == FB_KIND_TOPLEK) {
+    // numpy's pairwise recursion over n = w (np.sum of the sorted energies):
+    // leaves of <= 128 left to right, internal nodes in post-order
+    std::vector<int32_t> loff, llen, nl_, nr_;
+    std::function<int(int, int)> walk = [&](int o, int n) -> int {  // returns a node code
+      if (n <= 128) {
+        loff.push_back(o);
+        llen.push_back(n);
+        return -static_cast<int>(loff.size());  // leaf k -> -(k + 1)
+      }
+      int n2 = n / 2;
+      n2 -= n2 % 8;
+      const int a = walk(o, n2), b = walk(o + n2, n - n2);
+      nl_.push_back(a);
+      nr_.push_back(b);
+      return static_cast<int>(nl_.size()) - 1;  // internal node index
+    };
+    walk(0, static_cast<int>(w));
+    const int nlf = static_cast<int>(loff.size()), nnd = static_cast<int>(nl_.size());
+    if (nlf <= NPW_TAB_LEAVES) {
+      auto code = [&](int x) { return x < 0 ? -x - 1 : nlf + x; };
+      std::vector<int32_t> tab{nlf, nnd};
+      tab.insert(tab.end(), loff.begin(), loff.end());
+      tab.insert(tab.end(), llen.begin(), llen.end());
+      for (int q = 0; q < nnd; ++q) tab.push_back(code(nl_[q]));
+      for (int q = 0; q < nnd; ++q) tab.push_back(code(nr_[q]));
+      if (dalloc(ctx, &ctx->npw_tab, tab.size())) return fail(FB_ERR_CUDA);
+      CKC(cudaMemcpyAsync(ctx->npw_tab, tab.data(), sizeof(int32_t) * tab.size(),
+                          cudaMemcpyHostToDevice, ctx->st));
+    }
+  }
   // Full-client passes: the first wave's two CTAs per SM start on tiles of
   // different cost (the group's costliest tiles, then its cheapest), so the
   // co-resident CTAs do not run in lockstep and one's epilogue overlaps the
