@@ -464,7 +464,7 @@ int launch_compress(Ctx* ctx, cudaStream_t s, const int32_t* clients, int n_acti
           ctx->count, ctx->idx_list, ctx->val_list, ctx->cap, ctx->draws, em);
       break;
     case FB_KIND_TOPLEK:
-      k_toplek<<<n_active, TK_THREADS, static_cast<size_t>(ctx->toplek_P) * 12, s>>>(
+      k_toplek<<<n_active, TK_THREADS, toplek_smem_bytes(ctx->toplek_P), s>>>(
           ctl ? ctl : ctx->ctl, ctx->D, ctx->w, ctx->wb, c.k, clients, ctx->flags, c.run_seed,
           seeds, ctx->bitmap, ctx->count, ctx->idx_list, ctx->val_list, ctx->cap, ctx->draws,
           ctx->toplek_P, em, ctx->npw_tab);
@@ -986,7 +986,7 @@ int fb_create(const fb_config* cfg_in, void** out) {
   // dynamic shared memory limits are per-function process state: only ever
   // raise them, so contexts of different shapes can coexist
   static size_t max_toplek = 0, max_solve = 0;
-  max_toplek = std::max(max_toplek, static_cast<size_t>(std::max(ctx->toplek_P, 1)) * 12);
+  max_toplek = std::max(max_toplek, toplek_smem_bytes(std::max(ctx->toplek_P, 1)));
   max_solve = std::max(max_solve, std::max<size_t>(ctx->solve_smem, 1));
   CKC(cudaFuncSetAttribute(k_hessian<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            static_cast<int>(HESS_SMEM)));
