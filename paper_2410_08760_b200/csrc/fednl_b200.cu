@@ -1819,7 +1819,7 @@ int fb_oracle_eval(void* handle, const double* x, double* f, double* grad, doubl
   const int n = ctx->n, d = ctx->d;
   DevCtl h;
   TRY(read_status(ctx, &h));
-  if (h.halt) TRY(clear_status(ctx));
+  if (h.halt || h.code) TRY(clear_status(ctx));  // a previous failure's code too
   CK(cudaMemcpyAsync(ctx->x_new, x, sizeof(double) * d, cudaMemcpyHostToDevice, s));
   CK(cudaMemsetAsync(ctx->flags, 0, sizeof(int32_t) * n, s));
   TRY(launch_margins(ctx, s, ctx->x_new, nullptr, n));
@@ -1893,7 +1893,7 @@ int fb_eigen_clamp(void* handle, const double* a_packed, double floor, double* o
   const int d = ctx->d;
   DevCtl h;
   TRY(read_status(ctx, &h));
-  if (h.halt) TRY(clear_status(ctx));
+  if (h.halt || h.code) TRY(clear_status(ctx));  // a previous failure's code too
   CK(cudaMemcpyAsync(ctx->D, a_packed, sizeof(double) * ctx->w, cudaMemcpyHostToDevice, s));
   k_eig_clamp<<<1, EIG_THREADS, eig_smem_bytes(d), s>>>(ctx->ctl, d, ctx->D, nullptr, floor, ctx->eigA,
                                                        ctx->eigV, ctx->hclamp, ctx->zbuf, 1);
@@ -1923,7 +1923,7 @@ int fb_shifted_solve(void* handle, const double* h_packed, double shift, const d
   const int d = ctx->d;
   DevCtl h;
   TRY(read_status(ctx, &h));
-  if (h.halt) TRY(clear_status(ctx));
+  if (h.halt || h.code) TRY(clear_status(ctx));  // a previous failure's code too
   CK(cudaMemcpyAsync(ctx->D, h_packed, sizeof(double) * ctx->w, cudaMemcpyHostToDevice, s));
   CK(cudaMemcpyAsync(ctx->scalar, &shift, sizeof(double), cudaMemcpyHostToDevice, s));
   CK(cudaMemcpyAsync(ctx->zbuf, rhs, sizeof(double) * d, cudaMemcpyHostToDevice, s));

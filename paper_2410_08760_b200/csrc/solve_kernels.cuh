@@ -93,6 +93,7 @@ __global__ void __launch_bounds__(CH_THREADS, 1) k_chol_solve(
   // outputs at the end.  sm.failed is ordered before any DSMEM push by the
   // first cluster barrier below.
   if (tid == 0) sm.failed = 0;
+  for (int k2 = tid; k2 < PLD; k2 += CH_THREADS) pan[(d + NB) / NB * NB * PLD + k2] = 0.0;  // zero row
   const double shift = shift_ptr ? __ldcg(shift_ptr) : 0.0;
 
   // ---- M[j][i] = H[j][i] (+ shift on the diagonal); M[j][d] = rhs[j]
@@ -227,30 +228,67 @@ __global__ void __launch_bounds__(CH_THREADS, 1) k_chol_solve(
       break;
     }
     // ---- (C) trailing update M[j][i] -= sum_s L[i][s] L[j][s], p1 <= j <= i,
-    //          rows i in [p1, d] (row d updates the right-hand side)
+    //          rows i in [p1, d] (row d updates the right-hand side): the
+    //          lower-triangular 8 x 8 tiles (row tile ti >= column tile tj) of
+    //          P P^T on DMMA.8x8x4 (P = the m x NB panel in shared memory),
+    //          TB tiles per warp in flight, the M operands loaded first
     const int nb_next = min(NB, d - p1);
-    for (int r = gwarp; r < m; r += nwarps) {  // row i = p1 + r
-      const int i = p1 + r;
-      const int jmax = (i == d) ? r - 1 : r;  // the rhs row has no diagonal
-      double li[NB];
+    {
+      const int g = lane >> 2, tg = lane & 3;
+      const int mz = (d + NB) / NB * NB;  // a panel row never written: zeros (set up front)
+      const int T = (m + 7) >> 3;
+      const int ntile = T * (T + 1) / 2;
+      constexpr int TB = 4;
+      for (int q0 = gwarp * TB; q0 < ntile; q0 += nwarps * TB) {
+        int ti[TB], tj[TB];
+        double mv[TB][2], acc[TB][2];
 #pragma unroll
-      for (int s = 0; s < NB; ++s) li[s] = pan[r * PLD + s];
-      double* colp = M + i * ld;
-      for (int jr = lane; jr <= jmax; jr += 32) {
-        const int j = p1 + jr;
-        double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
-        const double* pj = pan + jr * PLD;
+        for (int u = 0; u < TB; ++u) {
+          const int q = q0 + u;
+          int a2 = static_cast<int>((sqrtf(8.0f * q + 1.0f) - 1.0f) * 0.5f);
+          while ((a2 + 1) * (a2 + 2) / 2 <= q) ++a2;
+          while (a2 * (a2 + 1) / 2 > q) --a2;
+          ti[u] = q < ntile ? a2 : -1;
+          tj[u] = q - a2 * (a2 + 1) / 2;
+          acc[u][0] = acc[u][1] = 0.0;
 #pragma unroll
-        for (int s = 0; s < NB; s += 4) {
-          a0 = fma(li[s], pj[s], a0);
-          a1 = fma(li[s + 1], pj[s + 1], a1);
-          a2 = fma(li[s + 2], pj[s + 2], a2);
-          a3 = fma(li[s + 3], pj[s + 3], a3);
+          for (int e = 0; e < 2; ++e) {
+            const int r = ti[u] * 8 + g, jr = tj[u] * 8 + 2 * tg + e;
+            const bool ok = ti[u] >= 0 && r < m && jr <= r && p1 + jr < d;
+            mv[u][e] = ok ? __ldcg(M + (p1 + jr) + static_cast<int64_t>(p1 + r) * ld) : 0.0;
+          }
         }
-        const double nv = __dsub_rn(__ldcg(colp + j), (a0 + a1) + (a2 + a3));
-        colp[j] = nv;
-        if (r < nb_next)  // next diagonal block (row r, col jr <= r) into every CTA
-          for (int q = 0; q < cs; ++q) cluster.map_shared_rank(&sm, q)->nxt[par ^ 1][r][jr] = nv;
+        const double* pa[TB];
+        const double* pb2[TB];
+#pragma unroll
+        for (int u = 0; u < TB; ++u) {  // rows past m read the zero row past the panel
+          const int ra = ti[u] * 8 + g, rb = tj[u] * 8 + g;
+          pa[u] = pan + (ti[u] >= 0 && ra < m ? ra : mz) * PLD + tg;
+          pb2[u] = pan + (ti[u] >= 0 && rb < m ? rb : mz) * PLD + tg;
+        }
+#pragma unroll
+        for (int k0 = 0; k0 < NB; k0 += 4) {
+          double av[TB], bv[TB];
+#pragma unroll
+          for (int u = 0; u < TB; ++u) {
+            av[u] = pa[u][k0];
+            bv[u] = pb2[u][k0];
+          }
+#pragma unroll
+          for (int u = 0; u < TB; ++u) dmma_8x8x4_nv(acc[u], av[u], bv[u]);
+        }
+#pragma unroll
+        for (int u = 0; u < TB; ++u) {
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            const int r = ti[u] * 8 + g, jr = tj[u] * 8 + 2 * tg + e;
+            if (!(ti[u] >= 0 && r < m && jr <= r && p1 + jr < d)) continue;
+            const double nv = __dsub_rn(mv[u][e], acc[u][e]);
+            M[(p1 + jr) + static_cast<int64_t>(p1 + r) * ld] = nv;
+            if (r < nb_next)  // next diagonal block (row r, col jr <= r) into every CTA
+              for (int qc = 0; qc < cs; ++qc) cluster.map_shared_rank(&sm, qc)->nxt[par ^ 1][r][jr] = nv;
+          }
+        }
       }
     }
     mark(6);

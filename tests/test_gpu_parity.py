@@ -762,3 +762,15 @@ def test_option_a_singular_system_raises():
     with pytest.raises(NotPositiveDefiniteError) as e:
         simulate(cfg, shards)
     assert e.value.pivot_index == 0
+
+
+def test_leaf_solve_after_not_pd_failure_is_clean():
+    """A NotPositiveDefiniteError from one leaf solve must not leak into the
+    next call on the same (cached) context."""
+    with pytest.raises(NotPositiveDefiniteError) as e:
+        leaf.cholesky_solve(np.array([[1.0, 2.0], [2.0, 1.0]]), np.array([1.0, 1.0]))
+    assert e.value.pivot_index == 1
+    p = leaf.cholesky_solve(np.diag([0.5, 4.0]), np.array([1.0, 8.0]))
+    assert np.allclose(p, [2.0, 2.0], rtol=0, atol=1e-12)
+    out = leaf.eigen_clamp_min(np.diag([-1.0, 4.0]), 0.5)
+    assert np.allclose(out, np.diag([0.5, 4.0]), rtol=0, atol=1e-15)
