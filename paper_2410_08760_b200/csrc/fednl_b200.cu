@@ -336,9 +336,18 @@ int launch_margins(Ctx* ctx, cudaStream_t s, const double* x, const int32_t* cli
   if (n_active >= ctx->num_sms * 3 / 4 && mc_smem_bytes(ctx->d, ctx->ldj) <= MC_SMEM_MAX &&
       !getenv("FB_MARGINS_OLD")) {
     // enough clients to fill the GPU: one CTA streams each client's rows
-    k_margins_cpc<<<n_active, MC_THREADS, mc_smem_bytes(ctx->d, ctx->ldj), s>>>(
-        with_ctl ? ctx->ctl : nullptr, ctx->Bt, ctx->d, ctx->ni, ctx->ldj, ctx->ldh, x, clients,
-        ctx->hcoef, ctx->gcoef, ctx->loss_part, ctx->nblk);
+    // two 512-thread CTAs per client (each half of its samples, two CTAs per
+    // SM) when that halves the row batches a thread streams; else one
+    static const int mc_split = getenv("FB_MARGINS_SPLIT") ? atoi(getenv("FB_MARGINS_SPLIT")) : 2;
+    if (mc_split == 2 && ctx->ldj / 2 > 64) {
+      k_margins_cpc<512, 2><<<2 * n_active, 512, mc_smem_bytes_nt(ctx->d, ctx->ldj, 2, 512), s>>>(
+          with_ctl ? ctx->ctl : nullptr, ctx->Bt, ctx->d, ctx->ni, ctx->ldj, ctx->ldh, x, clients,
+          ctx->hcoef, ctx->gcoef, ctx->loss_part, ctx->nblk);
+    } else {
+      k_margins_cpc<MC_THREADS, 1><<<n_active, MC_THREADS, mc_smem_bytes(ctx->d, ctx->ldj), s>>>(
+          with_ctl ? ctx->ctl : nullptr, ctx->Bt, ctx->d, ctx->ni, ctx->ldj, ctx->ldh, x, clients,
+          ctx->hcoef, ctx->gcoef, ctx->loss_part, ctx->nblk);
+    }
   } else {
     dim3 grid(ctx->nblk, n_active);
     k_margins<<<grid, MB_THREADS, ctx->d * sizeof(double), s>>>(
@@ -992,7 +1001,9 @@ int fb_create(const fb_config* cfg_in, void** out) {
                            static_cast<int>(HESS_SMEM)));
   CKC(cudaFuncSetAttribute(k_topk_smem, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            static_cast<int>(TKS_SMEM)));
-  CKC(cudaFuncSetAttribute(k_margins_cpc, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  CKC(cudaFuncSetAttribute(k_margins_cpc<MC_THREADS, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           static_cast<int>(MC_SMEM_MAX)));
+  CKC(cudaFuncSetAttribute(k_margins_cpc<512, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            static_cast<int>(MC_SMEM_MAX)));
   CKC(cudaFuncSetAttribute(k_topk_stream, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            static_cast<int>(tkst_smem_bytes(TKST_MAXW))));

@@ -119,15 +119,31 @@ __global__ void __launch_bounds__(MB_THREADS) k_margins(
 // grid n_active, block MC_THREADS, dynamic smem (d + G * 2 * SPc) doubles
 // where SPc = min(SP, MC_THREADS) (sample pairs per chunk).
 constexpr int MC_THREADS = 1024;
-__host__ __device__ constexpr int mc_pairs(int ldj) { return ldj / 2 < MC_THREADS ? ldj / 2 : MC_THREADS; }
-__host__ __device__ constexpr int mc_groups(int ldj) {
-  return MC_THREADS / mc_pairs(ldj) > 32 ? 32 : MC_THREADS / mc_pairs(ldj);
+// sample pairs per CTA when a client's samples are split over `nsplit` CTAs
+// (each a multiple of 32 pairs = 64 samples, so the loss blocks stay whole)
+__host__ __device__ constexpr int mc_split_pairs(int ldj, int nsplit) {
+  return nsplit <= 1 ? ldj / 2 : ((ldj / 2 + nsplit - 1) / nsplit + 31) / 32 * 32;
+}
+__host__ __device__ constexpr int mc_pairs_nt(int ldj, int nsplit, int nt) {
+  return mc_split_pairs(ldj, nsplit) < nt ? mc_split_pairs(ldj, nsplit) : nt;
+}
+__host__ __device__ constexpr int mc_groups_nt(int ldj, int nsplit, int nt) {
+  return nt / mc_pairs_nt(ldj, nsplit, nt) > 32 ? 32 : nt / mc_pairs_nt(ldj, nsplit, nt);
+}
+__host__ __device__ constexpr int mc_pairs(int ldj) { return mc_pairs_nt(ldj, 1, MC_THREADS); }
+__host__ __device__ constexpr int mc_groups(int ldj) { return mc_groups_nt(ldj, 1, MC_THREADS); }
+__host__ __device__ constexpr size_t mc_smem_bytes_nt(int d, int ldj, int nsplit, int nt) {
+  return (static_cast<size_t>(d) + static_cast<size_t>(mc_groups_nt(ldj, nsplit, nt)) * 2 *
+                                       mc_pairs_nt(ldj, nsplit, nt)) * sizeof(double);
 }
 __host__ __device__ constexpr size_t mc_smem_bytes(int d, int ldj) {
-  return (static_cast<size_t>(d) + static_cast<size_t>(mc_groups(ldj)) * 2 * mc_pairs(ldj)) * sizeof(double);
+  return mc_smem_bytes_nt(d, ldj, 1, MC_THREADS);
 }
 constexpr size_t MC_SMEM_MAX = 96 * 1024;
-__global__ void __launch_bounds__(MC_THREADS) k_margins_cpc(
+// NT threads per CTA, NS CTAs per client (client slot = blockIdx.x / NS,
+// sample pairs [part * SPS, (part + 1) * SPS) of SPS = mc_split_pairs).
+template <int NT, int NS>
+__global__ void __launch_bounds__(NT, NS > 1 ? 2 : 1) k_margins_cpc(
     const DevCtl* __restrict__ ctl, const double* __restrict__ Bt, int d, int ni, int ldj,
     int ldh, const double* __restrict__ x, const int32_t* __restrict__ clients,
     double* __restrict__ hcoef, double* __restrict__ gcoef, double* __restrict__ loss_part,
@@ -136,22 +152,25 @@ __global__ void __launch_bounds__(MC_THREADS) k_margins_cpc(
   asm volatile("griddepcontrol.launch_dependents;");
   if (ctl && ctl->halt) return;
   extern __shared__ double mcs[];
-  __shared__ double red[MC_THREADS / 32];
-  const int c = client_of(clients, blockIdx.x);
+  __shared__ double red[NT / 32];
+  const int c = client_of(clients, blockIdx.x / NS);
+  const int part = blockIdx.x % NS;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int SPc = mc_pairs(ldj), G = mc_groups(ldj);
+  const int SPS = mc_split_pairs(ldj, NS);
+  const int SPc = mc_pairs_nt(ldj, NS, NT), G = mc_groups_nt(ldj, NS, NT);
   double* xs = mcs;
-  double* part = mcs + d;  // [G][2 * SPc]
-  for (int a = tid; a < d; a += MC_THREADS) xs[a] = x[a];
+  double* part_m = mcs + d;  // [G][2 * SPc]
+  for (int a = tid; a < d; a += NT) xs[a] = x[a];
   __syncthreads();
   const int SP = ldj / 2;
+  const int sp_lo = part * SPS, sp_hi = min(SP, sp_lo + SPS);
   const int g = tid / SPc, sp_l = tid % SPc;
   const double2* base = reinterpret_cast<const double2*>(Bt + static_cast<int64_t>(c) * d * ldj);
   const int64_t rs = ldj / 2;  // row stride in double2
-  for (int sp0 = 0; sp0 < SP; sp0 += SPc) {
+  for (int sp0 = sp_lo; sp0 < sp_hi; sp0 += SPc) {
     // ---- partial margins of this chunk's sample pairs over row group g
     const int sp = sp0 + sp_l;
-    if (g < G && sp < SP) {
+    if (g < G && sp < sp_hi) {
       const double2* col = base + sp;
       double2 acc[2] = {make_double2(0.0, 0.0), make_double2(0.0, 0.0)};
       // 8 rows per batch, the last batch predicated (no one-row tail loop:
@@ -168,18 +187,19 @@ __global__ void __launch_bounds__(MC_THREADS) k_margins_cpc(
           acc[u & 1].y = fma(bv[u].y, xa, acc[u & 1].y);
         }
       }
-      part[g * 2 * SPc + 2 * sp_l] = acc[0].x + acc[1].x;
-      part[g * 2 * SPc + 2 * sp_l + 1] = acc[0].y + acc[1].y;
+      part_m[g * 2 * SPc + 2 * sp_l] = acc[0].x + acc[1].x;
+      part_m[g * 2 * SPc + 2 * sp_l + 1] = acc[0].y + acc[1].y;
     }
     __syncthreads();
     // ---- coefficients and loss partials of the chunk's samples
-    const int js0 = 2 * sp0;
-    for (int t0 = 0; t0 < 2 * SPc; t0 += MC_THREADS) {
+    const int js0 = 2 * sp0;  // a multiple of 64 (chunks and parts are)
+    const int nchunk = 2 * min(SPc, sp_hi - sp0);
+    for (int t0 = 0; t0 < nchunk; t0 += NT) {
       const int sl = t0 + tid, js = js0 + sl;
       double loss = 0.0;
-      if (sl < 2 * SPc && js < ldh) {
+      if (sl < nchunk && js < ldh) {
         double mm = 0.0;
-        for (int g2 = 0; g2 < G; ++g2) mm += part[g2 * 2 * SPc + sl];
+        for (int g2 = 0; g2 < G; ++g2) mm += part_m[g2 * 2 * SPc + sl];
         if (js < ni) {
           const double sig = stable_sigmoid(mm);
           const double nd = static_cast<double>(ni);
@@ -196,16 +216,17 @@ __global__ void __launch_bounds__(MC_THREADS) k_margins_cpc(
       __syncthreads();
       // block b = 64 consecutive samples: the sum of its two 32-sample warps
       const int b = (js0 + t0) / 64 + tid;
-      if (tid < MC_THREADS / 64 && b < nblk && 64 * tid < 2 * SPc - t0)
+      if (tid < NT / 64 && b < nblk && 64 * tid < nchunk - t0)
         loss_part[static_cast<int64_t>(c) * nblk + b] = red[2 * tid] + red[2 * tid + 1];
       __syncthreads();
     }
   }
   // padding samples past the last pair (ldj <= js < ldh) carry no weight
-  for (int js = 2 * SP + tid; js < ldh; js += MC_THREADS) {
-    hcoef[static_cast<int64_t>(c) * ldh + js] = 0.0;
-    gcoef[static_cast<int64_t>(c) * ldh + js] = 0.0;
-  }
+  if (part == NS - 1)
+    for (int js = 2 * SP + tid; js < ldh; js += NT) {
+      hcoef[static_cast<int64_t>(c) * ldh + js] = 0.0;
+      gcoef[static_cast<int64_t>(c) * ldh + js] = 0.0;
+    }
 }
 
 // Local gradients g_c = B_c gcoef_c + lam x (oracle.py:108-121).
