@@ -734,16 +734,32 @@ int enqueue_pp_round(Ctx* ctx) {
   cudaStream_t s = ctx->st;
   const int n = ctx->n, tau = ctx->tau;
   TRY(record(ctx, EV_START, s));
-  // metric probes over all clients at the current iterate (runtime.py:237-238)
-  TRY(launch_margins(ctx, s, ctx->x, nullptr, n));
-  TRY(launch_gradient(ctx, s, ctx->x, nullptr, n));
-  TRY(launch_reduce(ctx, s, ctx->x, nullptr, n, n, false, ctx->row_grad, ctx->row_f));
-  // participants and the new point (algorithms.py:422-433)
+  // the metric probes over all clients at the current iterate
+  // (runtime.py:237-238) only feed the row: they run on the second stream
+  // while the master forms the new point from the running averages
+  // (algorithms.py:422-433) into x_new (x <- x_new after the join).  The
+  // solve's cluster is launched first; the probes wait for its launch
+  // completion (as the FedNL round's compressor does).
+  static const bool pp_serial = (getenv("FB_PP_SERIAL") && atoi(getenv("FB_PP_SERIAL"))) ||
+                                getenv("CUDA_INJECTION64_PATH") != nullptr ||
+                                getenv("NV_NSIGHT_INJECTION_TRANSPORT_TYPE") != nullptr ||
+                                getenv("NV_TPS_LAUNCH_TOKEN") != nullptr;
   k_pp_select<<<1, 32, 0, s>>>(ctx->ctl, n, tau, ctx->subset, ctx->pool);
   CKL();
-  TRY(launch_solve(ctx, s, ctx->hmas, ctx->pp_shift, ctx->gvec, nullptr, ctx->pvec, ctx->x, 1, 0));
-  k_check_finite<<<1, 256, 0, s>>>(ctx->ctl, ctx->d, ctx->x);
+  TRY(launch_solve(ctx, s, ctx->hmas, ctx->pp_shift, ctx->gvec, nullptr, ctx->pvec, ctx->x_new, 1, 0,
+                   nullptr, pp_serial ? nullptr : ctx->ev_solve_launched));
+  cudaStream_t sp = pp_serial ? s : ctx->st2;
+  if (!pp_serial) CK(cudaStreamWaitEvent(sp, ctx->ev_solve_launched, 0));
+  TRY(launch_margins(ctx, sp, ctx->x, nullptr, n));
+  TRY(launch_gradient(ctx, sp, ctx->x, nullptr, n));
+  TRY(launch_reduce(ctx, sp, ctx->x, nullptr, n, n, false, ctx->row_grad, ctx->row_f));
+  k_check_finite<<<1, 256, 0, s>>>(ctx->ctl, ctx->d, ctx->x_new);
   CKL();
+  if (!pp_serial) {
+    CK(cudaEventRecord(ctx->ev_join, sp));
+    CK(cudaStreamWaitEvent(s, ctx->ev_join, 0));
+  }
+  CK(cudaMemcpyAsync(ctx->x, ctx->x_new, sizeof(double) * ctx->d, cudaMemcpyDeviceToDevice, s));
   TRY(record(ctx, EV_SOLVE_END, s));
   // participants' oracle at x_new (algorithms.py:240-249)
   CK(cudaMemsetAsync(ctx->flags, 0, sizeof(int32_t) * n, s));
