@@ -38,6 +38,7 @@ namespace cg = cooperative_groups;
 constexpr int CH_THREADS = 256;
 constexpr int CH_MAX_CLUSTER = 8;
 constexpr int CH_MAX_D = 1024;
+constexpr int CH_DMMA_MIN_D = 256;  // trailing update on DMMA tiles above this d
 
 template <int NB>
 struct SolveSmem {
@@ -233,7 +234,7 @@ __global__ void __launch_bounds__(CH_THREADS, 1) k_chol_solve(
     //          P P^T on DMMA.8x8x4 (P = the m x NB panel in shared memory),
     //          TB tiles per warp in flight, the M operands loaded first
     const int nb_next = min(NB, d - p1);
-    {
+    if (d > CH_DMMA_MIN_D) {  // DMMA tiles (large d: c4)
       const int g = lane >> 2, tg = lane & 3;
       const int mz = (d + NB) / NB * NB;  // a panel row never written: zeros (set up front)
       const int T = (m + 7) >> 3;
@@ -288,6 +289,32 @@ __global__ void __launch_bounds__(CH_THREADS, 1) k_chol_solve(
             if (r < nb_next)  // next diagonal block (row r, col jr <= r) into every CTA
               for (int qc = 0; qc < cs; ++qc) cluster.map_shared_rank(&sm, qc)->nxt[par ^ 1][r][jr] = nv;
           }
+        }
+      }
+    }
+    else {  // small d: one warp per row, FMA dot products against the panel
+      for (int r = gwarp; r < m; r += nwarps) {  // row i = p1 + r
+        const int i = p1 + r;
+        const int jmax = (i == d) ? r - 1 : r;  // the rhs row has no diagonal
+        double li[NB];
+#pragma unroll
+        for (int s = 0; s < NB; ++s) li[s] = pan[r * PLD + s];
+        double* colp = M + i * ld;
+        for (int jr = lane; jr <= jmax; jr += 32) {
+          const int j = p1 + jr;
+          double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+          const double* pj = pan + jr * PLD;
+#pragma unroll
+          for (int s = 0; s < NB; s += 4) {
+            a0 = fma(li[s], pj[s], a0);
+            a1 = fma(li[s + 1], pj[s + 1], a1);
+            a2 = fma(li[s + 2], pj[s + 2], a2);
+            a3 = fma(li[s + 3], pj[s + 3], a3);
+          }
+          const double nv = __dsub_rn(__ldcg(colp + j), (a0 + a1) + (a2 + a3));
+          colp[j] = nv;
+          if (r < nb_next)  // next diagonal block (row r, col jr <= r) into every CTA
+            for (int q = 0; q < cs; ++q) cluster.map_shared_rank(&sm, q)->nxt[par ^ 1][r][jr] = nv;
         }
       }
     }

@@ -1,7 +1,10 @@
-set -x
-O=gpurun_out/m1
+# Round-end measurement set (run under gpurun from the repo root):
+#   tests, smoke, bench lines c0-c4 + the reference arm, the c0 launch list,
+#   ncu full-set captures of the c0 Hessian and the c4 split TopK + fold.
+O=${O:-gpurun_out/m2}
 mkdir -p $O
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,power.draw --format=csv > $O/smi.txt
+timeout 900 python -m pytest tests -m gpu -q > $O/pytest_gpu.log 2>&1; echo "rc=$?" >> $O/pytest_gpu.log
 timeout 200 python -c "import __graft_entry__ as g; g.smoke()" > $O/smoke.log 2>&1
 for c in c0 c1 c2 c3 c4; do timeout 400 python bench.py --config $c > $O/bench_$c.json 2> $O/bench_$c.err; done
 timeout 300 python bench.py --impl reference > $O/bench_reference_c0.json 2> $O/bench_reference_c0.err
