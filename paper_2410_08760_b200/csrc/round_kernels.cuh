@@ -603,6 +603,7 @@ __global__ void __launch_bounds__(256) k_ls_decide(
       else s_fbest = fmin(s_fbest, ft);
     }
     __syncthreads();
+    if (s_acc >= 0) break;  // accepted: the batch's later trials are not needed (block-uniform)
   }
   const int acc = s_acc;
   if (acc >= 0) {
