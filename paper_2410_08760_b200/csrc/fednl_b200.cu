@@ -680,8 +680,6 @@ int enqueue_fednl_round(Ctx* ctx) {
   TRY(record(ctx, EV_SOLVE_END, s));
   int launches = ctx->topk_split ? 9 : 8;
   if (ls) {
-    k_dot<<<1, 256, 0, s>>>(ctx->ctl, ctx->d, ctx->gbar, ctx->pvec, ctx->sc);
-    CKL();
     dim3 grid(ctx->ls_nblk, n);
     k_ls_trials<<<grid, MARGIN_THREADS, LS_BATCH * ctx->d * sizeof(double), s>>>(
         ctx->ctl, ctx->Bt, ctx->d, ctx->ni, ctx->ldj, ctx->x, ctx->pvec, ctx->steps_table, n,
@@ -689,9 +687,10 @@ int enqueue_fednl_round(Ctx* ctx) {
     CKL();
     k_ls_decide<<<1, 256, 0, s>>>(ctx->ctl, ctx->d, n, ctx->ni, ctx->ls_nblk, ctx->cfg.lam,
                                   ctx->cfg.ls_c, ctx->steps_table, ctx->trial_x,
-                                  ctx->ls_loss_part, ctx->sc, ctx->x_new, LS_BATCH);
+                                  ctx->ls_loss_part, ctx->sc, ctx->x_new, LS_BATCH, ctx->gbar,
+                                  ctx->pvec);
     CKL();
-    launches += 3;
+    launches += 2;
   }
   CK(cudaStreamWaitEvent(s, ctx->ev_join, 0));
   if (fold_late)
@@ -1537,7 +1536,8 @@ int fb_run_rounds(void* handle, int32_t first_round, int32_t count, double stop_
       CKL();
       k_ls_decide<<<1, 256, 0, s>>>(ctx->ctl, ctx->d, n, ctx->ni, ctx->ls_nblk, ctx->cfg.lam,
                                     ctx->cfg.ls_c, ctx->steps_table, ctx->trial_x,
-                                    ctx->ls_loss_part, ctx->sc, ctx->x_new, LS_BATCH);
+                                    ctx->ls_loss_part, ctx->sc, ctx->x_new, LS_BATCH, ctx->gbar,
+                                    ctx->pvec);
       CKL();
       TRY(read_status(ctx, &h));
       if (h.code == 0 && !h.halt) {

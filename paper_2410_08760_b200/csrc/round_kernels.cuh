@@ -555,13 +555,21 @@ __global__ void __launch_bounds__(256) k_ls_decide(
     DevCtl* __restrict__ ctl, int d, int n, int ni, int nblk, double lam, double ls_c,
     const double* __restrict__ steps_table, const double* __restrict__ trial_x,
     const double* __restrict__ loss_part, RoundScalars* __restrict__ sc,
-    double* __restrict__ x_new, int batch) {
+    double* __restrict__ x_new, int batch, const double* __restrict__ gbar,
+    const double* __restrict__ p) {
   if (ctl->halt && ctl->code != ST_LS_PENDING) return;
   __shared__ double red[8];
   __shared__ int s_acc;
   __shared__ double s_fbest;
   __shared__ double s_lsum[LS_DECIDE_MAXN];  // per-client loss sums of one trial
   const int s0 = ctl->ls_next;
+  if (s0 == 0) {  // decrement = <gbar, p> (algorithms.py:302), as k_dot forms it
+    double part = 0.0;
+    for (int i = threadIdx.x; i < d; i += blockDim.x) part = fma(gbar[i], p[i], part);
+    const double dec = block_sum(part, red);
+    if (threadIdx.x == 0) sc->decrement = dec;
+    __syncthreads();
+  }
   if (threadIdx.x == 0) { s_acc = -1; s_fbest = (s0 == 0) ? INFINITY : ctl->f_best; }
   __syncthreads();
   for (int s = 0; s < batch; ++s) {
