@@ -743,12 +743,13 @@ int enqueue_pp_round(Ctx* ctx) {
                                 getenv("CUDA_INJECTION64_PATH") != nullptr ||
                                 getenv("NV_NSIGHT_INJECTION_TRANSPORT_TYPE") != nullptr ||
                                 getenv("NV_TPS_LAUNCH_TOKEN") != nullptr;
-  k_pp_select<<<1, 32, 0, s>>>(ctx->ctl, n, tau, ctx->subset, ctx->pool);
-  CKL();
   TRY(launch_solve(ctx, s, ctx->hmas, ctx->pp_shift, ctx->gvec, nullptr, ctx->pvec, ctx->x_new, 1, 0,
                    nullptr, pp_serial ? nullptr : ctx->ev_solve_launched));
   cudaStream_t sp = pp_serial ? s : ctx->st2;
   if (!pp_serial) CK(cudaStreamWaitEvent(sp, ctx->ev_solve_launched, 0));
+  // this round's participants (master subset stream) off the critical path too
+  k_pp_select<<<1, 128, 0, sp>>>(ctx->ctl, n, tau, ctx->subset, ctx->pool);
+  CKL();
   TRY(launch_margins(ctx, sp, ctx->x, nullptr, n));
   TRY(launch_gradient(ctx, sp, ctx->x, nullptr, n));
   TRY(launch_reduce(ctx, sp, ctx->x, nullptr, n, n, false, ctx->row_grad, ctx->row_f));

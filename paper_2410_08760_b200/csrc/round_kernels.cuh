@@ -361,18 +361,22 @@ __global__ void __launch_bounds__(256) k_finish(
 // (algorithms.py:422-425).  One thread.
 __global__ void k_pp_select(DevCtl* __restrict__ ctl, int n, int tau, int32_t* __restrict__ subset,
                             int32_t* __restrict__ pool) {
-  if (ctl->halt) return;
-  if (threadIdx.x != 0) return;
+  // the swap chain in shared memory when the pool fits (one thread draws)
+  constexpr int SMAX = 4096;
+  __shared__ int32_t pool_s[SMAX];
+  int32_t* pl = n <= SMAX ? pool_s : pool;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) pl[i] = i;
+  __syncthreads();
+  if (threadIdx.x != 0 || ctl->halt) return;
   Prg p(ctl->master_state);
-  for (int i = 0; i < n; ++i) pool[i] = i;
   for (int i = 0; i < tau; ++i) {
     const int j = i + static_cast<int>(p.randrange(static_cast<uint64_t>(n - i)));
-    const int32_t tmp = pool[i];
-    pool[i] = pool[j];
-    pool[j] = tmp;
+    const int32_t tmp = pl[i];
+    pl[i] = pl[j];
+    pl[j] = tmp;
   }
   ctl->master_state = p.state;
-  for (int i = 0; i < tau; ++i) subset[i] = pool[i];
+  for (int i = 0; i < tau; ++i) subset[i] = pl[i];
   for (int i = 1; i < tau; ++i) {  // insertion sort (tau is small)
     const int32_t v = subset[i];
     int j = i - 1;
@@ -455,7 +459,14 @@ __global__ void __launch_bounds__(256) k_pp_master(
   const double nn = static_cast<double>(n);
   for (int a = threadIdx.x; a < d; a += blockDim.x) {
     double g = gvec[a];
-    for (int i = 0; i < tau; ++i) g = __dadd_rn(g, __ddiv_rn(dgvec[static_cast<int64_t>(i) * d + a], nn));
+    for (int i0 = 0; i0 < tau; i0 += 8) {  // 8 loads in flight, added in client order
+      double v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) v[u] = i0 + u < tau ? dgvec[static_cast<int64_t>(i0 + u) * d + a] : 0.0;
+#pragma unroll
+      for (int u = 0; u < 8; ++u)
+        if (i0 + u < tau) g = __dadd_rn(g, __ddiv_rn(v[u], nn));
+    }
     gvec[a] = g;
   }
   if (threadIdx.x == 0) {
@@ -469,12 +480,16 @@ __global__ void __launch_bounds__(256) k_pp_master(
 __global__ void k_check_flags_pp(DevCtl* ctl, int tau, const int32_t* subset,
                                  const int32_t* flags) {
   if (ctl->halt) return;
-  if (threadIdx.x != 0) return;
-  for (int i = 0; i < tau; ++i) {
-    const int c = subset ? subset[i] : i;
-    if (flags[c] & 1) {
-      ctl->bad_client = c;
-      raise_status(ctl, ST_NONFINITE);
+  // one warp, 32 participants per step; the first bad one in subset order
+  for (int i0 = 0; i0 < tau; i0 += 32) {
+    const int i = i0 + static_cast<int>(threadIdx.x);
+    const int c = i < tau ? (subset ? subset[i] : i) : -1;
+    const uint32_t bad = __ballot_sync(0xffffffffu, c >= 0 && (flags[c] & 1));
+    if (bad) {
+      if (threadIdx.x == __ffs(bad) - 1) {
+        ctl->bad_client = c;
+        raise_status(ctl, ST_NONFINITE);
+      }
       return;
     }
   }
