@@ -265,7 +265,6 @@ __global__ void __launch_bounds__(MARGIN_THREADS) k_ls_trials(
     double* __restrict__ loss_part, int nblk) {
   if (ctl->halt && ctl->code != ST_LS_PENDING) return;
   extern __shared__ double xt[];  // [LS_BATCH][d]
-  __shared__ double red[MARGIN_THREADS / 32];
   const int s0 = ctl->ls_next;
   const int c = blockIdx.y;
   for (int e = threadIdx.x; e < LS_BATCH * d; e += blockDim.x) {
@@ -283,29 +282,34 @@ __global__ void __launch_bounds__(MARGIN_THREADS) k_ls_trials(
 #pragma unroll
   for (int s = 0; s < LS_BATCH; ++s) m[s] = 0.0;
   if (j < ni) {
+    // 16 independent loads in flight per batch; the last batch predicated
+    // (features in increasing order as before: the same fma chain)
     const double* col = Bt + static_cast<int64_t>(c) * d * ldj + j;
-    int a = 0;
-    for (; a + 8 <= d; a += 8) {  // 8 independent loads in flight
-      double b[8];
+    for (int a = 0; a < d; a += 16) {
+      double b[16];
 #pragma unroll
-      for (int u = 0; u < 8; ++u) b[u] = __ldg(col + static_cast<int64_t>(a + u) * ldj);
+      for (int u = 0; u < 16; ++u) b[u] = a + u < d ? __ldg(col + static_cast<int64_t>(a + u) * ldj) : 0.0;
 #pragma unroll
-      for (int u = 0; u < 8; ++u)
+      for (int u = 0; u < 16; ++u)
+        if (a + u < d)
 #pragma unroll
-        for (int s = 0; s < LS_BATCH; ++s) m[s] = fma(b[u], xt[s * d + a + u], m[s]);
-    }
-    for (; a < d; ++a) {
-      const double b = __ldg(col + static_cast<int64_t>(a) * ldj);
-#pragma unroll
-      for (int s = 0; s < LS_BATCH; ++s) m[s] = fma(b, xt[s * d + a], m[s]);
+          for (int s = 0; s < LS_BATCH; ++s) m[s] = fma(b[u], xt[s * d + a + u], m[s]);
     }
   }
+  // the LS_BATCH block sums with one barrier pair (block_sum's order per trial)
+  __shared__ double red4[LS_BATCH][MARGIN_THREADS / 32];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
 #pragma unroll
   for (int s = 0; s < LS_BATCH; ++s) {
-    const double loss = (j < ni) ? softplus_neg(m[s]) : 0.0;
-    const double tot = block_sum(loss, red);
-    if (threadIdx.x == 0)
-      loss_part[(static_cast<int64_t>(s) * n_clients + c) * nblk + blockIdx.x] = tot;
+    const double v = warp_sum((j < ni) ? softplus_neg(m[s]) : 0.0);
+    if (lane == 0) red4[s][wid] = v;
+  }
+  __syncthreads();
+  if (threadIdx.x < LS_BATCH) {
+    const int s = threadIdx.x;
+    double tot = 0.0;
+    for (int i = 0; i < nw; ++i) tot += red4[s][i];
+    loss_part[(static_cast<int64_t>(s) * n_clients + c) * nblk + blockIdx.x] = tot;
   }
 }
 
