@@ -553,6 +553,11 @@ bool dense_kind(const Ctx* ctx) {
 }
 // master fold Hout = Hin + (alpha/n) sum_c delta_c (ascending c); for the
 // dense kinds the client shift update rides along when `hest` is non-null
+// k_finish grid when it also copies H^{k+1} -> H^k: about 8 doubles per thread
+int finish_grid(const Ctx* ctx) {
+  return static_cast<int>(std::min<int64_t>(2 * ctx->num_sms, (ctx->w + 2047) / 2048));
+}
+
 int launch_master_fold(Ctx* ctx, cudaStream_t s, const int32_t* clients, int n_active,
                        double* hest, const double* h_in, double* h_out, bool client_update = false) {
   if (dense_kind(ctx)) {
@@ -696,9 +701,9 @@ int enqueue_fednl_round(Ctx* ctx) {
   if (fold_late)
     TRY(launch_master_fold(ctx, s, nullptr, n, dense_kind(ctx) ? ctx->hest : nullptr, ctx->hmas,
                            ctx->hmas2, cu_fold));
-  CK(cudaMemcpyAsync(ctx->hmas, ctx->hmas2, sizeof(double) * ctx->w, cudaMemcpyDeviceToDevice, s));
-  k_finish<<<1, 256, 0, s>>>(ctx->ctl, ctx->d, n, n, nullptr, ctx->x, ctx->x_new, 1, ctx->count,
-                             ctx->row_counts, ctx->row_ls);
+  k_finish<<<finish_grid(ctx), 256, 0, s>>>(ctx->ctl, ctx->d, n, n, nullptr, ctx->x, ctx->x_new, 1,
+                                            ctx->count, ctx->row_counts, ctx->row_ls, ctx->hmas2,
+                                            ctx->hmas, ctx->w);
   CKL();
   TRY(record(ctx, EV_END, s));
   ctx->launches_per_round = launches;
@@ -711,9 +716,9 @@ int enqueue_ls_tail(Ctx* ctx) {
   // the fold of this round already ran (it does not depend on the line
   // search); only the H^{k+1} copy and the round epilogue remain
   cudaStream_t s = ctx->st;
-  CK(cudaMemcpyAsync(ctx->hmas, ctx->hmas2, sizeof(double) * ctx->w, cudaMemcpyDeviceToDevice, s));
-  k_finish<<<1, 256, 0, s>>>(ctx->ctl, ctx->d, ctx->n, ctx->n, nullptr, ctx->x, ctx->x_new, 1,
-                             ctx->count, ctx->row_counts, ctx->row_ls);
+  k_finish<<<finish_grid(ctx), 256, 0, s>>>(ctx->ctl, ctx->d, ctx->n, ctx->n, nullptr, ctx->x,
+                                            ctx->x_new, 1, ctx->count, ctx->row_counts, ctx->row_ls,
+                                            ctx->hmas2, ctx->hmas, ctx->w);
   CKL();
   return FB_OK;
 }

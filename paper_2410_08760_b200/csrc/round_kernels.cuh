@@ -325,7 +325,14 @@ __global__ void __launch_bounds__(256) k_finish(
     DevCtl* __restrict__ ctl, int d, int n, int n_active, const int32_t* __restrict__ clients,
     double* __restrict__ x, const double* __restrict__ x_new, int copy_x,
     const int32_t* __restrict__ count, int32_t* __restrict__ row_counts,
-    int32_t* __restrict__ row_ls) {
+    int32_t* __restrict__ row_ls, const double* __restrict__ hcopy_src = nullptr,
+    double* __restrict__ hcopy_dst = nullptr, int64_t hcopy_n = 0) {
+  // H^{k+1} (the fold's second buffer) back into H^k, over every block of the
+  // grid (unconditionally, as the copy it replaces), then the epilogue on block 0
+  for (int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; t < hcopy_n;
+       t += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    hcopy_dst[t] = hcopy_src[t];
+  if (blockIdx.x != 0) return;
   if (ctl->halt) return;
   __shared__ int bad;
   if (threadIdx.x == 0) bad = 0;
