@@ -38,7 +38,8 @@ extern "C" {
 #define FB_ERR_DIVERGED 5      /* algorithms.py:52-57 DivergenceError        */
 #define FB_ERR_LINE_SEARCH 6   /* algorithms.py:41-49 LineSearchError        */
 #define FB_ERR_UNSUPPORTED 7   /* outside this build's envelope              */
-#define FB_ERR_LS_PENDING 8    /* internal: line search needs more trials    */
+/* (8 was an internal line-search continuation code, retired: the trial
+ * batches now loop inside the round graph) */
 #define FB_ERR_EIGEN 9         /* linalg.py:36 EigenConvergenceError         */
 
 /* compressor kinds (compressors.py:41-47) */
@@ -59,6 +60,12 @@ extern "C" {
 #define FB_OPTION_B 0
 #define FB_OPTION_A 1
 
+/* TopK variant for w > 32,767 (a tuning knob with no effect on results:
+ * every variant selects the same index set, bit for bit) */
+#define FB_TOPK_PATH_AUTO 0    /* by size: split when n * w >= 2^26           */
+#define FB_TOPK_PATH_STREAM 1  /* one CTA per client, one pass over D         */
+#define FB_TOPK_PATH_SPLIT 2   /* window / segmented pass / select kernels    */
+
 /* hessian_init (algorithms.py:37) */
 #define FB_INIT_LAMBDA_IDENTITY 0
 #define FB_INIT_ZERO 1
@@ -71,7 +78,7 @@ extern "C" {
 typedef struct fb_config {
   int32_t d;              /* dimension (features + intercept)          */
   int32_t n_clients;      /* n                                          */
-  int32_t n_samples;      /* n_i, equal for every client                */
+  int32_t n_samples;      /* n_i; the LARGEST shard's with fb_upload_shards_ex */
   int32_t algorithm;      /* FB_ALG_*                                   */
   int32_t kind;           /* FB_KIND_*                                  */
   int32_t k;              /* budget for the sparse kinds, else 0        */
@@ -80,12 +87,14 @@ typedef struct fb_config {
   int32_t hessian_init;   /* FB_INIT_*                                  */
   int32_t option;         /* FB_OPTION_*                                */
   double alpha;
-  double lam;
+  double lam;             /* RunConfig.lam (master lambda-identity init) */
   double ls_c;
   double ls_gamma;
   uint64_t run_seed;
   double ls_steps_table[61];
   double mu;              /* option a eigenvalue floor (effective_mu)   */
+  int32_t topk_path;      /* FB_TOPK_PATH_*                             */
+  int32_t reserved;
 } fb_config;
 
 /* Detail of the last failure raised by a round (mirrors the reference's
@@ -115,6 +124,9 @@ typedef struct fb_profile {
 } fb_profile;
 
 /* ---- lifecycle -------------------------------------------------------- */
+/* sizeof(fb_config), sizeof(fb_status), sizeof(fb_profile) as this library
+ * was compiled (a binding checks its struct mirrors against them; no GPU) */
+int fb_abi_sizes(int32_t* out3);
 /* Validate cfg, allocate every device buffer, build TMA descriptors.
  * Replaces runtime.simulate's setup (runtime.py:145-155). */
 int fb_create(const fb_config* cfg, void** ctx);
@@ -147,6 +159,14 @@ int fb_set_shard(void* ctx, int32_t world, int32_t rank, const uint8_t* nccl_id)
  * borrowed for the call.  Replaces ClientShard residency
  * (oracle.py:33-46, data.py:186-213). */
 int fb_upload_shards(void* ctx, const double* const* bmats);
+/* The same for shards of different sizes and regularisers, as the reference
+ * accepts them (runtime.py:145-151 checks only the dimension; each
+ * ClientShard carries its own n_samples and lam, oracle.py:33-46):
+ * n_samples[c] in [1, cfg.n_samples] columns of shard c (may be NULL: all
+ * cfg.n_samples), lam[c] its lambda (may be NULL: all cfg.lam), used by the
+ * client's oracle and its lambda-identity H_c^0. */
+int fb_upload_shards_ex(void* ctx, const double* const* bmats, const int32_t* n_samples,
+                        const double* lam);
 
 /* ---- run -------------------------------------------------------------- */
 /* Round-0 state: client/master Hessian estimates per hessian_init and, for
@@ -162,7 +182,10 @@ int fb_init_state(void* ctx, const double* x0);
  * the start of the call to the end of round r.  When timed != 0 per-kernel
  * CUDA-event times are collected (fb_get_profile).  Stops early at the first
  * failure (status set, *rounds_done = rounds completed) or when
- * stop_grad_norm >= 0 and a row's grad_norm <= stop_grad_norm. */
+ * stop_grad_norm >= 0 and a row's grad_norm <= stop_grad_norm: the rule is
+ * evaluated on the device inside each round, so no round runs past the
+ * stopping row (FedNL / LS: after that round's step, runtime.py:270-272;
+ * PP: before it, runtime.py:239-242). */
 int fb_run_rounds(void* ctx, int32_t first_round, int32_t count, double stop_grad_norm,
                   int32_t timed, double* grad_norm, double* f_value, int32_t* ls_steps,
                   int32_t* entry_counts, double* wall_ms, int32_t* rounds_done);

@@ -649,7 +649,10 @@ class OracleRun:
         self.d = bmats[0].shape[0]
         if any(b.shape[0] != self.d for b in bmats):
             raise ValueError("all shards must share one dimension")
-        self.lam = cfg.lam if lam is None else lam
+        # per-client lambda (ClientShard.lam, oracle.py:33-46): one value or one per shard
+        lam = cfg.lam if lam is None else lam
+        self.lams = [float(v) for v in lam] if np.ndim(lam) else [float(lam)] * self.n
+        self.lam = self.lams[0]
         self.w = packed_len(self.d)
         check_k(cfg.kind, cfg.k, self.w)
         self.alpha = default_alpha(cfg.kind, cfg.k, self.w) if cfg.alpha is None else cfg.alpha
@@ -689,7 +692,7 @@ class OracleRun:
         diag = diag_positions(d)
         pp = cfg.algorithm == "fednl-pp"
         need_hess = cfg.hessian_init == "exact" or pp
-        evals = self._map(lambda c: local_eval(self.bmats[c], self.lam, self.x,
+        evals = self._map(lambda c: local_eval(self.bmats[c], self.lams[c], self.x,
                                                need_hess=need_hess, need_f=False)
                           if need_hess else None, list(range(n)))
         for c in range(n):
@@ -697,7 +700,7 @@ class OracleRun:
                 self.h_cli[c] = 0.0
             elif cfg.hessian_init == "lambda-identity":
                 self.h_cli[c] = 0.0
-                self.h_cli[c, diag] += self.lam
+                self.h_cli[c, diag] += self.lams[c]
             else:
                 self.h_cli[c] = evals[c].hess
             if pp:
@@ -727,7 +730,7 @@ class OracleRun:
 
     # ---- one client's FedNL round (algorithms.py:225-238)
     def client_round(self, cid: int, rnd: int):
-        ev = local_eval(self.bmats[cid], self.lam, self.x, need_hess=True,
+        ev = local_eval(self.bmats[cid], self.lams[cid], self.x, need_hess=True,
                         need_f=True)
         diff = ev.hess - self.h_cli[cid]
         shift = frob(diff, self.d)
@@ -738,7 +741,7 @@ class OracleRun:
         return ev.grad, shift, delta, ev.f
 
     def mean_f(self, x) -> float:  # runtime.py:189-194
-        vals = self._map(lambda c: f_from_margins(margins(self.bmats[c], x), x, self.lam),
+        vals = self._map(lambda c: f_from_margins(margins(self.bmats[c], x), x, self.lams[c]),
                          list(range(self.n)))
         tot = 0.0
         for c in range(self.n):
@@ -747,7 +750,7 @@ class OracleRun:
 
     def mean_grad(self, x) -> np.ndarray:  # runtime.py:196-201
         vals = self._map(lambda c: grad_from_sigmoid(self.bmats[c], sigmoid(margins(self.bmats[c], x)),
-                                                      x, self.lam), list(range(self.n)))
+                                                      x, self.lams[c]), list(range(self.n)))
         acc = np.zeros(self.d)
         for c in range(self.n):
             acc += vals[c]
@@ -812,7 +815,7 @@ class OracleRun:
 
     # ---- FedNL-PP (runtime.py:236-253, algorithms.py:240-264, 422-442)
     def pp_client(self, cid: int, x_new: np.ndarray, rnd: int):
-        ev = local_eval(self.bmats[cid], self.lam, x_new, need_hess=True, need_f=False)
+        ev = local_eval(self.bmats[cid], self.lams[cid], x_new, need_hess=True, need_f=False)
         diff = ev.hess - self.h_cli[cid]
         delta = compress_packed(diff, self.d, self.cfg.kind, self.cfg.k,
                                 round_stream(self.cfg.run_seed, cid, rnd),

@@ -36,6 +36,8 @@ from fednl.data import (  # noqa: E402
     generate_synthetic,
     normalize_labels,
 )
+from fednl.algorithms import LineSearchError  # noqa: E402
+from fednl.oracle import ClientShard  # noqa: E402
 from fednl.runtime import simulate  # noqa: E402
 
 # The BASELINE configs; the shapes are used at reduced rounds.
@@ -452,6 +454,96 @@ def gen_ingest():
     return out
 
 
+# ---- round-2 additions (simulate_r2.npz): line-search continuation and
+# failure, ragged shards with per-shard lambda, a longer c0 trajectory with
+# the reference's own 1- vs 8-thread envelope
+SIM_R2 = {
+    # Armijo with c close to 1 backtracks s = 5..29 times every round: the
+    # trial batches continue past the first one inside every (mid-chunk) round
+    "ls_deep": (("synth", 8, 120, 4, 10), dict(rounds=8, algorithm="fednl-ls", compressor=("topk", 9),
+                                                ls_c=0.99, ls_gamma=0.9)),
+    "ls_deep8": (("synth", 8, 120, 4, 10), dict(rounds=8, algorithm="fednl-ls", compressor=("topk", 9),
+                                                 ls_c=0.999, ls_gamma=0.5)),
+    # shards of 40 / 23 / 57 / 31 / 49 samples, lambdas 1e-3 .. 5e-3
+    "ragged_topk": (("ragged", 7, (40, 23, 57, 31, 49), 21), dict(rounds=10, compressor=("topk", 7))),
+    "ragged_identity": (("ragged", 7, (40, 23, 57, 31, 49), 22), dict(rounds=8)),
+    "ragged_exact": (("ragged", 7, (40, 23, 57, 31, 49), 23), dict(rounds=8, hessian_init="exact",
+                                                                      compressor=("randseqk", 9))),
+    "ragged_ls": (("ragged", 7, (40, 23, 57, 31, 49), 24), dict(rounds=8, algorithm="fednl-ls",
+                                                                   compressor=("toplek", 9))),
+    "ragged_pp": (("ragged", 7, (40, 23, 57, 31, 49), 25), dict(rounds=12, algorithm="fednl-pp", tau=2,
+                                                                   compressor=("randk", 9))),
+    "c0_r20": (("baseline", "c0"), dict(rounds=20)),
+}
+RAGGED_LAMS = (1e-3, 2e-3, 3e-3, 4e-3, 5e-3)
+
+
+def ragged_shards(num_features, sizes, seed):
+    """One shuffled shard of sum(sizes) columns cut into consecutive pieces,
+    each a ClientShard with its own lambda (the shape load_client_shard
+    produces per client, data.py:236-254)."""
+    (whole,) = make_shards(num_features, sum(sizes), 1, seed)
+    out, lo = [], 0
+    for i, sz in enumerate(sizes):
+        out.append(ClientShard(bmat=np.asfortranarray(whole.bmat[:, lo:lo + sz]),
+                               lam=RAGGED_LAMS[i % len(RAGGED_LAMS)]))
+        lo += sz
+    return out
+
+
+def build_case_r2(name):
+    gen, kw = SIM_R2[name]
+    if gen[0] == "ragged":
+        _, nf, sizes, seed = gen
+        kw = dict(kw)
+        kw.setdefault("run_seed", seed)
+        comp = kw.pop("compressor", ("identity",))
+        spec = CompressorSpec(CompressorKind(comp[0]), k=comp[1] if len(comp) > 1 else None)
+        return RunConfig(compressor=spec, **kw), ragged_shards(nf, sizes, seed)
+    SIM_CASES[name] = SIM_R2[name]
+    try:
+        return build_case(name)
+    finally:
+        del SIM_CASES[name]
+
+
+def gen_sim_r2():
+    import threadpoolctl
+
+    out = {}
+    for name in SIM_R2:
+        cfg, shards = build_case_r2(name)
+        with threadpoolctl.threadpool_limits(1, "blas"):
+            rows = simulate(cfg, shards)
+        for k, v in rows_arrays(rows).items():
+            out[f"{name}__{k}"] = v
+        print(f"  sim {name}: {len(rows)} rows, final |g|={rows[-1].grad_norm:.3e}, "
+              f"ls {[r.ls_steps for r in rows]}")
+    cfg, shards = build_case_r2("c0_r20")
+    with threadpoolctl.threadpool_limits(8, "blas"):
+        rows = simulate(cfg, shards)
+    for k, v in rows_arrays(rows).items():
+        out[f"c0_r20_mt__{k}"] = v
+    # LineSearchError: Armijo c = 0.99 with gamma = 0.97 cannot pass in 61 trials
+    cfg, shards = build_case_r2("ls_deep")
+    cfg = RunConfig(compressor=cfg.compressor, rounds=4, algorithm="fednl-ls", ls_c=0.99,
+                    ls_gamma=0.97, run_seed=cfg.run_seed)
+    try:
+        with threadpoolctl.threadpool_limits(1, "blas"):
+            simulate(cfg, shards)
+        raise AssertionError("expected LineSearchError")
+    except LineSearchError as e:
+        import re
+
+        f_start, f_best = (float(v) for v in re.findall(r"f=([-0-9.eE+]+)", str(e)))
+        out["ls_fail__round"] = np.array(e.round)
+        out["ls_fail__f_start"] = np.array(f_start)
+        out["ls_fail__f_best"] = np.array(f_best)
+        out["ls_fail__message"] = np.array(str(e))
+        print(f"  ls_fail: {e}")
+    return out
+
+
 def gen_sim_opt_a():
     return gen_sim([n for n in SIM_CASES if "opt_a" in n])
 
@@ -469,6 +561,7 @@ def main(only=None):
         ("eigen.npz", gen_eigen),
         ("simulate_opt_a.npz", gen_sim_opt_a),
         ("ingest.npz", gen_ingest),
+        ("simulate_r2.npz", gen_sim_r2),
     ):
         if only and fname not in only:
             continue

@@ -13,8 +13,7 @@ import os
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-# FB_LIB_PATH: load another build of the same library (A/B experiments)
-LIB_PATH = os.environ.get("FB_LIB_PATH") or os.path.join(HERE, "libfednl_b200.so")
+LIB_PATH = os.path.join(HERE, "libfednl_b200.so")
 
 FB_OK = 0
 FB_ERR_CUDA = 1
@@ -25,6 +24,8 @@ FB_ERR_DIVERGED = 5
 FB_ERR_LINE_SEARCH = 6
 FB_ERR_UNSUPPORTED = 7
 FB_ERR_EIGEN = 9
+
+TOPK_PATH_AUTO, TOPK_PATH_STREAM, TOPK_PATH_SPLIT = 0, 1, 2
 
 ALG_CODE = {"fednl": 0, "fednl-ls": 1, "fednl-pp": 2}
 INIT_CODE = {"lambda-identity": 0, "zero": 1, "exact": 2}
@@ -49,6 +50,8 @@ class FbConfig(C.Structure):
         ("run_seed", C.c_uint64),
         ("ls_steps_table", C.c_double * 61),
         ("mu", C.c_double),
+        ("topk_path", C.c_int32),
+        ("reserved", C.c_int32),
     ]
 
 
@@ -87,6 +90,7 @@ _I64 = C.POINTER(C.c_int64)
 
 # every symbol include/fednl_b200.h declares, with its prototype
 PROTOTYPES = {
+    "fb_abi_sizes": (C.c_int, [_I32]),
     "fb_create": (C.c_int, [C.POINTER(FbConfig), C.POINTER(C.c_void_p)]),
     "fb_destroy": (None, [_P]),
     "fb_last_error": (C.c_char_p, [_P]),
@@ -95,6 +99,7 @@ PROTOTYPES = {
     "fb_nccl_unique_id": (C.c_int, [C.POINTER(C.c_uint8)]),
     "fb_set_shard": (C.c_int, [_P, C.c_int32, C.c_int32, C.POINTER(C.c_uint8)]),
     "fb_upload_shards": (C.c_int, [_P, C.POINTER(_D)]),
+    "fb_upload_shards_ex": (C.c_int, [_P, C.POINTER(_D), _I32, _D]),
     "fb_init_state": (C.c_int, [_P, _D]),
     "fb_run_rounds": (C.c_int, [_P, C.c_int32, C.c_int32, C.c_double, C.c_int32, _D, _D, _I32,
                                 _I32, _D, _I32]),

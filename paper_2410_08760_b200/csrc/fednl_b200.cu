@@ -81,7 +81,6 @@ struct Ctx {
   int32_t* local_clients = nullptr;  // device [c_hi - c_lo] = c_lo, c_lo + 1, ...
   ncclComm_t comm = nullptr;
   int prio_high = 0;
-  cudaEvent_t* direct_pool = nullptr;  // non-null: record() targets these (FB_NO_GRAPH)
   size_t solve_smem = 0;
   int toplek_P = 0;
   int32_t* npw_tab = nullptr;  // TopLEK: numpy pairwise-sum recursion for n = w
@@ -89,9 +88,12 @@ struct Ctx {
   std::string err;
 
   cudaStream_t st = nullptr, st2 = nullptr;
+  cudaStream_t st_body = nullptr;  // captures the line search's while-loop body
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr, ev_solve_launched = nullptr;
 
   DevCtl* ctl = nullptr;
+  int32_t* ni_arr = nullptr;  // [n] samples per client (ragged shards; <= cfg.n_samples)
+  double* lam_arr = nullptr;  // [n] lambda per client (ClientShard.lam)
   double *Bt = nullptr, *x = nullptr, *x_new = nullptr, *pvec = nullptr, *zbuf = nullptr;
   double *hcoef = nullptr, *gcoef = nullptr, *loss_part = nullptr, *grad = nullptr;
   double *gbar = nullptr, *f_cli = nullptr, *shift_cli = nullptr, *frob_part = nullptr;
@@ -143,7 +145,7 @@ thread_local std::string g_err;
   do {                                                                             \
     cudaError_t e_ = (call);                                                       \
     if (e_ != cudaSuccess) {                                                       \
-      char b_[512];                                                                \
+      char b_[2048];                                                                \
       snprintf(b_, sizeof b_, "%s failed: %s (%s:%d)", #call, cudaGetErrorString(e_), \
                __FILE__, __LINE__);                                                \
       ctx->err = b_;                                                               \
@@ -155,7 +157,7 @@ thread_local std::string g_err;
   do {                                                                             \
     cudaError_t e_ = cudaGetLastError();                                           \
     if (e_ != cudaSuccess) {                                                       \
-      char b_[512];                                                                \
+      char b_[2048];                                                                \
       snprintf(b_, sizeof b_, "kernel launch failed: %s (%s:%d)", cudaGetErrorString(e_), \
                __FILE__, __LINE__);                                                \
       ctx->err = b_;                                                               \
@@ -319,39 +321,36 @@ bool sharded(const Ctx* ctx) { return ctx->world > 1 || ctx->comm != nullptr; }
 // groups 250 us — the group's B rows stay in L2 for its tiles while each
 // group's last wave still ends on the cheap tiles.
 int hess_group(const Ctx* ctx) {
-  static const int env = getenv("FB_HESS_GROUP") ? atoi(getenv("FB_HESS_GROUP")) : 0;
-  if (env > 0) return env;
   return std::max(1, 5 * ctx->num_sms / std::max(1, ctx->n_pairs));
 }
 // programmatic dependent launch attributes, except under a profiler's
 // injection library (serialised launches there anyway)
-bool pdl_ok(const Ctx*) {
+bool under_profiler() {
   static const bool injected = getenv("CUDA_INJECTION64_PATH") != nullptr ||
                                getenv("NV_NSIGHT_INJECTION_TRANSPORT_TYPE") != nullptr ||
                                getenv("NV_TPS_LAUNCH_TOKEN") != nullptr;
-  return !injected && !getenv("FB_NO_PDL");
+  return injected;
 }
+bool pdl_ok(const Ctx*) { return !under_profiler(); }
 int launch_margins(Ctx* ctx, cudaStream_t s, const double* x, const int32_t* clients, int n_active,
                    bool with_ctl = true) {
-  if (n_active >= ctx->num_sms * 3 / 4 && mc_smem_bytes(ctx->d, ctx->ldj) <= MC_SMEM_MAX &&
-      !getenv("FB_MARGINS_OLD")) {
+  if (n_active >= ctx->num_sms * 3 / 4 && mc_smem_bytes(ctx->d, ctx->ldj) <= MC_SMEM_MAX) {
     // enough clients to fill the GPU: one CTA streams each client's rows
     // two 512-thread CTAs per client (each half of its samples, two CTAs per
     // SM) when that halves the row batches a thread streams; else one
-    static const int mc_split = getenv("FB_MARGINS_SPLIT") ? atoi(getenv("FB_MARGINS_SPLIT")) : 2;
-    if (mc_split == 2 && ctx->ldj / 2 > 64) {
+    if (ctx->ldj / 2 > 64) {
       k_margins_cpc<512, 2><<<2 * n_active, 512, mc_smem_bytes_nt(ctx->d, ctx->ldj, 2, 512), s>>>(
-          with_ctl ? ctx->ctl : nullptr, ctx->Bt, ctx->d, ctx->ni, ctx->ldj, ctx->ldh, x, clients,
+          with_ctl ? ctx->ctl : nullptr, ctx->Bt, ctx->d, ctx->ni_arr, ctx->ldj, ctx->ldh, x, clients,
           ctx->hcoef, ctx->gcoef, ctx->loss_part, ctx->nblk);
     } else {
       k_margins_cpc<MC_THREADS, 1><<<n_active, MC_THREADS, mc_smem_bytes(ctx->d, ctx->ldj), s>>>(
-          with_ctl ? ctx->ctl : nullptr, ctx->Bt, ctx->d, ctx->ni, ctx->ldj, ctx->ldh, x, clients,
+          with_ctl ? ctx->ctl : nullptr, ctx->Bt, ctx->d, ctx->ni_arr, ctx->ldj, ctx->ldh, x, clients,
           ctx->hcoef, ctx->gcoef, ctx->loss_part, ctx->nblk);
     }
   } else {
     dim3 grid(ctx->nblk, n_active);
     k_margins<<<grid, MB_THREADS, ctx->d * sizeof(double), s>>>(
-        with_ctl ? ctx->ctl : nullptr, ctx->Bt, ctx->d, ctx->ni, ctx->ldj, ctx->ldh, x, clients,
+        with_ctl ? ctx->ctl : nullptr, ctx->Bt, ctx->d, ctx->ni_arr, ctx->ldj, ctx->ldh, x, clients,
         ctx->hcoef, ctx->gcoef, ctx->loss_part, ctx->nblk);
   }
   CKL();
@@ -360,8 +359,8 @@ int launch_margins(Ctx* ctx, cudaStream_t s, const double* x, const int32_t* cli
 int launch_gradient(Ctx* ctx, cudaStream_t s, const double* x, const int32_t* clients,
                     int n_active, bool with_ctl = true) {
   dim3 grid((ctx->d + 7) / 8, n_active);
-  k_gradient<<<grid, 256, 0, s>>>(with_ctl ? ctx->ctl : nullptr, ctx->Bt, ctx->d, ctx->ni,
-                                  ctx->ldj, ctx->ldh, x, ctx->cfg.lam, clients, ctx->gcoef,
+  k_gradient<<<grid, 256, 0, s>>>(with_ctl ? ctx->ctl : nullptr, ctx->Bt, ctx->d, ctx->ni_arr,
+                                  ctx->ldj, ctx->ldh, x, ctx->lam_arr, clients, ctx->gcoef,
                                   ctx->grad);
   CKL();
   return FB_OK;
@@ -386,7 +385,8 @@ int launch_hessian(Ctx* ctx, cudaStream_t s, const int32_t* clients, int n_activ
   lc.numAttrs = pdl_ok(ctx) ? 1 : 0;
   const int32_t* disp = (clients == nullptr && n_active == ctx->n) ? ctx->hess_dispatch : nullptr;
   CK(cudaLaunchKernelEx(&lc, k_hessian<2>, ctx->tmap, static_cast<const DevCtl*>(with_ctl ? ctx->ctl : nullptr),
-                        ctx->d, ctx->ni, ctx->ldh, static_cast<const double*>(ctx->hcoef), ctx->cfg.lam, clients,
+                        ctx->d, static_cast<const int32_t*>(ctx->ni_arr), ctx->ldh,
+                        static_cast<const double*>(ctx->hcoef), static_cast<const double*>(ctx->lam_arr), clients,
                         hest, hest_stride, D, hess_out, ctx->frob_part, ctx->flags,
                         0u /* zero_mask: see mbar_arrive_dep */, static_cast<const double*>(ctx->gcoef),
                         fuse_grad_x, fuse_grad_x ? ctx->grad : nullptr,
@@ -408,8 +408,9 @@ int launch_reduce(Ctx* ctx, cudaStream_t s, const double* x, const int32_t* clie
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   lc.attrs = attr;
   lc.numAttrs = pdl_ok(ctx) ? 1 : 0;
-  CK(cudaLaunchKernelEx(&lc, k_reduce, ctx->ctl, n_active, clients, n_div, ctx->d, ctx->ni, ctx->nblk,
-                        ctx->n_pairs, x, ctx->cfg.lam, static_cast<const double*>(ctx->grad),
+  CK(cudaLaunchKernelEx(&lc, k_reduce, ctx->ctl, n_active, clients, n_div, ctx->d,
+                        static_cast<const int32_t*>(ctx->ni_arr), ctx->nblk, ctx->n_pairs, x,
+                        static_cast<const double*>(ctx->lam_arr), static_cast<const double*>(ctx->grad),
                         static_cast<const double*>(ctx->loss_part),
                         static_cast<const double*>(with_frob ? ctx->frob_part : nullptr),
                         static_cast<const int32_t*>(ctx->flags), ctx->gbar, ctx->f_cli, ctx->shift_cli, ctx->sc,
@@ -579,12 +580,8 @@ int record(Ctx* ctx, EvSlot slot, cudaStream_t s) {
   // per-kernel boundaries only in the instrumented graph: an event-record
   // node between two kernels costs the overlap of their launches (measured
   // 24 us per c0 round for the seven of them)
-  if (!ctx->phase_events && !ctx->direct_pool && slot != EV_START && slot != EV_END) return FB_OK;
+  if (!ctx->phase_events && slot != EV_START && slot != EV_END) return FB_OK;
   ctx->ev_used[slot] = true;
-  if (ctx->direct_pool) {  // direct (non-graph) launches: live events
-    CK(cudaEventRecord(ctx->direct_pool[slot], s));
-    return FB_OK;
-  }
   CK(cudaEventRecordWithFlags(ctx->ev_fixed[slot], s, cudaEventRecordExternal));
   return FB_OK;
 }
@@ -612,17 +609,16 @@ int enqueue_fednl_round(Ctx* ctx) {
   TRY(record(ctx, EV_HESS_END, s));
   // the round reduction: folded into the panel solve's prologue when that
   // kernel runs (its cluster forms the scalars it needs first), else k_reduce
-  static const bool no_fuse = getenv("FB_NO_FUSED_REDUCE") && atoi(getenv("FB_NO_FUSED_REDUCE"));
   const bool opt_a = ctx->cfg.option == FB_OPTION_A;
-  const bool fuse_red = ctx->solve_panels && !no_fuse && !opt_a;
+  const bool fuse_red = ctx->solve_panels && !opt_a;
   CpRed red{};
   if (fuse_red) {
     red.n_active = n;
     red.n_div = n;
-    red.ni = ctx->ni;
+    red.ni = ctx->ni_arr;
+    red.lam = ctx->lam_arr;
     red.nblk = ctx->nblk;
     red.n_pairs = ctx->n_pairs;
-    red.lam = ctx->cfg.lam;
     red.grad = ctx->grad;
     red.loss_part = ctx->loss_part;
     red.frob_part = ctx->frob_part;
@@ -644,10 +640,7 @@ int enqueue_fednl_round(Ctx* ctx) {
   // Under a profiler's injection library (ncu serialises every launch anyway)
   // the launch-completion attribute is not supported: order the compressor
   // after the solve instead.
-  static const bool serial = (getenv("FB_SERIAL_ROUND") && atoi(getenv("FB_SERIAL_ROUND"))) ||
-                             getenv("CUDA_INJECTION64_PATH") != nullptr ||
-                             getenv("NV_NSIGHT_INJECTION_TRANSPORT_TYPE") != nullptr ||
-                             getenv("NV_TPS_LAUNCH_TOKEN") != nullptr;
+  const bool serial = under_profiler();
   CK(cudaEventRecord(ctx->ev_fork, s));
   CK(cudaStreamWaitEvent(ctx->st2, ctx->ev_fork, 0));
   if (opt_a) {  // eigen_clamp_min(H^k, mu) of the pre-fold estimate, then its Cholesky solve
@@ -663,75 +656,84 @@ int enqueue_fednl_round(Ctx* ctx) {
     CK(cudaEventRecord(ctx->ev_solve_launched, s));
   }
   CK(cudaStreamWaitEvent(ctx->st2, ctx->ev_solve_launched, 0));
-  static const bool fold_late = getenv("FB_FOLD_LATE") && atoi(getenv("FB_FOLD_LATE"));
   TRY(record(ctx, EV_COMP_START, ctx->st2));
   // split TopK: the client shift update runs in the fold (K7), which stages
   // every client's entries per position range anyway
   const bool cu_fold = ctx->topk_split && !shd;
   TRY(launch_compress(ctx, ctx->st2, loc, n_loc, nullptr, nullptr, true, true, cu_fold));
   if (shd) {  // every rank folds every client's delta (ascending client id)
-    TRY(gather_clients(ctx, ctx->idx_list, ctx->cap, ncclUint32, ctx->st2));
-    TRY(gather_clients(ctx, ctx->val_list, ctx->cap, ncclFloat64, ctx->st2));
+    if (dense_kind(ctx)) {  // the dense update itself (natural: the rounded values)
+      TRY(gather_clients(ctx, ctx->D, static_cast<size_t>(ctx->w), ncclFloat64, ctx->st2));
+    } else {
+      TRY(gather_clients(ctx, ctx->idx_list, ctx->cap, ncclUint32, ctx->st2));
+      TRY(gather_clients(ctx, ctx->val_list, ctx->cap, ncclFloat64, ctx->st2));
+      TRY(gather_clients(ctx, ctx->rs, ctx->nr + 1, ncclInt32, ctx->st2));
+    }
     TRY(gather_clients(ctx, ctx->count, 1, ncclInt32, ctx->st2));
-    TRY(gather_clients(ctx, ctx->rs, ctx->nr + 1, ncclInt32, ctx->st2));
   }
   TRY(record(ctx, EV_COMP_END, ctx->st2));
   TRY(record(ctx, EV_FOLD_START, ctx->st2));
-  if (!fold_late)
-    TRY(launch_master_fold(ctx, ctx->st2, nullptr, n, dense_kind(ctx) ? ctx->hest : nullptr,
-                           ctx->hmas, ctx->hmas2, cu_fold));
+  // dense kinds: the client shift update rides in the fold over this rank's
+  // clients' rows (every rank folds all clients into H^{k+1})
+  TRY(launch_master_fold(ctx, ctx->st2, nullptr, n, dense_kind(ctx) ? ctx->hest : nullptr,
+                         ctx->hmas, ctx->hmas2, cu_fold));
   TRY(record(ctx, EV_FOLD_END, ctx->st2));
   CK(cudaEventRecord(ctx->ev_join, ctx->st2));
   TRY(record(ctx, EV_SOLVE_END, s));
   int launches = ctx->topk_split ? 9 : 8;
   if (ls) {
-    dim3 grid(ctx->ls_nblk, n);
-    k_ls_trials<<<grid, MARGIN_THREADS, LS_BATCH * ctx->d * sizeof(double), s>>>(
-        ctx->ctl, ctx->Bt, ctx->d, ctx->ni, ctx->ldj, ctx->x, ctx->pvec, ctx->steps_table, n,
+    // FedNL-LS: batches of LS_BATCH Armijo trials as the body of a
+    // while-conditional node; k_ls_decide keeps the loop going until a trial
+    // passes, or raises ST_LINE_SEARCH past s = 60 (algorithms.py:284-311)
+    cudaStreamCaptureStatus cst;
+    cudaGraph_t cg = nullptr;
+    const cudaGraphNode_t* deps = nullptr;
+    size_t ndeps = 0;
+    CK(cudaStreamGetCaptureInfo(s, &cst, nullptr, &cg, &deps, &ndeps));
+    cudaGraphConditionalHandle loop;
+    CK(cudaGraphConditionalHandleCreate(&loop, cg, 1, cudaGraphCondAssignDefault));
+    cudaGraphNodeParams cp{};
+    cp.type = cudaGraphNodeTypeConditional;
+    cp.conditional.handle = loop;
+    cp.conditional.type = cudaGraphCondTypeWhile;
+    cp.conditional.size = 1;
+    cudaGraphNode_t wnode;
+    CK(cudaGraphAddNode(&wnode, cg, deps, ndeps, &cp));
+    cudaGraph_t body = cp.conditional.phGraph_out[0];
+    CK(cudaStreamBeginCaptureToGraph(ctx->st_body, body, nullptr, nullptr, 0,
+                                     cudaStreamCaptureModeThreadLocal));
+    dim3 grid(ctx->ls_nblk, n_loc);
+    k_ls_trials<<<grid, MARGIN_THREADS, LS_BATCH * ctx->d * sizeof(double), ctx->st_body>>>(
+        ctx->ctl, ctx->Bt, ctx->d, ctx->ni_arr, ctx->ldj, loc, ctx->x, ctx->pvec, ctx->steps_table,
         ctx->trial_x, ctx->ls_loss_part, ctx->ls_nblk);
-    CKL();
-    k_ls_decide<<<1, 256, 0, s>>>(ctx->ctl, ctx->d, n, ctx->ni, ctx->ls_nblk, ctx->cfg.lam,
-                                  ctx->cfg.ls_c, ctx->steps_table, ctx->trial_x,
-                                  ctx->ls_loss_part, ctx->sc, ctx->x_new, LS_BATCH, ctx->gbar,
-                                  ctx->pvec);
-    CKL();
+    cudaError_t e1 = cudaGetLastError();
+    int r1 = FB_OK;
+    if (e1 == cudaSuccess && shd)  // the trials' per-client loss partials of every rank
+      r1 = gather_clients(ctx, ctx->ls_loss_part, static_cast<size_t>(LS_BATCH) * ctx->ls_nblk,
+                          ncclFloat64, ctx->st_body);
+    if (e1 == cudaSuccess && r1 == FB_OK) {
+      k_ls_decide<<<1, 256, 0, ctx->st_body>>>(ctx->ctl, ctx->d, n, ctx->ni_arr, ctx->lam_arr,
+                                               ctx->ls_nblk, ctx->cfg.ls_c, ctx->steps_table,
+                                               ctx->trial_x, ctx->ls_loss_part, ctx->sc, ctx->x_new,
+                                               LS_BATCH, ctx->gbar, ctx->pvec, loop);
+      e1 = cudaGetLastError();
+    }
+    cudaGraph_t body_out = body;
+    const cudaError_t e2 = cudaStreamEndCapture(ctx->st_body, &body_out);
+    if (r1 != FB_OK) return r1;
+    CK(e1);
+    CK(e2);
+    CK(cudaStreamUpdateCaptureDependencies(s, &wnode, 1, cudaStreamSetCaptureDependencies));
     launches += 2;
   }
   CK(cudaStreamWaitEvent(s, ctx->ev_join, 0));
-  if (fold_late)
-    TRY(launch_master_fold(ctx, s, nullptr, n, dense_kind(ctx) ? ctx->hest : nullptr, ctx->hmas,
-                           ctx->hmas2, cu_fold));
   k_finish<<<finish_grid(ctx), 256, 0, s>>>(ctx->ctl, ctx->d, n, n, nullptr, ctx->x, ctx->x_new, 1,
-                                            ctx->count, ctx->row_counts, ctx->row_ls, ctx->hmas2,
-                                            ctx->hmas, ctx->w);
+                                            ctx->count, ctx->row_counts, ctx->row_ls, ctx->row_grad,
+                                            ctx->hmas2, ctx->hmas, ctx->w);
   CKL();
   TRY(record(ctx, EV_END, s));
   ctx->launches_per_round = launches;
   return FB_OK;
-}
-
-// post-line-search tail of an LS round (fold + finish), launched directly by
-// the host after it drove extra trial batches
-int enqueue_ls_tail(Ctx* ctx) {
-  // the fold of this round already ran (it does not depend on the line
-  // search); only the H^{k+1} copy and the round epilogue remain
-  cudaStream_t s = ctx->st;
-  k_finish<<<finish_grid(ctx), 256, 0, s>>>(ctx->ctl, ctx->d, ctx->n, ctx->n, nullptr, ctx->x,
-                                            ctx->x_new, 1, ctx->count, ctx->row_counts, ctx->row_ls,
-                                            ctx->hmas2, ctx->hmas, ctx->w);
-  CKL();
-  return FB_OK;
-}
-
-__global__ void k_check_finite(DevCtl* ctl, int d, const double* x) {
-  if (ctl->halt) return;
-  __shared__ int bad;
-  if (threadIdx.x == 0) bad = 0;
-  __syncthreads();
-  for (int a = threadIdx.x; a < d; a += blockDim.x)
-    if (!isfinite(x[a])) bad = 1;
-  __syncthreads();
-  if (threadIdx.x == 0 && bad) raise_status(ctl, ST_DIVERGED);
 }
 
 int enqueue_pp_round(Ctx* ctx) {
@@ -744,10 +746,7 @@ int enqueue_pp_round(Ctx* ctx) {
   // (algorithms.py:422-433) into x_new (x <- x_new after the join).  The
   // solve's cluster is launched first; the probes wait for its launch
   // completion (as the FedNL round's compressor does).
-  static const bool pp_serial = (getenv("FB_PP_SERIAL") && atoi(getenv("FB_PP_SERIAL"))) ||
-                                getenv("CUDA_INJECTION64_PATH") != nullptr ||
-                                getenv("NV_NSIGHT_INJECTION_TRANSPORT_TYPE") != nullptr ||
-                                getenv("NV_TPS_LAUNCH_TOKEN") != nullptr;
+  const bool pp_serial = under_profiler();
   TRY(launch_solve(ctx, s, ctx->hmas, ctx->pp_shift, ctx->gvec, nullptr, ctx->pvec, ctx->x_new, 1, 0,
                    nullptr, pp_serial ? nullptr : ctx->ev_solve_launched));
   cudaStream_t sp = pp_serial ? s : ctx->st2;
@@ -758,13 +757,14 @@ int enqueue_pp_round(Ctx* ctx) {
   TRY(launch_margins(ctx, sp, ctx->x, nullptr, n));
   TRY(launch_gradient(ctx, sp, ctx->x, nullptr, n));
   TRY(launch_reduce(ctx, sp, ctx->x, nullptr, n, n, false, ctx->row_grad, ctx->row_f));
-  k_check_finite<<<1, 256, 0, s>>>(ctx->ctl, ctx->d, ctx->x_new);
-  CKL();
   if (!pp_serial) {
     CK(cudaEventRecord(ctx->ev_join, sp));
     CK(cudaStreamWaitEvent(s, ctx->ev_join, 0));
   }
-  CK(cudaMemcpyAsync(ctx->x, ctx->x_new, sizeof(double) * ctx->d, cudaMemcpyDeviceToDevice, s));
+  // the stop rule on the probe row, then x <- x_new (or DivergenceError)
+  k_pp_advance<<<1, 256, 0, s>>>(ctx->ctl, ctx->d, n, ctx->x, ctx->x_new, ctx->row_grad,
+                                 ctx->row_counts, ctx->row_ls);
+  CKL();
   TRY(record(ctx, EV_SOLVE_END, s));
   // participants' oracle at x_new (algorithms.py:240-249)
   CK(cudaMemsetAsync(ctx->flags, 0, sizeof(int32_t) * n, s));
@@ -795,7 +795,7 @@ int enqueue_pp_round(Ctx* ctx) {
   TRY(launch_master_fold(ctx, s, ctx->subset, tau, nullptr, ctx->hmas, ctx->hmas));
   TRY(record(ctx, EV_FOLD_END, s));
   k_finish<<<1, 256, 0, s>>>(ctx->ctl, ctx->d, n, tau, ctx->subset, ctx->x, nullptr, 0, ctx->count,
-                             ctx->row_counts, ctx->row_ls);
+                             ctx->row_counts, ctx->row_ls, nullptr);
   CKL();
   TRY(record(ctx, EV_END, s));
   ctx->launches_per_round = ctx->topk_split ? 17 : 16;
@@ -835,7 +835,10 @@ int build_graph(Ctx* ctx, bool phase_events) {
   CK(cudaGraphGetNodes(g, nodes.data(), &nn));
   for (auto nd : nodes) {
     cudaGraphNodeType ty;
-    CK(cudaGraphNodeGetType(nd, &ty));
+    if (cudaGraphNodeGetType(nd, &ty) != cudaSuccess) {  // (the LS loop's conditional node)
+      cudaGetLastError();
+      continue;
+    }
     if (ty != cudaGraphNodeTypeEventRecord) continue;
     cudaEvent_t ev;
     CK(cudaGraphEventRecordNodeGetEvent(nd, &ev));
@@ -860,7 +863,7 @@ int status_to_code(int32_t code) {
     case ST_TOPLEK_ZERO: return FB_ERR_INVALID;
     case ST_DIVERGED: return FB_ERR_DIVERGED;
     case ST_LINE_SEARCH: return FB_ERR_LINE_SEARCH;
-    case ST_LS_PENDING: return FB_ERR_LS_PENDING;
+    case ST_STOPPED: return FB_OK;
     case ST_EIGEN: return FB_ERR_EIGEN;
     default: return FB_ERR_CUDA;
   }
@@ -884,6 +887,14 @@ int clear_status(Ctx* ctx) {
 // C ABI
 // ======================================================================
 extern "C" {
+
+int fb_abi_sizes(int32_t* out3) {
+  if (!out3) return invalid(nullptr, "null argument");
+  out3[0] = static_cast<int32_t>(sizeof(fb_config));
+  out3[1] = static_cast<int32_t>(sizeof(fb_status));
+  out3[2] = static_cast<int32_t>(sizeof(fb_profile));
+  return FB_OK;
+}
 
 const char* fb_last_error(void* handle) {
   Ctx* ctx = static_cast<Ctx*>(handle);
@@ -922,6 +933,8 @@ int fb_create(const fb_config* cfg_in, void** out) {
   if (sparse && (c.k < 1 || c.k > w)) return invalid(nullptr, "k out of range");
   if (c.algorithm == FB_ALG_PP && (c.tau < 1 || c.tau > c.n_clients))
     return invalid(nullptr, "tau out of range");
+  if (c.topk_path < FB_TOPK_PATH_AUTO || c.topk_path > FB_TOPK_PATH_SPLIT)
+    return invalid(nullptr, "bad topk_path");
   if (c.kind == FB_KIND_TOPLEK && w > 8192)
     return invalid(nullptr, "toplek with d(d+1)/2 > 8192 is outside this build's envelope");
   if (c.kind == FB_KIND_RANDK && std::min<int64_t>(w, 2 * static_cast<int64_t>(c.k)) > 12000)
@@ -961,7 +974,6 @@ int fb_create(const fb_config* cfg_in, void** out) {
   // 6 CTAs below d = 512 leave the per-client compressor (one CTA per SM)
   // enough SMs to run in a single wave next to the solve
   ctx->solve_cs = c.d < 128 ? 1 : (c.d < 512 ? 6 : CH_MAX_CLUSTER);
-  if (const char* e = getenv("FB_SOLVE_CLUSTER")) ctx->solve_cs = std::max(1, std::min(8, atoi(e)));
   ctx->solve_nb = solve_panel_bytes<32>(c.d) <= 190 * 1024 ? 32 : 16;
   {
     // panel-owning solve: one or two 32-column panels per CTA of a portable
@@ -971,8 +983,7 @@ int fb_create(const fb_config* cfg_in, void** out) {
     ctx->cp_cs = (npan + ctx->cp_kp - 1) / ctx->cp_kp;
     // (three panels or fewer: the cluster-redundant solver is faster)
     ctx->solve_panels = npan >= 4 && c.d <= CP_MAX_D && ctx->cp_cs <= CH_MAX_CLUSTER &&
-                        static_cast<size_t>(ctx->cp_kp) * cp_panel_bytes(c.d) <= CP_DYN_SMEM_MAX &&
-                        !(getenv("FB_SOLVE_OLD") && atoi(getenv("FB_SOLVE_OLD")));
+                        static_cast<size_t>(ctx->cp_kp) * cp_panel_bytes(c.d) <= CP_DYN_SMEM_MAX;
   }
   ctx->solve_smem = ctx->solve_nb == 32 ? solve_panel_bytes<32>(c.d) : solve_panel_bytes<16>(c.d);
   int rc = FB_OK;
@@ -1009,6 +1020,7 @@ int fb_create(const fb_config* cfg_in, void** out) {
   }
   CKC(cudaStreamCreateWithFlags(&ctx->st, cudaStreamNonBlocking));
   CKC(cudaStreamCreateWithFlags(&ctx->st2, cudaStreamNonBlocking));
+  CKC(cudaStreamCreateWithFlags(&ctx->st_body, cudaStreamNonBlocking));
   CKC(cudaEventCreateWithFlags(&ctx->ev_fork, cudaEventDisableTiming));
   CKC(cudaEventCreateWithFlags(&ctx->ev_join, cudaEventDisableTiming));
   CKC(cudaEventCreateWithFlags(&ctx->ev_solve_launched, cudaEventDisableTiming));
@@ -1055,15 +1067,14 @@ int fb_create(const fb_config* cfg_in, void** out) {
   const size_t wn = static_cast<size_t>(w) * n;
   // one-pass sampled-window TopK from TKST_MINW up (c0: w = 45,451): one
   // read of D plus candidate work beats the shared-memory radix's passes
-  const char* ts_env = getenv("FB_TOPK_STREAM");
   const bool stream_topk = c.kind == FB_KIND_TOPK && w <= TKST_MAXW &&
-                           (ts_env ? atoi(ts_env) != 0 : (w > TKS_MAXW || w >= TKST_MINW));
+                           (w > TKS_MAXW || w >= TKST_MINW);
   ctx->topk_stream = stream_topk;
   // the stream as many small CTAs (about two waves of 8 per SM) + a select
-  // kernel; FB_TOPK_SPLIT=0 keeps the one-CTA-per-client k_topk_stream
-  const char* sp_env = getenv("FB_TOPK_SPLIT");
-  ctx->topk_split = stream_topk && (sp_env ? atoi(sp_env) != 0
-                                            : static_cast<int64_t>(w) * n >= (int64_t{1} << 26));
+  // kernel when n * w is large (c4); topk_path pins either variant (tests)
+  ctx->topk_split = stream_topk && (c.topk_path == FB_TOPK_PATH_AUTO
+                                        ? static_cast<int64_t>(w) * n >= (int64_t{1} << 26)
+                                        : c.topk_path == FB_TOPK_PATH_SPLIT);
   size_t cand_slots = stream_topk ? static_cast<size_t>(n) * TKST_CAP : 1;
   if (ctx->topk_split) {
     // positions per CTA: one wave of two CTAs per SM when that is 8..64
@@ -1083,6 +1094,7 @@ int fb_create(const fb_config* cfg_in, void** out) {
   }
   const int tau = ctx->tau;
   if (dalloc(ctx, &ctx->ctl, 1) || dalloc(ctx, &ctx->Bt, static_cast<size_t>(n) * d * ctx->ldj) ||
+      dalloc(ctx, &ctx->ni_arr, n) || dalloc(ctx, &ctx->lam_arr, n) ||
       dalloc(ctx, &ctx->x, d) || dalloc(ctx, &ctx->x_new, d) || dalloc(ctx, &ctx->pvec, d) ||
       dalloc(ctx, &ctx->zbuf, d) ||
       dalloc(ctx, &ctx->hcoef, static_cast<size_t>(n) * ctx->ldh) ||
@@ -1127,6 +1139,13 @@ int fb_create(const fb_config* cfg_in, void** out) {
       dalloc(ctx, &ctx->row_counts, static_cast<size_t>(ROW_CHUNK) * n) ||
       dalloc(ctx, &ctx->row_ls, ROW_CHUNK)) {
     return fail(FB_ERR_CUDA);
+  }
+  {  // every client n_i = n_samples, lambda = lam until fb_upload_shards_ex says otherwise
+    std::vector<int32_t> nis(n, c.n_samples);
+    std::vector<double> lams(n, c.lam);
+    CKC(cudaMemcpyAsync(ctx->ni_arr, nis.data(), sizeof(int32_t) * n, cudaMemcpyHostToDevice, ctx->st));
+    CKC(cudaMemcpyAsync(ctx->lam_arr, lams.data(), sizeof(double) * n, cudaMemcpyHostToDevice, ctx->st));
+    CKC(cudaStreamSynchronize(ctx->st));
   }
   double steps[64];
   for (int i = 0; i < 64; ++i) steps[i] = c.ls_steps_table[i <= 60 ? i : 60];
@@ -1189,9 +1208,8 @@ int fb_create(const fb_config* cfg_in, void** out) {
   // different cost (the group's costliest tiles, then its cheapest), so the
   // co-resident CTAs do not run in lockstep and one's epilogue overlaps the
   // other's DMMA main loop; the rest of the order is unchanged.
-  static const int hess_order = getenv("FB_HESS_ORDER") ? atoi(getenv("FB_HESS_ORDER")) : 1;
   std::vector<int32_t> disp;
-  if (hess_order == 1) {
+  {
     const int P = ctx->n_pairs, n_all = ctx->n, grp = hess_group(ctx);
     disp.resize(static_cast<size_t>(n_all) * P);
     for (int L = 0; L < n_all * P; ++L) {  // the kernel's default mapping
@@ -1238,6 +1256,7 @@ void fb_destroy(void* handle) {
   if (ctx->ev_solve_launched) cudaEventDestroy(ctx->ev_solve_launched);
   if (ctx->st) cudaStreamDestroy(ctx->st);
   if (ctx->st2) cudaStreamDestroy(ctx->st2);
+  if (ctx->st_body) cudaStreamDestroy(ctx->st_body);
   delete ctx;
 }
 
@@ -1313,8 +1332,8 @@ int fb_set_shard(void* handle, int32_t world, int32_t rank, const uint8_t* nccl_
   if (!ctx || !nccl_id) return invalid(ctx, "null argument");
   if (world < 1 || rank < 0 || rank >= world) return invalid(ctx, "bad world / rank");
   if (ctx->uploaded || ctx->initialised) return invalid(ctx, "fb_set_shard must precede fb_upload_shards");
-  if (ctx->cfg.algorithm != FB_ALG_FEDNL)
-    return fail_code(ctx, FB_ERR_UNSUPPORTED, "client sharding is implemented for FedNL (not LS / PP)");
+  if (ctx->cfg.algorithm == FB_ALG_PP)
+    return fail_code(ctx, FB_ERR_UNSUPPORTED, "client sharding is implemented for FedNL and FedNL-LS (not PP)");
   NcclApi& api = nccl_api();
   if (!api.ok) return invalid(ctx, "libnccl.so.2 could not be loaded");
   const int n = ctx->n;
@@ -1329,7 +1348,12 @@ int fb_set_shard(void* handle, int32_t world, int32_t rank, const uint8_t* nccl_
       dalloc(ctx, &ctx->frob_part, n_pad * ctx->n_pairs) || dalloc(ctx, &ctx->flags, n_pad) ||
       dalloc(ctx, &ctx->idx_list, n_pad * ctx->cap) || dalloc(ctx, &ctx->val_list, n_pad * ctx->cap) ||
       dalloc(ctx, &ctx->count, n_pad) || dalloc(ctx, &ctx->rs, n_pad * (ctx->nr + 1)) ||
+      dalloc(ctx, &ctx->ls_loss_part, n_pad * LS_BATCH * ctx->ls_nblk) ||
       dalloc(ctx, &ctx->local_clients, std::max(1, ctx->c_hi - ctx->c_lo)))
+    return FB_ERR_CUDA;
+  // dense kinds all-gather D every round; exact init all-gathers H_i(x0)
+  if (dense_kind(ctx) && dalloc(ctx, &ctx->D, n_pad * static_cast<size_t>(ctx->w) + 2)) return FB_ERR_CUDA;
+  if (ctx->cfg.hessian_init == FB_INIT_EXACT && dalloc(ctx, &ctx->hest, n_pad * static_cast<size_t>(ctx->w)))
     return FB_ERR_CUDA;
   std::vector<int32_t> loc(std::max(1, ctx->c_hi - ctx->c_lo));
   for (int c = ctx->c_lo; c < ctx->c_hi; ++c) loc[c - ctx->c_lo] = c;
@@ -1351,12 +1375,31 @@ int fb_set_shard(void* handle, int32_t world, int32_t rank, const uint8_t* nccl_
 }
 
 int fb_upload_shards(void* handle, const double* const* bmats) {
+  return fb_upload_shards_ex(handle, bmats, nullptr, nullptr);
+}
+
+int fb_upload_shards_ex(void* handle, const double* const* bmats, const int32_t* n_samples,
+                        const double* lam) {
   Ctx* ctx = static_cast<Ctx*>(handle);
   if (!ctx || !bmats) return invalid(ctx, "null argument");
+  const int d = ctx->d, n = ctx->n;
   for (int c = ctx->c_lo; c < ctx->c_hi; ++c)
     if (!bmats[c]) return invalid(ctx, "null shard pointer");
-  const int d = ctx->d, ni = ctx->ni, n = ctx->n;
-  const size_t bytes = static_cast<size_t>(d) * ni * sizeof(double);
+  std::vector<int32_t> nis(n, ctx->ni);
+  std::vector<double> lams(n, ctx->cfg.lam);
+  for (int c = 0; c < n; ++c) {
+    if (n_samples) {
+      if (n_samples[c] < 1 || n_samples[c] > ctx->ni)
+        return invalid(ctx, "shard n_samples must be in [1, fb_config.n_samples]");
+      nis[c] = n_samples[c];
+    }
+    if (lam) lams[c] = lam[c];
+  }
+  CK(cudaMemcpyAsync(ctx->ni_arr, nis.data(), sizeof(int32_t) * n, cudaMemcpyHostToDevice, ctx->st));
+  CK(cudaMemcpyAsync(ctx->lam_arr, lams.data(), sizeof(double) * n, cudaMemcpyHostToDevice, ctx->st));
+  CK(cudaStreamSynchronize(ctx->st));
+  const int ni = ctx->ni;
+  const size_t bytes = static_cast<size_t>(d) * ni * sizeof(double);  // staging slot: the largest shard
   UploadPool& pool = upload_pool();
   std::lock_guard<std::mutex> guard(pool.mu);
   const int L = std::max(1, std::min(UPLOAD_LANES, n));
@@ -1392,14 +1435,15 @@ int fb_upload_shards(void* handle, const double* const* bmats) {
     int slot = 0;
     for (int c = ctx->c_lo + l; c < ctx->c_hi && !failed.load(); c += L, slot ^= 1) {
       cudaError_t e = cudaEventSynchronize(ln.done[slot]);  // slot free again
+      const size_t cb = static_cast<size_t>(d) * nis[c] * sizeof(double);
       if (e == cudaSuccess) {
-        std::memcpy(ln.host[slot], bmats[c], bytes);
-        e = cudaMemcpyAsync(ln.dev[slot], ln.host[slot], bytes, cudaMemcpyHostToDevice, ln.st);
+        std::memcpy(ln.host[slot], bmats[c], cb);
+        e = cudaMemcpyAsync(ln.dev[slot], ln.host[slot], cb, cudaMemcpyHostToDevice, ln.st);
       }
       if (e == cudaSuccess) {
         dim3 grid((ctx->ldj + 31) / 32, (d + 31) / 32);
         k_transpose_shard<<<grid, dim3(32, 8), 0, ln.st>>>(
-            ln.dev[slot], ctx->Bt + static_cast<size_t>(c) * d * ctx->ldj, d, ni, ctx->ldj);
+            ln.dev[slot], ctx->Bt + static_cast<size_t>(c) * d * ctx->ldj, d, nis[c], ctx->ldj);
         e = cudaGetLastError();
       }
       if (e == cudaSuccess) e = cudaEventRecord(ln.done[slot], ln.st);
@@ -1442,18 +1486,23 @@ int fb_init_state(void* handle, const double* x0) {
   else CK(cudaMemsetAsync(ctx->x, 0, sizeof(double) * d, s));
   CK(cudaMemsetAsync(ctx->gvec, 0, sizeof(double) * d, s));
   CK(cudaMemsetAsync(ctx->pp_shift, 0, sizeof(double), s));
-  const double diag = (c.hessian_init == FB_INIT_LAMBDA_IDENTITY) ? c.lam : 0.0;
+  const bool lam_id = c.hessian_init == FB_INIT_LAMBDA_IDENTITY;
   dim3 gi(static_cast<unsigned>((ctx->w + 255) / 256), n + 1);
-  k_init_diag<<<gi, 256, 0, s>>>(ctx->w, n, diag, ctx->hest, ctx->hmas);
+  k_init_diag<<<gi, 256, 0, s>>>(ctx->w, n, lam_id ? ctx->lam_arr : nullptr, lam_id ? c.lam : 0.0,
+                                 ctx->hest, ctx->hmas);
   CKL();
   const bool pp = c.algorithm == FB_ALG_PP;
   if (c.hessian_init == FB_INIT_EXACT || pp) {
     CK(cudaMemsetAsync(ctx->flags, 0, sizeof(int32_t) * n, s));
-    TRY(launch_margins(ctx, s, ctx->x, nullptr, n));
-    TRY(launch_gradient(ctx, s, ctx->x, nullptr, n));
+    const bool shd = sharded(ctx);
+    const int32_t* loc = shd ? ctx->local_clients : nullptr;
+    const int n_loc = shd ? ctx->c_hi - ctx->c_lo : n;
+    TRY(launch_margins(ctx, s, ctx->x, loc, n_loc));
+    TRY(launch_gradient(ctx, s, ctx->x, loc, n_loc));
     if (c.hessian_init == FB_INIT_EXACT) {
       // D = H - 0 = H exactly; H_i^0 = H_i(x0), master = mean (algorithms.py:207-209, 336-341)
-      TRY(launch_hessian(ctx, s, nullptr, n, ctx->zeros_w, 0, ctx->hest, nullptr));
+      TRY(launch_hessian(ctx, s, loc, n_loc, ctx->zeros_w, 0, ctx->hest, nullptr));
+      if (shd) TRY(gather_clients(ctx, ctx->hest, static_cast<size_t>(ctx->w), ncclFloat64, s));
       k_mean_packed<<<static_cast<unsigned>((ctx->w + 255) / 256), 256, 0, s>>>(ctx->w, n,
                                                                                ctx->hest, ctx->hmas);
       CKL();
@@ -1486,10 +1535,12 @@ int fb_run_rounds(void* handle, int32_t first_round, int32_t count, double stop_
   const int n = ctx->n;
   DevCtl h;
   TRY(read_status(ctx, &h));
-  if (h.halt) return status_to_code(h.code);
-  if (h.round != first_round) {
-    h.round = first_round;
+  if (h.code == ST_STOPPED) {  // a previous call's stop: the run may continue
+    h.code = 0;
+    h.halt = 0;
   }
+  if (h.halt) return status_to_code(h.code);
+  h.stop_gn = stop_grad_norm;  // the stop rule runs on the device (k_finish / k_pp_advance)
   cudaEvent_t t0;
   CK(cudaEventCreate(&t0));
   CK(cudaEventRecord(t0, s));
@@ -1503,8 +1554,7 @@ int fb_run_rounds(void* handle, int32_t first_round, int32_t count, double stop_
     ctx->ev_ends.resize(ROW_CHUNK);
     for (auto& e : ctx->ev_ends) CK(cudaEventCreate(&e));
   }
-  static const bool no_graph = getenv("FB_NO_GRAPH") && atoi(getenv("FB_NO_GRAPH"));
-  if ((timed || no_graph) && ctx->ev_pool.empty()) {  // per-kernel event slots, on first use
+  if (timed && ctx->ev_pool.empty()) {  // per-kernel event slots, on first use
     ctx->ev_pool.resize(static_cast<size_t>(ROW_CHUNK) * EV_COUNT);
     for (auto& e : ctx->ev_pool) CK(cudaEventCreate(&e));
   }
@@ -1521,42 +1571,10 @@ int fb_run_rounds(void* handle, int32_t first_round, int32_t count, double stop_
             CK(cudaGraphExecEventRecordNodeSetEvent(ctx->gexec, ctx->ev_node[e],
                                                     ctx->ev_pool[static_cast<size_t>(i) * EV_COUNT + e]));
       }
-      if (no_graph) {  // diagnostics: the same round body, launched directly
-        ctx->direct_pool = &ctx->ev_pool[static_cast<size_t>(i) * EV_COUNT];
-        const int r2 = (ctx->cfg.algorithm == FB_ALG_PP) ? enqueue_pp_round(ctx) : enqueue_fednl_round(ctx);
-        ctx->direct_pool = nullptr;
-        if (r2 != FB_OK) return r2;
-      } else {
-        CK(cudaGraphLaunch(ctx->gexec, s));
-      }
+      CK(cudaGraphLaunch(ctx->gexec, s));
       CK(cudaEventRecord(ends[i], s));
     }
-    // drive line-search continuations (rare: no trial in the first batch passed)
     TRY(read_status(ctx, &h));
-    while (h.code == ST_LS_PENDING) {
-      const int r = h.round;
-      dim3 grid(ctx->ls_nblk, n);
-      k_ls_trials<<<grid, MARGIN_THREADS, LS_BATCH * ctx->d * sizeof(double), s>>>(
-          ctx->ctl, ctx->Bt, ctx->d, ctx->ni, ctx->ldj, ctx->x, ctx->pvec, ctx->steps_table, n,
-          ctx->trial_x, ctx->ls_loss_part, ctx->ls_nblk);
-      CKL();
-      k_ls_decide<<<1, 256, 0, s>>>(ctx->ctl, ctx->d, n, ctx->ni, ctx->ls_nblk, ctx->cfg.lam,
-                                    ctx->cfg.ls_c, ctx->steps_table, ctx->trial_x,
-                                    ctx->ls_loss_part, ctx->sc, ctx->x_new, LS_BATCH, ctx->gbar,
-                                    ctx->pvec);
-      CKL();
-      TRY(read_status(ctx, &h));
-      if (h.code == 0 && !h.halt) {
-        TRY(enqueue_ls_tail(ctx));
-        const int next = r + 1;
-        const int slot_done = next - (first_round + done);
-        for (int i = slot_done; i < chunk; ++i) {
-          CK(cudaGraphLaunch(ctx->gexec, s));
-          CK(cudaEventRecord(ends[i], s));
-        }
-        TRY(read_status(ctx, &h));
-      }
-    }
     const int completed = h.round - (first_round + done);
     CK(cudaMemcpyAsync(rg.data(), ctx->row_grad, sizeof(double) * chunk, cudaMemcpyDeviceToHost, s));
     CK(cudaMemcpyAsync(rf.data(), ctx->row_f, sizeof(double) * chunk, cudaMemcpyDeviceToHost, s));
@@ -1605,6 +1623,11 @@ int fb_run_rounds(void* handle, int32_t first_round, int32_t count, double stop_
     }
     if (stop) break;
     done += take;
+    if (h.code == ST_STOPPED) {  // cannot happen without a row <= stop_grad_norm
+      rc = FB_ERR_CUDA;
+      ctx->err = "device stop without a stopping row";
+      break;
+    }
     if (h.code != 0) {
       rc = status_to_code(h.code);
       break;
@@ -1617,6 +1640,7 @@ int fb_run_rounds(void* handle, int32_t first_round, int32_t count, double stop_
   }
   cudaGetLastError();
   cudaEventDestroy(t0);
+  if (rc == FB_OK && h.code == ST_STOPPED) TRY(clear_status(ctx));  // stopped, not failed
   if (timed && timed_rounds > 0) {
     fb_profile& p = ctx->prof;
     p.rounds = timed_rounds;
@@ -1859,8 +1883,8 @@ int fb_oracle_eval(void* handle, const double* x, double* f, double* grad, doubl
   TRY(launch_gradient(ctx, s, ctx->x_new, nullptr, n));
   if (hess_packed) TRY(launch_hessian(ctx, s, nullptr, n, ctx->zeros_w, 0, ctx->D, nullptr));
   // f via the reduction kernel without touching the row buffers or status
-  k_reduce<<<reduce_grid(d), RED_THREADS, 0, s>>>(ctx->ctl, n, nullptr, n, d, ctx->ni, ctx->nblk, ctx->n_pairs,
-                              ctx->x_new, ctx->cfg.lam, ctx->grad, ctx->loss_part, nullptr,
+  k_reduce<<<reduce_grid(d), RED_THREADS, 0, s>>>(ctx->ctl, n, nullptr, n, d, ctx->ni_arr, ctx->nblk, ctx->n_pairs,
+                              ctx->x_new, ctx->lam_arr, ctx->grad, ctx->loss_part, nullptr,
                               ctx->flags, ctx->gbar, ctx->f_cli, ctx->shift_cli, ctx->sc, nullptr,
                               nullptr, nullptr, 0);
   CKL();

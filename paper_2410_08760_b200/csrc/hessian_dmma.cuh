@@ -107,8 +107,9 @@ __device__ __forceinline__ void hess_consume(HessSmem& sm, bool diag, int nk, in
 // MINB = CTAs per SM the register budget is cut for (2 is used).
 template <int MINB>
 __global__ void __launch_bounds__(HTHREADS, MINB) k_hessian(
-    const __grid_constant__ CUtensorMap tmap_b, const DevCtl* __restrict__ ctl, int d, int ni,
-    int ldh, const double* __restrict__ hcoef, double lam, const int32_t* __restrict__ clients,
+    const __grid_constant__ CUtensorMap tmap_b, const DevCtl* __restrict__ ctl, int d,
+    const int32_t* __restrict__ ni_arr, int ldh, const double* __restrict__ hcoef,
+    const double* __restrict__ lam_arr, const int32_t* __restrict__ clients,
     const double* __restrict__ hest, int64_t hest_stride, double* __restrict__ D,
     double* __restrict__ hess_out, double* __restrict__ frob_part, int32_t* __restrict__ flags,
     uint32_t zero_mask, const double* __restrict__ gcoef, const double* __restrict__ x,
@@ -158,7 +159,8 @@ __global__ void __launch_bounds__(HTHREADS, MINB) k_hessian(
   const bool consumer = warp < HCONS && !(diag && rowbase > colbase);
   const bool grad_warp = fuse_grad && warp < HCONS && rowbase > colbase;
 
-  const int nk = (ni + HKC - 1) / HKC;
+  const int nk = (ni_arr[c] + HKC - 1) / HKC;  // this client's samples (ragged shards)
+  const double lam = lam_arr[c];
   const double* hrow = hcoef + static_cast<int64_t>(c) * ldh;
   const double* grow = fuse_grad ? gcoef + static_cast<int64_t>(c) * ldh : nullptr;
   const uint32_t stage_bytes =

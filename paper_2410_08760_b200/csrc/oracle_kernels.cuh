@@ -40,7 +40,8 @@ __device__ __forceinline__ double softplus_neg(double m) {
 constexpr int MB_SAMPLES = 64;
 constexpr int MB_THREADS = 256;
 __global__ void __launch_bounds__(MB_THREADS) k_margins(
-    const DevCtl* __restrict__ ctl, const double* __restrict__ Bt, int d, int ni, int ldj,
+    const DevCtl* __restrict__ ctl, const double* __restrict__ Bt, int d,
+    const int32_t* __restrict__ ni_arr, int ldj,
     int ldh, const double* __restrict__ x, const int32_t* __restrict__ clients,
     double* __restrict__ hcoef, double* __restrict__ gcoef, double* __restrict__ loss_part,
     int nblk) {
@@ -51,6 +52,7 @@ __global__ void __launch_bounds__(MB_THREADS) k_margins(
   __shared__ double part[8][MB_SAMPLES + 2];
   __shared__ double red[2];
   const int c = client_of(clients, blockIdx.y);
+  const int ni = ni_arr[c];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   for (int a = threadIdx.x; a < d; a += blockDim.x) xs[a] = x[a];
   __syncthreads();
@@ -144,7 +146,8 @@ constexpr size_t MC_SMEM_MAX = 96 * 1024;
 // sample pairs [part * SPS, (part + 1) * SPS) of SPS = mc_split_pairs).
 template <int NT, int NS>
 __global__ void __launch_bounds__(NT, NS > 1 ? 2 : 1) k_margins_cpc(
-    const DevCtl* __restrict__ ctl, const double* __restrict__ Bt, int d, int ni, int ldj,
+    const DevCtl* __restrict__ ctl, const double* __restrict__ Bt, int d,
+    const int32_t* __restrict__ ni_arr, int ldj,
     int ldh, const double* __restrict__ x, const int32_t* __restrict__ clients,
     double* __restrict__ hcoef, double* __restrict__ gcoef, double* __restrict__ loss_part,
     int nblk) {
@@ -154,6 +157,7 @@ __global__ void __launch_bounds__(NT, NS > 1 ? 2 : 1) k_margins_cpc(
   extern __shared__ double mcs[];
   __shared__ double red[NT / 32];
   const int c = client_of(clients, blockIdx.x / NS);
+  const int ni = ni_arr[c];
   const int part = blockIdx.x % NS;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int SPS = mc_split_pairs(ldj, NS);
@@ -232,11 +236,14 @@ __global__ void __launch_bounds__(NT, NS > 1 ? 2 : 1) k_margins_cpc(
 // Local gradients g_c = B_c gcoef_c + lam x (oracle.py:108-121).
 // grid (ceil(d / 8), n_active), block 256: one warp per feature row.
 __global__ void __launch_bounds__(256) k_gradient(
-    const DevCtl* __restrict__ ctl, const double* __restrict__ Bt, int d, int ni, int ldj,
-    int ldh, const double* __restrict__ x, double lam, const int32_t* __restrict__ clients,
+    const DevCtl* __restrict__ ctl, const double* __restrict__ Bt, int d,
+    const int32_t* __restrict__ ni_arr, int ldj, int ldh, const double* __restrict__ x,
+    const double* __restrict__ lam_arr, const int32_t* __restrict__ clients,
     const double* __restrict__ gcoef, double* __restrict__ grad) {
   if (ctl && ctl->halt) return;
   const int c = client_of(clients, blockIdx.y);
+  const int ni = ni_arr[c];
+  const double lam = lam_arr[c];
   const int a = blockIdx.x * 8 + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
   if (a >= d) return;
@@ -254,19 +261,23 @@ __global__ void __launch_bounds__(256) k_gradient(
 }
 
 // Line-search trials (algorithms.py:304-309, runtime.py:203-208):
-// trial_s = x - step_s * p for s in [s0, s0 + S); per client and trial the
-// loss partial sums.  grid (ceil(ni / 128), n), block 128,
+// trial_s = x - step_s * p for s in [s0, s0 + S), s0 = ctl->ls_next; per
+// client and trial the loss partial sums, client-major
+// loss_part[c][s][block] (one contiguous block per client, so a sharded run
+// all-gathers it in place).  grid (ceil(ldj / 128), n_active), block 128,
 // dynamic smem S * d doubles.
 constexpr int LS_BATCH = 4;
 __global__ void __launch_bounds__(MARGIN_THREADS) k_ls_trials(
-    const DevCtl* __restrict__ ctl, const double* __restrict__ Bt, int d, int ni, int ldj,
+    const DevCtl* __restrict__ ctl, const double* __restrict__ Bt, int d,
+    const int32_t* __restrict__ ni_arr, int ldj, const int32_t* __restrict__ clients,
     const double* __restrict__ x, const double* __restrict__ p,
-    const double* __restrict__ steps_table, int n_clients, double* __restrict__ trial_x,
+    const double* __restrict__ steps_table, double* __restrict__ trial_x,
     double* __restrict__ loss_part, int nblk) {
-  if (ctl->halt && ctl->code != ST_LS_PENDING) return;
+  if (ctl->halt) return;
   extern __shared__ double xt[];  // [LS_BATCH][d]
   const int s0 = ctl->ls_next;
-  const int c = blockIdx.y;
+  const int c = client_of(clients, blockIdx.y);
+  const int ni = ni_arr[c];
   for (int e = threadIdx.x; e < LS_BATCH * d; e += blockDim.x) {
     const int s = e / d, a = e - s * d;
     const int si = s0 + s;
@@ -309,7 +320,7 @@ __global__ void __launch_bounds__(MARGIN_THREADS) k_ls_trials(
     const int s = threadIdx.x;
     double tot = 0.0;
     for (int i = 0; i < nw; ++i) tot += red4[s][i];
-    loss_part[(static_cast<int64_t>(s) * n_clients + c) * nblk + blockIdx.x] = tot;
+    loss_part[(static_cast<int64_t>(c) * LS_BATCH + s) * nblk + blockIdx.x] = tot;
   }
 }
 

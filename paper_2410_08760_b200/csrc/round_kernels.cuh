@@ -10,7 +10,7 @@ namespace fb {
 
 // Cross-client reductions of one round (algorithms.py:351-359, 399-402;
 // runtime.py:189-201):
-//   f_cli[c]    = sum_b loss_part[c][b] / n_i + (0.5 lam) <x, x>
+//   f_cli[c]    = sum_b loss_part[c][b] / n_c + (0.5 lam_c) <x, x>
 //   shift_cli[c]= sqrt(sum_p frob_part[c][p])           (if frob_part)
 //   gbar        = (sum_c grad_c) / n_div
 //   out: ||gbar||, (sum_c f_c) / n_div, (sum_c shift_c) / n_div
@@ -34,7 +34,8 @@ constexpr int RED_THREADS = 1024;
 __host__ __device__ __forceinline__ int reduce_grid(int d) { return (d + 31) / 32; }
 __global__ void __launch_bounds__(RED_THREADS) k_reduce(
     DevCtl* __restrict__ ctl, int n_active, const int32_t* __restrict__ clients, int n_div, int d,
-    int ni, int nblk, int n_pairs, const double* __restrict__ x, double lam,
+    const int32_t* __restrict__ ni_arr, int nblk, int n_pairs, const double* __restrict__ x,
+    const double* __restrict__ lam_arr,
     const double* __restrict__ grad, const double* __restrict__ loss_part,
     const double* __restrict__ frob_part, const int32_t* __restrict__ flags,
     double* __restrict__ gbar, double* __restrict__ f_cli, double* __restrict__ shift_cli,
@@ -99,7 +100,6 @@ __global__ void __launch_bounds__(RED_THREADS) k_reduce(
     gp[q][lane] = sacc;
   }
   const double xx = block_sum(xx_part, red);  // also publishes stage / gp
-  const double reg = __dmul_rn(__dmul_rn(0.5, lam), xx);
   pc.mark(8);
   if (q == 0) {
     const int a = b * 32 + lane;
@@ -121,7 +121,8 @@ __global__ void __launch_bounds__(RED_THREADS) k_reduce(
       const double* st = stage + ii * per_c;
       double ls = 0.0;
       for (int r = 0; r < nblk; ++r) ls = __dadd_rn(ls, st[r]);
-      f_cli[c] = __dadd_rn(__ddiv_rn(ls, static_cast<double>(ni)), reg);
+      const double reg = __dmul_rn(__dmul_rn(0.5, lam_arr[c]), xx);
+      f_cli[c] = __dadd_rn(__ddiv_rn(ls, static_cast<double>(ni_arr[c])), reg);
       if (frob_part) {
         double fp = 0.0;
         for (int r = 0; r < n_pairs; ++r) fp = __dadd_rn(fp, st[nblk + r]);
@@ -320,13 +321,17 @@ __global__ void __launch_bounds__(FOLD_THREADS) k_master_fold(
 
 // Round epilogue (algorithms.py:385-387): x <- x_new, round += 1,
 // DivergenceError on a non-finite iterate; per-client entry counts into the
-// row buffers (-1 for clients that did not participate).
+// row buffers (-1 for clients that did not participate).  With
+// ctl->stop_gn >= 0 a FedNL round whose row grad_norm <= stop_gn ends the run
+// after its step (runtime.py:270-272): ST_STOPPED halts the later rounds of
+// the chunk.
 __global__ void __launch_bounds__(256) k_finish(
     DevCtl* __restrict__ ctl, int d, int n, int n_active, const int32_t* __restrict__ clients,
     double* __restrict__ x, const double* __restrict__ x_new, int copy_x,
     const int32_t* __restrict__ count, int32_t* __restrict__ row_counts,
-    int32_t* __restrict__ row_ls, const double* __restrict__ hcopy_src = nullptr,
-    double* __restrict__ hcopy_dst = nullptr, int64_t hcopy_n = 0) {
+    int32_t* __restrict__ row_ls, const double* __restrict__ row_grad,
+    const double* __restrict__ hcopy_src = nullptr, double* __restrict__ hcopy_dst = nullptr,
+    int64_t hcopy_n = 0) {
   // H^{k+1} (the fold's second buffer) back into H^k, over every block of the
   // grid (unconditionally, as the copy it replaces), then the epilogue on block 0
   for (int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; t < hcopy_n;
@@ -358,7 +363,47 @@ __global__ void __launch_bounds__(256) k_finish(
     if (row_ls) row_ls[slot] = ctl->ls_steps;
     ctl->round += 1;
     if (bad) raise_status(ctl, ST_DIVERGED);
+    else if (row_grad && ctl->stop_gn >= 0.0 && row_grad[slot] <= ctl->stop_gn)
+      raise_status(ctl, ST_STOPPED);
   }
+}
+
+// FedNL-PP between the master's new point and the participants' round
+// (runtime.py:235-243, algorithms.py:422-433): the row of round k describes
+// x^k (the metric probes); when its grad_norm <= stop_gn the run ends BEFORE
+// the step (the row counts, the round does not advance x).  Otherwise
+// x <- x_new, DivergenceError on a non-finite new point.  One CTA.
+__global__ void __launch_bounds__(256) k_pp_advance(DevCtl* __restrict__ ctl, int d, int n,
+                                                     double* __restrict__ x,
+                                                     const double* __restrict__ x_new,
+                                                     const double* __restrict__ row_grad,
+                                                     int32_t* __restrict__ row_counts,
+                                                     int32_t* __restrict__ row_ls) {
+  if (ctl->halt) return;
+  __shared__ int s_stop, bad;
+  const int slot = ctl->round - ctl->row_base;
+  if (threadIdx.x == 0) {
+    s_stop = ctl->stop_gn >= 0.0 && row_grad[slot] <= ctl->stop_gn;
+    bad = 0;
+  }
+  __syncthreads();
+  if (s_stop) {  // no participant this round
+    for (int c = threadIdx.x; c < n; c += blockDim.x) row_counts[static_cast<int64_t>(slot) * n + c] = -1;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      row_ls[slot] = 0;
+      ctl->round += 1;
+      raise_status(ctl, ST_STOPPED);
+    }
+    return;
+  }
+  for (int a = threadIdx.x; a < d; a += blockDim.x) {
+    const double v = x_new[a];
+    x[a] = v;
+    if (!isfinite(v)) bad = 1;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0 && bad) raise_status(ctl, ST_DIVERGED);
 }
 
 // ------------------------------------------------------------------ FedNL-PP
@@ -504,15 +549,19 @@ __global__ void k_check_flags_pp(DevCtl* ctl, int tau, const int32_t* subset,
 
 // ------------------------------------------------------------ initialisation
 
-// Hest[c] = lam I (or 0) for every client, Hmas likewise
-// (algorithms.py:202-206, 334-335).  grid (ceil(w/256), n + 1).
-__global__ void k_init_diag(int64_t w, int n, double diag_value, double* __restrict__ hest,
+// Hest[c] = lam_c I (cli_diag set: the shard's lambda) or 0 for every
+// client, Hmas = master_diag I (algorithms.py:202-206: ClientShard.lam;
+// 334-335: RunConfig.lam).  grid (ceil(w/256), n + 1).
+__global__ void k_init_diag(int64_t w, int n, const double* __restrict__ cli_diag,
+                            double master_diag, double* __restrict__ hest,
                             double* __restrict__ hmas) {
   const int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (t >= w) return;
-  const double v = packed_is_diag_fast(t) ? diag_value : 0.0;
-  if (blockIdx.y < static_cast<unsigned>(n)) hest[static_cast<int64_t>(blockIdx.y) * w + t] = v;
-  else if (hmas) hmas[t] = v;
+  const bool dg = packed_is_diag_fast(t);
+  if (blockIdx.y < static_cast<unsigned>(n))
+    hest[static_cast<int64_t>(blockIdx.y) * w + t] = (dg && cli_diag) ? cli_diag[blockIdx.y] : 0.0;
+  else if (hmas)
+    hmas[t] = dg ? master_diag : 0.0;
 }
 
 // exact init (algorithms.py:336-341): Hmas = (sum_c Hest_c) / n, ascending c.
@@ -569,22 +618,31 @@ __global__ void k_pp_init_master(int d, int n, const double* __restrict__ cli_sh
 
 // After a trial batch: f_trial[s] = mean_c (loss_sum / n_i + reg(trial_s));
 // accept the first s with f_trial <= f_x - c * step * decrement
-// (algorithms.py:302-311).  On acceptance x_new = trial; if the batch is
-// exhausted, ST_LS_PENDING (host drives more batches); past s = 60,
-// ST_LINE_SEARCH.  Single CTA of 256 threads.
+// (algorithms.py:302-311).  The trial/decide pair is the body of a
+// while-conditional graph node (`loop`): the body runs again (next batch of
+// LS_BATCH trials) until a trial is accepted, or past s = 60 ST_LINE_SEARCH
+// is raised.  Every exit path clears the loop condition, including a round
+// that is already halted.  Single CTA of 256 threads.
 constexpr int LS_DECIDE_MAXN = 4096;
 __global__ void __launch_bounds__(256) k_ls_decide(
-    DevCtl* __restrict__ ctl, int d, int n, int ni, int nblk, double lam, double ls_c,
+    DevCtl* __restrict__ ctl, int d, int n, const int32_t* __restrict__ ni_arr,
+    const double* __restrict__ lam_arr, int nblk, double ls_c,
     const double* __restrict__ steps_table, const double* __restrict__ trial_x,
     const double* __restrict__ loss_part, RoundScalars* __restrict__ sc,
     double* __restrict__ x_new, int batch, const double* __restrict__ gbar,
-    const double* __restrict__ p) {
-  if (ctl->halt && ctl->code != ST_LS_PENDING) return;
+    const double* __restrict__ p, cudaGraphConditionalHandle loop) {
+  const int s0 = ctl->ls_next;
+  if (ctl->halt || s0 > 60) {  // nothing to decide: leave the loop
+    if (threadIdx.x == 0) {
+      ctl->ls_next = 0;
+      cudaGraphSetConditional(loop, 0);
+    }
+    return;
+  }
   __shared__ double red[8];
   __shared__ int s_acc;
   __shared__ double s_fbest;
-  __shared__ double s_lsum[LS_DECIDE_MAXN];  // per-client loss sums of one trial
-  const int s0 = ctl->ls_next;
+  __shared__ double s_lsum[LS_DECIDE_MAXN];  // per-client f of one trial
   if (s0 == 0) {  // decrement = <gbar, p> (algorithms.py:302), as k_dot forms it
     double part = 0.0;
     for (int i = threadIdx.x; i < d; i += blockDim.x) part = fma(gbar[i], p[i], part);
@@ -594,38 +652,26 @@ __global__ void __launch_bounds__(256) k_ls_decide(
   }
   if (threadIdx.x == 0) { s_acc = -1; s_fbest = (s0 == 0) ? INFINITY : ctl->f_best; }
   __syncthreads();
+  auto client_f = [&](int s, int c, double xx) {  // oracle.py:95-105
+    const double* lp = loss_part + (static_cast<int64_t>(c) * LS_BATCH + s) * nblk;
+    double ls = 0.0;
+    for (int b = 0; b < nblk; ++b) ls = __dadd_rn(ls, __ldcg(lp + b));
+    const double reg = __dmul_rn(__dmul_rn(0.5, lam_arr[c]), xx);
+    return __dadd_rn(__ddiv_rn(ls, static_cast<double>(ni_arr[c])), reg);
+  };
   for (int s = 0; s < batch; ++s) {
     const int si = s0 + s;
     const double* xt = trial_x + static_cast<int64_t>(s) * d;
     double part = 0.0;
     for (int a = threadIdx.x; a < d; a += blockDim.x) part = fma(xt[a], xt[a], part);
-    // per-client sums of the trial's loss partials, in parallel (client order
-    // is restored by the sequential fold below)
-    for (int c = threadIdx.x; c < n && c < LS_DECIDE_MAXN; c += blockDim.x) {
-      double ls = 0.0;
-      for (int b = 0; b < nblk; ++b)
-        ls = __dadd_rn(ls, __ldcg(loss_part + (static_cast<int64_t>(s) * n + c) * nblk + b));
-      s_lsum[c] = ls;
-    }
-    const double xx = block_sum(part, red);  // also publishes s_lsum
-    const double reg = __dmul_rn(__dmul_rn(0.5, lam), xx);
-    for (int c = threadIdx.x; c < n && c < LS_DECIDE_MAXN; c += blockDim.x)  // f_c, in parallel
-      s_lsum[c] = __dadd_rn(__ddiv_rn(s_lsum[c], static_cast<double>(ni)), reg);
+    const double xx = block_sum(part, red);
+    // per-client f in parallel (client order is restored by the sequential
+    // fold below)
+    for (int c = threadIdx.x; c < n && c < LS_DECIDE_MAXN; c += blockDim.x) s_lsum[c] = client_f(s, c, xx);
     __syncthreads();
     if (threadIdx.x == 0 && s_acc < 0 && si <= 60) {
       double tot = 0.0;
-      for (int c = 0; c < n; ++c) {
-        double fc;
-        if (c < LS_DECIDE_MAXN) {
-          fc = s_lsum[c];
-        } else {
-          double ls = 0.0;
-          for (int b = 0; b < nblk; ++b)
-            ls = __dadd_rn(ls, __ldcg(loss_part + (static_cast<int64_t>(s) * n + c) * nblk + b));
-          fc = __dadd_rn(__ddiv_rn(ls, static_cast<double>(ni)), reg);
-        }
-        tot = __dadd_rn(tot, fc);
-      }
+      for (int c = 0; c < n; ++c) tot = __dadd_rn(tot, c < LS_DECIDE_MAXN ? s_lsum[c] : client_f(s, c, xx));
       const double ft = __ddiv_rn(tot, static_cast<double>(n));
       const double step = steps_table[si];
       const double rhs = __dsub_rn(sc->f_mean, __dmul_rn(__dmul_rn(ls_c, step), sc->decrement));
@@ -644,17 +690,17 @@ __global__ void __launch_bounds__(256) k_ls_decide(
     if (acc >= 0) {
       ctl->ls_steps = acc;
       ctl->ls_next = 0;
-      if (ctl->code == ST_LS_PENDING) { ctl->code = 0; ctl->halt = 0; }
+      cudaGraphSetConditional(loop, 0);
     } else if (s0 + batch > 60) {
       ctl->f_start = sc->f_mean;
       ctl->f_best = s_fbest;
-      if (ctl->code == ST_LS_PENDING) ctl->code = 0;
+      ctl->ls_next = 0;
       raise_status(ctl, ST_LINE_SEARCH);
-    } else {
+      cudaGraphSetConditional(loop, 0);
+    } else {  // the next batch of trials
       ctl->f_best = s_fbest;
       ctl->ls_next = s0 + batch;
-      if (ctl->code == 0) { ctl->code = ST_LS_PENDING; ctl->code_round = ctl->round; }
-      ctl->halt = 1;
+      cudaGraphSetConditional(loop, 1);
     }
   }
 }

@@ -452,8 +452,9 @@ constexpr int CP_MAX_D = CP_MAXP * CP_NB;
 // holds) and the per-client scalars of client chunk r; the cluster-wide sums
 // go through DSMEM in rank order, so every CTA derives the same shift.
 struct CpRed {
-  int n_active, n_div, ni, nblk, n_pairs;
-  double lam;
+  int n_active, n_div, nblk, n_pairs;
+  const int32_t* ni;         // [n] samples per client
+  const double* lam;         // [n] lambda per client
   const double* grad;        // [n][d] local gradients (Hessian pass)
   const double* loss_part;   // [n][nblk]
   const double* frob_part;   // [n][n_pairs]
@@ -816,7 +817,6 @@ __global__ void __launch_bounds__(CH_THREADS, 1) k_chol_panels(
     int bad_t = 0x7fffffff;
     __syncthreads();
     const double xx = block_sum(xx_p, sm.rscr);
-    const double reg = __dmul_rn(__dmul_rn(0.5, red.lam), xx);
     if (tid < 2 * CP_NB) {
       double t2 = 0.0;
 #pragma unroll
@@ -840,7 +840,8 @@ __global__ void __launch_bounds__(CH_THREADS, 1) k_chol_panels(
           else fp = __dadd_rn(fp, vi);
         }
       }
-      const double fc = __dadd_rn(__ddiv_rn(ls, static_cast<double>(red.ni)), reg);
+      const double reg = __dmul_rn(__dmul_rn(0.5, red.lam[c]), xx);
+      const double fc = __dadd_rn(__ddiv_rn(ls, static_cast<double>(red.ni[c])), reg);
       const double sc = sqrt(fp);
       if (lane == 0) {
         red.f_cli[c] = fc;

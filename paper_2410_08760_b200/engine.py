@@ -38,7 +38,7 @@ class RoundBatch:
     done: int
 
 
-def _fb_config(cfg: RunConfig, d: int, n: int, ni: int) -> _lib.FbConfig:
+def _fb_config(cfg: RunConfig, d: int, n: int, ni: int, topk_path: int = 0) -> _lib.FbConfig:
     w = packed_length(d)
     cfg.compressor.validate(w)
     c = _lib.FbConfig()
@@ -58,20 +58,27 @@ def _fb_config(cfg: RunConfig, d: int, n: int, ni: int) -> _lib.FbConfig:
     c.run_seed = int(cfg.run_seed)
     for s in range(61):  # gamma ** s exactly as the host evaluates it (algorithms.py:305)
         c.ls_steps_table[s] = cfg.ls_gamma ** s
+    c.topk_path = int(topk_path)
     return c
 
 
 class FedNLEngine:
-    """Device-resident FedNL run.  Not re-entrant; one host thread."""
+    """Device-resident FedNL run.  Not re-entrant; one host thread.
 
-    def __init__(self, cfg: RunConfig, d: int, n_clients: int, n_samples: int, lam: float | None = None):
+    `n_samples` is the largest shard's sample count (shards may be ragged);
+    `lam` is every shard's lambda unless `upload` is given per-shard values
+    (the master's lambda-identity init uses cfg.lam, algorithms.py:334-335);
+    `topk_path` pins a TopK kernel variant (_lib.TOPK_PATH_*; results are
+    identical, tests use it to cover both)."""
+
+    def __init__(self, cfg: RunConfig, d: int, n_clients: int, n_samples: int, lam: float | None = None,
+                 topk_path: int = 0):
         self.lib = _lib.load()
         self.cfg = cfg
         self.d, self.n, self.ni = d, n_clients, n_samples
         self.w = packed_length(d)
-        fc = _fb_config(cfg, d, n_clients, n_samples)
-        if lam is not None:
-            fc.lam = float(lam)
+        fc = _fb_config(cfg, d, n_clients, n_samples, topk_path)
+        self.default_lam = float(cfg.lam if lam is None else lam)
         self.alpha = fc.alpha
         h = C.c_void_p()
         rc = self.lib.fb_create(C.byref(fc), C.byref(h))
@@ -135,22 +142,31 @@ class FedNLEngine:
         self._check(self.lib.fb_set_shard(self.h, int(world), int(rank), buf), "fb_set_shard")
         self.world, self.rank = int(world), int(rank)
 
-    def upload(self, bmats: list[np.ndarray]) -> None:
+    def upload(self, bmats: list[np.ndarray], lams=None) -> None:
+        """Shards (d x n_c each, n_c <= n_samples) and optionally their own
+        lambdas (ClientShard.lam, oracle.py:33-46); another rank's shard may
+        be None under sharding."""
         if len(bmats) != self.n:
             raise ValueError(f"expected {self.n} shards, got {len(bmats)}")
         keep = []
         ptrs = (C.POINTER(C.c_double) * self.n)()
+        nis = np.full(self.n, self.ni, dtype=np.int32)
+        lam = np.full(self.n, self.default_lam) if lams is None else np.asarray(lams, dtype=np.float64)
+        if lam.shape != (self.n,):
+            raise ValueError(f"expected {self.n} lambdas")
         lo, hi = shard_range(self.n, getattr(self, "world", 1), getattr(self, "rank", 0))
         for c, b in enumerate(bmats):
             if b is None and not lo <= c < hi:  # another rank's client (sharded)
                 ptrs[c] = None
                 continue
-            if b.shape != (self.d, self.ni):
-                raise ValueError(f"shard {c} has shape {b.shape}, expected {(self.d, self.ni)}")
+            if b.ndim != 2 or b.shape[0] != self.d or not 1 <= b.shape[1] <= self.ni:
+                raise ValueError(f"shard {c} has shape {b.shape}, expected ({self.d}, 1..{self.ni})")
             a = np.asfortranarray(b, dtype=np.float64)
             keep.append(a)
+            nis[c] = b.shape[1]
             ptrs[c] = a.ctypes.data_as(C.POINTER(C.c_double))
-        self._check(self.lib.fb_upload_shards(self.h, ptrs), "fb_upload_shards")
+        self._check(self.lib.fb_upload_shards_ex(self.h, ptrs, _lib.ptr(nis, C.c_int32), _lib.ptr(lam)),
+                    "fb_upload_shards_ex")
 
     def init_state(self, x0: np.ndarray | None = None) -> None:
         x = None if x0 is None else np.ascontiguousarray(x0, dtype=np.float64)

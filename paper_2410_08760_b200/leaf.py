@@ -32,10 +32,16 @@ def _dim_from_packed(w: int) -> int:
     return d
 
 
+# TopK kernel variant of the compress engines (_lib.TOPK_PATH_*): results are
+# identical by construction; the parity tests pin each variant in turn
+TOPK_PATH = _lib.TOPK_PATH_AUTO
+
+
 @lru_cache(maxsize=32)
-def _compress_engine(d: int, n: int, kind: CompressorKind, k: int | None, weighted: bool) -> FedNLEngine:
+def _compress_engine(d: int, n: int, kind: CompressorKind, k: int | None, weighted: bool,
+                     topk_path: int = 0) -> FedNLEngine:
     cfg = RunConfig(compressor=CompressorSpec(kind, k=k, topk_weighted=weighted), alpha=1.0)
-    return FedNLEngine(cfg, d, n, 1)
+    return FedNLEngine(cfg, d, n, 1, topk_path=topk_path)
 
 
 def _upper_packed(m: np.ndarray) -> np.ndarray:
@@ -52,7 +58,7 @@ def compress_packed_batch(packed: np.ndarray, d: int, spec: CompressorSpec, seed
     spec.validate(w)
     P = np.ascontiguousarray(packed, dtype=np.float64).reshape(-1, w)
     n = P.shape[0]
-    eng = _compress_engine(d, n, spec.kind, spec.k, bool(spec.topk_weighted))
+    eng = _compress_engine(d, n, spec.kind, spec.k, bool(spec.topk_weighted), TOPK_PATH)
     sd = np.array([int(s) & ((1 << 64) - 1) for s in seeds], dtype=np.uint64)
     idx, val, cnt, drw = eng.compress(P, sd)
     out = []
@@ -88,10 +94,10 @@ def compress(m: np.ndarray, spec: CompressorSpec, prg: Prg) -> CompressedDelta:
 
 def oracle_eval(shards, x: np.ndarray, hessian: bool = True):
     """(f [n], grad [n, d], packed Hessians [n, w] | None) of every client at x."""
-    d, n, ni = shards[0].dim, len(shards), shards[0].n_samples
+    d, n, ni = shards[0].dim, len(shards), max(s.n_samples for s in shards)
     cfg = RunConfig(lam=shards[0].lam)
-    with FedNLEngine(cfg, d, n, ni, lam=shards[0].lam) as eng:
-        eng.upload([s.bmat for s in shards])
+    with FedNLEngine(cfg, d, n, ni) as eng:
+        eng.upload([s.bmat for s in shards], [s.lam for s in shards])
         return eng.oracle_eval(x, hessian=hessian)
 
 

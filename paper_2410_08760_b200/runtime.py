@@ -158,12 +158,7 @@ def _validate(cfg: RunConfig, shards: list[ClientShard]) -> tuple[int, int, int]
     if any(s.dim != d for s in shards):
         raise ValueError("all shards must share one dimension")
     cfg.validate(n)
-    ni = shards[0].n_samples
-    if any(s.n_samples != ni for s in shards):
-        raise ValueError("this build needs equal-size shards (augment_and_shard produces them)")
-    lam = shards[0].lam
-    if any(s.lam != lam for s in shards):
-        raise ValueError("all shards must share one lambda")
+    ni = max(s.n_samples for s in shards)  # shards may be ragged (runtime.py:145-151)
     packed_length(d)
     cfg.compressor.validate(packed_length(d))
     return n, d, ni
@@ -195,15 +190,16 @@ def simulate(cfg: RunConfig, shards: list[ClientShard], workers: int = 1,
 
     `workers` is accepted for signature compatibility and ignored: the
     trajectory and counters never depended on it (runtime.py:141-143).
-    The oracle uses the shards' own lambda (oracle.py:104,120,138).
+    Shards may differ in n_samples and lam: each client's oracle uses its
+    shard's own (oracle.py:95-139), as the reference does.
     """
     del workers
     n, d, ni = _validate(cfg, shards)
     t0 = time.perf_counter()
     own = engine is None
-    eng = engine or FedNLEngine(cfg, d, n, ni, lam=shards[0].lam)
+    eng = engine or FedNLEngine(cfg, d, n, ni)
     try:
-        eng.upload([s.bmat for s in shards])
+        eng.upload([s.bmat for s in shards], [s.lam for s in shards])
         eng.init_state()
         t_init = time.perf_counter() - t0
         up = down = 0

@@ -42,12 +42,18 @@ def test_library_loads_and_exports_every_symbol():
 
 
 def test_struct_layouts():
+    """The ctypes mirrors have the sizes the library was compiled with."""
+    import numpy as np
+
     from paper_2410_08760_b200 import _lib
 
-    # fb_config: 10 int32 + 4 double + u64 + 61 double
-    assert ctypes.sizeof(_lib.FbConfig) == 10 * 4 + 4 * 8 + 8 + 61 * 8 + 8
-    assert ctypes.sizeof(_lib.FbStatus) == 4 * 4 + 3 * 8
-    assert ctypes.sizeof(_lib.FbProfile) == 2 * 4 + 7 * 8
+    lib = _lib.load()
+    sizes = np.zeros(3, dtype=np.int32)
+    assert lib.fb_abi_sizes(_lib.ptr(sizes, ctypes.c_int32)) == 0
+    assert sizes.tolist() == [ctypes.sizeof(_lib.FbConfig), ctypes.sizeof(_lib.FbStatus),
+                              ctypes.sizeof(_lib.FbProfile)]
+    # fb_config: 10 int32 + 4 double + u64 + 61 double + mu + topk_path + reserved
+    assert ctypes.sizeof(_lib.FbConfig) == 10 * 4 + 4 * 8 + 8 + 61 * 8 + 8 + 2 * 4
 
 
 def test_no_cpu_fallback_when_library_missing(monkeypatch):

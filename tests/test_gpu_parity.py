@@ -26,6 +26,7 @@ from paper_2410_08760_b200 import (
     leaf,
     simulate,
 )
+from paper_2410_08760_b200 import _lib
 from paper_2410_08760_b200 import data as D
 from paper_2410_08760_b200.engine import FedNLEngine
 
@@ -74,11 +75,10 @@ def test_device_partial_shuffle_and_round_seeds():
 def topk_path(request, monkeypatch):
     """Both large-w TopK paths: the one-CTA-per-client k_topk_stream and the
     window / segmented pass / select kernels (chosen per context at creation;
-    FB_TOPK_SPLIT forces either, the compress engines are re-created)."""
-    monkeypatch.setenv("FB_TOPK_SPLIT", request.param)
-    leaf._compress_engine.cache_clear()
+    fb_config.topk_path pins either)."""
+    path = _lib.TOPK_PATH_SPLIT if request.param == "1" else _lib.TOPK_PATH_STREAM
+    monkeypatch.setattr(leaf, "TOPK_PATH", path)
     yield request.param
-    leaf._compress_engine.cache_clear()
 
 
 def _golden_compress_cases():
@@ -381,17 +381,18 @@ def test_round_fold_bit_exact_given_device_deltas(kind, k):
     eng.close()
 
 
-def test_split_topk_rounds_bit_identical_to_stream_path(monkeypatch):
+def test_split_topk_rounds_bit_identical_to_stream_path():
     """c0 rounds through the split TopK (client shift update moved into the
     master fold) reproduce the pinned k_topk_stream round bit for bit: same
     selections, same shift and fold arithmetic, same trajectory."""
     cfg, shards = sim_case("c0_r4")
     cfg = RunConfig(compressor=cfg.compressor, rounds=12, alpha=cfg.alpha, run_seed=cfg.run_seed)
     out = {}
-    for path in ("0", "1"):
-        monkeypatch.setenv("FB_TOPK_SPLIT", path)
-        out[path] = simulate(cfg, shards)
-    for a, b in zip(out["0"], out["1"]):
+    for path in (_lib.TOPK_PATH_STREAM, _lib.TOPK_PATH_SPLIT):
+        eng = FedNLEngine(cfg, shards[0].dim, len(shards), shards[0].n_samples, topk_path=path)
+        out[path] = simulate(cfg, shards, engine=eng)
+        eng.close()
+    for a, b in zip(out[_lib.TOPK_PATH_STREAM], out[_lib.TOPK_PATH_SPLIT]):
         assert (a.round, a.grad_norm, a.f_value, a.bytes_up_cum) == (b.round, b.grad_norm, b.f_value, b.bytes_up_cum)
 
 
@@ -480,19 +481,37 @@ def test_simulate_rows_match_reference(name):
     if name == "c0_r4":
         # TopK at a real shape: an ulp-level difference in D can legitimately
         # swap a k-th-boundary tie (the reference itself does so between BLAS
-        # thread counts), after which the trajectory moves within
-        # the envelope below; exactness up to the first swap is pinned by the
-        # teacher-forced test_teacher_forced_round_c0.
-        want = g["c0_r4__grad_norm"]
-        assert [r.round for r in rows] == g["c0_r4__round"].tolist()
-        for i in range(2):  # before any possible swap: 1e-10
-            assert abs(rows[i].grad_norm - want[i]) <= 1e-10 * want[i]
-            assert abs(rows[i].f_value - g["c0_r4__f_value"][i]) <= 1e-12 * abs(g["c0_r4__f_value"][i])
-        gn = np.array([r.grad_norm for r in rows])
-        assert np.all(np.abs(gn - want) <= 1e-3 * want)
-        assert [r.bytes_up_cum for r in rows] == g["c0_r4__bytes_up"].tolist()
+        # thread counts at round 3): judged against both of the
+        # reference's trajectories and its own envelope
+        _envelope_close(rows, g, "c0_r4", "c0_r4_mt")
     else:
         _rows_close(rows, g, [name])
+
+
+def _envelope_close(rows, g, base, mt):
+    """P6 for the tie-heavy TopK shapes: rows within 1e-10 of one of the
+    reference's two valid trajectories (1 and 8 BLAS threads) until the
+    first k-th-boundary swap, and every row within the reference's own
+    whole-run envelope E = max_i |g1_i - g8_i| / g1_i of the nearer one.
+    f_value is flat near its minimum, so one swap moves it by a
+    round-dependent amount: its bar is 10x the reference's own f envelope
+    (c0_r20 measured: 3.8x, at the GPU's swap in round 10)."""
+    g1, g8 = g[f"{base}__grad_norm"], g[f"{mt}__grad_norm"]
+    f1, f8 = g[f"{base}__f_value"], g[f"{mt}__f_value"]
+    assert [r.round for r in rows] == g[f"{base}__round"].tolist()
+    assert [r.bytes_up_cum for r in rows] == g[f"{base}__bytes_up"].tolist()
+    assert [r.bytes_down_cum for r in rows] == g[f"{base}__bytes_down"].tolist()
+    gn = np.array([r.grad_norm for r in rows])
+    fv = np.array([r.f_value for r in rows])
+    env = float(np.max(np.abs(g1 - g8) / g1))
+    env_f = float(np.max(np.abs(f1 - f8) / np.abs(f1)))
+    dev = np.minimum(np.abs(gn - g1) / g1, np.abs(gn - g8) / g8)
+    dev_f = np.minimum(np.abs(fv - f1) / np.abs(f1), np.abs(fv - f8) / np.abs(f8))
+    first = int(np.argmax(dev > 1e-10)) if np.any(dev > 1e-10) else len(rows)
+    assert first >= 3, ("left both references before their own first swap", first, dev)
+    assert np.all(dev <= env), (env, dev)
+    assert np.all(dev_f <= max(10 * env_f, 1e-12)), (env_f, dev_f)
+    return dev
 
 
 def _kth_boundary_ok(got_idx, want_idx, diff_gpu, diff_ref, k, ulps=4):
@@ -532,6 +551,7 @@ def test_teacher_forced_round_c0():
                                          O.round_stream(cfg.run_seed, c, 2)).indices)
     run.fednl_round(2)
     x_ref = run.x.copy()
+    run_h_mas = run.h_mas.copy()
     run.close()
     eng = FedNLEngine(cfg, d, n, shards[0].n_samples, lam=shards[0].lam)
     eng.upload([s.bmat for s in shards])
@@ -549,14 +569,22 @@ def test_teacher_forced_round_c0():
     for c in range(n):
         ref_g += O.local_eval(shards[c].bmat, shards[c].lam, x0, need_hess=False).grad
     assert normwise(mg, ref_g / n) <= 1e-10
+    h_fold = h_mas0.copy()  # the master fold of the GPU's own selections, in the oracle
     for c in range(n):
         dv = eng.round_diff(c)
         hmax = np.max(np.abs(ref_diff[c] + h_cli0[c]))
         assert np.max(np.abs(dv - ref_diff[c])) <= 1e-10 * hmax, c
-        idx, _ = eng.round_delta(c)
+        idx, val = eng.round_delta(c)
         swaps += _kth_boundary_ok(idx, ref_idx[c], dv, ref_diff[c], cfg.compressor.k)
+        assert np.array_equal(val, dv[idx])  # TopK values: unscaled D at the kept positions
+        O.apply_packed(h_fold, O.Delta("topk", d, ref_diff[c][idx], idx.astype(np.uint32)), eng.alpha / n)
+    # x^{k+1} = x^k - (H^k + l^k I)^{-1} gbar uses the pre-fold H^k: it does
+    # not depend on this round's selections, so it is checked even after swaps
+    assert normwise(eng.get_x(), x_ref) <= 1e-10
+    # H^{k+1}: the GPU's selections folded by the oracle from the reference's D
+    assert normwise(eng.get_master_hest(), h_fold) <= 1e-10
     if swaps == 0:
-        assert normwise(eng.get_x(), x_ref) <= 1e-10
+        assert normwise(eng.get_master_hest(), run_h_mas) <= 1e-10
     print(f"[P5 c0] boundary swaps in round 2: {swaps}")
     eng.close()
 

@@ -327,3 +327,33 @@ def test_oracle_option_a_matches_reference_rows(name):
     gn = np.array([r.grad_norm for r in rows])
     want_g = g[f"{name}__grad_norm"]
     assert np.all(np.abs(gn - want_g) <= 1e-9 * np.maximum(want_g, 1e-6 * want_g[0]))
+
+
+# ------------------------------------------------- round-2 cases (simulate_r2)
+
+from cases_r2 import LS_FAIL, SIM_R2, case_r2  # noqa: E402
+
+
+@pytest.mark.parametrize("name", [n for n in SIM_R2 if n != "c0_r20"])
+def test_oracle_round2_cases_match_reference_rows(name):
+    """Deep line searches, ragged shards with per-shard lambda: the oracle
+    restatement reproduces the reference's rows (bitwise on one BLAS thread)."""
+    kw, shards = case_r2(name)
+    cfg = O.OracleConfig(**kw)
+    rows = O.simulate(cfg, [s.bmat for s in shards], lam=[s.lam for s in shards])
+    g = golden("simulate_r2.npz")
+    assert [r.round for r in rows] == g[f"{name}__round"].tolist()
+    assert [r.bytes_up_cum for r in rows] == g[f"{name}__bytes_up"].tolist()
+    assert [r.bytes_down_cum for r in rows] == g[f"{name}__bytes_down"].tolist()
+    assert [r.ls_steps for r in rows] == g[f"{name}__ls_steps"].tolist()
+    assert np.array_equal([r.grad_norm for r in rows], g[f"{name}__grad_norm"])
+    assert np.array_equal([r.f_value for r in rows], g[f"{name}__f_value"])
+
+
+def test_oracle_line_search_failure_matches_reference():
+    kw, shards = case_r2(LS_FAIL["base"])
+    kw.update(ls_c=LS_FAIL["ls_c"], ls_gamma=LS_FAIL["ls_gamma"], rounds=LS_FAIL["rounds"])
+    g = golden("simulate_r2.npz")
+    with pytest.raises(O.LineSearchFailed) as exc:
+        O.simulate(O.OracleConfig(**kw), [s.bmat for s in shards], lam=shards[0].lam)
+    assert exc.value.round == int(g["ls_fail__round"])

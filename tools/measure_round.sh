@@ -10,4 +10,4 @@ for c in c0 c1 c2 c3 c4; do timeout 400 python bench.py --config $c > $O/bench_$
 timeout 300 python bench.py --impl reference > $O/bench_reference_c0.json 2> $O/bench_reference_c0.err
 timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file $O/launches_c0.csv python bench.py --steps 2 --warmup 3 --no-cpu-baseline > $O/ncu_launch.log 2>&1
 timeout 300 ncu --set full --import-source on --clock-control none -k regex:k_hessian -s 10 -c 1 -o $O/hessian_c0 python bench.py --steps 3 --warmup 3 --no-cpu-baseline > $O/ncu_full_c0.log 2>&1
-WARM=1 timeout 400 ncu --set full --import-source on --clock-control none -k regex:"k_tks_pass|k_master_fold" -c 2 -o $O/topk_c4 python tools/diag_round.py c4 > $O/ncu_full_c4.log 2>&1
+WARM=1 timeout 400 ncu --set full --import-source on --clock-control none -k regex:"k_tks_pass|k_master_fold" -c 2 -o $O/topk_c4 python tools/profile_round.py c4 > $O/ncu_full_c4.log 2>&1
