@@ -255,6 +255,11 @@ int fb_solve_phase_cycles(void* ctx, const double* h_packed, double shift, const
  * per-CTA durations of the last instrumented compressor launch; `enable`
  * arms the next run */
 int fb_debug_counters(int32_t enable, long long* out);
+/* diagnostic: out[2 s], out[2 s + 1] = first-CTA start / last-CTA end
+ * globaltimer ns of instrumented kernel slot s (16 slots) since the last
+ * call (which re-arms them); slots: 0 margins, 1 Hessian, 2 solve, 3 solve's
+ * wait for its producer, 4 TopK, 5 master fold, 6 round epilogue */
+int fb_debug_timeline(unsigned long long* out);
 
 /* ---- context-free device SplitMix64 (rng.py:37-136) -------------------- */
 int fb_prg_u64(uint64_t seed, int32_t count, uint64_t* out);

@@ -123,6 +123,7 @@ PROTOTYPES = {
     "fb_solve_phase_cycles": (C.c_int, [_P, _D, C.c_double, _D, C.c_int32, C.POINTER(C.c_longlong),
                                         C.POINTER(C.c_float)]),
     "fb_debug_counters": (C.c_int, [C.c_int32, C.POINTER(C.c_longlong)]),
+    "fb_debug_timeline": (C.c_int, [C.POINTER(C.c_ulonglong)]),
     "fb_prg_u64": (C.c_int, [C.c_uint64, C.c_int32, _U64]),
     "fb_prg_randrange": (C.c_int, [C.c_uint64, _U64, C.c_int32, C.c_int32, _U64, _U64]),
     "fb_prg_partial_shuffle": (C.c_int, [C.c_uint64, C.c_int64, C.c_int32, _I64]),

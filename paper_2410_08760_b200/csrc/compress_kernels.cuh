@@ -680,6 +680,7 @@ __global__ void __launch_bounds__(TK_THREADS, 1) k_topk_stream(
     double* __restrict__ val_list, int cap, int32_t* __restrict__ draws,
     uint64_t* __restrict__ cand_key, int32_t* __restrict__ cand_pos, Emit em) {
   if (ctl && ctl->halt) return;
+  if (threadIdx.x == 0) tl_mark(4, false);
   PhaseClock pc;
   extern __shared__ __align__(16) uint32_t tkst_dyn[];
   const int wi = static_cast<int>(w);
@@ -1026,6 +1027,7 @@ __global__ void __launch_bounds__(TK_THREADS, 1) k_topk_stream(
   }
   pc.mark(4);
   if (g_dbg_on && tid == 0 && s_fail) atomicAdd(reinterpret_cast<unsigned long long*>(&g_dbg[17]), 1ull);
+  if (tid == 0) tl_mark(4, true);
 }
 
 // ------------------------------------------- TopK, split streaming path

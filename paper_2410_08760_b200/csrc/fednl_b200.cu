@@ -71,7 +71,6 @@ struct Ctx {
   bool gexec_phase = false;    // the flavour the cached round graph was built with
   int num_sms = 148;
   int32_t* pair_order = nullptr;  // Hessian tile pairs, costliest first
-  int32_t* hess_dispatch = nullptr;  // per-CTA (pair << 16 | slot) for full-client passes, or null
   double* Lg = nullptr;       // k_chol_panels: released L panels
   double* pp_shift_part = nullptr;  // FedNL-PP: Frobenius partials [tau][PP_SB]
   // client sharding over `world` GPUs (fb_set_shard): this rank owns clients
@@ -92,6 +91,7 @@ struct Ctx {
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr, ev_solve_launched = nullptr;
 
   DevCtl* ctl = nullptr;
+  int32_t* hess_sched = nullptr;  // k_hessian_ws item tickets (zero between launches)
   int32_t* ni_arr = nullptr;  // [n] samples per client (ragged shards; <= cfg.n_samples)
   double* lam_arr = nullptr;  // [n] lambda per client (ClientShard.lam)
   double *Bt = nullptr, *x = nullptr, *x_new = nullptr, *pvec = nullptr, *zbuf = nullptr;
@@ -315,11 +315,11 @@ int gather_clients(Ctx* ctx, T* base, size_t per, ncclDataType_t type, cudaStrea
 }
 bool sharded(const Ctx* ctx) { return ctx->world > 1 || ctx->comm != nullptr; }
 
-// clients per Hessian dispatch group: about 2.5 waves of CTAs (2 per SM).
-// Measured at c0 (n=142, 15 pairs): one group (pure costliest-first) 244 us
-// and 586 MB of DRAM traffic, 3 groups of 48: 240 us and 218 MB, 10-client
-// groups 250 us — the group's B rows stay in L2 for its tiles while each
-// group's last wave still ends on the cheap tiles.
+// clients per Hessian item group: about 2.5 rounds of the 2 * num_sms tile
+// pipes.  Items run group by group, each group's tile pairs costliest first:
+// the group's B rows stay in L2 for all its tiles (round 1, one tile per CTA
+// at c0: one group 586 MB of DRAM traffic, groups of 48 clients 218 MB) and
+// the last items of the pass are cheap diagonal / edge tiles.
 int hess_group(const Ctx* ctx) {
   return std::max(1, 5 * ctx->num_sms / std::max(1, ctx->n_pairs));
 }
@@ -370,27 +370,28 @@ int launch_gradient(Ctx* ctx, cudaStream_t s, const double* x, const int32_t* cl
 int launch_hessian(Ctx* ctx, cudaStream_t s, const int32_t* clients, int n_active,
                    const double* hest, int64_t hest_stride, double* D, double* hess_out,
                    bool with_ctl = true, const double* fuse_grad_x = nullptr) {
-  // 2 CTAs per SM (the 3-CTA register budget measured slower once the ring
-  // release was made safe, see mbar_arrive_dep); programmatic dependent
-  // launch after the margins kernel (the TMA producer waits for it)
+  // persistent warp-specialised DMMA pass: one CTA (two tile pipes) per SM
+  // over the (client, tile pair) items; programmatic dependent launch after
+  // the margins kernel (the TMA producers wait for it)
   cudaLaunchConfig_t lc{};
-  lc.gridDim = dim3(n_active * ctx->n_pairs);
-  lc.blockDim = dim3(HTHREADS);
-  lc.dynamicSmemBytes = HESS_SMEM;
+  const int items = n_active * ctx->n_pairs;
+  lc.gridDim = dim3(std::min((items + HW_PIPES - 1) / HW_PIPES, ctx->num_sms));
+  lc.blockDim = dim3(HW_THREADS);
+  lc.dynamicSmemBytes = HESS_WS_SMEM;
   lc.stream = s;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   lc.attrs = attr;
   lc.numAttrs = pdl_ok(ctx) ? 1 : 0;
-  const int32_t* disp = (clients == nullptr && n_active == ctx->n) ? ctx->hess_dispatch : nullptr;
-  CK(cudaLaunchKernelEx(&lc, k_hessian<2>, ctx->tmap, static_cast<const DevCtl*>(with_ctl ? ctx->ctl : nullptr),
+  CK(cudaLaunchKernelEx(&lc, k_hessian_ws, ctx->tmap, static_cast<const DevCtl*>(with_ctl ? ctx->ctl : nullptr),
                         ctx->d, static_cast<const int32_t*>(ctx->ni_arr), ctx->ldh,
                         static_cast<const double*>(ctx->hcoef), static_cast<const double*>(ctx->lam_arr), clients,
                         hest, hest_stride, D, hess_out, ctx->frob_part, ctx->flags,
                         0u /* zero_mask: see mbar_arrive_dep */, static_cast<const double*>(ctx->gcoef),
                         fuse_grad_x, fuse_grad_x ? ctx->grad : nullptr,
-                        static_cast<const int32_t*>(ctx->pair_order), ctx->n_pairs, hess_group(ctx), disp));
+                        static_cast<const int32_t*>(ctx->pair_order), ctx->n_pairs, n_active, hess_group(ctx),
+                        ctx->hess_sched));
   return FB_OK;
 }
 int launch_reduce(Ctx* ctx, cudaStream_t s, const double* x, const int32_t* clients, int n_active,
@@ -1030,8 +1031,8 @@ int fb_create(const fb_config* cfg_in, void** out) {
   static size_t max_toplek = 0, max_solve = 0;
   max_toplek = std::max(max_toplek, toplek_smem_bytes(std::max(ctx->toplek_P, 1)));
   max_solve = std::max(max_solve, std::max<size_t>(ctx->solve_smem, 1));
-  CKC(cudaFuncSetAttribute(k_hessian<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           static_cast<int>(HESS_SMEM)));
+  CKC(cudaFuncSetAttribute(k_hessian_ws, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           static_cast<int>(HESS_WS_SMEM)));
   CKC(cudaFuncSetAttribute(k_topk_smem, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            static_cast<int>(TKS_SMEM)));
   CKC(cudaFuncSetAttribute(k_margins_cpc<MC_THREADS, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1094,7 +1095,7 @@ int fb_create(const fb_config* cfg_in, void** out) {
   }
   const int tau = ctx->tau;
   if (dalloc(ctx, &ctx->ctl, 1) || dalloc(ctx, &ctx->Bt, static_cast<size_t>(n) * d * ctx->ldj) ||
-      dalloc(ctx, &ctx->ni_arr, n) || dalloc(ctx, &ctx->lam_arr, n) ||
+      dalloc(ctx, &ctx->ni_arr, n) || dalloc(ctx, &ctx->lam_arr, n) || dalloc(ctx, &ctx->hess_sched, 2) ||
       dalloc(ctx, &ctx->x, d) || dalloc(ctx, &ctx->x_new, d) || dalloc(ctx, &ctx->pvec, d) ||
       dalloc(ctx, &ctx->zbuf, d) ||
       dalloc(ctx, &ctx->hcoef, static_cast<size_t>(n) * ctx->ldh) ||
@@ -1203,34 +1204,6 @@ int fb_create(const fb_config* cfg_in, void** out) {
       CKC(cudaMemcpyAsync(ctx->npw_tab, tab.data(), sizeof(int32_t) * tab.size(),
                           cudaMemcpyHostToDevice, ctx->st));
     }
-  }
-  // Full-client passes: the first wave's two CTAs per SM start on tiles of
-  // different cost (the group's costliest tiles, then its cheapest), so the
-  // co-resident CTAs do not run in lockstep and one's epilogue overlaps the
-  // other's DMMA main loop; the rest of the order is unchanged.
-  std::vector<int32_t> disp;
-  {
-    const int P = ctx->n_pairs, n_all = ctx->n, grp = hess_group(ctx);
-    disp.resize(static_cast<size_t>(n_all) * P);
-    for (int L = 0; L < n_all * P; ++L) {  // the kernel's default mapping
-      const int g0 = (L / (grp * P)) * grp, gs = std::min(grp, n_all - g0), rem = L - g0 * P;
-      disp[L] = (order[rem / gs] << 16) | (g0 + rem % gs);
-    }
-    const int G0 = std::min(grp, n_all) * P, S = ctx->num_sms;
-    if (G0 >= 3 * S) {
-      std::vector<int32_t> g(disp.begin(), disp.begin() + G0), h;
-      h.insert(h.end(), g.begin(), g.begin() + S);
-      h.insert(h.end(), g.end() - S, g.end());
-      h.insert(h.end(), g.begin() + S, g.end() - S);
-      std::copy(h.begin(), h.end(), disp.begin());
-    } else {
-      disp.clear();
-    }
-  }
-  if (!disp.empty() && n <= 0xFFFF) {
-    if (dalloc(ctx, &ctx->hess_dispatch, disp.size())) return fail(FB_ERR_CUDA);
-    CKC(cudaMemcpyAsync(ctx->hess_dispatch, disp.data(), sizeof(int32_t) * disp.size(),
-                        cudaMemcpyHostToDevice, ctx->st));
   }
   CKC(cudaStreamSynchronize(ctx->st));  // zero fills and the tables are in place
   if (make_tmap(ctx) != FB_OK) return fail(FB_ERR_CUDA);
@@ -2098,6 +2071,17 @@ int fb_debug_counters(int32_t enable, long long* out) {
   G_CK(cudaMemcpyToSymbol(g_dbg, zero, sizeof zero));
   const int on = enable ? 1 : 0;
   G_CK(cudaMemcpyToSymbol(g_dbg_on, &on, sizeof on));
+  return FB_OK;
+}
+
+int fb_debug_timeline(unsigned long long* out) {
+  if (out) G_CK(cudaMemcpyFromSymbol(out, g_tl, sizeof(g_tl)));
+  unsigned long long init[TL_SLOTS][2];
+  for (int i = 0; i < TL_SLOTS; ++i) {
+    init[i][0] = ~0ull;
+    init[i][1] = 0ull;
+  }
+  G_CK(cudaMemcpyToSymbol(g_tl, init, sizeof init));
   return FB_OK;
 }
 

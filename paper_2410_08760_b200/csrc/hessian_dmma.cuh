@@ -12,10 +12,10 @@
 // Optionally H itself is written (`hess_out`, FedNL-PP / exact init).
 //
 // Operands are staged by TMA: box {16 samples, 64 features} per operand and
-// stage, SWIZZLE_128B, NSTAGE-deep mbarrier ring; the h chunk rides on the
-// same barrier as a 128 B bulk copy.  Each of the 4 warps owns a 32x32
-// quadrant as 4x4 m8n8k4 fragments (32 fp64 accumulators per thread).  The
-// A fragment is scaled by h_j in registers (one DMUL per 16 DMMA).
+// stage, SWIZZLE_128B, HW_STAGE-deep mbarrier ring; the h chunk rides on the
+// same barrier as a 128 B bulk copy.  A tile's 8x8 fragments (m8n8k4 DMMA)
+// are split between four warps in balanced blocks of up to 4x4 (32 fp64
+// accumulators per thread); the A fragment is scaled by h_j in registers.
 #pragma once
 #include "common.cuh"
 
@@ -23,22 +23,7 @@ namespace fb {
 
 constexpr int HT = 64;          // tile edge (features)
 constexpr int HKC = 16;         // samples per stage (128 B rows)
-constexpr int HSTAGE = 4;       // pipeline depth
-constexpr int HCONS = 4;        // consumer (DMMA) warps, one 32x32 quadrant each
-constexpr int HTHREADS = (HCONS + 1) * 32;  // + one TMA producer warp
-constexpr int HC_LD = HT + 1;   // epilogue staging pitch
 
-struct HessSmem {
-  double a[HSTAGE][HT * HKC];  // 8 KB per stage, 1024 B aligned (swizzle-128B)
-  double b[HSTAGE][HT * HKC];
-  double h[HSTAGE][HKC];
-  double gc[HSTAGE][HKC];      // gradient coefficients (fused gradient, diagonal tiles)
-  uint64_t full[HSTAGE];       // TMA -> consumers (transaction count)
-  uint64_t empty[HSTAGE];      // consumers -> producer (one arrive per active warp)
-  double red[HTHREADS / 32];
-  int flag_or;
-};
-constexpr size_t HESS_SMEM = sizeof(HessSmem) + 1024;  // + alignment slack
 
 // The consumers hand a ring slot back to the TMA with an mbarrier arrive
 // whose address depends (through `zero_mask`: a kernel argument that is 0 at
@@ -59,32 +44,107 @@ __device__ __forceinline__ int swz(int r, int s) {
 }
 
 
-// One consumer warp's mainloop over all K-chunks, specialised at compile time
-// for its 32x32 quadrant: MR x NC valid 8x8 fragments (rows / columns past d
-// in the last tile are skipped, rounded up to 2 or 4) and TRI = a diagonal
-// quadrant, whose fragments strictly below the diagonal are skipped.  No
-// runtime branch sits between the DMMAs.
-template <int MR, int NC, bool TRI>
-__device__ __forceinline__ void hess_consume(HessSmem& sm, bool diag, int nk, int rowbase,
-                                             int colbase, int g, int t, int lane,
-                                             uint32_t zero_mask, double (&acc)[4][4][2]) {
+// ===================================================================
+// Persistent, warp-specialised variant (the production kernel).
+//
+// A one-tile-per-CTA kernel (round 1) paid, per 64x64 tile, the TMA pipeline
+// fill and an epilogue (stage -> H_i^k loads -> D / Frobenius) during which
+// its DMMA warps idle.  Here one CTA per SM runs two independent tile
+// pipes, each with its own stage ring and hand-off buffer, and every pipe
+// loops over tiles (items) with its roles running concurrently:
+//   4 DMMA warps   the current item (on a diagonal tile the lower-left warp
+//                  forms the fused local gradient), then hand the
+//                  accumulators to the epilogue through `cs` and go on;
+//   1 TMA warp     streams the stages of item j+1 while the DMMA warps
+//                  finish item j (the ring never drains between items);
+//   1 epilogue     item j-1: H_i^k loads, D in packed column segments, the
+//     warp         Frobenius partial and the flags.
+// Two pipes per CTA (not two CTAs per SM) so that the DMMA warps get 168
+// registers (a whole stage's fragments in flight) under one launch bound.
+// Items are (client slot, tile pair) in the order of the one-tile grid
+// (client groups, costliest tile pairs first); a pipe's producer claims the
+// next one with an atomic ticket and publishes it to its DMMA and epilogue
+// warps through a small queue in shared memory (the stage barrier it arms
+// next orders the write), so the pipes stay balanced to the last item.  The
+// hand-off pitch 66 makes the accumulator stores conflict-free.
+constexpr int HW_PIPES = 2;
+constexpr int HW_MMA = 4;  // DMMA warps per pipe
+constexpr int HW_THREADS = HW_PIPES * (HW_MMA + 2) * 32;
+constexpr int HW_LD = HT + 2;
+constexpr int HW_STAGE = 4;
+// the producer runs at most HW_STAGE items ahead of the DMMA warps, which
+// run at most one item ahead of the epilogue: a queue of 16 never wraps
+constexpr int HW_QUEUE = 16;
+
+struct __align__(1024) HwPipe {
+  double a[HW_STAGE][HT * HKC];  // 1024 B aligned (swizzle-128B)
+  double b[HW_STAGE][HT * HKC];
+  double h[HW_STAGE][HKC];
+  double gc[HW_STAGE][HKC];
+  double cs[HT * HW_LD];         // accumulator hand-off (column-major, pitch HW_LD)
+  uint64_t full[HW_STAGE];
+  uint64_t empty[HW_STAGE];
+  uint64_t cs_full;              // 4 DMMA warps -> epilogue warp
+  uint64_t cs_empty;             // epilogue warp -> DMMA warps
+  int32_t itemq[HW_QUEUE];       // claimed item of the pipe's j-th tile (-1: no more)
+};
+constexpr size_t HESS_WS_SMEM = HW_PIPES * sizeof(HwPipe) + 1024;
+
+struct HwItem {
+  int slot, c, pair, I, J, nk;
+  bool diag;
+};
+__device__ __forceinline__ HwItem hw_item(int L, int n_pairs, int n_act, int grp,
+                                          const int32_t* __restrict__ pair_order,
+                                          const int32_t* __restrict__ clients,
+                                          const int32_t* __restrict__ ni_arr) {
+  HwItem it;
+  const int g0 = (L / (grp * n_pairs)) * grp;  // first client of the group
+  const int gs = min(grp, n_act - g0);
+  const int rem = L - g0 * n_pairs;
+  it.slot = g0 + rem % gs;
+  it.pair = pair_order[rem / gs];
+  it.c = client_of(clients, it.slot);
+  int J = static_cast<int>((sqrtf(8.0f * it.pair + 1.0f) - 1.0f) * 0.5f);
+  while ((J + 1) * (J + 2) / 2 <= it.pair) ++J;
+  while (J * (J + 1) / 2 > it.pair) --J;
+  it.J = J;
+  it.I = it.pair - J * (J + 1) / 2;
+  it.diag = it.I == J;
+  it.nk = (ni_arr[it.c] + HKC - 1) / HKC;
+  return it;
+}
+
+// One DMMA warp's mainloop of one item over the pipe's global stages
+// [g0, g0 + nk): its task is the MR x NC block of 8x8 fragments at fragment
+// row r0, column c0 (TRI: only the fragments on or above the diagonal).
+// GRAD: also the fused local gradient of the block's rows from the same A
+// values (before their h scaling): gpart[mi] accumulates row 8(r0+mi)+g over
+// this lane's samples; the 4 lanes of a row are summed at the end.
+template <int MR, int NC, bool TRI, bool GRAD>
+__device__ __forceinline__ void hw_consume(HwPipe& sm, bool diag, int nk, int g0, int r0, int c0,
+                                           int g, int t, int lane, uint32_t zero_mask,
+                                           double (&acc)[4][4][2], double (&gpart)[4]) {
   for (int it = 0; it < nk; ++it) {
-    const int s2 = it % HSTAGE;
-    mbar_wait(&sm.full[s2], (it / HSTAGE) & 1);
+    const int gsn = g0 + it;
+    const int s2 = gsn % HW_STAGE;
+    mbar_wait(&sm.full[s2], (gsn / HW_STAGE) & 1);
     const double* sa = sm.a[s2];
     const double* sb = diag ? sm.a[s2] : sm.b[s2];
-    uint32_t ldep = 0;  // every value loaded from the slot feeds the release
+    uint32_t ldep = 0;
 #pragma unroll
     for (int kk = 0; kk < HKC / 4; ++kk) {
-      // k-step kk reads samples {2kk, 2kk+1, 2kk+8, 2kk+9}: with the 128B
-      // swizzle every half-warp then touches 16 distinct bank pairs
       const int ks = 2 * kk + (t & 1) + 8 * (t >> 1);
       const double hv = sm.h[s2][ks];
       double af[4], bf[4];
 #pragma unroll
-      for (int mi = 0; mi < MR; ++mi) af[mi] = sa[swz(rowbase + 8 * mi + g, ks)] * hv;
+      for (int mi = 0; mi < MR; ++mi) {
+        const double raw = sa[swz(8 * (r0 + mi) + g, ks)];
+        if (GRAD) gpart[mi] = fma(raw, sm.gc[s2][ks], gpart[mi]);
+        af[mi] = raw * hv;
+      }
 #pragma unroll
-      for (int nj = 0; nj < NC; ++nj) bf[nj] = sb[swz(colbase + 8 * nj + g, ks)];
+      for (int nj = 0; nj < NC; ++nj) bf[nj] = sb[swz(8 * (c0 + nj) + g, ks)];
 #pragma unroll
       for (int q = 0; q < MR; ++q) ldep ^= dep_of(af[q]);
 #pragma unroll
@@ -95,232 +155,294 @@ __device__ __forceinline__ void hess_consume(HessSmem& sm, bool diag, int nk, in
         for (int nj = 0; nj < NC; ++nj)
           if (!TRI || mi <= nj) dmma_8x8x4(acc[mi][nj], af[mi], bf[nj]);
     }
-    // release the slot once every fragment load of this stage completed
     if (lane == 0) mbar_arrive_dep(&sm.empty[s2], ldep, zero_mask);
   }
 }
 
-// grid (n_pairs, n_active), block HTHREADS, dynamic smem HESS_SMEM.
-// Warps 0..3 compute (warp q owns quadrant rows 32*(q&1), cols 32*(q>>1));
-// warp 4 is the TMA producer.  Stage s is refilled once every active
-// consumer warp has arrived on empty[s] (no CTA-wide barrier per stage).
-// MINB = CTAs per SM the register budget is cut for (2 is used).
-template <int MINB>
-__global__ void __launch_bounds__(HTHREADS, MINB) k_hessian(
+// the (MR, NC, TRI, GRAD) instantiation of a task (MR, NC in 1..4)
+template <bool TRI, bool GRAD>
+__device__ __forceinline__ void hw_consume_any(int mr, int nc, HwPipe& sm, bool diag, int nk, int g0,
+                                               int r0, int c0, int g, int t, int lane,
+                                               uint32_t zero_mask, double (&acc)[4][4][2],
+                                               double (&gpart)[4]) {
+#define HW_CASE(M, N)                                                                          \
+  case (M) * 8 + (N):                                                                          \
+    hw_consume<M, N, TRI, GRAD>(sm, diag, nk, g0, r0, c0, g, t, lane, zero_mask, acc, gpart); \
+    break;
+  if (TRI) {
+    switch (mr * 9) {  // square blocks only
+      HW_CASE(1, 1) HW_CASE(2, 2) HW_CASE(3, 3) HW_CASE(4, 4)
+    }
+  } else {
+    switch (mr * 8 + nc) {
+      HW_CASE(1, 1) HW_CASE(1, 2) HW_CASE(1, 3) HW_CASE(1, 4)
+      HW_CASE(2, 1) HW_CASE(2, 2) HW_CASE(2, 3) HW_CASE(2, 4)
+      HW_CASE(3, 1) HW_CASE(3, 2) HW_CASE(3, 3) HW_CASE(3, 4)
+      HW_CASE(4, 1) HW_CASE(4, 2) HW_CASE(4, 3) HW_CASE(4, 4)
+    }
+  }
+#undef HW_CASE
+}
+
+// The fragment task of DMMA warp q (0..3) of an item, balanced so that the
+// four warps — one per SM sub-partition, whose DMMA pipes are separate —
+// carry equal shares (an edge or diagonal tile otherwise leaves one pipe
+// idle and another full).  nv = valid 8-row fragments of the tile's rows
+// (diagonal) or columns (off-diagonal).
+//   diagonal:     t1 = ceil(nv / 2): q0 = tri [0, t1), q3 = tri [t1, nv),
+//                 q1 / q2 = the rectangle rows [0, t1) x cols [t1, nv),
+//                 split by columns; q0 and q3 also form the gradient
+//   off-diagonal: rows 0..3 / 4..7 (q0, q1 | q2, q3) x cols split at
+//                 ceil(nv / 2)
+struct HwTask {
+  int r0, c0, mr, nc;
+  bool tri, grad;
+};
+__device__ __forceinline__ HwTask hw_task(int q, bool diag, int nv) {
+  HwTask k;
+  k.tri = false;
+  k.grad = false;
+  if (diag) {
+    const int t1 = (nv + 1) / 2, t2 = nv - t1;
+    const int ca = (t2 + 1) / 2, cb = t2 - ca;
+    if (q == 0) { k.r0 = 0; k.c0 = 0; k.mr = t1; k.nc = t1; k.tri = true; k.grad = true; }
+    else if (q == 3) { k.r0 = t1; k.c0 = t1; k.mr = t2; k.nc = t2; k.tri = true; k.grad = true; }
+    else if (q == 1) { k.r0 = 0; k.c0 = t1; k.mr = t1; k.nc = ca; }
+    else { k.r0 = 0; k.c0 = t1 + ca; k.mr = t1; k.nc = cb; }
+  } else {
+    const int ca = (nv + 1) / 2;
+    k.r0 = (q & 1) * 4;
+    k.mr = 4;
+    k.c0 = (q >> 1) ? ca : 0;
+    k.nc = (q >> 1) ? nv - ca : ca;
+  }
+  return k;
+}
+
+// release a pipe's stages [g0, g0 + nk) without reading them
+__device__ __forceinline__ void hw_skip(HwPipe& sm, int nk, int g0, int lane) {
+  for (int it = 0; it < nk; ++it) {
+    const int gsn = g0 + it, s2 = gsn % HW_STAGE;
+    mbar_wait(&sm.full[s2], (gsn / HW_STAGE) & 1);
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&sm.empty[s2]);
+  }
+}
+
+__global__ void __launch_bounds__(HW_THREADS, 1) k_hessian_ws(
     const __grid_constant__ CUtensorMap tmap_b, const DevCtl* __restrict__ ctl, int d,
     const int32_t* __restrict__ ni_arr, int ldh, const double* __restrict__ hcoef,
     const double* __restrict__ lam_arr, const int32_t* __restrict__ clients,
     const double* __restrict__ hest, int64_t hest_stride, double* __restrict__ D,
     double* __restrict__ hess_out, double* __restrict__ frob_part, int32_t* __restrict__ flags,
     uint32_t zero_mask, const double* __restrict__ gcoef, const double* __restrict__ x,
-    double* __restrict__ grad, const int32_t* __restrict__ pair_order, int n_pairs_arg, int grp,
-    const int32_t* __restrict__ dispatch) {
+    double* __restrict__ grad, const int32_t* __restrict__ pair_order, int n_pairs, int n_act,
+    int grp, int32_t* __restrict__ sched) {
+  // sched[0]: next unclaimed item, sched[1]: producers finished (the last
+  // one re-arms both for the next launch)
   // the round reduction may launch now (it waits for this pass)
   asm volatile("griddepcontrol.launch_dependents;");
   if (ctl && ctl->halt) return;
+  if (threadIdx.x == 0) tl_mark(1, false);
   extern __shared__ uint8_t smem_raw[];
-  HessSmem& sm = *reinterpret_cast<HessSmem*>(
-      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
-
-  // 1-D grid over (client group, pair, client): groups of `grp` clients in
-  // order (a group's B rows stay in L2 while its tiles run); inside a group
-  // the tile pairs go costliest first (`pair_order`), so every wave — the
-  // last one included — ends on the cheap diagonal / edge tiles
-  const int n_pairs = n_pairs_arg;
-  const int n_act = static_cast<int>(gridDim.x) / n_pairs;
-  const int L = blockIdx.x;
-  const int g0 = (L / (grp * n_pairs)) * grp;  // first client of the group
-  const int gs = min(grp, n_act - g0);
-  const int rem = L - g0 * n_pairs;
-  int slot = g0 + rem % gs;
-  int pair = pair_order[rem / gs];
-  if (dispatch) {  // explicit (pair << 16 | client slot) per CTA
-    const int v = dispatch[L];
-    slot = v & 0xFFFF;
-    pair = v >> 16;
-  }
-  const int c = client_of(clients, slot);
-  // pair -> (I, J), I <= J, column-wise like the packed layout
-  int J = static_cast<int>((sqrtf(8.0f * pair + 1.0f) - 1.0f) * 0.5f);
-  while ((J + 1) * (J + 2) / 2 <= pair) ++J;
-  while (J * (J + 1) / 2 > pair) --J;
-  const int I = pair - J * (J + 1) / 2;
-  const bool diag = (I == J);
-
+  // 1024-byte alignment by pointer arithmetic on the shared array (keeps the
+  // shared address space: LDS with 32-bit addresses, not generic loads)
+  HwPipe* pipes = reinterpret_cast<HwPipe*>(smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u));
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int g = lane >> 2, t = lane & 3;
-  const int rowbase = 32 * (warp & 1), colbase = 32 * (warp >> 1);
-  // on a diagonal tile the lower-left quadrant is entirely below the diagonal;
-  // with `grad` set that warp computes the local gradient of the tile's 64
-  // features from the same stages instead (oracle.py:108-121, fused: B is
-  // streamed once for the Hessian and the gradient)
-  const bool fuse_grad = diag && grad != nullptr;
-  const int n_active_warps = (diag && !fuse_grad) ? HCONS - 1 : HCONS;
-  const bool consumer = warp < HCONS && !(diag && rowbase > colbase);
-  const bool grad_warp = fuse_grad && warp < HCONS && rowbase > colbase;
-
-  const int nk = (ni_arr[c] + HKC - 1) / HKC;  // this client's samples (ragged shards)
-  const double lam = lam_arr[c];
-  const double* hrow = hcoef + static_cast<int64_t>(c) * ldh;
-  const double* grow = fuse_grad ? gcoef + static_cast<int64_t>(c) * ldh : nullptr;
-  const uint32_t stage_bytes =
-      (diag ? 1u : 2u) * HT * HKC * 8u + HKC * 8u + (fuse_grad ? HKC * 8u : 0u);
-
-  const long long t_start = clock64();
-  if (tid == 0) {
-    tma_prefetch_desc(&tmap_b);
-    for (int s2 = 0; s2 < HSTAGE; ++s2) {
-      mbar_init(&sm.full[s2], 1);
-      mbar_init(&sm.empty[s2], n_active_warps);
+  const int total = n_act * n_pairs;
+  if (tid < HW_PIPES) {
+    HwPipe& pp = pipes[tid];
+    for (int s2 = 0; s2 < HW_STAGE; ++s2) {
+      mbar_init(&pp.full[s2], 1);
+      mbar_init(&pp.empty[s2], HW_MMA);
     }
+    mbar_init(&pp.cs_full, HW_MMA);
+    mbar_init(&pp.cs_empty, 1);
+    if (tid == 0) tma_prefetch_desc(&tmap_b);
     fence_barrier_init();
-    sm.flag_or = 0;
   }
   __syncthreads();
+  const int64_t w = packed_len(d);
+  // warps [0, 8): DMMA (pipe = warp / 4); 8, 9: TMA of pipe 0, 1; 10, 11: epilogue of pipe 0, 1
+  const int pipe = warp < HW_PIPES * HW_MMA ? warp / HW_MMA : (warp - HW_PIPES * HW_MMA) % HW_PIPES;
+  HwPipe& sm = pipes[pipe];
 
-  double acc[4][4][2];
-#pragma unroll
-  for (int mi = 0; mi < 4; ++mi)
-#pragma unroll
-    for (int nj = 0; nj < 4; ++nj) acc[mi][nj][0] = acc[mi][nj][1] = 0.0;
-
-  if (warp == HCONS) {
-    // ---------------- TMA producer
+  if (warp >= HW_PIPES * HW_MMA && warp < HW_PIPES * HW_MMA + HW_PIPES) {
+    // ------------------------------------------------------ TMA producer
     if (lane == 0) {
-      // programmatic dependent launch: the margins kernel's coefficients
-      asm volatile("griddepcontrol.wait;" ::: "memory");
-      for (int it = 0; it < nk; ++it) {
-        const int s2 = it % HSTAGE;
-        if (it >= HSTAGE) mbar_wait(&sm.empty[s2], ((it / HSTAGE) - 1) & 1);
-        mbar_arrive_expect_tx(&sm.full[s2], stage_bytes);
-        tma_load_3d(sm.a[s2], &tmap_b, &sm.full[s2], it * HKC, I * HT, c);
-        if (!diag) tma_load_3d(sm.b[s2], &tmap_b, &sm.full[s2], it * HKC, J * HT, c);
-        bulk_load(sm.h[s2], hrow + it * HKC, HKC * 8, &sm.full[s2]);
-        if (fuse_grad) bulk_load(sm.gc[s2], grow + it * HKC, HKC * 8, &sm.full[s2]);
+      asm volatile("griddepcontrol.wait;" ::: "memory");  // margins' coefficients
+      int gsn = 0;
+      for (int j = 0;; ++j) {
+        int L = atomicAdd(&sched[0], 1);
+        if (L >= total) L = -1;
+        sm.itemq[j % HW_QUEUE] = L;
+        if (L < 0) {  // publish the end through the next stage barrier
+          const int s2 = gsn % HW_STAGE;
+          if (gsn >= HW_STAGE) mbar_wait(&sm.empty[s2], ((gsn / HW_STAGE) - 1) & 1);
+          mbar_arrive(&sm.full[s2]);
+          break;
+        }
+        const HwItem itm = hw_item(L, n_pairs, n_act, grp, pair_order, clients, ni_arr);
+        const bool fuse_grad = itm.diag && grad != nullptr;
+        const uint32_t stage_bytes =
+            (itm.diag ? 1u : 2u) * HT * HKC * 8u + HKC * 8u + (fuse_grad ? HKC * 8u : 0u);
+        const double* hrow = hcoef + static_cast<int64_t>(itm.c) * ldh;
+        const double* grow = gcoef + static_cast<int64_t>(itm.c) * ldh;
+        for (int it = 0; it < itm.nk; ++it, ++gsn) {
+          const int s2 = gsn % HW_STAGE;
+          if (gsn >= HW_STAGE) mbar_wait(&sm.empty[s2], ((gsn / HW_STAGE) - 1) & 1);
+          mbar_arrive_expect_tx(&sm.full[s2], stage_bytes);
+          tma_load_3d(sm.a[s2], &tmap_b, &sm.full[s2], it * HKC, itm.I * HT, itm.c);
+          if (!itm.diag) tma_load_3d(sm.b[s2], &tmap_b, &sm.full[s2], it * HKC, itm.J * HT, itm.c);
+          bulk_load(sm.h[s2], hrow + it * HKC, HKC * 8, &sm.full[s2]);
+          if (fuse_grad) bulk_load(sm.gc[s2], grow + it * HKC, HKC * 8, &sm.full[s2]);
+        }
+      }
+      __threadfence();
+      if (atomicAdd(&sched[1], 1) == HW_PIPES * static_cast<int>(gridDim.x) - 1) {
+        atomicExch(&sched[0], 0);  // every producer has claimed its last item
+        atomicExch(&sched[1], 0);
       }
     }
-  } else if (grad_warp) {
-    // ---------------- fused gradient: lane owns features r = lane, lane + 32
-    double g0 = 0.0, g1 = 0.0;
-    for (int it = 0; it < nk; ++it) {
-      const int s2 = it % HSTAGE;
-      mbar_wait(&sm.full[s2], (it / HSTAGE) & 1);
-      const double* sa = sm.a[s2];
-      uint32_t ldep = 0;
+    return;
+  }
+
+  if (warp < HW_PIPES * HW_MMA) {
+    // ------------------------------------------------------ DMMA warps
+    const int q4 = warp % HW_MMA;
+    const int g = lane >> 2, t = lane & 3;
+    int gsn = 0;
+    for (int j = 0;; ++j) {
+      mbar_wait(&sm.full[gsn % HW_STAGE], (gsn / HW_STAGE) & 1);  // the item's first stage (or the end)
+      const int L = sm.itemq[j % HW_QUEUE];
+      if (L < 0) {  // tell the epilogue, once it has taken the last tile
+        if (j > 0) mbar_wait(&sm.cs_empty, (j - 1) & 1);
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&sm.cs_full);
+        break;
+      }
+      const HwItem itm = hw_item(L, n_pairs, n_act, grp, pair_order, clients, ni_arr);
+      const bool fuse_grad = itm.diag && grad != nullptr;
+      const int nv = min(8, (d - itm.J * HT + 7) / 8);
+      const HwTask tk = hw_task(q4, itm.diag, nv);
+      double acc[4][4][2];
+      double gpart[4] = {0.0, 0.0, 0.0, 0.0};
 #pragma unroll
-      for (int k2 = 0; k2 < HKC; ++k2) {
-        const double gk = sm.gc[s2][k2];
-        const double v0 = sa[swz(lane, k2)], v1 = sa[swz(lane + 32, k2)];
-        ldep ^= dep_of(v0) ^ dep_of(v1) ^ dep_of(gk);
-        g0 = fma(v0, gk, g0);
-        g1 = fma(v1, gk, g1);
+      for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+        for (int nj = 0; nj < 4; ++nj) acc[mi][nj][0] = acc[mi][nj][1] = 0.0;
+      const bool active = tk.mr > 0 && tk.nc > 0;
+      if (!active) {
+        hw_skip(sm, itm.nk, gsn, lane);
+      } else if (tk.tri) {
+        if (fuse_grad)
+          hw_consume_any<true, true>(tk.mr, tk.nc, sm, true, itm.nk, gsn, tk.r0, tk.c0, g, t, lane, zero_mask, acc, gpart);
+        else
+          hw_consume_any<true, false>(tk.mr, tk.nc, sm, true, itm.nk, gsn, tk.r0, tk.c0, g, t, lane, zero_mask, acc, gpart);
+      } else {
+        hw_consume_any<false, false>(tk.mr, tk.nc, sm, itm.diag, itm.nk, gsn, tk.r0, tk.c0, g, t, lane, zero_mask, acc,
+                                     gpart);
+      }
+      gsn += itm.nk;
+      if (fuse_grad && tk.grad) {  // local gradient rows 8 r0 .. (oracle.py:108-121)
+        const double lam = lam_arr[itm.c];
+#pragma unroll
+        for (int mi = 0; mi < 4; ++mi) {
+          double v = gpart[mi];
+          v += __shfl_xor_sync(0xffffffffu, v, 1);
+          v += __shfl_xor_sync(0xffffffffu, v, 2);
+          const int a = itm.I * HT + 8 * (tk.r0 + mi) + g;
+          if (mi < tk.mr && t == 0 && a < d)
+            grad[static_cast<int64_t>(itm.c) * d + a] = __dadd_rn(v, __dmul_rn(lam, x[a]));
+        }
+      }
+      // hand the accumulators to the epilogue once it has read the last tile
+      if (j > 0) mbar_wait(&sm.cs_empty, (j - 1) & 1);
+      if (active) {
+#pragma unroll
+        for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+          for (int nj = 0; nj < 4; ++nj)
+            if (mi < tk.mr && nj < tk.nc)
+#pragma unroll
+              for (int e = 0; e < 2; ++e)
+                sm.cs[(8 * (tk.c0 + nj) + 2 * t + e) * HW_LD + 8 * (tk.r0 + mi) + g] = acc[mi][nj][e];
       }
       __syncwarp();
-      if (lane == 0) mbar_arrive_dep(&sm.empty[s2], ldep, zero_mask);
+      if (lane == 0) mbar_arrive(&sm.cs_full);
     }
-    const double* xc = x;
-#pragma unroll
-    for (int h2 = 0; h2 < 2; ++h2) {
-      const int a = I * HT + lane + 32 * h2;
-      if (a < d)
-        grad[static_cast<int64_t>(c) * d + a] = __dadd_rn(h2 ? g1 : g0, __dmul_rn(lam, xc[a]));
-    }
-  } else if (consumer) {
-    // ---------------- DMMA consumers, specialised per quadrant shape
-    const int vr = (d - (I * HT + rowbase) + 7) / 8, vc = (d - (J * HT + colbase) + 7) / 8;
-    const int mr = vr >= 3 ? 4 : 2, nc = vc >= 3 ? 4 : 2;  // vr, vc >= 1 for an active quadrant
-    const bool tri = diag && rowbase == colbase;
-    if (tri) {
-      if (mr == 4) hess_consume<4, 4, true>(sm, diag, nk, rowbase, colbase, g, t, lane, zero_mask, acc);
-      else hess_consume<2, 2, true>(sm, diag, nk, rowbase, colbase, g, t, lane, zero_mask, acc);
-    } else if (mr == 4 && nc == 4) {
-      hess_consume<4, 4, false>(sm, diag, nk, rowbase, colbase, g, t, lane, zero_mask, acc);
-    } else if (mr == 4) {
-      hess_consume<4, 2, false>(sm, diag, nk, rowbase, colbase, g, t, lane, zero_mask, acc);
-    } else if (nc == 4) {
-      hess_consume<2, 4, false>(sm, diag, nk, rowbase, colbase, g, t, lane, zero_mask, acc);
-    } else {
-      hess_consume<2, 2, false>(sm, diag, nk, rowbase, colbase, g, t, lane, zero_mask, acc);
-    }
+    return;
   }
-  __syncthreads();  // all stages consumed; the ring is free for the epilogue
-  const long long t_main = clock64();
 
-  // ---- epilogue: stage the tile column-major, then stream packed columns
-  double* cs = &sm.a[0][0];  // [64 cols][HC_LD] — reuses the pipeline ring
-  if (consumer) {
+  // ------------------------------------------------------------ epilogue
+  for (int j = 0;; ++j) {
+    mbar_wait(&sm.cs_full, j & 1);
+    const int L = sm.itemq[j % HW_QUEUE];
+    if (L < 0) break;
+    const HwItem itm = hw_item(L, n_pairs, n_act, grp, pair_order, clients, ni_arr);
+    const double* hest_c = hest + static_cast<int64_t>(itm.c) * hest_stride;
+    const double lam = lam_arr[itm.c];
+    double* Dc = D + static_cast<int64_t>(itm.c) * w;
+    double* Hc = hess_out ? hess_out + static_cast<int64_t>(itm.slot) * w : nullptr;
+    const int ncol = min(HT, d - itm.J * HT);
+    // the first chunk's H_i^k operands before the tile lands
+    constexpr int ECH = 8;  // columns per chunk: 16 loads in flight per lane
+    double hk[ECH][2];
+    auto load_chunk = [&](int c0) {
 #pragma unroll
-    for (int mi = 0; mi < 4; ++mi)
+      for (int q = 0; q < ECH; ++q) {
+        const int col = c0 + q, b = itm.J * HT + col;
 #pragma unroll
-      for (int nj = 0; nj < 4; ++nj)
-#pragma unroll
-        for (int e = 0; e < 2; ++e) {
-          const int r = rowbase + 8 * mi + g;
-          const int col = colbase + 8 * nj + 2 * t + e;
-          cs[col * HC_LD + r] = acc[mi][nj][e];
+        for (int h2 = 0; h2 < 2; ++h2) {
+          const int a = itm.I * HT + lane + 32 * h2;
+          hk[q][h2] = (col < ncol && a <= b) ? __ldg(hest_c + packed_at(a, b)) : 0.0;
         }
-  }
-  __syncthreads();
-
-  const double* hest_c = hest + static_cast<int64_t>(c) * hest_stride;
-  const int64_t w = packed_len(d);
-  double* Dc = D + static_cast<int64_t>(c) * w;
-  double* Hc = hess_out ? hess_out + static_cast<int64_t>(slot) * w : nullptr;
-  double part = 0.0;
-  int fl = 0;
-  // every warp (producer included) streams columns col = warp, warp + 5, ...;
-  // the H_i^k operands of all its (column, row) pairs are loaded first so
-  // the global-memory latency is paid once per warp, not once per column
-  constexpr int NW = HTHREADS / 32;
-  constexpr int MAXC = (HT + NW - 1) / NW;  // columns per warp
-  double hk[MAXC][2];
+      }
+    };
+    load_chunk(0);
+    double part = 0.0;
+    int fl = 0;
+    for (int c0 = 0; c0 < ncol; c0 += ECH) {
+      double hv[ECH][2];
 #pragma unroll
-  for (int q = 0; q < MAXC; ++q) {
-    const int col = warp + q * NW;
-    const int b = J * HT + col;
+      for (int q = 0; q < ECH; ++q)
 #pragma unroll
-    for (int h2 = 0; h2 < 2; ++h2) {
-      const int a = I * HT + lane + 32 * h2;
-      const bool ok = col < HT && b < d && a <= b && a < d;
-      hk[q][h2] = ok ? __ldg(hest_c + packed_at(a, b)) : 0.0;
+        for (int h2 = 0; h2 < 2; ++h2) hv[q][h2] = sm.cs[(c0 + q) * HW_LD + lane + 32 * h2];
+      double hkc[ECH][2];
+#pragma unroll
+      for (int q = 0; q < ECH; ++q) hkc[q][0] = hk[q][0], hkc[q][1] = hk[q][1];
+      if (c0 + ECH < ncol) load_chunk(c0 + ECH);  // the next chunk's loads in flight
+#pragma unroll
+      for (int q = 0; q < ECH; ++q) {
+        const int col = c0 + q, b = itm.J * HT + col;
+        if (col >= ncol) continue;
+        const int64_t cbase = packed_at(0, b);
+#pragma unroll
+        for (int h2 = 0; h2 < 2; ++h2) {
+          const int a = itm.I * HT + lane + 32 * h2;
+          if (a > b) continue;
+          double h = hv[q][h2];
+          if (a == b) h = __dadd_rn(h, lam);
+          const double dv = __dsub_rn(h, hkc[q][h2]);
+          Dc[cbase + a] = dv;
+          if (Hc) Hc[cbase + a] = h;
+          const double wt = (a == b) ? 1.0 : 2.0;
+          part = fma(__dmul_rn(wt, dv), dv, part);
+          if (!isfinite(dv)) fl |= 1;
+          if (dv != 0.0) fl |= 2;
+        }
+      }
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&sm.cs_empty);  // the DMMA warps may stage the next tile
+    part = warp_sum(part);
+    fl = __reduce_or_sync(0xffffffffu, fl);
+    if (lane == 0) {
+      frob_part[static_cast<int64_t>(itm.c) * n_pairs + itm.pair] = part;
+      if (fl) atomicOr(&flags[itm.c], fl);
     }
   }
-#pragma unroll
-  for (int q = 0; q < MAXC; ++q) {
-    const int col = warp + q * NW;
-    const int b = J * HT + col;
-    if (col >= HT || b >= d) continue;
-    const int64_t cbase = packed_at(0, b);
-#pragma unroll
-    for (int h2 = 0; h2 < 2; ++h2) {
-      const int r = lane + 32 * h2;
-      const int a = I * HT + r;
-      if (a > b || a >= d) continue;
-      const int64_t tt = cbase + a;
-      double hv = cs[col * HC_LD + r];
-      if (a == b) hv = __dadd_rn(hv, lam);
-      const double dv = __dsub_rn(hv, hk[q][h2]);
-      Dc[tt] = dv;
-      if (Hc) Hc[tt] = hv;
-      const double wt = (a == b) ? 1.0 : 2.0;
-      part = fma(__dmul_rn(wt, dv), dv, part);
-      if (!isfinite(dv)) fl |= 1;
-      if (dv != 0.0) fl |= 2;
-    }
-  }
-  const double tot = block_sum(part, sm.red);
-  if (fl) atomicOr(&sm.flag_or, fl);
-  __syncthreads();
-  if (tid == 0) {
-    frob_part[static_cast<int64_t>(c) * n_pairs + pair] = tot;
-    if (sm.flag_or) atomicOr(&flags[c], sm.flag_or);
-    if (g_dbg_on) {  // diagnostics: CTA-summed mainloop / epilogue cycles
-      const long long t_end = clock64();
-      atomicAdd(reinterpret_cast<unsigned long long*>(&g_dbg[20]), static_cast<unsigned long long>(t_main - t_start));
-      atomicAdd(reinterpret_cast<unsigned long long*>(&g_dbg[21]), static_cast<unsigned long long>(t_end - t_main));
-      atomicAdd(reinterpret_cast<unsigned long long*>(&g_dbg[22]), 1ull);
-    }
-  }
+  if (lane == 0) tl_mark(1, true);
 }
 
 }  // namespace fb

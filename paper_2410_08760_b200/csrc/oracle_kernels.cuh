@@ -156,6 +156,7 @@ __global__ void __launch_bounds__(NT, NS > 1 ? 2 : 1) k_margins_cpc(
   if (ctl && ctl->halt) return;
   extern __shared__ double mcs[];
   __shared__ double red[NT / 32];
+  if (threadIdx.x == 0) tl_mark(0, false);
   const int c = client_of(clients, blockIdx.x / NS);
   const int ni = ni_arr[c];
   const int part = blockIdx.x % NS;
@@ -231,6 +232,7 @@ __global__ void __launch_bounds__(NT, NS > 1 ? 2 : 1) k_margins_cpc(
       hcoef[static_cast<int64_t>(c) * ldh + js] = 0.0;
       gcoef[static_cast<int64_t>(c) * ldh + js] = 0.0;
     }
+  if (tid == 0) tl_mark(0, true);
 }
 
 // Local gradients g_c = B_c gcoef_c + lam x (oracle.py:108-121).

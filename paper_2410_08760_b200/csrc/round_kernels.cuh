@@ -222,6 +222,7 @@ __global__ void __launch_bounds__(FOLD_THREADS) k_master_fold(
     const double* __restrict__ val_list, double alpha_n, const double* h_in, double* h_out,
     double* __restrict__ hest = nullptr, int64_t hest_stride = 0, double alpha = 0.0) {
   if (ctl->halt) return;
+  if (threadIdx.x == 0) tl_mark(5, false);
   extern __shared__ int32_t fold_sm[];  // beg[n], cnt[n], off[n+1]
   __shared__ double hs[FOLD_RANGE];
   __shared__ uint16_t st_t[FOLD_STAGE];
@@ -317,6 +318,7 @@ __global__ void __launch_bounds__(FOLD_THREADS) k_master_fold(
     ca = cb;
   }
   for (int i = threadIdx.x; i < len; i += FOLD_THREADS) h_out[t0 + i] = hs[i];
+  if (threadIdx.x == 0) tl_mark(5, true);
 }
 
 // Round epilogue (algorithms.py:385-387): x <- x_new, round += 1,
@@ -337,6 +339,7 @@ __global__ void __launch_bounds__(256) k_finish(
   for (int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; t < hcopy_n;
        t += static_cast<int64_t>(gridDim.x) * blockDim.x)
     hcopy_dst[t] = hcopy_src[t];
+  if (threadIdx.x == 0) tl_mark(6, false);
   if (blockIdx.x != 0) return;
   if (ctl->halt) return;
   __shared__ int bad;

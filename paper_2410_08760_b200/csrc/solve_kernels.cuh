@@ -673,6 +673,7 @@ __global__ void __launch_bounds__(CH_THREADS, 1) k_chol_panels(
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int npan = (d + CP_NB - 1) / CP_NB;
   const int RS = cp_rows(d);
+  if (tid == 0) tl_mark(2, false);
   long long t_mark = clock64();
   auto mark = [&](int slot) {
     if (CP_MARKS && dbg && tid == 0 && rank == 0) {
@@ -777,7 +778,9 @@ __global__ void __launch_bounds__(CH_THREADS, 1) k_chol_panels(
   // launch: this kernel may start while k_reduce still runs); the shift and
   // the right-hand side come from k_reduce, so wait for it here.  Without a
   // programmatic dependency the wait returns at once.
+  if (tid == 0) tl_mark(3, false);
   asm volatile("griddepcontrol.wait;" ::: "memory");
+  if (tid == 0) tl_mark(3, true);
   double shift = 0.0;
   const bool fused = red.grad != nullptr;
   bool skip_solve = false;  // fused reduction found a non-finite client (uniform)
@@ -1294,6 +1297,7 @@ __global__ void __launch_bounds__(CH_THREADS, 1) k_chol_panels(
     }
   }
   cluster.sync();  // no CTA leaves while its shared memory may be addressed
+  if (tid == 0) tl_mark(2, true);
   if (dbg)
     for (int i = tid; i < (CP_MAXP + 1) * 16; i += CH_THREADS) {
       const int row = i / 16, k = i % 16;

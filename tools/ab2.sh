@@ -1,0 +1,8 @@
+# production-graph c0 rounds/s for several library builds (A/B)
+run() { timeout 300 python bench.py --config c0 --no-cpu-baseline 2>/dev/null | python -c "import json,sys; d=json.loads(sys.stdin.read()); print('$1', d['value'], d['kernels_ms']['hessian'], d['kernels_ms']['round'])"; }
+cp paper_2410_08760_b200/libfednl_b200.so /tmp/cur.so
+for v in cur nopdl old cur nopdl old; do
+  if [ $v = cur ]; then cp /tmp/cur.so paper_2410_08760_b200/libfednl_b200.so; else cp tools/probe/lib_$v.so paper_2410_08760_b200/libfednl_b200.so; fi
+  run $v
+done
+cp /tmp/cur.so paper_2410_08760_b200/libfednl_b200.so
