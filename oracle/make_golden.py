@@ -544,6 +544,40 @@ def gen_sim_r2():
     return out
 
 
+def gaussian_shards_c4(d=1024, n=512, ni=2048, lam=1e-4, seed=1):
+    """SURVEY §8(d) c4 generator (numpy default_rng), as
+    paper_2410_08760_b200.data.gaussian_shards builds it, as reference
+    ClientShards."""
+    g = np.random.default_rng(seed)
+    wstar = g.standard_normal(d - 1) / np.sqrt(d)
+    out = []
+    for _ in range(n):
+        a = g.standard_normal((d - 1, ni))
+        y = np.sign(wstar @ a + g.normal(0.0, np.sqrt(0.1), ni))
+        y[y == 0] = 1.0
+        b = np.empty((d, ni), order="F")
+        b[: d - 1] = a
+        b[d - 1] = 1.0
+        b *= y
+        out.append(ClientShard(bmat=b, lam=lam))
+    return out
+
+
+def gen_c4():
+    """Two c4 rounds (d=1024, n=512, n_i=2048, TopK k=8192, lambda=1e-4) from
+    the reference simulate (8 worker threads, 1 BLAS thread each: the rows do
+    not depend on the worker count, runtime.py:141-143)."""
+    import threadpoolctl
+
+    shards = gaussian_shards_c4()
+    cfg = RunConfig(compressor=CompressorSpec(CompressorKind.TOPK, k=8192), rounds=2, lam=1e-4, run_seed=1)
+    with threadpoolctl.threadpool_limits(1, "blas"):
+        rows = simulate(cfg, shards, workers=8)
+    out = {f"c4_r2__{k}": v for k, v in rows_arrays(rows).items()}
+    print(f"  c4: {len(rows)} rows, |g| {[r.grad_norm for r in rows]}")
+    return out
+
+
 def gen_sim_opt_a():
     return gen_sim([n for n in SIM_CASES if "opt_a" in n])
 
@@ -562,6 +596,7 @@ def main(only=None):
         ("simulate_opt_a.npz", gen_sim_opt_a),
         ("ingest.npz", gen_ingest),
         ("simulate_r2.npz", gen_sim_r2),
+        ("simulate_c4.npz", gen_c4),
     ):
         if only and fname not in only:
             continue
