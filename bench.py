@@ -16,9 +16,10 @@ reference  the reference algorithm's CPU path (the oracle port; the reference
            is pure Python and not installed on the GPU box) on all host
            cores, one round per step; rank 0 only under torchrun.
 
-N > 1 (torchrun): independent replicas of the single-GPU run, one per rank
-(client sharding across GPUs is the next §8(f) item); value = sum over
-ranks of rounds / max-over-ranks device time.
+N > 1 (torchrun): FedNL and FedNL-LS shard the clients over the ranks
+(fb_set_shard: per-round NCCL all-gathers, every rank holds the identical
+master state; "scaling": "strong", value = rounds / max-over-ranks device
+time); FedNL-PP runs independent replicas (value = sum over ranks).
 """
 
 from __future__ import annotations
@@ -26,7 +27,6 @@ from __future__ import annotations
 import argparse
 import json
 import os
-import subprocess
 import sys
 import threading
 import time
@@ -46,65 +46,64 @@ def _env_rank():
 
 
 class ClockSampler:
-    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+    """SM clocks and clock-event (throttle) reasons sampled DURING the timed
+    region: an NVML thread polling every ~0.2 ms (a c0 run of 20 rounds lasts
+    under 10 ms, below nvidia-smi's 10 ms period)."""
 
-    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
-         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    NAMES = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
 
     def __init__(self, gpu: int):
         self.gpu = gpu
-        self.proc = None
-        self.lines: list[str] = []
+        self.samples: list[tuple[float, int]] = []  # (sm MHz, reasons bitmask)
+        self.smax = None
+        self.stop = threading.Event()
+        self.nv = None
 
     def __enter__(self):
         try:
-            self.proc = subprocess.Popen(
-                ["nvidia-smi", f"--id={self.gpu}", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
-                 "-lms", "10"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self.t = threading.Thread(target=self._read, daemon=True)
+            import pynvml as nv
+
+            nv.nvmlInit()
+            self.nv = nv
+            self.h = nv.nvmlDeviceGetHandleByIndex(self.gpu)
+            self.smax = float(nv.nvmlDeviceGetMaxClockInfo(self.h, nv.NVML_CLOCK_SM))
+            self.bits = {
+                "hw_slowdown": nv.nvmlClocksEventReasonHwSlowdown,
+                "hw_thermal_slowdown": nv.nvmlClocksEventReasonHwThermalSlowdown,
+                "sw_thermal_slowdown": nv.nvmlClocksEventReasonSwThermalSlowdown,
+                "sw_power_cap": nv.nvmlClocksEventReasonSwPowerCap,
+            }
+            self.t = threading.Thread(target=self._poll, daemon=True)
             self.t.start()
-            # nvidia-smi needs a moment to start: the timed region begins once
-            # it is sampling, and only samples taken inside the region count
-            t_end = time.time() + 5.0
-            while not self.lines and time.time() < t_end and self.proc.poll() is None:
-                time.sleep(0.005)
-            self.skip = len(self.lines)
-        except (OSError, FileNotFoundError):
-            self.proc = None
+        except Exception:  # noqa: BLE001 - no NVML: no samples (reported as such)
+            self.nv = None
         return self
 
-    def _read(self):
-        for line in self.proc.stdout:
-            self.lines.append(line.strip())
+    def _poll(self):
+        nv = self.nv
+        while not self.stop.is_set():
+            try:
+                sm = nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM)
+                rs = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                self.samples.append((float(sm), int(rs)))
+            except Exception:  # noqa: BLE001
+                return
+            time.sleep(0.0002)
 
     def __exit__(self, *exc):
-        self.n_in = len(self.lines)
-        if self.proc is not None:
-            self.proc.terminate()
-            try:
-                self.proc.wait(timeout=5)
-            except subprocess.TimeoutExpired:
-                self.proc.kill()
+        self.stop.set()
+        if self.nv is not None:
+            self.t.join(timeout=2)
 
     def summary(self) -> dict:
-        sm, smax, reasons = [], 0.0, set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in self.lines[getattr(self, "skip", 0):getattr(self, "n_in", len(self.lines))]:
-            p = [x.strip() for x in ln.split(",")]
-            if len(p) < 9:
-                continue
-            try:
-                sm.append(float(p[1]))
-                smax = max(smax, float(p[2]))
-            except ValueError:
-                continue
-            for nm, v in zip(names, p[5:9]):
-                if v.lower().startswith("active"):
+        sm = sorted(v for v, _ in self.samples)
+        reasons = set()
+        for _, rs in self.samples:
+            for nm in self.NAMES:
+                if rs & self.bits[nm]:
                     reasons.add(nm)
-        sm.sort()
-        return {"sm_mhz": sm[len(sm) // 2] if sm else None, "sm_max_mhz": smax or None,
-                "reasons": sorted(reasons), "samples": len(sm)}
+        return {"sm_mhz": sm[len(sm) // 2] if sm else None, "sm_max_mhz": self.smax,
+                "reasons": sorted(reasons), "samples": len(sm), "source": "NVML, ~0.2 ms period"}
 
 
 # ------------------------------------------------------------------- peaks
@@ -126,6 +125,43 @@ def build_inputs(config: str):
 
     shards = D.baseline_shards(config, seed=1)
     return shards
+
+
+def workload_label(config: str) -> str:
+    """The workload string both arms print (the driver compares them)."""
+    from paper_2410_08760_b200.data import BASELINE_CONFIGS
+
+    c = BASELINE_CONFIGS[config]
+    alg = {"fednl": "FedNL option b", "fednl-ls": "FedNL-LS option b (c=0.49, gamma=0.5)",
+           "fednl-pp": f"FedNL-PP option b (tau={c.get('tau')})"}[c["algorithm"]]
+    kind = {"topk": "TopK", "toplek": "TopLEK", "randk": "RandK", "randseqk": "RandSeqK"}[c["kind"]]
+    alpha = "alpha=1" if c["alpha"] == 1.0 else "alpha default"
+    gen = ("sparse-binary features" if c["gen"] == "binary" else "dense Gaussian features")
+    return (f"{config}: {alg}, {kind} k={c['k']}, {alpha}, d={c['d']}, n={c['n']}, n_i={c['ni']}, "
+            f"lambda={c['lam']:g}, {gen}")
+
+
+def data_label(config: str) -> str:
+    from paper_2410_08760_b200.data import BASELINE_CONFIGS
+
+    c = BASELINE_CONFIGS[config]
+    if c["gen"] == "binary":
+        return "synthetic (SURVEY §8(d) sparse-binary stand-in for the paper's LIBSVM shape, seed 1)"
+    return "synthetic (SURVEY §8(d) dense Gaussian stress input, numpy default_rng seed 1)"
+
+
+def hessian_traffic(config: str):
+    """ncu DRAM bytes per Hessian launch (dram__bytes_read.sum +
+    dram__bytes_write.sum), from the committed capture of the current kernel."""
+    tpath = os.path.join(ROOT, "profiles", "hessian_traffic.json")
+    if not os.path.exists(tpath):
+        return None, None
+    with open(tpath) as fh:
+        t = json.load(fh)
+    e = t.get(config)
+    if not isinstance(e, dict):
+        return None, None
+    return e.get("bytes_per_launch"), e.get("source")
 
 
 def algorithmic_counts(config: str) -> dict:
@@ -169,11 +205,11 @@ def run_ours(args) -> dict | None:
     d, n, ni = shards[0].dim, len(shards), shards[0].n_samples
     counts = algorithmic_counts(args.config)
 
-    # ---- multi-GPU (torchrun): FedNL shards the clients over the ranks
-    # (fb_set_shard: per-round NCCL all-gathers, bit-identical master state on
-    # every rank); FedNL-LS / PP run independent replicas
+    # ---- multi-GPU (torchrun): FedNL / FedNL-LS shard the clients over the
+    # ranks (fb_set_shard: per-round NCCL all-gathers, bit-identical master
+    # state on every rank); FedNL-PP runs independent replicas
     dist = None
-    sharded = world > 1 and cfg.algorithm == "fednl"
+    sharded = world > 1 and cfg.algorithm in ("fednl", "fednl-ls")
     nccl_id = None
     if world > 1:
         import torch
@@ -188,14 +224,14 @@ def run_ours(args) -> dict | None:
             nccl_id = box[0]
 
     def make_engine():
-        e = FedNLEngine(cfg, d, n, ni, lam=shards[0].lam)
+        e = FedNLEngine(cfg, d, n, ni)
         if sharded:
             e.set_shard(world, rank, nccl_id)
         return e
 
     # ---- device-resident throughput (value) + per-kernel CUDA events
     eng = make_engine()
-    eng.upload([s.bmat for s in shards])
+    eng.upload([s.bmat for s in shards], [s.lam for s in shards])
     eng.init_state()
     eng.run_rounds(W)  # warm-up: graph capture, caches, clocks
     if dist is not None:
@@ -229,7 +265,7 @@ def run_ours(args) -> dict | None:
     if sharded:  # the sharded engine from host shards: upload, init, K rounds, rows back
         t0 = time.perf_counter()
         e2 = make_engine()
-        e2.upload([s.bmat for s in shards])
+        e2.upload([s.bmat for s in shards], [s.lam for s in shards])
         e2.init_state()
         rows = e2.run_rounds(K)
         e2.close()
@@ -261,13 +297,9 @@ def run_ours(args) -> dict | None:
     hbm = float(peaks.get("hbm_gbs", 6650.0))
     comp_gbs = counts["compress_bytes"] / (prof["ms_compress"] * 1e-3) / 1e9 if prof["ms_compress"] else None
     fold_gbs = counts["fold_bytes"] / (prof["ms_fold"] * 1e-3) / 1e9 if prof["ms_fold"] else None
-    traffic = None
-    tpath = os.path.join(ROOT, "profiles", "hessian_traffic.json")
-    if os.path.exists(tpath):
-        with open(tpath) as fh:
-            traffic = json.load(fh).get(args.config)
+    traffic, traffic_src = hessian_traffic(args.config)
 
-    cpu = None if args.no_cpu_baseline else cpu_baseline(args.config, rounds=args.cpu_rounds)
+    cpu = None if args.no_cpu_baseline else cpu_baseline(args.config, budget_s=args.cpu_seconds)
 
     return {
         "metric": METRIC,
@@ -281,11 +313,12 @@ def run_ours(args) -> dict | None:
         "scaling": "strong" if sharded else "weak",
         "vs_baseline": None,
         "dtype": "f64",
-        "data": "synthetic (SURVEY §8(d) sparse-binary stand-in for the W8A shape, seed 1)",
+        "data": data_label(args.config),
         "config": {
-            "workload": f"{args.config}: FedNL option b, TopK k=8d, alpha=1, d={d}, n={n}, n_i={ni}, lambda=1e-3",
+            "workload": workload_label(args.config),
             "rounds_per_step": 1,
-            "l2": "inputs larger than L2: per-round working set B 119.7 MB + H_i^k 51.6 MB + D 51.6 MB > 126 MB",
+            "l2": (f"inputs larger than L2: per-round working set B {n * d * ni * 8 / 1e6:.1f} MB + "
+                   f"H_i^k {n * counts['w'] * 8 / 1e6:.1f} MB + D {n * counts['w'] * 8 / 1e6:.1f} MB > 126 MB"),
             "parallelism": ("single GPU" if world == 1 else
                             f"clients sharded over {world} GPUs (NCCL all-gathers per round)" if sharded
                             else f"{world} independent replicas"),
@@ -300,17 +333,19 @@ def run_ours(args) -> dict | None:
         },
         "gpu_launches": int(prof["launches_per_round"]) * K,
         "roofline": {
-            "kernel": "k_hessian (fp64 DMMA.8x8x4 SYRK + shift-difference epilogue)",
+            "kernel": "k_hessian_ws (fp64 DMMA.8x8x4 SYRK + shift-difference epilogue)",
             "bound": "tensor",
             "achieved": round(achieved, 3),
             "peak": round(dmma_peak, 3),
             "unit": "TFLOP/s",
             "frac": round(achieved / dmma_peak, 4),
             "traffic": traffic,
+            "traffic_unit": "bytes per launch",
+            "traffic_source": traffic_src,
             "peak_source": "in-repo fp64 DMMA microbenchmark (MEASURED_PEAKS.json has no fp64 entry)",
             "algorithmic_flop_per_launch": counts["hessian_flop"],
             "ms_per_launch": round(hess_ms, 5),
-            "timing": (f"CUDA events around k_hessian on the round stream, {K} rounds of the "
+            "timing": (f"CUDA events around k_hessian_ws on the round stream, {K} rounds of the "
                        "event-instrumented round graph run right after the timed region"),
         },
         "kernels_ms": {k[3:]: round(v, 5) for k, v in prof.items() if k.startswith("ms_")},
@@ -348,32 +383,45 @@ def _limit_blas_threads() -> None:
         pass
 
 
-def _cpu_sim(config: str, rounds: int, warmup: int, workers: int):
+def _cpu_run(config: str, workers: int):
     from oracle import fednl_oracle as O
     from paper_2410_08760_b200.data import baseline_run_config
 
     shards = build_inputs(config)
-    cfg = O.OracleConfig.from_run_config(baseline_run_config(config, rounds=rounds))
-    run = O.OracleRun(cfg, [s.bmat for s in shards], lam=shards[0].lam, workers=workers)
-    try:
-        run.init()
-        for r in range(warmup):
-            run.fednl_round(r)
-        t0 = time.perf_counter()
-        for r in range(warmup, warmup + rounds):
-            run.fednl_round(r)
-        return time.perf_counter() - t0
-    finally:
-        run.close()
+    cfg = O.OracleConfig.from_run_config(baseline_run_config(config, rounds=10**6))
+    run = O.OracleRun(cfg, [s.bmat for s in shards], lam=[s.lam for s in shards], workers=workers)
+    run.init()
+    return run
 
 
-def cpu_baseline(config: str, rounds: int = 4) -> dict:
+def _cpu_round(run, r: int) -> None:
+    if run.cfg.algorithm == "fednl-pp":
+        run.pp_round(r)
+    else:
+        run.fednl_round(r)
+
+
+def cpu_baseline(config: str, budget_s: float = 12.0) -> dict:
+    """The oracle port (oracle/, pinned to the reference's own rows) on the
+    host cores: rounds run until `budget_s` of CPU time has elapsed (at least
+    4), after one warm-up round."""
     _limit_blas_threads()
     workers = os.cpu_count() or 1
-    dt = _cpu_sim(config, rounds, 1, workers)
+    run = _cpu_run(config, workers)
+    try:
+        _cpu_round(run, 0)
+        t0 = time.perf_counter()
+        r = 1
+        while r < 5 or time.perf_counter() - t0 < budget_s:
+            _cpu_round(run, r)
+            r += 1
+        dt = time.perf_counter() - t0
+    finally:
+        run.close()
+    rounds = r - 1
     return {"value": round(rounds / dt, 4), "unit": "rounds/s", "cores": workers, "kind": "port",
-            "sample": f"{rounds} FedNL rounds of {config} after 1 warm-up round (numpy oracle port, "
-                      f"{workers} worker threads, OpenBLAS 1 thread each)"}
+            "sample": f"{rounds} rounds of {config} ({dt:.1f} s) after 1 warm-up round: numpy oracle port, "
+                      f"{workers} worker threads, OpenBLAS 1 thread each"}
 
 
 def run_reference(args) -> dict | None:
@@ -383,14 +431,23 @@ def run_reference(args) -> dict | None:
     _limit_blas_threads()
     workers = os.cpu_count() or 1
     K, W = args.steps, args.warmup
-    dt = _cpu_sim(args.config, K, W, workers)
+    run = _cpu_run(args.config, workers)
+    try:
+        for r in range(W):
+            _cpu_round(run, r)
+        t0 = time.perf_counter()
+        for r in range(W, W + K):
+            _cpu_round(run, r)
+        dt = time.perf_counter() - t0
+    finally:
+        run.close()
     v = K / dt
     return {
         "metric": METRIC, "value": round(v, 4), "unit": "rounds/s", "n_gpus": world, "steps": K,
         "warmup": W, "ms_per_step": round(1e3 * dt / K, 3), "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic (SURVEY §8(d) sparse-binary stand-in for the W8A shape, seed 1)",
-        "config": {"workload": f"{args.config}: FedNL option b, TopK k=8d, alpha=1, d=301, n=142, n_i=350",
+        "data": data_label(args.config),
+        "config": {"workload": workload_label(args.config),
                    "rounds_per_step": 1, "parallelism": f"CPU, {workers} threads"},
         "impl": "reference",
         "cpu_baseline": {"value": round(v, 4), "unit": "rounds/s", "cores": workers, "kind": "port",
@@ -407,7 +464,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--config", default="c0")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--cpu-rounds", type=int, default=4)
+    ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
     if args.warmup < 3:
