@@ -578,6 +578,54 @@ def gen_c4():
     return out
 
 
+def gen_compress_r2():
+    """Compressors past the one-CTA envelope of round 1: TopLEK at w = 45,451
+    (d = 301: the paper's W8A TopLEK[8d] shape) on tie-heavy round-0 c0
+    differences and on Gaussian inputs; RandK with k > 6000."""
+    out = {}
+    shards = baseline_shards("c0")
+    d = shards[0].dim
+    x = np.zeros(d)
+    g = np.random.default_rng(99)
+    inputs = {}
+    for cid in (0, 5, 77):
+        sh = shards[cid]
+        s = oracle.new_scratch(sh)
+        oracle.refresh_scratch(sh, x, s)
+        h = oracle.hessian(sh, x, s)
+        linalg.add_to_diagonal(h, -sh.lam)
+        inputs[f"c0client{cid}_round0"] = linalg.pack_upper(h)
+    a = g.standard_normal((d, d))
+    inputs["gauss301"] = linalg.pack_upper(np.asfortranarray((a + a.T) / 2))
+    names = sorted(inputs)
+    for name in names:
+        pk = inputs[name]
+        out[f"{name}__input"] = pk
+        m = linalg.unpack_to_symmetric(pk, d)
+        for kind, k in (("toplek", 301), ("toplek", 2408), ("toplek", 20000), ("randk", 8000),
+                        ("randk", 30000)):
+            for seed in (3, 0xC0FFEE):
+                prg = rng.Prg(seed)
+                delta = compress(m, CompressorSpec(CompressorKind(kind), k=k), prg)
+                tag = f"{name}__{kind}__k{k}__s{seed}"
+                out[tag + "__idx"] = np.asarray(delta.indices, dtype=np.uint32)
+                out[tag + "__val"] = np.asarray(delta.values, dtype=float)
+                out[tag + "__next"] = np.array(prg.next_u64(), dtype=np.uint64)
+    out["names"] = np.array(names)
+    out["d"] = np.array(d)
+    # FedNL-LS with TopLEK[8d] on the c0 data (the W8A TopLEK run's shape)
+    import threadpoolctl
+
+    cfg = RunConfig(algorithm="fednl-ls", compressor=CompressorSpec(CompressorKind.TOPLEK, k=8 * d),
+                    rounds=6, run_seed=1)
+    with threadpoolctl.threadpool_limits(1, "blas"):
+        rows = simulate(cfg, shards)
+    for k2, v in rows_arrays(rows).items():
+        out[f"ls_toplek8d_c0__{k2}"] = v
+    print(f"  ls_toplek8d_c0: |g| {[r.grad_norm for r in rows]}")
+    return out
+
+
 def gen_sim_opt_a():
     return gen_sim([n for n in SIM_CASES if "opt_a" in n])
 
@@ -597,6 +645,7 @@ def main(only=None):
         ("ingest.npz", gen_ingest),
         ("simulate_r2.npz", gen_sim_r2),
         ("simulate_c4.npz", gen_c4),
+        ("compress_r2.npz", gen_compress_r2),
     ):
         if only and fname not in only:
             continue

@@ -1879,14 +1879,26 @@ __global__ void __launch_bounds__(256) k_randseqk(
 // starts).
 // dynamic smem: pool region | draws[k] | bitmap[wb]; the pool region holds
 // either the whole pool (w <= RK_DIRECT_W) or keys[RK_TABLE] | vals[RK_TABLE]
+// (k <= RK_HASH_MAXK).  Past those (any k up to w, as the reference allows)
+// the draws and, for w > RK_DIRECT_W, the whole pool move to global scratch
+// (gjs [n][k], gpool [n][w]): the swap chain then runs over L2.
 constexpr int RK_TABLE = 16384;  // entries (key, value) -> 128 KB
+constexpr int RK_HASH_MAXK = 6000;  // swap chains this short fit the table (<= 2k keys, load < 0.75)
 constexpr int RK_THREADS = 256;
 constexpr int64_t RK_DIRECT_W = 46000;  // pools this small live directly in shared memory
-__host__ __device__ constexpr size_t rk_pool_words(int64_t w) {
-  return static_cast<size_t>(w <= RK_DIRECT_W ? (w > 2 * RK_TABLE ? w : 2 * RK_TABLE) : 2 * RK_TABLE);
+constexpr size_t RK_SMEM_MAX = 227 * 1024 - 1024;  // (+ the static shared memory)
+__host__ __device__ constexpr bool rk_global_pool(int k, int64_t w) { return w > RK_DIRECT_W && k > RK_HASH_MAXK; }
+__host__ __device__ constexpr size_t rk_pool_words(int k, int64_t w) {
+  return rk_global_pool(k, w) ? 0
+         : static_cast<size_t>(w <= RK_DIRECT_W ? (w > 2 * RK_TABLE ? w : 2 * RK_TABLE) : 2 * RK_TABLE);
+}
+// the draws in shared memory when they fit next to the pool and the bitmap
+__host__ __device__ constexpr bool rk_js_smem(int k, int wb, int64_t w) {
+  return (rk_pool_words(k, w) + static_cast<size_t>(k) + static_cast<size_t>(wb)) * 4 <= RK_SMEM_MAX;
 }
 __host__ __device__ constexpr size_t rk_smem_bytes(int k, int wb, int64_t w) {
-  return (rk_pool_words(w) + static_cast<size_t>(k) + static_cast<size_t>(wb)) * 4;
+  return (rk_pool_words(k, w) + (rk_js_smem(k, wb, w) ? static_cast<size_t>(k) : 0) +
+          static_cast<size_t>(wb)) * 4;
 }
 __device__ __forceinline__ int rk_slot(int32_t* keys, int32_t key) {
   uint32_t h = (static_cast<uint32_t>(key) * 2654435761u) & (RK_TABLE - 1);
@@ -1898,17 +1910,19 @@ __global__ void __launch_bounds__(RK_THREADS) k_randk(
     const int32_t* __restrict__ clients, const int32_t* __restrict__ flags, uint64_t run_seed,
     const uint64_t* __restrict__ seeds, uint32_t* __restrict__ bitmap,
     int32_t* __restrict__ count, uint32_t* __restrict__ idx_list, double* __restrict__ val_list,
-    int cap, int32_t* __restrict__ draws, Emit em) {
+    int cap, int32_t* __restrict__ draws, Emit em, int32_t* __restrict__ gjs, int32_t* __restrict__ gpool) {
   if (ctl && ctl->halt) return;
   extern __shared__ int32_t tab[];
   int32_t* keys = tab;
   int32_t* vals = tab + RK_TABLE;
-  const size_t pw = rk_pool_words(w);
-  int32_t* js = tab + pw;                                   // [k]
-  uint32_t* bm = reinterpret_cast<uint32_t*>(tab + pw + k);  // [wb]
+  const size_t pw = rk_pool_words(k, w);
+  const bool js_smem = rk_js_smem(k, wb, w);
+  const int c = client_of(clients, blockIdx.x);
+  int32_t* js = js_smem ? tab + pw : gjs + static_cast<int64_t>(c) * k;                // [k]
+  uint32_t* bm = reinterpret_cast<uint32_t*>(tab + pw + (js_smem ? k : 0));            // [wb]
+  const bool global_pool = rk_global_pool(k, w);
   __shared__ int ws[64];
   __shared__ int s_reject;
-  const int c = client_of(clients, blockIdx.x);
   const int tid = threadIdx.x;
   uint32_t* brow = bitmap + static_cast<int64_t>(c) * wb;
   if (!(flags[c] & 2)) {
@@ -1919,7 +1933,7 @@ __global__ void __launch_bounds__(RK_THREADS) k_randk(
   }
   const uint64_t seed = seeds ? seeds[blockIdx.x] : round_seed(run_seed, c, ctl->round);
   if (tid == 0) s_reject = 0;
-  if (w > RK_DIRECT_W)
+  if (w > RK_DIRECT_W && !global_pool)
     for (int i = tid; i < RK_TABLE; i += RK_THREADS) keys[i] = -1;
   for (int q = tid; q < wb; q += RK_THREADS) bm[q] = 0u;
   __syncthreads();
@@ -1939,9 +1953,10 @@ __global__ void __launch_bounds__(RK_THREADS) k_randk(
     s_reject = -1;
   }
   __syncthreads();
-  if (w <= RK_DIRECT_W) {
-    // small pool: the pool itself in shared memory (over the hash table)
-    int32_t* pool = tab;
+  if (w <= RK_DIRECT_W || global_pool) {
+    // the pool itself: in shared memory (over the hash table) when small,
+    // else this client's global scratch row
+    int32_t* pool = global_pool ? gpool + static_cast<int64_t>(c) * w : tab;
     for (int t = tid; t < w; t += RK_THREADS) pool[t] = t;
     __syncthreads();
     if (tid == 0) {
@@ -2461,6 +2476,166 @@ __global__ void __launch_bounds__(TK_THREADS) k_toplek(
   compact_bitmap(brow, wb, v, 1.0, idx_list + static_cast<int64_t>(c) * cap,
                  val_list + static_cast<int64_t>(c) * cap, ws, em, c);
   pc.mark(28);
+}
+
+// ------------------------------------------------------ TopLEK, large w
+// TopLEK when the w energies do not fit one CTA's shared memory (w > 8192:
+// e.g. the paper's W8A run, d = 301, w = 45,451).  Same rule as k_toplek
+// (compressors.py:179-233): one CTA per client sorts the energies in global
+// memory — a stable LSD radix sort of the 64-bit keys ~bits(energy) (energy
+// >= 0, so ascending keys = descending energy, ties keep ascending position:
+// lexsort((arange, -energy))) — then forms numpy's pairwise total of the
+// sorted energies (recursion table from the host, any w), the cumulative
+// shares over the first k, the single draw, and emits the first t positions.
+// Scratch per client (global): keys / positions twice (ping-pong), the
+// pairwise leaves and nodes.
+constexpr int TLB_THREADS = 1024;
+constexpr int TLB_MAXW_SMEM = 8192;  // above this k_toplek_big replaces k_toplek
+struct TlbScratch {
+  uint64_t* key[2];    // [n][w]
+  uint32_t* pos[2];    // [n][w]
+  double* npw;         // [n][9 * nl + nn]: red8 then leaf / node values
+  int64_t npw_stride;
+};
+__global__ void __launch_bounds__(TLB_THREADS, 1) k_toplek_big(
+    DevCtl* __restrict__ ctl, const double* __restrict__ D, int64_t w, int wb, int k,
+    const int32_t* __restrict__ clients, const int32_t* __restrict__ flags, uint64_t run_seed,
+    const uint64_t* __restrict__ seeds, uint32_t* __restrict__ bitmap,
+    int32_t* __restrict__ count, uint32_t* __restrict__ idx_list, double* __restrict__ val_list,
+    int cap, int32_t* __restrict__ draws, Emit em, const int32_t* __restrict__ npw_tab,
+    TlbScratch scr) {
+  if (ctl && ctl->halt) return;
+  __shared__ int hist[256];
+  __shared__ int base[256];
+  __shared__ int cnt[TLB_THREADS / 32][256];
+  __shared__ int ws[64];
+  __shared__ int s_t, s_skip;
+  const int c = client_of(clients, blockIdx.x);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int n = static_cast<int>(w);
+  const double* v = D + static_cast<int64_t>(c) * w;
+  uint32_t* brow = bitmap + static_cast<int64_t>(c) * wb;
+  clear_row(brow, wb);
+  if (!(flags[c] & 2)) {
+    emit_empty(em, c);
+    if (tid == 0) { count[c] = 0; if (draws) draws[c] = 0; }
+    return;
+  }
+  uint64_t* key[2] = {scr.key[0] + static_cast<int64_t>(c) * w, scr.key[1] + static_cast<int64_t>(c) * w};
+  uint32_t* pos[2] = {scr.pos[0] + static_cast<int64_t>(c) * w, scr.pos[1] + static_cast<int64_t>(c) * w};
+  for (int i = tid; i < n; i += TLB_THREADS) {
+    key[0][i] = ~static_cast<uint64_t>(__double_as_longlong(energy_of(v[i], i)));
+    pos[0][i] = static_cast<uint32_t>(i);
+  }
+  int cur = 0;
+  const uint32_t lt_mask = (1u << lane) - 1u;
+  for (int pass = 0; pass < 8; ++pass) {
+    const int sh = 8 * pass;
+    for (int b = tid; b < 256; b += TLB_THREADS) hist[b] = 0;
+    if (tid == 0) s_skip = 0;
+    __syncthreads();
+    for (int i = tid; i < n; i += TLB_THREADS) atomicAdd(&hist[(key[cur][i] >> sh) & 255u], 1);
+    __syncthreads();
+    if (tid < 256) {  // exclusive scan of the digit counts; a pass with one digit is the identity
+      int acc = 0;
+      for (int b = 0; b < tid; ++b) acc += hist[b];
+      base[tid] = acc;
+      if (hist[tid] == n) s_skip = 1;
+    }
+    __syncthreads();
+    if (s_skip) continue;
+    const uint64_t* ki = key[cur];
+    const uint32_t* pi = pos[cur];
+    uint64_t* ko = key[cur ^ 1];
+    uint32_t* po = pos[cur ^ 1];
+    for (int t0 = 0; t0 < n; t0 += TLB_THREADS) {
+      for (int e = tid; e < (TLB_THREADS / 32) * 256; e += TLB_THREADS) (&cnt[0][0])[e] = 0;
+      __syncthreads();
+      const int i = t0 + tid;
+      const bool ok = i < n;
+      const uint64_t kv = ok ? ki[i] : 0ull;
+      const uint32_t pv = ok ? pi[i] : 0u;
+      const int dg = ok ? static_cast<int>((kv >> sh) & 255u) : 256;
+      const uint32_t peers = __match_any_sync(0xffffffffu, dg);
+      const int rnk = __popc(peers & lt_mask);
+      if (ok && rnk == 0) cnt[warp][dg] = __popc(peers);
+      __syncthreads();
+      if (tid < 256) {  // stable: warps in order inside the tile, tiles in order
+        int run = base[tid];
+        for (int q = 0; q < TLB_THREADS / 32; ++q) {
+          const int t = cnt[q][tid];
+          cnt[q][tid] = run;
+          run += t;
+        }
+        base[tid] = run;
+      }
+      __syncthreads();
+      if (ok) {
+        const int dst = cnt[warp][dg] + rnk;
+        ko[dst] = kv;
+        po[dst] = pv;
+      }
+      __syncthreads();
+    }
+    cur ^= 1;
+  }
+  // sorted energies (descending) back as doubles, in place of the keys
+  double* en = reinterpret_cast<double*>(key[cur]);
+  for (int i = tid; i < n; i += TLB_THREADS) en[i] = __longlong_as_double(static_cast<long long>(~key[cur][i]));
+  __syncthreads();
+  const int nl = npw_tab[0];
+  double* red8 = scr.npw + static_cast<int64_t>(c) * scr.npw_stride;
+  const double total = np_pairwise_tab(en, npw_tab, red8 + 8 * nl, red8);
+  if (tid == 0) {
+    const uint64_t seed = seeds ? seeds[blockIdx.x] : round_seed(run_seed, c, ctl->round);
+    Prg p(seed);
+    int tsel;
+    if (!(total > 0.0)) {  // compressors.py:185-186
+      ctl->bad_client = c;
+      raise_status(ctl, ST_TOPLEK_ZERO);
+      tsel = 0;
+    } else {
+      const double target = static_cast<double>(k) / static_cast<double>(w);
+      double cum = 0.0, s_prev = 0.0, s_cur = 0.0;
+      int hi = -1;
+      for (int i = 0; i < k; ++i) {
+        cum = __dadd_rn(cum, en[i]);
+        const double shv = __ddiv_rn(cum, total);
+        if (shv >= target) { hi = i; s_cur = shv; break; }
+        s_prev = shv;
+      }
+      int lo_t, hi_t;
+      double p_lo;
+      if (hi < 0) {
+        lo_t = hi_t = k; p_lo = 1.0;
+      } else {
+        hi_t = hi + 1;
+        lo_t = hi_t - 1;
+        const double share_lo = (lo_t == 0) ? 0.0 : s_prev;
+        const double share_hi = s_cur;
+        if (share_hi <= share_lo || share_hi <= target) {
+          lo_t = hi_t; p_lo = 1.0;
+        } else {
+          p_lo = __ddiv_rn(__dsub_rn(share_hi, target), __dsub_rn(share_hi, share_lo));
+          p_lo = fmin(fmax(p_lo, 0.0), 1.0);
+        }
+      }
+      tsel = (p.next_f64() < p_lo) ? lo_t : hi_t;
+    }
+    s_t = tsel;
+    count[c] = tsel;
+    if (draws) draws[c] = p.draws;
+  }
+  __syncthreads();
+  const int tsel = s_t;
+  const uint32_t* ps = pos[cur];
+  for (int i = tid; i < tsel; i += TLB_THREADS) {
+    const uint32_t t = ps[i];
+    atomicOr(&brow[t >> 5], 1u << (t & 31));
+  }
+  __syncthreads();
+  compact_bitmap(brow, wb, v, 1.0, idx_list + static_cast<int64_t>(c) * cap,
+                 val_list + static_cast<int64_t>(c) * cap, ws, em, c);
 }
 
 // --------------------------------------------------------- identity / natural

@@ -83,6 +83,9 @@ struct Ctx {
   size_t solve_smem = 0;
   int toplek_P = 0;
   int32_t* npw_tab = nullptr;  // TopLEK: numpy pairwise-sum recursion for n = w
+  TlbScratch tlb{};            // TopLEK for w > TLB_MAXW_SMEM: global sort / sum scratch
+  int32_t* rk_js = nullptr;    // RandK draws [n][k] when they do not fit shared memory
+  int32_t* rk_pool = nullptr;  // RandK pools [n][w] when w > RK_DIRECT_W and k > RK_HASH_MAXK
   bool uploaded = false, initialised = false;
   std::string err;
 
@@ -472,9 +475,16 @@ int launch_compress(Ctx* ctx, cudaStream_t s, const int32_t* clients, int n_acti
     case FB_KIND_RANDK:
       k_randk<<<n_active, RK_THREADS, rk_smem_bytes(c.k, ctx->wb, ctx->w), s>>>(
           ctl, ctx->D, ctx->w, ctx->wb, c.k, clients, ctx->flags, c.run_seed, seeds, ctx->bitmap,
-          ctx->count, ctx->idx_list, ctx->val_list, ctx->cap, ctx->draws, em);
+          ctx->count, ctx->idx_list, ctx->val_list, ctx->cap, ctx->draws, em, ctx->rk_js, ctx->rk_pool);
       break;
     case FB_KIND_TOPLEK:
+      if (ctx->w > TLB_MAXW_SMEM) {
+        k_toplek_big<<<n_active, TLB_THREADS, 0, s>>>(
+            ctl ? ctl : ctx->ctl, ctx->D, ctx->w, ctx->wb, c.k, clients, ctx->flags, c.run_seed,
+            seeds, ctx->bitmap, ctx->count, ctx->idx_list, ctx->val_list, ctx->cap, ctx->draws, em,
+            ctx->npw_tab, ctx->tlb);
+        break;
+      }
       k_toplek<<<n_active, TK_THREADS, toplek_smem_bytes(ctx->toplek_P), s>>>(
           ctl ? ctl : ctx->ctl, ctx->D, ctx->w, ctx->wb, c.k, clients, ctx->flags, c.run_seed,
           seeds, ctx->bitmap, ctx->count, ctx->idx_list, ctx->val_list, ctx->cap, ctx->draws,
@@ -936,13 +946,8 @@ int fb_create(const fb_config* cfg_in, void** out) {
     return invalid(nullptr, "tau out of range");
   if (c.topk_path < FB_TOPK_PATH_AUTO || c.topk_path > FB_TOPK_PATH_SPLIT)
     return invalid(nullptr, "bad topk_path");
-  if (c.kind == FB_KIND_TOPLEK && w > 8192)
-    return invalid(nullptr, "toplek with d(d+1)/2 > 8192 is outside this build's envelope");
-  if (c.kind == FB_KIND_RANDK && std::min<int64_t>(w, 2 * static_cast<int64_t>(c.k)) > 12000)
-    return invalid(nullptr, "randk with min(w, 2k) > 12000 is outside this build's envelope");
-  if (c.kind == FB_KIND_RANDK &&
-      rk_smem_bytes(c.k, static_cast<int>((w + 31) / 32), w) > rk_smem_bytes(6000, 16400, 524800))
-    return invalid(nullptr, "randk needs k <= 6000 and d <= 1024 in this build");
+  if (c.kind == FB_KIND_RANDK && rk_smem_bytes(c.k, static_cast<int>((w + 31) / 32), w) > RK_SMEM_MAX)
+    return invalid(nullptr, "randk bitmap does not fit shared memory (d > 1024)");
 
   Ctx* ctx = new Ctx();
   ctx->cfg = c;
@@ -968,7 +973,7 @@ int fb_create(const fb_config* cfg_in, void** out) {
                         ? static_cast<double>(w) / static_cast<double>(c.k)
                         : 1.0;
   ctx->toplek_P = 1;
-  if (c.kind == FB_KIND_TOPLEK)
+  if (c.kind == FB_KIND_TOPLEK && w <= TLB_MAXW_SMEM)
     while (ctx->toplek_P < w || ctx->toplek_P < TK_THREADS) ctx->toplek_P <<= 1;
   // master solve: one cluster (8 CTAs from d >= 128); 32-wide panels while the
   // (d + 1) x 33 panel fits in shared memory, else 16-wide
@@ -1050,7 +1055,7 @@ int fb_create(const fb_config* cfg_in, void** out) {
   CKC(cudaFuncSetAttribute(k_master_fold, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            static_cast<int>(max_fold)));
   CKC(cudaFuncSetAttribute(k_randk, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           static_cast<int>(rk_smem_bytes(6000, 16400, 524800))));
+                           static_cast<int>(RK_SMEM_MAX)));
   CKC(cudaFuncSetAttribute(k_toplek, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            static_cast<int>(max_toplek)));
   CKC(cudaFuncSetAttribute(k_chol_solve<32>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1193,7 +1198,16 @@ int fb_create(const fb_config* cfg_in, void** out) {
     };
     walk(0, static_cast<int>(w));
     const int nlf = static_cast<int>(loff.size()), nnd = static_cast<int>(nl_.size());
-    if (nlf <= NPW_TAB_LEAVES) {
+    const bool big = w > TLB_MAXW_SMEM;  // k_toplek_big reads the table from global memory
+    if (big) {
+      const size_t nw = static_cast<size_t>(n) * w;
+      ctx->tlb.npw_stride = 9 * static_cast<int64_t>(nlf) + nnd;
+      if (dalloc(ctx, &ctx->tlb.key[0], nw) || dalloc(ctx, &ctx->tlb.key[1], nw) ||
+          dalloc(ctx, &ctx->tlb.pos[0], nw) || dalloc(ctx, &ctx->tlb.pos[1], nw) ||
+          dalloc(ctx, &ctx->tlb.npw, static_cast<size_t>(n) * ctx->tlb.npw_stride))
+        return fail(FB_ERR_CUDA);
+    }
+    if (nlf <= NPW_TAB_LEAVES || big) {
       auto code = [&](int x) { return x < 0 ? -x - 1 : nlf + x; };
       std::vector<int32_t> tab{nlf, nnd};
       tab.insert(tab.end(), loff.begin(), loff.end());
@@ -1204,6 +1218,13 @@ int fb_create(const fb_config* cfg_in, void** out) {
       CKC(cudaMemcpyAsync(ctx->npw_tab, tab.data(), sizeof(int32_t) * tab.size(),
                           cudaMemcpyHostToDevice, ctx->st));
     }
+  }
+  if (c.kind == FB_KIND_RANDK) {
+    const int wbk = static_cast<int>((w + 31) / 32);
+    if (!rk_js_smem(c.k, wbk, w) && dalloc(ctx, &ctx->rk_js, static_cast<size_t>(n) * c.k))
+      return fail(FB_ERR_CUDA);
+    if (rk_global_pool(c.k, w) && dalloc(ctx, &ctx->rk_pool, static_cast<size_t>(n) * w))
+      return fail(FB_ERR_CUDA);
   }
   CKC(cudaStreamSynchronize(ctx->st));  // zero fills and the tables are in place
   if (make_tmap(ctx) != FB_OK) return fail(FB_ERR_CUDA);

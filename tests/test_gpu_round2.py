@@ -115,3 +115,48 @@ def test_divergence_error_at_the_reference_round():
         eng.run_rounds(3)
     assert exc.value.round == 3  # the round counter after the failing step (2 -> 3)
     eng.close()
+
+
+def test_large_w_toplek_and_randk_bit_exact():
+    """TopLEK at w = 45,451 (k_toplek_big: global-memory radix sort + numpy's
+    pairwise total over any w) on tie-heavy c0 round-0 differences and a
+    Gaussian input, and RandK with k in {8000, 30000} (draws / pool past the
+    shared-memory envelope): indices, values and stream consumption equal
+    the reference's (tests/golden/compress_r2.npz)."""
+    from paper_2410_08760_b200 import CompressorKind, CompressorSpec, leaf
+
+    g = golden("compress_r2.npz")
+    d = int(g["d"])
+    names = g["names"].tolist()
+    P = np.stack([g[f"{nm}__input"] for nm in names])
+    tags = sorted({key[len(nm) + 2:-5] for nm in names for key in g.files
+                   if key.startswith(nm + "__") and key.endswith("__val")})
+    n_checked = 0
+    for tag in tags:
+        kind, k, seed = tag.split("__")
+        spec = CompressorSpec(CompressorKind(kind), k=int(k[1:]))
+        deltas = leaf.compress_packed_batch(P, d, spec, [int(seed[1:])] * len(names))
+        for nm, delta in zip(names, deltas):
+            base = f"{nm}__{tag}"
+            assert np.array_equal(delta.indices, g[base + "__idx"]), base
+            assert np.array_equal(delta.values, g[base + "__val"]), base
+            p = O.SplitMix64(int(seed[1:]))
+            for _ in range(delta.draws):
+                p.next_u64()
+            assert p.next_u64() == int(g[base + "__next"]), base
+            n_checked += 1
+    assert n_checked == 40
+
+
+def test_ls_toplek_8d_at_c0_shape_matches_reference():
+    """The paper's W8A TopLEK[8d] run shape (d = 301, w = 45,451, k = 2408)
+    through simulate: FedNL-LS rows against the reference's."""
+    from paper_2410_08760_b200 import CompressorKind, CompressorSpec
+    from paper_2410_08760_b200 import data as D
+
+    shards = D.baseline_shards("c0")
+    cfg = RunConfig(algorithm="fednl-ls", compressor=CompressorSpec(CompressorKind.TOPLEK, k=8 * 301),
+                    rounds=6, run_seed=1)
+    rows = simulate(cfg, shards)
+    g = golden("compress_r2.npz")
+    _rows_close(rows, g, ["ls_toplek8d_c0"])

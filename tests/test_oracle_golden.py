@@ -357,3 +357,25 @@ def test_oracle_line_search_failure_matches_reference():
     with pytest.raises(O.LineSearchFailed) as exc:
         O.simulate(O.OracleConfig(**kw), [s.bmat for s in shards], lam=shards[0].lam)
     assert exc.value.round == int(g["ls_fail__round"])
+
+
+def test_large_w_toplek_and_randk_against_reference():
+    """TopLEK at w = 45,451 (c0 round-0 differences: heavy ties) and RandK
+    with k > 6000: the restatement matches the reference bit for bit."""
+    g = golden("compress_r2.npz")
+    d = int(g["d"])
+    n_checked = 0
+    for name in g["names"].tolist():
+        pk = g[f"{name}__input"]
+        for key in g.files:
+            if key.startswith(name + "__") and key.endswith("__val"):
+                tag = key[len(name) + 2:-5]
+                kind, k, seed = tag.split("__")
+                prg = O.SplitMix64(int(seed[1:]))
+                delta = O.compress_packed(pk, d, kind, int(k[1:]), prg)
+                base = f"{name}__{tag}"
+                assert np.array_equal(delta.values, g[base + "__val"]), base
+                assert np.array_equal(delta.indices, g[base + "__idx"]), base
+                assert prg.next_u64() == int(g[base + "__next"]), base
+                n_checked += 1
+    assert n_checked == 40
