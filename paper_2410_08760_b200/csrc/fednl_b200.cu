@@ -78,6 +78,12 @@ struct Ctx {
   // world * npr clients so an in-place ncclAllGather fills them
   int world = 1, rank = 0, npr = 0, c_lo = 0, c_hi = 0;
   int32_t* local_clients = nullptr;  // device [c_hi - c_lo] = c_lo, c_lo + 1, ...
+  int32_t* xcode = nullptr;          // [world] status codes exchanged after rank-local work
+  // FedNL-PP across ranks: participant slots [s_lo, s_hi) of spr per rank
+  int spr = 0, s_lo = 0, s_hi = 0;
+  int32_t* sub_loc = nullptr;        // this rank's participants
+  PpX ppx{};
+  double *dgvec_all = nullptr, *dshift_all = nullptr;  // [tau][d], [tau]
   ncclComm_t comm = nullptr;
   int prio_high = 0;
   size_t solve_smem = 0;
@@ -313,6 +319,12 @@ NcclApi& nccl_api() {
 template <typename T>
 int gather_clients(Ctx* ctx, T* base, size_t per, ncclDataType_t type, cudaStream_t s) {
   const size_t cnt = static_cast<size_t>(ctx->npr) * per;
+  NCK(nccl_api().AllGather(base + static_cast<size_t>(ctx->rank) * cnt, base, cnt, type, ctx->comm, s));
+  return FB_OK;
+}
+// in-place all-gather of per-rank blocks of `cnt` elements (rank r's at r * cnt)
+template <typename T>
+int gather_blocks(Ctx* ctx, T* base, size_t cnt, ncclDataType_t type, cudaStream_t s) {
   NCK(nccl_api().AllGather(base + static_cast<size_t>(ctx->rank) * cnt, base, cnt, type, ctx->comm, s));
   return FB_OK;
 }
@@ -681,6 +693,12 @@ int enqueue_fednl_round(Ctx* ctx) {
       TRY(gather_clients(ctx, ctx->rs, ctx->nr + 1, ncclInt32, ctx->st2));
     }
     TRY(gather_clients(ctx, ctx->count, 1, ncclInt32, ctx->st2));
+    // a compressor failure is rank-local: every rank halts on the first one
+    k_code_post<<<1, 32, 0, ctx->st2>>>(ctx->ctl, ctx->rank, ctx->xcode);
+    CKL();
+    TRY(gather_blocks(ctx, ctx->xcode, 1, ncclInt32, ctx->st2));
+    k_code_sync<<<1, 32, 0, ctx->st2>>>(ctx->ctl, ctx->world, ctx->xcode);
+    CKL();
   }
   TRY(record(ctx, EV_COMP_END, ctx->st2));
   TRY(record(ctx, EV_FOLD_START, ctx->st2));
@@ -747,6 +765,68 @@ int enqueue_fednl_round(Ctx* ctx) {
   return FB_OK;
 }
 
+// FedNL-PP participants across ranks (fb_set_shard): this rank's slots
+// [s_lo, s_hi) of the replicated subset, then the slot exchange (k_pp_pack /
+// all-gathers / k_pp_unpack) and the replicated master update and fold.
+int enqueue_pp_participants_sharded(Ctx* ctx) {
+  cudaStream_t s = ctx->st;
+  const int n = ctx->n, tau = ctx->tau, d = ctx->d, m = ctx->s_hi - ctx->s_lo;
+  CK(cudaMemsetAsync(ctx->flags, 0, sizeof(int32_t) * n, s));
+  if (m > 0) {
+    k_pp_subloc<<<1, 32, 0, s>>>(ctx->subset, ctx->s_lo, m, ctx->sub_loc);
+    CKL();
+    TRY(launch_margins(ctx, s, ctx->x, ctx->sub_loc, m));
+    TRY(launch_gradient(ctx, s, ctx->x, ctx->sub_loc, m));
+    TRY(launch_hessian(ctx, s, ctx->sub_loc, m, ctx->hest, ctx->w, ctx->D, ctx->hess_part));
+    k_check_flags_pp<<<1, 32, 0, s>>>(ctx->ctl, m, ctx->sub_loc, ctx->flags);  // (exchanged below)
+    CKL();
+    TRY(launch_compress(ctx, s, ctx->sub_loc, m, nullptr, nullptr));
+    if (dense_kind(ctx)) TRY(launch_master_fold(ctx, s, ctx->sub_loc, m, ctx->hest, nullptr, nullptr));
+    k_pp_shift_part<<<dim3(PP_SB, m), 256, 0, s>>>(ctx->ctl, d, ctx->sub_loc, ctx->hest, ctx->hess_part,
+                                                   ctx->pp_shift_part);
+    CKL();
+    k_pp_client<<<dim3((d + 7) / 8, m), 256, 0, s>>>(ctx->ctl, d, ctx->sub_loc, ctx->hest, ctx->pp_shift_part,
+                                                     ctx->x, ctx->grad, ctx->cli_shift, ctx->cli_gvec,
+                                                     ctx->dshift, ctx->dgvec);
+    CKL();
+    k_pp_pack<<<m, 256, 0, s>>>(ctx->ctl, d, ctx->w, ctx->cap, ctx->nr, ctx->s_lo, ctx->rank, ctx->sub_loc,
+                                ctx->idx_list, ctx->val_list, ctx->count, ctx->rs, ctx->flags, ctx->cli_gvec,
+                                ctx->cli_shift, ctx->dgvec, ctx->dshift, ctx->D, ctx->ppx);
+    CKL();
+  }
+  k_code_post<<<1, 32, 0, s>>>(ctx->ctl, ctx->rank, ctx->ppx.code);
+  CKL();
+  const size_t sp = static_cast<size_t>(ctx->spr);
+  PpX& x = ctx->ppx;
+  TRY(gather_blocks(ctx, x.idx, sp * ctx->cap, ncclUint32, s));
+  TRY(gather_blocks(ctx, x.val, sp * ctx->cap, ncclFloat64, s));
+  TRY(gather_blocks(ctx, x.cnt, sp, ncclInt32, s));
+  TRY(gather_blocks(ctx, x.rs, sp * (ctx->nr + 1), ncclInt32, s));
+  TRY(gather_blocks(ctx, x.flags, sp, ncclInt32, s));
+  TRY(gather_blocks(ctx, x.gvec, sp * d, ncclFloat64, s));
+  TRY(gather_blocks(ctx, x.shift, sp, ncclFloat64, s));
+  TRY(gather_blocks(ctx, x.dg, sp * d, ncclFloat64, s));
+  TRY(gather_blocks(ctx, x.ds, sp, ncclFloat64, s));
+  if (x.dense) TRY(gather_blocks(ctx, x.dense, sp * static_cast<size_t>(ctx->w), ncclFloat64, s));
+  TRY(gather_blocks(ctx, x.code, 1, ncclInt32, s));
+  k_pp_unpack<<<tau, 256, 0, s>>>(ctx->ctl, d, ctx->w, ctx->cap, ctx->nr, ctx->s_lo, ctx->s_hi, ctx->world,
+                                  ctx->cfg.alpha, ctx->subset, x, ctx->idx_list, ctx->val_list, ctx->count,
+                                  ctx->rs, ctx->flags, ctx->cli_gvec, ctx->cli_shift, ctx->dgvec_all,
+                                  ctx->dshift_all, ctx->D, ctx->hest);
+  CKL();
+  k_check_flags_pp<<<1, 32, 0, s>>>(ctx->ctl, tau, ctx->subset, ctx->flags);
+  CKL();
+  k_pp_master<<<1, 256, 0, s>>>(ctx->ctl, d, n, tau, ctx->dshift_all, ctx->dgvec_all, ctx->gvec, ctx->pp_shift);
+  CKL();
+  TRY(launch_master_fold(ctx, s, ctx->subset, tau, nullptr, ctx->hmas, ctx->hmas));
+  k_finish<<<1, 256, 0, s>>>(ctx->ctl, d, n, tau, ctx->subset, ctx->x, nullptr, 0, ctx->count,
+                             ctx->row_counts, ctx->row_ls, nullptr);
+  CKL();
+  TRY(record(ctx, EV_END, s));
+  ctx->launches_per_round = 16;
+  return FB_OK;
+}
+
 int enqueue_pp_round(Ctx* ctx) {
   cudaStream_t s = ctx->st;
   const int n = ctx->n, tau = ctx->tau;
@@ -765,8 +845,16 @@ int enqueue_pp_round(Ctx* ctx) {
   // this round's participants (master subset stream) off the critical path too
   k_pp_select<<<1, 128, 0, sp>>>(ctx->ctl, n, tau, ctx->subset, ctx->pool);
   CKL();
-  TRY(launch_margins(ctx, sp, ctx->x, nullptr, n));
-  TRY(launch_gradient(ctx, sp, ctx->x, nullptr, n));
+  const bool shd = sharded(ctx);
+  if (shd) {  // the probes of this rank's client range, all-gathered
+    TRY(launch_margins(ctx, sp, ctx->x, ctx->local_clients, ctx->c_hi - ctx->c_lo));
+    TRY(launch_gradient(ctx, sp, ctx->x, ctx->local_clients, ctx->c_hi - ctx->c_lo));
+    TRY(gather_clients(ctx, ctx->grad, ctx->d, ncclFloat64, sp));
+    TRY(gather_clients(ctx, ctx->loss_part, ctx->nblk, ncclFloat64, sp));
+  } else {
+    TRY(launch_margins(ctx, sp, ctx->x, nullptr, n));
+    TRY(launch_gradient(ctx, sp, ctx->x, nullptr, n));
+  }
   TRY(launch_reduce(ctx, sp, ctx->x, nullptr, n, n, false, ctx->row_grad, ctx->row_f));
   if (!pp_serial) {
     CK(cudaEventRecord(ctx->ev_join, sp));
@@ -777,6 +865,7 @@ int enqueue_pp_round(Ctx* ctx) {
                                  ctx->row_counts, ctx->row_ls);
   CKL();
   TRY(record(ctx, EV_SOLVE_END, s));
+  if (shd) return enqueue_pp_participants_sharded(ctx);
   // participants' oracle at x_new (algorithms.py:240-249)
   CK(cudaMemsetAsync(ctx->flags, 0, sizeof(int32_t) * n, s));
   TRY(launch_margins(ctx, s, ctx->x, ctx->subset, tau));
@@ -1326,8 +1415,7 @@ int fb_set_shard(void* handle, int32_t world, int32_t rank, const uint8_t* nccl_
   if (!ctx || !nccl_id) return invalid(ctx, "null argument");
   if (world < 1 || rank < 0 || rank >= world) return invalid(ctx, "bad world / rank");
   if (ctx->uploaded || ctx->initialised) return invalid(ctx, "fb_set_shard must precede fb_upload_shards");
-  if (ctx->cfg.algorithm == FB_ALG_PP)
-    return fail_code(ctx, FB_ERR_UNSUPPORTED, "client sharding is implemented for FedNL and FedNL-LS (not PP)");
+
   NcclApi& api = nccl_api();
   if (!api.ok) return invalid(ctx, "libnccl.so.2 could not be loaded");
   const int n = ctx->n;
@@ -1345,8 +1433,29 @@ int fb_set_shard(void* handle, int32_t world, int32_t rank, const uint8_t* nccl_
       dalloc(ctx, &ctx->ls_loss_part, n_pad * LS_BATCH * ctx->ls_nblk) ||
       dalloc(ctx, &ctx->local_clients, std::max(1, ctx->c_hi - ctx->c_lo)))
     return FB_ERR_CUDA;
+  if (dalloc(ctx, &ctx->xcode, world)) return FB_ERR_CUDA;
+  if (ctx->cfg.algorithm == FB_ALG_PP) {
+    // participants by slot: B and every H_i^k on every rank (replicated
+    // client state), the slot outputs exchanged each round
+    const int tau = ctx->tau;
+    ctx->spr = (tau + world - 1) / world;
+    ctx->s_lo = std::min(tau, rank * ctx->spr);
+    ctx->s_hi = std::min(tau, ctx->s_lo + ctx->spr);
+    const size_t tp = static_cast<size_t>(world) * ctx->spr;
+    PpX& x = ctx->ppx;
+    if (dalloc(ctx, &ctx->sub_loc, std::max(1, ctx->spr)) || dalloc(ctx, &x.idx, tp * ctx->cap) ||
+        dalloc(ctx, &x.val, tp * ctx->cap) || dalloc(ctx, &x.cnt, tp) ||
+        dalloc(ctx, &x.rs, tp * (ctx->nr + 1)) || dalloc(ctx, &x.flags, tp) ||
+        dalloc(ctx, &x.gvec, tp * ctx->d) || dalloc(ctx, &x.shift, tp) || dalloc(ctx, &x.dg, tp * ctx->d) ||
+        dalloc(ctx, &x.ds, tp) || dalloc(ctx, &x.code, world) ||
+        dalloc(ctx, &ctx->dgvec_all, static_cast<size_t>(tau) * ctx->d) || dalloc(ctx, &ctx->dshift_all, tau) ||
+        (dense_kind(ctx) && dalloc(ctx, &x.dense, tp * static_cast<size_t>(ctx->w))))
+      return FB_ERR_CUDA;
+  }
   // dense kinds all-gather D every round; exact init all-gathers H_i(x0)
-  if (dense_kind(ctx) && dalloc(ctx, &ctx->D, n_pad * static_cast<size_t>(ctx->w) + 2)) return FB_ERR_CUDA;
+  if (dense_kind(ctx) && ctx->cfg.algorithm != FB_ALG_PP &&
+      dalloc(ctx, &ctx->D, n_pad * static_cast<size_t>(ctx->w) + 2))
+    return FB_ERR_CUDA;
   if (ctx->cfg.hessian_init == FB_INIT_EXACT && dalloc(ctx, &ctx->hest, n_pad * static_cast<size_t>(ctx->w)))
     return FB_ERR_CUDA;
   std::vector<int32_t> loc(std::max(1, ctx->c_hi - ctx->c_lo));
@@ -1377,7 +1486,10 @@ int fb_upload_shards_ex(void* handle, const double* const* bmats, const int32_t*
   Ctx* ctx = static_cast<Ctx*>(handle);
   if (!ctx || !bmats) return invalid(ctx, "null argument");
   const int d = ctx->d, n = ctx->n;
-  for (int c = ctx->c_lo; c < ctx->c_hi; ++c)
+  // FedNL-PP keeps every client's data on every rank (participants by slot)
+  const bool all = ctx->cfg.algorithm == FB_ALG_PP;
+  const int up_lo = all ? 0 : ctx->c_lo, up_hi = all ? n : ctx->c_hi;
+  for (int c = up_lo; c < up_hi; ++c)
     if (!bmats[c]) return invalid(ctx, "null shard pointer");
   std::vector<int32_t> nis(n, ctx->ni);
   std::vector<double> lams(n, ctx->cfg.lam);
@@ -1427,7 +1539,7 @@ int fb_upload_shards_ex(void* handle, const double* const* bmats, const int32_t*
   auto lane_body = [&](int l) {
     UploadLane& ln = pool.lanes[l];
     int slot = 0;
-    for (int c = ctx->c_lo + l; c < ctx->c_hi && !failed.load(); c += L, slot ^= 1) {
+    for (int c = up_lo + l; c < up_hi && !failed.load(); c += L, slot ^= 1) {
       cudaError_t e = cudaEventSynchronize(ln.done[slot]);  // slot free again
       const size_t cb = static_cast<size_t>(d) * nis[c] * sizeof(double);
       if (e == cudaSuccess) {
@@ -1488,7 +1600,7 @@ int fb_init_state(void* handle, const double* x0) {
   const bool pp = c.algorithm == FB_ALG_PP;
   if (c.hessian_init == FB_INIT_EXACT || pp) {
     CK(cudaMemsetAsync(ctx->flags, 0, sizeof(int32_t) * n, s));
-    const bool shd = sharded(ctx);
+    const bool shd = sharded(ctx) && !pp;  // PP: every rank holds every client
     const int32_t* loc = shd ? ctx->local_clients : nullptr;
     const int n_loc = shd ? ctx->c_hi - ctx->c_lo : n;
     TRY(launch_margins(ctx, s, ctx->x, loc, n_loc));

@@ -550,6 +550,141 @@ __global__ void k_check_flags_pp(DevCtl* ctl, int tau, const int32_t* subset,
   }
 }
 
+// ----------------------------------------------- FedNL-PP across GPUs
+// Sharded FedNL-PP (fb_set_shard): every rank draws the same participant
+// subset (replicated master stream) and rank r computes the participant
+// slots [r * spr, (r + 1) * spr) of it (B and every H_i^k are held by every
+// rank).  The owner's per-slot results go through a slot-major exchange
+// buffer (all-gathered in blocks of spr slots): the compressed delta, the
+// client's new shift / shifted gradient and their increments, the flags.
+// Every rank then holds every participant's outputs and applies the client
+// shift update of the slots it did not compute itself (the same
+// fl(h + fl(alpha v)) the owner applied), so all ranks keep identical state.
+struct PpX {
+  uint32_t* idx;    // [tau_pad][cap]
+  double* val;      // [tau_pad][cap]
+  int32_t* cnt;     // [tau_pad]
+  int32_t* rs;      // [tau_pad][nr + 1]
+  int32_t* flags;   // [tau_pad]
+  double* gvec;     // [tau_pad][d]  client's new shifted gradient
+  double* shift;    // [tau_pad]     client's new shift
+  double* dg;       // [tau_pad][d]  its increment (master running average)
+  double* ds;       // [tau_pad]
+  double* dense;    // [tau_pad][w]  dense kinds: the (rounded) update, else null
+  int32_t* code;    // [world]       each rank's status code after its slots
+};
+// this rank's participants: sub_loc[i] = subset[s_lo + i], i < m
+__global__ void k_pp_subloc(const int32_t* __restrict__ subset, int s_lo, int m,
+                            int32_t* __restrict__ sub_loc) {
+  for (int i = threadIdx.x; i < m; i += blockDim.x) sub_loc[i] = subset[s_lo + i];
+}
+// grid m (this rank's slots), block 256
+__global__ void __launch_bounds__(256) k_pp_pack(const DevCtl* __restrict__ ctl, int d, int64_t w,
+                                                 int cap, int nr, int s_lo, int rank,
+                                                 const int32_t* __restrict__ sub_loc,
+                                                 const uint32_t* __restrict__ idx_list,
+                                                 const double* __restrict__ val_list,
+                                                 const int32_t* __restrict__ count,
+                                                 const int32_t* __restrict__ rs,
+                                                 const int32_t* __restrict__ flags,
+                                                 const double* __restrict__ cli_gvec,
+                                                 const double* __restrict__ cli_shift,
+                                                 const double* __restrict__ dgvec,
+                                                 const double* __restrict__ dshift,
+                                                 const double* __restrict__ D, PpX x) {
+  const int i = blockIdx.x, j = s_lo + i;
+  const int c = sub_loc[i];
+  const int cn = count[c];
+  for (int e = threadIdx.x; e < cap; e += blockDim.x)
+    if (e < cn) {
+      x.idx[static_cast<int64_t>(j) * cap + e] = idx_list[static_cast<int64_t>(c) * cap + e];
+      x.val[static_cast<int64_t>(j) * cap + e] = val_list[static_cast<int64_t>(c) * cap + e];
+    }
+  for (int r = threadIdx.x; r <= nr; r += blockDim.x)
+    x.rs[static_cast<int64_t>(j) * (nr + 1) + r] = rs[static_cast<int64_t>(c) * (nr + 1) + r];
+  for (int a = threadIdx.x; a < d; a += blockDim.x) {
+    x.gvec[static_cast<int64_t>(j) * d + a] = cli_gvec[static_cast<int64_t>(c) * d + a];
+    x.dg[static_cast<int64_t>(j) * d + a] = dgvec[static_cast<int64_t>(i) * d + a];
+  }
+  if (x.dense)
+    for (int64_t t = threadIdx.x; t < w; t += blockDim.x)
+      x.dense[static_cast<int64_t>(j) * w + t] = D[static_cast<int64_t>(c) * w + t];
+  if (threadIdx.x == 0) {
+    x.cnt[j] = cn;
+    x.flags[j] = flags[c];
+    x.shift[j] = cli_shift[c];
+    x.ds[j] = dshift[i];
+  }
+}
+// grid tau (every slot), block 256: the per-client rows / state of every
+// participant, the slot-major increments, and the client shift update of the
+// slots owned by other ranks
+__global__ void __launch_bounds__(256) k_pp_unpack(DevCtl* __restrict__ ctl, int d, int64_t w,
+                                                   int cap, int nr, int s_lo, int s_hi, int world,
+                                                   double alpha, const int32_t* __restrict__ subset,
+                                                   PpX x, uint32_t* __restrict__ idx_list,
+                                                   double* __restrict__ val_list,
+                                                   int32_t* __restrict__ count, int32_t* __restrict__ rs,
+                                                   int32_t* __restrict__ flags,
+                                                   double* __restrict__ cli_gvec,
+                                                   double* __restrict__ cli_shift,
+                                                   double* __restrict__ dgvec_all,
+                                                   double* __restrict__ dshift_all,
+                                                   double* __restrict__ D, double* __restrict__ hest) {
+  const int j = blockIdx.x;
+  const int c = subset[j];
+  const bool mine = j >= s_lo && j < s_hi;
+  if (j == 0 && threadIdx.x == 0 && ctl->code == 0) {  // a rank-local failure halts every rank
+    for (int r = 0; r < world; ++r)
+      if (x.code[r] != 0) {
+        raise_status(ctl, x.code[r]);
+        break;
+      }
+  }
+  const int cn = x.cnt[j];
+  double* hc = hest + static_cast<int64_t>(c) * w;
+  for (int e = threadIdx.x; e < cn; e += blockDim.x) {
+    const uint32_t t = x.idx[static_cast<int64_t>(j) * cap + e];
+    const double v = x.val[static_cast<int64_t>(j) * cap + e];
+    idx_list[static_cast<int64_t>(c) * cap + e] = t;
+    val_list[static_cast<int64_t>(c) * cap + e] = v;
+    if (!mine && !x.dense) hc[t] = __dadd_rn(hc[t], __dmul_rn(alpha, v));  // distinct t
+  }
+  if (x.dense && cn != 0)
+    for (int64_t t = threadIdx.x; t < w; t += blockDim.x) {
+      const double v = x.dense[static_cast<int64_t>(j) * w + t];
+      D[static_cast<int64_t>(c) * w + t] = v;
+      if (!mine) hc[t] = __dadd_rn(hc[t], __dmul_rn(alpha, v));
+    }
+  for (int r = threadIdx.x; r <= nr; r += blockDim.x)
+    rs[static_cast<int64_t>(c) * (nr + 1) + r] = x.rs[static_cast<int64_t>(j) * (nr + 1) + r];
+  for (int a = threadIdx.x; a < d; a += blockDim.x) {
+    cli_gvec[static_cast<int64_t>(c) * d + a] = x.gvec[static_cast<int64_t>(j) * d + a];
+    dgvec_all[static_cast<int64_t>(j) * d + a] = x.dg[static_cast<int64_t>(j) * d + a];
+  }
+  if (threadIdx.x == 0) {
+    count[c] = cn;
+    flags[c] = x.flags[j];
+    cli_shift[c] = x.shift[j];
+    dshift_all[j] = x.ds[j];
+  }
+}
+
+// Sharded FedNL: every rank's status code after its own clients' work
+// (compressor failures are rank-local), all-gathered; the first raised code
+// halts every rank (otherwise the others would go on calling collectives)
+__global__ void k_code_post(const DevCtl* __restrict__ ctl, int rank, int32_t* __restrict__ code) {
+  if (threadIdx.x == 0) code[rank] = ctl->code;
+}
+__global__ void k_code_sync(DevCtl* __restrict__ ctl, int world, const int32_t* __restrict__ code) {
+  if (threadIdx.x != 0 || ctl->code != 0) return;
+  for (int r = 0; r < world; ++r)
+    if (code[r] != 0) {
+      raise_status(ctl, code[r]);
+      return;
+    }
+}
+
 // ------------------------------------------------------------ initialisation
 
 // Hest[c] = lam_c I (cli_diag set: the shard's lambda) or 0 for every

@@ -678,28 +678,31 @@ def test_round0_shift_norms_match_oracle(name):
         eng.close()
 
 
-def test_sharded_path_world1_matches_unsharded():
-    """The client-sharded round (NCCL all-gathers inside the captured graph)
-    with one rank reproduces the single-GPU trajectory bit for bit."""
+@pytest.mark.parametrize("name", ["c0_r4", "ls_topk", "fednl_natural", "fednl_exact_init", "pp_randk",
+                                  "pp_identity_stop", "c2_r30"])
+def test_sharded_path_world1_matches_unsharded(name):
+    """The client-sharded round (fb_set_shard: NCCL all-gathers inside the
+    captured graph — in the line search's while-loop body for FedNL-LS, the
+    dense updates for Identity / Natural, the round-0 Hessians for exact
+    init, the participant-slot exchange for FedNL-PP) with one rank
+    reproduces the single-GPU rows, iterate and master state bit for bit."""
     from paper_2410_08760_b200.engine import nccl_unique_id
 
-    shards = D.baseline_shards("c0")
-    cfg = D.baseline_run_config("c0", rounds=6)
-    d, n, ni, lam = shards[0].dim, len(shards), shards[0].n_samples, shards[0].lam
+    cfg, shards = sim_case(name)
+    d, n, ni = shards[0].dim, len(shards), shards[0].n_samples
     out = []
     for shard in (False, True):
-        eng = FedNLEngine(cfg, d, n, ni, lam=lam)
+        eng = FedNLEngine(cfg, d, n, ni)
         try:
             if shard:
                 eng.set_shard(1, 0, nccl_unique_id())
-            eng.upload([s.bmat for s in shards])
-            eng.init_state()
-            b = eng.run_rounds(6)
-            out.append((b.grad_norm.copy(), b.f_value.copy(), b.entry_counts.copy(), eng.get_x(),
-                        eng.get_master_hest(), eng.final_eval()))
+            rows = simulate(cfg, shards, engine=eng)
+            out.append(([(r.grad_norm, r.f_value, r.bytes_up_cum, r.ls_steps) for r in rows], eng.get_x(),
+                        eng.get_master_hest()))
         finally:
             eng.close()
-    for a, b in zip(out[0], out[1]):
+    assert out[0][0] == out[1][0]
+    for a, b in zip(out[0][1:], out[1][1:]):
         assert np.array_equal(np.asarray(a), np.asarray(b))
 
 

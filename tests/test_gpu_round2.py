@@ -160,3 +160,27 @@ def test_ls_toplek_8d_at_c0_shape_matches_reference():
     rows = simulate(cfg, shards)
     g = golden("compress_r2.npz")
     _rows_close(rows, g, ["ls_toplek8d_c0"])
+
+
+@pytest.mark.parametrize("name", ["ls_deep", "ragged_pp"])
+def test_sharded_world1_deep_line_search_and_ragged_pp(name):
+    """One-rank sharding with the NCCL gather inside the line search's
+    while-loop body (up to 8 trial batches per round), and sharded FedNL-PP
+    on ragged shards: bit-identical to the unsharded engine."""
+    from paper_2410_08760_b200.engine import nccl_unique_id
+
+    kw, shards = case_r2(name)
+    cfg = run_config(kw)
+    d, n, ni = shards[0].dim, len(shards), max(s.n_samples for s in shards)
+    out = []
+    for shard in (False, True):
+        eng = FedNLEngine(cfg, d, n, ni)
+        try:
+            if shard:
+                eng.set_shard(1, 0, nccl_unique_id())
+            rows = simulate(cfg, shards, engine=eng)
+            out.append(([(r.grad_norm, r.f_value, r.bytes_up_cum, r.ls_steps) for r in rows], eng.get_x()))
+        finally:
+            eng.close()
+    assert out[0][0] == out[1][0]
+    assert np.array_equal(out[0][1], out[1][1])

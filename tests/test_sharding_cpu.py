@@ -117,3 +117,98 @@ def test_shard_range_partitions_every_client_once():
                 assert 0 <= lo <= hi <= n
                 seen.extend(range(lo, hi))
             assert seen == list(range(n))
+
+
+def _worker_ls_pp(rank: int, world: int, port: int, out_q) -> None:
+    """FedNL-LS (trial losses per client, all-gathered per trial batch) and
+    FedNL-PP (participant slots split over the ranks, per-slot outputs
+    exchanged, the non-owners applying the client update) — the
+    decompositions fb_set_shard runs on the GPUs, replayed with the oracle."""
+    import torch.distributed as dist
+
+    from oracle import fednl_oracle as O
+    from paper_2410_08760_b200.engine import shard_range
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        bmats = _problem()
+        n, d = len(bmats), bmats[0].shape[0]
+        lo, hi = shard_range(n, world, rank)
+        results = {}
+
+        # ---- FedNL-LS: every client-map (round work and the trial f) sharded by client
+        class ShardedLS(O.OracleRun):
+            def _map(self, fn, cids):
+                mine = {c: fn(c) for c in cids if lo <= c < hi}
+                parts = [None] * world
+                dist.all_gather_object(parts, mine)
+                merged = {}
+                for p in parts:
+                    merged.update(p)
+                return merged
+
+        cfg = O.OracleConfig(algorithm="fednl-ls", kind="topk", k=2 * d, rounds=4, ls_c=0.99, ls_gamma=0.8,
+                             lam=1e-3, run_seed=5)
+        ref, run = O.OracleRun(cfg, bmats, lam=1e-3), ShardedLS(cfg, bmats, lam=1e-3)
+        ref_rows, rows = ref.run(), run.run()
+        results["ls"] = (np.array_equal(ref.x, run.x) and
+                         [(r.grad_norm, r.ls_steps) for r in ref_rows] == [(r.grad_norm, r.ls_steps) for r in rows]
+                         and max(r.ls_steps for r in rows) >= 4)
+
+        # ---- FedNL-PP: participant slots [r * spr, (r + 1) * spr) per rank
+        class ShardedPP(O.OracleRun):
+            def _map(self, fn, cids):
+                if fn.__name__ != "<lambda>" or len(cids) == self.n:  # probes: by client range
+                    mine = {c: fn(c) for c in cids if lo <= c < hi}
+                    parts = [None] * world
+                    dist.all_gather_object(parts, mine)
+                    merged = {}
+                    for p in parts:
+                        merged.update(p)
+                    return merged
+                spr = (len(cids) + world - 1) // world
+                mine_slots = cids[rank * spr:(rank + 1) * spr]
+                mine = {}
+                for c in mine_slots:
+                    res = fn(c)  # the owner applies its client's update itself
+                    mine[c] = (res, self.h_cli[c].copy(), self.cli_shift[c], self.cli_gvec[c].copy())
+                parts = [None] * world
+                dist.all_gather_object(parts, mine)
+                merged = {}
+                for p in parts:
+                    for c, (res, h, sh, gv) in p.items():
+                        if c not in mine:  # a non-owner: the owner's client state
+                            self.h_cli[c] = h
+                            self.cli_shift[c] = sh
+                            self.cli_gvec[c] = gv
+                        merged[c] = res
+                return merged
+
+        cfg = O.OracleConfig(algorithm="fednl-pp", kind="randk", k=d, rounds=6, tau=3, lam=1e-3, run_seed=9)
+        ref, run = O.OracleRun(cfg, bmats, lam=1e-3), ShardedPP(cfg, bmats, lam=1e-3)
+        ref_rows, rows = ref.run(), run.run()
+        results["pp"] = (np.array_equal(ref.x, run.x) and np.array_equal(ref.h_cli, run.h_cli) and
+                         [r.grad_norm for r in ref_rows] == [r.grad_norm for r in rows])
+        out_q.put((rank, results))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_two_rank_ls_and_pp_sharding_reproduce_single_process_rounds():
+    import torch.multiprocessing as mp
+
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker_ls_pp, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=240) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+    for rank, r in sorted(res):
+        assert r["ls"], f"rank {rank}: sharded FedNL-LS diverged"
+        assert r["pp"], f"rank {rank}: sharded FedNL-PP diverged"
