@@ -626,6 +626,43 @@ def gen_compress_r2():
     return out
 
 
+def gen_csv():
+    """The reference's metrics CSV text and canonical_config lines
+    (runtime.py:69-113, transport.py:205-232) for fixed rows and configs."""
+    import io
+
+    from fednl.runtime import MetricsRow, write_csv
+    from fednl.transport import canonical_config
+
+    rows = [MetricsRow(0, 0.0, 0.24282060357349974, 0.6931471805599453, 0, 42784, 0),
+            MetricsRow(1, 0.012345678901234568, 1e-300, -0.0, 31312, 85568, 3),
+            MetricsRow(2, 1.5, 5e-324, 1.7976931348623157e308, 2**40, 2**41, 60)]
+    out = {}
+    cfgs = {
+        "default": RunConfig(),
+        "c0": RunConfig(compressor=CompressorSpec(CompressorKind.TOPK, k=2408), alpha=1.0, rounds=100, run_seed=1),
+        "ls": RunConfig(algorithm="fednl-ls", compressor=CompressorSpec(CompressorKind.TOPLEK, k=69),
+                        ls_c=0.3, ls_gamma=0.7, lam=1e-4),
+        "pp": RunConfig(algorithm="fednl-pp", tau=12, compressor=CompressorSpec(CompressorKind.RANDK, k=301),
+                        reconstruct_indices=False, hessian_init="exact", run_seed=2**40),
+        "opt_a": RunConfig(option="a", mu=0.05, compressor=CompressorSpec(CompressorKind.TOPK, k=9,
+                                                                            topk_weighted=True)),
+        "natural": RunConfig(compressor=CompressorSpec(CompressorKind.NATURAL), hessian_init="zero"),
+    }
+    names = sorted(cfgs)
+    for name in names:
+        line = canonical_config(cfgs[name], 301 if name != "ls" else 69, 142)
+        buf = io.StringIO()
+        write_csv(rows, buf, config_line=line)
+        out[f"{name}__line"] = np.array(line)
+        out[f"{name}__csv"] = np.array(buf.getvalue())
+    buf = io.StringIO()
+    write_csv(rows, buf)
+    out["noconfig__csv"] = np.array(buf.getvalue())
+    out["names"] = np.array(names)
+    return out
+
+
 def gen_sim_opt_a():
     return gen_sim([n for n in SIM_CASES if "opt_a" in n])
 
@@ -646,6 +683,7 @@ def main(only=None):
         ("simulate_r2.npz", gen_sim_r2),
         ("simulate_c4.npz", gen_c4),
         ("compress_r2.npz", gen_compress_r2),
+        ("csv.npz", gen_csv),
     ):
         if only and fname not in only:
             continue

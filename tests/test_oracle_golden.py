@@ -379,3 +379,46 @@ def test_large_w_toplek_and_randk_against_reference():
                 assert prg.next_u64() == int(g[base + "__next"]), base
                 n_checked += 1
     assert n_checked == 40
+
+
+def test_csv_and_canonical_config_match_reference_text(tmp_path):
+    """write_csv (with and without the '# config:' line) and canonical_config
+    produce the reference's bytes (runtime.py:69-113, transport.py:205-232);
+    read_csv round-trips every float exactly."""
+    import io
+
+    from paper_2410_08760_b200 import CompressorKind, CompressorSpec, RunConfig
+    from paper_2410_08760_b200.runtime import MetricsRow, canonical_config, read_csv, write_csv
+
+    g = golden("csv.npz")
+    rows = [MetricsRow(0, 0.0, 0.24282060357349974, 0.6931471805599453, 0, 42784, 0),
+            MetricsRow(1, 0.012345678901234568, 1e-300, -0.0, 31312, 85568, 3),
+            MetricsRow(2, 1.5, 5e-324, 1.7976931348623157e308, 2**40, 2**41, 60)]
+    cfgs = {
+        "default": RunConfig(),
+        "c0": RunConfig(compressor=CompressorSpec(CompressorKind.TOPK, k=2408), alpha=1.0, rounds=100, run_seed=1),
+        "ls": RunConfig(algorithm="fednl-ls", compressor=CompressorSpec(CompressorKind.TOPLEK, k=69),
+                        ls_c=0.3, ls_gamma=0.7, lam=1e-4),
+        "pp": RunConfig(algorithm="fednl-pp", tau=12, compressor=CompressorSpec(CompressorKind.RANDK, k=301),
+                        reconstruct_indices=False, hessian_init="exact", run_seed=2**40),
+        "opt_a": RunConfig(option="a", mu=0.05, compressor=CompressorSpec(CompressorKind.TOPK, k=9,
+                                                                            topk_weighted=True)),
+        "natural": RunConfig(compressor=CompressorSpec(CompressorKind.NATURAL), hessian_init="zero"),
+    }
+    assert sorted(cfgs) == g["names"].tolist()
+    for name, cfg in cfgs.items():
+        line = canonical_config(cfg, 301 if name != "ls" else 69, 142)
+        assert line == str(g[f"{name}__line"]), name
+        buf = io.StringIO()
+        write_csv(rows, buf, config_line=line)
+        assert buf.getvalue() == str(g[f"{name}__csv"]), name
+    buf = io.StringIO()
+    write_csv(rows, buf)
+    assert buf.getvalue() == str(g["noconfig__csv"])
+    path = tmp_path / "rows.csv"
+    path.write_text(str(g["c0__csv"]))
+    line, back = read_csv(str(path))
+    assert line == str(g["c0__line"])
+    assert [(r.round, r.wall_seconds, r.grad_norm, r.f_value, r.bytes_up_cum, r.bytes_down_cum, r.ls_steps)
+            for r in back] == [(r.round, r.wall_seconds, r.grad_norm, r.f_value, r.bytes_up_cum,
+                                r.bytes_down_cum, r.ls_steps) for r in rows]
