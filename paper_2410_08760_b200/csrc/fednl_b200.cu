@@ -663,7 +663,11 @@ int enqueue_fednl_round(Ctx* ctx) {
   // Under a profiler's injection library (ncu serialises every launch anyway)
   // the launch-completion attribute is not supported: order the compressor
   // after the solve instead.
+#ifdef FB_SERIAL_EXP
+  const bool serial = true;
+#else
   const bool serial = under_profiler();
+#endif
   CK(cudaEventRecord(ctx->ev_fork, s));
   CK(cudaStreamWaitEvent(ctx->st2, ctx->ev_fork, 0));
   if (opt_a) {  // eigen_clamp_min(H^k, mu) of the pre-fold estimate, then its Cholesky solve
@@ -679,6 +683,10 @@ int enqueue_fednl_round(Ctx* ctx) {
     CK(cudaEventRecord(ctx->ev_solve_launched, s));
   }
   CK(cudaStreamWaitEvent(ctx->st2, ctx->ev_solve_launched, 0));
+  if (fuse_red && !serial) {  // the compressor waits for the solve's reduction (k_wait_reduce)
+    k_wait_reduce<<<1, 32, 0, ctx->st2>>>(ctx->ctl);
+    CKL();
+  }
   TRY(record(ctx, EV_COMP_START, ctx->st2));
   // split TopK: the client shift update runs in the fold (K7), which stages
   // every client's entries per position range anyway

@@ -173,6 +173,24 @@ __global__ void __launch_bounds__(RED_THREADS) k_reduce(
   }
 }
 
+// Holds the compressor (stream-ordered behind this one-thread kernel) until
+// the solve's fused round reduction is done: the compressor streams the
+// whole D through HBM, and the reduction's dependent loads (gradients,
+// partials, x) would otherwise each wait several microseconds behind it
+// (c0: 21 -> 12 us).  The factorisation that follows has ~20 us of slack
+// over the compressor and fold.  Returns at once on a halted round; a gate
+// that never opens traps (a loud failure, not a hang).
+__global__ void k_wait_reduce(const DevCtl* __restrict__ ctl) {
+  if (threadIdx.x != 0) return;
+  const volatile int32_t* gate = &ctl->red_gate;
+  const volatile int32_t* halt = &ctl->halt;
+  const int32_t want = ctl->round + 1;
+  for (uint32_t spin = 0; *gate != want && !*halt; ++spin) {
+    __nanosleep(256);
+    if (spin > (1u << 24)) asm volatile("trap;");
+  }
+}
+
 // Dense kinds (identity / natural): client shift update + master fold per
 // packed position t, clients in ascending id (compressors.py:373-393,
 // algorithms.py:234, 369-372):

@@ -795,13 +795,38 @@ __global__ void __launch_bounds__(CH_THREADS, 1) k_chol_panels(
     const int a0 = q_lo * CP_NB + lane;
     const int a1 = (KP > 1 && q_lo + cs < npan) ? (q_lo + cs) * CP_NB + lane : d;
     constexpr int GU = 18;  // clients per warp and batch: n <= 144 in one round trip
+    // Every load of the reduction is issued before any is consumed: a
+    // dependent round trip costs 1-2 us while the compressor streams D.
+    // (b) staging: this CTA's client chunk's loss / Frobenius partials and
+    // lambda / n_i / flags, in the rcv buffer (free until panel 0's push)
+    const int cpc = (n + cs - 1) / cs;
+    const int c_lo = min(n, rank * cpc), c_hi = min(n, c_lo + cpc);
+    const int per_c = red.nblk + red.n_pairs;
+    const int per_s = per_c + 3;
+    double* stage = &sm.rcv[0][0];
+    const int chunk = max(1, (2 * CP_NB * CP_LS) / per_s);
+    auto stage_chunk = [&](int i0, int nc) {
+      for (int e = tid; e < nc * per_s; e += CH_THREADS) {
+        const int ii = e / per_s, r = e - ii * per_s, c = i0 + ii;
+        double v;
+        if (r < red.nblk) v = __ldcg(red.loss_part + static_cast<int64_t>(c) * red.nblk + r);
+        else if (r < per_c) v = __ldcg(red.frob_part + static_cast<int64_t>(c) * red.n_pairs + (r - red.nblk));
+        else if (r == per_c) v = red.lam[c];
+        else if (r == per_c + 1) v = static_cast<double>(red.ni[c]);
+        else v = static_cast<double>(__ldcg(red.flags + c));
+        stage[e] = v;
+      }
+    };
+    double v0[GU], v1[GU];
     for (int c0 = warp; c0 < n; c0 += 8 * GU) {
-      double v0[GU], v1[GU];
 #pragma unroll
       for (int u = 0; u < GU; ++u) {
         const int c = c0 + 8 * u;
         v0[u] = (c < n && a0 < d) ? __ldcg(red.grad + static_cast<int64_t>(c) * d + a0) : 0.0;
         v1[u] = (c < n && a1 < d) ? __ldcg(red.grad + static_cast<int64_t>(c) * d + a1) : 0.0;
+      }
+      if (c0 == warp) {  // with the first gradient batch in flight
+        stage_chunk(c_lo, min(chunk, c_hi - c_lo));
       }
 #pragma unroll
       for (int u = 0; u < GU; ++u) {
@@ -809,11 +834,10 @@ __global__ void __launch_bounds__(CH_THREADS, 1) k_chol_panels(
         acc1 = __dadd_rn(acc1, v1[u]);
       }
     }
+    if (n <= warp) stage_chunk(c_lo, min(chunk, c_hi - c_lo));  // (no gradient batch on this warp)
+    if (tid == 0) tl_mark(9, true);
     rwork[warp][lane] = acc0;
     rwork[warp][CP_NB + lane] = acc1;
-    // (b) per-client scalars of chunk `rank`
-    const int cpc = (n + cs - 1) / cs;
-    const int c_lo = min(n, rank * cpc), c_hi = min(n, c_lo + cpc);
     double xx_p = 0.0;
     for (int a = tid; a < d; a += CH_THREADS) xx_p = fma(x[a], x[a], xx_p);
     double fs_t = 0.0, ss_t = 0.0;
@@ -826,35 +850,32 @@ __global__ void __launch_bounds__(CH_THREADS, 1) k_chol_panels(
       for (int w2 = 0; w2 < 8; ++w2) t2 = __dadd_rn(t2, rwork[w2][tid]);
       sm.gown[tid] = __ddiv_rn(t2, static_cast<double>(red.n_div));
     }
-    // warp per client: the lanes load its loss / Frobenius partials at once,
-    // the sums run in partial order through shuffles
-    const int per_c = red.nblk + red.n_pairs;
-    for (int c = c_lo + warp; c < c_hi; c += 8) {
-      double ls = 0.0, fp = 0.0;
-      for (int r0 = 0; r0 < per_c; r0 += 32) {
-        const int r = r0 + lane;
-        const double v = r < red.nblk ? __ldcg(red.loss_part + static_cast<int64_t>(c) * red.nblk + r)
-                         : r < per_c   ? __ldcg(red.frob_part + static_cast<int64_t>(c) * red.n_pairs + (r - red.nblk))
-                                       : 0.0;
-        const int m = min(32, per_c - r0);
-        for (int i = 0; i < m; ++i) {
-          const double vi = __shfl_sync(0xffffffffu, v, i);
-          if (r0 + i < red.nblk) ls = __dadd_rn(ls, vi);
-          else fp = __dadd_rn(fp, vi);
-        }
+    // per-client scalars: thread per client, the partials summed in order
+    for (int i0 = c_lo; i0 < c_hi; i0 += chunk) {
+      const int nc = min(chunk, c_hi - i0);
+      if (i0 != c_lo) {
+        __syncthreads();
+        stage_chunk(i0, nc);
+        __syncthreads();
       }
-      const double reg = __dmul_rn(__dmul_rn(0.5, red.lam[c]), xx);
-      const double fc = __dadd_rn(__ddiv_rn(ls, static_cast<double>(red.ni[c])), reg);
-      const double sc = sqrt(fp);
-      if (lane == 0) {
+      for (int ii = tid; ii < nc; ii += CH_THREADS) {
+        const int c = i0 + ii;
+        const double* st = stage + ii * per_s;
+        double ls = 0.0, fp = 0.0;
+        for (int r = 0; r < red.nblk; ++r) ls = __dadd_rn(ls, st[r]);
+        for (int r = red.nblk; r < per_c; ++r) fp = __dadd_rn(fp, st[r]);
+        const double reg = __dmul_rn(__dmul_rn(0.5, st[per_c]), xx);
+        const double fc = __dadd_rn(__ddiv_rn(ls, st[per_c + 1]), reg);
+        const double sc = sqrt(fp);
         red.f_cli[c] = fc;
         red.shift_cli[c] = sc;
         fs_t += fc;
         ss_t += sc;
-        if (red.flags[c] & 1) bad_t = min(bad_t, c);
+        if (static_cast<int>(st[per_c + 2]) & 1) bad_t = min(bad_t, c);
       }
     }
     __syncthreads();
+    if (tid == 0) tl_mark(10, true);
     double gg_t = 0.0;
     if (tid < 2 * CP_NB) {
       const int a = tid < CP_NB ? a0 - lane + tid : (a1 < d ? a1 - lane + tid - CP_NB : d);
@@ -888,7 +909,9 @@ __global__ void __launch_bounds__(CH_THREADS, 1) k_chol_panels(
     if (tid < CP_NB)
       Pq[rs * CP_LS + tid] = tid < pb ? (fused ? sm.gown[k * CP_NB + tid] : __ldcg(rhs + q0 + tid)) : 0.0;
   }
+  if (tid == 0) tl_mark(11, false);
   cluster.sync();  // barriers initialised and reduction partials published cluster-wide
+  if (tid == 0) tl_mark(11, true);
   if (fused) {
     // cluster sums in rank order (identical in every CTA)
     double gg = 0.0, fs = 0.0, ss = 0.0, bad = 2147483647.0;
@@ -900,6 +923,10 @@ __global__ void __launch_bounds__(CH_THREADS, 1) k_chol_panels(
       bad = fmin(bad, rp[3]);
     }
     shift = __ddiv_rn(ss, static_cast<double>(red.n_div));
+    if (rank == 0 && tid == 0) {  // the compressor may start streaming D now (k_wait_reduce)
+      __threadfence();
+      atomicExch(&ctl->red_gate, ctl->round + 1);
+    }
     if (rank == 0 && tid == 0) {
       red.out->grad_norm = sqrt(gg);
       red.out->f_mean = __ddiv_rn(fs, static_cast<double>(red.n_div));
@@ -926,6 +953,7 @@ __global__ void __launch_bounds__(CH_THREADS, 1) k_chol_panels(
     if (tid < pb) Pq[tid * CP_LS + tid] = __dadd_rn(Pq[tid * CP_LS + tid], shift);
   }
   __syncthreads();
+  if (tid == 0) tl_mark(7, true);
   mark(0);
 
   // ---- factorisation.  Panel p - 1's owner pushes L_{p-1}'s slots 32..95
@@ -1234,6 +1262,7 @@ __global__ void __launch_bounds__(CH_THREADS, 1) k_chol_panels(
     mark(8);
   }
   mark(1);
+  if (tid == 0) tl_mark(8, true);
   if (rank == 0) stamp(63, 0);
   cluster.sync();  // failure flags settled cluster-wide
   if (rank == 0) stamp(63, 1);

@@ -14,7 +14,7 @@ eng.run_rounds(5)
 lib = _lib.load()
 buf = (C.c_ulonglong * 32)()
 cnt = (C.c_longlong * (32 + 1024 + 2048))()
-names = ["margins", "hessian", "solve", "solve_wait", "topk", "fold", "finish"]
+names = ["margins", "hessian", "solve", "solve_wait", "topk", "fold", "finish", "reduce_done", "factor_done", "red_loads", "red_clients", "red_csync"]
 acc = {}
 for rep in range(8):
     lib.fb_debug_timeline(buf)           # re-arm
@@ -25,9 +25,9 @@ for rep in range(8):
     t0 = buf[0]
     for s, nm in enumerate(names):
         a, b = buf[2 * s], buf[2 * s + 1]
-        if a == 2**64 - 1 or b == 0:
+        if b == 0:
             continue
-        acc.setdefault(nm, []).append(((a - t0) / 1e3, (b - t0) / 1e3))
+        acc.setdefault(nm, []).append((((a - t0) / 1e3) if a != 2**64 - 1 else float("nan"), (b - t0) / 1e3))
 for nm in names:
     if nm in acc:
         v = np.array(acc[nm])
