@@ -2379,6 +2379,7 @@ __global__ void __launch_bounds__(TK_THREADS) k_toplek(
     int32_t* __restrict__ count, uint32_t* __restrict__ idx_list, double* __restrict__ val_list,
     int cap, int32_t* __restrict__ draws, int P, Emit em, const int32_t* __restrict__ npw_tab) {
   if (ctl && ctl->halt) return;
+  if (threadIdx.x == 0) tl_mark(4, false);
   PhaseClock pc;
   __shared__ int32_t s_tab[NPW_TAB_MAX];
   __shared__ double s_red8[8 * NPW_TAB_LEAVES];
@@ -2476,6 +2477,7 @@ __global__ void __launch_bounds__(TK_THREADS) k_toplek(
   compact_bitmap(brow, wb, v, 1.0, idx_list + static_cast<int64_t>(c) * cap,
                  val_list + static_cast<int64_t>(c) * cap, ws, em, c);
   pc.mark(28);
+  if (threadIdx.x == 0) tl_mark(4, true);
 }
 
 // ------------------------------------------------------ TopLEK, large w

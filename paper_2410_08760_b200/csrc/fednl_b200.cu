@@ -719,8 +719,9 @@ int enqueue_fednl_round(Ctx* ctx) {
   TRY(record(ctx, EV_SOLVE_END, s));
   int launches = ctx->topk_split ? 9 : 8;
   if (ls) {
-    // FedNL-LS: batches of LS_BATCH Armijo trials as the body of a
-    // while-conditional node; k_ls_decide keeps the loop going until a trial
+    // FedNL-LS: the first batch of LS_BATCH Armijo trials in line, later
+    // batches (rare) as the body of a while-conditional node that the first
+    // k_ls_decide arms; k_ls_decide keeps the loop going until a trial
     // passes, or raises ST_LINE_SEARCH past s = 60 (algorithms.py:284-311)
     cudaStreamCaptureStatus cst;
     cudaGraph_t cg = nullptr;
@@ -728,7 +729,24 @@ int enqueue_fednl_round(Ctx* ctx) {
     size_t ndeps = 0;
     CK(cudaStreamGetCaptureInfo(s, &cst, nullptr, &cg, &deps, &ndeps));
     cudaGraphConditionalHandle loop;
-    CK(cudaGraphConditionalHandleCreate(&loop, cg, 1, cudaGraphCondAssignDefault));
+    CK(cudaGraphConditionalHandleCreate(&loop, cg, 0, cudaGraphCondAssignDefault));
+    auto ls_batch = [&](cudaStream_t q) -> int {
+      dim3 grid(ctx->ls_nblk, n_loc);
+      k_ls_trials<<<grid, MARGIN_THREADS, LS_BATCH * ctx->d * sizeof(double), q>>>(
+          ctx->ctl, ctx->Bt, ctx->d, ctx->ni_arr, ctx->ldj, loc, ctx->x, ctx->pvec, ctx->steps_table,
+          ctx->trial_x, ctx->ls_loss_part, ctx->ls_nblk);
+      CKL();
+      if (shd)  // the trials' per-client loss partials of every rank
+        TRY(gather_clients(ctx, ctx->ls_loss_part, static_cast<size_t>(LS_BATCH) * ctx->ls_nblk,
+                           ncclFloat64, q));
+      k_ls_decide<<<1, 256, 0, q>>>(ctx->ctl, ctx->d, n, ctx->ni_arr, ctx->lam_arr, ctx->ls_nblk,
+                                    ctx->cfg.ls_c, ctx->steps_table, ctx->trial_x, ctx->ls_loss_part,
+                                    ctx->sc, ctx->x_new, LS_BATCH, ctx->gbar, ctx->pvec, loop);
+      CKL();
+      return FB_OK;
+    };
+    TRY(ls_batch(s));
+    CK(cudaStreamGetCaptureInfo(s, &cst, nullptr, &cg, &deps, &ndeps));
     cudaGraphNodeParams cp{};
     cp.type = cudaGraphNodeTypeConditional;
     cp.conditional.handle = loop;
@@ -739,26 +757,10 @@ int enqueue_fednl_round(Ctx* ctx) {
     cudaGraph_t body = cp.conditional.phGraph_out[0];
     CK(cudaStreamBeginCaptureToGraph(ctx->st_body, body, nullptr, nullptr, 0,
                                      cudaStreamCaptureModeThreadLocal));
-    dim3 grid(ctx->ls_nblk, n_loc);
-    k_ls_trials<<<grid, MARGIN_THREADS, LS_BATCH * ctx->d * sizeof(double), ctx->st_body>>>(
-        ctx->ctl, ctx->Bt, ctx->d, ctx->ni_arr, ctx->ldj, loc, ctx->x, ctx->pvec, ctx->steps_table,
-        ctx->trial_x, ctx->ls_loss_part, ctx->ls_nblk);
-    cudaError_t e1 = cudaGetLastError();
-    int r1 = FB_OK;
-    if (e1 == cudaSuccess && shd)  // the trials' per-client loss partials of every rank
-      r1 = gather_clients(ctx, ctx->ls_loss_part, static_cast<size_t>(LS_BATCH) * ctx->ls_nblk,
-                          ncclFloat64, ctx->st_body);
-    if (e1 == cudaSuccess && r1 == FB_OK) {
-      k_ls_decide<<<1, 256, 0, ctx->st_body>>>(ctx->ctl, ctx->d, n, ctx->ni_arr, ctx->lam_arr,
-                                               ctx->ls_nblk, ctx->cfg.ls_c, ctx->steps_table,
-                                               ctx->trial_x, ctx->ls_loss_part, ctx->sc, ctx->x_new,
-                                               LS_BATCH, ctx->gbar, ctx->pvec, loop);
-      e1 = cudaGetLastError();
-    }
+    const int r1 = ls_batch(ctx->st_body);
     cudaGraph_t body_out = body;
     const cudaError_t e2 = cudaStreamEndCapture(ctx->st_body, &body_out);
     if (r1 != FB_OK) return r1;
-    CK(e1);
     CK(e2);
     CK(cudaStreamUpdateCaptureDependencies(s, &wnode, 1, cudaStreamSetCaptureDependencies));
     launches += 2;

@@ -48,6 +48,7 @@ __global__ void __launch_bounds__(MB_THREADS) k_margins(
   // the Hessian pass may launch now (it waits for these coefficients)
   asm volatile("griddepcontrol.launch_dependents;");
   if (ctl && ctl->halt) return;
+  if (threadIdx.x == 0) tl_mark(0, false);
   extern __shared__ double xs[];
   __shared__ double part[8][MB_SAMPLES + 2];
   __shared__ double red[2];
@@ -108,7 +109,10 @@ __global__ void __launch_bounds__(MB_THREADS) k_margins(
     if (lane == 0) red[warp] = tot;
   }
   __syncthreads();
-  if (threadIdx.x == 0) loss_part[static_cast<int64_t>(c) * nblk + blockIdx.x] = red[0] + red[1];
+  if (threadIdx.x == 0) {
+    loss_part[static_cast<int64_t>(c) * nblk + blockIdx.x] = red[0] + red[1];
+    tl_mark(0, true);
+  }
 }
 
 // The same outputs with one CTA per client (used when the clients alone
@@ -276,6 +280,7 @@ __global__ void __launch_bounds__(MARGIN_THREADS) k_ls_trials(
     const double* __restrict__ steps_table, double* __restrict__ trial_x,
     double* __restrict__ loss_part, int nblk) {
   if (ctl->halt) return;
+  if (threadIdx.x == 0) tl_mark(13, false);
   extern __shared__ double xt[];  // [LS_BATCH][d]
   const int s0 = ctl->ls_next;
   const int c = client_of(clients, blockIdx.y);
@@ -324,6 +329,7 @@ __global__ void __launch_bounds__(MARGIN_THREADS) k_ls_trials(
     for (int i = 0; i < nw; ++i) tot += red4[s][i];
     loss_part[(static_cast<int64_t>(c) * LS_BATCH + s) * nblk + blockIdx.x] = tot;
   }
+  if (threadIdx.x == 0) tl_mark(13, true);
 }
 
 }  // namespace fb

@@ -44,6 +44,7 @@ __global__ void __launch_bounds__(RED_THREADS) k_reduce(
   // the next kernel (the master solve) may start its H^k setup now
   asm volatile("griddepcontrol.launch_dependents;");
   if (ctl->halt) return;
+  if (threadIdx.x == 0) tl_mark(12, false);
   PhaseClock pc;
   // warm L2 with the next kernel's input (the master H^k for the solve)
   if (l2_prefetch)
@@ -170,6 +171,7 @@ __global__ void __launch_bounds__(RED_THREADS) k_reduce(
       ctl->bad_client = 0x7fffffff - bad;
       raise_status(ctl, ST_NONFINITE);
     }
+    tl_mark(12, true);
   }
 }
 
@@ -788,6 +790,7 @@ __global__ void __launch_bounds__(256) k_ls_decide(
     double* __restrict__ x_new, int batch, const double* __restrict__ gbar,
     const double* __restrict__ p, cudaGraphConditionalHandle loop) {
   const int s0 = ctl->ls_next;
+  if (threadIdx.x == 0) tl_mark(14, true);
   if (ctl->halt || s0 > 60) {  // nothing to decide: leave the loop
     if (threadIdx.x == 0) {
       ctl->ls_next = 0;

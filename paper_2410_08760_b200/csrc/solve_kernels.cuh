@@ -94,6 +94,7 @@ __global__ void __launch_bounds__(CH_THREADS, 1) k_chol_solve(
   // outputs at the end.  sm.failed is ordered before any DSMEM push by the
   // first cluster barrier below.
   if (tid == 0) sm.failed = 0;
+  if (tid == 0) tl_mark(2, false);
   for (int k2 = tid; k2 < PLD; k2 += CH_THREADS) pan[(d + NB) / NB * NB * PLD + k2] = 0.0;  // zero row
   const double shift = shift_ptr ? __ldcg(shift_ptr) : 0.0;
 
@@ -387,6 +388,7 @@ __global__ void __launch_bounds__(CH_THREADS, 1) k_chol_solve(
     }
   }
   mark(9);
+  if (tid == 0) tl_mark(2, true);
   if (!ignore_halt && ctl->halt) return;
   for (int i = tid; i < d; i += CH_THREADS) {
     const double zi = y[i];

@@ -14,7 +14,7 @@ eng.run_rounds(5)
 lib = _lib.load()
 buf = (C.c_ulonglong * 32)()
 cnt = (C.c_longlong * (32 + 1024 + 2048))()
-names = ["margins", "hessian", "solve", "solve_wait", "topk", "fold", "finish", "reduce_done", "factor_done", "red_loads", "red_clients", "red_csync"]
+names = ["margins", "hessian", "solve", "solve_wait", "topk", "fold", "finish", "reduce_done", "factor_done", "red_loads", "red_clients", "red_csync", "k_reduce", "ls_trials", "ls_decide"]
 acc = {}
 for rep in range(8):
     lib.fb_debug_timeline(buf)           # re-arm
@@ -22,7 +22,7 @@ for rep in range(8):
     eng.run_rounds(1)
     lib.fb_debug_counters(0, cnt)
     lib.fb_debug_timeline(buf)
-    t0 = buf[0]
+    t0 = min(buf[2 * s] for s in range(16) if buf[2 * s] != 2**64 - 1)
     for s, nm in enumerate(names):
         a, b = buf[2 * s], buf[2 * s + 1]
         if b == 0:
