@@ -391,6 +391,9 @@ int launch_hessian(Ctx* ctx, cudaStream_t s, const int32_t* clients, int n_activ
   cudaLaunchConfig_t lc{};
   const int items = n_active * ctx->n_pairs;
   lc.gridDim = dim3(std::min((items + HW_PIPES - 1) / HW_PIPES, ctx->num_sms));
+  // about two tiles per pipe or fewer: no later tile to hide an epilogue
+  // behind, so each pipe's five warps finish every tile together
+  const int solo = items <= 2 * HW_PIPES * static_cast<int>(lc.gridDim.x) ? 1 : 0;
   lc.blockDim = dim3(HW_THREADS);
   lc.dynamicSmemBytes = HESS_WS_SMEM;
   lc.stream = s;
@@ -399,7 +402,7 @@ int launch_hessian(Ctx* ctx, cudaStream_t s, const int32_t* clients, int n_activ
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   lc.attrs = attr;
   lc.numAttrs = pdl_ok(ctx) ? 1 : 0;
-  CK(cudaLaunchKernelEx(&lc, k_hessian_ws, ctx->tmap, static_cast<const DevCtl*>(with_ctl ? ctx->ctl : nullptr),
+  CK(cudaLaunchKernelEx(&lc, solo ? k_hessian_ws<true> : k_hessian_ws<false>, ctx->tmap, static_cast<const DevCtl*>(with_ctl ? ctx->ctl : nullptr),
                         ctx->d, static_cast<const int32_t*>(ctx->ni_arr), ctx->ldh,
                         static_cast<const double*>(ctx->hcoef), static_cast<const double*>(ctx->lam_arr), clients,
                         hest, hest_stride, D, hess_out, ctx->frob_part, ctx->flags,
@@ -1135,7 +1138,9 @@ int fb_create(const fb_config* cfg_in, void** out) {
   static size_t max_toplek = 0, max_solve = 0;
   max_toplek = std::max(max_toplek, toplek_smem_bytes(std::max(ctx->toplek_P, 1)));
   max_solve = std::max(max_solve, std::max<size_t>(ctx->solve_smem, 1));
-  CKC(cudaFuncSetAttribute(k_hessian_ws, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  CKC(cudaFuncSetAttribute(k_hessian_ws<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           static_cast<int>(HESS_WS_SMEM)));
+  CKC(cudaFuncSetAttribute(k_hessian_ws<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            static_cast<int>(HESS_WS_SMEM)));
   CKC(cudaFuncSetAttribute(k_topk_smem, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            static_cast<int>(TKS_SMEM)));

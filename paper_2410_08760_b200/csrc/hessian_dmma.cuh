@@ -87,6 +87,8 @@ struct __align__(1024) HwPipe {
   uint64_t cs_full;              // 4 DMMA warps -> epilogue warp
   uint64_t cs_empty;             // epilogue warp -> DMMA warps
   int32_t itemq[HW_QUEUE];       // claimed item of the pipe's j-th tile (-1: no more)
+  int32_t solo_item;             // solo mode: the tile the pipe's five warps finish together
+  double solo_part[HW_MMA + 1];  // solo mode: per-warp Frobenius partials (summed in warp order)
 };
 constexpr size_t HESS_WS_SMEM = HW_PIPES * sizeof(HwPipe) + 1024;
 
@@ -229,6 +231,82 @@ __device__ __forceinline__ void hw_skip(HwPipe& sm, int nk, int g0, int lane) {
   }
 }
 
+// The epilogue of a tile over columns c0, c0 + step, ... (the epilogue warp
+// alone: 0, 1; in solo mode each of the pipe's five warps: r, 5): D = H (+ lam
+// on the diagonal) - H_i^k in packed column segments (H too when
+// requested); returns the warp's Frobenius partial (all lanes), ORs flags.
+// H_i^k operands are loaded 8 columns at a time, the next 8 in flight.
+__device__ __forceinline__ double hw_epi_cols(HwPipe& sm, const HwItem& itm, int c0, int step, int d,
+                                              int64_t w, const double* __restrict__ hest, int64_t hest_stride,
+                                              const double* __restrict__ lam_arr, double* __restrict__ D,
+                                              double* __restrict__ hess_out, int32_t* __restrict__ flags,
+                                              int lane, uint64_t* release = nullptr) {
+  const double* hest_c = hest + static_cast<int64_t>(itm.c) * hest_stride;
+  const double lam = lam_arr[itm.c];
+  double* Dc = D + static_cast<int64_t>(itm.c) * w;
+  double* Hc = hess_out ? hess_out + static_cast<int64_t>(itm.slot) * w : nullptr;
+  const int ncol = min(HT, d - itm.J * HT);
+  constexpr int ECH = 8;  // columns per chunk: 16 loads in flight per lane
+  double hk[ECH][2];
+  auto load_chunk = [&](int k0) {
+#pragma unroll
+    for (int q = 0; q < ECH; ++q) {
+      const int col = c0 + (k0 + q) * step, b = itm.J * HT + col;
+#pragma unroll
+      for (int h2 = 0; h2 < 2; ++h2) {
+        const int a = itm.I * HT + lane + 32 * h2;
+        hk[q][h2] = (col < ncol && a <= b) ? __ldg(hest_c + packed_at(a, b)) : 0.0;
+      }
+    }
+  };
+  const int nmine = ncol > c0 ? (ncol - c0 + step - 1) / step : 0;  // this warp's columns
+  load_chunk(0);
+  double part = 0.0;
+  int fl = 0;
+  for (int k0 = 0; k0 < nmine; k0 += ECH) {
+    double hv[ECH][2];
+#pragma unroll
+    for (int q = 0; q < ECH; ++q) {
+      const int col = min(c0 + (k0 + q) * step, HT - 1);
+#pragma unroll
+      for (int h2 = 0; h2 < 2; ++h2) hv[q][h2] = sm.cs[col * HW_LD + lane + 32 * h2];
+    }
+    double hkc[ECH][2];
+#pragma unroll
+    for (int q = 0; q < ECH; ++q) hkc[q][0] = hk[q][0], hkc[q][1] = hk[q][1];
+    if (k0 + ECH < nmine) load_chunk(k0 + ECH);  // the next chunk's loads in flight
+#pragma unroll
+    for (int q = 0; q < ECH; ++q) {
+      const int col = c0 + (k0 + q) * step, b = itm.J * HT + col;
+      if (col >= ncol) continue;
+      const int64_t cbase = packed_at(0, b);
+#pragma unroll
+      for (int h2 = 0; h2 < 2; ++h2) {
+        const int a = itm.I * HT + lane + 32 * h2;
+        if (a > b) continue;
+        double h = hv[q][h2];
+        if (a == b) h = __dadd_rn(h, lam);
+        const double dv = __dsub_rn(h, hkc[q][h2]);
+        Dc[cbase + a] = dv;
+        if (Hc) Hc[cbase + a] = h;
+        const double wt = (a == b) ? 1.0 : 2.0;
+        part = fma(__dmul_rn(wt, dv), dv, part);
+        if (!isfinite(dv)) fl |= 1;
+        if (dv != 0.0) fl |= 2;
+      }
+    }
+  }
+  if (release) {  // every read of `cs` is done: hand it back before the sums
+    __syncwarp();
+    if (lane == 0) mbar_arrive(release);
+  }
+  part = warp_sum(part);
+  fl = __reduce_or_sync(0xffffffffu, fl);
+  if (lane == 0 && fl) atomicOr(&flags[itm.c], fl);
+  return part;
+}
+
+template <bool solo>
 __global__ void __launch_bounds__(HW_THREADS, 1) k_hessian_ws(
     const __grid_constant__ CUtensorMap tmap_b, const DevCtl* __restrict__ ctl, int d,
     const int32_t* __restrict__ ni_arr, int ldh, const double* __restrict__ hcoef,
@@ -316,6 +394,11 @@ __global__ void __launch_bounds__(HW_THREADS, 1) k_hessian_ws(
       mbar_wait(&sm.full[gsn % HW_STAGE], (gsn / HW_STAGE) & 1);  // the item's first stage (or the end)
       const int L = sm.itemq[j % HW_QUEUE];
       if (L < 0) {  // tell the epilogue, once it has taken the last tile
+        if constexpr (solo) {
+          if (q4 == 0 && lane == 0) sm.solo_item = -1;
+          asm volatile("bar.sync %0, %1;" ::"r"(1 + pipe), "r"((HW_MMA + 1) * 32) : "memory");
+          break;
+        }
         if (j > 0) mbar_wait(&sm.cs_empty, (j - 1) & 1);
         __syncwarp();
         if (lane == 0) mbar_arrive(&sm.cs_full);
@@ -357,7 +440,7 @@ __global__ void __launch_bounds__(HW_THREADS, 1) k_hessian_ws(
         }
       }
       // hand the accumulators to the epilogue once it has read the last tile
-      if (j > 0) mbar_wait(&sm.cs_empty, (j - 1) & 1);
+      if (j > 0 && !solo) mbar_wait(&sm.cs_empty, (j - 1) & 1);
       if (active) {
 #pragma unroll
         for (int mi = 0; mi < 4; ++mi)
@@ -368,6 +451,15 @@ __global__ void __launch_bounds__(HW_THREADS, 1) k_hessian_ws(
               for (int e = 0; e < 2; ++e)
                 sm.cs[(8 * (tk.c0 + nj) + 2 * t + e) * HW_LD + 8 * (tk.r0 + mi) + g] = acc[mi][nj][e];
       }
+      if constexpr (solo) {  // few tiles per pipe: the five warps finish this one together
+        if (q4 == 0 && lane == 0) sm.solo_item = L;
+        asm volatile("bar.sync %0, %1;" ::"r"(1 + pipe), "r"((HW_MMA + 1) * 32) : "memory");
+        const double part = hw_epi_cols(sm, itm, q4, HW_MMA + 1, d, w, hest, hest_stride, lam_arr, D,
+                                        hess_out, flags, lane);
+        if (lane == 0) sm.solo_part[q4] = part;
+        asm volatile("bar.sync %0, %1;" ::"r"(1 + pipe), "r"((HW_MMA + 1) * 32) : "memory");
+        continue;
+      }
       __syncwarp();
       if (lane == 0) mbar_arrive(&sm.cs_full);
     }
@@ -375,71 +467,32 @@ __global__ void __launch_bounds__(HW_THREADS, 1) k_hessian_ws(
   }
 
   // ------------------------------------------------------------ epilogue
-  for (int j = 0;; ++j) {
-    mbar_wait(&sm.cs_full, j & 1);
-    const int L = sm.itemq[j % HW_QUEUE];
-    if (L < 0) break;
-    const HwItem itm = hw_item(L, n_pairs, n_act, grp, pair_order, clients, ni_arr);
-    const double* hest_c = hest + static_cast<int64_t>(itm.c) * hest_stride;
-    const double lam = lam_arr[itm.c];
-    double* Dc = D + static_cast<int64_t>(itm.c) * w;
-    double* Hc = hess_out ? hess_out + static_cast<int64_t>(itm.slot) * w : nullptr;
-    const int ncol = min(HT, d - itm.J * HT);
-    // the first chunk's H_i^k operands before the tile lands
-    constexpr int ECH = 8;  // columns per chunk: 16 loads in flight per lane
-    double hk[ECH][2];
-    auto load_chunk = [&](int c0) {
+  if constexpr (solo) {
+    for (;;) {
+      asm volatile("bar.sync %0, %1;" ::"r"(1 + pipe), "r"((HW_MMA + 1) * 32) : "memory");
+      const int L = sm.solo_item;
+      if (L < 0) break;
+      const HwItem itm = hw_item(L, n_pairs, n_act, grp, pair_order, clients, ni_arr);
+      const double part = hw_epi_cols(sm, itm, HW_MMA, HW_MMA + 1, d, w, hest, hest_stride, lam_arr, D,
+                                      hess_out, flags, lane);
+      if (lane == 0) sm.solo_part[HW_MMA] = part;
+      asm volatile("bar.sync %0, %1;" ::"r"(1 + pipe), "r"((HW_MMA + 1) * 32) : "memory");
+      if (lane == 0) {
+        double tot = 0.0;
 #pragma unroll
-      for (int q = 0; q < ECH; ++q) {
-        const int col = c0 + q, b = itm.J * HT + col;
-#pragma unroll
-        for (int h2 = 0; h2 < 2; ++h2) {
-          const int a = itm.I * HT + lane + 32 * h2;
-          hk[q][h2] = (col < ncol && a <= b) ? __ldg(hest_c + packed_at(a, b)) : 0.0;
-        }
-      }
-    };
-    load_chunk(0);
-    double part = 0.0;
-    int fl = 0;
-    for (int c0 = 0; c0 < ncol; c0 += ECH) {
-      double hv[ECH][2];
-#pragma unroll
-      for (int q = 0; q < ECH; ++q)
-#pragma unroll
-        for (int h2 = 0; h2 < 2; ++h2) hv[q][h2] = sm.cs[(c0 + q) * HW_LD + lane + 32 * h2];
-      double hkc[ECH][2];
-#pragma unroll
-      for (int q = 0; q < ECH; ++q) hkc[q][0] = hk[q][0], hkc[q][1] = hk[q][1];
-      if (c0 + ECH < ncol) load_chunk(c0 + ECH);  // the next chunk's loads in flight
-#pragma unroll
-      for (int q = 0; q < ECH; ++q) {
-        const int col = c0 + q, b = itm.J * HT + col;
-        if (col >= ncol) continue;
-        const int64_t cbase = packed_at(0, b);
-#pragma unroll
-        for (int h2 = 0; h2 < 2; ++h2) {
-          const int a = itm.I * HT + lane + 32 * h2;
-          if (a > b) continue;
-          double h = hv[q][h2];
-          if (a == b) h = __dadd_rn(h, lam);
-          const double dv = __dsub_rn(h, hkc[q][h2]);
-          Dc[cbase + a] = dv;
-          if (Hc) Hc[cbase + a] = h;
-          const double wt = (a == b) ? 1.0 : 2.0;
-          part = fma(__dmul_rn(wt, dv), dv, part);
-          if (!isfinite(dv)) fl |= 1;
-          if (dv != 0.0) fl |= 2;
-        }
+        for (int q = 0; q <= HW_MMA; ++q) tot += sm.solo_part[q];
+        frob_part[static_cast<int64_t>(itm.c) * n_pairs + itm.pair] = tot;
       }
     }
-    __syncwarp();
-    if (lane == 0) mbar_arrive(&sm.cs_empty);  // the DMMA warps may stage the next tile
-    part = warp_sum(part);
-    fl = __reduce_or_sync(0xffffffffu, fl);
-    if (lane == 0) {
-      frob_part[static_cast<int64_t>(itm.c) * n_pairs + itm.pair] = part;
-      if (fl) atomicOr(&flags[itm.c], fl);
+  } else {
+    for (int j = 0;; ++j) {
+      mbar_wait(&sm.cs_full, j & 1);
+      const int L = sm.itemq[j % HW_QUEUE];
+      if (L < 0) break;
+      const HwItem itm = hw_item(L, n_pairs, n_act, grp, pair_order, clients, ni_arr);
+      const double part = hw_epi_cols(sm, itm, 0, 1, d, w, hest, hest_stride, lam_arr, D, hess_out, flags, lane,
+                                      &sm.cs_empty);  // (the DMMA warps may stage the next tile)
+      if (lane == 0) frob_part[static_cast<int64_t>(itm.c) * n_pairs + itm.pair] = part;
     }
   }
   if (lane == 0) tl_mark(1, true);
