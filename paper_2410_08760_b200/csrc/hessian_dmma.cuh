@@ -236,33 +236,47 @@ __device__ __forceinline__ void hw_skip(HwPipe& sm, int nk, int g0, int lane) {
 // on the diagonal) - H_i^k in packed column segments (H too when
 // requested); returns the warp's Frobenius partial (all lanes), ORs flags.
 // H_i^k operands are loaded 8 columns at a time, the next 8 in flight.
-__device__ __forceinline__ double hw_epi_cols(HwPipe& sm, const HwItem& itm, int c0, int step, int d,
-                                              int64_t w, const double* __restrict__ hest, int64_t hest_stride,
-                                              const double* __restrict__ lam_arr, double* __restrict__ D,
-                                              double* __restrict__ hess_out, int32_t* __restrict__ flags,
-                                              int lane, uint64_t* release = nullptr) {
-  const double* hest_c = hest + static_cast<int64_t>(itm.c) * hest_stride;
-  const double lam = lam_arr[itm.c];
-  double* Dc = D + static_cast<int64_t>(itm.c) * w;
-  double* Hc = hess_out ? hess_out + static_cast<int64_t>(itm.slot) * w : nullptr;
-  const int ncol = min(HT, d - itm.J * HT);
+//
+// The FP64 pipe is the DMMA pipe: every DADD / DMUL here waits behind the
+// DMMA warps' issue, and one warp runs a whole tile's epilogue, so the loop is
+// kept to two FP64 instructions per element (the difference, one FMA into
+// the Frobenius partial) and a few integer ones.  On a diagonal tile lam is
+// first added to this warp's diagonal entries of `cs` (column c of the tile
+// holds (c, c) at row c); every term is weighted 2 in the loop and the
+// diagonal terms' surplus is taken back after it.  Flags: non-finite iff the
+// largest |high word| reaches the exponent mask; nonzero iff any bit of
+// |dv| is set (so -0.0 counts as zero, NaN as nonzero, like dv != 0.0).
+template <bool DIAG>
+__device__ __forceinline__ double hw_epi_body(HwPipe& sm, const HwItem& itm, int c0, int step, int nmine, int ncol,
+                                              const double* __restrict__ hest_c, double* __restrict__ Dc,
+                                              double* __restrict__ Hc, double lam, int lane, uint32_t& hmax,
+                                              uint32_t& nzb) {
   constexpr int ECH = 8;  // columns per chunk: 16 loads in flight per lane
+  const int a0 = itm.I * HT + lane;
   double hk[ECH][2];
   auto load_chunk = [&](int k0) {
 #pragma unroll
     for (int q = 0; q < ECH; ++q) {
       const int col = c0 + (k0 + q) * step, b = itm.J * HT + col;
+      const int cb = b * (b + 1) / 2;  // packed column start (< 2^31 for d <= 46340)
 #pragma unroll
       for (int h2 = 0; h2 < 2; ++h2) {
-        const int a = itm.I * HT + lane + 32 * h2;
-        hk[q][h2] = (col < ncol && a <= b) ? __ldg(hest_c + packed_at(a, b)) : 0.0;
+        const int a = a0 + 32 * h2;
+        hk[q][h2] = (col < ncol && (!DIAG || a <= b)) ? __ldg(hest_c + cb + a) : 0.0;
       }
     }
   };
-  const int nmine = ncol > c0 ? (ncol - c0 + step - 1) / step : 0;  // this warp's columns
+  if (DIAG) {
+#pragma unroll
+    for (int h2 = 0; h2 < 2; ++h2) {
+      const int cc = lane + 32 * h2;
+      if (cc < ncol && cc >= c0 && (cc - c0) % step == 0)
+        sm.cs[cc * HW_LD + cc] = __dadd_rn(sm.cs[cc * HW_LD + cc], lam);
+    }
+    __syncwarp();
+  }
   load_chunk(0);
-  double part = 0.0;
-  int fl = 0;
+  double po = 0.0;
   for (int k0 = 0; k0 < nmine; k0 += ECH) {
     double hv[ECH][2];
 #pragma unroll
@@ -279,29 +293,56 @@ __device__ __forceinline__ double hw_epi_cols(HwPipe& sm, const HwItem& itm, int
     for (int q = 0; q < ECH; ++q) {
       const int col = c0 + (k0 + q) * step, b = itm.J * HT + col;
       if (col >= ncol) continue;
-      const int64_t cbase = packed_at(0, b);
+      const int cb = b * (b + 1) / 2;
+      double* dcol = Dc + cb + a0;
 #pragma unroll
       for (int h2 = 0; h2 < 2; ++h2) {
-        const int a = itm.I * HT + lane + 32 * h2;
-        if (a > b) continue;
-        double h = hv[q][h2];
-        if (a == b) h = __dadd_rn(h, lam);
+        if (DIAG && a0 + 32 * h2 > b) continue;
+        const double h = hv[q][h2];
         const double dv = __dsub_rn(h, hkc[q][h2]);
-        Dc[cbase + a] = dv;
-        if (Hc) Hc[cbase + a] = h;
-        const double wt = (a == b) ? 1.0 : 2.0;
-        part = fma(__dmul_rn(wt, dv), dv, part);
-        if (!isfinite(dv)) fl |= 1;
-        if (dv != 0.0) fl |= 2;
+        dcol[32 * h2] = dv;
+        if (Hc) Hc[cb + a0 + 32 * h2] = h;
+        po = fma(dv, dv, po);
+        const uint32_t habs = static_cast<uint32_t>(__double2hiint(dv)) & 0x7fffffffu;
+        hmax = max(hmax, habs);
+        nzb |= habs | static_cast<uint32_t>(__double2loint(dv));
       }
     }
   }
+  double part = 2.0 * po;
+  if (DIAG) {  // the diagonal terms count once: take one of the two back
+#pragma unroll
+    for (int h2 = 0; h2 < 2; ++h2) {
+      const int cc = lane + 32 * h2, a = a0 + 32 * h2;
+      if (cc < ncol && cc >= c0 && (cc - c0) % step == 0) {
+        const double dv = __dsub_rn(sm.cs[cc * HW_LD + cc], __ldg(hest_c + a * (a + 1) / 2 + a));
+        part = fma(-dv, dv, part);
+      }
+    }
+  }
+  return part;
+}
+
+__device__ __forceinline__ double hw_epi_cols(HwPipe& sm, const HwItem& itm, int c0, int step, int d,
+                                              int64_t w, const double* __restrict__ hest, int64_t hest_stride,
+                                              const double* __restrict__ lam_arr, double* __restrict__ D,
+                                              double* __restrict__ hess_out, int32_t* __restrict__ flags,
+                                              int lane, uint64_t* release = nullptr) {
+  const double* hest_c = hest + static_cast<int64_t>(itm.c) * hest_stride;
+  const double lam = lam_arr[itm.c];
+  double* Dc = D + static_cast<int64_t>(itm.c) * w;
+  double* Hc = hess_out ? hess_out + static_cast<int64_t>(itm.slot) * w : nullptr;
+  const int ncol = min(HT, d - itm.J * HT);
+  const int nmine = ncol > c0 ? (ncol - c0 + step - 1) / step : 0;  // this warp's columns
+  uint32_t hmax = 0, nzb = 0;
+  double part = itm.diag ? hw_epi_body<true>(sm, itm, c0, step, nmine, ncol, hest_c, Dc, Hc, lam, lane, hmax, nzb)
+                         : hw_epi_body<false>(sm, itm, c0, step, nmine, ncol, hest_c, Dc, Hc, lam, lane, hmax, nzb);
   if (release) {  // every read of `cs` is done: hand it back before the sums
     __syncwarp();
     if (lane == 0) mbar_arrive(release);
   }
   part = warp_sum(part);
-  fl = __reduce_or_sync(0xffffffffu, fl);
+  const int fl = __reduce_or_sync(0xffffffffu, (hmax >= 0x7ff00000u ? 1 : 0) | (nzb != 0 ? 2 : 0));
   if (lane == 0 && fl) atomicOr(&flags[itm.c], fl);
   return part;
 }
