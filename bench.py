@@ -224,7 +224,7 @@ def run_ours(args) -> dict | None:
             nccl_id = box[0]
 
     def make_engine():
-        e = FedNLEngine(cfg, d, n, ni)
+        e = FedNLEngine(cfg, d, n, ni, topk_path=args.topk_path)
         if sharded:
             e.set_shard(world, rank, nccl_id)
         return e
@@ -466,6 +466,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--topk-path", type=int, default=0, help=argparse.SUPPRESS)  # A/B of TopK variants
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

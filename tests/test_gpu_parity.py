@@ -142,16 +142,24 @@ def test_compressors_bit_exact_at_c0_size(kind, k, topk_path):
     d = 301
     w = O.packed_len(d)
     rng = np.random.default_rng(7)
-    P = rng.standard_normal((6, w))
+    P = rng.standard_normal((9, w))
     P[1] = np.round(P[1] * 4) / 4  # massive ties
     P[2] = 0.0  # empty delta
     P[3, ::3] = 0.0
     P[4] = np.abs(P[4])
     P[5] = -0.0 * P[5]  # negative zeros only -> all-zero
-    seeds = [O.round_seed(9, c, 4) for c in range(6)]
+    # zeros complete the set (converged / structurally zero entries), with and
+    # without subnormal keys above them; subnormals deciding the selection
+    P[6] = 0.0
+    P[6, rng.choice(w, 100, replace=False)] = rng.standard_normal(100)
+    P[7] = 0.0
+    P[7, rng.choice(w, 80, replace=False)] = np.concatenate([rng.standard_normal(50), rng.standard_normal(30) * 1e-310])
+    P[8] = 0.0
+    P[8, rng.choice(w, 3000, replace=False)] = np.concatenate([rng.standard_normal(2000), rng.standard_normal(1000) * 1e-310])
+    seeds = [O.round_seed(9, c, 4) for c in range(len(P))]
     spec = CompressorSpec(CompressorKind(kind), k=k)
     got = leaf.compress_packed_batch(P, d, spec, seeds)
-    for c in range(6):
+    for c in range(len(P)):
         want = O.compress_packed(P[c], d, kind, k, O.SplitMix64(seeds[c]))
         assert got[c].entry_count == want.count, c
         assert np.array_equal(got[c].indices, want.indices), c
@@ -388,12 +396,14 @@ def test_split_topk_rounds_bit_identical_to_stream_path():
     cfg, shards = sim_case("c0_r4")
     cfg = RunConfig(compressor=cfg.compressor, rounds=12, alpha=cfg.alpha, run_seed=cfg.run_seed)
     out = {}
-    for path in (_lib.TOPK_PATH_STREAM, _lib.TOPK_PATH_SPLIT):
+    paths = (_lib.TOPK_PATH_STREAM, _lib.TOPK_PATH_SPLIT)
+    for path in paths:
         eng = FedNLEngine(cfg, shards[0].dim, len(shards), shards[0].n_samples, topk_path=path)
         out[path] = simulate(cfg, shards, engine=eng)
         eng.close()
-    for a, b in zip(out[_lib.TOPK_PATH_STREAM], out[_lib.TOPK_PATH_SPLIT]):
-        assert (a.round, a.grad_norm, a.f_value, a.bytes_up_cum) == (b.round, b.grad_norm, b.f_value, b.bytes_up_cum)
+    for path in paths[1:]:
+        for a, b in zip(out[_lib.TOPK_PATH_STREAM], out[path]):
+            assert (a.round, a.grad_norm, a.f_value, a.bytes_up_cum) == (b.round, b.grad_norm, b.f_value, b.bytes_up_cum)
 
 
 # --------------------------------------------------------------------- P6
