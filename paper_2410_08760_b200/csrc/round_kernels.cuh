@@ -230,12 +230,24 @@ __global__ void __launch_bounds__(256) k_fold_dense(
 
 // Master fold of the sparse kinds (algorithms.py:369-372): one CTA per range
 // of FOLD_RANGE packed positions.  Every client's ascending (idx, val) list is
-// sliced by the compressor's range starts rs[c][r]; the slices are staged in
-// shared memory (coalesced, all clients at once), then applied in ascending
+// sliced by the compressor's range starts rs[c][r] and applied in ascending
 // client order:  Hout[t] = fl(Hin[t] + fl((alpha/n) v_c))  — the reference's
 // sequential sparse fold, bit for bit.  Hin may alias Hout.
+//
+// Per pass over a chunk of clients (at most FOLD_PC clients / FOLD_STAGE
+// entries): every thread loads its entries (FOLD_EPT, all loads in flight)
+// and sets bit (client) of its position's client mask; thread p then owns
+// position p: its entry count is the mask's popcount, a block scan gives the
+// position's slot range, each entry's rank inside it is the popcount of the
+// mask below its client (so the slots hold the position's entries in client
+// order), and thread p adds them in that order.  No step is sequential over
+// clients.
 constexpr int FOLD_THREADS = 256;
-constexpr int FOLD_STAGE = 4096;  // staged entries per pass
+constexpr int FOLD_EPT = 12;                           // entries per thread and pass
+constexpr int FOLD_STAGE = FOLD_EPT * FOLD_THREADS;    // entries per pass
+constexpr int FOLD_PC = 512;                           // clients per pass
+constexpr int FOLD_MW = FOLD_PC / 32;                  // mask words per position
+static_assert(FOLD_RANGE == FOLD_THREADS, "thread p owns position p of the range");
 __global__ void __launch_bounds__(FOLD_THREADS) k_master_fold(
     const DevCtl* __restrict__ ctl, int64_t w, int n_active, const int32_t* __restrict__ clients,
     int cap, int nr, const int32_t* __restrict__ rs, const uint32_t* __restrict__ idx_list,
@@ -244,18 +256,19 @@ __global__ void __launch_bounds__(FOLD_THREADS) k_master_fold(
   if (ctl->halt) return;
   if (threadIdx.x == 0) tl_mark(5, false);
   extern __shared__ int32_t fold_sm[];  // beg[n], cnt[n], off[n+1]
-  __shared__ double hs[FOLD_RANGE];
-  __shared__ uint16_t st_t[FOLD_STAGE];
-  __shared__ double st_v[FOLD_STAGE];
+  __shared__ uint32_t mask[FOLD_RANGE][FOLD_MW + 1];  // +1: conflict-free rows
+  __shared__ double sv[FOLD_STAGE];
+  __shared__ int pstart[FOLD_RANGE + 1];
   __shared__ int ws[64];
   int32_t* beg = fold_sm;
   int32_t* cnt = fold_sm + n_active;
   int32_t* off = fold_sm + 2 * n_active;
+  const int tid = threadIdx.x;
   const int r = blockIdx.x;
   const int64_t t0 = static_cast<int64_t>(r) * FOLD_RANGE;
   const int len = static_cast<int>((w - t0 < FOLD_RANGE) ? (w - t0) : FOLD_RANGE);
-  for (int i = threadIdx.x; i < len; i += FOLD_THREADS) hs[i] = h_in[t0 + i];
-  for (int i = threadIdx.x; i < n_active; i += FOLD_THREADS) {
+  double h = tid < len ? h_in[t0 + tid] : 0.0;  // thread p owns position p
+  for (int i = tid; i < n_active; i += FOLD_THREADS) {
     const int c = client_of(clients, i);
     const int32_t* rc = rs + static_cast<int64_t>(c) * (nr + 1);
     const int b = rc[r];
@@ -267,77 +280,90 @@ __global__ void __launch_bounds__(FOLD_THREADS) k_master_fold(
   {
     int carry = 0;
     for (int base = 0; base < n_active; base += FOLD_THREADS) {
-      const int i = base + threadIdx.x;
+      const int i = base + tid;
       const int v = (i < n_active) ? cnt[i] : 0;
       int total;
       const int o = block_excl_scan(v, ws, &total) + carry;
       if (i < n_active) off[i] = o;
       carry += total;
     }
-    if (threadIdx.x == 0) off[n_active] = carry;
+    if (tid == 0) off[n_active] = carry;
   }
   __syncthreads();
-  // passes over [first client, last client) whose entries fit the stage
   int ca = 0;
   while (ca < n_active) {
-    // largest cb with off[cb] - off[ca] <= FOLD_STAGE (at least one client)
-    int lo = ca + 1, hi = n_active;
+    // largest cb with off[cb] - off[ca] <= FOLD_STAGE, cb - ca <= FOLD_PC (at least one client)
+    int lo = ca + 1, hi = min(n_active, ca + FOLD_PC);
     while (lo < hi) {
       const int mid = (lo + hi + 1) >> 1;
       if (off[mid] - off[ca] <= FOLD_STAGE) lo = mid; else hi = mid - 1;
     }
     const int cb = lo;
     const int e0 = off[ca], e1 = off[cb];  // a client's slice is <= FOLD_RANGE < FOLD_STAGE
-    // stage entries [e0, e1): entry e belongs to the client i with off[i] <= e < off[i+1]
-    constexpr int UF = 4;  // entries per thread in flight
-    for (int eb = e0; eb < e1; eb += UF * FOLD_THREADS) {
-      uint32_t ti[UF];
-      double tv[UF];
+    const int mwp = (cb - ca + 31) >> 5;
+    for (int q = tid; q < FOLD_RANGE * mwp; q += FOLD_THREADS) mask[q / mwp][q % mwp] = 0u;
+    // this thread's entries: client (binary search in the staged offsets),
+    // then every load in flight
+    int ci[FOLD_EPT], pp[FOLD_EPT];
+    int64_t src[FOLD_EPT];
 #pragma unroll
-      for (int u = 0; u < UF; ++u) {
-        const int e = eb + u * FOLD_THREADS + threadIdx.x;
-        if (e < e1) {
-          int a = ca, b = cb - 1;
-          while (a < b) {
-            const int mid = (a + b + 1) >> 1;
-            if (off[mid] <= e) a = mid; else b = mid - 1;
-          }
-          const int c = client_of(clients, a);
-          const int64_t src = static_cast<int64_t>(c) * cap + beg[a] + (e - off[a]);
-          ti[u] = idx_list[src];
-          tv[u] = val_list[src];
-          if (hest) {  // the client shift update (compressors.py:373-393), distinct (c, t)
-            double* hp = hest + static_cast<int64_t>(c) * hest_stride + ti[u];
-            *hp = __dadd_rn(*hp, __dmul_rn(alpha, tv[u]));
-          }
+    for (int u = 0; u < FOLD_EPT; ++u) {
+      const int e = e0 + u * FOLD_THREADS + tid;
+      ci[u] = -1;
+      src[u] = 0;
+      if (e < e1) {
+        int a = ca, b = cb - 1;
+        while (a < b) {
+          const int mid = (a + b + 1) >> 1;
+          if (off[mid] <= e) a = mid; else b = mid - 1;
         }
-      }
-#pragma unroll
-      for (int u = 0; u < UF; ++u) {
-        const int e = eb + u * FOLD_THREADS + threadIdx.x;
-        if (e < e1) {
-          st_t[e - e0] = static_cast<uint16_t>(ti[u] - t0);
-          st_v[e - e0] = tv[u];
-        }
+        ci[u] = a;
+        src[u] = static_cast<int64_t>(client_of(clients, a)) * cap + beg[a] + (e - off[a]);
       }
     }
-    __syncthreads();
-    if (threadIdx.x < 32) {  // apply in ascending client order (distinct t within a client)
-      const int lane = threadIdx.x;
-      for (int i = ca; i < cb; ++i) {
-        const int n_i = off[i + 1] - off[i];
-        for (int e = lane; e < n_i; e += 32) {
-          const int q = off[i] - e0 + e;
-          const int tt = st_t[q];
-          hs[tt] = __dadd_rn(hs[tt], __dmul_rn(alpha_n, st_v[q]));
-        }
-        __syncwarp();
+    uint32_t ti[FOLD_EPT];
+    double tv[FOLD_EPT];
+#pragma unroll
+    for (int u = 0; u < FOLD_EPT; ++u) {
+      ti[u] = ci[u] >= 0 ? idx_list[src[u]] : 0u;
+      tv[u] = ci[u] >= 0 ? val_list[src[u]] : 0.0;
+    }
+    __syncthreads();  // masks cleared
+#pragma unroll
+    for (int u = 0; u < FOLD_EPT; ++u) {
+      if (ci[u] < 0) continue;
+      if (hest) {  // the client shift update (compressors.py:373-393), distinct (c, t)
+        double* hp = hest + static_cast<int64_t>(client_of(clients, ci[u])) * hest_stride + ti[u];
+        *hp = __dadd_rn(*hp, __dmul_rn(alpha, tv[u]));
       }
+      pp[u] = static_cast<int>(ti[u] - t0);
+      const int k = ci[u] - ca;
+      atomicOr(&mask[pp[u]][k >> 5], 1u << (k & 31));
     }
     __syncthreads();
+    // position p's slot range: its mask's popcount, scanned over the range
+    {
+      int np = 0;
+      for (int q = 0; q < mwp; ++q) np += __popc(mask[tid][q]);
+      int total;
+      pstart[tid] = block_excl_scan(np, ws, &total);
+      if (tid == 0) pstart[FOLD_RANGE] = total;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int u = 0; u < FOLD_EPT; ++u) {
+      if (ci[u] < 0) continue;
+      const int k = ci[u] - ca, p = pp[u];
+      int rank = __popc(mask[p][k >> 5] & ((1u << (k & 31)) - 1u));
+      for (int q = 0; q < (k >> 5); ++q) rank += __popc(mask[p][q]);
+      sv[pstart[p] + rank] = tv[u];
+    }
+    __syncthreads();
+    for (int j = pstart[tid]; j < pstart[tid + 1]; ++j) h = __dadd_rn(h, __dmul_rn(alpha_n, sv[j]));
+    __syncthreads();  // sv / pstart / mask are rewritten by the next pass
     ca = cb;
   }
-  for (int i = threadIdx.x; i < len; i += FOLD_THREADS) h_out[t0 + i] = hs[i];
+  if (tid < len) h_out[t0 + tid] = h;
   if (threadIdx.x == 0) tl_mark(5, true);
 }
 
