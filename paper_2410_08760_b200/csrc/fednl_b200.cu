@@ -528,8 +528,7 @@ int launch_solve(Ctx* ctx, cudaStream_t s, const double* hpk, const double* shif
   cudaLaunchConfig_t lc{};
   lc.gridDim = dim3(cs);
   lc.blockDim = dim3(CH_THREADS);
-  lc.dynamicSmemBytes = panels ? static_cast<size_t>(ctx->cp_kp) * cp_panel_bytes(ctx->d) +
-                                     (dbg ? CP_STAMP_BYTES : 0)
+  lc.dynamicSmemBytes = panels ? static_cast<size_t>(ctx->cp_kp) * cp_panel_bytes(ctx->d) + CP_STAMP_BYTES
                                : ctx->solve_smem;
   lc.stream = s;
   cudaLaunchAttribute attr[4];

@@ -262,7 +262,7 @@ __device__ __forceinline__ double hw_epi_body(HwPipe& sm, const HwItem& itm, int
 #pragma unroll
       for (int h2 = 0; h2 < 2; ++h2) {
         const int a = a0 + 32 * h2;
-        hk[q][h2] = (col < ncol && (!DIAG || a <= b)) ? __ldg(hest_c + cb + a) : 0.0;
+        hk[q][h2] = (col < ncol && (!DIAG || a <= b)) ? __ldcs(hest_c + cb + a) : 0.0;
       }
     }
   };
@@ -300,7 +300,7 @@ __device__ __forceinline__ double hw_epi_body(HwPipe& sm, const HwItem& itm, int
         if (DIAG && a0 + 32 * h2 > b) continue;
         const double h = hv[q][h2];
         const double dv = __dsub_rn(h, hkc[q][h2]);
-        dcol[32 * h2] = dv;
+        __stcs(dcol + 32 * h2, dv);
         if (Hc) Hc[cb + a0 + 32 * h2] = h;
         po = fma(dv, dv, po);
         const uint32_t habs = static_cast<uint32_t>(__double2hiint(dv)) & 0x7fffffffu;
@@ -391,6 +391,7 @@ __global__ void __launch_bounds__(HW_THREADS, 1) k_hessian_ws(
     if (lane == 0) {
       asm volatile("griddepcontrol.wait;" ::: "memory");  // margins' coefficients
       int gsn = 0;
+      const uint64_t pol = l2_evict_first_policy();
       for (int j = 0;; ++j) {
         int L = atomicAdd(&sched[0], 1);
         if (L >= total) L = -1;
@@ -411,8 +412,8 @@ __global__ void __launch_bounds__(HW_THREADS, 1) k_hessian_ws(
           const int s2 = gsn % HW_STAGE;
           if (gsn >= HW_STAGE) mbar_wait(&sm.empty[s2], ((gsn / HW_STAGE) - 1) & 1);
           mbar_arrive_expect_tx(&sm.full[s2], stage_bytes);
-          tma_load_3d(sm.a[s2], &tmap_b, &sm.full[s2], it * HKC, itm.I * HT, itm.c);
-          if (!itm.diag) tma_load_3d(sm.b[s2], &tmap_b, &sm.full[s2], it * HKC, itm.J * HT, itm.c);
+          tma_load_3d_hint(sm.a[s2], &tmap_b, &sm.full[s2], it * HKC, itm.I * HT, itm.c, pol);
+          if (!itm.diag) tma_load_3d_hint(sm.b[s2], &tmap_b, &sm.full[s2], it * HKC, itm.J * HT, itm.c, pol);
           bulk_load(sm.h[s2], hrow + it * HKC, HKC * 8, &sm.full[s2]);
           if (fuse_grad) bulk_load(sm.gc[s2], grow + it * HKC, HKC * 8, &sm.full[s2]);
         }

@@ -690,8 +690,10 @@ __global__ void __launch_bounds__(CH_THREADS, 1) k_chol_panels(
   auto srow = [&](int p) { return p < CP_MAXP ? p : (p == 63 ? CP_MAXP : -1); };
   // a predicated store, not a branch: a branch taken by one lane would leave
   // the warp split for the code that follows (twice the issue slots)
+  // (also in the production round while g_dbg_on: to g_dbg_cta, row p = panel)
+  const bool stamping = dbg != nullptr || g_dbg_on;
   auto stamp_if = [&](bool on, int p, int k) {
-    if (dbg) {
+    if (stamping) {
       const long long tv = globaltimer_ns();
       const int row = srow(p);
       const uint32_t addr = smem_u32(stamps + (row < 0 ? 0 : row) * 16 + k);
@@ -702,7 +704,7 @@ __global__ void __launch_bounds__(CH_THREADS, 1) k_chol_panels(
   };
   auto stamp = [&](int p, int k) { stamp_if(tid == 0, p, k); };  // dbg[16 + 16 p + k], thread 0
   auto stamp_w = [&](int p, int k, int w) { stamp_if(tid == 32 * w, p, k); };  // lane 0 of warp w
-  if (dbg)
+  if (stamping)
     for (int i = tid; i < (CP_MAXP + 1) * 16; i += CH_THREADS) stamps[i] = 0;
   auto Lglob = [&](int p) { return Lg + static_cast<size_t>(p) * RS * CP_LS; };
   const int last_own = rank + ((npan - 1 - rank) / cs) * cs;  // highest own panel (rank < npan)
@@ -1329,10 +1331,12 @@ __global__ void __launch_bounds__(CH_THREADS, 1) k_chol_panels(
   }
   cluster.sync();  // no CTA leaves while its shared memory may be addressed
   if (tid == 0) tl_mark(2, true);
-  if (dbg)
+  if (stamping)
     for (int i = tid; i < (CP_MAXP + 1) * 16; i += CH_THREADS) {
       const int row = i / 16, k = i % 16;
-      if (stamps[i]) dbg[16 + (row < CP_MAXP ? row : 63) * 16 + k] = stamps[i];
+      if (!stamps[i]) continue;
+      if (dbg) dbg[16 + (row < CP_MAXP ? row : 63) * 16 + k] = stamps[i];
+      else g_dbg_cta[(row < CP_MAXP ? row : 63) * 16 + k] = stamps[i];
     }
 }
 
