@@ -382,6 +382,14 @@ int launch_gradient(Ctx* ctx, cudaStream_t s, const double* x, const int32_t* cl
 }
 // fuse_grad: the diagonal-tile CTAs also compute the local gradients at x
 // (ctx->grad), replacing k_gradient in the FedNL round
+// B's TMA tiles are marked L2 evict-first when a client's rows are small
+// (c0: 0.8 MB, re-read by its tile pairs within microseconds): the round's
+// streamed bytes then no longer push the latency-bound solve's code and state
+// out of L2.  A large client (c4: 16.8 MB) is re-read over milliseconds and
+// keeps the normal policy (evict-first there tripled its DRAM traffic).
+bool hess_b_evict_first(const Ctx* ctx) {
+  return static_cast<size_t>(ctx->d) * ctx->ldj * sizeof(double) <= (size_t{4} << 20);
+}
 int launch_hessian(Ctx* ctx, cudaStream_t s, const int32_t* clients, int n_active,
                    const double* hest, int64_t hest_stride, double* D, double* hess_out,
                    bool with_ctl = true, const double* fuse_grad_x = nullptr) {
@@ -409,7 +417,7 @@ int launch_hessian(Ctx* ctx, cudaStream_t s, const int32_t* clients, int n_activ
                         0u /* zero_mask: see mbar_arrive_dep */, static_cast<const double*>(ctx->gcoef),
                         fuse_grad_x, fuse_grad_x ? ctx->grad : nullptr,
                         static_cast<const int32_t*>(ctx->pair_order), ctx->n_pairs, n_active, hess_group(ctx),
-                        ctx->hess_sched));
+                        ctx->hess_sched, hess_b_evict_first(ctx) ? 1 : 0));
   return FB_OK;
 }
 int launch_reduce(Ctx* ctx, cudaStream_t s, const double* x, const int32_t* clients, int n_active,

@@ -356,7 +356,7 @@ __global__ void __launch_bounds__(HW_THREADS, 1) k_hessian_ws(
     double* __restrict__ hess_out, double* __restrict__ frob_part, int32_t* __restrict__ flags,
     uint32_t zero_mask, const double* __restrict__ gcoef, const double* __restrict__ x,
     double* __restrict__ grad, const int32_t* __restrict__ pair_order, int n_pairs, int n_act,
-    int grp, int32_t* __restrict__ sched) {
+    int grp, int32_t* __restrict__ sched, int b_evict_first) {
   // sched[0]: next unclaimed item, sched[1]: producers finished (the last
   // one re-arms both for the next launch)
   // the round reduction may launch now (it waits for this pass)
@@ -391,7 +391,7 @@ __global__ void __launch_bounds__(HW_THREADS, 1) k_hessian_ws(
     if (lane == 0) {
       asm volatile("griddepcontrol.wait;" ::: "memory");  // margins' coefficients
       int gsn = 0;
-      const uint64_t pol = l2_evict_first_policy();
+      const uint64_t pol = b_evict_first ? l2_evict_first_policy() : l2_evict_normal_policy();
       for (int j = 0;; ++j) {
         int L = atomicAdd(&sched[0], 1);
         if (L >= total) L = -1;
