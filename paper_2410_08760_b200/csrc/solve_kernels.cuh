@@ -488,6 +488,7 @@ struct CpSmem {
   double rpart[4];           // fused reduction: this CTA's partials (gg, fs, ss, bad)
   double gown[2 * CP_NB];    // fused reduction: gbar of the own panels' features
   double rscr[8];
+  double rscr3[3 * CH_THREADS / 32];
   int rbad;
   int failed;
 };
@@ -889,9 +890,8 @@ __global__ void __launch_bounds__(CH_THREADS, 1) k_chol_panels(
         gg_t = g * g;
       }
     }
-    const double gg = block_sum(gg_t, sm.rscr);
-    const double fs = block_sum(fs_t, sm.rscr);
-    const double ss = block_sum(ss_t, sm.rscr);
+    double gg = gg_t, fs = fs_t, ss = ss_t;
+    block_sum3(gg, fs, ss, sm.rscr3);
     bad_t = __reduce_min_sync(0xffffffffu, bad_t);
     if (lane == 0 && bad_t != 0x7fffffff) atomicMin(&sm.rbad, bad_t);
     __syncthreads();
@@ -927,10 +927,6 @@ __global__ void __launch_bounds__(CH_THREADS, 1) k_chol_panels(
       bad = fmin(bad, rp[3]);
     }
     shift = __ddiv_rn(ss, static_cast<double>(red.n_div));
-    if (rank == 0 && tid == 0) {  // the compressor may start streaming D now (k_wait_reduce)
-      __threadfence();
-      atomicExch(&ctl->red_gate, ctl->round + 1);
-    }
     if (rank == 0 && tid == 0) {
       red.out->grad_norm = sqrt(gg);
       red.out->f_mean = __ddiv_rn(fs, static_cast<double>(red.n_div));
@@ -958,6 +954,13 @@ __global__ void __launch_bounds__(CH_THREADS, 1) k_chol_panels(
   }
   __syncthreads();
   if (tid == 0) tl_mark(7, true);
+  // the compressor may start streaming D now (k_wait_reduce): released by a
+  // warp that is idle while panel 0 is factored (the fence is cumulative over
+  // the reduction's writes this thread observed through the barrier)
+  if (fused && rank == 0 && tid == CH_THREADS - 32) {
+    __threadfence();
+    atomicExch(&ctl->red_gate, ctl->round + 1);
+  }
   mark(0);
 
   // ---- factorisation.  Panel p - 1's owner pushes L_{p-1}'s slots 32..95
