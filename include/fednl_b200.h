@@ -66,6 +66,13 @@ extern "C" {
 #define FB_TOPK_PATH_STREAM 1  /* one CTA per client, one pass over D         */
 #define FB_TOPK_PATH_SPLIT 2   /* window / segmented pass / select kernels    */
 
+/* Storage of the design matrices for the margins-type passes (margins,
+ * gradient, line-search trials; no effect on results): AUTO keeps a compact
+ * int8 / float copy when every uploaded value converts to it exactly (e.g.
+ * binary LIBSVM features with the labels absorbed), F64 never does. */
+#define FB_BSTORE_AUTO 0
+#define FB_BSTORE_F64 1
+
 /* hessian_init (algorithms.py:37) */
 #define FB_INIT_LAMBDA_IDENTITY 0
 #define FB_INIT_ZERO 1
@@ -94,7 +101,7 @@ typedef struct fb_config {
   double ls_steps_table[61];
   double mu;              /* option a eigenvalue floor (effective_mu)   */
   int32_t topk_path;      /* FB_TOPK_PATH_*                             */
-  int32_t reserved;
+  int32_t b_store;        /* FB_BSTORE_*                                */
 } fb_config;
 
 /* Detail of the last failure raised by a round (mirrors the reference's
@@ -167,6 +174,10 @@ int fb_upload_shards(void* ctx, const double* const* bmats);
  * client's oracle and its lambda-identity H_c^0. */
 int fb_upload_shards_ex(void* ctx, const double* const* bmats, const int32_t* n_samples,
                         const double* lam);
+/* The copy of the design matrices the margins-type passes read after the
+ * last upload (fb_config.b_store): 0 = the fp64 matrices, 1 = float,
+ * 2 = int8 (diagnostic; results are identical). */
+int fb_bstore_kind(void* ctx);
 
 /* ---- run -------------------------------------------------------------- */
 /* Round-0 state: client/master Hessian estimates per hessian_init and, for

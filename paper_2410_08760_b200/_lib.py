@@ -26,6 +26,7 @@ FB_ERR_UNSUPPORTED = 7
 FB_ERR_EIGEN = 9
 
 TOPK_PATH_AUTO, TOPK_PATH_STREAM, TOPK_PATH_SPLIT = 0, 1, 2
+BSTORE_AUTO, BSTORE_F64 = 0, 1
 
 ALG_CODE = {"fednl": 0, "fednl-ls": 1, "fednl-pp": 2}
 INIT_CODE = {"lambda-identity": 0, "zero": 1, "exact": 2}
@@ -51,7 +52,7 @@ class FbConfig(C.Structure):
         ("ls_steps_table", C.c_double * 61),
         ("mu", C.c_double),
         ("topk_path", C.c_int32),
-        ("reserved", C.c_int32),
+        ("b_store", C.c_int32),
     ]
 
 
@@ -100,6 +101,7 @@ PROTOTYPES = {
     "fb_set_shard": (C.c_int, [_P, C.c_int32, C.c_int32, C.POINTER(C.c_uint8)]),
     "fb_upload_shards": (C.c_int, [_P, C.POINTER(_D)]),
     "fb_upload_shards_ex": (C.c_int, [_P, C.POINTER(_D), _I32, _D]),
+    "fb_bstore_kind": (C.c_int, [_P]),
     "fb_init_state": (C.c_int, [_P, _D]),
     "fb_run_rounds": (C.c_int, [_P, C.c_int32, C.c_int32, C.c_double, C.c_int32, _D, _D, _I32,
                                 _I32, _D, _I32]),

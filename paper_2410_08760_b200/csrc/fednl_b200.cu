@@ -23,6 +23,7 @@
 #include <string>
 #include <functional>
 #include <vector>
+#include <type_traits>
 
 #include "../../include/fednl_b200.h"
 #include "common.cuh"
@@ -104,6 +105,10 @@ struct Ctx {
   int32_t* ni_arr = nullptr;  // [n] samples per client (ragged shards; <= cfg.n_samples)
   double* lam_arr = nullptr;  // [n] lambda per client (ClientShard.lam)
   double *Bt = nullptr, *x = nullptr, *x_new = nullptr, *pvec = nullptr, *zbuf = nullptr;
+  // compact copy of Bt for the margins-type passes (oracle_kernels.cuh BPair):
+  // bkind 0 = none (fp64 Bt), 1 = float, 2 = int8; chosen after each upload
+  void* Bc = nullptr;
+  int bkind = 0;
   double *hcoef = nullptr, *gcoef = nullptr, *loss_part = nullptr, *grad = nullptr;
   double *gbar = nullptr, *f_cli = nullptr, *shift_cli = nullptr, *frob_part = nullptr;
   int32_t* flags = nullptr;
@@ -347,26 +352,116 @@ bool under_profiler() {
   return injected;
 }
 bool pdl_ok(const Ctx*) { return !under_profiler(); }
+// bit 0: every value is an integer in [-128, 127] (int8; -0.0 maps to 0,
+// see BPair); bit 1: double -> float -> double bit for bit (cleared by any
+// value that does not)
+__global__ void k_b_exact(const double* __restrict__ Bt, int64_t count, int32_t* __restrict__ flags) {
+  int ok = 3;
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < count;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const double v = __ldcs(Bt + i);
+    const uint64_t bits = static_cast<uint64_t>(__double_as_longlong(v));
+    const bool i8 = v >= -128.0 && v <= 127.0 && v == rint(v);
+    const bool f32 = static_cast<uint64_t>(__double_as_longlong(static_cast<double>(__double2float_rn(v)))) == bits;
+    ok &= (i8 ? 1 : 0) | (f32 ? 2 : 0);
+  }
+  ok = __reduce_and_sync(0xffffffffu, ok);
+  if ((threadIdx.x & 31) == 0 && ok != 3) atomicAnd(flags, ok);
+}
+template <class T>
+__global__ void k_b_convert(const double* __restrict__ Bt, int64_t count, T* __restrict__ Bc) {
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < count;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    Bc[i] = static_cast<T>(__ldcs(Bt + i));  // exact (k_b_exact)
+}
+// picks the compact copy after an upload (fb_config.b_store = AUTO); the
+// round graph is rebuilt when the choice changes
+int choose_bstore(Ctx* ctx) {
+  const int64_t count = static_cast<int64_t>(ctx->n) * ctx->d * ctx->ldj;
+  int kind = 0;
+  if (ctx->cfg.b_store == FB_BSTORE_AUTO) {
+    int32_t* flags = nullptr;
+    CK(cudaMalloc(&flags, sizeof(int32_t)));
+    const int32_t init = 3;
+    CK(cudaMemcpyAsync(flags, &init, sizeof init, cudaMemcpyHostToDevice, ctx->st));
+    k_b_exact<<<4 * ctx->num_sms, 256, 0, ctx->st>>>(ctx->Bt, count, flags);
+    int32_t got = 0;
+    CK(cudaMemcpyAsync(&got, flags, sizeof got, cudaMemcpyDeviceToHost, ctx->st));
+    CK(cudaStreamSynchronize(ctx->st));
+    cudaFree(flags);
+    kind = (got & 1) ? 2 : (got & 2) ? 1 : 0;
+  }
+  if (kind != ctx->bkind) {
+    if (ctx->Bc) {
+      for (auto it = ctx->allocs.begin(); it != ctx->allocs.end(); ++it)
+        if (it->first == ctx->Bc) {
+          cache_release(it->first, it->second);
+          ctx->allocs.erase(it);
+          break;
+        }
+      ctx->Bc = nullptr;
+    }
+    if (kind == 1) {
+      float* b = nullptr;
+      TRY(dalloc(ctx, &b, static_cast<size_t>(count)));
+      ctx->Bc = b;
+    } else if (kind == 2) {
+      int8_t* b = nullptr;
+      TRY(dalloc(ctx, &b, static_cast<size_t>(count)));
+      ctx->Bc = b;
+    }
+    ctx->bkind = kind;
+    if (ctx->gexec) {
+      cudaGraphExecDestroy(ctx->gexec);
+      ctx->gexec = nullptr;
+    }
+    if (ctx->graph) {
+      cudaGraphDestroy(ctx->graph);
+      ctx->graph = nullptr;
+    }
+  }
+  if (kind == 1)
+    k_b_convert<<<4 * ctx->num_sms, 256, 0, ctx->st>>>(ctx->Bt, count, static_cast<float*>(ctx->Bc));
+  else if (kind == 2)
+    k_b_convert<<<4 * ctx->num_sms, 256, 0, ctx->st>>>(ctx->Bt, count, static_cast<int8_t*>(ctx->Bc));
+  CKL();
+  CK(cudaStreamSynchronize(ctx->st));
+  return FB_OK;
+}
+// f(B) with B the margins-type passes' copy of Bt (typed)
+template <class F>
+void with_b(const Ctx* ctx, F f) {
+  if (ctx->bkind == 2) f(static_cast<const int8_t*>(ctx->Bc));
+  else if (ctx->bkind == 1) f(static_cast<const float*>(ctx->Bc));
+  else f(static_cast<const double*>(ctx->Bt));
+}
+
 int launch_margins(Ctx* ctx, cudaStream_t s, const double* x, const int32_t* clients, int n_active,
                    bool with_ctl = true) {
   if (n_active >= ctx->num_sms * 3 / 4 && mc_smem_bytes(ctx->d, ctx->ldj) <= MC_SMEM_MAX) {
     // enough clients to fill the GPU: one CTA streams each client's rows
     // two 512-thread CTAs per client (each half of its samples, two CTAs per
     // SM) when that halves the row batches a thread streams; else one
-    if (ctx->ldj / 2 > 64) {
-      k_margins_cpc<512, 2><<<2 * n_active, 512, mc_smem_bytes_nt(ctx->d, ctx->ldj, 2, 512), s>>>(
-          with_ctl ? ctx->ctl : nullptr, ctx->Bt, ctx->d, ctx->ni_arr, ctx->ldj, ctx->ldh, x, clients,
-          ctx->hcoef, ctx->gcoef, ctx->loss_part, ctx->nblk);
-    } else {
-      k_margins_cpc<MC_THREADS, 1><<<n_active, MC_THREADS, mc_smem_bytes(ctx->d, ctx->ldj), s>>>(
-          with_ctl ? ctx->ctl : nullptr, ctx->Bt, ctx->d, ctx->ni_arr, ctx->ldj, ctx->ldh, x, clients,
-          ctx->hcoef, ctx->gcoef, ctx->loss_part, ctx->nblk);
-    }
+    with_b(ctx, [&](auto B) {
+      using T = std::remove_cv_t<std::remove_pointer_t<decltype(B)>>;
+      if (ctx->ldj / 2 > 64) {
+        k_margins_cpc<512, 2, T><<<2 * n_active, 512, mc_smem_bytes_nt(ctx->d, ctx->ldj, 2, 512), s>>>(
+            with_ctl ? ctx->ctl : nullptr, B, ctx->d, ctx->ni_arr, ctx->ldj, ctx->ldh, x, clients,
+            ctx->hcoef, ctx->gcoef, ctx->loss_part, ctx->nblk);
+      } else {
+        k_margins_cpc<MC_THREADS, 1, T><<<n_active, MC_THREADS, mc_smem_bytes(ctx->d, ctx->ldj), s>>>(
+            with_ctl ? ctx->ctl : nullptr, B, ctx->d, ctx->ni_arr, ctx->ldj, ctx->ldh, x, clients,
+            ctx->hcoef, ctx->gcoef, ctx->loss_part, ctx->nblk);
+      }
+    });
   } else {
     dim3 grid(ctx->nblk, n_active);
-    k_margins<<<grid, MB_THREADS, ctx->d * sizeof(double), s>>>(
-        with_ctl ? ctx->ctl : nullptr, ctx->Bt, ctx->d, ctx->ni_arr, ctx->ldj, ctx->ldh, x, clients,
-        ctx->hcoef, ctx->gcoef, ctx->loss_part, ctx->nblk);
+    with_b(ctx, [&](auto B) {
+      using T = std::remove_cv_t<std::remove_pointer_t<decltype(B)>>;
+      k_margins<T><<<grid, MB_THREADS, ctx->d * sizeof(double), s>>>(
+          with_ctl ? ctx->ctl : nullptr, B, ctx->d, ctx->ni_arr, ctx->ldj, ctx->ldh, x, clients,
+          ctx->hcoef, ctx->gcoef, ctx->loss_part, ctx->nblk);
+    });
   }
   CKL();
   return FB_OK;
@@ -374,9 +469,12 @@ int launch_margins(Ctx* ctx, cudaStream_t s, const double* x, const int32_t* cli
 int launch_gradient(Ctx* ctx, cudaStream_t s, const double* x, const int32_t* clients,
                     int n_active, bool with_ctl = true) {
   dim3 grid((ctx->d + 7) / 8, n_active);
-  k_gradient<<<grid, 256, 0, s>>>(with_ctl ? ctx->ctl : nullptr, ctx->Bt, ctx->d, ctx->ni_arr,
-                                  ctx->ldj, ctx->ldh, x, ctx->lam_arr, clients, ctx->gcoef,
-                                  ctx->grad);
+  with_b(ctx, [&](auto B) {
+    using T = std::remove_cv_t<std::remove_pointer_t<decltype(B)>>;
+    k_gradient<T><<<grid, 256, 0, s>>>(with_ctl ? ctx->ctl : nullptr, B, ctx->d, ctx->ni_arr,
+                                       ctx->ldj, ctx->ldh, x, ctx->lam_arr, clients, ctx->gcoef,
+                                       ctx->grad);
+  });
   CKL();
   return FB_OK;
 }
@@ -742,9 +840,12 @@ int enqueue_fednl_round(Ctx* ctx) {
     CK(cudaGraphConditionalHandleCreate(&loop, cg, 0, cudaGraphCondAssignDefault));
     auto ls_batch = [&](cudaStream_t q) -> int {
       dim3 grid(ctx->ls_nblk, n_loc);
-      k_ls_trials<<<grid, MARGIN_THREADS, LS_BATCH * ctx->d * sizeof(double), q>>>(
-          ctx->ctl, ctx->Bt, ctx->d, ctx->ni_arr, ctx->ldj, loc, ctx->x, ctx->pvec, ctx->steps_table,
-          ctx->trial_x, ctx->ls_loss_part, ctx->ls_nblk);
+      with_b(ctx, [&](auto B) {
+        using T = std::remove_cv_t<std::remove_pointer_t<decltype(B)>>;
+        k_ls_trials<T><<<grid, MARGIN_THREADS, LS_BATCH * ctx->d * sizeof(double), q>>>(
+            ctx->ctl, B, ctx->d, ctx->ni_arr, ctx->ldj, loc, ctx->x, ctx->pvec, ctx->steps_table,
+            ctx->trial_x, ctx->ls_loss_part, ctx->ls_nblk);
+      });
       CKL();
       if (shd)  // the trials' per-client loss partials of every rank
         TRY(gather_clients(ctx, ctx->ls_loss_part, static_cast<size_t>(LS_BATCH) * ctx->ls_nblk,
@@ -1151,10 +1252,15 @@ int fb_create(const fb_config* cfg_in, void** out) {
                            static_cast<int>(HESS_WS_SMEM)));
   CKC(cudaFuncSetAttribute(k_topk_smem, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            static_cast<int>(TKS_SMEM)));
-  CKC(cudaFuncSetAttribute(k_margins_cpc<MC_THREADS, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+#define FB_MC_ATTR(T)                                                                                  \
+  CKC(cudaFuncSetAttribute(k_margins_cpc<MC_THREADS, 1, T>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                           static_cast<int>(MC_SMEM_MAX)));                                               \
+  CKC(cudaFuncSetAttribute(k_margins_cpc<512, 2, T>, cudaFuncAttributeMaxDynamicSharedMemorySize,        \
                            static_cast<int>(MC_SMEM_MAX)));
-  CKC(cudaFuncSetAttribute(k_margins_cpc<512, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           static_cast<int>(MC_SMEM_MAX)));
+  FB_MC_ATTR(double)
+  FB_MC_ATTR(float)
+  FB_MC_ATTR(int8_t)
+#undef FB_MC_ATTR
   CKC(cudaFuncSetAttribute(k_topk_stream, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            static_cast<int>(tkst_smem_bytes(TKST_MAXW))));
   CKC(cudaFuncSetAttribute(k_tks_pass<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1499,6 +1605,11 @@ int fb_set_shard(void* handle, int32_t world, int32_t rank, const uint8_t* nccl_
   return FB_OK;
 }
 
+int fb_bstore_kind(void* handle) {
+  const Ctx* ctx = static_cast<const Ctx*>(handle);
+  return ctx ? ctx->bkind : -1;
+}
+
 int fb_upload_shards(void* handle, const double* const* bmats) {
   return fb_upload_shards_ex(handle, bmats, nullptr, nullptr);
 }
@@ -1596,6 +1707,7 @@ int fb_upload_shards_ex(void* handle, const double* const* bmats, const int32_t*
     ctx->err = err;
     return FB_ERR_CUDA;
   }
+  TRY(choose_bstore(ctx));
   ctx->uploaded = true;
   return FB_OK;
 }

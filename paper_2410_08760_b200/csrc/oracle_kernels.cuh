@@ -18,6 +18,37 @@ namespace fb {
 
 constexpr int MARGIN_THREADS = 128;
 
+// The margins-type passes (margins, gradient, line-search trials) read B
+// from a compact copy when every value of the uploaded shards converts to a
+// narrower type and back (fb_upload_shards: binary / count features with the
+// labels absorbed, {-1, 0, 1}, as int8; float-exact values as float): each
+// value is widened to the same double before the same fma, so the results
+// are identical and the pass moves 8x (2x) fewer bytes.  (int8 drops the
+// sign of a -0.0 entry, which no sum can see: every accumulation starts at
+// +0.0, and +0.0 + -0.0 = +0.0.)  The Hessian's TMA tiles stay fp64.
+template <class T> struct BPair;  // two consecutive samples of one row
+template <> struct BPair<double> {
+  using V = double2;
+  __device__ static V ld(const double* p) { return __ldcs(reinterpret_cast<const double2*>(p)); }
+  __device__ static double x(V v) { return v.x; }
+  __device__ static double y(V v) { return v.y; }
+};
+template <> struct BPair<float> {
+  using V = float2;
+  __device__ static V ld(const float* p) { return __ldcs(reinterpret_cast<const float2*>(p)); }
+  __device__ static double x(V v) { return static_cast<double>(v.x); }
+  __device__ static double y(V v) { return static_cast<double>(v.y); }
+};
+template <> struct BPair<int8_t> {
+  using V = short;
+  __device__ static V ld(const int8_t* p) { return __ldcs(reinterpret_cast<const short*>(p)); }
+  __device__ static double x(V v) { return static_cast<double>(static_cast<int8_t>(v & 0xFF)); }
+  __device__ static double y(V v) { return static_cast<double>(static_cast<int8_t>(v >> 8)); }
+};
+template <class T> __device__ __forceinline__ double bload(const T* p) { return static_cast<double>(__ldg(p)); }
+// rows per batch of the streaming loops: the same bytes in flight per thread
+template <class T> __host__ __device__ constexpr int b_rows_per_batch() { return sizeof(T) >= 8 ? 8 : sizeof(T) >= 4 ? 16 : 32; }
+
 // stable logistic, oracle.py:64-71
 __device__ __forceinline__ double stable_sigmoid(double m) {
   if (m >= 0.0) return 1.0 / (1.0 + exp(-m));
@@ -39,8 +70,9 @@ __device__ __forceinline__ double softplus_neg(double m) {
 // grid (ceil(ldh / 64), n_active), block 256, dynamic smem d doubles.
 constexpr int MB_SAMPLES = 64;
 constexpr int MB_THREADS = 256;
+template <class T>
 __global__ void __launch_bounds__(MB_THREADS) k_margins(
-    const DevCtl* __restrict__ ctl, const double* __restrict__ Bt, int d,
+    const DevCtl* __restrict__ ctl, const T* __restrict__ Bt, int d,
     const int32_t* __restrict__ ni_arr, int ldj,
     int ldh, const double* __restrict__ x, const int32_t* __restrict__ clients,
     double* __restrict__ hcoef, double* __restrict__ gcoef, double* __restrict__ loss_part,
@@ -60,27 +92,27 @@ __global__ void __launch_bounds__(MB_THREADS) k_margins(
   const int j = blockIdx.x * MB_SAMPLES + 2 * lane;  // this lane's samples j, j + 1
   double m0 = 0.0, m1 = 0.0;
   if (j < ldj) {  // ldj even: j + 1 < ldj too (zero padded beyond ni)
-    const double2* col = reinterpret_cast<const double2*>(Bt + static_cast<int64_t>(c) * d * ldj + j);
-    const int64_t rs = ldj / 2;  // row stride in double2
+    using P = BPair<T>;
+    const T* col = Bt + static_cast<int64_t>(c) * d * ldj + j;
     double2 acc[4];
 #pragma unroll
     for (int u = 0; u < 4; ++u) acc[u] = make_double2(0.0, 0.0);
     int a0 = warp;
     for (; a0 + 56 < d; a0 += 64) {
-      double2 bv[8];
+      typename P::V bv[8];
 #pragma unroll
-      for (int u = 0; u < 8; ++u) bv[u] = __ldcs(col + static_cast<int64_t>(a0 + 8 * u) * rs);
+      for (int u = 0; u < 8; ++u) bv[u] = P::ld(col + static_cast<int64_t>(a0 + 8 * u) * ldj);
 #pragma unroll
       for (int u = 0; u < 8; ++u) {
         const double xa = xs[a0 + 8 * u];
-        acc[u & 3].x = fma(bv[u].x, xa, acc[u & 3].x);
-        acc[u & 3].y = fma(bv[u].y, xa, acc[u & 3].y);
+        acc[u & 3].x = fma(P::x(bv[u]), xa, acc[u & 3].x);
+        acc[u & 3].y = fma(P::y(bv[u]), xa, acc[u & 3].y);
       }
     }
     for (; a0 < d; a0 += 8) {
-      const double2 bv = __ldcs(col + static_cast<int64_t>(a0) * rs);
-      acc[0].x = fma(bv.x, xs[a0], acc[0].x);
-      acc[0].y = fma(bv.y, xs[a0], acc[0].y);
+      const typename P::V bv = P::ld(col + static_cast<int64_t>(a0) * ldj);
+      acc[0].x = fma(P::x(bv), xs[a0], acc[0].x);
+      acc[0].y = fma(P::y(bv), xs[a0], acc[0].y);
     }
     m0 = (acc[0].x + acc[1].x) + (acc[2].x + acc[3].x);
     m1 = (acc[0].y + acc[1].y) + (acc[2].y + acc[3].y);
@@ -148,9 +180,9 @@ __host__ __device__ constexpr size_t mc_smem_bytes(int d, int ldj) {
 constexpr size_t MC_SMEM_MAX = 96 * 1024;
 // NT threads per CTA, NS CTAs per client (client slot = blockIdx.x / NS,
 // sample pairs [part * SPS, (part + 1) * SPS) of SPS = mc_split_pairs).
-template <int NT, int NS>
+template <int NT, int NS, class T>
 __global__ void __launch_bounds__(NT, NS > 1 ? 2 : 1) k_margins_cpc(
-    const DevCtl* __restrict__ ctl, const double* __restrict__ Bt, int d,
+    const DevCtl* __restrict__ ctl, const T* __restrict__ Bt, int d,
     const int32_t* __restrict__ ni_arr, int ldj,
     int ldh, const double* __restrict__ x, const int32_t* __restrict__ clients,
     double* __restrict__ hcoef, double* __restrict__ gcoef, double* __restrict__ loss_part,
@@ -174,26 +206,29 @@ __global__ void __launch_bounds__(NT, NS > 1 ? 2 : 1) k_margins_cpc(
   const int SP = ldj / 2;
   const int sp_lo = part * SPS, sp_hi = min(SP, sp_lo + SPS);
   const int g = tid / SPc, sp_l = tid % SPc;
-  const double2* base = reinterpret_cast<const double2*>(Bt + static_cast<int64_t>(c) * d * ldj);
-  const int64_t rs = ldj / 2;  // row stride in double2
+  using P = BPair<T>;
+  constexpr int RB = b_rows_per_batch<T>();
+  const T* base = Bt + static_cast<int64_t>(c) * d * ldj;
   for (int sp0 = sp_lo; sp0 < sp_hi; sp0 += SPc) {
     // ---- partial margins of this chunk's sample pairs over row group g
     const int sp = sp0 + sp_l;
     if (g < G && sp < sp_hi) {
-      const double2* col = base + sp;
+      const T* col = base + 2 * sp;
       double2 acc[2] = {make_double2(0.0, 0.0), make_double2(0.0, 0.0)};
-      // 8 rows per batch, the last batch predicated (no one-row tail loop:
-      // every batch is one memory round trip)
-      for (int a = g; a < d; a += 8 * G) {
-        double2 bv[8];
+      // RB rows per batch (the same bytes in flight for every element type),
+      // the last batch predicated (no one-row tail loop: every batch is one
+      // memory round trip); within a batch the rows are added in the fp64
+      // path's order (two accumulators alternating over the rows)
+      for (int a = g; a < d; a += RB * G) {
+        typename P::V bv[RB];
 #pragma unroll
-        for (int u = 0; u < 8; ++u)  // rows past d re-read row d-1 (weight 0): no branch
-          bv[u] = __ldcs(col + static_cast<int64_t>(min(a + u * G, d - 1)) * rs);
+        for (int u = 0; u < RB; ++u)  // rows past d re-read row d-1 (weight 0): no branch
+          bv[u] = P::ld(col + static_cast<int64_t>(min(a + u * G, d - 1)) * ldj);
 #pragma unroll
-        for (int u = 0; u < 8; ++u) {
+        for (int u = 0; u < RB; ++u) {
           const double xa = a + u * G < d ? xs[a + u * G] : 0.0;
-          acc[u & 1].x = fma(bv[u].x, xa, acc[u & 1].x);
-          acc[u & 1].y = fma(bv[u].y, xa, acc[u & 1].y);
+          acc[u & 1].x = fma(P::x(bv[u]), xa, acc[u & 1].x);
+          acc[u & 1].y = fma(P::y(bv[u]), xa, acc[u & 1].y);
         }
       }
       part_m[g * 2 * SPc + 2 * sp_l] = acc[0].x + acc[1].x;
@@ -241,8 +276,9 @@ __global__ void __launch_bounds__(NT, NS > 1 ? 2 : 1) k_margins_cpc(
 
 // Local gradients g_c = B_c gcoef_c + lam x (oracle.py:108-121).
 // grid (ceil(d / 8), n_active), block 256: one warp per feature row.
+template <class T>
 __global__ void __launch_bounds__(256) k_gradient(
-    const DevCtl* __restrict__ ctl, const double* __restrict__ Bt, int d,
+    const DevCtl* __restrict__ ctl, const T* __restrict__ Bt, int d,
     const int32_t* __restrict__ ni_arr, int ldj, int ldh, const double* __restrict__ x,
     const double* __restrict__ lam_arr, const int32_t* __restrict__ clients,
     const double* __restrict__ gcoef, double* __restrict__ grad) {
@@ -253,15 +289,15 @@ __global__ void __launch_bounds__(256) k_gradient(
   const int a = blockIdx.x * 8 + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
   if (a >= d) return;
-  const double* row = Bt + (static_cast<int64_t>(c) * d + a) * ldj;
+  const T* row = Bt + (static_cast<int64_t>(c) * d + a) * ldj;
   const double* gc = gcoef + static_cast<int64_t>(c) * ldh;
   double s0 = 0.0, s1 = 0.0;
   int j = lane;
   for (; j + 32 < ni; j += 64) {
-    s0 = fma(__ldg(row + j), __ldg(gc + j), s0);
-    s1 = fma(__ldg(row + j + 32), __ldg(gc + j + 32), s1);
+    s0 = fma(bload(row + j), __ldg(gc + j), s0);
+    s1 = fma(bload(row + j + 32), __ldg(gc + j + 32), s1);
   }
-  if (j < ni) s0 = fma(__ldg(row + j), __ldg(gc + j), s0);
+  if (j < ni) s0 = fma(bload(row + j), __ldg(gc + j), s0);
   const double s = warp_sum(s0 + s1);
   if (lane == 0) grad[static_cast<int64_t>(c) * d + a] = __dadd_rn(s, __dmul_rn(lam, x[a]));
 }
@@ -273,8 +309,9 @@ __global__ void __launch_bounds__(256) k_gradient(
 // all-gathers it in place).  grid (ceil(ldj / 128), n_active), block 128,
 // dynamic smem S * d doubles.
 constexpr int LS_BATCH = 4;
+template <class T>
 __global__ void __launch_bounds__(MARGIN_THREADS) k_ls_trials(
-    const DevCtl* __restrict__ ctl, const double* __restrict__ Bt, int d,
+    const DevCtl* __restrict__ ctl, const T* __restrict__ Bt, int d,
     const int32_t* __restrict__ ni_arr, int ldj, const int32_t* __restrict__ clients,
     const double* __restrict__ x, const double* __restrict__ p,
     const double* __restrict__ steps_table, double* __restrict__ trial_x,
@@ -302,11 +339,11 @@ __global__ void __launch_bounds__(MARGIN_THREADS) k_ls_trials(
   if (j < ni) {
     // 16 independent loads in flight per batch; the last batch predicated
     // (features in increasing order as before: the same fma chain)
-    const double* col = Bt + static_cast<int64_t>(c) * d * ldj + j;
+    const T* col = Bt + static_cast<int64_t>(c) * d * ldj + j;
     for (int a = 0; a < d; a += 16) {
       double b[16];
 #pragma unroll
-      for (int u = 0; u < 16; ++u) b[u] = a + u < d ? __ldg(col + static_cast<int64_t>(a + u) * ldj) : 0.0;
+      for (int u = 0; u < 16; ++u) b[u] = a + u < d ? bload(col + static_cast<int64_t>(a + u) * ldj) : 0.0;
 #pragma unroll
       for (int u = 0; u < 16; ++u)
         if (a + u < d)

@@ -38,7 +38,8 @@ class RoundBatch:
     done: int
 
 
-def _fb_config(cfg: RunConfig, d: int, n: int, ni: int, topk_path: int = 0) -> _lib.FbConfig:
+def _fb_config(cfg: RunConfig, d: int, n: int, ni: int, topk_path: int = 0,
+               b_store: int = 0) -> _lib.FbConfig:
     w = packed_length(d)
     cfg.compressor.validate(w)
     c = _lib.FbConfig()
@@ -59,6 +60,7 @@ def _fb_config(cfg: RunConfig, d: int, n: int, ni: int, topk_path: int = 0) -> _
     for s in range(61):  # gamma ** s exactly as the host evaluates it (algorithms.py:305)
         c.ls_steps_table[s] = cfg.ls_gamma ** s
     c.topk_path = int(topk_path)
+    c.b_store = int(b_store)
     return c
 
 
@@ -69,15 +71,17 @@ class FedNLEngine:
     `lam` is every shard's lambda unless `upload` is given per-shard values
     (the master's lambda-identity init uses cfg.lam, algorithms.py:334-335);
     `topk_path` pins a TopK kernel variant (_lib.TOPK_PATH_*; results are
-    identical, tests use it to cover both)."""
+    identical, tests use it to cover both); `b_store` = _lib.BSTORE_F64 keeps
+    the margins-type passes on the fp64 design matrices (no compact copy;
+    results identical, tests compare both)."""
 
     def __init__(self, cfg: RunConfig, d: int, n_clients: int, n_samples: int, lam: float | None = None,
-                 topk_path: int = 0):
+                 topk_path: int = 0, b_store: int = 0):
         self.lib = _lib.load()
         self.cfg = cfg
         self.d, self.n, self.ni = d, n_clients, n_samples
         self.w = packed_length(d)
-        fc = _fb_config(cfg, d, n_clients, n_samples, topk_path)
+        fc = _fb_config(cfg, d, n_clients, n_samples, topk_path, b_store)
         self.default_lam = float(cfg.lam if lam is None else lam)
         self.alpha = fc.alpha
         h = C.c_void_p()

@@ -18,7 +18,9 @@ import pytest
 from cases_r2 import LS_FAIL, SIM_R2, case_r2, run_config
 from conftest import golden
 from oracle import fednl_oracle as O
-from paper_2410_08760_b200 import DivergenceError, LineSearchError, RunConfig, simulate
+from paper_2410_08760_b200 import (CompressorKind, CompressorSpec, DivergenceError, LineSearchError, RunConfig,
+                                   simulate)
+from paper_2410_08760_b200 import data as D
 from paper_2410_08760_b200.engine import FedNLEngine
 from test_gpu_parity import _envelope_close, _rows_close
 
@@ -182,5 +184,69 @@ def test_sharded_world1_deep_line_search_and_ragged_pp(name):
             out.append(([(r.grad_norm, r.f_value, r.bytes_up_cum, r.ls_steps) for r in rows], eng.get_x()))
         finally:
             eng.close()
+    assert out[0][0] == out[1][0]
+    assert np.array_equal(out[0][1], out[1][1])
+
+
+# ----------------------------------------------- compact design-matrix copy
+
+def _float_exact_shards(seed: int):
+    """Shards whose features are multiples of 1/8 in [-4, 4): float-exact,
+    not uint8-exact (the float copy)."""
+    from paper_2410_08760_b200 import ClientShard
+
+    rng = np.random.default_rng(seed)
+    out = []
+    for _ in range(6):
+        b = np.floor(rng.standard_normal((9, 40)) * 8) / 8
+        b[-1] = 1.0  # intercept
+        y = np.where(rng.random(40) < 0.5, 1.0, -1.0)
+        out.append(ClientShard(bmat=np.asfortranarray(b * y), lam=1e-3))
+    return out
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name", ["c0_binary", "ls_binary", "pp_binary", "float_exact", "gaussian"])
+def test_compact_design_matrix_bit_identical(name):
+    """The margins-type passes read an int8 / float copy of B when every value
+    converts exactly (binary features with the labels absorbed, float-exact
+    values): the rows, the
+    final iterate and the line-search counts are bit-identical to the fp64
+    matrices (fb_config.b_store = F64); Gaussian data keeps fp64."""
+    from paper_2410_08760_b200 import _lib
+
+    if name == "c0_binary":
+        shards = D.baseline_shards("c0")
+        cfg = RunConfig(compressor=CompressorSpec(CompressorKind.TOPK, k=2408), rounds=6, alpha=1.0, run_seed=1)
+        want = 2
+    elif name == "ls_binary":
+        shards = D.baseline_shards("c2")
+        cfg = RunConfig(algorithm="fednl-ls", compressor=CompressorSpec(CompressorKind.TOPLEK, k=69),
+                        rounds=8, run_seed=2)
+        want = 2
+    elif name == "pp_binary":
+        shards = D.baseline_shards("c3")
+        cfg = RunConfig(algorithm="fednl-pp", tau=12, compressor=CompressorSpec(CompressorKind.RANDK, k=301),
+                        rounds=8, run_seed=3)
+        want = 2
+    elif name == "float_exact":
+        shards = _float_exact_shards(5)
+        cfg = RunConfig(compressor=CompressorSpec(CompressorKind.TOPK, k=12), rounds=8, run_seed=5)
+        want = 1
+    else:
+        shards = D.gaussian_shards(33, 6, 70, 1e-3, seed=4)
+        cfg = RunConfig(compressor=CompressorSpec(CompressorKind.TOPK, k=60), rounds=6, run_seed=4)
+        want = 0
+    d, n, ni = shards[0].dim, len(shards), max(s.n_samples for s in shards)
+    out = []
+    for b_store in (_lib.BSTORE_AUTO, _lib.BSTORE_F64):
+        eng = FedNLEngine(cfg, d, n, ni, b_store=b_store)
+        try:
+            rows = simulate(cfg, shards, engine=eng)
+            kind = eng.lib.fb_bstore_kind(eng.h)
+            out.append(([(r.grad_norm, r.f_value, r.bytes_up_cum, r.ls_steps) for r in rows], eng.get_x(), kind))
+        finally:
+            eng.close()
+    assert out[0][2] == want and out[1][2] == 0
     assert out[0][0] == out[1][0]
     assert np.array_equal(out[0][1], out[1][1])
