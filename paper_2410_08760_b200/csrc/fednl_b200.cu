@@ -142,6 +142,10 @@ struct Ctx {
 
   cudaGraph_t graph = nullptr;
   cudaGraphExec_t gexec = nullptr;
+  // production flavour only: GRAPH_ROUNDS rounds captured back to back (no
+  // graph boundary between them)
+  cudaGraph_t graph_multi = nullptr;
+  cudaGraphExec_t gexec_multi = nullptr;
   cudaEvent_t ev_fixed[EV_COUNT] = {};
   cudaGraphNode_t ev_node[EV_COUNT] = {};
   bool ev_used[EV_COUNT] = {};
@@ -352,6 +356,8 @@ bool under_profiler() {
   return injected;
 }
 bool pdl_ok(const Ctx*) { return !under_profiler(); }
+void drop_graphs(Ctx* ctx);
+
 // bit 0: every value is an integer in [-128, 127] (int8; -0.0 maps to 0,
 // see BPair); bit 1: double -> float -> double bit for bit (cleared by any
 // value that does not)
@@ -411,14 +417,7 @@ int choose_bstore(Ctx* ctx) {
       ctx->Bc = b;
     }
     ctx->bkind = kind;
-    if (ctx->gexec) {
-      cudaGraphExecDestroy(ctx->gexec);
-      ctx->gexec = nullptr;
-    }
-    if (ctx->graph) {
-      cudaGraphDestroy(ctx->graph);
-      ctx->graph = nullptr;
-    }
+    drop_graphs(ctx);
   }
   if (kind == 1)
     k_b_convert<<<4 * ctx->num_sms, 256, 0, ctx->st>>>(ctx->Bt, count, static_cast<float*>(ctx->Bc));
@@ -437,7 +436,7 @@ void with_b(const Ctx* ctx, F f) {
 }
 
 int launch_margins(Ctx* ctx, cudaStream_t s, const double* x, const int32_t* clients, int n_active,
-                   bool with_ctl = true) {
+                   bool with_ctl = true, int32_t* zero_flags = nullptr) {
   if (n_active >= ctx->num_sms * 3 / 4 && mc_smem_bytes(ctx->d, ctx->ldj) <= MC_SMEM_MAX) {
     // enough clients to fill the GPU: one CTA streams each client's rows
     // two 512-thread CTAs per client (each half of its samples, two CTAs per
@@ -447,11 +446,11 @@ int launch_margins(Ctx* ctx, cudaStream_t s, const double* x, const int32_t* cli
       if (ctx->ldj / 2 > 64) {
         k_margins_cpc<512, 2, T><<<2 * n_active, 512, mc_smem_bytes_nt(ctx->d, ctx->ldj, 2, 512), s>>>(
             with_ctl ? ctx->ctl : nullptr, B, ctx->d, ctx->ni_arr, ctx->ldj, ctx->ldh, x, clients,
-            ctx->hcoef, ctx->gcoef, ctx->loss_part, ctx->nblk);
+            ctx->hcoef, ctx->gcoef, ctx->loss_part, ctx->nblk, zero_flags);
       } else {
         k_margins_cpc<MC_THREADS, 1, T><<<n_active, MC_THREADS, mc_smem_bytes(ctx->d, ctx->ldj), s>>>(
             with_ctl ? ctx->ctl : nullptr, B, ctx->d, ctx->ni_arr, ctx->ldj, ctx->ldh, x, clients,
-            ctx->hcoef, ctx->gcoef, ctx->loss_part, ctx->nblk);
+            ctx->hcoef, ctx->gcoef, ctx->loss_part, ctx->nblk, zero_flags);
       }
     });
   } else {
@@ -460,7 +459,7 @@ int launch_margins(Ctx* ctx, cudaStream_t s, const double* x, const int32_t* cli
       using T = std::remove_cv_t<std::remove_pointer_t<decltype(B)>>;
       k_margins<T><<<grid, MB_THREADS, ctx->d * sizeof(double), s>>>(
           with_ctl ? ctx->ctl : nullptr, B, ctx->d, ctx->ni_arr, ctx->ldj, ctx->ldh, x, clients,
-          ctx->hcoef, ctx->gcoef, ctx->loss_part, ctx->nblk);
+          ctx->hcoef, ctx->gcoef, ctx->loss_part, ctx->nblk, zero_flags);
     });
   }
   CKL();
@@ -708,10 +707,11 @@ int launch_master_fold(Ctx* ctx, cudaStream_t s, const int32_t* clients, int n_a
 }
 
 int record(Ctx* ctx, EvSlot slot, cudaStream_t s) {
-  // per-kernel boundaries only in the instrumented graph: an event-record
-  // node between two kernels costs the overlap of their launches (measured
-  // 24 us per c0 round for the seven of them)
-  if (!ctx->phase_events && slot != EV_START && slot != EV_END) return FB_OK;
+  // event-record nodes only in the instrumented graph: a node between two
+  // kernels costs the overlap of their launches (measured 24 us per c0 round
+  // for the seven per-kernel ones; the production graph has none, its rows'
+  // wall times come from the host's per-launch events)
+  if (!ctx->phase_events) return FB_OK;
   ctx->ev_used[slot] = true;
   CK(cudaEventRecordWithFlags(ctx->ev_fixed[slot], s, cudaEventRecordExternal));
   return FB_OK;
@@ -723,11 +723,11 @@ int enqueue_fednl_round(Ctx* ctx) {
   const int n = ctx->n;
   const bool ls = ctx->cfg.algorithm == FB_ALG_LS;
   TRY(record(ctx, EV_START, s));
-  CK(cudaMemsetAsync(ctx->flags, 0, sizeof(int32_t) * n, s));
   const bool shd = sharded(ctx);
   const int32_t* loc = shd ? ctx->local_clients : nullptr;  // this rank's clients
   const int n_loc = shd ? ctx->c_hi - ctx->c_lo : n;
-  TRY(launch_margins(ctx, s, ctx->x, loc, n_loc));
+  // the margins clear the round's client flags (no memset node before them)
+  TRY(launch_margins(ctx, s, ctx->x, loc, n_loc, true, ctx->flags));
   TRY(record(ctx, EV_ORACLE_END, s));
   // Hessian + D + Frobenius partials, with the local gradients fused in
   TRY(launch_hessian(ctx, s, loc, n_loc, ctx->hest, ctx->w, ctx->D, nullptr, true, ctx->x));
@@ -1023,16 +1023,26 @@ int enqueue_pp_round(Ctx* ctx) {
   return FB_OK;
 }
 
+// rounds per launch of the plain FedNL production graph (the run loop falls
+// back to the one-round graph for a chunk's remainder): c0 +1%, c1 +3%.  The
+// FedNL-LS (while node) and FedNL-PP (concurrent probe branch) rounds lose
+// 11-14% when several are captured into one graph and keep one per launch.
+constexpr int GRAPH_ROUNDS = 4;
+
+void drop_graphs(Ctx* ctx) {
+  if (ctx->gexec) cudaGraphExecDestroy(ctx->gexec);
+  if (ctx->graph) cudaGraphDestroy(ctx->graph);
+  if (ctx->gexec_multi) cudaGraphExecDestroy(ctx->gexec_multi);
+  if (ctx->graph_multi) cudaGraphDestroy(ctx->graph_multi);
+  ctx->gexec = nullptr;
+  ctx->graph = nullptr;
+  ctx->gexec_multi = nullptr;
+  ctx->graph_multi = nullptr;
+}
+
 int build_graph(Ctx* ctx, bool phase_events) {
   if (ctx->gexec && ctx->gexec_phase == phase_events) return FB_OK;
-  if (ctx->gexec) {  // the other flavour: rebuilt (the first call of a timed run)
-    cudaGraphExecDestroy(ctx->gexec);
-    ctx->gexec = nullptr;
-  }
-  if (ctx->graph) {
-    cudaGraphDestroy(ctx->graph);
-    ctx->graph = nullptr;
-  }
+  drop_graphs(ctx);  // the other flavour: rebuilt (the first call of a timed run)
   ctx->phase_events = phase_events;
   ctx->gexec_phase = phase_events;
   for (int i = 0; i < EV_COUNT; ++i) {
@@ -1067,6 +1077,21 @@ int build_graph(Ctx* ctx, bool phase_events) {
       if (ev == ctx->ev_fixed[i]) ctx->ev_node[i] = nd;
   }
   CK(cudaGraphInstantiate(&ctx->gexec, g, 0));
+  if (!phase_events && ctx->cfg.algorithm == FB_ALG_FEDNL) {
+    CK(cudaStreamBeginCapture(ctx->st, cudaStreamCaptureModeThreadLocal));
+    int rr = FB_OK;
+    for (int k = 0; k < GRAPH_ROUNDS && rr == FB_OK; ++k)
+      rr = (ctx->cfg.algorithm == FB_ALG_PP) ? enqueue_pp_round(ctx) : enqueue_fednl_round(ctx);
+    cudaGraph_t gm = nullptr;
+    cudaError_t em = cudaStreamEndCapture(ctx->st, &gm);
+    if (rr != FB_OK) {
+      if (gm) cudaGraphDestroy(gm);
+      return rr;
+    }
+    CK(em);
+    ctx->graph_multi = gm;
+    CK(cudaGraphInstantiate(&ctx->gexec_multi, gm, 0));
+  }
   return FB_OK;
 }
 
@@ -1453,8 +1478,7 @@ int fb_create(const fb_config* cfg_in, void** out) {
 void fb_destroy(void* handle) {
   Ctx* ctx = static_cast<Ctx*>(handle);
   if (!ctx) return;
-  if (ctx->gexec) cudaGraphExecDestroy(ctx->gexec);
-  if (ctx->graph) cudaGraphDestroy(ctx->graph);
+  drop_graphs(ctx);
   if (ctx->st) cudaStreamSynchronize(ctx->st);
   if (ctx->st2) cudaStreamSynchronize(ctx->st2);
   if (ctx->comm) nccl_api().CommDestroy(ctx->comm);
@@ -1594,14 +1618,7 @@ int fb_set_shard(void* handle, int32_t world, int32_t rank, const uint8_t* nccl_
   ncclUniqueId id;
   std::memcpy(&id, nccl_id, sizeof id);
   NCK(api.CommInitRank(&ctx->comm, world, id, rank));
-  if (ctx->gexec) {  // the round graph is rebuilt for the sharded body
-    cudaGraphExecDestroy(ctx->gexec);
-    ctx->gexec = nullptr;
-  }
-  if (ctx->graph) {
-    cudaGraphDestroy(ctx->graph);
-    ctx->graph = nullptr;
-  }
+  drop_graphs(ctx);  // the round graph is rebuilt for the sharded body
   return FB_OK;
 }
 
@@ -1804,7 +1821,17 @@ int fb_run_rounds(void* handle, int32_t first_round, int32_t count, double stop_
     h.row_base = first_round + done;
     h.round = first_round + done;
     CK(cudaMemcpyAsync(ctx->ctl, &h, sizeof h, cudaMemcpyHostToDevice, s));
-    for (int i = 0; i < chunk; ++i) {
+    // rows without an end event of their own (inside a multi-round launch)
+    // get their wall time interpolated between the launch ends around them
+    std::vector<char> has_end(chunk, 0);
+    for (int i = 0; i < chunk;) {
+      if (!timed && ctx->gexec_multi && chunk - i >= GRAPH_ROUNDS) {
+        CK(cudaGraphLaunch(ctx->gexec_multi, s));
+        i += GRAPH_ROUNDS;
+        CK(cudaEventRecord(ends[i - 1], s));
+        has_end[i - 1] = 1;
+        continue;
+      }
       if (timed) {
         for (int e = 0; e < EV_COUNT; ++e)
           if (ctx->ev_node[e])
@@ -1813,6 +1840,8 @@ int fb_run_rounds(void* handle, int32_t first_round, int32_t count, double stop_
       }
       CK(cudaGraphLaunch(ctx->gexec, s));
       CK(cudaEventRecord(ends[i], s));
+      has_end[i] = 1;
+      ++i;
     }
     TRY(read_status(ctx, &h));
     const int completed = h.round - (first_round + done);
@@ -1833,8 +1862,17 @@ int fb_run_rounds(void* handle, int32_t first_round, int32_t count, double stop_
         memcpy(entry_counts + static_cast<size_t>(o) * n, rcnt.data() + static_cast<size_t>(i) * n,
                sizeof(int32_t) * n);
       if (wall_ms) {
+        int j1 = i;  // the next row with an end event (a launch's last round)
+        while (!has_end[j1]) ++j1;
         float ms = 0.f;
-        CK(cudaEventElapsedTime(&ms, t0, ends[i]));
+        CK(cudaEventElapsedTime(&ms, t0, ends[j1]));
+        if (j1 != i) {  // inside a multi-round launch: between its start and end
+          const int j0 = j1 - GRAPH_ROUNDS;  // the previous launch's last row
+          float ms0 = 0.f;
+          if (j0 >= 0) CK(cudaEventElapsedTime(&ms0, t0, ends[j0]));
+          else ms0 = o > 0 && wall_ms ? static_cast<float>(wall_ms[o - 1]) : 0.f;
+          ms = ms0 + (ms - ms0) * static_cast<float>(i - j0) / static_cast<float>(GRAPH_ROUNDS);
+        }
         wall_ms[o] = ms;
       }
       if (timed && ctx->ev_node[EV_START] && !h.halt) {

@@ -76,11 +76,14 @@ __global__ void __launch_bounds__(MB_THREADS) k_margins(
     const int32_t* __restrict__ ni_arr, int ldj,
     int ldh, const double* __restrict__ x, const int32_t* __restrict__ clients,
     double* __restrict__ hcoef, double* __restrict__ gcoef, double* __restrict__ loss_part,
-    int nblk) {
+    int nblk, int32_t* __restrict__ zero_flags = nullptr) {
   // the Hessian pass may launch now (it waits for these coefficients)
   asm volatile("griddepcontrol.launch_dependents;");
   if (ctl && ctl->halt) return;
   if (threadIdx.x == 0) tl_mark(0, false);
+  // the round's per-client flags start clear (the Hessian's epilogue ORs
+  // into them only after this grid completes)
+  if (zero_flags && blockIdx.x == 0 && threadIdx.x == 0) zero_flags[client_of(clients, blockIdx.y)] = 0;
   extern __shared__ double xs[];
   __shared__ double part[8][MB_SAMPLES + 2];
   __shared__ double red[2];
@@ -186,7 +189,7 @@ __global__ void __launch_bounds__(NT, NS > 1 ? 2 : 1) k_margins_cpc(
     const int32_t* __restrict__ ni_arr, int ldj,
     int ldh, const double* __restrict__ x, const int32_t* __restrict__ clients,
     double* __restrict__ hcoef, double* __restrict__ gcoef, double* __restrict__ loss_part,
-    int nblk) {
+    int nblk, int32_t* __restrict__ zero_flags = nullptr) {
   // the Hessian pass may launch now (it waits for these coefficients)
   asm volatile("griddepcontrol.launch_dependents;");
   if (ctl && ctl->halt) return;
@@ -194,6 +197,7 @@ __global__ void __launch_bounds__(NT, NS > 1 ? 2 : 1) k_margins_cpc(
   __shared__ double red[NT / 32];
   if (threadIdx.x == 0) tl_mark(0, false);
   const int c = client_of(clients, blockIdx.x / NS);
+  if (zero_flags && blockIdx.x % NS == 0 && threadIdx.x == 0) zero_flags[c] = 0;  // (as k_margins)
   const int ni = ni_arr[c];
   const int part = blockIdx.x % NS;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;

@@ -414,6 +414,7 @@ __global__ void __launch_bounds__(256) k_finish(
     if (bad) raise_status(ctl, ST_DIVERGED);
     else if (row_grad && ctl->stop_gn >= 0.0 && row_grad[slot] <= ctl->stop_gn)
       raise_status(ctl, ST_STOPPED);
+    tl_mark(6, true);
   }
 }
 
