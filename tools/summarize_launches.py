@@ -6,7 +6,7 @@ import csv
 import sys
 
 
-def main(path: str, skip_prefix: tuple = ("k_transpose_shard", "fb::k_init", "fb::k_peak")) -> None:
+def main(path: str, skip_prefix: tuple = ("k_transpose_shard", "fb::k_init", "fb::k_peak", "<unnamed>::k_b_")) -> None:
     hdr, agg = None, collections.OrderedDict()
     for r in csv.reader(open(path)):
         if "Kernel Name" in r:
