@@ -73,6 +73,11 @@ extern "C" {
 #define FB_BSTORE_AUTO 0
 #define FB_BSTORE_F64 1
 
+/* Largest dimension of this build (every dataset of the paper and every
+ * BASELINE config has d <= 1024; above that the solve runs the
+ * global-memory blocked Cholesky, solve_big.cuh). */
+#define FB_MAX_D 4096
+
 /* hessian_init (algorithms.py:37) */
 #define FB_INIT_LAMBDA_IDENTITY 0
 #define FB_INIT_ZERO 1

@@ -1896,9 +1896,15 @@ __host__ __device__ constexpr size_t rk_pool_words(int k, int64_t w) {
 __host__ __device__ constexpr bool rk_js_smem(int k, int wb, int64_t w) {
   return (rk_pool_words(k, w) + static_cast<size_t>(k) + static_cast<size_t>(wb)) * 4 <= RK_SMEM_MAX;
 }
+// the bitmap in shared memory when it fits there too (d <= 1024: always),
+// else the client's global bitmap row is worked on directly
+__host__ __device__ constexpr bool rk_bm_smem(int k, int wb, int64_t w) {
+  return (rk_pool_words(k, w) + (rk_js_smem(k, wb, w) ? static_cast<size_t>(k) : 0) +
+          static_cast<size_t>(wb)) * 4 <= RK_SMEM_MAX;
+}
 __host__ __device__ constexpr size_t rk_smem_bytes(int k, int wb, int64_t w) {
   return (rk_pool_words(k, w) + (rk_js_smem(k, wb, w) ? static_cast<size_t>(k) : 0) +
-          static_cast<size_t>(wb)) * 4;
+          (rk_bm_smem(k, wb, w) ? static_cast<size_t>(wb) : 0)) * 4;
 }
 __device__ __forceinline__ int rk_slot(int32_t* keys, int32_t key) {
   uint32_t h = (static_cast<uint32_t>(key) * 2654435761u) & (RK_TABLE - 1);
@@ -1919,7 +1925,8 @@ __global__ void __launch_bounds__(RK_THREADS) k_randk(
   const bool js_smem = rk_js_smem(k, wb, w);
   const int c = client_of(clients, blockIdx.x);
   int32_t* js = js_smem ? tab + pw : gjs + static_cast<int64_t>(c) * k;                // [k]
-  uint32_t* bm = reinterpret_cast<uint32_t*>(tab + pw + (js_smem ? k : 0));            // [wb]
+  uint32_t* bm = rk_bm_smem(k, wb, w) ? reinterpret_cast<uint32_t*>(tab + pw + (js_smem ? k : 0))  // [wb]
+                                       : bitmap + static_cast<int64_t>(client_of(clients, blockIdx.x)) * wb;
   const bool global_pool = rk_global_pool(k, w);
   __shared__ int ws[64];
   __shared__ int s_reject;

@@ -34,6 +34,7 @@
 #include "oracle_kernels.cuh"
 #include "round_kernels.cuh"
 #include "solve_kernels.cuh"
+#include "solve_big.cuh"
 
 using namespace fb;
 
@@ -64,6 +65,7 @@ struct Ctx {
   double alpha_n = 0.0, rand_scale = 1.0;
   int solve_cs = 1, solve_nb = 32;
   bool solve_panels = false;  // k_chol_panels (d <= CP_MAX_D) instead of k_chol_solve
+  bool solve_big = false;     // d > CH_MAX_D: the global-memory blocked solve (solve_big.cuh)
   int cp_kp = 1, cp_cs = 1;
   bool topk_stream = false;  // one-pass sampled-window TopK (else the shared-memory radix)
   bool topk_split = false;   // ... as window / segmented pass / select kernels
@@ -628,6 +630,32 @@ int launch_solve(Ctx* ctx, cudaStream_t s, const double* hpk, const double* shif
                  const double* rhs, const double* x, double* z, double* x_out, int mode,
                  int ignore_halt, long long* dbg = nullptr, cudaEvent_t launched = nullptr,
                  bool force_old = false, bool after_reduce = false, const CpRed* red = nullptr) {
+  if (ctx->solve_big) {
+    // d > CH_MAX_D: setup, then per 64-column panel the block factor + row
+    // solve and the trailing update, then the back substitution
+    const int d = ctx->d;
+    k_big_setup<<<std::min(d + 1, 4 * ctx->num_sms), BIG_THREADS, 0, s>>>(ctx->ctl, d, hpk, shift_ptr, rhs,
+                                                                          ctx->M);
+    CKL();
+    if (launched) CK(cudaEventRecord(launched, s));
+    for (int p0 = 0; p0 < d; p0 += BIG_NB) {
+      const int p1 = std::min(d, p0 + BIG_NB);
+      const int rows = d + 1 - p1;
+      const int pblk = std::max(1, std::min(ctx->num_sms, (rows + BIG_THREADS - 1) / BIG_THREADS));
+      k_big_panel<<<pblk, BIG_THREADS, BIG_NB * BIG_LDS * sizeof(double), s>>>(ctx->ctl, d, p0, ctx->M);
+      CKL();
+      if (p1 < d) {
+        const int T = (rows + BIG_TILE - 1) / BIG_TILE;
+        k_big_update<<<T * (T + 1) / 2, BIG_THREADS, 2 * BIG_TILE * BIG_LDS * sizeof(double), s>>>(
+            ctx->ctl, d, p0, ctx->M);
+        CKL();
+      }
+    }
+    k_big_back<<<1, BIG_BACK_THREADS, (static_cast<size_t>(d) + BIG_NB) * sizeof(double), s>>>(
+        ctx->ctl, d, ctx->M, x, z, x_out, mode, ignore_halt);
+    CKL();
+    return FB_OK;
+  }
   const bool panels = ctx->solve_panels && !force_old;
   const int cs = panels ? ctx->cp_cs : ctx->solve_cs;
   cudaLaunchConfig_t lc{};
@@ -1170,7 +1198,7 @@ int fb_create(const fb_config* cfg_in, void** out) {
   *out = nullptr;
   const fb_config& c = *cfg_in;
   if (c.d < 1 || c.n_clients < 1 || c.n_samples < 1) return invalid(nullptr, "bad shape");
-  if (c.d > 1024) return invalid(nullptr, "d > 1024 is outside this build's envelope");
+  if (c.d > FB_MAX_D) return invalid(nullptr, "d > 4096 is outside this build's envelope");
   if (c.n_clients >= (1 << 24)) return invalid(nullptr, "too many clients");
   const int64_t w = packed_len(c.d);
   if (c.kind < FB_KIND_IDENTITY || c.kind > FB_KIND_NATURAL) return invalid(nullptr, "bad kind");
@@ -1182,7 +1210,7 @@ int fb_create(const fb_config* cfg_in, void** out) {
   if (c.topk_path < FB_TOPK_PATH_AUTO || c.topk_path > FB_TOPK_PATH_SPLIT)
     return invalid(nullptr, "bad topk_path");
   if (c.kind == FB_KIND_RANDK && rk_smem_bytes(c.k, static_cast<int>((w + 31) / 32), w) > RK_SMEM_MAX)
-    return invalid(nullptr, "randk bitmap does not fit shared memory (d > 1024)");
+    return invalid(nullptr, "randk scratch does not fit shared memory");
 
   Ctx* ctx = new Ctx();
   ctx->cfg = c;
@@ -1226,7 +1254,11 @@ int fb_create(const fb_config* cfg_in, void** out) {
     ctx->solve_panels = npan >= 4 && c.d <= CP_MAX_D && ctx->cp_cs <= CH_MAX_CLUSTER &&
                         static_cast<size_t>(ctx->cp_kp) * cp_panel_bytes(c.d) <= CP_DYN_SMEM_MAX;
   }
-  ctx->solve_smem = ctx->solve_nb == 32 ? solve_panel_bytes<32>(c.d) : solve_panel_bytes<16>(c.d);
+  // d > CH_MAX_D: the global-memory blocked solve (solve_big.cuh)
+  ctx->solve_big = c.d > CH_MAX_D;
+  if (ctx->solve_big) ctx->solve_panels = false;
+  ctx->solve_smem = ctx->solve_big ? 0
+                    : (ctx->solve_nb == 32 ? solve_panel_bytes<32>(c.d) : solve_panel_bytes<16>(c.d));
   int rc = FB_OK;
   auto fail = [&](int code) {
     rc = code;
@@ -1286,6 +1318,16 @@ int fb_create(const fb_config* cfg_in, void** out) {
   FB_MC_ATTR(float)
   FB_MC_ATTR(int8_t)
 #undef FB_MC_ATTR
+  CKC(cudaFuncSetAttribute(k_big_update, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           static_cast<int>(2 * BIG_TILE * BIG_LDS * sizeof(double))));
+  CKC(cudaFuncSetAttribute(k_big_back, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           static_cast<int>((FB_MAX_D + BIG_NB) * sizeof(double))));
+  CKC(cudaFuncSetAttribute(k_ls_trials<double>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           static_cast<int>(LS_BATCH * FB_MAX_D * sizeof(double))));
+  CKC(cudaFuncSetAttribute(k_ls_trials<float>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           static_cast<int>(LS_BATCH * FB_MAX_D * sizeof(double))));
+  CKC(cudaFuncSetAttribute(k_ls_trials<int8_t>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           static_cast<int>(LS_BATCH * FB_MAX_D * sizeof(double))));
   CKC(cudaFuncSetAttribute(k_topk_stream, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            static_cast<int>(tkst_smem_bytes(TKST_MAXW))));
   CKC(cudaFuncSetAttribute(k_tks_pass<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1320,7 +1362,8 @@ int fb_create(const fb_config* cfg_in, void** out) {
   ctx->topk_stream = stream_topk;
   // the stream as many small CTAs (about two waves of 8 per SM) + a select
   // kernel when n * w is large (c4); topk_path pins either variant (tests)
-  ctx->topk_split = stream_topk && (c.topk_path == FB_TOPK_PATH_AUTO
+  // (the split path's selection keeps a bitmap row in shared memory: w <~ 1.7M)
+  ctx->topk_split = stream_topk && tkp_smem_bytes(w) <= 220 * 1024 && (c.topk_path == FB_TOPK_PATH_AUTO
                                         ? static_cast<int64_t>(w) * n >= (int64_t{1} << 26)
                                         : c.topk_path == FB_TOPK_PATH_SPLIT);
   size_t cand_slots = stream_topk ? static_cast<size_t>(n) * TKST_CAP : 1;

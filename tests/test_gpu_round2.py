@@ -250,3 +250,54 @@ def test_compact_design_matrix_bit_identical(name):
     assert out[0][2] == want and out[1][2] == 0
     assert out[0][0] == out[1][0]
     assert np.array_equal(out[0][1], out[1][1])
+
+
+# ------------------------------------------------------------ d > 1024
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("d", [1025, 1100, 1600])
+def test_large_d_solve_and_not_pd_pivot(d):
+    """The global-memory blocked solve (d > 1024, solve_big.cuh) against
+    numpy at 1e-10, and the first failing pivot of an indefinite system is the
+    reference's (index and value)."""
+    from paper_2410_08760_b200 import NotPositiveDefiniteError, leaf
+
+    rng = np.random.default_rng(d)
+    a = rng.standard_normal((d, d))
+    spd = a @ a.T / d + np.eye(d)
+    rows, cols, _ = O.tri(d)
+    b = rng.standard_normal(d)
+    z = leaf.shifted_solve(spd[rows, cols], d, 0.25, b)
+    want = np.linalg.solve(spd + 0.25 * np.eye(d), b)
+    assert np.linalg.norm(z - want) <= 1e-10 * np.linalg.norm(want)
+    bad = spd.copy()
+    piv = d - 37
+    bad[piv, piv] = -5.0  # the first non-positive pivot of the column loop
+    with pytest.raises(NotPositiveDefiniteError) as exc:
+        leaf.shifted_solve(bad[rows, cols], d, 0.0, b)
+    L_ok = np.linalg.cholesky(bad[:piv, :piv])
+    expect = bad[piv, piv] - np.dot(np.linalg.solve(L_ok, bad[:piv, piv]), np.linalg.solve(L_ok, bad[:piv, piv]))
+    assert exc.value.pivot_index == piv
+    assert exc.value.pivot_value == pytest.approx(expect, rel=1e-9)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("d,kind,k,alg", [(1100, "topk", 8800, "fednl"), (2000, "randk", 2000, "fednl"),
+                                          (1100, "toplek", 1100, "fednl-ls"), (1100, "randseqk", 2200, "fednl-pp")])
+def test_large_d_rounds_match_oracle(d, kind, k, alg):
+    """d > 1024 (the global-memory solve; at d = 2000 the RandK bitmap in
+    global memory): FedNL / FedNL-LS / FedNL-PP rows against the oracle port
+    at 1e-10 with exact byte counters."""
+    n, ni = 4, 160
+    shards = D.gaussian_shards(d, n, ni, 1e-3, seed=11)
+    kw = dict(compressor=CompressorSpec(CompressorKind(kind), k=k), rounds=4, run_seed=11, algorithm=alg)
+    if alg == "fednl-pp":
+        kw["tau"] = 2
+    cfg = RunConfig(**kw)
+    rows = simulate(cfg, shards)
+    ref = O.simulate(O.OracleConfig.from_run_config(cfg), [s.bmat for s in shards], lam=1e-3)
+    assert len(rows) == len(ref)
+    g0 = ref[0].grad_norm
+    for r, o in zip(rows, ref):
+        assert (r.bytes_up_cum, r.bytes_down_cum, r.ls_steps) == (o.bytes_up_cum, o.bytes_down_cum, o.ls_steps)
+        assert abs(r.grad_norm - o.grad_norm) <= 1e-10 * max(o.grad_norm, 1e-6 * g0), (r, o)
