@@ -663,6 +663,33 @@ def gen_csv():
     return out
 
 
+FULL_CASES = {  # the BASELINE configs' full round counts
+    "c0_full": (("baseline", "c0"), dict(rounds=100)),
+    "c1_full": (("baseline", "c1"), dict(rounds=200)),
+    "c2_full": (("baseline", "c2"), dict(rounds=200)),
+    "c3_full": (("baseline", "c3"), dict(rounds=500)),
+}
+
+
+def gen_full():
+    """Whole BASELINE runs of c1 / c2 / c3 from the reference's simulate on 1
+    and on 8 BLAS threads (two equally valid trajectories: the row check
+    accepts either)."""
+    import threadpoolctl
+
+    out = {}
+    for name, (gen, kw) in FULL_CASES.items():
+        SIM_CASES[name] = (gen, kw)
+        cfg, shards = build_case(name)
+        for threads, tag in ((1, name), (8, name + "_mt")):
+            with threadpoolctl.threadpool_limits(threads, "blas"):
+                rows = simulate(cfg, shards)
+            for k, v in rows_arrays(rows).items():
+                out[f"{tag}__{k}"] = v
+            print(f"  full {tag}: {len(rows)} rows, final |g|={rows[-1].grad_norm:.3e}")
+    return out
+
+
 def gen_sim_opt_a():
     return gen_sim([n for n in SIM_CASES if "opt_a" in n])
 
@@ -684,6 +711,7 @@ def main(only=None):
         ("simulate_c4.npz", gen_c4),
         ("compress_r2.npz", gen_compress_r2),
         ("csv.npz", gen_csv),
+        ("simulate_full.npz", gen_full),
     ):
         if only and fname not in only:
             continue
