@@ -67,8 +67,12 @@ __global__ void __launch_bounds__(RED_THREADS) k_reduce(
   const int per_c = nblk + (frob_part ? n_pairs : 0);
   const int cpb = (n_active + G - 1) / G;
   const int c_lo = min(n_active, b * cpb), c_hi = min(n_active, c_lo + cpb);
-  const int chunk = max(1, 2048 / per_c);
+  // a client's partials are staged when they fit the buffer (else read in
+  // place: d > ~2800)
+  const bool staged = per_c <= 2048;
+  const int chunk = staged ? 2048 / per_c : 1 << 30;
   auto stage_load = [&](int i0, int nc) {
+    if (!staged) return;
     for (int e = threadIdx.x; e < nc * per_c; e += RED_THREADS) {
       const int ii = e / per_c, r = e - ii * per_c;
       const int c = client_of(clients, i0 + ii);
@@ -120,13 +124,18 @@ __global__ void __launch_bounds__(RED_THREADS) k_reduce(
     for (int ii = threadIdx.x; ii < nc; ii += RED_THREADS) {
       const int c = client_of(clients, i0 + ii);
       const double* st = stage + ii * per_c;
+      auto part = [&](int r) {
+        return staged ? st[r]
+                      : (r < nblk ? __ldcg(loss_part + static_cast<int64_t>(c) * nblk + r)
+                                  : __ldcg(frob_part + static_cast<int64_t>(c) * n_pairs + (r - nblk)));
+      };
       double ls = 0.0;
-      for (int r = 0; r < nblk; ++r) ls = __dadd_rn(ls, st[r]);
+      for (int r = 0; r < nblk; ++r) ls = __dadd_rn(ls, part(r));
       const double reg = __dmul_rn(__dmul_rn(0.5, lam_arr[c]), xx);
       f_cli[c] = __dadd_rn(__ddiv_rn(ls, static_cast<double>(ni_arr[c])), reg);
       if (frob_part) {
         double fp = 0.0;
-        for (int r = 0; r < n_pairs; ++r) fp = __dadd_rn(fp, st[nblk + r]);
+        for (int r = 0; r < n_pairs; ++r) fp = __dadd_rn(fp, part(nblk + r));
         shift_cli[c] = sqrt(fp);
         if (flags[c] & 1) atomicMin(&s_bad, c);
       }

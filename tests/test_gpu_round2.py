@@ -283,11 +283,13 @@ def test_large_d_solve_and_not_pd_pivot(d):
 
 @pytest.mark.gpu
 @pytest.mark.parametrize("d,kind,k,alg", [(1100, "topk", 8800, "fednl"), (2000, "randk", 2000, "fednl"),
-                                          (1100, "toplek", 1100, "fednl-ls"), (1100, "randseqk", 2200, "fednl-pp")])
+                                          (1100, "toplek", 1100, "fednl-ls"), (1100, "randseqk", 2200, "fednl-pp"),
+                                          (3000, "randseqk", 3000, "fednl")])
 def test_large_d_rounds_match_oracle(d, kind, k, alg):
     """d > 1024 (the global-memory solve; at d = 2000 the RandK bitmap in
-    global memory): FedNL / FedNL-LS / FedNL-PP rows against the oracle port
-    at 1e-10 with exact byte counters."""
+    global memory; at d = 3000 the round reduction reads the per-client
+    partials in place): FedNL / FedNL-LS / FedNL-PP rows against the oracle
+    port at 1e-10 with exact byte counters."""
     n, ni = 4, 160
     shards = D.gaussian_shards(d, n, ni, 1e-3, seed=11)
     kw = dict(compressor=CompressorSpec(CompressorKind(kind), k=k), rounds=4, run_seed=11, algorithm=alg)
