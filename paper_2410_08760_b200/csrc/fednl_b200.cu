@@ -1248,10 +1248,15 @@ int fb_create(const fb_config* cfg_in, void** out) {
     // panel-owning solve: one or two 32-column panels per CTA of a portable
     // (<= 8) cluster, while the panels fit in shared memory
     const int npan = (c.d + CP_NB - 1) / CP_NB;
-    ctx->cp_kp = npan <= CH_MAX_CLUSTER ? 1 : 2;
+    // one panel per CTA (a cluster of up to 16) when the round's compressor
+    // CTAs (one per active client, one SM each: the solve CTA's registers
+    // leave no room beside it) still fit the other SMs in one wave; else two
+    // panels per CTA of a portable cluster
+    const int comp_ctas = c.algorithm == FB_ALG_PP ? c.tau : c.n_clients;
+    ctx->cp_kp = (npan <= CH_MAX_CLUSTER || (npan <= CP_MAX_CLUSTER && comp_ctas + npan <= ctx->num_sms)) ? 1 : 2;
     ctx->cp_cs = (npan + ctx->cp_kp - 1) / ctx->cp_kp;
     // (three panels or fewer: the cluster-redundant solver is faster)
-    ctx->solve_panels = npan >= 4 && c.d <= CP_MAX_D && ctx->cp_cs <= CH_MAX_CLUSTER &&
+    ctx->solve_panels = npan >= 4 && c.d <= CP_MAX_D && ctx->cp_cs <= CP_MAX_CLUSTER &&
                         static_cast<size_t>(ctx->cp_kp) * cp_panel_bytes(c.d) <= CP_DYN_SMEM_MAX;
   }
   // d > CH_MAX_D: the global-memory blocked solve (solve_big.cuh)
@@ -1346,6 +1351,7 @@ int fb_create(const fb_config* cfg_in, void** out) {
                            static_cast<int>(std::max(max_solve, solve_panel_bytes<32>(1)))));
   static size_t max_cp = 0;
   max_cp = std::max(max_cp, static_cast<size_t>(ctx->cp_kp) * cp_panel_bytes(c.d));
+  CKC(cudaFuncSetAttribute(k_chol_panels<1>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
   CKC(cudaFuncSetAttribute(k_chol_panels<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            static_cast<int>(std::min<size_t>(max_cp + CP_STAMP_BYTES, CP_DYN_SMEM_MAX))));
   CKC(cudaFuncSetAttribute(k_chol_panels<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,

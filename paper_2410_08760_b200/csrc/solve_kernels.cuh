@@ -447,6 +447,12 @@ constexpr int CP_MAXP = 16;
 #define CP_REST_WARPS 0xECu
 #endif
 constexpr int CP_MAX_D = CP_MAXP * CP_NB;
+// one panel per CTA up to this many panels: a non-portable cluster (B200
+// allows 16), so no CTA serves two panels (at c0's 10 panels the owner of
+// two competed between its next factor and the other panel's updates)
+#ifndef CP_MAX_CLUSTER
+#define CP_MAX_CLUSTER 16
+#endif
 
 // The round reduction (k_reduce's outputs, round_kernels.cuh) folded into the
 // solve cluster's prologue: `grad` non-null selects it.  CTA r forms gbar
