@@ -1060,7 +1060,12 @@ constexpr int TKP_CW = TKP_CONS / 32;          // consumer warps (list regions p
 constexpr int TKP_CH = 2048;                   // positions per ring stage (16 KB)
 constexpr int TKP_NST = 6;                     // ring stages
 constexpr int TKP_STRIDE = TKP_CH + 2;         // stage stride (16-byte aligned, +1 lead)
-constexpr size_t TKP_SMEM = static_cast<size_t>(TKP_NST) * TKP_STRIDE * 8;
+constexpr int TKP_CH2 = 4096;                  // merged-list layout: positions per stage (32 KB)
+constexpr int TKP_NST2 = 3;                    //   ring stages
+constexpr size_t TKP_SMEM1 = static_cast<size_t>(TKP_NST) * TKP_STRIDE * 8;
+constexpr size_t TKP_SMEM2 = static_cast<size_t>(TKP_NST2) * TKP_CH2 * 8;
+constexpr size_t TKP_SMEM = TKP_SMEM1 > TKP_SMEM2 ? TKP_SMEM1 : TKP_SMEM2;
+static_assert(TKP_NST2 <= TKP_NST, "the merged layout reuses the ring's barriers");
 constexpr int TKP_SEGCAP = 16384;              // candidate slots per segment (max)
 constexpr int TKP_MAXSEG = 16;                 // segments per client (max)
 constexpr int TKP_MAXSUB = TKP_MAXSEG * TKP_CONS / 32;  // list regions per client (max)
@@ -1290,6 +1295,89 @@ __device__ __forceinline__ void tkp_consume(const double* ring, uint64_t* full, 
   }
 }
 
+
+// Merged-list layout (no zero tie class): ring stages of TKP_CH2 positions
+// starting at the segment's 16-byte aligned position `a0`; a consumer warp
+// owns a contiguous 1/TKP_CW slice of every stage.  Each lane reads its
+// elements as 16-byte pairs (pair j * 32 + lane of the slice: conflict-free),
+// keeps one bit per element whose key high word exceeds the window's lower
+// end (above the window and inside it alike: the selection tells them apart),
+// and the warp appends the flagged (position, raw value) entries to its list
+// region once per stage: a warp scan of the lanes' counts, then each lane
+// writes its own entries (values re-read from the stage).
+template <bool W, bool CHECK>
+__device__ __forceinline__ void tkp_stage_m(const double* __restrict__ wb_, int pos0, int t0, int t1,
+                                            int hlo, int lane, uint64_t* __restrict__ ck,
+                                            int32_t* __restrict__ cp, int capw, int& m_cnt) {
+  constexpr int PPL = TKP_CH2 / TKP_CW / 64;  // pairs per lane per stage
+  static_assert(PPL * 2 <= 32, "one mask bit per element");
+  const double2* pr = reinterpret_cast<const double2*>(wb_);
+  double2 x[PPL];
+#pragma unroll
+  for (int j = 0; j < PPL; ++j) x[j] = pr[j * 32 + lane];
+  uint32_t mask = 0u;
+#pragma unroll
+  for (int j = 0; j < PPL; ++j) {
+    const int t = pos0 + 2 * (j * 32 + lane);
+    int h0, h1;
+    if (W) {
+      h0 = static_cast<int>(rank_key(x[j].x, t, 1) >> 32);
+      h1 = static_cast<int>(rank_key(x[j].y, t + 1, 1) >> 32);
+    } else {
+      h0 = __double2hiint(x[j].x) & 0x7FFFFFFF;
+      h1 = __double2hiint(x[j].y) & 0x7FFFFFFF;
+    }
+    bool c0 = h0 > hlo, c1 = h1 > hlo;
+    if (CHECK) {
+      c0 = c0 && t >= t0 && t < t1;
+      c1 = c1 && t + 1 >= t0 && t + 1 < t1;
+    }
+    if (c0) mask |= 1u << (2 * j);
+    if (c1) mask |= 2u << (2 * j);
+  }
+  if (__any_sync(0xffffffffu, mask != 0u)) {
+    const int n = __popc(mask);
+    int incl = n;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += y;
+    }
+    int slot = m_cnt + incl - n;
+    m_cnt += __shfl_sync(0xffffffffu, incl, 31);
+    while (mask) {
+      const int b = __ffs(mask) - 1;
+      mask &= mask - 1u;
+      const int e = 2 * ((b >> 1) * 32 + lane) + (b & 1);
+      if (slot < capw) {
+        ck[slot] = static_cast<uint64_t>(__double_as_longlong(wb_[e]));
+        cp[slot] = pos0 + e;
+      }
+      ++slot;
+    }
+  }
+}
+
+template <bool W>
+__device__ __forceinline__ void tkp_consume_m(const double* ring, uint64_t* full, uint64_t* empty,
+                                              int nch, int a0, int t0, int t1, int hlo, int warp,
+                                              int lane, uint64_t* ck, int32_t* cp, int capw,
+                                              int& m_cnt) {
+  constexpr int SL = TKP_CH2 / TKP_CW;  // the warp's slice of a stage
+  for (int i = 0; i < nch; ++i) {
+    const int st = i % TKP_NST2;
+    mbar_wait_short(&full[st], (i / TKP_NST2) & 1);
+    const int cb = a0 + i * TKP_CH2;
+    const double* wb_ = ring + st * TKP_CH2 + warp * SL;
+    if (cb >= t0 && cb + TKP_CH2 <= t1)
+      tkp_stage_m<W, false>(wb_, cb + warp * SL, t0, t1, hlo, lane, ck, cp, capw, m_cnt);
+    else
+      tkp_stage_m<W, true>(wb_, cb + warp * SL, t0, t1, hlo, lane, ck, cp, capw, m_cnt);
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[st]);
+  }
+}
+
 __device__ __noinline__ void tks_select_client(
     int c, uint32_t* sg, const double* __restrict__ D, int64_t w, int wbp, int k, int weighted,
     int S_seg, int capw, const int32_t* __restrict__ clients, const TkWin* __restrict__ win,
@@ -1320,10 +1408,13 @@ __global__ void __launch_bounds__(TKP_THREADS) k_tks_pass(
   const int S = gridDim.x, s = blockIdx.x;
   const int wi = static_cast<int>(w);
   const int t0 = s * lseg, t1 = min(wi, t0 + lseg);
-  const int nch = (t1 - t0 + TKP_CH - 1) / TKP_CH;
   const double* v = D + static_cast<int64_t>(c) * w;
   // bulk copies need 16-byte aligned sources: start one position early on odd rows
   const int lead = static_cast<int>((reinterpret_cast<uintptr_t>(v + t0) & 15u) >> 3);
+  // no zero tie class: the merged-list layout (aligned stages of TKP_CH2)
+  const bool merged = !wn.zero;
+  const int a0 = t0 - lead;
+  const int nch = merged ? (t1 - a0 + TKP_CH2 - 1) / TKP_CH2 : (t1 - t0 + TKP_CH - 1) / TKP_CH;
   if (tid == 0) {
     for (int i = 0; i < TKP_NST; ++i) {
       mbar_init(&full[i], 1);
@@ -1333,7 +1424,16 @@ __global__ void __launch_bounds__(TKP_THREADS) k_tks_pass(
   }
   __syncthreads();
   if (warp == TKP_CW) {  // producer
-    if (lane == 0) {
+    if (lane == 0 && merged) {
+      for (int i = 0; i < nch; ++i) {
+        const int st = i % TKP_NST2;
+        if (i >= TKP_NST2) mbar_wait_short(&empty[st], ((i / TKP_NST2) - 1) & 1);
+        const int nel = min(TKP_CH2, t1 - a0 - i * TKP_CH2);
+        const uint32_t bytes = static_cast<uint32_t>((nel + 1) & ~1) * 8u;
+        mbar_arrive_expect_tx(&full[st], bytes);
+        bulk_load(ring + st * TKP_CH2, v + a0 + i * TKP_CH2, bytes, &full[st]);
+      }
+    } else if (lane == 0) {
       for (int i = 0; i < nch; ++i) {
         const int st = i % TKP_NST;
         if (i >= TKP_NST) mbar_wait_short(&empty[st], ((i / TKP_NST) - 1) & 1);
@@ -1353,9 +1453,8 @@ __global__ void __launch_bounds__(TKP_THREADS) k_tks_pass(
                          cand_key + lbase, cand_pos + lbase, gt_val + lbase, gt_pos + lbase, capw,
                          m_cnt, g_cnt, z_cnt);
   else
-    tkp_consume<W, false>(ring, full, empty, nch, lead, t0, t1, wn.hhi, wn.hlo, tid, lane, zrow,
-                          cand_key + lbase, cand_pos + lbase, gt_val + lbase, gt_pos + lbase,
-                          capw, m_cnt, g_cnt, z_cnt);
+    tkp_consume_m<W>(ring, full, empty, nch, a0, t0, t1, wn.hlo, warp, lane, cand_key + lbase,
+                     cand_pos + lbase, capw, m_cnt);
   if (lane == 0) seg[sub] = TkSeg{g_cnt, m_cnt, z_cnt, 0};
   }
   // the last of the client's segment CTAs to finish runs its selection (the
@@ -1505,15 +1604,37 @@ __device__ __noinline__ void tks_select_client(
     }
   }
   __syncthreads();
-  const int G = s_G, M = s_M, Z = wn.zero ? s_Z : 0;
-  const bool ok = !s_over && G < k && G + M + Z >= k;
   constexpr int UB = 4;  // list entries per lane in flight
   const uint64_t KMASK = 0x7FFFFFFFFFFFFFFFull;
+  // merged lists (no zero tie class, see tkp_stage_m): the candidate regions
+  // also hold the entries above the window.  Their rank key reads as all
+  // ones here (above every prefix: outside the histograms, marked by the
+  // final pass) and they are counted first (G).
+  const bool merged = !wn.zero;
   auto ckey = [&](int sl) {  // candidate slot -> rank key (raw value bits stored)
     const uint64_t b = __ldcg(ck + sl);
-    return weighted ? rank_key(__longlong_as_double(static_cast<long long>(b)), __ldcg(cp + sl), 1)
-                    : (b & KMASK);
+    const uint64_t key =
+        weighted ? rank_key(__longlong_as_double(static_cast<long long>(b)), __ldcg(cp + sl), 1)
+                 : (b & KMASK);
+    return (merged && static_cast<int>(key >> 32) > wn.hhi) ? ~0ull : key;
   };
+  if (merged && !s_over) {
+    int g = 0;
+    tksel_regions<UB>(mcnt, NR, capw, [&](const int* sl, const bool* vl_) {
+      uint64_t kk[UB];
+#pragma unroll
+      for (int u = 0; u < UB; ++u) kk[u] = vl_[u] ? ckey(sl[u]) : 0ull;
+#pragma unroll
+      for (int u = 0; u < UB; ++u) g += kk[u] == ~0ull;
+    });
+    g = warp_sum_int(g);
+    if (lane == 0 && g) atomicAdd(&s_G, g);
+    __syncthreads();
+    if (tid == 0) s_M -= s_G;
+    __syncthreads();
+  }
+  const int G = s_G, M = s_M, Z = wn.zero ? s_Z : 0;
+  const bool ok = !s_over && G < k && G + M + Z >= k;
   auto mark = [&](int t) { atomicOr(&sg[t >> 5], 1u << (t & 31)); };
   auto mark_eq = [&](int t) { atomicOr(&zrow[t >> 5], 1u << (t & 31)); };
   int need = k;
