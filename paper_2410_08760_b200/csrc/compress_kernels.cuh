@@ -1303,8 +1303,8 @@ __device__ __forceinline__ void tkp_consume(const double* ring, uint64_t* full, 
 // keeps one bit per element whose key high word exceeds the window's lower
 // end (above the window and inside it alike: the selection tells them apart),
 // and the warp appends the flagged (position, raw value) entries to its list
-// region once per stage: a warp scan of the lanes' counts, then each lane
-// writes its own entries (values re-read from the stage).
+// region once per stage in rounds: every lane that still holds a flagged
+// element writes one per round (values re-read from the stage).
 template <bool W, bool CHECK>
 __device__ __forceinline__ void tkp_stage_m(const double* __restrict__ wb_, int pos0, int t0, int t1,
                                             int hlo, int lane, uint64_t* __restrict__ ck,
@@ -1335,26 +1335,23 @@ __device__ __forceinline__ void tkp_stage_m(const double* __restrict__ wb_, int 
     if (c0) mask |= 1u << (2 * j);
     if (c1) mask |= 2u << (2 * j);
   }
-  if (__any_sync(0xffffffffu, mask != 0u)) {
-    const int n = __popc(mask);
-    int incl = n;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const int y = __shfl_up_sync(0xffffffffu, incl, o);
-      if (lane >= o) incl += y;
-    }
-    int slot = m_cnt + incl - n;
-    m_cnt += __shfl_sync(0xffffffffu, incl, 31);
-    while (mask) {
+  // append rounds: in round r every lane that still has a flagged element
+  // emits one (slot = running count + the rank of the lane among them)
+  const uint32_t lt = (1u << lane) - 1u;
+  for (;;) {
+    const uint32_t hb = __ballot_sync(0xffffffffu, mask != 0u);
+    if (!hb) break;
+    if (mask) {
       const int b = __ffs(mask) - 1;
       mask &= mask - 1u;
       const int e = 2 * ((b >> 1) * 32 + lane) + (b & 1);
+      const int slot = m_cnt + __popc(hb & lt);
       if (slot < capw) {
         ck[slot] = static_cast<uint64_t>(__double_as_longlong(wb_[e]));
         cp[slot] = pos0 + e;
       }
-      ++slot;
     }
+    m_cnt += __popc(hb);
   }
 }
 
@@ -1364,17 +1361,21 @@ __device__ __forceinline__ void tkp_consume_m(const double* ring, uint64_t* full
                                               int lane, uint64_t* ck, int32_t* cp, int capw,
                                               int& m_cnt) {
   constexpr int SL = TKP_CH2 / TKP_CW;  // the warp's slice of a stage
+  int st = 0;
+  uint32_t par = 0;
+  const double* wb_ = ring + warp * SL;
+  int pos0 = a0 + warp * SL;
   for (int i = 0; i < nch; ++i) {
-    const int st = i % TKP_NST2;
-    mbar_wait_short(&full[st], (i / TKP_NST2) & 1);
-    const int cb = a0 + i * TKP_CH2;
-    const double* wb_ = ring + st * TKP_CH2 + warp * SL;
+    mbar_wait_short(&full[st], par);
+    const int cb = pos0 - warp * SL;
     if (cb >= t0 && cb + TKP_CH2 <= t1)
-      tkp_stage_m<W, false>(wb_, cb + warp * SL, t0, t1, hlo, lane, ck, cp, capw, m_cnt);
+      tkp_stage_m<W, false>(wb_ + st * TKP_CH2, pos0, t0, t1, hlo, lane, ck, cp, capw, m_cnt);
     else
-      tkp_stage_m<W, true>(wb_, cb + warp * SL, t0, t1, hlo, lane, ck, cp, capw, m_cnt);
+      tkp_stage_m<W, true>(wb_ + st * TKP_CH2, pos0, t0, t1, hlo, lane, ck, cp, capw, m_cnt);
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[st]);
+    pos0 += TKP_CH2;
+    if (++st == TKP_NST2) { st = 0; par ^= 1u; }
   }
 }
 
@@ -1618,23 +1619,11 @@ __device__ __noinline__ void tks_select_client(
                  : (b & KMASK);
     return (merged && static_cast<int>(key >> 32) > wn.hhi) ? ~0ull : key;
   };
-  if (merged && !s_over) {
-    int g = 0;
-    tksel_regions<UB>(mcnt, NR, capw, [&](const int* sl, const bool* vl_) {
-      uint64_t kk[UB];
-#pragma unroll
-      for (int u = 0; u < UB; ++u) kk[u] = vl_[u] ? ckey(sl[u]) : 0ull;
-#pragma unroll
-      for (int u = 0; u < UB; ++u) g += kk[u] == ~0ull;
-    });
-    g = warp_sum_int(g);
-    if (lane == 0 && g) atomicAdd(&s_G, g);
-    __syncthreads();
-    if (tid == 0) s_M -= s_G;
-    __syncthreads();
-  }
-  const int G = s_G, M = s_M, Z = wn.zero ? s_Z : 0;
-  const bool ok = !s_over && G < k && G + M + Z >= k;
+  // merged: G is counted by the first radix level's pass (s_M = G + M until then)
+  int G = s_G, M = s_M;
+  const int Z = wn.zero ? s_Z : 0;
+  const bool ok = !s_over && (merged ? M >= k : (G < k && G + M + Z >= k));
+  bool miss = false;  // merged: the window's upper end is at or below the k-th key
   auto mark = [&](int t) { atomicOr(&sg[t >> 5], 1u << (t & 31)); };
   auto mark_eq = [&](int t) { atomicOr(&zrow[t >> 5], 1u << (t & 31)); };
   int need = k;
@@ -1649,7 +1638,7 @@ __device__ __noinline__ void tks_select_client(
         if (tt[u] >= 0) mark(tt[u]);
     });
   }
-  if (ok && G + M >= k) {
+  if (ok && (merged || G + M >= k)) {
     // the k-th key is a candidate; zeros (if tracked) are not needed
     if (wn.zero) {
       for (int q = tid; q < wbp; q += TKSEL_THREADS) zrow[q] = 0u;
@@ -1669,6 +1658,7 @@ __device__ __noinline__ void tks_select_client(
       const uint32_t dmask = (1u << bits) - 1u;
       for (int i = tid; i < 2048; i += TKSEL_THREADS) hist[i] = 0u;
       __syncthreads();
+      int g = 0;
       tksel_regions<UB>(mcnt, NR, capw, [&](const int* sl, const bool* vl_) {
         uint64_t kk[UB];
 #pragma unroll
@@ -1677,10 +1667,21 @@ __device__ __noinline__ void tks_select_client(
         for (int u = 0; u < UB; ++u) {
           uint32_t dig = 0xFFFFFFFFu;
           if (vl_[u] && (kk[u] >> hi_excl) == pf) dig = static_cast<uint32_t>(kk[u] >> sh) & dmask;
+          g += kk[u] == ~0ull;
           tks_add(hist, dig, lane);
         }
       });
+      if (merged && lv == 0) {
+        g = warp_sum_int(g);
+        if (lane == 0 && g) atomicAdd(&s_G, g);
+      }
       __syncthreads();
+      if (merged && lv == 0) {
+        G = s_G;
+        M -= G;
+        need = k - G;
+        if (G >= k) { miss = true; break; }
+      }
       tk_find_digit_n(hist, 1 << bits, need, ws, &s_digit, &s_above);
       need -= s_above;
       pf = (pf << bits) | static_cast<uint64_t>(s_digit);
@@ -1694,7 +1695,7 @@ __device__ __noinline__ void tks_select_client(
     // (or, when the whole bin is taken, selected as well; or, when the final
     // bin is a tie class larger than the list, tie-marked directly)
     const bool direct = !all && nbin > TKSEL_LCAP;
-    tksel_regions<UB>(mcnt, NR, capw, [&](const int* sl, const bool* vl_) {
+    if (!miss) tksel_regions<UB>(mcnt, NR, capw, [&](const int* sl, const bool* vl_) {
       uint64_t kk[UB];
       int tt[UB];
 #pragma unroll
@@ -1720,7 +1721,9 @@ __device__ __noinline__ void tks_select_client(
       }
     });
     __syncthreads();
-    if (all) {
+    if (miss) {
+      if (tid == 0) s_fail = 1;
+    } else if (all) {
       need = 0;
     } else if (direct) {
       // the eq take below picks the first `need` tied positions
