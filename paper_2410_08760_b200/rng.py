@@ -1,6 +1,6 @@
 """Host-side SplitMix64 seeding helpers (mirror of the reference's rng API).
 
-The device kernels carry their own SplitMix64 (csrc/rng.cuh); this host copy
+The device kernels carry their own SplitMix64 (`Prg` in csrc/common.cuh); this host copy
 serves the public API (`Prg`, `derive_round_seed`, ...) and one-time input
 preparation (the TAG_SHUFFLE shard permutation).  Stream conventions follow
 reference rng.py:1-136:
