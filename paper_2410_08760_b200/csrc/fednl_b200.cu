@@ -65,7 +65,7 @@ struct Ctx {
   double alpha_n = 0.0, rand_scale = 1.0;
   int solve_cs = 1, solve_nb = 32;
   bool solve_panels = false;  // k_chol_panels (d <= CP_MAX_D) instead of k_chol_solve
-  bool solve_big = false;     // d > CH_MAX_D: the global-memory blocked solve (solve_big.cuh)
+  bool solve_big = false;     // d > CP_MAX_D: the global-memory blocked solve (solve_big.cuh)
   int cp_kp = 1, cp_cs = 1;
   bool topk_stream = false;  // one-pass sampled-window TopK (else the shared-memory radix)
   bool topk_split = false;   // ... as window / segmented pass / select kernels
@@ -75,6 +75,8 @@ struct Ctx {
   int num_sms = 148;
   int32_t* pair_order = nullptr;  // Hessian tile pairs, costliest first
   double* Lg = nullptr;       // k_chol_panels: released L panels
+  double* Lbig = nullptr;     // solve_big: the factor below the diagonal blocks ((d+1) x (d+1))
+  double* Tbig = nullptr;     // solve_big: inverse diagonal blocks, [panels][32][32]
   double* pp_shift_part = nullptr;  // FedNL-PP: Frobenius partials [tau][PP_SB]
   // client sharding over `world` GPUs (fb_set_shard): this rank owns clients
   // [c_lo, c_hi) of blocks of npr; per-client exchange arrays are padded to
@@ -630,9 +632,10 @@ int launch_solve(Ctx* ctx, cudaStream_t s, const double* hpk, const double* shif
                  const double* rhs, const double* x, double* z, double* x_out, int mode,
                  int ignore_halt, long long* dbg = nullptr, cudaEvent_t launched = nullptr,
                  bool force_old = false, bool after_reduce = false, const CpRed* red = nullptr) {
-  if (ctx->solve_big) {
-    // d > CH_MAX_D: setup, then per 64-column panel the block factor + row
-    // solve and the trailing update, then the back substitution
+  if (ctx->solve_big && !(force_old && ctx->d <= CH_MAX_D)) {
+    // d > CP_MAX_D: setup, then one kernel per 32-column panel (block factor,
+    // panel rows and the trailing update of one tile per CTA), then the back
+    // substitution (solve_big.cuh)
     const int d = ctx->d;
     k_big_setup<<<std::min(d + 1, 4 * ctx->num_sms), BIG_THREADS, 0, s>>>(ctx->ctl, d, hpk, shift_ptr, rhs,
                                                                           ctx->M);
@@ -640,19 +643,13 @@ int launch_solve(Ctx* ctx, cudaStream_t s, const double* hpk, const double* shif
     if (launched) CK(cudaEventRecord(launched, s));
     for (int p0 = 0; p0 < d; p0 += BIG_NB) {
       const int p1 = std::min(d, p0 + BIG_NB);
-      const int rows = d + 1 - p1;
-      const int pblk = std::max(1, std::min(ctx->num_sms, (rows + BIG_THREADS - 1) / BIG_THREADS));
-      k_big_panel<<<pblk, BIG_THREADS, BIG_NB * BIG_LDS * sizeof(double), s>>>(ctx->ctl, d, p0, ctx->M);
+      const int T = (d + 1 - p1 + BIG_TILE - 1) / BIG_TILE;  // tiles of rows p1..d (the rhs row included)
+      k_big_panel<<<T * (T + 1) / 2, BIG_THREADS, sizeof(BigSmem), s>>>(ctx->ctl, d, p0, ctx->M, ctx->Lbig,
+                                                                        ctx->Tbig);
       CKL();
-      if (p1 < d) {
-        const int T = (rows + BIG_TILE - 1) / BIG_TILE;
-        k_big_update<<<T * (T + 1) / 2, BIG_THREADS, 2 * BIG_TILE * BIG_LDS * sizeof(double), s>>>(
-            ctx->ctl, d, p0, ctx->M);
-        CKL();
-      }
     }
-    k_big_back<<<1, BIG_BACK_THREADS, (static_cast<size_t>(d) + BIG_NB) * sizeof(double), s>>>(
-        ctx->ctl, d, ctx->M, x, z, x_out, mode, ignore_halt);
+    k_big_back<<<1, BIG_BACK_THREADS, big_back_smem(d), s>>>(ctx->ctl, d, ctx->Lbig, ctx->Tbig, x, z, x_out,
+                                                             mode, ignore_halt);
     CKL();
     return FB_OK;
   }
@@ -1259,10 +1256,10 @@ int fb_create(const fb_config* cfg_in, void** out) {
     ctx->solve_panels = npan >= 4 && c.d <= CP_MAX_D && ctx->cp_cs <= CP_MAX_CLUSTER &&
                         static_cast<size_t>(ctx->cp_kp) * cp_panel_bytes(c.d) <= CP_DYN_SMEM_MAX;
   }
-  // d > CH_MAX_D: the global-memory blocked solve (solve_big.cuh)
-  ctx->solve_big = c.d > CH_MAX_D;
+  // d > CP_MAX_D: the global-memory blocked solve (solve_big.cuh)
+  ctx->solve_big = c.d > CP_MAX_D;
   if (ctx->solve_big) ctx->solve_panels = false;
-  ctx->solve_smem = ctx->solve_big ? 0
+  ctx->solve_smem = c.d > CH_MAX_D ? 0
                     : (ctx->solve_nb == 32 ? solve_panel_bytes<32>(c.d) : solve_panel_bytes<16>(c.d));
   int rc = FB_OK;
   auto fail = [&](int code) {
@@ -1323,10 +1320,10 @@ int fb_create(const fb_config* cfg_in, void** out) {
   FB_MC_ATTR(float)
   FB_MC_ATTR(int8_t)
 #undef FB_MC_ATTR
-  CKC(cudaFuncSetAttribute(k_big_update, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           static_cast<int>(2 * BIG_TILE * BIG_LDS * sizeof(double))));
+  CKC(cudaFuncSetAttribute(k_big_panel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           static_cast<int>(sizeof(BigSmem))));
   CKC(cudaFuncSetAttribute(k_big_back, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           static_cast<int>((FB_MAX_D + BIG_NB) * sizeof(double))));
+                           static_cast<int>(big_back_smem(FB_MAX_D))));
   CKC(cudaFuncSetAttribute(k_ls_trials<double>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            static_cast<int>(LS_BATCH * FB_MAX_D * sizeof(double))));
   CKC(cudaFuncSetAttribute(k_ls_trials<float>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1406,6 +1403,8 @@ int fb_create(const fb_config* cfg_in, void** out) {
       dalloc(ctx, &ctx->eigV, static_cast<size_t>(d) * d) || dalloc(ctx, &ctx->hclamp, w) ||
       dalloc(ctx, &ctx->rs, static_cast<size_t>(n) * (ctx->nr + 1)) ||
       dalloc(ctx, &ctx->M, static_cast<size_t>(d + 1) * (d + 1)) ||
+      dalloc(ctx, &ctx->Lbig, ctx->solve_big ? static_cast<size_t>(d + 1) * (d + 1) : 1) ||
+      dalloc(ctx, &ctx->Tbig, ctx->solve_big ? static_cast<size_t>((d + BIG_NB - 1) / BIG_NB) * BIG_NB * BIG_NB : 1) ||
       dalloc(ctx, &ctx->Lg, ctx->solve_panels ? static_cast<size_t>((d + CP_NB - 1) / CP_NB) *
                                                     cp_rows(d) * CP_LS : 1) ||
       dalloc(ctx, &ctx->bitmap, static_cast<size_t>(n) * tks_wbp(w)) || dalloc(ctx, &ctx->count, n) ||

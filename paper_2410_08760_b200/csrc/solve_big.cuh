@@ -1,27 +1,33 @@
 // solve_big.cuh — the shifted Cholesky solve (H + shift I) z = rhs for
-// d > CH_MAX_D (reference algorithms.py:361-367 option b, linalg.py:133-186),
-// where the cluster solvers' panels and vectors no longer fit shared memory.
-// Every BASELINE config has d <= 1024; this path lifts the envelope (the
-// reference has no limit on d) with plain blocked kernels on the workspace M:
+// d > CP_MAX_D (reference algorithms.py:361-367 option b, linalg.py:133-186),
+// where the panel-owning cluster solver's panels no longer fit shared memory
+// (c4: d = 1024; the reference has no limit on d).  A right-looking blocked
+// factorisation over global memory (the matrix lives in L2), ONE kernel per
+// 32-column panel:
 //
 //   M ((d+1) x (d+1) doubles, column-major, ld = d + 1): the LOWER triangle
 //   A[r][c] = H[c][r] (+ shift on the diagonal) for c <= r < d, and the
 //   right-hand side as row d, A[d][c] = rhs[c] — factorising the augmented
-//   matrix leaves L below the diagonal and y = L^-1 rhs in row d.
+//   matrix leaves y = L^-1 rhs in row d of L.
+//   L (same shape, a second buffer): the factor below the diagonal blocks.
+//   Tg[p] (32 x 32): T_p = L_pp^-1, the inverse of panel p's diagonal block.
 //
-// Per BIG_NB-column panel p0 (right-looking):
-//   k_big_panel   every CTA factors the diagonal block in shared memory
-//                 (identical inputs: identical bits), CTA 0 writes L_pp back
-//                 and reports the first pivot <= 0 or not finite
-//                 (NotPositiveDefiniteError(index, value), pivots in index
-//                 order); then each CTA solves its share of the rows below
-//                 (rhs row included) against L_pp: L_ip = A_ip L_pp^-T;
-//   k_big_update  the trailing update A[i][j] -= L_ip . L_jp over the lower
-//                 triangle of [p1, d] in 64 x 64 tiles (rhs row included: the
-//                 forward substitution rides along).
-// k_big_back     one CTA: z = L^-T y block by block from the last (the
-//                 later blocks' contribution as a matvec, then the block's
-//                 triangular solve), then x_out per mode as k_chol_solve.
+// k_big_panel(p): one CTA per 64 x 64 tile (ti >= tj) of the trailing matrix
+//   [p1, d] x [p1, d).  Every CTA factors the panel's 32 x 32 diagonal block
+//   itself (identical inputs: identical bits; warp 0 the block factor with
+//   lane c owning column c of the symmetric Schur complement, warp 1 the
+//   inverse T one pivot behind it — the scheme of k_chol_panels), forms the
+//   panel rows of BOTH its tiles, X = A_ip T^T (a 64 x 32 x 32 product:
+//   cheaper than waiting for another CTA's), and applies
+//   C_ij -= X_i X_j^T to its tile.  The CTAs of the diagonal tiles write their
+//   X rows to L (a second buffer: other CTAs still read A's panel columns),
+//   CTA 0 writes T_p.  No cross-CTA dependency inside a kernel; the next
+//   panel's kernel follows in stream order.  The first pivot <= 0 or not
+//   finite raises NotPositiveDefiniteError(index, value) (pivots in index
+//   order).
+// k_big_back: one CTA: z_b = T_b^T (y_b - sum_{k >= b1} L[k][b] z_k) block by
+//   block from the last (a warp per column for the sum, then a 32 x 32
+//   product), then x_out per mode as k_chol_solve.
 // The factorisation order differs from the reference's column loop; results
 // agree to rounding (parity bar 1e-10).
 #pragma once
@@ -29,10 +35,10 @@
 
 namespace fb {
 
-constexpr int BIG_NB = 64;
+constexpr int BIG_NB = 32;
 constexpr int BIG_THREADS = 256;
 constexpr int BIG_TILE = 64;
-constexpr int BIG_LDS = BIG_NB + 1;  // shared-memory row pitch of a 64-wide block
+constexpr int BIG_LDS = BIG_NB + 1;  // shared-memory row pitch of a 32-wide block
 
 // A[r][c] (r >= c) from packed H (column-wise upper: H[c][r] at r(r+1)/2 + c)
 __global__ void __launch_bounds__(BIG_THREADS) k_big_setup(const DevCtl* __restrict__ ctl, int d,
@@ -59,114 +65,162 @@ __global__ void __launch_bounds__(BIG_THREADS) k_big_setup(const DevCtl* __restr
   }
 }
 
-// dynamic smem: the diagonal block, BIG_NB x BIG_LDS doubles
-__global__ void __launch_bounds__(BIG_THREADS) k_big_panel(DevCtl* __restrict__ ctl, int d, int p0,
-                                                           double* __restrict__ M) {
-  extern __shared__ double Ls[];  // Ls[r * BIG_LDS + c], r >= c
-  __shared__ int s_fail;
-  __shared__ double s_fval;
-  if (ctl->halt) return;
-  const int64_t ld = d + 1;
-  const int pb = min(BIG_NB, d - p0), p1 = p0 + pb;
-  const int tid = threadIdx.x;
-  for (int e = tid; e < pb * pb; e += BIG_THREADS) {
-    const int r = e / pb, c = e % pb;
-    Ls[r * BIG_LDS + c] = c <= r ? M[(p0 + r) + static_cast<int64_t>(p0 + c) * ld] : 0.0;
-  }
-  if (tid == 0) s_fail = -1;
-  __syncthreads();
-  // right-looking factorisation of the block (column j: pivot, scale, update)
-  for (int j = 0; j < pb; ++j) {
-    const double piv = Ls[j * BIG_LDS + j];
-    if (!(piv > 0.0 && isfinite(piv))) {  // uniform: every thread reads the same pivot
-      if (tid == 0) {
-        s_fail = j;
-        s_fval = piv;
-      }
-      break;
-    }
-    const double ljj = sqrt(piv);
-    const double inv = 1.0 / ljj;
-    __syncthreads();  // every thread has read the pivot
-    for (int r = j + 1 + tid; r < pb; r += BIG_THREADS) Ls[r * BIG_LDS + j] *= inv;
-    if (tid == 0) Ls[j * BIG_LDS + j] = ljj;
-    __syncthreads();
-    const int m = pb - j - 1;  // trailing rows / columns j+1 .. pb-1
-    for (int e = tid; e < m * m; e += BIG_THREADS) {
-      const int r = j + 1 + e / m, c = j + 1 + e % m;
-      if (c <= r) Ls[r * BIG_LDS + c] = fma(-Ls[r * BIG_LDS + j], Ls[c * BIG_LDS + j], Ls[r * BIG_LDS + c]);
-    }
-    __syncthreads();
-  }
-  __syncthreads();
-  if (s_fail >= 0) {
-    if (blockIdx.x == 0 && tid == 0) {
-      ctl->pivot_index = p0 + s_fail;
-      ctl->pivot_value = s_fval;
-      raise_status(ctl, ST_NOT_PD);
-    }
-    return;
-  }
-  if (blockIdx.x == 0)
-    for (int e = tid; e < pb * pb; e += BIG_THREADS) {
-      const int r = e / pb, c = e % pb;
-      if (c <= r) M[(p0 + r) + static_cast<int64_t>(p0 + c) * ld] = Ls[r * BIG_LDS + c];
-    }
-  // rows i in [p1, d] (row d: the right-hand side): x L_pp^T = a, one row
-  // per thread, forward substitution over the block's columns
-  for (int i = p1 + blockIdx.x * BIG_THREADS + tid; i <= d; i += gridDim.x * BIG_THREADS) {
-    double x[BIG_NB];
-#pragma unroll
-    for (int s = 0; s < BIG_NB; ++s) x[s] = s < pb ? M[i + static_cast<int64_t>(p0 + s) * ld] : 0.0;
-#pragma unroll
-    for (int s = 0; s < BIG_NB; ++s) {
-      if (s < pb) {
-        double v = x[s];
-#pragma unroll
-        for (int t = 0; t < s; ++t) v = fma(-x[t], Ls[s * BIG_LDS + t], v);
-        x[s] = v / Ls[s * BIG_LDS + s];
-      }
-    }
-#pragma unroll
-    for (int s = 0; s < BIG_NB; ++s)
-      if (s < pb) M[i + static_cast<int64_t>(p0 + s) * ld] = x[s];
-  }
-}
 
-// trailing update of the lower triangle of [p1, d] x [p1, d): tile (ti, tj),
-// ti >= tj, of BIG_TILE rows / columns; blockIdx.x enumerates the tiles.
-// dynamic smem: the panel rows of both tiles, 2 x BIG_TILE x BIG_LDS doubles
-__global__ void __launch_bounds__(BIG_THREADS) k_big_update(const DevCtl* __restrict__ ctl, int d, int p0,
-                                                            double* __restrict__ M) {
-  extern __shared__ double Ps[];  // Pa[r][s] rows of tile ti, Pb[r][s] rows of tile tj
+struct BigSmem {
+  double S[BIG_NB][BIG_LDS];     // the diagonal block (symmetric), then unused
+  double R[BIG_NB][BIG_LDS];     // row j of the Schur complement at pivot j
+  double T[BIG_NB][BIG_LDS];     // L_pp^-1 (lower triangular)
+  double A[2][BIG_TILE][BIG_LDS];  // panel rows of tile ti / tj as loaded
+  double X[2][BIG_TILE][BIG_LDS];  // A T^T
+  double inv[BIG_NB];
+  uint64_t barF[BIG_NB];
+  int failed;
+};
+
+__global__ void __launch_bounds__(BIG_THREADS) k_big_panel(DevCtl* __restrict__ ctl, int d, int p0,
+                                                           double* __restrict__ M,
+                                                           double* __restrict__ L,
+                                                           double* __restrict__ Tg) {
+  extern __shared__ __align__(16) uint8_t big_raw[];
+  BigSmem& sm = *reinterpret_cast<BigSmem*>(big_raw);
   if (ctl->halt) return;
   const int64_t ld = d + 1;
   const int pb = min(BIG_NB, d - p0), p1 = p0 + pb;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int q = blockIdx.x;
   int ti = static_cast<int>((sqrtf(8.0f * q + 1.0f) - 1.0f) * 0.5f);
   while ((ti + 1) * (ti + 2) / 2 <= q) ++ti;
   while (ti * (ti + 1) / 2 > q) --ti;
   const int tj = q - ti * (ti + 1) / 2;
   const int r0 = p1 + ti * BIG_TILE, c0 = p1 + tj * BIG_TILE;
-  double* Pa = Ps;
-  double* Pb = Ps + BIG_TILE * BIG_LDS;
-  const int tid = threadIdx.x;
+  if (tid < BIG_NB) mbar_init(&sm.barF[tid], 1);
+  if (tid == 0) {
+    sm.failed = 0;
+    fence_barrier_init();
+  }
+  // the diagonal block in full (padded with the identity past pb)
+  for (int e = tid; e < BIG_NB * BIG_NB; e += BIG_THREADS) {
+    const int r = e & (BIG_NB - 1), c = e >> 5;
+    const int hi = max(r, c), lo = min(r, c);
+    sm.S[r][c] = hi < pb ? __ldcg(M + (p0 + hi) + static_cast<int64_t>(p0 + lo) * ld) : (r == c ? 1.0 : 0.0);
+  }
+  // the panel rows of both tiles (coalesced along the rows)
   for (int e = tid; e < BIG_TILE * BIG_NB; e += BIG_THREADS) {
-    const int r = e % BIG_TILE, s = e / BIG_TILE;  // coalesced along the rows
+    const int r = e & (BIG_TILE - 1), s = e >> 6;
     const bool sv = s < pb;
-    Pa[r * BIG_LDS + s] = (sv && r0 + r <= d) ? M[(r0 + r) + static_cast<int64_t>(p0 + s) * ld] : 0.0;
-    Pb[r * BIG_LDS + s] = (sv && c0 + r < d) ? M[(c0 + r) + static_cast<int64_t>(p0 + s) * ld] : 0.0;
+    sm.A[0][r][s] = (sv && r0 + r <= d) ? __ldcg(M + (r0 + r) + static_cast<int64_t>(p0 + s) * ld) : 0.0;
+    if (ti != tj)
+      sm.A[1][r][s] = (sv && c0 + r <= d) ? __ldcg(M + (c0 + r) + static_cast<int64_t>(p0 + s) * ld) : 0.0;
   }
   __syncthreads();
-  // thread: rows ty + 16 a, columns tx + 16 b (a, b < 4)
-  const int tx = tid & 15, ty = tid >> 4;
+  if (warp == 0) {
+    // block factor on the symmetric Schur complement: lane c owns column c
+    // (a[r] = S[r][c]); by symmetry its multiplier S[c][j] is its own a[j],
+    // so per pivot only 1/sqrt(S[j][j]) crosses lanes
+    double a[BIG_NB];
+#pragma unroll
+    for (int r = 0; r < BIG_NB; ++r) a[r] = sm.S[r][lane];
+    double myir = 0.0, mypiv = 0.0;
+    sm.R[0][lane] = a[0];
+    {
+      const double y = rsqrt_nr(a[0]);
+      if (lane == 0) { sm.inv[0] = y; mypiv = a[0]; }
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&sm.barF[0]);
+    double ir = sm.inv[0];
+#pragma unroll
+    for (int j = 0; j < BIG_NB; ++j) {
+      const double* b = &sm.R[j][0];
+      myir = (lane == j) ? ir : myir;
+      const double ir2 = ir * ir;
+      const double m = (lane > j) ? a[j] * ir2 : 0.0;  // columns < j are final
+      if (j + 1 < BIG_NB) {
+        a[j + 1] = fma(-m, b[j + 1], a[j + 1]);
+        sm.R[j + 1][lane] = a[j + 1];
+        const double y = rsqrt_nr(a[j + 1]);
+        mypiv = (lane == j + 1) ? a[j + 1] : mypiv;
+        if (lane == j + 1) sm.inv[j + 1] = y;
+      }
+#pragma unroll
+      for (int r = j + 2; r < BIG_NB; ++r) a[r] = fma(-m, b[r], a[r]);
+      __syncwarp();
+      if (j + 1 < BIG_NB) {
+        if (lane == 0) mbar_arrive(&sm.barF[j + 1]);
+        ir = sm.inv[j + 1];
+      }
+    }
+    // first pivot (in index order) that is <= 0 or not finite
+    const unsigned bad = __ballot_sync(0xffffffffu, lane < pb && !(mypiv > 0.0 && isfinite(mypiv)));
+    if (bad) {
+      const int fail = __ffs(bad) - 1;
+      const double fv = __shfl_sync(0xffffffffu, mypiv, fail);
+      if (lane == 0) {
+        sm.failed = 1;
+        if (q == 0) {
+          ctl->pivot_index = p0 + fail;
+          ctl->pivot_value = fv;
+          raise_status(ctl, ST_NOT_PD);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // T = L^-1, right-looking, lane c owning column c, one pivot behind
+    // warp 0: t_j = t[j] / L_jj, t[r] -= L[r][j] t_j with L[r][j] = R_j[r] ir_j
+    double t[BIG_NB];
+#pragma unroll
+    for (int r = 0; r < BIG_NB; ++r) t[r] = (r == lane) ? 1.0 : 0.0;
+#pragma unroll
+    for (int j = 0; j < BIG_NB; ++j) {
+      mbar_wait(&sm.barF[j], 0);
+      const double irj = sm.inv[j];
+      const double u = t[j] * irj * irj;
+      t[j] *= irj;
+#pragma unroll
+      for (int r = j + 1; r < BIG_NB; ++r) t[r] = fma(-u, sm.R[j][r], t[r]);
+    }
+#pragma unroll
+    for (int r = 0; r < BIG_NB; ++r) sm.T[r][lane] = t[r];
+  }
+  __syncthreads();
+  if (sm.failed) return;
+  if (q == 0)
+    for (int e = tid; e < BIG_NB * BIG_NB; e += BIG_THREADS)
+      Tg[static_cast<int64_t>(p0 / BIG_NB) * BIG_NB * BIG_NB + e] = sm.T[e >> 5][e & 31];
+  // X = A T^T: thread (row r, 8 columns); T's upper triangle is zero
+  {
+    const int r = tid & (BIG_TILE - 1), s0 = (tid >> 6) * 8;
+    for (int h = 0; h < (ti != tj ? 2 : 1); ++h) {
+      double acc[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) acc[u] = 0.0;
+#pragma unroll 8
+      for (int t = 0; t < BIG_NB; ++t) {
+        const double av = sm.A[h][r][t];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) acc[u] = fma(av, sm.T[s0 + u][t], acc[u]);
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) sm.X[h][r][s0 + u] = acc[u];
+    }
+  }
+  __syncthreads();
+  const int hb = ti != tj ? 1 : 0;
+  if (ti == tj)  // this tile's rows of L_p (row d: y)
+    for (int e = tid; e < BIG_TILE * BIG_NB; e += BIG_THREADS) {
+      const int r = e & (BIG_TILE - 1), s = e >> 6;
+      if (s < pb && r0 + r <= d) L[(r0 + r) + static_cast<int64_t>(p0 + s) * ld] = sm.X[0][r][s];
+    }
+  // C[i][j] -= X_i . X_j: thread rows tr + 16 a (contiguous in memory), columns tc + 16 b
+  const int tr = tid & 15, tc = tid >> 4;
   double acc[4][4] = {};
-  for (int s = 0; s < pb; ++s) {
+#pragma unroll 4
+  for (int s = 0; s < BIG_NB; ++s) {
     double av[4], bv[4];
 #pragma unroll
-    for (int a = 0; a < 4; ++a) av[a] = Pa[(ty + 16 * a) * BIG_LDS + s];
+    for (int a = 0; a < 4; ++a) av[a] = sm.X[0][tr + 16 * a][s];
 #pragma unroll
-    for (int b = 0; b < 4; ++b) bv[b] = Pb[(tx + 16 * b) * BIG_LDS + s];
+    for (int b = 0; b < 4; ++b) bv[b] = sm.X[hb][tc + 16 * b][s];
 #pragma unroll
     for (int a = 0; a < 4; ++a)
 #pragma unroll
@@ -174,68 +228,79 @@ __global__ void __launch_bounds__(BIG_THREADS) k_big_update(const DevCtl* __rest
   }
 #pragma unroll
   for (int b = 0; b < 4; ++b) {
-    const int j = c0 + tx + 16 * b;
+    const int j = c0 + tc + 16 * b;
 #pragma unroll
     for (int a = 0; a < 4; ++a) {
-      const int i = r0 + ty + 16 * a;
+      const int i = r0 + tr + 16 * a;
       if (i <= d && j < d && j <= i) {
         double* pm = M + i + static_cast<int64_t>(j) * ld;
-        *pm = __dsub_rn(*pm, acc[a][b]);
+        *pm = __dsub_rn(__ldcg(pm), acc[a][b]);
       }
     }
   }
 }
 
-// z = L^-T y (y = row d of M), then the outputs (modes as k_chol_solve).
-// one CTA of BIG_BACK_THREADS; dynamic smem: z (d doubles) + a 64-entry block
+// z = L^-T y (y = row d of L), then the outputs (modes as k_chol_solve).
+// one CTA of BIG_BACK_THREADS (a warp per column of a block);
+// dynamic smem: z (d doubles, padded) + t[32] + T_b[32][33]
 constexpr int BIG_BACK_THREADS = 1024;
+__host__ __device__ constexpr size_t big_back_smem(int d) {
+  return (static_cast<size_t>(d) + BIG_NB + BIG_NB + BIG_NB * BIG_LDS) * sizeof(double);
+}
 __global__ void __launch_bounds__(BIG_BACK_THREADS) k_big_back(DevCtl* __restrict__ ctl, int d,
-                                                               const double* __restrict__ M,
+                                                               const double* __restrict__ L,
+                                                               const double* __restrict__ Tg,
                                                                const double* __restrict__ x,
                                                                double* __restrict__ z,
                                                                double* __restrict__ x_out, int mode,
                                                                int ignore_halt) {
-  extern __shared__ double zs[];  // [d] then t[BIG_NB]
-  double* tb = zs + d;
+  extern __shared__ double zs[];  // [d rounded up to 32] then t[32] then Tb[32][33]
+  const int dp = (d + BIG_NB - 1) / BIG_NB * BIG_NB;
+  double* tb = zs + dp;
+  double* Tb = tb + BIG_NB;
   if (ctl->halt) {
     if (threadIdx.x == 0) tl_mark(2, true);
     return;
   }
   const int64_t ld = d + 1;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  constexpr int NW = BIG_BACK_THREADS / 32;
-  for (int i = tid; i < d; i += BIG_BACK_THREADS) zs[i] = M[d + static_cast<int64_t>(i) * ld];  // y
+  for (int i = tid; i < dp; i += BIG_BACK_THREADS) zs[i] = i < d ? __ldcg(L + d + static_cast<int64_t>(i) * ld) : 0.0;  // y
   __syncthreads();
   const int nblk = (d + BIG_NB - 1) / BIG_NB;
   for (int kb = nblk - 1; kb >= 0; --kb) {
     const int b0 = kb * BIG_NB, bn = min(BIG_NB, d - b0), b1 = b0 + bn;
-    // t_c = y_c - sum_{k >= b1} L[k][c] z_k for the block's columns c: warp
-    // per column, lanes over k (column c of M is contiguous in k)
-    for (int cc = warp; cc < bn; cc += NW) {
-      const int c = b0 + cc;
-      const double* col = M + static_cast<int64_t>(c) * ld;
+    Tb[warp * BIG_LDS + lane] = __ldcg(Tg + static_cast<int64_t>(kb) * BIG_NB * BIG_NB + warp * BIG_NB + lane);
+    // t_c = y_c - sum_{k >= b1} L[k][c] z_k: warp per column, lanes over k
+    // (column c of L is contiguous in k), eight loads in flight
+    {
+      const int c = b0 + warp;
       double s = 0.0;
-      for (int k = b1 + lane; k < d; k += 32) s = fma(col[k], zs[k], s);
-      s = warp_sum(s);
-      if (lane == 0) tb[cc] = zs[c] - s;
+      if (warp < bn) {
+        const double* col = L + static_cast<int64_t>(c) * ld;
+        for (int k0 = b1; k0 < d; k0 += 256) {
+          double v[8];
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {
+            const int k = k0 + u * 32 + lane;
+            v[u] = k < d ? __ldcg(col + k) : 0.0;
+          }
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {
+            const int k = k0 + u * 32 + lane;
+            s = fma(v[u], zs[k < d ? k : b1], s);
+          }
+        }
+        s = warp_sum(s);
+      }
+      if (lane == 0) tb[warp] = warp < bn ? zs[c] - s : 0.0;
     }
     __syncthreads();
-    // L_bb^T z_b = t: warp 0, lane = row, from the last row up
+    // z_b = T_b^T t: z_r = sum_{s >= r} T[s][r] t_s
     if (warp == 0) {
-      double zi0 = lane < bn ? tb[lane] : 0.0;
-      double zi1 = lane + 32 < bn ? tb[lane + 32] : 0.0;
-      for (int s2 = bn - 1; s2 >= 0; --s2) {
-        const bool own0 = lane == s2, own1 = lane + 32 == s2;
-        const double diag = M[(b0 + s2) + static_cast<int64_t>(b0 + s2) * ld];
-        if (own0) zi0 /= diag;
-        if (own1) zi1 /= diag;
-        const double zs2 = __shfl_sync(0xffffffffu, s2 < 32 ? zi0 : zi1, s2 & 31);
-        // rows r < s2: t_r -= L[s2][r] z_s2
-        if (lane < s2) zi0 = fma(-M[(b0 + s2) + static_cast<int64_t>(b0 + lane) * ld], zs2, zi0);
-        if (lane + 32 < s2) zi1 = fma(-M[(b0 + s2) + static_cast<int64_t>(b0 + lane + 32) * ld], zs2, zi1);
-      }
-      if (lane < bn) zs[b0 + lane] = zi0;
-      if (lane + 32 < bn) zs[b0 + lane + 32] = zi1;
+      double zr = 0.0;
+#pragma unroll 8
+      for (int s2 = 0; s2 < BIG_NB; ++s2) zr = fma(Tb[s2 * BIG_LDS + lane], tb[s2], zr);
+      if (lane < bn) zs[b0 + lane] = zr;
     }
     __syncthreads();
   }
