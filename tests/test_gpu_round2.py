@@ -255,9 +255,9 @@ def test_compact_design_matrix_bit_identical(name):
 # ------------------------------------------------------------ d > 1024
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("d", [1025, 1100, 1600])
+@pytest.mark.parametrize("d", [513, 1000, 1025, 1100, 1600])
 def test_large_d_solve_and_not_pd_pivot(d):
-    """The global-memory blocked solve (d > 1024, solve_big.cuh) against
+    """The global-memory blocked solve (d > 512, solve_big.cuh) against
     numpy at 1e-10, and the first failing pivot of an indefinite system is the
     reference's (index and value)."""
     from paper_2410_08760_b200 import NotPositiveDefiniteError, leaf
