@@ -637,20 +637,40 @@ int launch_solve(Ctx* ctx, cudaStream_t s, const double* hpk, const double* shif
     // panel rows and the trailing update of one tile per CTA), then the back
     // substitution (solve_big.cuh)
     const int d = ctx->d;
-    k_big_setup<<<std::min(d + 1, 4 * ctx->num_sms), BIG_THREADS, 0, s>>>(ctx->ctl, d, hpk, shift_ptr, rhs,
-                                                                          ctx->M);
-    CKL();
+    // high priority, as the cluster solvers: the panel kernels' CTAs take
+    // the SM slots the concurrent compressor's CTAs free, ahead of its own
+    // pending ones (at default priority the solve only ran after the c4
+    // TopK pass had dispatched its last CTA)
+    cudaLaunchAttribute pattr[1];
+    pattr[0].id = cudaLaunchAttributePriority;
+    pattr[0].val.priority = ctx->prio_high;
+    auto cfg = [&](int grid, int block, size_t smem) {
+      cudaLaunchConfig_t lc{};
+      lc.gridDim = dim3(grid);
+      lc.blockDim = dim3(block);
+      lc.dynamicSmemBytes = smem;
+      lc.stream = s;
+      lc.attrs = pattr;
+      lc.numAttrs = 1;
+      return lc;
+    };
+    {
+      cudaLaunchConfig_t lc = cfg(std::min(d + 1, 4 * ctx->num_sms), BIG_THREADS, 0);
+      CK(cudaLaunchKernelEx(&lc, k_big_setup, static_cast<const DevCtl*>(ctx->ctl), d, hpk, shift_ptr, rhs,
+                            ctx->M));
+    }
     if (launched) CK(cudaEventRecord(launched, s));
     for (int p0 = 0; p0 < d; p0 += BIG_NB) {
       const int p1 = std::min(d, p0 + BIG_NB);
       const int T = (d + 1 - p1 + BIG_TILE - 1) / BIG_TILE;  // tiles of rows p1..d (the rhs row included)
-      k_big_panel<<<T * (T + 1) / 2, BIG_THREADS, sizeof(BigSmem), s>>>(ctx->ctl, d, p0, ctx->M, ctx->Lbig,
-                                                                        ctx->Tbig);
-      CKL();
+      cudaLaunchConfig_t lc = cfg(T * (T + 1) / 2, BIG_THREADS, sizeof(BigSmem));
+      CK(cudaLaunchKernelEx(&lc, k_big_panel, ctx->ctl, d, p0, ctx->M, ctx->Lbig, ctx->Tbig));
     }
-    k_big_back<<<1, BIG_BACK_THREADS, big_back_smem(d), s>>>(ctx->ctl, d, ctx->Lbig, ctx->Tbig, x, z, x_out,
-                                                             mode, ignore_halt);
-    CKL();
+    {
+      cudaLaunchConfig_t lc = cfg(1, BIG_BACK_THREADS, big_back_smem(d));
+      CK(cudaLaunchKernelEx(&lc, k_big_back, ctx->ctl, d, static_cast<const double*>(ctx->Lbig),
+                            static_cast<const double*>(ctx->Tbig), x, z, x_out, mode, ignore_halt));
+    }
     return FB_OK;
   }
   const bool panels = ctx->solve_panels && !force_old;
