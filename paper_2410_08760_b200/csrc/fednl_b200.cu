@@ -641,17 +641,22 @@ int launch_solve(Ctx* ctx, cudaStream_t s, const double* hpk, const double* shif
     // the SM slots the concurrent compressor's CTAs free, ahead of its own
     // pending ones (at default priority the solve only ran after the c4
     // TopK pass had dispatched its last CTA)
-    cudaLaunchAttribute pattr[1];
+    cudaLaunchAttribute pattr[2];
     pattr[0].id = cudaLaunchAttributePriority;
     pattr[0].val.priority = ctx->prio_high;
-    auto cfg = [&](int grid, int block, size_t smem) {
+    // the panel kernels and the back substitution chain with programmatic
+    // dependent launch (each waits for its predecessor after its prologue)
+    pattr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    pattr[1].val.programmaticStreamSerializationAllowed = 1;
+    const bool pdl = pdl_ok(ctx);
+    auto cfg = [&](int grid, int block, size_t smem, bool dep = false) {
       cudaLaunchConfig_t lc{};
       lc.gridDim = dim3(grid);
       lc.blockDim = dim3(block);
       lc.dynamicSmemBytes = smem;
       lc.stream = s;
       lc.attrs = pattr;
-      lc.numAttrs = 1;
+      lc.numAttrs = (dep && pdl) ? 2 : 1;
       return lc;
     };
     {
@@ -663,11 +668,11 @@ int launch_solve(Ctx* ctx, cudaStream_t s, const double* hpk, const double* shif
     for (int p0 = 0; p0 < d; p0 += BIG_NB) {
       const int p1 = std::min(d, p0 + BIG_NB);
       const int T = (d + 1 - p1 + BIG_TILE - 1) / BIG_TILE;  // tiles of rows p1..d (the rhs row included)
-      cudaLaunchConfig_t lc = cfg(T * (T + 1) / 2, BIG_THREADS, sizeof(BigSmem));
+      cudaLaunchConfig_t lc = cfg(T * (T + 1) / 2, BIG_THREADS, sizeof(BigSmem), p0 > 0);
       CK(cudaLaunchKernelEx(&lc, k_big_panel, ctx->ctl, d, p0, ctx->M, ctx->Lbig, ctx->Tbig));
     }
     {
-      cudaLaunchConfig_t lc = cfg(1, BIG_BACK_THREADS, big_back_smem(d));
+      cudaLaunchConfig_t lc = cfg(1, BIG_BACK_THREADS, big_back_smem(d), true);
       CK(cudaLaunchKernelEx(&lc, k_big_back, ctx->ctl, d, static_cast<const double*>(ctx->Lbig),
                             static_cast<const double*>(ctx->Tbig), x, z, x_out, mode, ignore_halt));
     }

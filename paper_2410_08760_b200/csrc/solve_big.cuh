@@ -83,7 +83,6 @@ __global__ void __launch_bounds__(BIG_THREADS) k_big_panel(DevCtl* __restrict__ 
                                                            double* __restrict__ Tg) {
   extern __shared__ __align__(16) uint8_t big_raw[];
   BigSmem& sm = *reinterpret_cast<BigSmem*>(big_raw);
-  if (ctl->halt) return;
   const int64_t ld = d + 1;
   const int pb = min(BIG_NB, d - p0), p1 = p0 + pb;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -98,21 +97,62 @@ __global__ void __launch_bounds__(BIG_THREADS) k_big_panel(DevCtl* __restrict__ 
     sm.failed = 0;
     fence_barrier_init();
   }
-  // the diagonal block in full (padded with the identity past pb)
-  for (int e = tid; e < BIG_NB * BIG_NB; e += BIG_THREADS) {
-    const int r = e & (BIG_NB - 1), c = e >> 5;
-    const int hi = max(r, c), lo = min(r, c);
-    sm.S[r][c] = hi < pb ? __ldcg(M + (p0 + hi) + static_cast<int64_t>(p0 + lo) * ld) : (r == c ? 1.0 : 0.0);
+  // programmatic dependent launch: this prologue overlapped the previous
+  // panel's kernel; the next panel's kernel may launch once every CTA of
+  // this one is past the wait (so at most two panel kernels hold SM slots)
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;");
+  if (ctl->halt) return;
+  // diagnostics: CTA 0's phase stamps of panel p in g_dbg_span[8 p ..]
+  const bool stamp_on = g_dbg_on && q == 0 && tid == 0 && p0 / BIG_NB < 128;
+  auto stamp = [&](int ph) {
+    if (stamp_on) g_dbg_span[8 * (p0 / BIG_NB) + ph] = globaltimer_ns();
+  };
+  stamp(0);
+  // every global load of the CTA is issued here, before any is consumed: the
+  // diagonal block (lower triangle, mirrored in shared memory; the identity
+  // past pb), the panel rows of both tiles (coalesced along the rows), and
+  // the trailing tile itself (kept in registers until the update: its
+  // latency hides behind the block factor)
+  const int tr = tid & 15, tc = tid >> 4;
+  double sv[4], av[2][8], cv[4][4];
+#pragma unroll
+  for (int u = 0; u < 4; ++u) {
+    const int e = tid + u * BIG_THREADS, r = e & (BIG_NB - 1), c = e >> 5;
+    sv[u] = (c <= r && r < pb) ? __ldcg(M + (p0 + r) + static_cast<int64_t>(p0 + c) * ld) : (r == c ? 1.0 : 0.0);
   }
-  // the panel rows of both tiles (coalesced along the rows)
-  for (int e = tid; e < BIG_TILE * BIG_NB; e += BIG_THREADS) {
-    const int r = e & (BIG_TILE - 1), s = e >> 6;
-    const bool sv = s < pb;
-    sm.A[0][r][s] = (sv && r0 + r <= d) ? __ldcg(M + (r0 + r) + static_cast<int64_t>(p0 + s) * ld) : 0.0;
-    if (ti != tj)
-      sm.A[1][r][s] = (sv && c0 + r <= d) ? __ldcg(M + (c0 + r) + static_cast<int64_t>(p0 + s) * ld) : 0.0;
+#pragma unroll
+  for (int u = 0; u < 8; ++u) {
+    const int e = tid + u * BIG_THREADS, r = e & (BIG_TILE - 1), s2 = e >> 6;
+    const bool ok = s2 < pb;
+    av[0][u] = (ok && r0 + r <= d) ? __ldcg(M + (r0 + r) + static_cast<int64_t>(p0 + s2) * ld) : 0.0;
+    av[1][u] = (ok && ti != tj && c0 + r <= d) ? __ldcg(M + (c0 + r) + static_cast<int64_t>(p0 + s2) * ld) : 0.0;
+  }
+#pragma unroll
+  for (int b = 0; b < 4; ++b) {
+    const int j = c0 + tc + 16 * b;
+#pragma unroll
+    for (int a = 0; a < 4; ++a) {
+      const int i = r0 + tr + 16 * a;
+      cv[a][b] = (i <= d && j < d && j <= i) ? __ldcg(M + i + static_cast<int64_t>(j) * ld) : 0.0;
+    }
+  }
+#pragma unroll
+  for (int u = 0; u < 4; ++u) {
+    const int e = tid + u * BIG_THREADS, r = e & (BIG_NB - 1), c = e >> 5;
+    if (c <= r) {
+      sm.S[r][c] = sv[u];
+      sm.S[c][r] = sv[u];
+    }
+  }
+#pragma unroll
+  for (int u = 0; u < 8; ++u) {
+    const int e = tid + u * BIG_THREADS, r = e & (BIG_TILE - 1), s2 = e >> 6;
+    sm.A[0][r][s2] = av[0][u];
+    if (ti != tj) sm.A[1][r][s2] = av[1][u];
   }
   __syncthreads();
+  stamp(1);
   if (warp == 0) {
     // block factor on the symmetric Schur complement: lane c owns column c
     // (a[r] = S[r][c]); by symmetry its multiplier S[c][j] is its own a[j],
@@ -183,6 +223,7 @@ __global__ void __launch_bounds__(BIG_THREADS) k_big_panel(DevCtl* __restrict__ 
     for (int r = 0; r < BIG_NB; ++r) sm.T[r][lane] = t[r];
   }
   __syncthreads();
+  stamp(2);
   if (sm.failed) return;
   if (q == 0)
     for (int e = tid; e < BIG_NB * BIG_NB; e += BIG_THREADS)
@@ -205,6 +246,7 @@ __global__ void __launch_bounds__(BIG_THREADS) k_big_panel(DevCtl* __restrict__ 
     }
   }
   __syncthreads();
+  stamp(3);
   const int hb = ti != tj ? 1 : 0;
   if (ti == tj)  // this tile's rows of L_p (row d: y)
     for (int e = tid; e < BIG_TILE * BIG_NB; e += BIG_THREADS) {
@@ -212,19 +254,18 @@ __global__ void __launch_bounds__(BIG_THREADS) k_big_panel(DevCtl* __restrict__ 
       if (s < pb && r0 + r <= d) L[(r0 + r) + static_cast<int64_t>(p0 + s) * ld] = sm.X[0][r][s];
     }
   // C[i][j] -= X_i . X_j: thread rows tr + 16 a (contiguous in memory), columns tc + 16 b
-  const int tr = tid & 15, tc = tid >> 4;
   double acc[4][4] = {};
 #pragma unroll 4
   for (int s = 0; s < BIG_NB; ++s) {
-    double av[4], bv[4];
+    double xa[4], xb[4];
 #pragma unroll
-    for (int a = 0; a < 4; ++a) av[a] = sm.X[0][tr + 16 * a][s];
+    for (int a = 0; a < 4; ++a) xa[a] = sm.X[0][tr + 16 * a][s];
 #pragma unroll
-    for (int b = 0; b < 4; ++b) bv[b] = sm.X[hb][tc + 16 * b][s];
+    for (int b = 0; b < 4; ++b) xb[b] = sm.X[hb][tc + 16 * b][s];
 #pragma unroll
     for (int a = 0; a < 4; ++a)
 #pragma unroll
-      for (int b = 0; b < 4; ++b) acc[a][b] = fma(av[a], bv[b], acc[a][b]);
+      for (int b = 0; b < 4; ++b) acc[a][b] = fma(xa[a], xb[b], acc[a][b]);
   }
 #pragma unroll
   for (int b = 0; b < 4; ++b) {
@@ -232,12 +273,10 @@ __global__ void __launch_bounds__(BIG_THREADS) k_big_panel(DevCtl* __restrict__ 
 #pragma unroll
     for (int a = 0; a < 4; ++a) {
       const int i = r0 + tr + 16 * a;
-      if (i <= d && j < d && j <= i) {
-        double* pm = M + i + static_cast<int64_t>(j) * ld;
-        *pm = __dsub_rn(__ldcg(pm), acc[a][b]);
-      }
+      if (i <= d && j < d && j <= i) M[i + static_cast<int64_t>(j) * ld] = __dsub_rn(cv[a][b], acc[a][b]);
     }
   }
+  stamp(4);
 }
 
 // z = L^-T y (y = row d of L), then the outputs (modes as k_chol_solve).
@@ -258,6 +297,7 @@ __global__ void __launch_bounds__(BIG_BACK_THREADS) k_big_back(DevCtl* __restric
   const int dp = (d + BIG_NB - 1) / BIG_NB * BIG_NB;
   double* tb = zs + dp;
   double* Tb = tb + BIG_NB;
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   if (ctl->halt) {
     if (threadIdx.x == 0) tl_mark(2, true);
     return;
