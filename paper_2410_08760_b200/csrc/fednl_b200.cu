@@ -1126,7 +1126,13 @@ int build_graph(Ctx* ctx, bool phase_events) {
     for (int i = 0; i < EV_COUNT; ++i)
       if (ev == ctx->ev_fixed[i]) ctx->ev_node[i] = nd;
   }
-  CK(cudaGraphInstantiate(&ctx->gexec, g, 0));
+  // the blocked solve's many launches need their per-node priority honoured
+  // (without the flag a graph runs every node at the launch stream's
+  // priority: each panel kernel queued behind the c4 TopK pass and the fold;
+  // c4 solve 1.16 -> 0.63 ms in the round).  The cluster solvers launch once
+  // and hold the compressor back until resident: no flag there (c1 -3% with it)
+  const unsigned gflags = ctx->solve_big ? cudaGraphInstantiateFlagUseNodePriority : 0;
+  CK(cudaGraphInstantiateWithFlags(&ctx->gexec, g, gflags));
   if (!phase_events && ctx->cfg.algorithm == FB_ALG_FEDNL) {
     CK(cudaStreamBeginCapture(ctx->st, cudaStreamCaptureModeThreadLocal));
     int rr = FB_OK;
@@ -1140,7 +1146,7 @@ int build_graph(Ctx* ctx, bool phase_events) {
     }
     CK(em);
     ctx->graph_multi = gm;
-    CK(cudaGraphInstantiate(&ctx->gexec_multi, gm, 0));
+    CK(cudaGraphInstantiateWithFlags(&ctx->gexec_multi, gm, gflags));
   }
   return FB_OK;
 }
