@@ -178,7 +178,11 @@ def algorithmic_counts(config: str) -> dict:
         comp_bytes = n_act * (16 * k + 8)
     else:
         comp_bytes = n_act * 20 * k
+    # the shift update's random 8-byte read-modify-writes of H_i^k move whole
+    # 32-byte sectors: (4 + 8) list bytes + a sector read and a sector written
+    # per entry, the master's H^k once (contiguous)
     return {"hessian_flop": flops, "compress_bytes": comp_bytes, "fold_bytes": n_act * k * 44,
+            "fold_sector_bytes": n_act * k * (12 + 64) + 16 * w,
             "oracle_bytes": n * d * ni * 8 * 2, "d": d, "n": n, "ni": ni, "k": k, "w": w}
 
 
@@ -297,6 +301,7 @@ def run_ours(args) -> dict | None:
     hbm = float(peaks.get("hbm_gbs", 6650.0))
     comp_gbs = counts["compress_bytes"] / (prof["ms_compress"] * 1e-3) / 1e9 if prof["ms_compress"] else None
     fold_gbs = counts["fold_bytes"] / (prof["ms_fold"] * 1e-3) / 1e9 if prof["ms_fold"] else None
+    fold_sec_gbs = counts["fold_sector_bytes"] / (prof["ms_fold"] * 1e-3) / 1e9 if prof["ms_fold"] else None
     traffic, traffic_src = hessian_traffic(args.config)
 
     cpu = None if args.no_cpu_baseline else cpu_baseline(args.config, budget_s=args.cpu_seconds)
@@ -354,6 +359,8 @@ def run_ours(args) -> dict | None:
             "compress_frac_hbm": None if comp_gbs is None else round(comp_gbs / hbm, 4),
             "fold_gbs": None if fold_gbs is None else round(fold_gbs, 1),
             "fold_frac_hbm": None if fold_gbs is None else round(fold_gbs / hbm, 4),
+            "fold_sector_gbs": None if fold_sec_gbs is None else round(fold_sec_gbs, 1),
+            "fold_sector_frac_hbm": None if fold_sec_gbs is None else round(fold_sec_gbs / hbm, 4),
             "hbm_peak_gbs": hbm,
         },
         "fp64_peaks_tflops": {"dmma": round(dmma_peak, 2), "dfma": round(dfma_peak, 2)},
