@@ -429,7 +429,11 @@ __global__ void __launch_bounds__(HW_THREADS, 1) k_hessian_ws(
 
   if (warp < HW_PIPES * HW_MMA) {
     // ------------------------------------------------------ DMMA warps
-    const int q4 = warp % HW_MMA;
+    // warp k of either pipe runs on sub-partition k: the second pipe takes the
+    // tasks pairwise swapped, so a diagonal tile's two triangle tasks (10
+    // fragments at nv = 8) share their sub-partitions' DMMA pipes with the
+    // other pipe's rectangle tasks (8) when both pipes hold diagonal tiles
+    const int q4 = (warp % HW_MMA) ^ (pipe & 1);
     const int g = lane >> 2, t = lane & 3;
     int gsn = 0;
     for (int j = 0;; ++j) {
