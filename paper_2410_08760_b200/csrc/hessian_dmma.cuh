@@ -429,11 +429,16 @@ __global__ void __launch_bounds__(HW_THREADS, 1) k_hessian_ws(
 
   if (warp < HW_PIPES * HW_MMA) {
     // ------------------------------------------------------ DMMA warps
-    // warp k of either pipe runs on sub-partition k: the second pipe takes the
-    // tasks pairwise swapped, so a diagonal tile's two triangle tasks (10
-    // fragments at nv = 8) share their sub-partitions' DMMA pipes with the
-    // other pipe's rectangle tasks (8) when both pipes hold diagonal tiles
-    const int q4 = (warp % HW_MMA) ^ (pipe & 1);
+    // Task -> sub-partition placement (warp k of either pipe runs on
+    // sub-partition k; the epilogue warps sit on sub-partitions 2 and 3, the
+    // idle-most TMA warps on 0 and 1).  A diagonal tile has two 10-fragment
+    // triangle tasks (which also form the gradient) and two 8-fragment
+    // rectangles.  Few tiles per dimension (d <= 512, where diagonal tiles
+    // are a third of the items): both triangles on sub-partitions 0 and 1,
+    // away from the epilogue warps' FP64 / issue load (c0 195.3 -> 188.8 us).
+    // Many tiles (c4): the second pipe takes the tasks pairwise swapped, so
+    // triangles meet the other pipe's rectangles (c4 34.57 -> 34.49 ms).
+    const int q4 = n_pairs <= 36 ? ((0x2130 >> (4 * (warp % HW_MMA))) & 3) : ((warp % HW_MMA) ^ (pipe & 1));
     const int g = lane >> 2, t = lane & 3;
     int gsn = 0;
     for (int j = 0;; ++j) {
