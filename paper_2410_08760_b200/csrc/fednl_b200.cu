@@ -343,13 +343,20 @@ int gather_blocks(Ctx* ctx, T* base, size_t cnt, ncclDataType_t type, cudaStream
 }
 bool sharded(const Ctx* ctx) { return ctx->world > 1 || ctx->comm != nullptr; }
 
-// clients per Hessian item group: about 2.5 rounds of the 2 * num_sms tile
-// pipes.  Items run group by group, each group's tile pairs costliest first:
-// the group's B rows stay in L2 for all its tiles (round 1, one tile per CTA
-// at c0: one group 586 MB of DRAM traffic, groups of 48 clients 218 MB) and
-// the last items of the pass are cheap diagonal / edge tiles.
-int hess_group(const Ctx* ctx) {
-  return std::max(1, 5 * ctx->num_sms / std::max(1, ctx->n_pairs));
+// clients per Hessian item group.  Items run group by group, each group's
+// tile pairs costliest first: the group's B rows stay in L2 for all its tiles
+// (round 1, one tile per CTA at c0: one group 586 MB of DRAM traffic, groups
+// of 48 clients 218 MB) and the last items of the pass are cheap diagonal /
+// edge tiles.  Base size: about 2.5 rounds of the 2 * num_sms tile pipes
+// (3.75 for small clients, B_c <= 4 MB: their rows are loaded evict-first);
+// the groups are then made equal, so the last one — the pass's tail — has as
+// many items to balance with as the others (c0, n = 142: 49 + 49 + 44 ->
+// 71 + 71, Hessian 190.2 -> 187.8 us; 57 / 64 / 80 / 95 are all worse).
+int hess_group(const Ctx* ctx, int n_active) {
+  const bool small = static_cast<size_t>(ctx->d) * ctx->ldj * sizeof(double) <= (size_t{4} << 20);
+  const int base = std::max(1, (small ? 15 : 10) * ctx->num_sms / (2 * std::max(1, ctx->n_pairs)));
+  const int groups = std::max(1, (n_active + base - 1) / base);
+  return std::max(1, (n_active + groups - 1) / groups);
 }
 // programmatic dependent launch attributes, except under a profiler's
 // injection library (serialised launches there anyway)
@@ -517,7 +524,7 @@ int launch_hessian(Ctx* ctx, cudaStream_t s, const int32_t* clients, int n_activ
                         hest, hest_stride, D, hess_out, ctx->frob_part, ctx->flags,
                         0u /* zero_mask: see mbar_arrive_dep */, static_cast<const double*>(ctx->gcoef),
                         fuse_grad_x, fuse_grad_x ? ctx->grad : nullptr,
-                        static_cast<const int32_t*>(ctx->pair_order), ctx->n_pairs, n_active, hess_group(ctx),
+                        static_cast<const int32_t*>(ctx->pair_order), ctx->n_pairs, n_active, hess_group(ctx, n_active),
                         ctx->hess_sched, hess_b_evict_first(ctx) ? 1 : 0));
   return FB_OK;
 }
